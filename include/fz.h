@@ -1,0 +1,193 @@
+/*
+ * fz.h -- C ABI of the B200-native FZ-GPU compressor (arXiv 2304.12557), libfz.so.
+ *
+ * Citation key: P:n = PAPER.md line n, S:n = SPEC.md line n, SV = SURVEY.md, DESIGN.md §3
+ * lists the readings R1-R22 that fix everything the paper leaves open.
+ *
+ * Problem statement: the data is produced on the GPU and compressed "directly ...
+ * from the GPU memory"; the compressed stream is cached in GPU memory and "decompressed on the
+ * GPU directly", or saved to disk via the CPU.  Hence: every field/stream pointer below is a
+ * DEVICE pointer unless its name starts with h_, and work is enqueued on `stream`
+ * (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *
+ * Ownership: the caller allocates every buffer (typically torch tensors).  The library never
+ * allocates device memory and retains no pointer after a call returns.  Calls are re-entrant
+ * given separate workspaces.  Device pointers must be 16-byte aligned.
+ *
+ * Errors: status codes only (fz_status); nothing crosses the ABI as an exception.  A CUDA
+ * runtime failure returns FZ_ERR_CUDA (the CUDA error string is available from
+ * fz_last_cuda_error()).
+ */
+#ifndef FZ_H
+#define FZ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { FZ_EB_ABS = 0, FZ_EB_REL = 1 } fz_eb_mode;   /* REL = eb * (max-min) */
+
+typedef enum {
+    FZ_OK = 0,
+    FZ_ERR_ARG = 1,          /* ndim not in {1,2,3}, zero extent, N >= 2^32, eb <= 0 or
+                                non-finite, NULL or misaligned pointer                     */
+    FZ_ERR_NONFINITE = 2,    /* NaN/Inf in the field; first index reported           */
+    FZ_ERR_EB_TOO_SMALL = 3, /* bin width w below FLT_MIN (reading R17)                     */
+    FZ_ERR_CAPACITY = 4,     /* output too small: *out_size = required size, nothing
+                                written past out_cap (snprintf convention)                 */
+    FZ_ERR_CORRUPT = 5,      /* stream fails magic/version/size-law/popcount/index checks   */
+    FZ_ERR_WORKSPACE = 6,    /* workspace smaller than fz_*workspace_bytes()                */
+    FZ_ERR_CUDA = 7
+} fz_status;
+
+/* Field shape: dims[0] slowest (z), dims[ndim-1] fastest (x); row-major fp32. */
+typedef struct {
+    uint32_t ndim;
+    uint32_t reserved;
+    uint64_t dims[3];
+} fz_shape;
+
+/* Quantization parameters (P:129-134 with reading R2 = SURVEY Appendix A). */
+typedef struct {
+    double eb_input;   /* eb as given                                             */
+    double eb_abs;     /* eb (ABS) or eb*(max-min) (REL)                    */
+    float w;           /* bin width: RD32(2 eb_abs - U), U = ulp of binade above M */
+    float r;           /* (float)(1/(double)w)                                     */
+    float eb32;        /* RD32(eb_abs)                                             */
+    float mn, mx;      /* field range (-0.0 counted as +0.0, R18)                  */
+    uint32_t mode;     /* fz_eb_mode                                               */
+    uint32_t fallback; /* 1 when the margin mode is infeasible (R2)                */
+} fz_params;
+
+/* Section sizes of one stream (or of one slab's share of it). */
+typedef struct {
+    uint64_t nnz;      /* nonzero 16-byte blocks      */
+    uint64_t n_delta;  /* delta outliers, |delta| > 32767 (R7) */
+    uint64_t n_value;  /* value outliers (R20)                 */
+} fz_counts;
+
+/* Decoded 128-byte header. */
+typedef struct {
+    fz_shape shape;
+    uint64_t n, tiles, total_size;
+    fz_counts counts;
+    fz_params params;
+    uint32_t version, flags;
+} fz_info;
+
+/* ---------------------------------------------------------------------------------------
+ * Sizes.  T = ceil(N / 2048) tiles of 32x32 words, 2 codes per word.
+ * ------------------------------------------------------------------------------------- */
+/* 128 + 32T + 4096T + 16N: safe upper bound of the stream (every block and every element
+ * an outlier).  0 if the shape is invalid. */
+size_t fz_compress_bound(const fz_shape* s);
+/* Device workspace needed by fz_compress / fz_compress_with_params / slab calls. */
+size_t fz_workspace_bytes(const fz_shape* s);
+/* Device workspace needed by fz_decompress. */
+size_t fz_decompress_workspace_bytes(const fz_shape* s);
+
+/* ---------------------------------------------------------------------------------------
+ * Parameters (host).  Appendix A of SURVEY.md; identical on every rank for identical
+ * (min, max, mode, eb).
+ * ------------------------------------------------------------------------------------- */
+fz_status fz_derive_params(float mn, float mx, int eb_mode, double eb, fz_params* h_params);
+
+/* ---------------------------------------------------------------------------------------
+ * Compression: range -> prequantize -> Lorenzo -> codes -> bitshuffle -> block
+ * flags -> exclusive scan -> compaction, fused in one persistent kernel after the range
+ * pass.  Blocks once on `stream` to return *out_size (host).
+ *   d_field   : N fp32, device, row-major
+ *   d_out     : device, out_cap bytes; receives header || flags || payload || outliers
+ *   d_work    : device workspace of fz_workspace_bytes(s) bytes
+ *   *h_first_bad (optional, may be NULL): first non-finite index on FZ_ERR_NONFINITE
+ * ------------------------------------------------------------------------------------- */
+fz_status fz_compress(const float* d_field, const fz_shape* s, int eb_mode, double eb,
+                      void* d_out, size_t out_cap, size_t* h_out_size,
+                      void* d_work, size_t work_bytes, void* stream);
+
+/* Same with parameters supplied by the caller (skips the range pass; multi-GPU ranks and
+ * idempotence tests use it).  h_params must come from fz_derive_params. */
+fz_status fz_compress_with_params(const float* d_field, const fz_shape* s,
+                                  const fz_params* h_params,
+                                  void* d_out, size_t out_cap, size_t* h_out_size,
+                                  void* d_work, size_t work_bytes, void* stream);
+
+/* Decompression: parse, offsets from flags, gather, un-shuffle, unpack + delta patch,
+ * inverse-Lorenzo prefix sums, x-hat = fl32(fl32(q) * w) + value patch.  Blocks once on
+ * `stream` to read the header.  d_field receives n fp32 values (n must equal the header's N). */
+fz_status fz_decompress(const void* d_in, size_t in_size, float* d_field, uint64_t n,
+                        void* d_work, size_t work_bytes, void* stream);
+
+/* Host-buffer variants (end-to-end path): H2D of the input, the device call, D2H of the
+ * result, all on `stream`.  The caller passes device scratch of the stated sizes.
+ *   compress  : d_field_scratch >= 4N bytes, d_out_scratch >= d_out_cap bytes.
+ *   decompress: d_in_scratch >= in_size bytes, d_field_scratch >= 4n bytes. */
+fz_status fz_compress_host(const float* h_field, const fz_shape* s, int eb_mode, double eb,
+                           void* h_out, size_t out_cap, size_t* h_out_size,
+                           float* d_field_scratch, void* d_out_scratch, size_t d_out_cap,
+                           void* d_work, size_t work_bytes, void* stream);
+fz_status fz_decompress_host(const void* h_in, size_t in_size, float* h_field, uint64_t n,
+                             void* d_in_scratch, float* d_field_scratch,
+                             void* d_work, size_t work_bytes, void* stream);
+
+/* Parse and validate a header (host memory, n >= 128 bytes).  Checks magic, version, shape
+ * and the size law; popcount and index checks need the whole stream (fz_decompress). */
+fz_status fz_peek_header(const void* h_hdr, size_t n, fz_info* h_info);
+
+const char* fz_strerror(int status);
+const char* fz_last_cuda_error(void);
+
+/* ---------------------------------------------------------------------------------------
+ * Slab API for multi-GPU z-slab partitioning ("embarrassingly parallel"; SV §8.e).
+ * Rank-local calls; the caller does the NCCL all_gathers.  Tiles are global: rank k owns
+ * tiles [tile_begin, tile_end).  The slab buffer d_slab holds the global elements
+ * [slab_first, slab_first + slab_elems), which must cover [2048*tile_begin - (P + nx + 1),
+ * min(N, 2048*tile_end)) clamped at 0 (the read-only 1-plane + 1-row + 1-element Lorenzo
+ * halo).  slab_first must be a multiple of 4.
+ * ------------------------------------------------------------------------------------- */
+
+/* Range of d_slab[0..n): min, max (R18), first non-finite index (-1 if none). */
+fz_status fz_slab_range(const float* d_slab, uint64_t n, float* h_min, float* h_max,
+                        int64_t* h_first_bad, void* d_work, size_t work_bytes, void* stream);
+
+/* Compress the slab's tiles into d_stage laid out as the slab's share of every section:
+ * flags (32 * ntiles) || payload (16 * nnz) || delta records (8 * n_delta) || value records
+ * (8 * n_value).  *h_counts receives the local counts.  stage_cap >= fz_slab_stage_bound. */
+size_t fz_slab_stage_bound(const fz_shape* global, uint64_t tile_begin, uint64_t tile_end);
+fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t slab_elems,
+                           const fz_shape* global, uint64_t tile_begin, uint64_t tile_end,
+                           const fz_params* h_params, void* d_stage, size_t stage_cap,
+                           fz_counts* h_counts, void* d_work, size_t work_bytes, void* stream);
+
+/* Copy a staged slab to its final place in the global stream buffer d_out (total bytes
+ * out_cap): `before` = exclusive prefix of the counts of lower ranks, `totals` = global sums.
+ * The rank owning tile 0 also passes write_header = 1. */
+fz_status fz_slab_place(const void* d_stage, const fz_shape* global, uint64_t tile_begin,
+                        uint64_t tile_end, const fz_counts* local, const fz_counts* before,
+                        const fz_counts* totals, const fz_params* h_params, int write_header,
+                        void* d_out, size_t out_cap, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Stage hooks for parity tests (north star: codes and outlier lists match the oracle).
+ * ------------------------------------------------------------------------------------- */
+/* C1-C3: uint16 codes of every element and both outlier lists (ascending index). */
+fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_params* h_params,
+                            uint16_t* d_codes,
+                            uint32_t* d_didx, int32_t* d_dval, uint64_t dcap, uint64_t* h_nd,
+                            uint32_t* d_vidx, uint32_t* d_vbits, uint64_t vcap, uint64_t* h_nv,
+                            void* d_work, size_t work_bytes, void* stream);
+/* D1-D5: reconstructed integer codes q (before dequantization), n int32 values. */
+fz_status fz_debug_decode_q(const void* d_in, size_t in_size, int32_t* d_q, uint64_t n,
+                            void* d_work, size_t work_bytes, void* stream);
+
+/* Number of kernel launches issued by the last fz_compress / fz_decompress on this thread
+ * (bench accounting of "gpu_launches"). */
+int fz_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FZ_H */

@@ -1,0 +1,586 @@
+// fz_api.cu -- the C ABI of libfz (include/fz.h): validation, workspace carving, launch
+// sequences, host<->device control-block round trips, status mapping.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "fz_launch.h"
+
+namespace fz {
+static thread_local int t_launches = 0;
+void count_launch() { ++t_launches; }
+}  // namespace fz
+
+using namespace fz;
+
+static thread_local char g_cuda_err[256] = "";
+static thread_local int g_last_launches = 0;
+
+namespace {
+
+struct LaunchScope {
+    LaunchScope() { fz::t_launches = 0; }
+    ~LaunchScope() { g_last_launches = fz::t_launches; }
+};
+
+fz_status cuda_fail(cudaError_t e)
+{
+    snprintf(g_cuda_err, sizeof g_cuda_err, "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return FZ_ERR_CUDA;
+}
+
+#define FZ_CUDA(call)                                \
+    do {                                             \
+        cudaError_t e_ = (call);                     \
+        if (e_ != cudaSuccess) return cuda_fail(e_); \
+    } while (0)
+
+bool shape_n(const fz_shape* s, uint64_t* n)
+{
+    if (s == nullptr || s->ndim < 1 || s->ndim > 3) return false;
+    uint64_t m = 1;
+    for (uint32_t k = 0; k < s->ndim; ++k) {
+        if (s->dims[k] == 0 || s->dims[k] > 0xFFFFFFFFull) return false;
+        m *= s->dims[k];
+        if (m > 0xFFFFFFFFull) return false;   // element indices are u32 (R16)
+    }
+    *n = m;
+    return true;
+}
+
+Geom geom_of(const fz_shape& s, uint64_t n)
+{
+    Geom g{};
+    g.n = (uint32_t)n;
+    g.ndim = s.ndim;
+    if (s.ndim == 1) { g.nx = (uint32_t)n; g.P = (uint32_t)n; }
+    else if (s.ndim == 2) { g.nx = (uint32_t)s.dims[1]; g.P = (uint32_t)n; }
+    else { g.nx = (uint32_t)s.dims[2]; g.P = (uint32_t)(s.dims[1] * s.dims[2]); }
+    return g;
+}
+
+uint64_t tiles_of(uint64_t n) { return (n + kTileCodes - 1) / kTileCodes; }
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+struct Work {
+    Layout L;
+    uint8_t* base;
+    Ctrl* ctrl() const { return reinterpret_cast<Ctrl*>(base + L.ctrl); }
+    unsigned long long* status() const { return reinterpret_cast<unsigned long long*>(base + L.status); }
+    uint32_t* aggv() const { return reinterpret_cast<uint32_t*>(base + L.aggv); }
+    uint32_t* inclv() const { return reinterpret_cast<uint32_t*>(base + L.inclv); }
+    uint2* tpre() const { return reinterpret_cast<uint2*>(base + L.tpre); }
+    uint2* dstage() const { return reinterpret_cast<uint2*>(base + L.dstage); }
+    uint2* vstage() const { return reinterpret_cast<uint2*>(base + L.vstage); }
+};
+
+CompressArgs make_args(const Work& W, const float* field, uint64_t base, const Geom& g,
+                       uint32_t tb, uint32_t te)
+{
+    CompressArgs a{};
+    a.field = field;
+    a.base = base;
+    a.g = g;
+    a.tile_begin = tb;
+    a.tile_end = te;
+    a.dstage = W.dstage();
+    a.vstage = W.vstage();
+    a.dcap = W.L.dcap;
+    a.vcap = W.L.vcap;
+    a.status = W.status();
+    a.aggv = W.aggv();
+    a.inclv = W.inclv();
+    a.tpre = W.tpre();
+    a.ctrl = W.ctrl();
+    return a;
+}
+
+fz_status read_ctrl(const Work& W, Ctrl* h, cudaStream_t st)
+{
+    FZ_CUDA(cudaMemcpyAsync(h, W.ctrl(), sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    FZ_CUDA(cudaStreamSynchronize(st));
+    return FZ_OK;
+}
+
+// Outliers did not fit the staging area: recompute them tile by tile and write straight to
+// their final offsets (the per-tile exclusive counts were recorded by the first pass).
+fz_status rescan(const Work& W, CompressArgs a, const Ctrl& h, uint2* dfinal, uint2* vfinal,
+                 cudaStream_t st)
+{
+    FZ_CUDA(cudaMemsetAsync(&W.ctrl()->ticket, 0, sizeof(uint32_t), st));
+    a.rescan = 1;
+    a.dstage = dfinal;
+    a.vstage = vfinal;
+    a.dcap = h.nd;
+    a.vcap = h.nv;
+    FZ_CUDA(launch_compress(a, st));
+    return FZ_OK;
+}
+
+void write_header_host(uint8_t* h, const fz_shape& s, uint64_t n, uint64_t T, const fz_params& p,
+                       const fz_counts& c, uint64_t total)
+{
+    memset(h, 0, 128);
+    memcpy(h, "FZB2", 4);
+    const uint16_t ver = 1, fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u));
+    memcpy(h + 4, &ver, 2);
+    memcpy(h + 6, &fl, 2);
+    h[8] = (uint8_t)s.ndim;
+    for (uint32_t k = 0; k < 3; ++k) {
+        uint64_t d = k < s.ndim ? s.dims[k] : 1;
+        memcpy(h + 16 + 8 * k, &d, 8);
+    }
+    memcpy(h + 40, &n, 8);
+    memcpy(h + 48, &p.eb_input, 8);
+    memcpy(h + 56, &p.eb_abs, 8);
+    memcpy(h + 64, &p.w, 4);
+    memcpy(h + 68, &p.r, 4);
+    memcpy(h + 72, &p.mn, 4);
+    memcpy(h + 76, &p.mx, 4);
+    uint64_t cnt[5] = {T, c.nnz, c.n_delta, c.n_value, total};
+    memcpy(h + 80, cnt, 40);
+}
+
+fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params* hp, int mode,
+                        double eb, void* d_out, size_t out_cap, size_t* out_size, void* d_work,
+                        size_t work_bytes, cudaStream_t st)
+{
+    uint64_t n;
+    if (!shape_n(s, &n) || d_field == nullptr || d_out == nullptr || out_size == nullptr ||
+        d_work == nullptr || !aligned16(d_field) || !aligned16(d_out) || !aligned16(d_work))
+        return FZ_ERR_ARG;
+    if (hp == nullptr && (!(eb > 0.0) || !std::isfinite(eb) || (mode != FZ_EB_ABS && mode != FZ_EB_REL)))
+        return FZ_ERR_ARG;
+    const uint64_t T = tiles_of(n);
+    Work W{compress_layout(n, T), static_cast<uint8_t*>(d_work)};
+    if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
+    const Geom g = geom_of(*s, n);
+    uint8_t* out = static_cast<uint8_t*>(d_out);
+
+    FZ_CUDA(launch_init(W.ctrl(), W.status(), (uint32_t)T, hp, st));
+    if (hp == nullptr) {
+        FZ_CUDA(launch_range(d_field, n, W.ctrl(), st));
+        FZ_CUDA(launch_params(W.ctrl(), mode, eb, n, st));
+    }
+    CompressArgs a = make_args(W, d_field, 0, g, 0, (uint32_t)T);
+    const uint64_t fbase = kHeaderBytes, pbase = kHeaderBytes + 32 * T;
+    a.flags_out = out + fbase;
+    a.flags_cap = out_cap > fbase ? out_cap - fbase : 0;
+    a.payload_out = out + pbase;
+    a.payload_cap = out_cap > pbase ? out_cap - pbase : 0;
+    FZ_CUDA(launch_compress(a, st));
+    FZ_CUDA(launch_finalize(out, out_cap, *s, n, T, W.dstage(), W.vstage(), W.ctrl(), st));
+    Ctrl h;
+    fz_status rs = read_ctrl(W, &h, st);
+    if (rs != FZ_OK) return rs;
+    if (h.err != 0) return (fz_status)h.err;
+    *out_size = (size_t)h.total;
+    if (h.total > out_cap) return FZ_ERR_CAPACITY;
+    if (h.stage_overflow) {
+        const uint64_t dbase = pbase + 16 * h.nnz, vbase = dbase + 8 * h.nd;
+        rs = rescan(W, a, h, reinterpret_cast<uint2*>(out + dbase), reinterpret_cast<uint2*>(out + vbase), st);
+        if (rs != FZ_OK) return rs;
+        FZ_CUDA(cudaStreamSynchronize(st));
+    }
+    return FZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t fz_compress_bound(const fz_shape* s)
+{
+    uint64_t n;
+    if (!shape_n(s, &n)) return 0;
+    const uint64_t T = tiles_of(n);
+    return (size_t)(kHeaderBytes + 32 * T + 4096 * T + 16 * n);
+}
+
+size_t fz_workspace_bytes(const fz_shape* s)
+{
+    uint64_t n;
+    if (!shape_n(s, &n)) return 0;
+    return compress_layout(n, tiles_of(n)).total;
+}
+
+size_t fz_decompress_workspace_bytes(const fz_shape* s)
+{
+    uint64_t n;
+    if (!shape_n(s, &n)) return 0;
+    return decode_layout(*s).total;
+}
+
+fz_status fz_derive_params(float mn, float mx, int eb_mode, double eb, fz_params* p)
+{
+    if (p == nullptr) return FZ_ERR_ARG;
+    return (fz_status)derive_params(mn, mx, eb_mode, eb, p);
+}
+
+fz_status fz_compress(const float* d_field, const fz_shape* s, int eb_mode, double eb, void* d_out,
+                      size_t out_cap, size_t* out_size, void* d_work, size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    return compress_impl(d_field, s, nullptr, eb_mode, eb, d_out, out_cap, out_size, d_work,
+                         work_bytes, static_cast<cudaStream_t>(stream));
+}
+
+fz_status fz_compress_with_params(const float* d_field, const fz_shape* s, const fz_params* p,
+                                  void* d_out, size_t out_cap, size_t* out_size, void* d_work,
+                                  size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    if (p == nullptr || !(p->w >= 1.17549435e-38f) || !std::isfinite(p->w)) return FZ_ERR_ARG;
+    return compress_impl(d_field, s, p, (int)p->mode, p->eb_input, d_out, out_cap, out_size, d_work,
+                         work_bytes, static_cast<cudaStream_t>(stream));
+}
+
+fz_status fz_peek_header(const void* h_hdr, size_t nbytes, fz_info* info)
+{
+    if (h_hdr == nullptr || info == nullptr || nbytes < kHeaderBytes) return FZ_ERR_ARG;
+    const uint8_t* h = static_cast<const uint8_t*>(h_hdr);
+    fz_info I{};
+    if (memcmp(h, "FZB2", 4) != 0) return FZ_ERR_CORRUPT;
+    uint16_t ver, fl;
+    memcpy(&ver, h + 4, 2);
+    memcpy(&fl, h + 6, 2);
+    if (ver != 1) return FZ_ERR_CORRUPT;
+    I.version = ver;
+    I.flags = fl;
+    I.shape.ndim = h[8];
+    if (I.shape.ndim < 1 || I.shape.ndim > 3) return FZ_ERR_CORRUPT;
+    for (int k = 0; k < 3; ++k) memcpy(&I.shape.dims[k], h + 16 + 8 * k, 8);
+    for (uint32_t k = I.shape.ndim; k < 3; ++k) {
+        if (I.shape.dims[k] != 1) return FZ_ERR_CORRUPT;
+        I.shape.dims[k] = 0;
+    }
+    uint64_t n;
+    if (!shape_n(&I.shape, &n)) return FZ_ERR_CORRUPT;
+    for (uint32_t k = I.shape.ndim; k < 3; ++k) I.shape.dims[k] = 1;
+    memcpy(&I.n, h + 40, 8);
+    if (I.n != n) return FZ_ERR_CORRUPT;
+    memcpy(&I.params.eb_input, h + 48, 8);
+    memcpy(&I.params.eb_abs, h + 56, 8);
+    memcpy(&I.params.w, h + 64, 4);
+    memcpy(&I.params.r, h + 68, 4);
+    memcpy(&I.params.mn, h + 72, 4);
+    memcpy(&I.params.mx, h + 76, 4);
+    I.params.mode = (fl & 1u) ? FZ_EB_REL : FZ_EB_ABS;
+    I.params.fallback = (fl & 2u) ? 1u : 0u;
+    if (!(I.params.w > 0.0f) || !std::isfinite(I.params.w)) return FZ_ERR_CORRUPT;
+    uint64_t cnt[5];
+    memcpy(cnt, h + 80, 40);
+    I.tiles = cnt[0];
+    I.counts.nnz = cnt[1];
+    I.counts.n_delta = cnt[2];
+    I.counts.n_value = cnt[3];
+    I.total_size = cnt[4];
+    if (I.tiles != tiles_of(n)) return FZ_ERR_CORRUPT;
+    if (I.counts.nnz > I.tiles * kTileBlocks || I.counts.n_delta > n || I.counts.n_value > n)
+        return FZ_ERR_CORRUPT;
+    if (I.total_size != kHeaderBytes + 32 * I.tiles + 16 * I.counts.nnz + 8 * I.counts.n_delta +
+                            8 * I.counts.n_value)
+        return FZ_ERR_CORRUPT;
+    *info = I;
+    return FZ_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int32_t* d_q, uint64_t n,
+                          void* d_work, size_t work_bytes, cudaStream_t st)
+{
+    if (d_in == nullptr || (d_field == nullptr && d_q == nullptr) || d_work == nullptr ||
+        !aligned16(d_in) || !aligned16(d_work) || in_size < kHeaderBytes)
+        return FZ_ERR_ARG;
+    uint8_t hdr[128];
+    FZ_CUDA(cudaMemcpyAsync(hdr, d_in, 128, cudaMemcpyDeviceToHost, st));
+    FZ_CUDA(cudaStreamSynchronize(st));
+    fz_info I;
+    fz_status rs = fz_peek_header(hdr, 128, &I);
+    if (rs != FZ_OK) return rs;
+    if (I.n != n) return FZ_ERR_ARG;
+    if (in_size < I.total_size) return FZ_ERR_CORRUPT;
+    const DecodeLayout L = decode_layout(I.shape);
+    if (work_bytes < L.total) return FZ_ERR_WORKSPACE;
+    uint8_t* wb = static_cast<uint8_t*>(d_work);
+    Ctrl* ctrl = reinterpret_cast<Ctrl*>(wb + L.ctrl);
+    auto* st_nnz = reinterpret_cast<unsigned long long*>(wb + L.st_nnz);
+    auto* st_x = reinterpret_cast<unsigned long long*>(wb + L.st_x);
+    auto* sums = reinterpret_cast<uint32_t*>(wb + L.sums);
+    const uint8_t* in = static_cast<const uint8_t*>(d_in);
+    const uint64_t T = I.tiles;
+    const uint64_t pbase = kHeaderBytes + 32 * T, dbase = pbase + 16 * I.counts.nnz,
+                   vbase = dbase + 8 * I.counts.n_delta;
+    const uint2* drec = reinterpret_cast<const uint2*>(in + dbase);
+    const uint2* vrec = reinterpret_cast<const uint2*>(in + vbase);
+    const Geom g = geom_of(I.shape, n);
+    int32_t* q = d_q ? d_q : reinterpret_cast<int32_t*>(d_field);
+    const bool deq = d_q == nullptr;
+
+    FZ_CUDA(launch_decode_init(ctrl, st_nnz, st_x, (uint32_t)T, st));
+    FZ_CUDA(launch_validate_outliers(drec, I.counts.n_delta, n, ctrl, st));
+    FZ_CUDA(launch_validate_outliers(vrec, I.counts.n_value, n, ctrl, st));
+    DecodeArgs a{};
+    a.flags = in + kHeaderBytes;
+    a.payload = in + pbase;
+    a.drec = drec;
+    a.nnz_total = I.counts.nnz;
+    a.nd = I.counts.n_delta;
+    a.g = g;
+    a.tiles = (uint32_t)T;
+    a.w = I.params.w;
+    a.q_out = q;
+    a.x_out = (deq && I.shape.ndim == 1) ? d_field : nullptr;
+    a.st_nnz = st_nnz;
+    a.st_x = st_x;
+    a.ctrl = ctrl;
+    FZ_CUDA(launch_decode_tiles(a, st));
+    const float wq = deq ? I.params.w : 0.0f;
+    if (I.shape.ndim == 2) {
+        FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1], sums, wq, st));
+    } else if (I.shape.ndim == 3) {
+        FZ_CUDA(launch_scan_axis(q, I.shape.dims[0], I.shape.dims[1], I.shape.dims[2], sums, 0.0f, st));
+        FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], sums, wq, st));
+    }
+    if (deq) FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+    Ctrl h;
+    FZ_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    FZ_CUDA(cudaStreamSynchronize(st));
+    if (h.err != 0) return (fz_status)h.err;
+    if (h.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;   // sum of popcount(flags) == nnz
+    return FZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fz_status fz_decompress(const void* d_in, size_t in_size, float* d_field, uint64_t n, void* d_work,
+                        size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    if (d_field == nullptr || !aligned16(d_field)) return FZ_ERR_ARG;
+    return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
+                           static_cast<cudaStream_t>(stream));
+}
+
+fz_status fz_debug_decode_q(const void* d_in, size_t in_size, int32_t* d_q, uint64_t n, void* d_work,
+                            size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    if (d_q == nullptr || !aligned16(d_q)) return FZ_ERR_ARG;
+    return decompress_impl(d_in, in_size, nullptr, d_q, n, d_work, work_bytes,
+                           static_cast<cudaStream_t>(stream));
+}
+
+fz_status fz_compress_host(const float* h_field, const fz_shape* s, int eb_mode, double eb, void* h_out,
+                           size_t out_cap, size_t* out_size, float* d_field_scratch, void* d_out_scratch,
+                           size_t d_out_cap, void* d_work, size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    uint64_t n;
+    if (!shape_n(s, &n) || h_field == nullptr || h_out == nullptr || out_size == nullptr)
+        return FZ_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FZ_CUDA(cudaMemcpyAsync(d_field_scratch, h_field, 4 * n, cudaMemcpyHostToDevice, st));
+    fz_status rs = compress_impl(d_field_scratch, s, nullptr, eb_mode, eb, d_out_scratch, d_out_cap,
+                                 out_size, d_work, work_bytes, st);
+    if (rs != FZ_OK) return rs;
+    if (*out_size > out_cap) return FZ_ERR_CAPACITY;
+    FZ_CUDA(cudaMemcpyAsync(h_out, d_out_scratch, *out_size, cudaMemcpyDeviceToHost, st));
+    FZ_CUDA(cudaStreamSynchronize(st));
+    return FZ_OK;
+}
+
+fz_status fz_decompress_host(const void* h_in, size_t in_size, float* h_field, uint64_t n,
+                             void* d_in_scratch, float* d_field_scratch, void* d_work, size_t work_bytes,
+                             void* stream)
+{
+    LaunchScope ls;
+    if (h_in == nullptr || h_field == nullptr) return FZ_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FZ_CUDA(cudaMemcpyAsync(d_in_scratch, h_in, in_size, cudaMemcpyHostToDevice, st));
+    fz_status rs = decompress_impl(d_in_scratch, in_size, d_field_scratch, nullptr, n, d_work,
+                                   work_bytes, st);
+    if (rs != FZ_OK) return rs;
+    FZ_CUDA(cudaMemcpyAsync(h_field, d_field_scratch, 4 * n, cudaMemcpyDeviceToHost, st));
+    FZ_CUDA(cudaStreamSynchronize(st));
+    return FZ_OK;
+}
+
+const char* fz_strerror(int status)
+{
+    switch (status) {
+        case FZ_OK: return "ok";
+        case FZ_ERR_ARG: return "invalid argument";
+        case FZ_ERR_NONFINITE: return "non-finite value in the field";
+        case FZ_ERR_EB_TOO_SMALL: return "error bound too small for fp32";
+        case FZ_ERR_CAPACITY: return "output buffer too small";
+        case FZ_ERR_CORRUPT: return "corrupt stream";
+        case FZ_ERR_WORKSPACE: return "workspace too small";
+        case FZ_ERR_CUDA: return "CUDA error";
+        default: return "unknown status";
+    }
+}
+
+const char* fz_last_cuda_error(void) { return g_cuda_err; }
+
+int fz_last_launch_count(void) { return g_last_launches; }
+
+// ---------------------------------------------------------------------------------------
+// Slab API (multi-GPU z-slabs, SV §8.e)
+// ---------------------------------------------------------------------------------------
+fz_status fz_slab_range(const float* d_slab, uint64_t n, float* h_min, float* h_max, int64_t* h_first_bad,
+                        void* d_work, size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    if (d_slab == nullptr || !aligned16(d_slab) || d_work == nullptr || work_bytes < 512 || n == 0)
+        return FZ_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Ctrl* ctrl = static_cast<Ctrl*>(d_work);
+    FZ_CUDA(launch_init(ctrl, nullptr, 0, nullptr, st));
+    FZ_CUDA(launch_range(d_slab, n, ctrl, st));
+    Ctrl h;
+    FZ_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    FZ_CUDA(cudaStreamSynchronize(st));
+    if (h_min) *h_min = ord2f(h.mn_enc);
+    if (h_max) *h_max = ord2f(h.mx_enc);
+    if (h_first_bad) *h_first_bad = h.first_bad == ~0ull ? -1 : (int64_t)h.first_bad;
+    return h.first_bad == ~0ull ? FZ_OK : FZ_ERR_NONFINITE;
+}
+
+size_t fz_slab_stage_bound(const fz_shape* global, uint64_t tb, uint64_t te)
+{
+    uint64_t n;
+    if (!shape_n(global, &n) || te <= tb || te > tiles_of(n)) return 0;
+    const uint64_t nt = te - tb;
+    const uint64_t e1 = te * kTileCodes < n ? te * kTileCodes : n;
+    const uint64_t elems = e1 - tb * kTileCodes;
+    return (size_t)(32 * nt + 4096 * nt + 16 * elems);
+}
+
+fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t slab_elems,
+                           const fz_shape* global, uint64_t tb, uint64_t te, const fz_params* p,
+                           void* d_stage, size_t stage_cap, fz_counts* h_counts, void* d_work,
+                           size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    uint64_t n;
+    if (!shape_n(global, &n) || d_slab == nullptr || p == nullptr || d_stage == nullptr ||
+        h_counts == nullptr || d_work == nullptr || !aligned16(d_slab) || !aligned16(d_stage) ||
+        !aligned16(d_work) || (slab_first & 3) != 0)
+        return FZ_ERR_ARG;
+    const uint64_t T = tiles_of(n);
+    if (te <= tb || te > T) return FZ_ERR_ARG;
+    const Geom g = geom_of(*global, n);
+    const uint64_t halo = (uint64_t)(global->ndim == 3 ? g.P : 0) + (global->ndim >= 2 ? g.nx : 0) + 1;
+    const uint64_t need_lo = tb * kTileCodes > halo ? tb * kTileCodes - halo : 0;
+    const uint64_t need_hi = te * kTileCodes < n ? te * kTileCodes : n;
+    if (slab_first > need_lo || slab_first + slab_elems < need_hi) return FZ_ERR_ARG;
+    Work W{compress_layout(n, T), static_cast<uint8_t*>(d_work)};
+    if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t nt = te - tb;
+    uint8_t* stage = static_cast<uint8_t*>(d_stage);
+
+    FZ_CUDA(launch_init(W.ctrl(), W.status() + tb, (uint32_t)nt, p, st));
+    CompressArgs a = make_args(W, d_slab, slab_first, g, (uint32_t)tb, (uint32_t)te);
+    a.flags_out = stage;
+    a.flags_cap = stage_cap < 32 * nt ? stage_cap : 32 * nt;
+    a.payload_out = stage + 32 * nt;
+    a.payload_cap = stage_cap > 32 * nt ? stage_cap - 32 * nt : 0;
+    FZ_CUDA(launch_compress(a, st));
+    Ctrl h;
+    fz_status rs = read_ctrl(W, &h, st);
+    if (rs != FZ_OK) return rs;
+    if (h.err != 0) return (fz_status)h.err;
+    h_counts->nnz = h.nnz;
+    h_counts->n_delta = h.nd;
+    h_counts->n_value = h.nv;
+    const uint64_t dbase = 32 * nt + 16 * h.nnz, vbase = dbase + 8 * h.nd, need = vbase + 8 * h.nv;
+    if (need > stage_cap) return FZ_ERR_CAPACITY;
+    if (h.stage_overflow) {
+        rs = rescan(W, a, h, reinterpret_cast<uint2*>(stage + dbase), reinterpret_cast<uint2*>(stage + vbase), st);
+        if (rs != FZ_OK) return rs;
+    } else {
+        if (h.nd) FZ_CUDA(cudaMemcpyAsync(stage + dbase, W.dstage(), 8 * h.nd, cudaMemcpyDeviceToDevice, st));
+        if (h.nv) FZ_CUDA(cudaMemcpyAsync(stage + vbase, W.vstage(), 8 * h.nv, cudaMemcpyDeviceToDevice, st));
+    }
+    FZ_CUDA(cudaStreamSynchronize(st));
+    return FZ_OK;
+}
+
+fz_status fz_slab_place(const void* d_stage, const fz_shape* global, uint64_t tb, uint64_t te,
+                        const fz_counts* local, const fz_counts* before, const fz_counts* totals,
+                        const fz_params* p, int write_header, void* d_out, size_t out_cap, void* stream)
+{
+    LaunchScope ls;
+    uint64_t n;
+    if (!shape_n(global, &n) || d_stage == nullptr || local == nullptr || before == nullptr ||
+        totals == nullptr || d_out == nullptr || (write_header && p == nullptr))
+        return FZ_ERR_ARG;
+    const uint64_t T = tiles_of(n);
+    if (te <= tb || te > T) return FZ_ERR_ARG;
+    const uint64_t nt = te - tb;
+    const uint64_t total = kHeaderBytes + 32 * T + 16 * totals->nnz + 8 * totals->n_delta + 8 * totals->n_value;
+    if (total > out_cap) return FZ_ERR_CAPACITY;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint8_t* s8 = static_cast<const uint8_t*>(d_stage);
+    uint8_t* o = static_cast<uint8_t*>(d_out);
+    const uint64_t pbase = kHeaderBytes + 32 * T, dbase = pbase + 16 * totals->nnz,
+                   vbase = dbase + 8 * totals->n_delta;
+    const uint64_t sd = 32 * nt + 16 * local->nnz, sv = sd + 8 * local->n_delta;
+    FZ_CUDA(cudaMemcpyAsync(o + kHeaderBytes + 32 * tb, s8, 32 * nt, cudaMemcpyDeviceToDevice, st));
+    if (local->nnz)
+        FZ_CUDA(cudaMemcpyAsync(o + pbase + 16 * before->nnz, s8 + 32 * nt, 16 * local->nnz, cudaMemcpyDeviceToDevice, st));
+    if (local->n_delta)
+        FZ_CUDA(cudaMemcpyAsync(o + dbase + 8 * before->n_delta, s8 + sd, 8 * local->n_delta, cudaMemcpyDeviceToDevice, st));
+    if (local->n_value)
+        FZ_CUDA(cudaMemcpyAsync(o + vbase + 8 * before->n_value, s8 + sv, 8 * local->n_value, cudaMemcpyDeviceToDevice, st));
+    if (write_header) {
+        uint8_t h[128];
+        write_header_host(h, *global, n, T, *p, *totals, total);
+        FZ_CUDA(cudaMemcpyAsync(o, h, 128, cudaMemcpyHostToDevice, st));
+    }
+    FZ_CUDA(cudaStreamSynchronize(st));
+    return FZ_OK;
+}
+
+fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_params* p, uint16_t* d_codes,
+                            uint32_t* d_didx, int32_t* d_dval, uint64_t dcap, uint64_t* h_nd,
+                            uint32_t* d_vidx, uint32_t* d_vbits, uint64_t vcap, uint64_t* h_nv,
+                            void* d_work, size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    uint64_t n;
+    if (!shape_n(s, &n) || d_field == nullptr || p == nullptr || d_codes == nullptr || h_nd == nullptr ||
+        h_nv == nullptr || !aligned16(d_field) || !aligned16(d_work))
+        return FZ_ERR_ARG;
+    const uint64_t T = tiles_of(n);
+    Work W{compress_layout(n, T), static_cast<uint8_t*>(d_work)};
+    if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FZ_CUDA(launch_init(W.ctrl(), W.status(), (uint32_t)T, p, st));
+    CompressArgs a = make_args(W, d_field, 0, geom_of(*s, n), 0, (uint32_t)T);
+    a.codes_out = d_codes;
+    a.o_didx = d_didx;
+    a.o_dval = d_dval;
+    a.o_vidx = d_vidx;
+    a.o_vbits = d_vbits;
+    a.dcap = dcap;
+    a.vcap = vcap;
+    FZ_CUDA(launch_compress(a, st));
+    Ctrl h;
+    fz_status rs = read_ctrl(W, &h, st);
+    if (rs != FZ_OK) return rs;
+    if (h.err != 0) return (fz_status)h.err;
+    *h_nd = h.nd;
+    *h_nv = h.nv;
+    return (h.nd > dcap || h.nv > vcap) ? FZ_ERR_CAPACITY : FZ_OK;
+}
+
+}  // extern "C"

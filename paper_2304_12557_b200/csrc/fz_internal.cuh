@@ -1,0 +1,286 @@
+// fz_internal.cuh -- device-side building blocks of libfz (B200, sm_100a).
+//
+// Nothing here is shared with oracle/: the oracle is an independent C program.
+// Citation key: P:n = PAPER.md line n; SV = SURVEY.md; R# = DESIGN.md §3 readings.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/fz.h"
+
+namespace fz {
+
+constexpr int kTileCodes = 2048;   // 32x32 u32 words, 2 codes per word
+constexpr int kTileWords = 1024;
+constexpr int kTileBlocks = 256;   // 16-byte blocks per tile (P:253, 256 byte flags)
+constexpr int kCta = 256;          // threads per CTA: one 16-byte block per thread
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr size_t kHeaderBytes = 128;
+
+// ------------------------------------------------------------------------------------
+// Device control block (first 512 bytes of every workspace).
+// ------------------------------------------------------------------------------------
+struct Ctrl {
+    // range pass (C0)
+    uint32_t mn_enc, mx_enc;         // order-preserving encodings of min / max
+    unsigned long long first_bad;    // first non-finite index, ~0 if none
+    // parameters (Appendix A), written by k_params or k_init
+    fz_params p;
+    float h;                         // w / 2
+    int32_t err;                     // fz_status of the device-side steps
+    uint32_t ticket;                 // persistent-tile ticket
+    uint32_t stage_overflow;         // outlier staging overflowed -> rescan pass
+    // results (written by the last tile / k_finalize)
+    unsigned long long nnz, nd, nv, total;
+    uint32_t ticket2;                // decoder x-scan ticket
+    uint32_t pad;
+};
+static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
+
+// Workspace carve (host computes it identically for every call).
+struct Layout {
+    size_t ctrl, status, aggv, inclv, tpre, dstage, vstage, total;
+    uint64_t dcap, vcap;             // staging capacities in records
+};
+
+inline Layout compress_layout(uint64_t n, uint64_t tiles)
+{
+    Layout L{};
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    size_t off = 0;
+    L.ctrl = off;   off += 512;
+    L.status = off; off = al(off + 8 * tiles);
+    L.aggv = off;   off = al(off + 4 * tiles);
+    L.inclv = off;  off = al(off + 4 * tiles);
+    L.tpre = off;   off = al(off + 8 * tiles);
+    L.dcap = n / 64 + 1024;
+    L.vcap = n / 64 + 1024;
+    L.dstage = off; off = al(off + 8 * L.dcap);
+    L.vstage = off; off = al(off + 8 * L.vcap);
+    L.total = off;
+    return L;
+}
+
+// ------------------------------------------------------------------------------------
+// Order-preserving float <-> u32 (for atomicMin/Max of the range).
+// ------------------------------------------------------------------------------------
+__host__ __device__ inline uint32_t f2ord(float f)
+{
+    uint32_t b;
+#ifdef __CUDA_ARCH__
+    b = __float_as_uint(f);
+#else
+    memcpy(&b, &f, 4);
+#endif
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__host__ __device__ inline float ord2f(uint32_t u)
+{
+    uint32_t b = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+    float f;
+#ifdef __CUDA_ARCH__
+    f = __uint_as_float(b);
+#else
+    memcpy(&f, &b, 4);
+#endif
+    return f;
+}
+
+// ------------------------------------------------------------------------------------
+// Memory-model helpers for the decoupled look-back (gpu scope).
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p)
+{
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// 16-byte streaming load of the read-only field.
+__device__ __forceinline__ float4 ldg_f4(const float* p)
+{
+    return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+// ------------------------------------------------------------------------------------
+// 32x32 bit transpose across an 8-lane group (C5).
+// Lane k (= lane & 7) of the group holds words v[4k+i], i = 0..3, of one 32-word row
+// (row c of A for the shuffle, column c of O for the un-shuffle).  Afterwards lane k
+// holds T[4k+i] with T[r] bit j = v[j] bit r.  Each stage swaps word-index bit s with
+// bit-position bit s; stages commute.  Stages 16/8/4 cross lanes (shfl_xor 4/2/1),
+// stages 2/1 stay in registers.  ~6.5 ALU + 1.5 SHFL lane-ops per element.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void xpose_pair(uint32_t& lo, uint32_t& hi, int s, uint32_t m)
+{
+    uint32_t t = ((lo >> s) ^ hi) & m;
+    hi ^= t;
+    lo ^= t << s;
+}
+
+__device__ __forceinline__ void transpose32_group8(uint32_t (&a)[4], int k)
+{
+#pragma unroll
+    for (int st = 0; st < 3; ++st) {
+        const int s = 16 >> st;
+        const int lm = s >> 2;
+        const uint32_t m = st == 0 ? 0x0000FFFFu : (st == 1 ? 0x00FF00FFu : 0x0F0F0F0Fu);
+        const bool lower = (k & lm) == 0;
+        const uint32_t keep = lower ? m : ~m;
+        const int rot = lower ? s : 32 - s;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            uint32_t p = __shfl_xor_sync(kFull, a[i], lm);
+            // lower: (a & m) | ((p << s) & ~m); upper: (a & ~m) | ((p >> s) & m).
+            // A rotate puts the wanted bits in place; wrapped bits fall in the kept field.
+            uint32_t r = __funnelshift_l(p, p, rot);
+            a[i] = (a[i] & keep) | (r & ~keep);
+        }
+    }
+    xpose_pair(a[0], a[2], 2, 0x33333333u);
+    xpose_pair(a[1], a[3], 2, 0x33333333u);
+    xpose_pair(a[0], a[1], 1, 0x55555555u);
+    xpose_pair(a[2], a[3], 1, 0x55555555u);
+}
+
+// ------------------------------------------------------------------------------------
+// C1 prequantization, exact nearest bin with ties to even (R1, R3), fp32
+// IEEE ops with explicit rounding (no contraction, no fast-math):
+//   v = fl(d*r); t = fl(v + 1.5*2^23); q = bits(t) - bits(1.5*2^23); e = fma(-q, w, d)
+//   exactly; +-1 correction; then the bound check |fl(fl(q)*w) - d| <= eb (R20).
+// Returns q; *vout = value outlier.
+// ------------------------------------------------------------------------------------
+struct QuantP {
+    float w, r, h, eb32;
+};
+
+__device__ __forceinline__ int prequant(float d, const QuantP& P, bool& vout)
+{
+    const float kMagic = 12582912.0f;   // 1.5 * 2^23
+    float v = __fmul_rn(d, P.r);
+    bool big = fabsf(v) >= 4194302.0f;  // 2^22 - 2: magic rounding no longer exact
+    float t = __fadd_rn(v, kMagic);
+    int q = __float_as_int(t) - 0x4B400000;
+    float qf = __fsub_rn(t, kMagic);
+    float e = __fmaf_rn(-qf, P.w, d);   // exact residual d - q*w
+    int adj = (e > P.h) - (e < -P.h);
+    if (fabsf(e) == P.h && (q & 1)) adj = e > 0.0f ? 1 : -1;
+    q += adj;
+    bool toolarge = big || (q >= 2097152) || (q <= -2097152);   // |q| >= 2^21
+    if (toolarge) q = 0;
+    float qq = __fsub_rn(__int_as_float(q + 0x4B400000), kMagic);   // exact fl32(q)
+    float xh = __fmul_rn(qq, P.w);
+    float diff = __fsub_rn(xh, d);
+    vout = toolarge || (fabsf(diff) > P.eb32);
+    return q;
+}
+
+// q only (halo elements): identical arithmetic, no bound check.
+__device__ __forceinline__ int prequant_q(float d, const QuantP& P)
+{
+    const float kMagic = 12582912.0f;
+    float v = __fmul_rn(d, P.r);
+    bool big = fabsf(v) >= 4194302.0f;
+    float t = __fadd_rn(v, kMagic);
+    int q = __float_as_int(t) - 0x4B400000;
+    float qf = __fsub_rn(t, kMagic);
+    float e = __fmaf_rn(-qf, P.w, d);
+    int adj = (e > P.h) - (e < -P.h);
+    if (fabsf(e) == P.h && (q & 1)) adj = e > 0.0f ? 1 : -1;
+    q += adj;
+    if (big || q >= 2097152 || q <= -2097152) q = 0;
+    return q;
+}
+
+// ------------------------------------------------------------------------------------
+// Parameter derivation (Appendix A, R2/R4/R17), used on the host (fz_derive_params,
+// slab API) and on the device (k_params).  Compiled with --fmad=false on the device and
+// -ffp-contract=off on the host: every f64 op is one IEEE rounding on both sides.
+// ------------------------------------------------------------------------------------
+__host__ __device__ inline float rd32(double t)
+{
+    float f = (float)t;
+    if ((double)f > t) f = nextafterf(f, -INFINITY);
+    return f;
+}
+
+__host__ __device__ inline int derive_params(float mn, float mx, int mode, double eb,
+                                             fz_params* p)
+{
+    if (!(eb > 0.0) || !isfinite(eb)) return FZ_ERR_ARG;
+    if (mode != FZ_EB_ABS && mode != FZ_EB_REL) return FZ_ERR_ARG;
+    double eb_abs = eb;
+    if (mode == FZ_EB_REL && !(mx == mn)) eb_abs = eb * ((double)mx - (double)mn);
+    if (!(eb_abs > 0.0) || !isfinite(eb_abs)) return FZ_ERR_EB_TOO_SMALL;
+    float M = fmaxf(fabsf(mn), fabsf(mx));
+    double U = 0.0;
+    if (M > 0.0f) {
+        int e;
+        frexp((double)M, &e);
+        U = ldexp(1.0, e - 23);
+    }
+    float w = rd32(2.0 * eb_abs - U);
+    uint32_t fallback = 0;
+    if (!(w > 0.0f && (double)M * (1.0 / (double)w) < 2097151.0)) {
+        fallback = 1;
+        w = rd32(2.0 * eb_abs);
+    }
+    if (!(w >= 1.17549435e-38f)) return FZ_ERR_EB_TOO_SMALL;
+    p->eb_input = eb;
+    p->eb_abs = eb_abs;
+    p->w = w;
+    p->r = (float)(1.0 / (double)w);
+    p->eb32 = rd32(eb_abs);
+    p->mn = mn;
+    p->mx = mx;
+    p->mode = (uint32_t)mode;
+    p->fallback = fallback;
+    return FZ_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// Kernel argument bundles.
+// ------------------------------------------------------------------------------------
+struct Geom {
+    uint32_t n;       // global N
+    uint32_t nx;      // x extent (1-D: N)
+    uint32_t P;       // plane size (1-D/2-D: N)
+    uint32_t ndim;
+};
+
+struct CompressArgs {
+    const float* field;       // element g at field[g - base]
+    uint64_t base;
+    Geom g;
+    uint32_t tile_begin, tile_end;
+    uint8_t* flags_out;       // 32 B per tile, tile t at (t - tile_begin) * 32
+    uint8_t* payload_out;     // 16 B blocks
+    uint64_t flags_cap;       // bytes writable at flags_out
+    uint64_t payload_cap;     // bytes writable at payload_out
+    uint2* dstage;            // (idx, delta) records
+    uint2* vstage;            // (idx, bits) records
+    uint64_t dcap, vcap;      // staging capacities (records)
+    unsigned long long* status;
+    uint32_t* aggv;
+    uint32_t* inclv;
+    uint2* tpre;              // per-tile exclusive (n_delta, n_value)
+    Ctrl* ctrl;
+    uint16_t* codes_out;      // debug hook: codes at element index (may be null)
+    uint32_t* o_didx;         // debug hook: split outlier lists at final positions (may be null)
+    int32_t* o_dval;
+    uint32_t* o_vidx;
+    uint32_t* o_vbits;
+    int rescan;               // 1: outliers only, straight to final offsets via tpre
+};
+
+}  // namespace fz

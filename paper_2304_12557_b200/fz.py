@@ -1,0 +1,289 @@
+"""Thin ctypes binding of libfz.so (include/fz.h): argument marshalling only.
+
+Every step of the compression path runs in the CUDA kernels of libfz.so.  PyTorch provides
+device memory and streams.  There is no CPU fallback: if libfz.so is missing the import of
+this module's functions raises (run `python -m paper_2304_12557_b200.build` or
+`__graft_entry__.build()`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libfz.so")
+
+ABS, REL = 0, 1
+STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_EB_TOO_SMALL", 4: "ERR_CAPACITY",
+          5: "ERR_CORRUPT", 6: "ERR_WORKSPACE", 7: "ERR_CUDA"}
+OK, ERR_ARG, ERR_NONFINITE, ERR_EB_TOO_SMALL, ERR_CAPACITY, ERR_CORRUPT, ERR_WORKSPACE, ERR_CUDA = range(8)
+
+
+class FZError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = f"{where}: {STATUS.get(status, status)}"
+        if status == ERR_CUDA:
+            msg += " (" + lib().fz_last_cuda_error().decode() + ")"
+        super().__init__(msg)
+
+
+class Shape(C.Structure):
+    _fields_ = [("ndim", C.c_uint32), ("reserved", C.c_uint32), ("dims", C.c_uint64 * 3)]
+
+
+class Params(C.Structure):
+    _fields_ = [("eb_input", C.c_double), ("eb_abs", C.c_double), ("w", C.c_float), ("r", C.c_float),
+                ("eb32", C.c_float), ("mn", C.c_float), ("mx", C.c_float), ("mode", C.c_uint32),
+                ("fallback", C.c_uint32)]
+
+
+class Counts(C.Structure):
+    _fields_ = [("nnz", C.c_uint64), ("n_delta", C.c_uint64), ("n_value", C.c_uint64)]
+
+
+class Info(C.Structure):
+    _fields_ = [("shape", Shape), ("n", C.c_uint64), ("tiles", C.c_uint64), ("total_size", C.c_uint64),
+                ("counts", Counts), ("params", Params), ("version", C.c_uint32), ("flags", C.c_uint32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libfz.so (fails loudly when the CUDA library has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libfz.so not built at {LIB_PATH}; run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    P, S, u64, i = C.c_void_p, C.c_size_t, C.c_uint64, C.c_int
+    pS, pP, pC = C.POINTER(Shape), C.POINTER(Params), C.POINTER(Counts)
+    sig = {
+        "fz_compress_bound": ([pS], S),
+        "fz_workspace_bytes": ([pS], S),
+        "fz_decompress_workspace_bytes": ([pS], S),
+        "fz_derive_params": ([C.c_float, C.c_float, i, C.c_double, pP], i),
+        "fz_compress": ([P, pS, i, C.c_double, P, S, C.POINTER(S), P, S, P], i),
+        "fz_compress_with_params": ([P, pS, pP, P, S, C.POINTER(S), P, S, P], i),
+        "fz_decompress": ([P, S, P, u64, P, S, P], i),
+        "fz_compress_host": ([P, pS, i, C.c_double, P, S, C.POINTER(S), P, P, S, P, S, P], i),
+        "fz_decompress_host": ([P, S, P, u64, P, P, P, S, P], i),
+        "fz_peek_header": ([P, S, C.POINTER(Info)], i),
+        "fz_strerror": ([i], C.c_char_p),
+        "fz_last_cuda_error": ([], C.c_char_p),
+        "fz_slab_range": ([P, u64, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_int64), P, S, P], i),
+        "fz_slab_stage_bound": ([pS, u64, u64], S),
+        "fz_slab_compress": ([P, u64, u64, pS, u64, u64, pP, P, S, pC, P, S, P], i),
+        "fz_slab_place": ([P, pS, u64, u64, pC, pC, pC, pP, i, P, S, P], i),
+        "fz_debug_quantize": ([P, pS, pP, P, P, P, u64, C.POINTER(u64), P, P, u64, C.POINTER(u64), P, S, P], i),
+        "fz_debug_decode_q": ([P, S, P, u64, P, S, P], i),
+        "fz_last_launch_count": ([], i),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        raise FZError(st, where)
+
+
+def make_shape(dims) -> Shape:
+    dims = tuple(int(d) for d in dims)
+    s = Shape()
+    s.ndim = len(dims)
+    for k in range(3):
+        s.dims[k] = dims[k] if k < len(dims) else 1
+    return s
+
+
+def _ptr(t) -> int:
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def compress_bound(dims) -> int:
+    return lib().fz_compress_bound(C.byref(make_shape(dims)))
+
+
+def workspace_bytes(dims) -> int:
+    return lib().fz_workspace_bytes(C.byref(make_shape(dims)))
+
+
+def decompress_workspace_bytes(dims) -> int:
+    return lib().fz_decompress_workspace_bytes(C.byref(make_shape(dims)))
+
+
+def derive_params(mn: float, mx: float, mode: int, eb: float) -> Params:
+    p = Params()
+    _check(lib().fz_derive_params(mn, mx, mode, eb, C.byref(p)), "fz_derive_params")
+    return p
+
+
+def last_launch_count() -> int:
+    return lib().fz_last_launch_count()
+
+
+def _u8(n, device):
+    import torch
+    # 16-byte alignment: torch's caching allocator returns >= 512-byte aligned blocks
+    return torch.empty(max(int(n), 16), dtype=torch.uint8, device=device)
+
+
+class Codec:
+    """Holds device buffers for repeated compress/decompress of one shape (no allocation
+    inside the timed calls)."""
+
+    def __init__(self, dims, device="cuda"):
+        self.dims = tuple(int(d) for d in dims)
+        self.shape = make_shape(self.dims)
+        self.n = int(np.prod(self.dims))
+        self.device = device
+        self.cap = compress_bound(self.dims)
+        self.out = _u8(self.cap, device)
+        self.work = _u8(workspace_bytes(self.dims), device)
+        self.dwork = _u8(decompress_workspace_bytes(self.dims), device)
+
+    def compress(self, field, mode=REL, eb=1e-3, params: Params | None = None, stream=None):
+        """Returns (uint8 view of the stream, size)."""
+        size = C.c_size_t()
+        if params is None:
+            st = lib().fz_compress(_ptr(field), C.byref(self.shape), mode, eb, _ptr(self.out), self.cap,
+                                   C.byref(size), _ptr(self.work), self.work.numel(), _stream(stream))
+        else:
+            st = lib().fz_compress_with_params(_ptr(field), C.byref(self.shape), C.byref(params),
+                                               _ptr(self.out), self.cap, C.byref(size), _ptr(self.work),
+                                               self.work.numel(), _stream(stream))
+        _check(st, "fz_compress")
+        return self.out[: size.value], size.value
+
+    def decompress(self, buf, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty(self.dims, dtype=torch.float32, device=self.device)
+        st = lib().fz_decompress(_ptr(buf), buf.numel(), _ptr(out), self.n, _ptr(self.dwork),
+                                 self.dwork.numel(), _stream(stream))
+        _check(st, "fz_decompress")
+        return out
+
+
+def compress(field, mode=REL, eb=1e-3, params: Params | None = None, stream=None):
+    """fz_compress on a CUDA float32 tensor; returns a fresh uint8 tensor with the stream."""
+    codec = Codec(tuple(field.shape), field.device)
+    buf, size = codec.compress(field.contiguous(), mode, eb, params, stream)
+    return buf.clone()
+
+
+def decompress(buf, dims=None, stream=None):
+    import torch
+    info = peek_header(buf[:128].cpu().numpy().tobytes())
+    if dims is None:
+        dims = tuple(int(info.shape.dims[k]) for k in range(info.shape.ndim))
+    n = int(np.prod(dims))
+    out = torch.empty(dims, dtype=torch.float32, device=buf.device)
+    dwork = _u8(decompress_workspace_bytes(dims), buf.device)
+    st = lib().fz_decompress(_ptr(buf), buf.numel(), _ptr(out), n, _ptr(dwork), dwork.numel(), _stream(stream))
+    _check(st, "fz_decompress")
+    return out
+
+
+def peek_header(hdr: bytes) -> Info:
+    info = Info()
+    b = C.create_string_buffer(bytes(hdr), len(hdr))
+    _check(lib().fz_peek_header(b, len(hdr), C.byref(info)), "fz_peek_header")
+    return info
+
+
+def debug_quantize(field, params: Params, cap: int | None = None, stream=None):
+    """Stage hook C1-C3: (codes uint16, didx, dval, vidx, vbits) as CUDA tensors."""
+    import torch
+    dims = tuple(field.shape)
+    n = field.numel()
+    cap = n if cap is None else cap
+    dev = field.device
+    codes = torch.empty(n, dtype=torch.int16, device=dev)
+    didx = torch.empty(max(cap, 4), dtype=torch.int32, device=dev)
+    dval = torch.empty(max(cap, 4), dtype=torch.int32, device=dev)
+    vidx = torch.empty(max(cap, 4), dtype=torch.int32, device=dev)
+    vbits = torch.empty(max(cap, 4), dtype=torch.int32, device=dev)
+    work = _u8(workspace_bytes(dims), dev)
+    nd, nv = C.c_uint64(), C.c_uint64()
+    st = lib().fz_debug_quantize(_ptr(field), C.byref(make_shape(dims)), C.byref(params), _ptr(codes),
+                                 _ptr(didx), _ptr(dval), cap, C.byref(nd), _ptr(vidx), _ptr(vbits), cap,
+                                 C.byref(nv), _ptr(work), work.numel(), _stream(stream))
+    _check(st, "fz_debug_quantize")
+    return codes, didx[: nd.value], dval[: nd.value], vidx[: nv.value], vbits[: nv.value]
+
+
+def debug_decode_q(buf, dims, stream=None):
+    import torch
+    n = int(np.prod(dims))
+    q = torch.empty(n, dtype=torch.int32, device=buf.device)
+    dwork = _u8(decompress_workspace_bytes(dims), buf.device)
+    st = lib().fz_debug_decode_q(_ptr(buf), buf.numel(), _ptr(q), n, _ptr(dwork), dwork.numel(), _stream(stream))
+    _check(st, "fz_debug_decode_q")
+    return q
+
+
+def compress_host(h_field: np.ndarray, mode, eb, d_field, d_out, work, h_out: np.ndarray, stream=None):
+    """fz_compress_host: host fp32 array in, host stream bytes out (H2D + kernels + D2H)."""
+    dims = h_field.shape
+    size = C.c_size_t()
+    st = lib().fz_compress_host(h_field.ctypes.data_as(C.c_void_p), C.byref(make_shape(dims)), mode, eb,
+                                h_out.ctypes.data_as(C.c_void_p), h_out.nbytes, C.byref(size), _ptr(d_field),
+                                _ptr(d_out), d_out.numel(), _ptr(work), work.numel(), _stream(stream))
+    _check(st, "fz_compress_host")
+    return size.value
+
+
+def decompress_host(h_in: np.ndarray, size: int, h_field: np.ndarray, d_in, d_field, dwork, stream=None):
+    st = lib().fz_decompress_host(h_in.ctypes.data_as(C.c_void_p), size, h_field.ctypes.data_as(C.c_void_p),
+                                  h_field.size, _ptr(d_in), _ptr(d_field), _ptr(dwork), dwork.numel(),
+                                  _stream(stream))
+    _check(st, "fz_decompress_host")
+
+
+# ---- slab API (multi-GPU) ------------------------------------------------------------
+def slab_range(slab, work, stream=None):
+    mn, mx, bad = C.c_float(), C.c_float(), C.c_int64()
+    st = lib().fz_slab_range(_ptr(slab), slab.numel(), C.byref(mn), C.byref(mx), C.byref(bad), _ptr(work),
+                             work.numel(), _stream(stream))
+    if st == ERR_NONFINITE:
+        return mn.value, mx.value, bad.value
+    _check(st, "fz_slab_range")
+    return mn.value, mx.value, -1
+
+
+def slab_stage_bound(dims, tb, te) -> int:
+    return lib().fz_slab_stage_bound(C.byref(make_shape(dims)), tb, te)
+
+
+def slab_compress(slab, slab_first, dims, tb, te, params: Params, stage, work, stream=None) -> Counts:
+    c = Counts()
+    st = lib().fz_slab_compress(_ptr(slab), slab_first, slab.numel(), C.byref(make_shape(dims)), tb, te,
+                                C.byref(params), _ptr(stage), stage.numel(), C.byref(c), _ptr(work),
+                                work.numel(), _stream(stream))
+    _check(st, "fz_slab_compress")
+    return c
+
+
+def slab_place(stage, dims, tb, te, local: Counts, before: Counts, totals: Counts, params: Params,
+               write_header: bool, out, stream=None):
+    st = lib().fz_slab_place(_ptr(stage), C.byref(make_shape(dims)), tb, te, C.byref(local), C.byref(before),
+                             C.byref(totals), C.byref(params), int(write_header), _ptr(out), out.numel(),
+                             _stream(stream))
+    _check(st, "fz_slab_place")

@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Compared element by element on the same seeded inputs: the compressed byte stream, the
+uint16 quant codes, both outlier lists, the reconstructed integer codes and the decompressed
+fp32 array (BJ north star: "GPU output must match the oracle bit-exactly").
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_2304_12557_b200 import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2304_12557_b200 import fz  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def _gpu_stream(d: np.ndarray, mode, eb, params=None):
+    codec = fz.Codec(d.shape, DEV)
+    field = torch.from_numpy(np.ascontiguousarray(d)).to(DEV)
+    buf, size = codec.compress(field, mode, eb, params)
+    out = buf.cpu().numpy().copy()
+    xh = codec.decompress(buf).cpu().numpy().reshape(-1)
+    torch.cuda.synchronize()
+    return out, xh, codec
+
+
+def _assert_stream_equal(got: np.ndarray, ref: np.ndarray, name=""):
+    if got.size != ref.size or not np.array_equal(got, ref):
+        n = min(got.size, ref.size)
+        diff = np.nonzero(got[:n] != ref[:n])[0]
+        first = int(diff[0]) if diff.size else n
+        raise AssertionError(f"{name}: sizes {got.size} vs {ref.size}, first differing byte {first}")
+
+
+def _check_full(d: np.ndarray, mode, eb, name=""):
+    st, ref = O.compress(d, mode, eb)
+    assert st == O.OK
+    got, xh, codec = _gpu_stream(d, mode, eb)
+    _assert_stream_equal(got, ref, name)
+    st, xref = O.decompress(ref, d.size)
+    assert st == O.OK
+    bad = np.nonzero(xh.view(np.uint32) != xref.view(np.uint32))[0]
+    assert bad.size == 0, f"{name}: {bad.size} decoded values differ, first at {bad[:5]}"
+    return ref
+
+
+SMALL = [
+    ("sines3d", lambda: synth.generate("sines3d", (64, 64, 64))),
+    ("sines3d_ragged", lambda: synth.generate("sines3d", (33, 47, 61))),
+    ("cesm_t", lambda: synth.generate("cesm_t", (180, 360))),
+    ("cesm_cld", lambda: synth.generate("cesm_cld", (181, 359))),
+    ("cesm_wide", lambda: synth.generate("cesm_t", (7, 5000))),          # nx > tile
+    ("hurr_qsnow", lambda: synth.generate("hurr_qsnow", (10, 50, 50))),
+    ("hurr_u", lambda: synth.generate("hurr_u", (10, 50, 50))),
+    ("nyx_rho", lambda: synth.generate("nyx_rho", (32, 32, 32))),
+    ("nyx_v", lambda: synth.generate("nyx_v", (32, 32, 32))),
+    ("rtm", lambda: synth.generate("rtm", (40, 40, 22))),
+    ("qmc", lambda: synth.generate("qmc", (60, 9, 9))),
+    ("tiny_nx", lambda: synth.generate("sines3d", (9, 5, 3))),
+    ("noise1d", lambda: synth.adversarial("noise", 10007)),
+    ("ramp1d", lambda: synth.adversarial("ramp", 4097)),
+    ("const1d", lambda: synth.adversarial("constant", 3000)),
+    ("zeros", lambda: synth.adversarial("zeros", 2049)),
+    ("one", lambda: np.array([1.5], np.float32)),
+]
+
+
+@pytest.mark.parametrize("name,gen", SMALL, ids=[s[0] for s in SMALL])
+@pytest.mark.parametrize("rel", [1e-2, 1e-3, 1e-4])
+def test_stream_and_decode_parity(name, gen, rel):
+    _check_full(gen(), O.REL, rel, f"{name}@{rel}")
+
+
+@pytest.mark.parametrize("eb", [0.5, 1e-3, 1e-6])
+def test_abs_mode_parity(eb):
+    _check_full(synth.generate("hurr_u", (12, 40, 40)), O.ABS, eb, f"abs{eb}")
+
+
+def test_codes_and_outlier_lists_parity():
+    """Stage hook C1-C3: uint16 codes and both outlier lists equal the oracle's."""
+    cases = [synth.generate("sines3d", (40, 41, 42)), synth.adversarial("spike", 20000),
+             synth.adversarial("offset", 9000), np.array([1e30, -1e30, 1.0, 0.0] * 700, np.float32)]
+    for d, mode, eb in zip(cases, [O.REL, O.ABS, O.REL, O.ABS], [1e-3, 1e-3, 1e-6, 1e-3]):
+        p = O.params_for(d, mode, eb)
+        codes, didx, dval, vidx, vbits = O.quantize_field(d, p)
+        gp = fz.derive_params(p.mn, p.mx, mode, eb)
+        field = torch.from_numpy(d).to(DEV)
+        c2, di2, dv2, vi2, vb2 = fz.debug_quantize(field, gp)
+        assert np.array_equal(c2.cpu().numpy().view(np.uint16), codes)
+        assert np.array_equal(di2.cpu().numpy().view(np.uint32), didx)
+        assert np.array_equal(dv2.cpu().numpy(), dval)
+        assert np.array_equal(vi2.cpu().numpy().view(np.uint32), vidx)
+        assert np.array_equal(vb2.cpu().numpy().view(np.uint32), vbits)
+
+
+def test_outlier_streams_and_staging_overflow():
+    # delta outliers (spike), fallback + value outliers (offset), and a case with more value
+    # outliers than the staging area holds (N/64 + 1024), which takes the rescan path
+    _check_full(synth.adversarial("spike", 50000), O.ABS, 1e-3, "spike")
+    _check_full(synth.adversarial("offset", 30000), O.REL, 1e-6, "offset")
+    big = np.tile(np.array([1e30, -1e30, 1.0, 0.0], np.float32), 20000)
+    ref = _check_full(big, O.ABS, 1e-3, "overflow")
+    assert int.from_bytes(ref[104:112].tobytes(), "little") > big.size // 64 + 1024
+
+
+def test_decode_q_parity():
+    d = synth.generate("nyx_v", (24, 30, 33))
+    st, ref = O.compress(d, O.REL, 1e-4)
+    st, qref = O.decode_q(ref, d.size)
+    buf = torch.from_numpy(ref).to(DEV)
+    q = fz.debug_decode_q(buf, d.shape)
+    assert np.array_equal(q.cpu().numpy(), qref)
+
+
+def test_error_bound_and_idempotence():
+    d = synth.generate("cesm_t", (200, 400))
+    ref = _check_full(d, O.REL, 1e-4, "bound")
+    info = fz.peek_header(ref[:128].tobytes())
+    st, xh = O.decompress(ref, d.size)
+    assert np.abs(xh.astype(np.float64) - d.reshape(-1)).max() <= info.params.eb_abs
+    # with params pinned (ABS), recompressing x-hat on the GPU is byte-identical (R22)
+    p = fz.derive_params(float(d.min()), float(d.max()), fz.ABS, 0.01)
+    got1, xh1, _ = _gpu_stream(d, fz.ABS, 0.01, params=p)
+    got2, _, _ = _gpu_stream(xh1.reshape(d.shape), fz.ABS, 0.01, params=p)
+    assert np.array_equal(got1, got2)
+
+
+def test_nonfinite_capacity_and_corrupt():
+    d = synth.generate("sines3d", (16, 16, 16)).copy()
+    d.reshape(-1)[1234] = np.nan
+    codec = fz.Codec(d.shape, DEV)
+    with pytest.raises(fz.FZError) as e:
+        codec.compress(torch.from_numpy(d).to(DEV), fz.REL, 1e-3)
+    assert e.value.status == fz.ERR_NONFINITE
+    # capacity: snprintf convention, nothing written past the cap
+    d = synth.generate("sines3d", (16, 16, 16))
+    st, ref = O.compress(d, O.REL, 1e-3)
+    field = torch.from_numpy(d).to(DEV)
+    cap = ref.size - 1
+    out = torch.full((cap + 64,), 0xAB, dtype=torch.uint8, device=DEV)
+    work = torch.empty(fz.workspace_bytes(d.shape), dtype=torch.uint8, device=DEV)
+    import ctypes as C
+    size = C.c_size_t()
+    stt = fz.lib().fz_compress(C.c_void_p(field.data_ptr()), C.byref(fz.make_shape(d.shape)), fz.REL, 1e-3,
+                               C.c_void_p(out.data_ptr()), cap, C.byref(size), C.c_void_p(work.data_ptr()),
+                               work.numel(), None)
+    torch.cuda.synchronize()
+    assert stt == fz.ERR_CAPACITY and size.value == ref.size
+    assert (out[cap:].cpu().numpy() == 0xAB).all()
+    # corrupt streams never crash: structured error or a decode
+    rng = np.random.default_rng(3)
+    codec = fz.Codec(d.shape, DEV)
+    for k in range(60):
+        m = ref.copy()
+        for _ in range(rng.integers(1, 4)):
+            i = int(rng.integers(0, m.size))
+            m[i] ^= np.uint8(1 << int(rng.integers(0, 8)))
+        try:
+            codec.decompress(torch.from_numpy(m).to(DEV))
+        except fz.FZError as e:
+            assert e.status in (fz.ERR_CORRUPT, fz.ERR_ARG)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 3, 8])
+def test_fake_multirank_slabs_byte_identical(ranks):
+    """SV §8.e: tile-aligned z-slabs with a read-only halo, counts exchanged, placed at
+    global offsets -> byte-identical to the single-GPU stream (and the oracle's)."""
+    from paper_2304_12557_b200 import dist
+    d = synth.generate("nyx_v", (64, 64, 64))
+    st, ref = O.compress(d, O.REL, 1e-3)
+    out = dist.compress_sharded_single_process(d, fz.REL, 1e-3, ranks, DEV)
+    _assert_stream_equal(out, ref, f"ranks={ranks}")
+
+
+def test_host_buffer_entry_points():
+    d = synth.generate("hurr_u", (10, 50, 50))
+    st, ref = O.compress(d, O.REL, 1e-3)
+    cap = fz.compress_bound(d.shape)
+    d_field = torch.empty(d.shape, dtype=torch.float32, device=DEV)
+    d_out = torch.empty(cap, dtype=torch.uint8, device=DEV)
+    work = torch.empty(fz.workspace_bytes(d.shape), dtype=torch.uint8, device=DEV)
+    h_out = np.empty(cap, np.uint8)
+    size = fz.compress_host(np.ascontiguousarray(d), fz.REL, 1e-3, d_field, d_out, work, h_out)
+    assert np.array_equal(h_out[:size], ref)
+    h_x = np.empty(d.shape, np.float32)
+    dwork = torch.empty(fz.decompress_workspace_bytes(d.shape), dtype=torch.uint8, device=DEV)
+    fz.decompress_host(h_out, size, h_x, d_out, d_field, dwork)
+    st, xref = O.decompress(ref, d.size)
+    assert np.array_equal(h_x.reshape(-1).view(np.uint32), xref.view(np.uint32))
