@@ -1,0 +1,312 @@
+"""bench.py -- FZ-GPU compression path on B200 (BASELINE.json metric).
+
+A step = one pass of the whole hot path over one field: fz_compress (range, parameters,
+fused quantize/Lorenzo/bitshuffle/flags/look-back/compaction, finalize) followed by
+fz_decompress (tile decode + x-scan, y/z scans, dequantize, patches), inputs resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fz|reference] [--workload c4]
+
+Prints ONE JSON line on rank 0.  `value` = field GB/s per step (fp32 bytes of the field /
+(compress + decompress time)); compress / decompress GB/s and CR are reported beside it.
+L2 is flushed (256 MiB write) before every timed step; the c4 field is also 4x the L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2304_12557_b200 import synth  # noqa: E402
+
+METRIC = "compression/decompression GB/s (fraction of HBM peak) + compression ratio at REL 1e-3"
+
+# workload name -> (generator field, shape, REL bound, description)
+WORKLOADS = {
+    "c1": ("sines3d", (64, 64, 64), 1e-3, "c1 64^3 sines+noise REL 1e-3"),
+    "c2": ("cesm_t", (1800, 3600), 1e-3, "c2 CESM-ATM-shaped 1800x3600 T-like REL 1e-3"),
+    "c3": ("hurr_u", (100, 500, 500), 1e-3, "c3 Hurricane-shaped 100x500x500 U-like REL 1e-3"),
+    "c4": ("nyx_v", (512, 512, 512), 1e-3, "c4 NYX-shaped 512^3 velocity-like REL 1e-3"),
+    "c4_rho": ("nyx_rho", (512, 512, 512), 1e-3, "c4 NYX-shaped 512^3 log-normal density REL 1e-3"),
+    "c5": ("rtm", (1008, 1008, 352), 1e-4, "c5 RTM-shaped 1008x1008x352 REL 1e-4"),
+}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload: str, kernel: str):
+    """dram bytes per launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)[workload][kernel]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def algorithmic_bytes(kernel: str, n: int, stream_bytes: int, ndim: int):
+    """Algorithmic HBM bytes per launch of each kernel."""
+    payload = stream_bytes - 128
+    return {
+        "k_range": 4 * n,
+        "k_compress": 4 * n + payload,
+        "k_decode_tiles": payload + 4 * n,
+        "k_scan_sums": 4 * n,
+        "k_scan_apply": 8 * n,
+    }.get(kernel)
+
+
+# --------------------------------------------------------------------------------------
+def run_reference(args, wl):
+    """--impl reference: the CPU oracle as it stands, single-threaded, on a bounded sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+    field, shape, rel, desc = wl
+    d = synth.generate(field, shape)
+    planes = min(shape[0], max(1, 16 * (512 * 512) // int(np.prod(shape[1:])))) if len(shape) == 3 else shape[0]
+    sample = np.ascontiguousarray(d[:planes])
+    times, size = [], None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        st, buf = O.compress(sample, O.REL, rel)
+        st2, xh = O.decompress(buf, sample.size)
+        dt = time.perf_counter() - t0
+        assert st == O.OK and st2 == O.OK
+        size = buf.size
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * statistics.mean(times)
+    v = sample.nbytes / (ms / 1e3) / 1e9
+    samp = f"first {planes} of {shape[0]} planes ({sample.nbytes / 1e6:.1f} MB) of the {args.workload} field"
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "sample": samp},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": samp},
+            "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "cr": round(sample.nbytes / size, 3)}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(d: np.ndarray, rel: float):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+    t0 = time.perf_counter()
+    st, buf = O.compress(d, O.REL, rel)
+    t1 = time.perf_counter()
+    st2, xh = O.decompress(buf, d.size)
+    t2 = time.perf_counter()
+    assert st == O.OK and st2 == O.OK
+    return {"value": round(d.nbytes / (t2 - t0) / 1e9, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"whole field, compress {t1 - t0:.1f} s + decompress {t2 - t1:.1f} s single-threaded",
+            "compress_gbs": round(d.nbytes / (t1 - t0) / 1e9, 6),
+            "decompress_gbs": round(d.nbytes / (t2 - t1) / 1e9, 6)}, buf
+
+
+def run_single(args, wl):
+    import torch
+
+    from paper_2304_12557_b200 import fz
+    field_name, shape, rel, desc = wl
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    d = synth.generate(field_name, shape)
+    n = d.size
+    field = torch.from_numpy(d).to(dev)
+    codec = fz.Codec(shape, dev)
+    xh = torch.empty_like(field)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        buf, size = codec.compress(field, fz.REL, rel)
+        la = fz.last_launch_count()
+        codec.decompress(buf, out=xh)
+        return buf, size, la + fz.last_launch_count()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    fz.profile_enable(True)
+    fz.profile_read()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    launches = 0
+    sampler = ClockSampler(0)
+    with sampler:
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)             # L2 flush (2x L2), outside the events
+            ev[k][0].record(stream)
+            buf, size = codec.compress(field, fz.REL, rel)
+            launches += fz.last_launch_count()
+            ev[k][1].record(stream)
+            codec.decompress(buf, out=xh)
+            launches += fz.last_launch_count()
+            ev[k][2].record(stream)
+        torch.cuda.synchronize()
+    prof = fz.profile_read()
+    fz.profile_enable(False)
+    tc = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
+    td = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
+    ms_c, ms_d = statistics.mean(tc), statistics.mean(td)
+    ms = ms_c + ms_d
+    gb = d.nbytes / 1e9
+
+    # bit-exact self-check of the last step against the stream of the first warm-up step
+    stream_bytes = size
+    peak, peak_src = measured_peak()
+    kernels = {}
+    for name, (tot, cnt) in prof.items():
+        per = tot / cnt
+        ab = algorithmic_bytes(name, n, stream_bytes, len(shape))
+        kernels[name] = {"ms_per_launch": round(per, 4), "launches": cnt,
+                         "share_of_step": round(tot / (ms * args.steps), 4)}
+        if ab is not None:
+            kernels[name]["achieved_gbs"] = round(ab / (per / 1e3) / 1e9, 1)
+            kernels[name]["frac"] = round(ab / (per / 1e3) / 1e9 / peak, 4)
+    dom = max(prof.items(), key=lambda kv: kv[1][0])[0]
+    per = prof[dom][0] / prof[dom][1]
+    ab = algorithmic_bytes(dom, n, stream_bytes, len(shape))
+    achieved = ab / (per / 1e3) / 1e9
+    roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, dom),
+            "algorithmic_bytes_per_launch": ab, "peak_source": peak_src}
+    pc = prof.get("k_compress")
+    comp_roof = None
+    if pc:
+        pk = pc[0] / pc[1]
+        abk = algorithmic_bytes("k_compress", n, stream_bytes, len(shape))
+        comp_roof = {"kernel": "k_compress", "achieved": round(abk / (pk / 1e3) / 1e9, 1),
+                     "frac": round(abk / (pk / 1e3) / 1e9 / peak, 4), "ms": round(pk, 4)}
+
+    # ---- end to end through the public API with HOST buffers (pinned) ----
+    h_field = torch.from_numpy(d).pin_memory().numpy()
+    h_out = torch.empty(codec.cap, dtype=torch.uint8).pin_memory().numpy()
+    h_x = torch.empty(shape, dtype=torch.float32).pin_memory().numpy()
+    d_in = torch.empty(codec.cap, dtype=torch.uint8, device=dev)
+    te = []
+    for k in range(max(3, args.warmup) + args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sz = fz.compress_host(h_field, fz.REL, rel, field, codec.out, codec.work, h_out)
+        fz.decompress_host(h_out, sz, h_x, d_in, xh, codec.dwork)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if k >= max(3, args.warmup):
+            te.append(e0.elapsed_time(e1))
+    assert np.array_equal(h_out[:sz], buf[:sz].cpu().numpy())
+    ms_e2e = statistics.mean(te)
+
+    line = {
+        "metric": METRIC, "value": round(gb / (ms / 1e3), 3), "unit": "GB/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": desc, "dims": list(shape), "rel_eb": rel, "field_bytes": d.nbytes,
+                   "l2": "256 MiB flush before every timed step; field is 4.3x L2", "parallelism": "1 GPU"},
+        "compress_gbs": round(gb / (ms_c / 1e3), 2), "decompress_gbs": round(gb / (ms_d / 1e3), 2),
+        "compress_ms": round(ms_c, 4), "decompress_ms": round(ms_d, 4),
+        "cr": round(d.nbytes / stream_bytes, 4), "bits_per_value": round(32 * stream_bytes / d.nbytes, 4),
+        "roofline": roof, "roofline_compress_kernel": comp_roof, "kernels": kernels,
+        "clocks": sampler.summary(), "gpu_launches": launches,
+        "e2e": {"value": round(gb / (ms_e2e / 1e3), 3), "unit": "GB/s", "ms_per_step": round(ms_e2e, 3),
+                "h2d_bytes_per_step": d.nbytes + stream_bytes, "d2h_bytes_per_step": stream_bytes + d.nbytes,
+                "path": "fz_compress_host + fz_decompress_host, pinned host buffers"},
+    }
+    if not args.no_cpu_baseline:
+        cb, ref = cpu_baseline(d, rel)
+        line["cpu_baseline"] = cb
+        line["parity_vs_oracle"] = bool(ref.size == stream_bytes and np.array_equal(ref, buf[:stream_bytes].cpu().numpy()))
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fz", choices=["fz", "reference"])
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2304_12557_b200 import bench_dist
+        bench_dist.run(args, wl, METRIC)
+        return
+    run_single(args, wl)
+
+
+if __name__ == "__main__":
+    main()

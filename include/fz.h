@@ -187,6 +187,14 @@ fz_status fz_debug_decode_q(const void* d_in, size_t in_size, int32_t* d_q, uint
  * (bench accounting of "gpu_launches"). */
 int fz_last_launch_count(void);
 
+/* Per-kernel CUDA-event timing (tracing).  When enabled, every libfz kernel launch is
+ * bracketed by two CUDA events recorded on its launch stream.  fz_profile_read waits for
+ * the pending events, writes the summed milliseconds and launch counts per kernel kind
+ * (indices 0..n-1, names from fz_kernel_name) and resets the totals; returns n. */
+void fz_profile_enable(int on);
+int fz_profile_read(double* h_ms, int* h_launches, int max_kernels);
+const char* fz_kernel_name(int id);
+
 #ifdef __cplusplus
 }
 #endif

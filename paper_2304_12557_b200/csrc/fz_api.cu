@@ -3,12 +3,57 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "fz_launch.h"
 
 namespace fz {
 static thread_local int t_launches = 0;
-void count_launch() { ++t_launches; }
+
+// ---- per-kernel CUDA-event profiling (tracing) ----
+namespace {
+struct ProfRec {
+    int id;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof_pending;
+std::vector<cudaEvent_t> g_prof_pool;
+double g_prof_ms[K_COUNT];
+int g_prof_n[K_COUNT];
+
+cudaEvent_t prof_event()
+{
+    if (!g_prof_pool.empty()) {
+        cudaEvent_t e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+LaunchProf::LaunchProf(KernelId id_, cudaStream_t st_) : id(id_), st(st_), slot(-1)
+{
+    ++t_launches;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (!g_prof_on) return;
+    ProfRec r{id, prof_event(), prof_event()};
+    cudaEventRecord(r.a, st);
+    g_prof_pending.push_back(r);
+    slot = (int)g_prof_pending.size() - 1;
+}
+
+LaunchProf::~LaunchProf()
+{
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (slot < (int)g_prof_pending.size()) cudaEventRecord(g_prof_pending[slot].b, st);
+}
 }  // namespace fz
 
 using namespace fz;
@@ -68,9 +113,9 @@ struct Work {
     uint8_t* base;
     Ctrl* ctrl() const { return reinterpret_cast<Ctrl*>(base + L.ctrl); }
     unsigned long long* status() const { return reinterpret_cast<unsigned long long*>(base + L.status); }
-    uint32_t* aggv() const { return reinterpret_cast<uint32_t*>(base + L.aggv); }
-    uint32_t* inclv() const { return reinterpret_cast<uint32_t*>(base + L.inclv); }
-    uint2* tpre() const { return reinterpret_cast<uint2*>(base + L.tpre); }
+    uint2* ocnt() const { return reinterpret_cast<uint2*>(base + L.ocnt); }
+    uint2* obase() const { return reinterpret_cast<uint2*>(base + L.obase); }
+    uint2* opre() const { return reinterpret_cast<uint2*>(base + L.opre); }
     uint2* dstage() const { return reinterpret_cast<uint2*>(base + L.dstage); }
     uint2* vstage() const { return reinterpret_cast<uint2*>(base + L.vstage); }
 };
@@ -89,9 +134,9 @@ CompressArgs make_args(const Work& W, const float* field, uint64_t base, const G
     a.dcap = W.L.dcap;
     a.vcap = W.L.vcap;
     a.status = W.status();
-    a.aggv = W.aggv();
-    a.inclv = W.inclv();
-    a.tpre = W.tpre();
+    a.ocnt = W.ocnt();
+    a.obase = W.obase();
+    a.opre = W.opre();
     a.ctrl = W.ctrl();
     return a;
 }
@@ -103,18 +148,57 @@ fz_status read_ctrl(const Work& W, Ctrl* h, cudaStream_t st)
     return FZ_OK;
 }
 
-// Outliers did not fit the staging area: recompute them tile by tile and write straight to
-// their final offsets (the per-tile exclusive counts were recorded by the first pass).
-fz_status rescan(const Work& W, CompressArgs a, const Ctrl& h, uint2* dfinal, uint2* vfinal,
-                 cudaStream_t st)
+// Where the outlier records of a compressed range go (records or split lists).
+struct OutDest {
+    uint2* drec = nullptr;
+    uint2* vrec = nullptr;
+    uint32_t* didx = nullptr;
+    int32_t* dval = nullptr;
+    uint32_t* vidx = nullptr;
+    uint32_t* vbits = nullptr;
+};
+
+// Phase 1: init (+ range + params on the device) -> fused kernel -> totals (+ header).
+fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp, int mode, double eb,
+                       uint8_t* hdr_out, uint64_t out_cap, const fz_shape& s, uint64_t n, Ctrl* h,
+                       cudaStream_t st)
 {
-    FZ_CUDA(cudaMemsetAsync(&W.ctrl()->ticket, 0, sizeof(uint32_t), st));
-    a.rescan = 1;
-    a.dstage = dfinal;
-    a.vstage = vfinal;
-    a.dcap = h.nd;
-    a.vcap = h.nv;
+    const uint32_t tb = a.tile_begin, nt = a.tile_end - a.tile_begin;
+    FZ_CUDA(launch_init(W.ctrl(), W.status() + tb, W.ocnt() + tb, nt, hp, st));
+    if (hp == nullptr) {
+        FZ_CUDA(launch_range(a.field, n, W.ctrl(), st));
+        FZ_CUDA(launch_params(W.ctrl(), mode, eb, n, st));
+    }
     FZ_CUDA(launch_compress(a, st));
+    FZ_CUDA(launch_finalize(hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
+    return read_ctrl(W, h, st);
+}
+
+// Phase 2 (only when outliers exist): per-tile exclusive offsets, then either a copy of
+// the staged records or -- when the staging area overflowed -- a rescan of the tiles that
+// writes the records straight to their final places.
+fz_status place_outliers(const Work& W, CompressArgs a, const Ctrl& h, const OutDest& d, cudaStream_t st)
+{
+    if (h.nd + h.nv == 0) return FZ_OK;
+    const uint32_t tb = a.tile_begin, nt = a.tile_end - a.tile_begin;
+    FZ_CUDA(launch_outlier_scan(W.ocnt() + tb, W.opre() + tb, nt, st));
+    if (!h.stage_overflow) {
+        FZ_CUDA(launch_outlier_place(W.ocnt() + tb, W.obase() + tb, W.opre() + tb, nt, W.dstage(), W.vstage(),
+                                     d.drec, d.vrec, d.didx, d.dval, d.vidx, d.vbits, st));
+    } else {
+        FZ_CUDA(cudaMemsetAsync(&W.ctrl()->ticket, 0, sizeof(uint32_t), st));
+        a.rescan = 1;
+        a.dstage = d.drec;
+        a.vstage = d.vrec;
+        a.o_didx = d.didx;
+        a.o_dval = d.dval;
+        a.o_vidx = d.vidx;
+        a.o_vbits = d.vbits;
+        a.dcap = h.nd;
+        a.vcap = h.nv;
+        FZ_CUDA(launch_compress(a, st));
+    }
+    FZ_CUDA(cudaStreamSynchronize(st));
     return FZ_OK;
 }
 
@@ -158,32 +242,22 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     const Geom g = geom_of(*s, n);
     uint8_t* out = static_cast<uint8_t*>(d_out);
 
-    FZ_CUDA(launch_init(W.ctrl(), W.status(), (uint32_t)T, hp, st));
-    if (hp == nullptr) {
-        FZ_CUDA(launch_range(d_field, n, W.ctrl(), st));
-        FZ_CUDA(launch_params(W.ctrl(), mode, eb, n, st));
-    }
     CompressArgs a = make_args(W, d_field, 0, g, 0, (uint32_t)T);
     const uint64_t fbase = kHeaderBytes, pbase = kHeaderBytes + 32 * T;
     a.flags_out = out + fbase;
     a.flags_cap = out_cap > fbase ? out_cap - fbase : 0;
     a.payload_out = out + pbase;
     a.payload_cap = out_cap > pbase ? out_cap - pbase : 0;
-    FZ_CUDA(launch_compress(a, st));
-    FZ_CUDA(launch_finalize(out, out_cap, *s, n, T, W.dstage(), W.vstage(), W.ctrl(), st));
     Ctrl h;
-    fz_status rs = read_ctrl(W, &h, st);
+    fz_status rs = compress_run(W, a, hp, mode, eb, out, out_cap, *s, n, &h, st);
     if (rs != FZ_OK) return rs;
     if (h.err != 0) return (fz_status)h.err;
     *out_size = (size_t)h.total;
     if (h.total > out_cap) return FZ_ERR_CAPACITY;
-    if (h.stage_overflow) {
-        const uint64_t dbase = pbase + 16 * h.nnz, vbase = dbase + 8 * h.nd;
-        rs = rescan(W, a, h, reinterpret_cast<uint2*>(out + dbase), reinterpret_cast<uint2*>(out + vbase), st);
-        if (rs != FZ_OK) return rs;
-        FZ_CUDA(cudaStreamSynchronize(st));
-    }
-    return FZ_OK;
+    OutDest d;
+    d.drec = reinterpret_cast<uint2*>(out + pbase + 16 * h.nnz);
+    d.vrec = reinterpret_cast<uint2*>(out + pbase + 16 * h.nnz + 8 * h.nd);
+    return place_outliers(W, a, h, d, st);
 }
 
 }  // namespace
@@ -431,6 +505,44 @@ const char* fz_last_cuda_error(void) { return g_cuda_err; }
 
 int fz_last_launch_count(void) { return g_last_launches; }
 
+void fz_profile_enable(int on)
+{
+    std::lock_guard<std::mutex> g(fz::g_prof_mu);
+    fz::g_prof_on = on != 0;
+}
+
+int fz_profile_read(double* h_ms, int* h_launches, int max_kernels)
+{
+    std::lock_guard<std::mutex> g(fz::g_prof_mu);
+    for (auto& r : fz::g_prof_pending) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+            fz::g_prof_ms[r.id] += ms;
+            fz::g_prof_n[r.id] += 1;
+        }
+        fz::g_prof_pool.push_back(r.a);
+        fz::g_prof_pool.push_back(r.b);
+    }
+    fz::g_prof_pending.clear();
+    for (int k = 0; k < fz::K_COUNT && k < max_kernels; ++k) {
+        if (h_ms) h_ms[k] = fz::g_prof_ms[k];
+        if (h_launches) h_launches[k] = fz::g_prof_n[k];
+        fz::g_prof_ms[k] = 0.0;
+        fz::g_prof_n[k] = 0;
+    }
+    return fz::K_COUNT;
+}
+
+const char* fz_kernel_name(int id)
+{
+    static const char* names[] = {"k_init", "k_range", "k_params", "k_compress", "k_finalize",
+                                  "k_decode_init", "k_validate_outliers", "k_decode_tiles",
+                                  "k_scan_sums", "k_scan_chunks", "k_scan_apply", "k_value_patch",
+                                  "k_outliers"};
+    return (id >= 0 && id < fz::K_COUNT) ? names[id] : "?";
+}
+
 // ---------------------------------------------------------------------------------------
 // Slab API (multi-GPU z-slabs, SV §8.e)
 // ---------------------------------------------------------------------------------------
@@ -442,7 +554,7 @@ fz_status fz_slab_range(const float* d_slab, uint64_t n, float* h_min, float* h_
         return FZ_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Ctrl* ctrl = static_cast<Ctrl*>(d_work);
-    FZ_CUDA(launch_init(ctrl, nullptr, 0, nullptr, st));
+    FZ_CUDA(launch_init(ctrl, nullptr, nullptr, 0, nullptr, st));
     FZ_CUDA(launch_range(d_slab, n, ctrl, st));
     Ctrl h;
     FZ_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
@@ -487,15 +599,13 @@ fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t sl
     const uint64_t nt = te - tb;
     uint8_t* stage = static_cast<uint8_t*>(d_stage);
 
-    FZ_CUDA(launch_init(W.ctrl(), W.status() + tb, (uint32_t)nt, p, st));
     CompressArgs a = make_args(W, d_slab, slab_first, g, (uint32_t)tb, (uint32_t)te);
     a.flags_out = stage;
     a.flags_cap = stage_cap < 32 * nt ? stage_cap : 32 * nt;
     a.payload_out = stage + 32 * nt;
     a.payload_cap = stage_cap > 32 * nt ? stage_cap - 32 * nt : 0;
-    FZ_CUDA(launch_compress(a, st));
     Ctrl h;
-    fz_status rs = read_ctrl(W, &h, st);
+    fz_status rs = compress_run(W, a, p, (int)p->mode, p->eb_input, nullptr, 0, *global, n, &h, st);
     if (rs != FZ_OK) return rs;
     if (h.err != 0) return (fz_status)h.err;
     h_counts->nnz = h.nnz;
@@ -503,15 +613,10 @@ fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t sl
     h_counts->n_value = h.nv;
     const uint64_t dbase = 32 * nt + 16 * h.nnz, vbase = dbase + 8 * h.nd, need = vbase + 8 * h.nv;
     if (need > stage_cap) return FZ_ERR_CAPACITY;
-    if (h.stage_overflow) {
-        rs = rescan(W, a, h, reinterpret_cast<uint2*>(stage + dbase), reinterpret_cast<uint2*>(stage + vbase), st);
-        if (rs != FZ_OK) return rs;
-    } else {
-        if (h.nd) FZ_CUDA(cudaMemcpyAsync(stage + dbase, W.dstage(), 8 * h.nd, cudaMemcpyDeviceToDevice, st));
-        if (h.nv) FZ_CUDA(cudaMemcpyAsync(stage + vbase, W.vstage(), 8 * h.nv, cudaMemcpyDeviceToDevice, st));
-    }
-    FZ_CUDA(cudaStreamSynchronize(st));
-    return FZ_OK;
+    OutDest d;
+    d.drec = reinterpret_cast<uint2*>(stage + dbase);
+    d.vrec = reinterpret_cast<uint2*>(stage + vbase);
+    return place_outliers(W, a, h, d, st);
 }
 
 fz_status fz_slab_place(const void* d_stage, const fz_shape* global, uint64_t tb, uint64_t te,
@@ -564,23 +669,21 @@ fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_pa
     Work W{compress_layout(n, T), static_cast<uint8_t*>(d_work)};
     if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    FZ_CUDA(launch_init(W.ctrl(), W.status(), (uint32_t)T, p, st));
     CompressArgs a = make_args(W, d_field, 0, geom_of(*s, n), 0, (uint32_t)T);
     a.codes_out = d_codes;
-    a.o_didx = d_didx;
-    a.o_dval = d_dval;
-    a.o_vidx = d_vidx;
-    a.o_vbits = d_vbits;
-    a.dcap = dcap;
-    a.vcap = vcap;
-    FZ_CUDA(launch_compress(a, st));
     Ctrl h;
-    fz_status rs = read_ctrl(W, &h, st);
+    fz_status rs = compress_run(W, a, p, (int)p->mode, p->eb_input, nullptr, 0, *s, n, &h, st);
     if (rs != FZ_OK) return rs;
     if (h.err != 0) return (fz_status)h.err;
     *h_nd = h.nd;
     *h_nv = h.nv;
-    return (h.nd > dcap || h.nv > vcap) ? FZ_ERR_CAPACITY : FZ_OK;
+    if (h.nd > dcap || h.nv > vcap) return FZ_ERR_CAPACITY;
+    OutDest d;
+    d.didx = d_didx;
+    d.dval = d_dval;
+    d.vidx = d_vidx;
+    d.vbits = d_vbits;
+    return place_outliers(W, a, h, d, st);
 }
 
 }  // extern "C"

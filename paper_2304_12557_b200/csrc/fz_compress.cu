@@ -1,11 +1,12 @@
 // fz_compress.cu -- compression kernels of libfz (B200, sm_100a).
 //
-//   k_init      reset the control block / tile status words (and optionally set params)
-//   k_range     C0: min, max, first non-finite index
-//   k_params    C0: Appendix-A parameters on the device (no host round trip)
-//   k_compress  C1-C8 fused: prequantize -> Lorenzo -> codes -> bitshuffle -> block flags ->
-//               decoupled look-back scan -> compaction, persistent CTAs with a tile ticket
-//   k_finalize  C9: header + outlier sections
+//   k_init          reset the control block / tile status words (and optionally set params)
+//   k_range         C0: min, max, first non-finite index
+//   k_params        C0: Appendix-A parameters on the device (no host round trip)
+//   k_compress      C1-C8 fused: prequantize -> Lorenzo -> codes -> bitshuffle -> block flags
+//                   -> decoupled look-back scan -> compaction; persistent CTAs, tile ticket
+//   k_finalize      C9: header
+//   k_outlier_scan / k_outlier_place: outlier sections (only launched when outliers exist)
 //
 // Citation key: P:n = PAPER.md line n; R# = DESIGN.md §3 readings; SV = SURVEY.md.
 #include "fz_internal.cuh"
@@ -13,26 +14,30 @@
 
 namespace fz {
 
-// Q arrays hold q of 2049 consecutive elements; index m stored at m + (m >> 3) so that the
-// stride-8 per-thread access pattern is bank-conflict free.
-constexpr int kQStride = 2312;
-__device__ __forceinline__ int qaddr(int m) { return m + (m >> 3); }
+// Shared q arrays: element m stored at m + (m >> 3) so that the stride-8 per-thread access
+// pattern of the Lorenzo stage is (at most 2-way) bank-conflict free.
+__device__ __forceinline__ int pad(int m) { return m + (m >> 3); }
+inline uint32_t pad_words(uint32_t len) { return len + (len >> 3) + 8; }
+constexpr uint32_t kUnionHaloMax = 4097;   // union arrays when the row halo nx+1 fits
 
 // ------------------------------------------------------------------------------------
-__global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint32_t ntiles, int set_params,
-                       fz_params p)
+__global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint32_t ntiles,
+                       int set_params, fz_params p)
 {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    for (uint32_t k = i; k < ntiles; k += gridDim.x * blockDim.x) status[k] = 0ull;
+    for (uint32_t k = i; k < ntiles; k += gridDim.x * blockDim.x) {
+        status[k] = 0ull;
+        ocnt[k] = make_uint2(0, 0);
+    }
     if (i == 0) {
         ctrl->mn_enc = 0xFFFFFFFFu;
         ctrl->mx_enc = 0u;
         ctrl->first_bad = ~0ull;
         ctrl->err = 0;
         ctrl->ticket = 0;
-        ctrl->ticket2 = 0;
         ctrl->stage_overflow = 0;
         ctrl->nnz = ctrl->nd = ctrl->nv = ctrl->total = 0;
+        ctrl->dcount = ctrl->vcount = 0;
         if (set_params) {
             ctrl->p = p;
             ctrl->h = 0.5f * p.w;
@@ -87,96 +92,81 @@ __global__ void k_params(Ctrl* ctrl, int mode, double eb, uint64_t n)
 }
 
 // ------------------------------------------------------------------------------------
-// Loads 8 consecutive elements g0..g0+7 (g0 may be negative: zero outside the field).
+// Field loads: element g (may be negative or past N: 0 outside the field).
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ void load8(const CompressArgs& a, int64_t g0, float (&v)[8])
-{
-    const int64_t n = a.g.n;
-    const int64_t base = (int64_t)a.base;
-    if (g0 >= base && g0 + 8 <= n && ((g0 - base) & 3) == 0) {
-        const float* p = a.field + (g0 - base);
-        float4 x = ldg_f4(p), y = ldg_f4(p + 4);
-        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-        v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
-    } else {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            int64_t g = g0 + u;
-            v[u] = (g >= base && g < n) ? __ldg(a.field + (g - base)) : 0.0f;
-        }
-    }
-}
-
 __device__ __forceinline__ float load1(const CompressArgs& a, int64_t g)
 {
     return (g >= (int64_t)a.base && g < (int64_t)a.g.n) ? __ldg(a.field + (g - (int64_t)a.base)) : 0.0f;
 }
 
-// ------------------------------------------------------------------------------------
-// Decoupled look-back over tiles (C7): status word = state(2) | nnz(30) | nd(32),
-// value-outlier counts in companion arrays written before the release of the status word.
-// Returns the exclusive prefix (nnz, nd, nv) of tile t.  Warp-wide call.
-// ------------------------------------------------------------------------------------
-__device__ __forceinline__ void lookback3(const CompressArgs& a, uint32_t t, uint32_t nnz,
-                                          uint32_t nd, uint32_t nv, unsigned long long& e_nnz,
-                                          unsigned long long& e_nd, unsigned long long& e_nv)
+template <int K>
+__device__ __forceinline__ void loadk(const CompressArgs& a, int64_t g0, float (&v)[K])
 {
-    const int lane = threadIdx.x & 31;
-    const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62;
-    e_nnz = e_nd = e_nv = 0;
-    if (t == a.tile_begin) {
-        if (lane == 0) {
-            a.inclv[t] = nv;
-            st_release_u64(&a.status[t], kInc | ((unsigned long long)nnz << 32) | nd);
+    const int64_t base = (int64_t)a.base;
+    if (g0 >= base && g0 + K <= (int64_t)a.g.n) {   // g0 - base is a multiple of 4 here
+        const float* p = a.field + (g0 - base);
+#pragma unroll
+        for (int c = 0; c < K / 4; ++c) {
+            float4 x = ldg_f4(p + 4 * c);
+            v[4 * c] = x.x; v[4 * c + 1] = x.y; v[4 * c + 2] = x.z; v[4 * c + 3] = x.w;
         }
-        return;
+    } else {
+#pragma unroll
+        for (int u = 0; u < K; ++u) v[u] = load1(a, g0 + u);
     }
-    if (lane == 0) {
-        a.aggv[t] = nv;
-        st_release_u64(&a.status[t], kAgg | ((unsigned long long)nnz << 32) | nd);
-    }
-    int64_t p = (int64_t)t - 1;
-    while (true) {
-        const int64_t q = p - lane;
-        unsigned long long s = kInc;
-        uint32_t v = 0;
-        if (q >= (int64_t)a.tile_begin) {
-            do { s = ld_acquire_u64(&a.status[q]); } while ((s >> 62) == 0);
-            v = ((s >> 62) == 1) ? ld_relaxed_u32(&a.aggv[q]) : ld_relaxed_u32(&a.inclv[q]);
+}
+
+// q of one halo element (no bound check needed: only own elements can be value outliers).
+template <bool FB>
+__device__ __forceinline__ int quant_q(float d, const QuantP& P)
+{
+    if (FB) return prequant_q(d, P);
+    bool hard;
+    float qf;
+    int q = prequant_fast(d, P, hard, qf);
+    if (hard) q = prequant_q(d, P);
+    return q;
+}
+
+// Cooperative fill of arr[pad(g - g_lo)] = q(g) for g in [g_lo, g_lo + len), in 4-element
+// aligned chunks (16-byte loads).  Elements outside the field get q = 0 (masked later).
+template <bool FB>
+__device__ __forceinline__ void fill_range(const CompressArgs& a, const QuantP& P, int* arr,
+                                           int64_t g_lo, int len)
+{
+    if (len <= 0) return;
+    const int64_t a0 = g_lo & ~(int64_t)3;
+    const int nch = (int)((g_lo + len - a0 + 3) >> 2);
+    for (int c = threadIdx.x; c < nch; c += kCta) {
+        const int64_t gc = a0 + 4 * c;
+        float v[4];
+        loadk<4>(a, gc, v);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t m = gc + u - g_lo;
+            if (m >= 0 && m < len) arr[pad((int)m)] = quant_q<FB>(v[u], P);
         }
-        const uint32_t incl = __ballot_sync(kFull, (s >> 62) == 2);
-        const int stop = incl ? __ffs(incl) - 1 : 31;
-        unsigned long long cn = 0, cd = 0, cv = 0;
-        if (lane <= stop) { cn = (s >> 32) & 0x3FFFFFFFull; cd = s & 0xFFFFFFFFull; cv = v; }
-        for (int o = 16; o; o >>= 1) {
-            cn += __shfl_xor_sync(kFull, cn, o);
-            cd += __shfl_xor_sync(kFull, cd, o);
-            cv += __shfl_xor_sync(kFull, cv, o);
-        }
-        e_nnz += cn; e_nd += cd; e_nv += cv;
-        if (incl) break;
-        p -= 32;
-    }
-    if (lane == 0) {
-        a.inclv[t] = (uint32_t)(e_nv + nv);
-        st_release_u64(&a.status[t], kInc | ((e_nnz + nnz) << 32) | (uint32_t)(e_nd + nd));
     }
 }
 
 // ------------------------------------------------------------------------------------
-// The fused compression kernel.  One CTA of 256 threads works on one 2048-code tile at a
-// time; thread t owns tile elements 8t..8t+7 (= words 4t..4t+3 = A[t/8][4(t%8)..+3]).
+// The fused compression kernel.  One CTA of 256 threads works on one 2048-code tile per
+// iteration; thread t owns tile elements 8t..8t+7 (= words 4t..4t+3 = A[t/8][4(t%8)..+3]).
+// The scan over tiles is a decoupled look-back delayed by one iteration: the aggregate of
+// tile i is published as soon as its flags are known, its look-back and payload stores
+// happen while the CTA already holds tile i+1, so predecessors have had a full tile time
+// to publish their inclusive prefixes.
 // ------------------------------------------------------------------------------------
-template <int NDIM>
-__global__ void __launch_bounds__(kCta) k_compress(CompressArgs a)
+template <int NDIM, bool FB>
+__device__ __forceinline__ void compress_body(const CompressArgs& a)
 {
-    constexpr int NQ = NDIM == 1 ? 1 : (NDIM == 2 ? 2 : 4);
     extern __shared__ int smem[];
-    int* Q = smem;                                          // NQ x kQStride
-    uint32_t* Obuf = reinterpret_cast<uint32_t*>(smem + NQ * kQStride);   // 32 x 33
     __shared__ uint32_t s_tile[2];
-    __shared__ uint32_t s_F[8], s_cd[8], s_cv[8];
-    __shared__ unsigned long long s_ex[3];
+    __shared__ uint32_t s_F[2][8];
+    __shared__ uint32_t s_cd[8], s_cv[8];
+    __shared__ uint32_t s_tnnz[2];
+    __shared__ unsigned long long s_ex;
+    __shared__ unsigned long long s_ob[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Ctrl* ctrl = a.ctrl;
@@ -184,243 +174,365 @@ __global__ void __launch_bounds__(kCta) k_compress(CompressArgs a)
     QuantP P;
     P.w = ctrl->p.w; P.r = ctrl->p.r; P.h = ctrl->h; P.eb32 = ctrl->p.eb32;
     const uint32_t n = a.g.n, nx = a.g.nx, PL = a.g.P;
-    // neighbour offsets of the Q ranges: own, y-1, z-1, y-1 & z-1
-    const int64_t off[4] = {0, (int64_t)nx, (int64_t)PL, (int64_t)PL + nx};
+    const int qs = (int)a.qstride;
+    uint32_t* Obuf;
+    // neighbour streams: array base (words) and m offset of own element j = 0
+    int ab[4], mo[4];
+    if (NDIM == 1) {
+        ab[0] = 0; mo[0] = 1;
+        Obuf = reinterpret_cast<uint32_t*>(smem + qs);
+    } else if (a.union_mode) {
+        const int HA = (int)nx + 1;
+        ab[0] = 0; mo[0] = HA; ab[1] = 0; mo[1] = 1;
+        ab[2] = qs; mo[2] = HA; ab[3] = qs; mo[3] = 1;
+        Obuf = reinterpret_cast<uint32_t*>(smem + (NDIM == 3 ? 2 : 1) * qs);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { ab[k] = k * qs; mo[k] = 1; }
+        Obuf = reinterpret_cast<uint32_t*>(smem + (NDIM == 3 ? 4 : 2) * qs);
+    }
+    constexpr int NS = NDIM == 1 ? 1 : (NDIM == 2 ? 2 : 4);
 
     if (tid == 0) s_tile[0] = a.tile_begin + atomicAdd(&ctrl->ticket, 1u);
     __syncthreads();
+    uint32_t tp = 0xFFFFFFFFu;      // pending tile (payload not yet stored)
+    uint4 pblk = make_uint4(0, 0, 0, 0);
+    bool pnz = false;
     for (int it = 0;; ++it) {
-        const uint32_t t = s_tile[it & 1];
-        if (t >= a.tile_end) break;
-        const int64_t s = (int64_t)t * kTileCodes;
-        const int64_t g0 = s + 8 * tid;
-
-        // ---- A: prequantize own elements (with bound check) and the halo ranges ----
-        float dv[8];
-        int qo[8];
-        uint32_t vmask = 0;
-        load8(a, g0, dv);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            bool vo;
-            qo[u] = prequant(dv[u], P, vo);
-            if (vo && g0 + u < (int64_t)n) vmask |= 1u << u;
-            Q[qaddr(1 + 8 * tid + u)] = qo[u];
-        }
-        if (tid == 0) Q[qaddr(0)] = prequant_q(load1(a, s - 1), P);
-#pragma unroll
-        for (int k = 1; k < NQ; ++k) {
-            float hv[8];
-            load8(a, g0 - off[k], hv);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) Q[k * kQStride + qaddr(1 + 8 * tid + u)] = prequant_q(hv[u], P);
-            if (tid == 0) Q[k * kQStride + qaddr(0)] = prequant_q(load1(a, s - off[k] - 1), P);
-        }
-        __syncthreads();
-        if (tid == 0) s_tile[(it + 1) & 1] = a.tile_begin + atomicAdd(&ctrl->ticket, 1u);
-
-        // ---- B: Lorenzo residual (C2), codes (C3), words (C4) ----
-        uint32_t x = (uint32_t)(g0 % nx), pp = (uint32_t)(g0 % PL);
-        int qn[NQ][9];
-        qn[0][0] = Q[qaddr(8 * tid)];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) qn[0][u + 1] = qo[u];
-#pragma unroll
-        for (int k = 1; k < NQ; ++k)
-#pragma unroll
-            for (int u = 0; u < 9; ++u) qn[k][u] = Q[k * kQStride + qaddr(8 * tid + u)];
-        uint32_t code[8];
-        int32_t dl[8];
-        uint32_t dmask = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const bool mx = x != 0, my = pp >= nx, mz = (g0 + u) >= (int64_t)PL;
-            uint32_t r0 = (uint32_t)qn[0][u + 1] - (mx ? (uint32_t)qn[0][u] : 0u);
-            uint32_t dd = r0;
-            if (NDIM >= 2) {
-                uint32_t r1 = (uint32_t)qn[1][u + 1] - (mx ? (uint32_t)qn[1][u] : 0u);
-                if (NDIM == 3) {
-                    uint32_t r2 = (uint32_t)qn[2][u + 1] - (mx ? (uint32_t)qn[2][u] : 0u);
-                    uint32_t r3 = (uint32_t)qn[3][u + 1] - (mx ? (uint32_t)qn[3][u] : 0u);
-                    dd -= my ? r1 : 0u;
-                    dd -= mz ? (r2 - (my ? r3 : 0u)) : 0u;
-                } else {
-                    dd -= my ? r1 : 0u;
-                }
-            }
-            const bool valid = (g0 + u) < (int64_t)n;
-            const int32_t di = (int32_t)dd;
-            const uint32_t mag = di < 0 ? (0u - dd) : dd;
-            const bool out = valid && mag > 32767u;
-            code[u] = (valid && !out) ? ((di < 0 ? 0x8000u : 0u) | mag) : 0u;
-            dl[u] = di;
-            if (out) dmask |= 1u << u;
-            if (++x == nx) x = 0;
-            if (++pp == PL) pp = 0;
-        }
-        if (a.codes_out != nullptr) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (g0 + u < (int64_t)n) a.codes_out[g0 + u] = (uint16_t)code[u];
-        }
-        const int cd = __popc(dmask), cv = __popc(vmask);
-        const int wd = __reduce_add_sync(kFull, cd), wv = __reduce_add_sync(kFull, cv);
-
-        if (!a.rescan) {
-            // ---- C: bitshuffle (C5) in registers: row c = tid/8, lanes k = tid%8 ----
-            uint32_t w4[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) w4[i] = code[2 * i] | (code[2 * i + 1] << 16);
-            transpose32_group8(w4, lane & 7);
-            const int c = tid >> 3, kk = tid & 7;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) Obuf[(4 * kk + i) * 33 + c] = w4[i];
-        }
-        if (lane == 0) { s_cd[warp] = wd; s_cv[warp] = wv; }
-        __syncthreads();
-
-        // ---- D: block flags (C6): thread b owns block b = 8r + x ----
+        const int cur = it & 1;
+        const uint32_t t = s_tile[cur];
+        const bool work = t < a.tile_end;
+        if (!work && tp == 0xFFFFFFFFu) break;
         uint4 blk = make_uint4(0, 0, 0, 0);
-        uint32_t F = 0;
         bool nz = false;
-        if (!a.rescan) {
-            const int r = tid >> 3, xb = tid & 7;
-            const uint32_t* row = Obuf + r * 33 + 4 * xb;
-            blk = make_uint4(row[0], row[1], row[2], row[3]);
-            nz = (blk.x | blk.y | blk.z | blk.w) != 0;
-            F = __ballot_sync(kFull, nz);
-            if (lane == 0) s_F[warp] = F;
-        }
-        __syncthreads();
+        if (work) {
+            const int64_t s = (int64_t)t * kTileCodes;
+            const uint32_t g0 = (uint32_t)s + 8u * tid;
 
-        // ---- E: exclusive scan over tiles (C7) ----
-        uint32_t tnd = 0, tnv = 0, wpre_d = 0, wpre_v = 0, tnnz = 0, wpre_n = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            tnd += s_cd[w]; tnv += s_cv[w];
-            if (w < warp) { wpre_d += s_cd[w]; wpre_v += s_cv[w]; }
-            if (!a.rescan) {
-                const uint32_t pc = __popc(s_F[w]);
-                tnnz += pc;
-                if (w < warp) wpre_n += pc;
-            }
-        }
-        if (!a.rescan) {
-            if (warp == 0) {
-                unsigned long long en, ed, ev;
-                lookback3(a, t, tnnz, tnd, tnv, en, ed, ev);
-                if (lane == 0) {
-                    s_ex[0] = en; s_ex[1] = ed; s_ex[2] = ev;
-                    a.tpre[t] = make_uint2((uint32_t)ed, (uint32_t)ev);
-                    if (t == a.tile_end - 1) {
-                        ctrl->nnz = en + tnnz;
-                        ctrl->nd = ed + tnd;
-                        ctrl->nv = ev + tnv;
-                    }
+            // ---- A: prequantize own elements (+ bound check) and the halo ranges ----
+            float dv[8];
+            int qo[8];
+            uint32_t vmask = 0;
+            loadk<8>(a, (int64_t)g0, dv);
+            if (NDIM == 1 || !a.union_mode) {
+                if (tid == 0) smem[pad(0)] = quant_q<FB>(load1(a, s - 1), P);
+                if (NDIM >= 2) fill_range<FB>(a, P, smem + ab[1], s - (int64_t)nx - 1, kTileCodes + 1);
+                if (NDIM == 3) {
+                    fill_range<FB>(a, P, smem + ab[2], s - (int64_t)PL - 1, kTileCodes + 1);
+                    fill_range<FB>(a, P, smem + ab[3], s - (int64_t)PL - nx - 1, kTileCodes + 1);
                 }
+            } else {
+                fill_range<FB>(a, P, smem, s - (int64_t)nx - 1, (int)nx + 1);
+                if (NDIM == 3) fill_range<FB>(a, P, smem + qs, s - (int64_t)PL - nx - 1, kTileCodes + (int)nx + 1);
             }
-            if (tid < 8) {
-                const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * tid;
-                if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = s_F[tid];
-            }
-            __syncthreads();
-            // ---- F: compaction (C8): nonzero blocks in (tile, block) order ----
-            if (nz) {
-                const uint64_t bi = s_ex[0] + wpre_n + __popc(F & ((1u << lane) - 1u));
-                const uint64_t bo = 16 * bi;
-                if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = blk;
-            }
-        } else {
-            if (tid == 0) {
-                const uint2 tp = a.tpre[t];
-                s_ex[1] = tp.x; s_ex[2] = tp.y;
-            }
-            __syncthreads();
-        }
-
-        // ---- outlier records (rare): ascending element index (R7, R20) ----
-        if (tnd + tnv != 0) {
-            int id = cd, iv = cv;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int yd = __shfl_up_sync(kFull, id, o), yv = __shfl_up_sync(kFull, iv, o);
-                if (lane >= o) { id += yd; iv += yv; }
-            }
-            uint64_t pd = s_ex[1] + wpre_d + (id - cd), pv = s_ex[2] + wpre_v + (iv - cv);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const uint32_t gi = (uint32_t)(g0 + u);
-                if (dmask & (1u << u)) {
-                    if (pd < a.dcap) {
-                        if (a.o_didx) { a.o_didx[pd] = gi; a.o_dval[pd] = dl[u]; }
-                        else a.dstage[pd] = make_uint2(gi, (uint32_t)dl[u]);
+                bool vo;
+                if (FB) {
+                    qo[u] = prequant(dv[u], P, vo);
+                } else {
+                    bool hard;
+                    float qf;
+                    qo[u] = prequant_fast(dv[u], P, hard, qf);
+                    if (hard) {
+                        qo[u] = prequant(dv[u], P, vo);
                     } else {
-                        atomicOr(&ctrl->stage_overflow, 1u);
+                        const float diff = __fsub_rn(__fmul_rn(qf, P.w), dv[u]);
+                        vo = fabsf(diff) > P.eb32;
                     }
-                    ++pd;
                 }
-                if (vmask & (1u << u)) {
-                    if (pv < a.vcap) {
-                        if (a.o_vidx) { a.o_vidx[pv] = gi; a.o_vbits[pv] = __float_as_uint(dv[u]); }
-                        else a.vstage[pv] = make_uint2(gi, __float_as_uint(dv[u]));
+                if (vo && g0 + u < n) vmask |= 1u << u;
+                smem[ab[0] + pad(mo[0] + 8 * tid + u)] = qo[u];
+            }
+            __syncthreads();
+            if (tid == 0) s_tile[cur ^ 1] = a.tile_begin + atomicAdd(&ctrl->ticket, 1u);
+
+            // ---- B: Lorenzo residual (C2), codes (C3), words (C4) ----
+            int qn[NS][9];
+            qn[0][0] = smem[ab[0] + pad(mo[0] + 8 * tid - 1)];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) qn[0][u + 1] = qo[u];
+#pragma unroll
+            for (int k = 1; k < NS; ++k)
+#pragma unroll
+                for (int u = 0; u < 9; ++u) qn[k][u] = smem[ab[k] + pad(mo[k] + 8 * tid - 1 + u)];
+            uint32_t mxb = 0, myb = 0, mzb = 0;   // per-element "neighbour exists" bits
+            if (nx >= 8) {
+                uint32_t x = fmod_(g0, a.dnx), pp = fmod_(g0, a.dP);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    mxb |= (uint32_t)(x != 0) << u;
+                    myb |= (uint32_t)(pp >= nx) << u;
+                    mzb |= (uint32_t)(g0 + u >= PL) << u;
+                    if (++x == nx) x = 0;
+                    if (++pp == PL) pp = 0;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t g = g0 + u;
+                    mxb |= (uint32_t)(fmod_(g, a.dnx) != 0) << u;
+                    myb |= (uint32_t)(fmod_(g, a.dP) >= nx) << u;
+                    mzb |= (uint32_t)(g >= PL) << u;
+                }
+            }
+            uint32_t code[8];
+            int32_t dl[8];
+            uint32_t dmask = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t X = (mxb >> u) & 1u ? 0xFFFFFFFFu : 0u;
+                uint32_t dd = (uint32_t)qn[0][u + 1] - ((uint32_t)qn[0][u] & X);
+                if (NDIM >= 2) {
+                    const uint32_t Y = (myb >> u) & 1u ? 0xFFFFFFFFu : 0u;
+                    const uint32_t r1 = (uint32_t)qn[1][u + 1] - ((uint32_t)qn[1][u] & X);
+                    if (NDIM == 3) {
+                        const uint32_t Z = (mzb >> u) & 1u ? 0xFFFFFFFFu : 0u;
+                        const uint32_t r2 = (uint32_t)qn[2][u + 1] - ((uint32_t)qn[2][u] & X);
+                        const uint32_t r3 = (uint32_t)qn[3][u + 1] - ((uint32_t)qn[3][u] & X);
+                        dd -= r1 & Y;
+                        dd -= (r2 - (r3 & Y)) & Z;
                     } else {
-                        atomicOr(&ctrl->stage_overflow, 1u);
+                        dd -= r1 & Y;
                     }
-                    ++pv;
+                }
+                const bool valid = g0 + u < n;
+                const int32_t di = (int32_t)dd;
+                const uint32_t mag = di < 0 ? 0u - dd : dd;
+                const bool outl = valid && mag > 32767u;
+                code[u] = (valid && !outl) ? (((dd >> 16) & 0x8000u) | mag) : 0u;
+                dl[u] = di;
+                if (outl) dmask |= 1u << u;
+            }
+            if (a.codes_out != nullptr) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (g0 + u < n) a.codes_out[g0 + u] = (uint16_t)code[u];
+            }
+            const int cd = __popc(dmask), cv = __popc(vmask);
+            const int wd = __reduce_add_sync(kFull, cd), wv = __reduce_add_sync(kFull, cv);
+            if (!a.rescan) {
+                // ---- C5 bitshuffle in registers: row c = tid/8 of A, lanes k = tid%8 ----
+                uint32_t w4[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) w4[i] = __byte_perm(code[2 * i], code[2 * i + 1], 0x5410);
+                transpose32_group8(w4, lane & 7);
+                const int c = tid >> 3, kk = tid & 7;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) Obuf[(4 * kk + i) * 33 + c] = w4[i];
+            }
+            if (lane == 0) { s_cd[warp] = wd; s_cv[warp] = wv; }
+            __syncthreads();
+
+            // ---- C6 block flags: thread b owns block b = 8r + x of the shuffled tile ----
+            if (!a.rescan) {
+                const uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+                blk = make_uint4(row[0], row[1], row[2], row[3]);
+                nz = (blk.x | blk.y | blk.z | blk.w) != 0;
+                const uint32_t F = __ballot_sync(kFull, nz);
+                if (lane == 0) s_F[cur][warp] = F;
+            }
+
+            // ---- outlier records (rare; R7, R20): ascending element index ----
+            uint32_t tnd = 0, tnv = 0, wpre_d = 0, wpre_v = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                tnd += s_cd[w]; tnv += s_cv[w];
+                if (w < warp) { wpre_d += s_cd[w]; wpre_v += s_cv[w]; }
+            }
+            if (tnd + tnv != 0) {
+                if (tid == 0) {
+                    if (a.rescan) {
+                        const uint2 o = a.opre[t];
+                        s_ob[0] = o.x; s_ob[1] = o.y;
+                    } else {
+                        s_ob[0] = tnd ? atomicAdd(&ctrl->dcount, (unsigned long long)tnd) : 0ull;
+                        s_ob[1] = tnv ? atomicAdd(&ctrl->vcount, (unsigned long long)tnv) : 0ull;
+                        a.ocnt[t] = make_uint2(tnd, tnv);
+                        a.obase[t] = make_uint2((uint32_t)s_ob[0], (uint32_t)s_ob[1]);
+                    }
+                }
+                int id = cd, iv = cv;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int yd = __shfl_up_sync(kFull, id, o), yv = __shfl_up_sync(kFull, iv, o);
+                    if (lane >= o) { id += yd; iv += yv; }
+                }
+                __syncthreads();
+                uint64_t pd = s_ob[0] + wpre_d + (id - cd), pv = s_ob[1] + wpre_v + (iv - cv);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t gi = g0 + u;
+                    if (dmask & (1u << u)) {
+                        if (pd < a.dcap) {
+                            if (a.o_didx) { a.o_didx[pd] = gi; a.o_dval[pd] = dl[u]; }
+                            else a.dstage[pd] = make_uint2(gi, (uint32_t)dl[u]);
+                        } else {
+                            atomicOr(&ctrl->stage_overflow, 1u);
+                        }
+                        ++pd;
+                    }
+                    if (vmask & (1u << u)) {
+                        if (pv < a.vcap) {
+                            if (a.o_vidx) { a.o_vidx[pv] = gi; a.o_vbits[pv] = __float_as_uint(dv[u]); }
+                            else a.vstage[pv] = make_uint2(gi, __float_as_uint(dv[u]));
+                        } else {
+                            atomicOr(&ctrl->stage_overflow, 1u);
+                        }
+                        ++pv;
+                    }
                 }
             }
         }
+        if (a.rescan) {
+            __syncthreads();
+            if (!work) break;
+            continue;
+        }
+        __syncthreads();
+
+        // ---- C7: publish the aggregate of t, look back for the pending tile tp ----
+        if (warp == 0) {
+            if (work) {
+                uint32_t tn = 0;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) tn += __popc(s_F[cur][w]);
+                if (lane == 0) {
+                    s_tnnz[cur] = tn;
+                    st_relaxed_u64(&a.status[t], (t == a.tile_begin ? kStInc : kStAgg) | tn);
+                }
+                if (lane < 8) {
+                    const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * lane;
+                    if (fo + 4 <= a.flags_cap)
+                        *reinterpret_cast<uint32_t*>(a.flags_out + fo) = s_F[cur][lane];
+                }
+            }
+            if (tp != 0xFFFFFFFFu) {
+                unsigned long long ex = 0;
+                if (tp != a.tile_begin) {
+                    ex = lookback_wide<8, false>(a.status, tp, a.tile_begin, kStInc - 1);
+                    if (lane == 0) st_relaxed_u64(&a.status[tp], kStInc | (ex + s_tnnz[cur ^ 1]));
+                }
+                if (lane == 0) {
+                    s_ex = ex;
+                    if (tp == a.tile_end - 1) ctrl->nnz = ex + s_tnnz[cur ^ 1];
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- C8: compaction of the pending tile's nonzero blocks (tile, block order) ----
+        if (tp != 0xFFFFFFFFu && pnz) {
+            const uint32_t Fp = s_F[cur ^ 1][warp];
+            uint32_t wpre = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w)
+                if (w < warp) wpre += __popc(s_F[cur ^ 1][w]);
+            const uint64_t bo = 16 * (s_ex + wpre + __popc(Fp & ((1u << lane) - 1u)));
+            if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = pblk;
+        }
+        tp = work ? t : 0xFFFFFFFFu;
+        pblk = blk;
+        pnz = nz;
+        if (!work) break;
     }
 }
 
-// ------------------------------------------------------------------------------------
-// C9: header + outlier sections.  Grid-stride copy of the staged records.
-// ------------------------------------------------------------------------------------
-__global__ void k_finalize(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64_t d0,
-                           uint64_t d1, uint64_t d2, uint64_t n, uint64_t T,
-                           const uint2* dstage, const uint2* vstage, Ctrl* ctrl)
+// The margin/fallback mode (R2) is known only on the device when fz_compress derives the
+// parameters there, so the kernel dispatches on it (block-uniform branch).
+template <int NDIM>
+__global__ void __launch_bounds__(kCta) k_compress(CompressArgs a)
 {
-    if (ctrl->err != 0) return;
-    const uint64_t nnz = ctrl->nnz, nd = ctrl->nd, nv = ctrl->nv;
+    if (a.ctrl->p.fallback) compress_body<NDIM, true>(a);
+    else compress_body<NDIM, false>(a);
+}
+
+// ------------------------------------------------------------------------------------
+// C9: header (outlier sections are placed by k_outlier_place when there are any).
+// ------------------------------------------------------------------------------------
+__global__ void k_finalize(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64_t d0, uint64_t d1,
+                           uint64_t d2, uint64_t n, uint64_t T, Ctrl* ctrl)
+{
+    if (ctrl->err != 0 || threadIdx.x != 0) return;
+    const uint64_t nnz = ctrl->nnz, nd = ctrl->dcount, nv = ctrl->vcount;
     const uint64_t total = kHeaderBytes + 32 * T + 16 * nnz + 8 * nd + 8 * nv;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->total = total;
-    if (total > out_cap) return;
-    const uint64_t dbase = kHeaderBytes + 32 * T + 16 * nnz, vbase = dbase + 8 * nd;
-    if (!ctrl->stage_overflow) {
-        const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        const uint64_t st = (uint64_t)gridDim.x * blockDim.x;
-        for (uint64_t k = i0; k < nd; k += st) {
-            uint2 r = dstage[k];
-            *reinterpret_cast<uint2*>(out + dbase + 8 * k) = r;
+    ctrl->nd = nd;
+    ctrl->nv = nv;
+    ctrl->total = total;
+    if (total > out_cap || out == nullptr) return;
+    const fz_params& p = ctrl->p;
+    uint8_t h[128];
+    for (int i = 0; i < 128; ++i) h[i] = 0;
+    h[0] = 'F'; h[1] = 'Z'; h[2] = 'B'; h[3] = '2';
+    const uint16_t ver = 1, fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u));
+    memcpy(h + 4, &ver, 2);
+    memcpy(h + 6, &fl, 2);
+    h[8] = (uint8_t)ndim;
+    uint64_t dims[3] = {d0, d1, d2};
+    memcpy(h + 16, dims, 24);
+    memcpy(h + 40, &n, 8);
+    memcpy(h + 48, &p.eb_input, 8);
+    memcpy(h + 56, &p.eb_abs, 8);
+    memcpy(h + 64, &p.w, 4);
+    memcpy(h + 68, &p.r, 4);
+    memcpy(h + 72, &p.mn, 4);
+    memcpy(h + 76, &p.mx, 4);
+    uint64_t cnt[5] = {T, nnz, nd, nv, total};
+    memcpy(h + 80, cnt, 40);
+    uint4* o = reinterpret_cast<uint4*>(out);
+    const uint4* hs = reinterpret_cast<const uint4*>(h);
+    for (int i = 0; i < 8; ++i) o[i] = hs[i];
+}
+
+// Exclusive scan of the per-tile outlier counts (one block; only when outliers exist).
+__global__ void __launch_bounds__(1024) k_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles)
+{
+    __shared__ uint32_t wd[32], wv[32];
+    __shared__ uint32_t carry_d, carry_v;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) { carry_d = 0; carry_v = 0; }
+    __syncthreads();
+    for (uint32_t base = 0; base < ntiles; base += 1024) {
+        const uint32_t t = base + tid;
+        const uint2 c = t < ntiles ? ocnt[t] : make_uint2(0, 0);
+        uint32_t id = c.x, iv = c.y;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t yd = __shfl_up_sync(kFull, id, o), yv = __shfl_up_sync(kFull, iv, o);
+            if (lane >= o) { id += yd; iv += yv; }
         }
-        for (uint64_t k = i0; k < nv; k += st) {
-            uint2 r = vstage[k];
-            *reinterpret_cast<uint2*>(out + vbase + 8 * k) = r;
-        }
+        if (lane == 31) { wd[warp] = id; wv[warp] = iv; }
+        __syncthreads();
+        uint32_t pd = carry_d, pv = carry_v;
+        for (int w = 0; w < warp; ++w) { pd += wd[w]; pv += wv[w]; }
+        if (t < ntiles) opre[t] = make_uint2(pd + id - c.x, pv + iv - c.y);
+        __syncthreads();
+        if (tid == 1023) { carry_d = pd + id; carry_v = pv + iv; }
+        __syncthreads();
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const fz_params& p = ctrl->p;
-        uint8_t h[128];
-        for (int i = 0; i < 128; ++i) h[i] = 0;
-        h[0] = 'F'; h[1] = 'Z'; h[2] = 'B'; h[3] = '2';
-        const uint16_t ver = 1, fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u));
-        memcpy(h + 4, &ver, 2);
-        memcpy(h + 6, &fl, 2);
-        h[8] = (uint8_t)ndim;
-        uint64_t dims[3] = {d0, d1, d2};
-        memcpy(h + 16, dims, 24);
-        memcpy(h + 40, &n, 8);
-        memcpy(h + 48, &p.eb_input, 8);
-        memcpy(h + 56, &p.eb_abs, 8);
-        memcpy(h + 64, &p.w, 4);
-        memcpy(h + 68, &p.r, 4);
-        memcpy(h + 72, &p.mn, 4);
-        memcpy(h + 76, &p.mx, 4);
-        uint64_t cnt[5] = {T, nnz, nd, nv, total};
-        memcpy(h + 80, cnt, 40);
-        uint4* o = reinterpret_cast<uint4*>(out);
-        const uint4* hs = reinterpret_cast<const uint4*>(h);
-        for (int i = 0; i < 8; ++i) o[i] = hs[i];
+}
+
+// Copies each tile's staged records to its final place (records, or split lists).
+__global__ void k_outlier_place(const uint2* ocnt, const uint2* obase, const uint2* opre, uint32_t ntiles,
+                                const uint2* dstage, const uint2* vstage, uint2* dout, uint2* vout,
+                                uint32_t* didx, int32_t* dval, uint32_t* vidx, uint32_t* vbits)
+{
+    const int lane = threadIdx.x & 31;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t t = wid; t < ntiles; t += nw) {
+        const uint2 c = ocnt[t];
+        if ((c.x | c.y) == 0) continue;
+        const uint2 b = obase[t], p = opre[t];
+        for (uint32_t k = lane; k < c.x; k += 32) {
+            const uint2 r = dstage[b.x + k];
+            if (didx) { didx[p.x + k] = r.x; dval[p.x + k] = (int32_t)r.y; }
+            else dout[p.x + k] = r;
+        }
+        for (uint32_t k = lane; k < c.y; k += 32) {
+            const uint2 r = vstage[b.y + k];
+            if (vidx) { vidx[p.y + k] = r.x; vbits[p.y + k] = r.y; }
+            else vout[p.y + k] = r;
+        }
     }
 }
 
@@ -439,21 +551,32 @@ int num_sms()
     return g_sms;
 }
 
-static size_t compress_smem(int ndim)
+// Shared q arrays for a shape: fills a.union_mode / a.qstride; returns dynamic smem bytes.
+static size_t plan_smem(CompressArgs& a)
 {
-    const int nq = ndim == 1 ? 1 : (ndim == 2 ? 2 : 4);
-    return sizeof(int) * (size_t)(nq * kQStride + 32 * 33);
+    const uint32_t ndim = a.g.ndim;
+    uint32_t narr, len;
+    if (ndim == 1) {
+        narr = 1;
+        len = kTileCodes + 1;
+        a.union_mode = 0;
+    } else if (a.g.nx + 1 <= kUnionHaloMax) {
+        a.union_mode = 1;
+        narr = ndim == 3 ? 2 : 1;
+        len = kTileCodes + a.g.nx + 1;
+    } else {
+        a.union_mode = 0;
+        narr = ndim == 3 ? 4 : 2;
+        len = kTileCodes + 1;
+    }
+    a.qstride = (pad_words(len) + 31) & ~31u;
+    return sizeof(int) * ((size_t)narr * a.qstride + 32 * 33);
 }
 
 template <int NDIM>
-static cudaError_t launch_compress_t(const CompressArgs& a, uint32_t ntiles, cudaStream_t st)
+static cudaError_t launch_compress_t(const CompressArgs& a, size_t sm, uint32_t ntiles, cudaStream_t st)
 {
-    const size_t sm = compress_smem(NDIM);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_compress<NDIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr = true;
-    }
+    cudaFuncSetAttribute(k_compress<NDIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compress<NDIM>, kCta, sm);
     if (per_sm < 1) per_sm = 1;
@@ -464,27 +587,31 @@ static cudaError_t launch_compress_t(const CompressArgs& a, uint32_t ntiles, cud
     return cudaGetLastError();
 }
 
-cudaError_t launch_compress(const CompressArgs& a, cudaStream_t st)
+cudaError_t launch_compress(const CompressArgs& a_in, cudaStream_t st)
 {
+    CompressArgs a = a_in;
+    a.dnx = make_fastdiv(a.g.nx);
+    a.dP = make_fastdiv(a.g.P);
+    const size_t sm = plan_smem(a);
     const uint32_t ntiles = a.tile_end - a.tile_begin;
-    count_launch();
+    LaunchProf lp(K_COMPRESS, st);
     switch (a.g.ndim) {
-        case 1: return launch_compress_t<1>(a, ntiles, st);
-        case 2: return launch_compress_t<2>(a, ntiles, st);
-        default: return launch_compress_t<3>(a, ntiles, st);
+        case 1: return launch_compress_t<1>(a, sm, ntiles, st);
+        case 2: return launch_compress_t<2>(a, sm, ntiles, st);
+        default: return launch_compress_t<3>(a, sm, ntiles, st);
     }
 }
 
-cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint32_t ntiles, const fz_params* p,
-                        cudaStream_t st)
+cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint32_t ntiles,
+                        const fz_params* p, cudaStream_t st)
 {
     fz_params pp{};
     if (p) pp = *p;
     unsigned grid = (unsigned)((ntiles + 255) / 256);
     if (grid < 1) grid = 1;
     if (grid > 1024) grid = 1024;
-    count_launch();
-    k_init<<<grid, 256, 0, st>>>(ctrl, status, ntiles, p ? 1 : 0, pp);
+    LaunchProf lp(K_INIT, st);
+    k_init<<<grid, 256, 0, st>>>(ctrl, status, ocnt, ntiles, p ? 1 : 0, pp);
     return cudaGetLastError();
 }
 
@@ -493,25 +620,45 @@ cudaError_t launch_range(const float* d, uint64_t n, Ctrl* ctrl, cudaStream_t st
     uint64_t want = (n / 4 + 255) / 256;
     uint64_t cap = (uint64_t)num_sms() * 8;
     unsigned grid = (unsigned)(want < 1 ? 1 : (want > cap ? cap : want));
-    count_launch();
+    LaunchProf lp(K_RANGE, st);
     k_range<<<grid, 256, 0, st>>>(d, n, ctrl);
     return cudaGetLastError();
 }
 
 cudaError_t launch_params(Ctrl* ctrl, int mode, double eb, uint64_t n, cudaStream_t st)
 {
-    count_launch();
+    LaunchProf lp(K_PARAMS, st);
     k_params<<<1, 32, 0, st>>>(ctrl, mode, eb, n);
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint64_t n, uint64_t T,
-                            const uint2* dstage, const uint2* vstage, Ctrl* ctrl, cudaStream_t st)
+cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint64_t n, uint64_t T, Ctrl* ctrl,
+                            cudaStream_t st)
 {
     uint64_t d[3] = {1, 1, 1};
     for (uint32_t k = 0; k < s.ndim; ++k) d[k] = s.dims[k];
-    count_launch();
-    k_finalize<<<num_sms(), 256, 0, st>>>(out, cap, s.ndim, d[0], d[1], d[2], n, T, dstage, vstage, ctrl);
+    LaunchProf lp(K_FINALIZE, st);
+    k_finalize<<<1, 32, 0, st>>>(out, cap, s.ndim, d[0], d[1], d[2], n, T, ctrl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st)
+{
+    LaunchProf lp(K_OUTLIERS, st);
+    k_outlier_scan<<<1, 1024, 0, st>>>(ocnt, opre, ntiles);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_outlier_place(const uint2* ocnt, const uint2* obase, const uint2* opre, uint32_t ntiles,
+                                 const uint2* dstage, const uint2* vstage, uint2* dout, uint2* vout,
+                                 uint32_t* didx, int32_t* dval, uint32_t* vidx, uint32_t* vbits, cudaStream_t st)
+{
+    LaunchProf lp(K_OUTLIERS, st);
+    unsigned grid = (unsigned)((ntiles + 7) / 8);
+    if (grid > (unsigned)num_sms() * 8) grid = num_sms() * 8;
+    if (grid < 1) grid = 1;
+    k_outlier_place<<<grid, 256, 0, st>>>(ocnt, obase, opre, ntiles, dstage, vstage, dout, vout, didx, dval,
+                                          vidx, vbits);
     return cudaGetLastError();
 }
 

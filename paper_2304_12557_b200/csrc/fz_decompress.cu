@@ -62,37 +62,6 @@ __global__ void k_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, 
     }
 }
 
-// Look-back with one 62-bit count (payload offsets).
-__device__ __forceinline__ unsigned long long lookback_count(unsigned long long* st, uint32_t t,
-                                                             unsigned long long cnt)
-{
-    const int lane = threadIdx.x & 31;
-    const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kMask = kAgg - 1;
-    if (t == 0) {
-        if (lane == 0) st_release_u64(&st[0], kInc | cnt);
-        return 0;
-    }
-    if (lane == 0) st_release_u64(&st[t], kAgg | cnt);
-    unsigned long long ex = 0;
-    int64_t p = (int64_t)t - 1;
-    while (true) {
-        const int64_t q = p - lane;
-        unsigned long long s = kInc;
-        if (q >= 0) {
-            do { s = ld_acquire_u64(&st[q]); } while ((s >> 62) == 0);
-        }
-        const uint32_t incl = __ballot_sync(kFull, (s >> 62) == 2);
-        const int stop = incl ? __ffs(incl) - 1 : 31;
-        unsigned long long c = lane <= stop ? (s & kMask) : 0;
-        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-        ex += c;
-        if (incl) break;
-        p -= 32;
-    }
-    if (lane == 0) st_release_u64(&st[t], kInc | (ex + cnt));
-    return ex;
-}
-
 // Segmented-sum element: (reset flag, value).  combine(earlier, later).
 struct Seg {
     uint32_t f, v;
@@ -102,192 +71,222 @@ __device__ __forceinline__ Seg seg_combine(Seg e, Seg l)
     return l.f ? l : Seg{e.f, e.v + l.v};
 }
 
-// Look-back for the segmented x-scan: status = state(2) | reset(1) @32 | value(32).
-// Returns the carry into tile t (sum since the last row start before the tile).
-__device__ __forceinline__ uint32_t lookback_seg(unsigned long long* st, uint32_t t, Seg agg)
-{
-    const int lane = threadIdx.x & 31;
-    const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62;
-    auto pack = [](Seg s) { return ((unsigned long long)s.f << 32) | s.v; };
-    if (t == 0) {
-        if (lane == 0) st_release_u64(&st[0], kInc | pack(agg));
-        return 0;
-    }
-    // a tile containing a row start has a carry-independent inclusive value
-    if (lane == 0) st_release_u64(&st[t], (agg.f ? kInc : kAgg) | pack(agg));
-    Seg acc{0, 0};
-    int64_t p = (int64_t)t - 1;
-    while (true) {
-        const int64_t q = p - lane;
-        unsigned long long s = kInc;   // before tile 0: identity, inclusive
-        if (q >= 0) {
-            do { s = ld_acquire_u64(&st[q]); } while ((s >> 62) == 0);
-        }
-        Seg e{(uint32_t)((s >> 32) & 1u), (uint32_t)s};
-        const bool term = ((s >> 62) == 2) || e.f;
-        const uint32_t tm = __ballot_sync(kFull, term);
-        const int stop = tm ? __ffs(tm) - 1 : 31;
-        if (lane > stop) e = Seg{0, 0};
-        // ordered reduction: lane i holds range [i, i+o); higher lanes are earlier tiles
-        for (int o = 1; o < 32; o <<= 1) {
-            Seg hi{__shfl_down_sync(kFull, e.f, o), __shfl_down_sync(kFull, e.v, o)};
-            if (lane + o < 32) e = seg_combine(hi, e);
-        }
-        acc = seg_combine(Seg{__shfl_sync(kFull, e.f, 0), __shfl_sync(kFull, e.v, 0)}, acc);
-        if (tm) break;
-        p -= 32;
-    }
-    if (lane == 0 && !agg.f) st_release_u64(&st[t], kInc | pack(seg_combine(acc, agg)));
-    return acc.v;
-}
-
+// ------------------------------------------------------------------------------------
+// Tile decoder, a 3-stage software pipeline per CTA (tiles from a ticket):
+//   stage 1 (tile t)  : read its 8 flag words, publish its block count (aggregate);
+//   stage 2 (tile t1) : payload offset by wide look-back, gather the 16-byte blocks (D2),
+//                       un-shuffle (D3), unpack + delta patch (D4), local segmented x-scan,
+//                       publish the x aggregate (a tile holding a row start is terminal);
+//   stage 3 (tile t2) : x carry by wide look-back, final x-scanned q written (D5 along x;
+//                       1-D fields are dequantized here, D6).
+// Each look-back targets a tile whose predecessors have had a whole iteration to publish.
+// ------------------------------------------------------------------------------------
 template <int NDIM>
 __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
 {
     __shared__ uint32_t Obuf[32 * 33];
     __shared__ int32_t D[kTileCodes];
-    __shared__ uint32_t s_tile[2], s_F[8], s_wf[8], s_wv[8];
+    __shared__ uint32_t s_tile[2], s_F[2][8], s_tnnz[2], s_wf[8], s_wv[8];
     __shared__ unsigned long long s_off;
     __shared__ uint32_t s_carry;
+    __shared__ uint32_t s_tagf[2], s_tagv[2];
     __shared__ uint64_t s_lo, s_hi;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Ctrl* ctrl = a.ctrl;
     if (ctrl->err != 0) return;
     const uint32_t n = a.g.n, nx = a.g.nx;
+    constexpr uint32_t NONE = 0xFFFFFFFFu;
 
     if (tid == 0) s_tile[0] = atomicAdd(&ctrl->ticket, 1u);
     __syncthreads();
+    uint32_t t1 = NONE, t2 = NONE;
+    // stage-3 state of tile t2, per thread
+    uint32_t loc2[8];
+    uint32_t rmask2 = 0;
+    Seg wp2{0, 0}, lx2{0, 0};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) loc2[u] = 0;
+
     for (int it = 0;; ++it) {
-        const uint32_t t = s_tile[it & 1];
-        if (t >= a.tiles) break;
-        const int64_t s = (int64_t)t * kTileCodes;
-        const int64_t g0 = s + 8 * tid;
+        const int cur = it & 1;
+        const uint32_t t = s_tile[cur];
+        const bool work = t < a.tiles;
+        if (!work && t1 == NONE && t2 == NONE) break;
 
-        // ---- D1: flags and payload offsets ----
-        const uint32_t F = reinterpret_cast<const uint32_t*>(a.flags)[8 * (uint64_t)t + warp];
-        const bool nz = (F >> lane) & 1u;
-        if (lane == 0) s_F[warp] = F;
-        if (tid == 0 && a.nd > 0) {
-            uint64_t lo = 0, hi = a.nd;           // first record with idx >= s
-            while (lo < hi) { uint64_t m = (lo + hi) / 2; if ((int64_t)a.drec[m].x < s) lo = m + 1; else hi = m; }
+        // ---- stage 1: flags of tile t ----
+        if (work && lane == 0) s_F[cur][warp] = reinterpret_cast<const uint32_t*>(a.flags)[8 * (uint64_t)t + warp];
+        __syncthreads();
+        if (tid == 0 && work) s_tile[cur ^ 1] = atomicAdd(&ctrl->ticket, 1u);
+        if (warp == 0) {
+            if (work) {
+                uint32_t tn = 0;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) tn += __popc(s_F[cur][w]);
+                if (lane == 0) {
+                    s_tnnz[cur] = tn;
+                    st_relaxed_u64(&a.st_nnz[t], (t == 0 ? kStInc : kStAgg) | tn);
+                }
+            }
+            if (t1 != NONE) {
+                unsigned long long ex = 0;
+                if (t1 != 0) {
+                    ex = lookback_wide<8, false>(a.st_nnz, t1, 0, kStInc - 1);
+                    if (lane == 0) st_relaxed_u64(&a.st_nnz[t1], kStInc | (ex + s_tnnz[cur ^ 1]));
+                }
+                if (lane == 0) {
+                    s_off = ex;
+                    if (t1 == a.tiles - 1) ctrl->nnz = ex + s_tnnz[cur ^ 1];
+                }
+            }
+        }
+        if (tid == 32 && t1 != NONE) {
+            uint64_t lo = 0, hi = 0;
+            if (a.nd > 0) {
+                const int64_t s1 = (int64_t)t1 * kTileCodes;
+                uint64_t l = 0, h = a.nd;
+                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < s1) l = m + 1; else h = m; }
+                lo = l;
+                h = a.nd;
+                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < s1 + kTileCodes) l = m + 1; else h = m; }
+                hi = l;
+            }
             s_lo = lo;
-            hi = a.nd;                            // first record with idx >= s + 2048
-            while (lo < hi) { uint64_t m = (lo + hi) / 2; if ((int64_t)a.drec[m].x < s + kTileCodes) lo = m + 1; else hi = m; }
-            s_hi = lo;
-        } else if (tid == 0) {
-            s_lo = s_hi = 0;
-        }
-        __syncthreads();
-        if (tid == 0) s_tile[(it + 1) & 1] = atomicAdd(&ctrl->ticket, 1u);
-        uint32_t tnnz = 0, wpre = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const uint32_t pc = __popc(s_F[w]);
-            tnnz += pc;
-            if (w < warp) wpre += pc;
-        }
-        if (warp == 0) {
-            unsigned long long ex = lookback_count(a.st_nnz, t, tnnz);
-            if (lane == 0) {
-                s_off = ex;
-                if (t == a.tiles - 1) ctrl->nnz = ex + tnnz;
-            }
+            s_hi = hi;
         }
         __syncthreads();
 
-        // ---- D2: gather block b = tid into the shuffled tile O ----
-        {
-            uint4 blk = make_uint4(0, 0, 0, 0);
-            if (nz) {
-                const uint64_t bi = s_off + wpre + __popc(F & ((1u << lane) - 1u));
-                if (bi < a.nnz_total) blk = reinterpret_cast<const uint4*>(a.payload)[bi];
-                else atomicExch(&ctrl->err, (int)FZ_ERR_CORRUPT);
-            }
-            const int r = tid >> 3, xb = tid & 7;
-            uint32_t* row = Obuf + r * 33 + 4 * xb;
-            row[0] = blk.x; row[1] = blk.y; row[2] = blk.z; row[3] = blk.w;
-        }
-        __syncthreads();
-
-        // ---- D3: un-shuffle: column c of O -> row c of A (same 32x32 bit transpose) ----
-        uint32_t w4[4];
-        {
-            const int c = tid >> 3, kk = tid & 7;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) w4[i] = Obuf[(4 * kk + i) * 33 + c];
-            transpose32_group8(w4, lane & 7);
-        }
-        // ---- D4: unpack (0x8000 -> 0, R8) ----
-        int32_t dl[8];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t lo16 = w4[i] & 0xFFFFu, hi16 = w4[i] >> 16;
-            dl[2 * i] = (lo16 & 0x8000u) ? -(int32_t)(lo16 & 0x7FFFu) : (int32_t)lo16;
-            dl[2 * i + 1] = (hi16 & 0x8000u) ? -(int32_t)(hi16 & 0x7FFFu) : (int32_t)hi16;
-        }
-        if (s_hi > s_lo) {   // delta outliers of this tile (rare; uniform branch)
-#pragma unroll
-            for (int u = 0; u < 8; ++u) D[8 * tid + u] = dl[u];
-            __syncthreads();
-            for (uint64_t k = s_lo + tid; k < s_hi; k += kCta) {
-                const uint2 r = a.drec[k];
-                D[r.x - (uint32_t)s] = (int32_t)r.y;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int u = 0; u < 8; ++u) dl[u] = D[8 * tid + u];
-        }
-
-        // ---- D5 (x): segmented inclusive scan, resets at row starts x == 0 ----
+        // ---- stage 2: decode tile t1 ----
         uint32_t loc[8];
-        uint32_t rmask = 0;     // bit u: a row start at or before u inside this thread
-        Seg me{0, 0};
-        {
-            uint32_t x = (uint32_t)(g0 % nx);
+        uint32_t rmask = 0;
+        Seg wp{0, 0}, lex{0, 0};
+        if (t1 != NONE) {
+            const int64_t s1 = (int64_t)t1 * kTileCodes;
+            const uint32_t g0 = (uint32_t)s1 + 8u * tid;
+            {
+                const uint32_t F = s_F[cur ^ 1][warp];
+                uint32_t wpre = 0;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (x == 0) { me.f = 1; me.v = 0; }
-                me.v += (uint32_t)dl[u];
-                loc[u] = me.v;
-                if (me.f) rmask |= 1u << u;
-                if (++x == nx) x = 0;
+                for (int w = 0; w < 8; ++w)
+                    if (w < warp) wpre += __popc(s_F[cur ^ 1][w]);
+                uint4 blk = make_uint4(0, 0, 0, 0);
+                if ((F >> lane) & 1u) {
+                    const uint64_t bi = s_off + wpre + __popc(F & ((1u << lane) - 1u));
+                    if (bi < a.nnz_total) blk = reinterpret_cast<const uint4*>(a.payload)[bi];
+                    else atomicExch(&ctrl->err, (int)FZ_ERR_CORRUPT);
+                }
+                uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+                row[0] = blk.x; row[1] = blk.y; row[2] = blk.z; row[3] = blk.w;
+            }
+            __syncthreads();
+            // D3: column c of O -> row c of A (the same 32x32 bit transpose)
+            uint32_t w4[4];
+            {
+                const int c = tid >> 3, kk = tid & 7;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) w4[i] = Obuf[(4 * kk + i) * 33 + c];
+                transpose32_group8(w4, lane & 7);
+            }
+            // D4: unpack (0x8000 -> 0, R8), delta outliers
+            int32_t dl[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t lo16 = w4[i] & 0xFFFFu, hi16 = w4[i] >> 16;
+                dl[2 * i] = (lo16 & 0x8000u) ? -(int32_t)(lo16 & 0x7FFFu) : (int32_t)lo16;
+                dl[2 * i + 1] = (hi16 & 0x8000u) ? -(int32_t)(hi16 & 0x7FFFu) : (int32_t)hi16;
+            }
+            if (s_hi > s_lo) {   // rare, block-uniform
+#pragma unroll
+                for (int u = 0; u < 8; ++u) D[8 * tid + u] = dl[u];
+                __syncthreads();
+                for (uint64_t k = s_lo + tid; k < s_hi; k += kCta) {
+                    const uint2 r = a.drec[k];
+                    D[r.x - (uint32_t)s1] = (int32_t)r.y;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int u = 0; u < 8; ++u) dl[u] = D[8 * tid + u];
+            }
+            // local segmented inclusive x-scan, resets at row starts (x == 0)
+            Seg me{0, 0};
+            if (nx >= 8) {
+                uint32_t x = fmod_(g0, a.dnx);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (x == 0) { me.f = 1; me.v = 0; }
+                    me.v += (uint32_t)dl[u];
+                    loc[u] = me.v;
+                    if (me.f) rmask |= 1u << u;
+                    if (++x == nx) x = 0;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (fmod_(g0 + u, a.dnx) == 0) { me.f = 1; me.v = 0; }
+                    me.v += (uint32_t)dl[u];
+                    loc[u] = me.v;
+                    if (me.f) rmask |= 1u << u;
+                }
+            }
+            Seg inc = me;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const Seg up{__shfl_up_sync(kFull, inc.f, o), __shfl_up_sync(kFull, inc.v, o)};
+                if (lane >= o) inc = seg_combine(up, inc);
+            }
+            lex = Seg{__shfl_up_sync(kFull, inc.f, 1), __shfl_up_sync(kFull, inc.v, 1)};
+            if (lane == 0) lex = Seg{0, 0};
+            if (lane == 31) { s_wf[warp] = inc.f; s_wv[warp] = inc.v; }
+            __syncthreads();
+            Seg tagg{0, 0};
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const Seg sw{s_wf[w], s_wv[w]};
+                if (w < warp) wp = seg_combine(wp, sw);
+                tagg = seg_combine(tagg, sw);
+            }
+            if (tid == 0) {
+                s_tagf[cur] = tagg.f;
+                s_tagv[cur] = tagg.v;
+                // a row start inside the tile makes its value carry-independent: terminal
+                st_relaxed_u64(&a.st_x[t1], ((tagg.f || t1 == 0) ? kStInc : kStAgg) | tagg.v);
             }
         }
-        // warp inclusive segmented scan
-        Seg inc = me;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            Seg up{__shfl_up_sync(kFull, inc.f, o), __shfl_up_sync(kFull, inc.v, o)};
-            if (lane >= o) inc = seg_combine(up, inc);
-        }
-        Seg lex{__shfl_up_sync(kFull, inc.f, 1), __shfl_up_sync(kFull, inc.v, 1)};
-        if (lane == 0) lex = Seg{0, 0};
-        if (lane == 31) { s_wf[warp] = inc.f; s_wv[warp] = inc.v; }
-        __syncthreads();
-        Seg wp{0, 0}, tagg{0, 0};
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const Seg sw{s_wf[w], s_wv[w]};
-            if (w < warp) wp = seg_combine(wp, sw);
-            tagg = seg_combine(tagg, sw);
-        }
-        if (warp == 0) {
-            const uint32_t carry = lookback_seg(a.st_x, t, tagg);
+
+        // ---- stage 3: x carry of tile t2 ----
+        if (warp == 0 && t2 != NONE) {
+            uint32_t carry = 0;
+            if (t2 != 0) {
+                carry = (uint32_t)lookback_wide<8, false>(a.st_x, t2, 0, 0xFFFFFFFFull);
+                if (lane == 0 && !s_tagf[cur ^ 1])
+                    st_relaxed_u64(&a.st_x[t2], kStInc | (uint32_t)(carry + s_tagv[cur ^ 1]));
+            }
             if (lane == 0) s_carry = carry;
         }
         __syncthreads();
-        Seg acc{0, s_carry};
-        acc = seg_combine(acc, wp);
-        acc = seg_combine(acc, lex);
+        if (t2 != NONE) {
+            const int64_t s2 = (int64_t)t2 * kTileCodes;
+            Seg acc{0, s_carry};
+            acc = seg_combine(acc, wp2);
+            acc = seg_combine(acc, lx2);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int64_t g = g0 + u;
-            if (g < (int64_t)n) {
-                const uint32_t qv = ((rmask >> u) & 1u) ? loc[u] : acc.v + loc[u];
-                if (NDIM == 1 && a.x_out != nullptr) a.x_out[g] = __fmul_rn(__int2float_rn((int32_t)qv), a.w);
-                else a.q_out[g] = (int32_t)qv;
+            for (int u = 0; u < 8; ++u) {
+                const int64_t g = s2 + 8 * tid + u;
+                if (g < (int64_t)n) {
+                    const uint32_t qv = ((rmask2 >> u) & 1u) ? loc2[u] : acc.v + loc2[u];
+                    if (NDIM == 1 && a.x_out != nullptr) a.x_out[g] = __fmul_rn(__int2float_rn((int32_t)qv), a.w);
+                    else a.q_out[g] = (int32_t)qv;
+                }
             }
         }
+        t2 = t1;
+        if (t1 != NONE) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) loc2[u] = loc[u];
+            rmask2 = rmask;
+            wp2 = wp;
+            lx2 = lex;
+        }
+        t1 = work ? t : NONE;
     }
 }
 
@@ -365,7 +364,7 @@ static unsigned grid_for(uint64_t work, int per_thread = 1)
 cudaError_t launch_decode_init(Ctrl* ctrl, unsigned long long* st_nnz, unsigned long long* st_x,
                                uint32_t ntiles, cudaStream_t st)
 {
-    count_launch();
+    LaunchProf lp(K_DINIT, st);
     k_decode_init<<<grid_for(ntiles), 256, 0, st>>>(ctrl, st_nnz, st_x, ntiles);
     return cudaGetLastError();
 }
@@ -374,14 +373,16 @@ cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n,
                                      cudaStream_t st)
 {
     if (cnt == 0) return cudaSuccess;
-    count_launch();
+    LaunchProf lp(K_VALIDATE, st);
     k_validate_outliers<<<grid_for(cnt), 256, 0, st>>>(rec, cnt, n, ctrl);
     return cudaGetLastError();
 }
 
 template <int NDIM>
-static cudaError_t launch_decode_t(const DecodeArgs& a, cudaStream_t st)
+static cudaError_t launch_decode_t(const DecodeArgs& a_in, cudaStream_t st)
 {
+    DecodeArgs a = a_in;
+    a.dnx = make_fastdiv(a.g.nx);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_tiles<NDIM>, kCta, 0);
     if (per_sm < 1) per_sm = 1;
@@ -394,7 +395,7 @@ static cudaError_t launch_decode_t(const DecodeArgs& a, cudaStream_t st)
 
 cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st)
 {
-    count_launch();
+    LaunchProf lp(K_DECODE, st);
     switch (a.g.ndim) {
         case 1: return launch_decode_t<1>(a, st);
         case 2: return launch_decode_t<2>(a, st);
@@ -407,19 +408,25 @@ cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t
 {
     const uint64_t nch = (L + kScanChunk - 1) / kScanChunk;
     const uint64_t work = outer * nch * W;
-    count_launch();
-    k_scan_sums<<<grid_for(work), 256, 0, st>>>(data, outer, L, W, nch, sums);
-    count_launch();
-    k_scan_chunks<<<grid_for(outer * W), 256, 0, st>>>(outer, W, nch, sums);
-    count_launch();
-    k_scan_apply<<<grid_for(work), 256, 0, st>>>(data, outer, L, W, nch, sums, dequant_w);
+    {
+        LaunchProf lp(K_SCAN_SUMS, st);
+        k_scan_sums<<<grid_for(work), 256, 0, st>>>(data, outer, L, W, nch, sums);
+    }
+    {
+        LaunchProf lp(K_SCAN_CHUNKS, st);
+        k_scan_chunks<<<grid_for(outer * W), 256, 0, st>>>(outer, W, nch, sums);
+    }
+    {
+        LaunchProf lp(K_SCAN_APPLY, st);
+        k_scan_apply<<<grid_for(work), 256, 0, st>>>(data, outer, L, W, nch, sums, dequant_w);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint64_t n, cudaStream_t st)
 {
     if (cnt == 0) return cudaSuccess;
-    count_launch();
+    LaunchProf lp(K_VPATCH, st);
     k_value_patch<<<grid_for(cnt), 256, 0, st>>>(out, vrec, cnt, n);
     return cudaGetLastError();
 }

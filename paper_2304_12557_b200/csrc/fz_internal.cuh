@@ -33,14 +33,16 @@ struct Ctrl {
     uint32_t stage_overflow;         // outlier staging overflowed -> rescan pass
     // results (written by the last tile / k_finalize)
     unsigned long long nnz, nd, nv, total;
-    uint32_t ticket2;                // decoder x-scan ticket
-    uint32_t pad;
+    unsigned long long dcount, vcount;   // outlier staging allocation counters (= totals)
 };
 static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 
 // Workspace carve (host computes it identically for every call).
+//   status : per-tile look-back word, state(2) | inclusive-or-aggregate nnz(62)
+//   ocnt   : per-tile (n_delta, n_value); obase: staging offsets of the tile's records;
+//   opre   : per-tile exclusive outlier offsets (filled only when outliers exist)
 struct Layout {
-    size_t ctrl, status, aggv, inclv, tpre, dstage, vstage, total;
+    size_t ctrl, status, ocnt, obase, opre, dstage, vstage, total;
     uint64_t dcap, vcap;             // staging capacities in records
 };
 
@@ -51,15 +53,43 @@ inline Layout compress_layout(uint64_t n, uint64_t tiles)
     size_t off = 0;
     L.ctrl = off;   off += 512;
     L.status = off; off = al(off + 8 * tiles);
-    L.aggv = off;   off = al(off + 4 * tiles);
-    L.inclv = off;  off = al(off + 4 * tiles);
-    L.tpre = off;   off = al(off + 8 * tiles);
+    L.ocnt = off;   off = al(off + 8 * tiles);
+    L.obase = off;  off = al(off + 8 * tiles);
+    L.opre = off;   off = al(off + 8 * tiles);
     L.dcap = n / 64 + 1024;
     L.vcap = n / 64 + 1024;
     L.dstage = off; off = al(off + 8 * L.dcap);
     L.vstage = off; off = al(off + 8 * L.vcap);
     L.total = off;
     return L;
+}
+
+// ------------------------------------------------------------------------------------
+// Fast 32-bit unsigned division by a runtime constant (round-up multiplier method):
+//   n / d = (umulhi(n, m) + n) >> s,  s = ceil(log2 d),  m = floor(2^32 (2^s - d) / d) + 1.
+// ------------------------------------------------------------------------------------
+struct FastDiv {
+    uint32_t d, m, s;
+};
+
+inline FastDiv make_fastdiv(uint32_t d)
+{
+    FastDiv f{d, 0, 0};
+    uint32_t s = 0;
+    while ((1ull << s) < d) ++s;
+    f.s = s;
+    f.m = (uint32_t)((((1ull << s) - d) << 32) / d + 1);
+    return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f)
+{
+    const uint64_t hi = __umulhi(n, f.m);
+    return (uint32_t)((hi + n) >> f.s);
+}
+__device__ __forceinline__ uint32_t fmod_(uint32_t n, const FastDiv& f)
+{
+    return n - fdiv(n, f) * f.d;
 }
 
 // ------------------------------------------------------------------------------------
@@ -105,6 +135,78 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p)
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ------------------------------------------------------------------------------------
+// Wide decoupled look-back (C7).  Status word of tile t: state(2) | value(62),
+// state 1 = aggregate, 2 = inclusive prefix.  `term` additionally marks aggregates that do
+// not depend on earlier tiles (segmented scans: a row start inside the tile, bit 61).
+// One warp reads W = 32 * PER_LANE predecessors per round (relaxed gpu-scope loads, no L1
+// invalidation: each status word is self-contained), finds the nearest terminal entry and
+// sums the values from it up to t-1.  Entries before `first` count as inclusive zeros.
+// Must be called by a full warp; returns the sum (exclusive prefix / carry) in every lane.
+// ------------------------------------------------------------------------------------
+constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62;
+constexpr unsigned long long kStTerm = 1ull << 61;
+
+template <int PER_LANE, bool SEG>
+__device__ __forceinline__ unsigned long long lookback_wide(const unsigned long long* st, int64_t t,
+                                                            int64_t first, unsigned long long vmask)
+{
+    const int lane = threadIdx.x & 31;
+    unsigned long long sum = 0;
+    int64_t hi = t - 1;
+    while (hi >= first) {
+        unsigned long long v[PER_LANE];
+        uint32_t termbits, zerobits;
+        for (;;) {
+            termbits = 0;
+            zerobits = 0;
+#pragma unroll
+            for (int k = 0; k < PER_LANE; ++k) {
+                const int64_t idx = hi - (int64_t)lane * PER_LANE - k;   // k = 0 nearest
+                unsigned long long s = kStInc;
+                if (idx >= first) s = ld_relaxed_u64(st + idx);
+                v[k] = s;
+                const bool term = (s >> 62) == 2 || (SEG && (s & kStTerm));
+                termbits |= (uint32_t)term << k;
+                zerobits |= (uint32_t)((s >> 62) == 0) << k;
+            }
+            // nearest terminal: lowest lane having one, lowest k inside that lane
+            const uint32_t lanes_t = __ballot_sync(0xFFFFFFFFu, termbits != 0);
+            const int tl = lanes_t ? __ffs(lanes_t) - 1 : 32;
+            // all entries nearer than the terminal must be published
+            uint32_t need = 0;
+            if (lane < tl) need = zerobits;
+            else if (lane == tl) need = zerobits & ((termbits & (0u - termbits)) - 1u);
+            if (__ballot_sync(0xFFFFFFFFu, need != 0) == 0) {
+                unsigned long long part = 0;
+                if (lane <= tl) {
+                    const int kmax = (lane == tl) ? __ffs(termbits) - 1 : PER_LANE - 1;
+#pragma unroll
+                    for (int k = 0; k < PER_LANE; ++k)
+                        if (k <= kmax) part += v[k] & vmask;
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
+                sum += part;
+                if (lanes_t) return sum;
+                break;
+            }
+        }
+        hi -= 32 * PER_LANE;
+    }
+    return sum;
 }
 
 // 16-byte streaming load of the read-only field.
@@ -185,6 +287,21 @@ __device__ __forceinline__ int prequant(float d, const QuantP& P, bool& vout)
     return q;
 }
 
+// Margin-mode fast path: the magic-rounded q is the exact nearest bin whenever the exact
+// residual satisfies |e| < w/2 (no tie, no correction); otherwise `hard` is raised and the
+// caller re-runs the full rule (rare: d/w within ~|d/w| 2^-23 of a half-integer).
+// In margin mode |q| < 2^21 always (Appendix A), so no range checks are needed.
+__device__ __forceinline__ int prequant_fast(float d, const QuantP& P, bool& hard, float& qf)
+{
+    const float kMagic = 12582912.0f;
+    float v = __fmul_rn(d, P.r);
+    float t = __fadd_rn(v, kMagic);
+    qf = __fsub_rn(t, kMagic);
+    float e = __fmaf_rn(-qf, P.w, d);
+    hard = fabsf(e) >= P.h;
+    return __float_as_int(t) - 0x4B400000;
+}
+
 // q only (halo elements): identical arithmetic, no bound check.
 __device__ __forceinline__ int prequant_q(float d, const QuantP& P)
 {
@@ -262,7 +379,12 @@ struct CompressArgs {
     const float* field;       // element g at field[g - base]
     uint64_t base;
     Geom g;
+    FastDiv dnx, dP;          // x extent, plane size
     uint32_t tile_begin, tile_end;
+    // neighbour streams (SV §7 hard part 3): q of the element and of its y-1, z-1, (y-1,z-1)
+    // neighbours live in shared arrays; union = [s-nx-1, e) and [s-P-nx-1, e-P)
+    int union_mode;           // 1: one array per plane; 0: one 2049-element array per stream
+    uint32_t qstride;         // padded words per shared q array
     uint8_t* flags_out;       // 32 B per tile, tile t at (t - tile_begin) * 32
     uint8_t* payload_out;     // 16 B blocks
     uint64_t flags_cap;       // bytes writable at flags_out
@@ -271,16 +393,16 @@ struct CompressArgs {
     uint2* vstage;            // (idx, bits) records
     uint64_t dcap, vcap;      // staging capacities (records)
     unsigned long long* status;
-    uint32_t* aggv;
-    uint32_t* inclv;
-    uint2* tpre;              // per-tile exclusive (n_delta, n_value)
+    uint2* ocnt;              // per-tile (n_delta, n_value)
+    uint2* obase;             // per-tile staging offsets
+    const uint2* opre;        // rescan: per-tile final (exclusive) outlier offsets
     Ctrl* ctrl;
     uint16_t* codes_out;      // debug hook: codes at element index (may be null)
-    uint32_t* o_didx;         // debug hook: split outlier lists at final positions (may be null)
+    uint32_t* o_didx;         // rescan into split lists (debug hook), else records
     int32_t* o_dval;
     uint32_t* o_vidx;
     uint32_t* o_vbits;
-    int rescan;               // 1: outliers only, straight to final offsets via tpre
+    int rescan;               // 1: outliers only, straight to final offsets via opre
 };
 
 }  // namespace fz

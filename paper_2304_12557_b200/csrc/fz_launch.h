@@ -7,18 +7,37 @@
 
 namespace fz {
 
-void count_launch();
 int num_sms();
 
+// Kernel kinds for launch accounting and per-kernel CUDA-event timing (fz_profile_*).
+enum KernelId {
+    K_INIT = 0, K_RANGE, K_PARAMS, K_COMPRESS, K_FINALIZE, K_DINIT, K_VALIDATE, K_DECODE,
+    K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_COUNT
+};
+
+// Counts one launch of `id` and, when profiling is on, brackets it with CUDA events on the
+// launch stream.  Construct right before the <<<>>> launch; the destructor records the end.
+struct LaunchProf {
+    LaunchProf(KernelId id, cudaStream_t st);
+    ~LaunchProf();
+    KernelId id;
+    cudaStream_t st;
+    int slot;
+};
+
 // compression (fz_compress.cu)
-cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint32_t ntiles,
+cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint32_t ntiles,
                         const fz_params* p, cudaStream_t st);
 cudaError_t launch_range(const float* d, uint64_t n, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_params(Ctrl* ctrl, int mode, double eb, uint64_t n, cudaStream_t st);
 cudaError_t launch_compress(const CompressArgs& a, cudaStream_t st);
 cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint64_t n,
-                            uint64_t T, const uint2* dstage, const uint2* vstage, Ctrl* ctrl,
-                            cudaStream_t st);
+                            uint64_t T, Ctrl* ctrl, cudaStream_t st);
+cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st);
+cudaError_t launch_outlier_place(const uint2* ocnt, const uint2* obase, const uint2* opre,
+                                 uint32_t ntiles, const uint2* dstage, const uint2* vstage,
+                                 uint2* dout, uint2* vout, uint32_t* didx, int32_t* dval,
+                                 uint32_t* vidx, uint32_t* vbits, cudaStream_t st);
 
 // decompression (fz_decompress.cu)
 struct DecodeArgs {
@@ -28,6 +47,7 @@ struct DecodeArgs {
     uint64_t nnz_total;         // header nnz (bounds every payload read)
     uint64_t nd;
     Geom g;
+    FastDiv dnx;
     uint32_t tiles;
     float w;
     int32_t* q_out;             // integer codes (2-D/3-D), aliases the output field

@@ -82,6 +82,9 @@ def lib():
         "fz_debug_quantize": ([P, pS, pP, P, P, P, u64, C.POINTER(u64), P, P, u64, C.POINTER(u64), P, S, P], i),
         "fz_debug_decode_q": ([P, S, P, u64, P, S, P], i),
         "fz_last_launch_count": ([], i),
+        "fz_profile_enable": ([i], None),
+        "fz_profile_read": ([C.POINTER(C.c_double), C.POINTER(C.c_int), i], i),
+        "fz_kernel_name": ([i], C.c_char_p),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -136,6 +139,18 @@ def derive_params(mn: float, mx: float, mode: int, eb: float) -> Params:
 
 def last_launch_count() -> int:
     return lib().fz_last_launch_count()
+
+
+def profile_enable(on: bool = True):
+    lib().fz_profile_enable(int(on))
+
+
+def profile_read() -> dict:
+    """{kernel name: (total ms, launches)} since the last read (CUDA events per launch)."""
+    ms = (C.c_double * 32)()
+    cnt = (C.c_int * 32)()
+    k = lib().fz_profile_read(ms, cnt, 32)
+    return {lib().fz_kernel_name(i).decode(): (ms[i], cnt[i]) for i in range(k) if cnt[i]}
 
 
 def _u8(n, device):
