@@ -141,6 +141,15 @@ CompressArgs make_args(const Work& W, const float* field, uint64_t base, const G
     return a;
 }
 
+fz_status err_status(int32_t e)
+{
+    if (e == kErrStall) {
+        snprintf(g_cuda_err, sizeof g_cuda_err, "look-back watchdog fired (device-side stall)");
+        return FZ_ERR_CUDA;
+    }
+    return (fz_status)e;
+}
+
 fz_status read_ctrl(const Work& W, Ctrl* h, cudaStream_t st)
 {
     FZ_CUDA(cudaMemcpyAsync(h, W.ctrl(), sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
@@ -164,7 +173,8 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
                        cudaStream_t st)
 {
     const uint32_t tb = a.tile_begin, nt = a.tile_end - a.tile_begin;
-    FZ_CUDA(launch_init(W.ctrl(), W.status() + tb, W.ocnt() + tb, nt, hp, st));
+    // status words are per scan unit, indexed from the range start; outlier counts per tile
+    FZ_CUDA(launch_init(W.ctrl(), W.status(), W.ocnt() + tb, nt, hp, st));
     if (hp == nullptr) {
         FZ_CUDA(launch_range(a.field, n, W.ctrl(), st));
         FZ_CUDA(launch_params(W.ctrl(), mode, eb, n, st));
@@ -251,7 +261,7 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     Ctrl h;
     fz_status rs = compress_run(W, a, hp, mode, eb, out, out_cap, *s, n, &h, st);
     if (rs != FZ_OK) return rs;
-    if (h.err != 0) return (fz_status)h.err;
+    if (h.err != 0) return err_status(h.err);
     *out_size = (size_t)h.total;
     if (h.total > out_cap) return FZ_ERR_CAPACITY;
     OutDest d;
@@ -424,7 +434,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     Ctrl h;
     FZ_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     FZ_CUDA(cudaStreamSynchronize(st));
-    if (h.err != 0) return (fz_status)h.err;
+    if (h.err != 0) return err_status(h.err);
     if (h.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;   // sum of popcount(flags) == nnz
     return FZ_OK;
 }
@@ -607,7 +617,7 @@ fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t sl
     Ctrl h;
     fz_status rs = compress_run(W, a, p, (int)p->mode, p->eb_input, nullptr, 0, *global, n, &h, st);
     if (rs != FZ_OK) return rs;
-    if (h.err != 0) return (fz_status)h.err;
+    if (h.err != 0) return err_status(h.err);
     h_counts->nnz = h.nnz;
     h_counts->n_delta = h.nd;
     h_counts->n_value = h.nv;
@@ -674,7 +684,7 @@ fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_pa
     Ctrl h;
     fz_status rs = compress_run(W, a, p, (int)p->mode, p->eb_input, nullptr, 0, *s, n, &h, st);
     if (rs != FZ_OK) return rs;
-    if (h.err != 0) return (fz_status)h.err;
+    if (h.err != 0) return err_status(h.err);
     *h_nd = h.nd;
     *h_nv = h.nv;
     if (h.nd > dcap || h.nv > vcap) return FZ_ERR_CAPACITY;

@@ -26,7 +26,7 @@ __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint
 {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     for (uint32_t k = i; k < ntiles; k += gridDim.x * blockDim.x) {
-        status[k] = 0ull;
+        status[k] = 0ull;   // per-unit look-back words (at most one per tile)
         ocnt[k] = make_uint2(0, 0);
     }
     if (i == 0) {
@@ -116,6 +116,21 @@ __device__ __forceinline__ void loadk(const CompressArgs& a, int64_t g0, float (
     }
 }
 
+// cp.async.bulk.prefetch.L2 of the field elements [g, g + cnt) (16-byte aligned, clamped).
+__device__ __forceinline__ void prefetch_l2_range(const CompressArgs& a, uint64_t g, uint64_t cnt)
+{
+    if (g < a.base) return;
+    uint64_t e = g + cnt;
+    if (e > a.g.n) e = a.g.n;
+    uint64_t lo = (g - a.base) & ~uint64_t(3), hi = (e - a.base) & ~uint64_t(3);
+    while (lo < hi) {
+        const uint64_t chunk = (hi - lo) > 16384 ? 16384 : (hi - lo);   // elements
+        const float* p = a.field + lo;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((uint32_t)(chunk * 4)) : "memory");
+        lo += chunk;
+    }
+}
+
 // q of one halo element (no bound check needed: only own elements can be value outliers).
 template <bool FB>
 __device__ __forceinline__ int quant_q(float d, const QuantP& P)
@@ -150,22 +165,24 @@ __device__ __forceinline__ void fill_range(const CompressArgs& a, const QuantP& 
 }
 
 // ------------------------------------------------------------------------------------
-// The fused compression kernel.  One CTA of 256 threads works on one 2048-code tile per
-// iteration; thread t owns tile elements 8t..8t+7 (= words 4t..4t+3 = A[t/8][4(t%8)..+3]).
-// The scan over tiles is a decoupled look-back delayed by one iteration: the aggregate of
-// tile i is published as soon as its flags are known, its look-back and payload stores
-// happen while the CTA already holds tile i+1, so predecessors have had a full tile time
-// to publish their inclusive prefixes.
+// The fused compression kernel.  One CTA of 256 threads; thread t owns the elements
+// 8t..8t+7 of the current tile (= words 4t..4t+3 = A[t/8][4(t%8)..+3]).
+// Scan granularity: a "unit" of kUnitTiles consecutive tiles.  The CTA compacts each tile's
+// nonzero blocks into a shared stage (double-buffered per unit), publishes the unit's block
+// count once its last tile is done, and resolves the unit's global offset by a wide
+// decoupled look-back one tile later (while computing the next unit's first tile), then
+// copies the stage to the payload with coalesced 16-byte stores.
 // ------------------------------------------------------------------------------------
+constexpr int kUnitTiles = 4;
+
 template <int NDIM, bool FB>
 __device__ __forceinline__ void compress_body(const CompressArgs& a)
 {
     extern __shared__ int smem[];
-    __shared__ uint32_t s_tile[2];
-    __shared__ uint32_t s_F[2][8];
+    __shared__ uint32_t s_unit[2];
+    __shared__ uint32_t s_F[8];
     __shared__ uint32_t s_cd[8], s_cv[8];
-    __shared__ uint32_t s_tnnz[2];
-    __shared__ unsigned long long s_ex;
+    __shared__ unsigned long long s_off;
     __shared__ unsigned long long s_ob[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -175,39 +192,64 @@ __device__ __forceinline__ void compress_body(const CompressArgs& a)
     P.w = ctrl->p.w; P.r = ctrl->p.r; P.h = ctrl->h; P.eb32 = ctrl->p.eb32;
     const uint32_t n = a.g.n, nx = a.g.nx, PL = a.g.P;
     const int qs = (int)a.qstride;
-    uint32_t* Obuf;
     // neighbour streams: array base (words) and m offset of own element j = 0
     int ab[4], mo[4];
+    int narr;
     if (NDIM == 1) {
-        ab[0] = 0; mo[0] = 1;
-        Obuf = reinterpret_cast<uint32_t*>(smem + qs);
+        ab[0] = 0; mo[0] = 1; narr = 1;
     } else if (a.union_mode) {
         const int HA = (int)nx + 1;
         ab[0] = 0; mo[0] = HA; ab[1] = 0; mo[1] = 1;
         ab[2] = qs; mo[2] = HA; ab[3] = qs; mo[3] = 1;
-        Obuf = reinterpret_cast<uint32_t*>(smem + (NDIM == 3 ? 2 : 1) * qs);
+        narr = NDIM == 3 ? 2 : 1;
     } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k) { ab[k] = k * qs; mo[k] = 1; }
-        Obuf = reinterpret_cast<uint32_t*>(smem + (NDIM == 3 ? 4 : 2) * qs);
+        narr = NDIM == 3 ? 4 : 2;
     }
-    constexpr int NS = NDIM == 1 ? 1 : (NDIM == 2 ? 2 : 4);
+    uint32_t* Obuf = reinterpret_cast<uint32_t*>(smem + narr * qs);              // 32 x 33
+    uint4* stage = reinterpret_cast<uint4*>(smem + narr * qs + 32 * 33 + 3);     // 2 x units
+    stage = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(stage) + 15) & ~uintptr_t(15));
+    constexpr int kStageBlocks = kUnitTiles * kTileBlocks;
 
-    if (tid == 0) s_tile[0] = a.tile_begin + atomicAdd(&ctrl->ticket, 1u);
+    const uint32_t nunits = (a.tile_end - a.tile_begin + kUnitTiles - 1) / kUnitTiles;
+    constexpr uint32_t NONE = 0xFFFFFFFFu;
+    if (tid == 0) s_unit[0] = atomicAdd(&ctrl->ticket, 1u);
     __syncthreads();
-    uint32_t tp = 0xFFFFFFFFu;      // pending tile (payload not yet stored)
-    uint4 pblk = make_uint4(0, 0, 0, 0);
-    bool pnz = false;
+    uint32_t pu = NONE;       // pending unit: aggregate published, offset unknown
+    uint32_t pcnt = 0;        // its block count
+    int buf = 0;              // stage buffer of the current unit
     for (int it = 0;; ++it) {
-        const int cur = it & 1;
-        const uint32_t t = s_tile[cur];
-        const bool work = t < a.tile_end;
-        if (!work && tp == 0xFFFFFFFFu) break;
-        uint4 blk = make_uint4(0, 0, 0, 0);
-        bool nz = false;
-        if (work) {
+        const uint32_t u = s_unit[it & 1];
+        const bool work = u < nunits;
+        if (!work && pu == NONE) break;
+        if (!work) {
+            // ---- flush the last pending unit ----
+            if (warp == 0) {
+                unsigned long long ex = 0;
+                if (pu != 0) {
+                    ex = lookback_wide<8, false>(a.status, pu, 0, kStAgg - 1, &ctrl->err);
+                    if (lane == 0) st_relaxed_u64(&a.status[pu], kStInc | (ex + pcnt));
+                }
+                if (lane == 0) s_off = ex;
+            }
+            __syncthreads();
+            const uint4* ps = stage + (buf ^ 1) * kStageBlocks;
+            for (uint32_t i = tid; i < pcnt; i += kCta) {
+                const uint64_t bo = 16 * (s_off + i);
+                if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = ps[i];
+            }
+            if (tid == 0 && pu == nunits - 1) ctrl->nnz = s_off + pcnt;
+            break;
+        }
+        const uint32_t t_first = a.tile_begin + u * kUnitTiles;
+        const uint32_t t_last = min(a.tile_end, t_first + kUnitTiles);
+        uint32_t cnt = 0;                         // blocks staged for this unit (uniform)
+        uint4* st = stage + buf * kStageBlocks;
+        for (uint32_t t = t_first; t < t_last; ++t) {
             const int64_t s = (int64_t)t * kTileCodes;
             const uint32_t g0 = (uint32_t)s + 8u * tid;
+            const bool full = s + kTileCodes <= (int64_t)n;
 
             // ---- A: prequantize own elements (+ bound check) and the halo ranges ----
             float dv[8];
@@ -226,91 +268,138 @@ __device__ __forceinline__ void compress_body(const CompressArgs& a)
                 if (NDIM == 3) fill_range<FB>(a, P, smem + qs, s - (int64_t)PL - nx - 1, kTileCodes + (int)nx + 1);
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int e = 0; e < 8; ++e) {
                 bool vo;
                 if (FB) {
-                    qo[u] = prequant(dv[u], P, vo);
+                    qo[e] = prequant(dv[e], P, vo);
                 } else {
                     bool hard;
                     float qf;
-                    qo[u] = prequant_fast(dv[u], P, hard, qf);
+                    qo[e] = prequant_fast(dv[e], P, hard, qf);
                     if (hard) {
-                        qo[u] = prequant(dv[u], P, vo);
+                        qo[e] = prequant(dv[e], P, vo);
                     } else {
-                        const float diff = __fsub_rn(__fmul_rn(qf, P.w), dv[u]);
-                        vo = fabsf(diff) > P.eb32;
+                        vo = fabsf(__fsub_rn(__fmul_rn(qf, P.w), dv[e])) > P.eb32;
                     }
                 }
-                if (vo && g0 + u < n) vmask |= 1u << u;
-                smem[ab[0] + pad(mo[0] + 8 * tid + u)] = qo[u];
+                if (vo) vmask |= 1u << e;
+                smem[ab[0] + pad(mo[0] + 8 * tid + e)] = qo[e];
             }
+            if (!full) vmask &= (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
             __syncthreads();
-            if (tid == 0) s_tile[cur ^ 1] = a.tile_begin + atomicAdd(&ctrl->ticket, 1u);
+            if (t == t_first && tid == 0) {
+                const uint32_t nu = atomicAdd(&ctrl->ticket, 1u);
+                s_unit[(it & 1) ^ 1] = nu;
+                // TMA L2 prefetch of the next unit's input (~kUnitTiles tiles ahead): keeps
+                // HBM busy independently of how many loads the registers can hold
+                if (nu < nunits) prefetch_l2_range(a, (uint64_t)(a.tile_begin + nu * kUnitTiles) * kTileCodes,
+                                                   (uint64_t)kUnitTiles * kTileCodes);
+            }
 
-            // ---- B: Lorenzo residual (C2), codes (C3), words (C4) ----
-            int qn[NS][9];
-            qn[0][0] = smem[ab[0] + pad(mo[0] + 8 * tid - 1)];
+            // ---- B: Lorenzo residual (C2) as delta(e) = S(e+1) - [x>0] S(e), where S(j)
+            // combines the element at j-1 with its y-1, z-1, (y-1,z-1) neighbours ----
+            int S[9];
+            bool fast_yz = true;
+            uint32_t xmask = 0xFFu;
+            if (NDIM == 1) {
+                S[0] = smem[ab[0] + pad(mo[0] + 8 * tid - 1)];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) qn[0][u + 1] = qo[u];
+                for (int j = 1; j < 9; ++j) S[j] = qo[j - 1];
+                if (nx >= 8) {
+                    const uint32_t x0 = fmod_(g0, a.dnx);
+                    const uint32_t us = x0 == 0 ? 0u : nx - x0;
+                    if (us < 8) xmask &= ~(1u << us);
+                } else {
 #pragma unroll
-            for (int k = 1; k < NS; ++k)
-#pragma unroll
-                for (int u = 0; u < 9; ++u) qn[k][u] = smem[ab[k] + pad(mo[k] + 8 * tid - 1 + u)];
-            uint32_t mxb = 0, myb = 0, mzb = 0;   // per-element "neighbour exists" bits
-            if (nx >= 8) {
-                uint32_t x = fmod_(g0, a.dnx), pp = fmod_(g0, a.dP);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    mxb |= (uint32_t)(x != 0) << u;
-                    myb |= (uint32_t)(pp >= nx) << u;
-                    mzb |= (uint32_t)(g0 + u >= PL) << u;
-                    if (++x == nx) x = 0;
-                    if (++pp == PL) pp = 0;
+                    for (int e = 0; e < 8; ++e)
+                        if (fmod_(g0 + e, a.dnx) == 0) xmask &= ~(1u << e);
                 }
             } else {
+                int qy[9], qz[9], qyz[9];
+                const int o0 = ab[0] + pad(mo[0] + 8 * tid - 1);
+                const int own0 = smem[o0];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const uint32_t g = g0 + u;
-                    mxb |= (uint32_t)(fmod_(g, a.dnx) != 0) << u;
-                    myb |= (uint32_t)(fmod_(g, a.dP) >= nx) << u;
-                    mzb |= (uint32_t)(g >= PL) << u;
+                for (int j = 0; j < 9; ++j) qy[j] = smem[ab[1] + pad(mo[1] + 8 * tid - 1 + j)];
+                if (NDIM == 3) {
+#pragma unroll
+                    for (int j = 0; j < 9; ++j) {
+                        qz[j] = smem[ab[2] + pad(mo[2] + 8 * tid - 1 + j)];
+                        qyz[j] = smem[ab[3] + pad(mo[3] + 8 * tid - 1 + j)];
+                    }
+                }
+                uint32_t ymask = 0xFFu, zmask = 0xFFu;   // bit e: neighbour exists for element e
+                if (nx >= 8) {
+                    const uint32_t x0 = fmod_(g0, a.dnx);
+                    const uint32_t us = x0 == 0 ? 0u : nx - x0;
+                    if (us < 8) xmask &= ~(1u << us);
+                    const uint32_t p0 = fmod_(g0, a.dP);
+                    fast_yz = p0 >= nx && p0 + 7 < PL && (NDIM == 2 || g0 >= PL);
+                    if (!fast_yz) {
+                        uint32_t pp = p0;
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            if (pp < nx) ymask &= ~(1u << e);
+                            if (g0 + e < PL) zmask &= ~(1u << e);
+                            if (++pp == PL) pp = 0;
+                        }
+                    }
+                } else {
+                    fast_yz = false;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        if (fmod_(g0 + e, a.dnx) == 0) xmask &= ~(1u << e);
+                        if (fmod_(g0 + e, a.dP) < nx) ymask &= ~(1u << e);
+                        if (g0 + e < PL) zmask &= ~(1u << e);
+                    }
+                }
+                if (NDIM == 2) zmask = 0;
+                if (fast_yz) {
+                    S[0] = (int)((uint32_t)own0 - (uint32_t)qy[0] - (NDIM == 3 ? (uint32_t)qz[0] - (uint32_t)qyz[0] : 0u));
+#pragma unroll
+                    for (int j = 1; j < 9; ++j)
+                        S[j] = (int)((uint32_t)qo[j - 1] - (uint32_t)qy[j] -
+                                     (NDIM == 3 ? (uint32_t)qz[j] - (uint32_t)qyz[j] : 0u));
+                } else {
+                    // masks of element j-1 for S(j); of element 0 for S(0)
+#pragma unroll
+                    for (int j = 0; j < 9; ++j) {
+                        const int e = j == 0 ? 0 : j - 1;
+                        const uint32_t Y = (ymask >> e) & 1u ? 0xFFFFFFFFu : 0u;
+                        const uint32_t Z = (zmask >> e) & 1u ? 0xFFFFFFFFu : 0u;
+                        const uint32_t ow = j == 0 ? (uint32_t)own0 : (uint32_t)qo[j - 1];
+                        uint32_t v = ow - ((uint32_t)qy[j] & Y);
+                        if (NDIM == 3) v -= ((uint32_t)qz[j] - ((uint32_t)qyz[j] & Y)) & Z;
+                        S[j] = (int)v;
+                    }
                 }
             }
+            // ---- C3 codes, C4 words ----
             uint32_t code[8];
             int32_t dl[8];
             uint32_t dmask = 0;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t X = (mxb >> u) & 1u ? 0xFFFFFFFFu : 0u;
-                uint32_t dd = (uint32_t)qn[0][u + 1] - ((uint32_t)qn[0][u] & X);
-                if (NDIM >= 2) {
-                    const uint32_t Y = (myb >> u) & 1u ? 0xFFFFFFFFu : 0u;
-                    const uint32_t r1 = (uint32_t)qn[1][u + 1] - ((uint32_t)qn[1][u] & X);
-                    if (NDIM == 3) {
-                        const uint32_t Z = (mzb >> u) & 1u ? 0xFFFFFFFFu : 0u;
-                        const uint32_t r2 = (uint32_t)qn[2][u + 1] - ((uint32_t)qn[2][u] & X);
-                        const uint32_t r3 = (uint32_t)qn[3][u + 1] - ((uint32_t)qn[3][u] & X);
-                        dd -= r1 & Y;
-                        dd -= (r2 - (r3 & Y)) & Z;
-                    } else {
-                        dd -= r1 & Y;
-                    }
-                }
-                const bool valid = g0 + u < n;
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t X = (xmask >> e) & 1u ? 0xFFFFFFFFu : 0u;
+                const uint32_t dd = (uint32_t)S[e + 1] - ((uint32_t)S[e] & X);
                 const int32_t di = (int32_t)dd;
-                const uint32_t mag = di < 0 ? 0u - dd : dd;
-                const bool outl = valid && mag > 32767u;
-                code[u] = (valid && !outl) ? (((dd >> 16) & 0x8000u) | mag) : 0u;
-                dl[u] = di;
-                if (outl) dmask |= 1u << u;
+                const uint32_t mag = (uint32_t)abs(di);
+                const bool outl = mag > 32767u;
+                code[e] = outl ? 0u : (((dd >> 16) & 0x8000u) | mag);
+                dl[e] = di;
+                if (outl) dmask |= 1u << e;
+            }
+            if (!full) {
+                const uint32_t vm = (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
+                dmask &= vm;
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (!((vm >> e) & 1u)) code[e] = 0u;
             }
             if (a.codes_out != nullptr) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (g0 + u < n) a.codes_out[g0 + u] = (uint16_t)code[u];
+                for (int e = 0; e < 8; ++e)
+                    if (g0 + e < n) a.codes_out[g0 + e] = (uint16_t)code[e];
             }
-            const int cd = __popc(dmask), cv = __popc(vmask);
-            const int wd = __reduce_add_sync(kFull, cd), wv = __reduce_add_sync(kFull, cv);
             if (!a.rescan) {
                 // ---- C5 bitshuffle in registers: row c = tid/8 of A, lanes k = tid%8 ----
                 uint32_t w4[4];
@@ -321,26 +410,20 @@ __device__ __forceinline__ void compress_body(const CompressArgs& a)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) Obuf[(4 * kk + i) * 33 + c] = w4[i];
             }
-            if (lane == 0) { s_cd[warp] = wd; s_cv[warp] = wv; }
-            __syncthreads();
-
-            // ---- C6 block flags: thread b owns block b = 8r + x of the shuffled tile ----
-            if (!a.rescan) {
-                const uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
-                blk = make_uint4(row[0], row[1], row[2], row[3]);
-                nz = (blk.x | blk.y | blk.z | blk.w) != 0;
-                const uint32_t F = __ballot_sync(kFull, nz);
-                if (lane == 0) s_F[cur][warp] = F;
-            }
+            const int any_out = __syncthreads_or((dmask | vmask) != 0);
 
             // ---- outlier records (rare; R7, R20): ascending element index ----
-            uint32_t tnd = 0, tnv = 0, wpre_d = 0, wpre_v = 0;
+            if (any_out) {
+                const int cd = __popc(dmask), cv = __popc(vmask);
+                const int wd = __reduce_add_sync(kFull, cd), wv = __reduce_add_sync(kFull, cv);
+                if (lane == 0) { s_cd[warp] = wd; s_cv[warp] = wv; }
+                __syncthreads();
+                uint32_t tnd = 0, tnv = 0, wpre_d = 0, wpre_v = 0;
 #pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                tnd += s_cd[w]; tnv += s_cv[w];
-                if (w < warp) { wpre_d += s_cd[w]; wpre_v += s_cv[w]; }
-            }
-            if (tnd + tnv != 0) {
+                for (int w = 0; w < 8; ++w) {
+                    tnd += s_cd[w]; tnv += s_cv[w];
+                    if (w < warp) { wpre_d += s_cd[w]; wpre_v += s_cv[w]; }
+                }
                 if (tid == 0) {
                     if (a.rescan) {
                         const uint2 o = a.opre[t];
@@ -361,87 +444,90 @@ __device__ __forceinline__ void compress_body(const CompressArgs& a)
                 __syncthreads();
                 uint64_t pd = s_ob[0] + wpre_d + (id - cd), pv = s_ob[1] + wpre_v + (iv - cv);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const uint32_t gi = g0 + u;
-                    if (dmask & (1u << u)) {
+                for (int e = 0; e < 8; ++e) {
+                    const uint32_t gi = g0 + e;
+                    if (dmask & (1u << e)) {
                         if (pd < a.dcap) {
-                            if (a.o_didx) { a.o_didx[pd] = gi; a.o_dval[pd] = dl[u]; }
-                            else a.dstage[pd] = make_uint2(gi, (uint32_t)dl[u]);
+                            if (a.o_didx) { a.o_didx[pd] = gi; a.o_dval[pd] = dl[e]; }
+                            else a.dstage[pd] = make_uint2(gi, (uint32_t)dl[e]);
                         } else {
                             atomicOr(&ctrl->stage_overflow, 1u);
                         }
                         ++pd;
                     }
-                    if (vmask & (1u << u)) {
+                    if (vmask & (1u << e)) {
                         if (pv < a.vcap) {
-                            if (a.o_vidx) { a.o_vidx[pv] = gi; a.o_vbits[pv] = __float_as_uint(dv[u]); }
-                            else a.vstage[pv] = make_uint2(gi, __float_as_uint(dv[u]));
+                            if (a.o_vidx) { a.o_vidx[pv] = gi; a.o_vbits[pv] = __float_as_uint(dv[e]); }
+                            else a.vstage[pv] = make_uint2(gi, __float_as_uint(dv[e]));
                         } else {
                             atomicOr(&ctrl->stage_overflow, 1u);
                         }
                         ++pv;
                     }
                 }
+                __syncthreads();
+            }
+            if (a.rescan) continue;
+
+            // ---- C6 block flags: thread b owns block b = 8r + x of the shuffled tile ----
+            const uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+            const uint4 blk = make_uint4(row[0], row[1], row[2], row[3]);
+            const bool nz = (blk.x | blk.y | blk.z | blk.w) != 0;
+            const uint32_t F = __ballot_sync(kFull, nz);
+            if (lane == 0) s_F[warp] = F;
+            // the pending unit's look-back overlaps the other warps' flag work
+            if (t == t_first && pu != NONE && warp == 0) {
+                unsigned long long ex = 0;
+                if (pu != 0) {
+                    ex = lookback_wide<8, false>(a.status, pu, 0, kStAgg - 1, &ctrl->err);
+                    if (lane == 0) st_relaxed_u64(&a.status[pu], kStInc | (ex + pcnt));
+                }
+                if (lane == 0) s_off = ex;
+            }
+            __syncthreads();
+            uint32_t tn = 0, wpre = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const uint32_t pc = __popc(s_F[w]);
+                tn += pc;
+                if (w < warp) wpre += pc;
+            }
+            if (tid < 8) {
+                const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * tid;
+                if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = s_F[tid];
+            }
+            // ---- C8 (local): compact the tile's nonzero blocks into the unit stage ----
+            if (nz) st[cnt + wpre + __popc(F & ((1u << lane) - 1u))] = blk;
+            cnt += tn;
+            if (t == t_first && pu != NONE) {
+                // ---- C8 (global): the pending unit's stage goes to its final offset ----
+                const uint4* ps = stage + (buf ^ 1) * kStageBlocks;
+                const unsigned long long off = s_off;
+                for (uint32_t i = tid; i < pcnt; i += kCta) {
+                    const uint64_t bo = 16 * (off + i);
+                    if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = ps[i];
+                }
+                if (tid == 0 && pu == nunits - 1) ctrl->nnz = off + pcnt;
+                pu = NONE;
             }
         }
         if (a.rescan) {
             __syncthreads();
-            if (!work) break;
             continue;
         }
+        // ---- C7: publish the unit's aggregate (inclusive for unit 0) ----
+        if (tid == 0) st_relaxed_u64(&a.status[u], (u == 0 ? kStInc : kStAgg) | cnt);
+        pu = u;
+        pcnt = cnt;
+        buf ^= 1;
         __syncthreads();
-
-        // ---- C7: publish the aggregate of t, look back for the pending tile tp ----
-        if (warp == 0) {
-            if (work) {
-                uint32_t tn = 0;
-#pragma unroll
-                for (int w = 0; w < 8; ++w) tn += __popc(s_F[cur][w]);
-                if (lane == 0) {
-                    s_tnnz[cur] = tn;
-                    st_relaxed_u64(&a.status[t], (t == a.tile_begin ? kStInc : kStAgg) | tn);
-                }
-                if (lane < 8) {
-                    const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * lane;
-                    if (fo + 4 <= a.flags_cap)
-                        *reinterpret_cast<uint32_t*>(a.flags_out + fo) = s_F[cur][lane];
-                }
-            }
-            if (tp != 0xFFFFFFFFu) {
-                unsigned long long ex = 0;
-                if (tp != a.tile_begin) {
-                    ex = lookback_wide<8, false>(a.status, tp, a.tile_begin, kStInc - 1);
-                    if (lane == 0) st_relaxed_u64(&a.status[tp], kStInc | (ex + s_tnnz[cur ^ 1]));
-                }
-                if (lane == 0) {
-                    s_ex = ex;
-                    if (tp == a.tile_end - 1) ctrl->nnz = ex + s_tnnz[cur ^ 1];
-                }
-            }
-        }
-        __syncthreads();
-
-        // ---- C8: compaction of the pending tile's nonzero blocks (tile, block order) ----
-        if (tp != 0xFFFFFFFFu && pnz) {
-            const uint32_t Fp = s_F[cur ^ 1][warp];
-            uint32_t wpre = 0;
-#pragma unroll
-            for (int w = 0; w < 8; ++w)
-                if (w < warp) wpre += __popc(s_F[cur ^ 1][w]);
-            const uint64_t bo = 16 * (s_ex + wpre + __popc(Fp & ((1u << lane) - 1u)));
-            if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = pblk;
-        }
-        tp = work ? t : 0xFFFFFFFFu;
-        pblk = blk;
-        pnz = nz;
-        if (!work) break;
     }
 }
 
 // The margin/fallback mode (R2) is known only on the device when fz_compress derives the
 // parameters there, so the kernel dispatches on it (block-uniform branch).
 template <int NDIM>
-__global__ void __launch_bounds__(kCta) k_compress(CompressArgs a)
+__global__ void __launch_bounds__(kCta, 2) k_compress(CompressArgs a)
 {
     if (a.ctrl->p.fallback) compress_body<NDIM, true>(a);
     else compress_body<NDIM, false>(a);
@@ -570,7 +656,7 @@ static size_t plan_smem(CompressArgs& a)
         len = kTileCodes + 1;
     }
     a.qstride = (pad_words(len) + 31) & ~31u;
-    return sizeof(int) * ((size_t)narr * a.qstride + 32 * 33);
+    return sizeof(int) * ((size_t)narr * a.qstride + 32 * 33 + 8) + 2 * 16 * (size_t)kUnitTiles * kTileBlocks;
 }
 
 template <int NDIM>
@@ -581,7 +667,8 @@ static cudaError_t launch_compress_t(const CompressArgs& a, size_t sm, uint32_t 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compress<NDIM>, kCta, sm);
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)per_sm * num_sms();
-    if (grid > ntiles) grid = ntiles;
+    const uint32_t nunits = (ntiles + kUnitTiles - 1) / kUnitTiles;
+    if (grid > nunits) grid = nunits;
     if (grid == 0) return cudaSuccess;
     k_compress<NDIM><<<(unsigned)grid, kCta, sm, st>>>(a);
     return cudaGetLastError();

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
         // ---- stage 1: flags of tile t ----
         if (work && lane == 0) s_F[cur][warp] = reinterpret_cast<const uint32_t*>(a.flags)[8 * (uint64_t)t + warp];
         __syncthreads();
-        if (tid == 0 && work) s_tile[cur ^ 1] = atomicAdd(&ctrl->ticket, 1u);
+        if (tid == 0) s_tile[cur ^ 1] = work ? atomicAdd(&ctrl->ticket, 1u) : NONE;
         if (warp == 0) {
             if (work) {
                 uint32_t tn = 0;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
             if (t1 != NONE) {
                 unsigned long long ex = 0;
                 if (t1 != 0) {
-                    ex = lookback_wide<8, false>(a.st_nnz, t1, 0, kStInc - 1);
+                    ex = lookback_wide<8, false>(a.st_nnz, t1, 0, kStAgg - 1, &ctrl->err);
                     if (lane == 0) st_relaxed_u64(&a.st_nnz[t1], kStInc | (ex + s_tnnz[cur ^ 1]));
                 }
                 if (lane == 0) {
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
         if (warp == 0 && t2 != NONE) {
             uint32_t carry = 0;
             if (t2 != 0) {
-                carry = (uint32_t)lookback_wide<8, false>(a.st_x, t2, 0, 0xFFFFFFFFull);
+                carry = (uint32_t)lookback_wide<8, false>(a.st_x, t2, 0, 0xFFFFFFFFull, &ctrl->err);
                 if (lane == 0 && !s_tagf[cur ^ 1])
                     st_relaxed_u64(&a.st_x[t2], kStInc | (uint32_t)(carry + s_tagv[cur ^ 1]));
             }

@@ -159,17 +159,27 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
 constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62;
 constexpr unsigned long long kStTerm = 1ull << 61;
 
+// Watchdog: a look-back that spins for ~seconds raises kErrStall in *err and returns, so a
+// logic error can never hang the device (the caller reports FZ_ERR_CUDA).
+constexpr int32_t kErrStall = 100;
+
 template <int PER_LANE, bool SEG>
 __device__ __forceinline__ unsigned long long lookback_wide(const unsigned long long* st, int64_t t,
-                                                            int64_t first, unsigned long long vmask)
+                                                            int64_t first, unsigned long long vmask,
+                                                            int32_t* err)
 {
     const int lane = threadIdx.x & 31;
     unsigned long long sum = 0;
     int64_t hi = t - 1;
+    uint32_t spins = 0;
     while (hi >= first) {
         unsigned long long v[PER_LANE];
         uint32_t termbits, zerobits;
         for (;;) {
+            if (++spins > (1u << 22)) {
+                if (lane == 0) atomicExch(err, kErrStall);
+                return sum;
+            }
             termbits = 0;
             zerobits = 0;
 #pragma unroll
