@@ -9,6 +9,8 @@
 //   k_outlier_scan / k_outlier_place: outlier sections (only launched when outliers exist)
 //
 // Citation key: P:n = PAPER.md line n; R# = DESIGN.md §3 readings; SV = SURVEY.md.
+#include <cstdlib>
+
 #include "fz_internal.cuh"
 #include "fz_launch.h"
 
@@ -19,6 +21,28 @@ namespace fz {
 __device__ __forceinline__ int pad(int m) { return m + (m >> 3); }
 inline uint32_t pad_words(uint32_t len) { return len + (len >> 3) + 8; }
 constexpr uint32_t kUnionHaloMax = 4097;   // union arrays when the row halo nx+1 fits
+
+// h = w/2; hU = RD32(w/2 - U) with U = 2^(e-23), M = max|d| = m 2^e (Appendix A): the
+// fast-path threshold of pq_fast.  Fallback mode: hU = -1 (every element takes the exact
+// rule and the bound check).
+__device__ void set_quant_consts(Ctrl* ctrl)
+{
+    const fz_params& p = ctrl->p;
+    ctrl->h = 0.5f * p.w;
+    if (p.fallback) {
+        ctrl->hU = -1.0f;
+        return;
+    }
+    const float M = fmaxf(fabsf(p.mn), fabsf(p.mx));
+    double U = 0.0;
+    if (M > 0.0f) {
+        int e;
+        frexp((double)M, &e);
+        U = ldexp(1.0, e - 23);
+    }
+    const double t = (double)ctrl->h - U;
+    ctrl->hU = t > 0.0 ? rd32(t) : -1.0f;
+}
 
 // ------------------------------------------------------------------------------------
 __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint32_t ntiles,
@@ -38,9 +62,10 @@ __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint
         ctrl->stage_overflow = 0;
         ctrl->nnz = ctrl->nd = ctrl->nv = ctrl->total = 0;
         ctrl->dcount = ctrl->vcount = 0;
+        ctrl->dbg[0] = ctrl->dbg[1] = ctrl->dbg[2] = ctrl->dbg[3] = 0;
         if (set_params) {
             ctrl->p = p;
-            ctrl->h = 0.5f * p.w;
+            set_quant_consts(ctrl);
         }
     }
 }
@@ -88,7 +113,7 @@ __global__ void k_params(Ctrl* ctrl, int mode, double eb, uint64_t n)
     int st = derive_params(mn, mx, mode, eb, &p);
     if (st != FZ_OK) { ctrl->err = st; return; }
     ctrl->p = p;
-    ctrl->h = 0.5f * p.w;
+    set_quant_consts(ctrl);
 }
 
 // ------------------------------------------------------------------------------------
@@ -131,406 +156,1128 @@ __device__ __forceinline__ void prefetch_l2_range(const CompressArgs& a, uint64_
     }
 }
 
-// q of one halo element (no bound check needed: only own elements can be value outliers).
-template <bool FB>
-__device__ __forceinline__ int quant_q(float d, const QuantP& P)
-{
-    if (FB) return prequant_q(d, P);
-    bool hard;
-    float qf;
-    int q = prequant_fast(d, P, hard, qf);
-    if (hard) q = prequant_q(d, P);
-    return q;
-}
-
-// Cooperative fill of arr[pad(g - g_lo)] = q(g) for g in [g_lo, g_lo + len), in 4-element
-// aligned chunks (16-byte loads).  Elements outside the field get q = 0 (masked later).
-template <bool FB>
-__device__ __forceinline__ void fill_range(const CompressArgs& a, const QuantP& P, int* arr,
-                                           int64_t g_lo, int len)
-{
-    if (len <= 0) return;
-    const int64_t a0 = g_lo & ~(int64_t)3;
-    const int nch = (int)((g_lo + len - a0 + 3) >> 2);
-    for (int c = threadIdx.x; c < nch; c += kCta) {
-        const int64_t gc = a0 + 4 * c;
-        float v[4];
-        loadk<4>(a, gc, v);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int64_t m = gc + u - g_lo;
-            if (m >= 0 && m < len) arr[pad((int)m)] = quant_q<FB>(v[u], P);
-        }
-    }
-}
-
 // ------------------------------------------------------------------------------------
-// The fused compression kernel.  One CTA of 256 threads; thread t owns the elements
+// The fused compression kernels.  One CTA of 256 threads; thread t owns the elements
 // 8t..8t+7 of the current tile (= words 4t..4t+3 = A[t/8][4(t%8)..+3]).
 // Scan granularity: a "unit" of kUnitTiles consecutive tiles.  The CTA compacts each tile's
 // nonzero blocks into a shared stage (double-buffered per unit), publishes the unit's block
 // count once its last tile is done, and resolves the unit's global offset by a wide
 // decoupled look-back one tile later (while computing the next unit's first tile), then
 // copies the stage to the payload with coalesced 16-byte stores.
+//
+// Two front ends produce the Lorenzo residuals of a tile:
+//   front_vec  (nx % 4 == 0, row halo <= 6140): quantized values live in power-of-two rings
+//              in shared memory; per tile the CTA quantizes its 2048 own elements and the
+//              2048 new elements of the previous plane (= the z neighbours, kept in
+//              registers); the row and plane halos come from the unit's earlier tiles
+//              (filled at a unit's first tile).  128-bit LDS/STS, x-1 neighbour by SHFL.
+//   front_gen  (any shape): both halo ranges are re-quantized for every tile into padded
+//              linear arrays (element m at m + m/8).
+// Both feed the same tail (codes, bitshuffle, flags, outliers, staging, look-back).
 // ------------------------------------------------------------------------------------
 constexpr int kUnitTiles = 4;
+constexpr int kFillBatch = 4;     // halo chunks (4 elements each) per thread per batch
+constexpr int kStageBlocks = kUnitTiles * kTileBlocks;
 
-template <int NDIM, bool FB>
-__device__ __forceinline__ void compress_body(const CompressArgs& a)
+// Fast-path prequantization (C1, R2/R3): magic-rounded q0 = rint(fl(d*r)) and the exact
+// residual e = d - q0*w.  When |e| < hU (= w/2 - U, rounded down) q0 is the exact nearest
+// bin (no tie) and |fl32(q0*w) - d| <= |e| + U/2 < w/2 <= eb: no correction and no bound
+// check are needed.  Otherwise (rare; always in fallback mode, hU = -1) `hard` is set and
+// the caller applies the exact rule + bound check.
+__device__ __forceinline__ int pq_fast(float d, const QuantP& P, bool& hard)
 {
-    extern __shared__ int smem[];
-    __shared__ uint32_t s_unit[2];
-    __shared__ uint32_t s_F[8];
-    __shared__ uint32_t s_cd[8], s_cv[8];
-    __shared__ unsigned long long s_off;
-    __shared__ unsigned long long s_ob[2];
+    const float kMagic = 12582912.0f;
+    const float t = __fadd_rn(__fmul_rn(d, P.r), kMagic);
+    const float qf = __fsub_rn(t, kMagic);
+    const float e = __fmaf_rn(-qf, P.w, d);
+    hard = !(fabsf(e) < P.hU);
+    return __float_as_int(t) - 0x4B400000;
+}
 
+// Quantizes K values (q only, halo elements) with the fast path and a warp-uniform slow path.
+template <int K>
+__device__ __forceinline__ void pq_many(const float (&v)[K], int (&q)[K], const QuantP& P)
+{
+    uint32_t hard = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        bool h;
+        q[i] = pq_fast(v[i], P, h);
+        hard |= (uint32_t)h << i;
+    }
+    if (__any_sync(kFull, hard != 0)) {
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if ((hard >> i) & 1u) q[i] = prequant_q(v[i], P);
+    }
+}
+
+// Own elements: q plus the exact rule + bound check where the fast path does not apply.
+__device__ __forceinline__ void pq_own(const float (&v)[8], int (&q)[8], uint32_t& vmask, const QuantP& P)
+{
+    uint32_t hard = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        bool h;
+        q[i] = pq_fast(v[i], P, h);
+        hard |= (uint32_t)h << i;
+    }
+    vmask = 0;
+    if (__any_sync(kFull, hard != 0)) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if ((hard >> i) & 1u) {
+                bool vo;
+                q[i] = prequant(v[i], P, vo);
+                if (vo) vmask |= 1u << i;
+            }
+    }
+}
+
+// Block-uniform shared state of the compression kernels.
+struct CompShared {
+    uint32_t lbok;          // pending unit's offset resolved this tile
+    uint32_t unit[2];
+    uint32_t F[8];
+    uint32_t cd[8], cv[8];
+    unsigned long long off;
+    unsigned long long ob[2];
+};
+
+// Per-thread copy of the (block-uniform) unit bookkeeping.
+struct UnitState {
+    uint32_t pu;       // pending unit: aggregate published, offset unknown
+    uint32_t pcnt;     // its block count
+    uint32_t cnt;      // blocks staged for the current unit
+    int buf;           // stage buffer of the current unit
+    uint32_t nunits;
+    int it;
+};
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+__device__ __forceinline__ void flush_unit(const CompressArgs& a, CompShared& sh, const uint4* ps,
+                                           const UnitState& us, unsigned long long off)
+{
+    if (a.exp & 2) return;
+    for (uint32_t i = threadIdx.x; i < us.pcnt; i += kCta) {
+        const uint64_t bo = 16 * (off + i);
+        if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = ps[i];
+    }
+    if (threadIdx.x == 0 && us.pu == us.nunits - 1) a.ctrl->nnz = off + us.pcnt;
+}
+
+constexpr int kLbLane = 16;   // look-back window: 32 x 16 = 512 units per round
+
+__device__ __forceinline__ void lookback_unit(const CompressArgs& a, CompShared& sh, const UnitState& us,
+                                              const unsigned long long* pre = nullptr)
+{
+    const int lane = threadIdx.x & 31;
+    unsigned long long ex = 0;
+    if (us.pu != 0) {
+        ex = lookback_wide<kLbLane, false>(a.status, us.pu, 0, kStAgg - 1, &a.ctrl->err, pre);
+        if (lane == 0) st_relaxed_u64(&a.status[us.pu], kStInc | (ex + us.pcnt));
+    }
+    if (lane == 0) sh.off = ex;
+}
+
+// ------------------------------------------------------------------------------------
+// Tail of a tile: C3 codes, C5 bitshuffle, outlier records, C6 flags, C8 local compaction
+// into the unit stage; at the first tile of a unit, the pending unit's look-back (C7) and
+// its global compaction.  dl = Lorenzo residuals (already masked), vmask = value outliers.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void tile_tail(const CompressArgs& a, CompShared& sh, uint32_t* Obuf, uint4* stage,
+                                          UnitState& us, uint32_t t, bool first, bool lbt, uint32_t g0, uint32_t vm,
+                                          const int32_t (&dl)[8], uint32_t vmask, const float (&dv)[8],
+                                          const unsigned long long* pre)
+{
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Ctrl* ctrl = a.ctrl;
-    if (ctrl->err != 0) return;
-    QuantP P;
-    P.w = ctrl->p.w; P.r = ctrl->p.r; P.h = ctrl->h; P.eb32 = ctrl->p.eb32;
+    const uint32_t n = a.g.n;
+    // ---- C3 codes: sign-magnitude, |delta| > 32767 -> code 0 + delta outlier (R7) ----
+    uint32_t code[8];
+    uint32_t dmask = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const uint32_t dd = (uint32_t)dl[e];
+        const uint32_t mag = (uint32_t)abs(dl[e]);
+        const bool outl = mag > 32767u;
+        code[e] = outl ? 0u : (((dd >> 16) & 0x8000u) | mag);
+        if (outl) dmask |= 1u << e;
+    }
+    if (vm != 0xFFu) {
+        dmask &= vm;
+        vmask &= vm;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (!((vm >> e) & 1u)) code[e] = 0u;
+    }
+    if (a.codes_out != nullptr) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (g0 + e < n) a.codes_out[g0 + e] = (uint16_t)code[e];
+    }
+    if (!a.rescan) {
+        // ---- C4 words, C5 bitshuffle in registers: row c = tid/8 of A ----
+        uint32_t w4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w4[i] = __byte_perm(code[2 * i], code[2 * i + 1], 0x5410);
+        transpose32_group8(w4, lane & 7);
+        const int c = tid >> 3, kk = tid & 7;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Obuf[(4 * kk + i) * 33 + c] = w4[i];
+    }
+    const int any_out = __syncthreads_or((dmask | vmask) != 0);
+    if (first && tid == 0) {
+        const uint32_t nu = atomicAdd(&ctrl->ticket, 1u);
+        sh.unit[(us.it & 1) ^ 1] = nu;
+        // TMA L2 prefetch of the next unit's input (~kUnitTiles tiles ahead)
+        if (nu < us.nunits)
+            prefetch_l2_range(a, (uint64_t)(a.tile_begin + nu * kUnitTiles) * kTileCodes,
+                              (uint64_t)kUnitTiles * kTileCodes);
+    }
+
+    // ---- outlier records (rare; R7, R20): ascending element index ----
+    if (any_out) {
+        const int cd = __popc(dmask), cv = __popc(vmask);
+        const int wd = __reduce_add_sync(kFull, cd), wv = __reduce_add_sync(kFull, cv);
+        if (lane == 0) { sh.cd[warp] = wd; sh.cv[warp] = wv; }
+        __syncthreads();
+        uint32_t tnd = 0, tnv = 0, wpre_d = 0, wpre_v = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            tnd += sh.cd[w]; tnv += sh.cv[w];
+            if (w < warp) { wpre_d += sh.cd[w]; wpre_v += sh.cv[w]; }
+        }
+        if (tid == 0) {
+            if (a.rescan) {
+                const uint2 o = a.opre[t];
+                sh.ob[0] = o.x; sh.ob[1] = o.y;
+            } else {
+                sh.ob[0] = tnd ? atomicAdd(&ctrl->dcount, (unsigned long long)tnd) : 0ull;
+                sh.ob[1] = tnv ? atomicAdd(&ctrl->vcount, (unsigned long long)tnv) : 0ull;
+                a.ocnt[t] = make_uint2(tnd, tnv);
+                a.obase[t] = make_uint2((uint32_t)sh.ob[0], (uint32_t)sh.ob[1]);
+            }
+        }
+        int id = cd, iv = cv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yd = __shfl_up_sync(kFull, id, o), yv = __shfl_up_sync(kFull, iv, o);
+            if (lane >= o) { id += yd; iv += yv; }
+        }
+        __syncthreads();
+        uint64_t pd = sh.ob[0] + wpre_d + (id - cd), pv = sh.ob[1] + wpre_v + (iv - cv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint32_t gi = g0 + e;
+            if (dmask & (1u << e)) {
+                if (pd < a.dcap) {
+                    if (a.o_didx) { a.o_didx[pd] = gi; a.o_dval[pd] = dl[e]; }
+                    else a.dstage[pd] = make_uint2(gi, (uint32_t)dl[e]);
+                } else {
+                    atomicOr(&ctrl->stage_overflow, 1u);
+                }
+                ++pd;
+            }
+            if (vmask & (1u << e)) {
+                if (pv < a.vcap) {
+                    if (a.o_vidx) { a.o_vidx[pv] = gi; a.o_vbits[pv] = __float_as_uint(dv[e]); }
+                    else a.vstage[pv] = make_uint2(gi, __float_as_uint(dv[e]));
+                } else {
+                    atomicOr(&ctrl->stage_overflow, 1u);
+                }
+                ++pv;
+            }
+        }
+        __syncthreads();
+    }
+    if (a.rescan) return;
+
+    if (a.exp & 4) { us.cnt += 1; __syncthreads(); return; }
+    // ---- C6 block flags: thread b owns block b = 8r + x of the shuffled tile ----
+    const uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+    const uint4 blk = make_uint4(row[0], row[1], row[2], row[3]);
+    const bool nz = (blk.x | blk.y | blk.z | blk.w) != 0;
+    const uint32_t F = __ballot_sync(kFull, nz);
+    if (lane == 0) sh.F[warp] = F;
+    // the pending unit's look-back (window prefetched at the top of the tile) overlaps the
+    // other warps' flag work; it only blocks at the unit's last tile (lbt)
+    if (us.pu != kNone && warp == 0) {
+        unsigned long long ex = 0;
+        bool ok = true;
+        if (us.pu != 0 && !(a.exp & 1)) {
+            if (pre != nullptr) ok = lookback_try<kLbLane>(a.status, us.pu, 0, kStAgg - 1, &ctrl->err, *reinterpret_cast<const unsigned long long (*)[kLbLane]>(pre), ex, (a.exp & 8) ? &ctrl->dbg[3] : nullptr);
+            else ok = false;
+            if ((a.exp & 8) && lane == 0) {
+                atomicAdd(&ctrl->dbg[0], 1ull);
+                if (!ok) atomicAdd(&ctrl->dbg[1], 1ull);
+                if (!ok && lbt) atomicAdd(&ctrl->dbg[2], 1ull);
+            }
+            if (!ok && lbt) {
+                ex = lookback_wide<kLbLane, false>(a.status, us.pu, 0, kStAgg - 1, &ctrl->err);
+                ok = true;
+            }
+            if (ok && lane == 0) st_relaxed_u64(&a.status[us.pu], kStInc | (ex + us.pcnt));
+        }
+        if (lane == 0) {
+            sh.off = ex;
+            sh.lbok = ok;
+        }
+    }
+    __syncthreads();
+    uint32_t tn = 0, wpre = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const uint32_t pc = __popc(sh.F[w]);
+        tn += pc;
+        if (w < warp) wpre += pc;
+    }
+    if (tid < 8) {
+        const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * tid;
+        if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = sh.F[tid];
+    }
+    // ---- C8 (local): compact the tile's nonzero blocks into the unit stage ----
+    if (nz) stage[us.buf * kStageBlocks + us.cnt + wpre + __popc(F & ((1u << lane) - 1u))] = blk;
+    us.cnt += tn;
+    if (us.pu != kNone && sh.lbok) {
+        // ---- C8 (global): the pending unit's stage goes to its final offset ----
+        flush_unit(a, sh, stage + (us.buf ^ 1) * kStageBlocks, us, sh.off);
+        us.pu = kNone;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Lorenzo masks of a thread's 8 elements: bit e of xmask/ymask/zmask = the x-1 / y-1 / z-1
+// neighbour of element g0+e exists (zero boundary outside the field, R5).  `fast` = all set.
+// ------------------------------------------------------------------------------------
+template <int NDIM>
+__device__ __forceinline__ void lorenzo_masks(const CompressArgs& a, uint32_t g0, uint32_t& xm, uint32_t& ym,
+                                              uint32_t& zm, bool& fast_yz)
+{
+    const uint32_t nx = a.g.nx, PL = a.g.P;
+    xm = 0xFFu; ym = 0xFFu; zm = 0xFFu;
+    fast_yz = true;
+    if (nx >= 8) {
+        const uint32_t x0 = fmod_(g0, a.dnx);
+        const uint32_t us = x0 == 0 ? 0u : nx - x0;
+        if (us < 8) xm &= ~(1u << us);
+        if (NDIM >= 2) {
+            const uint32_t p0 = fmod_(g0, a.dP);
+            fast_yz = p0 >= nx && p0 + 7 < PL && (NDIM == 2 || g0 >= PL);
+            if (!fast_yz) {
+                uint32_t pp = p0;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    if (pp < nx) ym &= ~(1u << e);
+                    if (g0 + e < PL) zm &= ~(1u << e);
+                    if (++pp == PL) pp = 0;
+                }
+            }
+        }
+    } else {
+        fast_yz = false;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if (fmod_(g0 + e, a.dnx) == 0) xm &= ~(1u << e);
+            if (fmod_(g0 + e, a.dP) < nx) ym &= ~(1u << e);
+            if (g0 + e < PL) zm &= ~(1u << e);
+        }
+    }
+    if (NDIM == 1) { ym = 0; zm = 0; }
+    if (NDIM == 2) zm = 0;
+}
+
+// delta(e) = S(e+1) - [x>0] S(e), with S(j) the y/z combination at element g0-1+j (C2).
+__device__ __forceinline__ void residuals(const uint32_t (&S)[9], uint32_t xm, int32_t (&dl)[8])
+{
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const uint32_t X = (xm >> e) & 1u ? 0xFFFFFFFFu : 0u;
+        dl[e] = (int32_t)(S[e + 1] - (S[e] & X));
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// front_gen: generic shapes (padded linear arrays, halos re-quantized per tile).
+// ------------------------------------------------------------------------------------
+// Cooperative prequantization of two ranges into shared arrays (word offsets o0, o1 in
+// smem): element m of range r at o_r + m + (m >> 3).  4-element aligned chunks.
+__device__ __forceinline__ void fill_halo(const CompressArgs& a, const QuantP& P, int* smem, int o0, int64_t g0lo,
+                                          int len0, int o1, int64_t g1lo, int len1)
+{
+    const int64_t a0 = g0lo & ~(int64_t)3, a1 = g1lo & ~(int64_t)3;
+    const int n0 = len0 > 0 ? (int)((g0lo + len0 - a0 + 3) >> 2) : 0;
+    const int n1 = len1 > 0 ? (int)((g1lo + len1 - a1 + 3) >> 2) : 0;
+    const int total = n0 + n1;
+    for (int c0 = 0; c0 < total; c0 += kCta * kFillBatch) {
+        float v[4 * kFillBatch];
+        int64_t gc[kFillBatch];
+#pragma unroll
+        for (int i = 0; i < kFillBatch; ++i) {
+            const int c = c0 + threadIdx.x + i * kCta;
+            gc[i] = c < n0 ? a0 + 4 * (int64_t)c : a1 + 4 * (int64_t)(c - n0);
+            float x[4];
+            if (c < total) {
+                loadk<4>(a, gc[i], x);
+            } else {
+                x[0] = x[1] = x[2] = x[3] = 0.0f;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[4 * i + u] = x[u];
+        }
+        int q[4 * kFillBatch];
+        pq_many<4 * kFillBatch>(v, q, P);
+#pragma unroll
+        for (int i = 0; i < kFillBatch; ++i) {
+            const int c = c0 + threadIdx.x + i * kCta;
+            if (c >= total) continue;
+            const bool r0 = c < n0;
+            const int ob = r0 ? o0 : o1;
+            const int m0 = (int)(gc[i] - (r0 ? g0lo : g1lo));
+            const int len = r0 ? len0 : len1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int m = m0 + u;
+                if (m >= 0 && m < len) smem[ob + m + (m >> 3)] = q[4 * i + u];
+            }
+        }
+    }
+}
+
+template <int NDIM>
+__device__ __forceinline__ void front_gen(const CompressArgs& a, const QuantP& P, int* smem, uint32_t t,
+                                          int32_t (&dl)[8], uint32_t& vmask, float (&dv)[8], uint32_t& vm)
+{
+    const int tid = threadIdx.x;
     const uint32_t n = a.g.n, nx = a.g.nx, PL = a.g.P;
     const int qs = (int)a.qstride;
-    // neighbour streams: array base (words) and m offset of own element j = 0
     int ab[4], mo[4];
-    int narr;
     if (NDIM == 1) {
-        ab[0] = 0; mo[0] = 1; narr = 1;
+        ab[0] = ab[1] = ab[2] = ab[3] = 0; mo[0] = mo[1] = mo[2] = mo[3] = 1;
     } else if (a.union_mode) {
         const int HA = (int)nx + 1;
         ab[0] = 0; mo[0] = HA; ab[1] = 0; mo[1] = 1;
         ab[2] = qs; mo[2] = HA; ab[3] = qs; mo[3] = 1;
-        narr = NDIM == 3 ? 2 : 1;
     } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k) { ab[k] = k * qs; mo[k] = 1; }
-        narr = NDIM == 3 ? 4 : 2;
     }
-    uint32_t* Obuf = reinterpret_cast<uint32_t*>(smem + narr * qs);              // 32 x 33
-    uint4* stage = reinterpret_cast<uint4*>(smem + narr * qs + 32 * 33 + 3);     // 2 x units
-    stage = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(stage) + 15) & ~uintptr_t(15));
-    constexpr int kStageBlocks = kUnitTiles * kTileBlocks;
-
-    const uint32_t nunits = (a.tile_end - a.tile_begin + kUnitTiles - 1) / kUnitTiles;
-    constexpr uint32_t NONE = 0xFFFFFFFFu;
-    if (tid == 0) s_unit[0] = atomicAdd(&ctrl->ticket, 1u);
+    const int tb9 = 9 * tid;       // (8 tid) + ((8 tid) >> 3)
+    const int64_t s = (int64_t)t * kTileCodes;
+    const uint32_t g0 = (uint32_t)s + 8u * tid;
+    loadk<8>(a, (int64_t)g0, dv);
+    if (NDIM == 1) {
+        fill_halo(a, P, smem, 0, s - 1, 1, 0, 0, 0);
+    } else if (a.union_mode) {
+        fill_halo(a, P, smem, 0, s - (int64_t)nx - 1, (int)nx + 1, qs, s - (int64_t)PL - nx - 1,
+                  NDIM == 3 ? kTileCodes + (int)nx + 1 : 0);
+    } else {
+        fill_halo(a, P, smem, 0, s - 1, 1, ab[1], s - (int64_t)nx - 1, kTileCodes + 1);
+        if (NDIM == 3)
+            fill_halo(a, P, smem, ab[2], s - (int64_t)PL - 1, kTileCodes + 1, ab[3], s - (int64_t)PL - nx - 1,
+                      kTileCodes + 1);
+    }
+    int qo[8];
+    pq_own(dv, qo, vmask, P);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int m = mo[0] + e;
+        smem[ab[0] + tb9 + m + (m >> 3)] = qo[e];
+    }
+    vm = 0xFFu;
+    if (s + kTileCodes > (int64_t)n) vm = (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
     __syncthreads();
-    uint32_t pu = NONE;       // pending unit: aggregate published, offset unknown
-    uint32_t pcnt = 0;        // its block count
-    int buf = 0;              // stage buffer of the current unit
-    for (int it = 0;; ++it) {
-        const uint32_t u = s_unit[it & 1];
-        const bool work = u < nunits;
-        if (!work && pu == NONE) break;
+
+    uint32_t xm, ym, zm;
+    bool fast_yz;
+    lorenzo_masks<NDIM>(a, g0, xm, ym, zm, fast_yz);
+    uint32_t S[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        uint32_t ow;
+        if (j == 0) {
+            const int m = mo[0] - 1;
+            ow = (uint32_t)smem[ab[0] + tb9 + m + (m >> 3)];
+        } else {
+            ow = (uint32_t)qo[j - 1];
+        }
+        uint32_t v = ow;
+        if (NDIM >= 2) {
+            const int m1 = mo[1] - 1 + j;
+            const uint32_t qy = (uint32_t)smem[ab[1] + tb9 + m1 + (m1 >> 3)];
+            uint32_t qz = 0, qyz = 0;
+            if (NDIM == 3) {
+                const int m2 = mo[2] - 1 + j, m3 = mo[3] - 1 + j;
+                qz = (uint32_t)smem[ab[2] + tb9 + m2 + (m2 >> 3)];
+                qyz = (uint32_t)smem[ab[3] + tb9 + m3 + (m3 >> 3)];
+            }
+            if (fast_yz) {
+                v = ow - qy - (qz - qyz);
+            } else {
+                // masks of element j-1 for S(j), of element 0 for S(0)
+                const int e = j == 0 ? 0 : j - 1;
+                const uint32_t Y = (ym >> e) & 1u ? 0xFFFFFFFFu : 0u;
+                const uint32_t Z = (zm >> e) & 1u ? 0xFFFFFFFFu : 0u;
+                v = ow - (qy & Y) - ((qz - (qyz & Y)) & Z);
+            }
+        }
+        S[j] = v;
+    }
+    residuals(S, xm, dl);
+}
+
+// ------------------------------------------------------------------------------------
+// front_vec: nx % 4 == 0.  Rings RA (this plane) and RB (previous plane), R = rmask + 1
+// elements each, element g at index g & rmask.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void load8_vec(const CompressArgs& a, int64_t g, bool inb, float (&v)[8])
+{
+    if (inb) {
+        const float* p = a.field + (g - (int64_t)a.base);
+        const float4 x = ldg_f4(p), y = ldg_f4(p + 4);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+    } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = load1(a, g + u);
+    }
+}
+
+// Quantize the quads [lo4, hi) (lo4 4-aligned) of ring `R` (word offset ro) cooperatively.
+__device__ __forceinline__ void fill_ring(const CompressArgs& a, const QuantP& P, int* smem, int ro,
+                                          uint32_t rmask, int64_t lo4, int64_t hi)
+{
+    const int nq = (int)((hi - lo4 + 3) >> 2);
+    const int64_t base = (int64_t)a.base;
+    for (int c0 = 0; c0 < nq; c0 += kCta * 2) {
+        float v[8];
+        int64_t g[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int c = c0 + threadIdx.x + i * kCta;
+            g[i] = lo4 + 4 * (int64_t)c;
+            float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            if (c < nq) {
+                if (g[i] >= base && g[i] + 4 <= (int64_t)a.g.n) {
+                    const float4 f = ldg_f4(a.field + (g[i] - base));
+                    x[0] = f.x; x[1] = f.y; x[2] = f.z; x[3] = f.w;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) x[u] = load1(a, g[i] + u);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[4 * i + u] = x[u];
+        }
+        int q[8];
+        pq_many<8>(v, q, P);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int c = c0 + threadIdx.x + i * kCta;
+            if (c < nq)
+                *reinterpret_cast<int4*>(smem + ro + ((uint32_t)g[i] & rmask)) =
+                    make_int4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
+        }
+    }
+}
+
+template <int NDIM>
+__device__ __forceinline__ void front_vec(const CompressArgs& a, const QuantP& P, int* smem, uint32_t rmask,
+                                          uint32_t t, bool first, int32_t (&dl)[8], uint32_t& vmask,
+                                          float (&dv)[8], uint32_t& vm)
+{
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t n = a.g.n, nx = a.g.nx, PL = a.g.P;
+    const int RB = (int)rmask + 1;                  // word offset of the previous-plane ring
+    const int64_t s = (int64_t)t * kTileCodes;
+    const uint32_t g0 = (uint32_t)s + 8u * tid;
+    const int64_t base = (int64_t)a.base;
+    const int64_t H = NDIM >= 2 ? (int64_t)nx + 1 : 1;
+    const bool full = s + kTileCodes <= (int64_t)n;
+    const bool own_in = full && s >= base;
+    const bool b_in = full && s - (int64_t)PL >= base;
+    // ---- A: loads (own + previous plane), halos at a unit's first tile ----
+    float bz[8];
+    load8_vec(a, (int64_t)g0, own_in, dv);
+    if (NDIM == 3) load8_vec(a, (int64_t)g0 - PL, b_in, bz);
+    if (first) {
+        fill_ring(a, P, smem, 0, rmask, (s - H) & ~(int64_t)3, s);
+        if (NDIM == 3) fill_ring(a, P, smem, RB, rmask, (s - (int64_t)PL - H) & ~(int64_t)3, s - (int64_t)PL);
+    }
+    int qo[8], qz[8];
+    pq_own(dv, qo, vmask, P);
+    if (NDIM == 3) pq_many<8>(bz, qz, P);
+    *reinterpret_cast<int4*>(smem + (g0 & rmask)) = make_int4(qo[0], qo[1], qo[2], qo[3]);
+    *reinterpret_cast<int4*>(smem + ((g0 + 4) & rmask)) = make_int4(qo[4], qo[5], qo[6], qo[7]);
+    if (NDIM == 3) {
+        const uint32_t gb = g0 - PL;
+        *reinterpret_cast<int4*>(smem + RB + (gb & rmask)) = make_int4(qz[0], qz[1], qz[2], qz[3]);
+        *reinterpret_cast<int4*>(smem + RB + ((gb + 4) & rmask)) = make_int4(qz[4], qz[5], qz[6], qz[7]);
+    }
+    vm = 0xFFu;
+    if (!full) vm = (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
+    __syncthreads();
+
+    // ---- B: Lorenzo (C2) ----
+    uint32_t xm, ym, zm;
+    bool fast_yz;
+    lorenzo_masks<NDIM>(a, g0, xm, ym, zm, fast_yz);
+    uint32_t S[9];
+    if (NDIM == 1) {
+#pragma unroll
+        for (int j = 1; j < 9; ++j) S[j] = (uint32_t)qo[j - 1];
+    } else if (fast_yz) {
+        uint32_t y[8], yz[8];
+        {
+            const int4 p = *reinterpret_cast<const int4*>(smem + ((g0 - nx) & rmask));
+            const int4 q = *reinterpret_cast<const int4*>(smem + ((g0 - nx + 4) & rmask));
+            y[0] = p.x; y[1] = p.y; y[2] = p.z; y[3] = p.w; y[4] = q.x; y[5] = q.y; y[6] = q.z; y[7] = q.w;
+        }
+        if (NDIM == 3) {
+            const uint32_t gb = g0 - PL - nx;
+            const int4 p = *reinterpret_cast<const int4*>(smem + RB + (gb & rmask));
+            const int4 q = *reinterpret_cast<const int4*>(smem + RB + ((gb + 4) & rmask));
+            yz[0] = p.x; yz[1] = p.y; yz[2] = p.z; yz[3] = p.w; yz[4] = q.x; yz[5] = q.y; yz[6] = q.z; yz[7] = q.w;
+        }
+#pragma unroll
+        for (int j = 1; j < 9; ++j) {
+            uint32_t v = (uint32_t)qo[j - 1] - y[j - 1];
+            if (NDIM == 3) v -= (uint32_t)qz[j - 1] - yz[j - 1];
+            S[j] = v;
+        }
+    } else {
+        // boundary thread: every neighbour from the rings, masked per element
+#pragma unroll
+        for (int j = 1; j < 9; ++j) {
+            const uint32_t pos = g0 + j - 1;
+            const int e = j - 1;
+            const uint32_t Y = (ym >> e) & 1u ? 0xFFFFFFFFu : 0u;
+            const uint32_t Z = (zm >> e) & 1u ? 0xFFFFFFFFu : 0u;
+            const uint32_t qy = (uint32_t)smem[(pos - nx) & rmask];
+            uint32_t v = (uint32_t)qo[e] - (qy & Y);
+            if (NDIM == 3) {
+                const uint32_t qzz = (uint32_t)smem[RB + ((pos - PL) & rmask)];
+                const uint32_t qyz = (uint32_t)smem[RB + ((pos - PL - nx) & rmask)];
+                v -= (qzz - (qyz & Y)) & Z;
+            }
+            S[j] = v;
+        }
+    }
+    // S(0) at element g0-1: S(8) of the previous lane, computed directly by lane 0
+    S[0] = __shfl_up_sync(kFull, S[8], 1);
+    if (lane == 0 || !fast_yz) {
+        const uint32_t pos = g0 - 1;
+        const uint32_t Y = (ym & 1u) ? 0xFFFFFFFFu : 0u;
+        const uint32_t Z = (zm & 1u) ? 0xFFFFFFFFu : 0u;
+        uint32_t v = (uint32_t)smem[pos & rmask];
+        if (NDIM >= 2) v -= (uint32_t)smem[(pos - nx) & rmask] & Y;
+        if (NDIM == 3)
+            v -= ((uint32_t)smem[RB + ((pos - PL) & rmask)] - ((uint32_t)smem[RB + ((pos - PL - nx) & rmask)] & Y)) & Z;
+        S[0] = v;
+    }
+    residuals(S, xm, dl);
+}
+
+// ------------------------------------------------------------------------------------
+template <int NDIM, bool VEC>
+__device__ __forceinline__ void compress_body(const CompressArgs& a)
+{
+    extern __shared__ int smem[];
+    __shared__ CompShared sh;
+    const int tid = threadIdx.x;
+    Ctrl* ctrl = a.ctrl;
+    if (ctrl->err != 0) return;
+    QuantP P;
+    P.w = ctrl->p.w; P.r = ctrl->p.r; P.h = ctrl->h; P.eb32 = ctrl->p.eb32; P.hU = ctrl->hU;
+    uint32_t* Obuf = reinterpret_cast<uint32_t*>(smem + a.qwords);          // 32 x 33
+    uint4* stage = reinterpret_cast<uint4*>(smem + a.qwords + 32 * 33 + 4);  // 16-byte aligned
+    const uint32_t rmask = a.qstride - 1;                                    // ring mask (VEC)
+
+    UnitState us;
+    us.nunits = (a.tile_end - a.tile_begin + kUnitTiles - 1) / kUnitTiles;
+    us.pu = kNone;
+    us.pcnt = 0;
+    us.buf = 0;
+    if (tid == 0) sh.unit[0] = atomicAdd(&ctrl->ticket, 1u);
+    __syncthreads();
+    for (us.it = 0;; ++us.it) {
+        const uint32_t u = sh.unit[us.it & 1];
+        const bool work = u < us.nunits;
+        if (!work && us.pu == kNone) break;
         if (!work) {
             // ---- flush the last pending unit ----
-            if (warp == 0) {
-                unsigned long long ex = 0;
-                if (pu != 0) {
-                    ex = lookback_wide<8, false>(a.status, pu, 0, kStAgg - 1, &ctrl->err);
-                    if (lane == 0) st_relaxed_u64(&a.status[pu], kStInc | (ex + pcnt));
-                }
-                if (lane == 0) s_off = ex;
-            }
+            if ((tid >> 5) == 0) lookback_unit(a, sh, us);
             __syncthreads();
-            const uint4* ps = stage + (buf ^ 1) * kStageBlocks;
-            for (uint32_t i = tid; i < pcnt; i += kCta) {
-                const uint64_t bo = 16 * (s_off + i);
-                if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = ps[i];
-            }
-            if (tid == 0 && pu == nunits - 1) ctrl->nnz = s_off + pcnt;
+            flush_unit(a, sh, stage + (us.buf ^ 1) * kStageBlocks, us, sh.off);
             break;
         }
         const uint32_t t_first = a.tile_begin + u * kUnitTiles;
         const uint32_t t_last = min(a.tile_end, t_first + kUnitTiles);
-        uint32_t cnt = 0;                         // blocks staged for this unit (uniform)
-        uint4* st = stage + buf * kStageBlocks;
+        us.cnt = 0;
+        // the pending unit is resolved at the first tile where its window is complete, at
+        // the latest at the unit's last tile (before its stage buffer is reused)
         for (uint32_t t = t_first; t < t_last; ++t) {
-            const int64_t s = (int64_t)t * kTileCodes;
-            const uint32_t g0 = (uint32_t)s + 8u * tid;
-            const bool full = s + kTileCodes <= (int64_t)n;
-
-            // ---- A: prequantize own elements (+ bound check) and the halo ranges ----
-            float dv[8];
-            int qo[8];
-            uint32_t vmask = 0;
-            loadk<8>(a, (int64_t)g0, dv);
-            if (NDIM == 1 || !a.union_mode) {
-                if (tid == 0) smem[pad(0)] = quant_q<FB>(load1(a, s - 1), P);
-                if (NDIM >= 2) fill_range<FB>(a, P, smem + ab[1], s - (int64_t)nx - 1, kTileCodes + 1);
-                if (NDIM == 3) {
-                    fill_range<FB>(a, P, smem + ab[2], s - (int64_t)PL - 1, kTileCodes + 1);
-                    fill_range<FB>(a, P, smem + ab[3], s - (int64_t)PL - nx - 1, kTileCodes + 1);
-                }
-            } else {
-                fill_range<FB>(a, P, smem, s - (int64_t)nx - 1, (int)nx + 1);
-                if (NDIM == 3) fill_range<FB>(a, P, smem + qs, s - (int64_t)PL - nx - 1, kTileCodes + (int)nx + 1);
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                bool vo;
-                if (FB) {
-                    qo[e] = prequant(dv[e], P, vo);
-                } else {
-                    bool hard;
-                    float qf;
-                    qo[e] = prequant_fast(dv[e], P, hard, qf);
-                    if (hard) {
-                        qo[e] = prequant(dv[e], P, vo);
-                    } else {
-                        vo = fabsf(__fsub_rn(__fmul_rn(qf, P.w), dv[e])) > P.eb32;
-                    }
-                }
-                if (vo) vmask |= 1u << e;
-                smem[ab[0] + pad(mo[0] + 8 * tid + e)] = qo[e];
-            }
-            if (!full) vmask &= (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
-            __syncthreads();
-            if (t == t_first && tid == 0) {
-                const uint32_t nu = atomicAdd(&ctrl->ticket, 1u);
-                s_unit[(it & 1) ^ 1] = nu;
-                // TMA L2 prefetch of the next unit's input (~kUnitTiles tiles ahead): keeps
-                // HBM busy independently of how many loads the registers can hold
-                if (nu < nunits) prefetch_l2_range(a, (uint64_t)(a.tile_begin + nu * kUnitTiles) * kTileCodes,
-                                                   (uint64_t)kUnitTiles * kTileCodes);
-            }
-
-            // ---- B: Lorenzo residual (C2) as delta(e) = S(e+1) - [x>0] S(e), where S(j)
-            // combines the element at j-1 with its y-1, z-1, (y-1,z-1) neighbours ----
-            int S[9];
-            bool fast_yz = true;
-            uint32_t xmask = 0xFFu;
-            if (NDIM == 1) {
-                S[0] = smem[ab[0] + pad(mo[0] + 8 * tid - 1)];
-#pragma unroll
-                for (int j = 1; j < 9; ++j) S[j] = qo[j - 1];
-                if (nx >= 8) {
-                    const uint32_t x0 = fmod_(g0, a.dnx);
-                    const uint32_t us = x0 == 0 ? 0u : nx - x0;
-                    if (us < 8) xmask &= ~(1u << us);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        if (fmod_(g0 + e, a.dnx) == 0) xmask &= ~(1u << e);
-                }
-            } else {
-                int qy[9], qz[9], qyz[9];
-                const int o0 = ab[0] + pad(mo[0] + 8 * tid - 1);
-                const int own0 = smem[o0];
-#pragma unroll
-                for (int j = 0; j < 9; ++j) qy[j] = smem[ab[1] + pad(mo[1] + 8 * tid - 1 + j)];
-                if (NDIM == 3) {
-#pragma unroll
-                    for (int j = 0; j < 9; ++j) {
-                        qz[j] = smem[ab[2] + pad(mo[2] + 8 * tid - 1 + j)];
-                        qyz[j] = smem[ab[3] + pad(mo[3] + 8 * tid - 1 + j)];
-                    }
-                }
-                uint32_t ymask = 0xFFu, zmask = 0xFFu;   // bit e: neighbour exists for element e
-                if (nx >= 8) {
-                    const uint32_t x0 = fmod_(g0, a.dnx);
-                    const uint32_t us = x0 == 0 ? 0u : nx - x0;
-                    if (us < 8) xmask &= ~(1u << us);
-                    const uint32_t p0 = fmod_(g0, a.dP);
-                    fast_yz = p0 >= nx && p0 + 7 < PL && (NDIM == 2 || g0 >= PL);
-                    if (!fast_yz) {
-                        uint32_t pp = p0;
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            if (pp < nx) ymask &= ~(1u << e);
-                            if (g0 + e < PL) zmask &= ~(1u << e);
-                            if (++pp == PL) pp = 0;
-                        }
-                    }
-                } else {
-                    fast_yz = false;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        if (fmod_(g0 + e, a.dnx) == 0) xmask &= ~(1u << e);
-                        if (fmod_(g0 + e, a.dP) < nx) ymask &= ~(1u << e);
-                        if (g0 + e < PL) zmask &= ~(1u << e);
-                    }
-                }
-                if (NDIM == 2) zmask = 0;
-                if (fast_yz) {
-                    S[0] = (int)((uint32_t)own0 - (uint32_t)qy[0] - (NDIM == 3 ? (uint32_t)qz[0] - (uint32_t)qyz[0] : 0u));
-#pragma unroll
-                    for (int j = 1; j < 9; ++j)
-                        S[j] = (int)((uint32_t)qo[j - 1] - (uint32_t)qy[j] -
-                                     (NDIM == 3 ? (uint32_t)qz[j] - (uint32_t)qyz[j] : 0u));
-                } else {
-                    // masks of element j-1 for S(j); of element 0 for S(0)
-#pragma unroll
-                    for (int j = 0; j < 9; ++j) {
-                        const int e = j == 0 ? 0 : j - 1;
-                        const uint32_t Y = (ymask >> e) & 1u ? 0xFFFFFFFFu : 0u;
-                        const uint32_t Z = (zmask >> e) & 1u ? 0xFFFFFFFFu : 0u;
-                        const uint32_t ow = j == 0 ? (uint32_t)own0 : (uint32_t)qo[j - 1];
-                        uint32_t v = ow - ((uint32_t)qy[j] & Y);
-                        if (NDIM == 3) v -= ((uint32_t)qz[j] - ((uint32_t)qyz[j] & Y)) & Z;
-                        S[j] = (int)v;
-                    }
-                }
-            }
-            // ---- C3 codes, C4 words ----
-            uint32_t code[8];
+            const bool lbt = t == t_last - 1;
+            unsigned long long pre[kLbLane];
+            const bool use_pre = VEC && us.pu != kNone && us.pu != 0;
+            if (use_pre && (tid >> 5) == 0) lookback_load<kLbLane>(a.status, (int64_t)us.pu - 1, 0, pre);
             int32_t dl[8];
-            uint32_t dmask = 0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const uint32_t X = (xmask >> e) & 1u ? 0xFFFFFFFFu : 0u;
-                const uint32_t dd = (uint32_t)S[e + 1] - ((uint32_t)S[e] & X);
-                const int32_t di = (int32_t)dd;
-                const uint32_t mag = (uint32_t)abs(di);
-                const bool outl = mag > 32767u;
-                code[e] = outl ? 0u : (((dd >> 16) & 0x8000u) | mag);
-                dl[e] = di;
-                if (outl) dmask |= 1u << e;
-            }
-            if (!full) {
-                const uint32_t vm = (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
-                dmask &= vm;
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if (!((vm >> e) & 1u)) code[e] = 0u;
-            }
-            if (a.codes_out != nullptr) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if (g0 + e < n) a.codes_out[g0 + e] = (uint16_t)code[e];
-            }
-            if (!a.rescan) {
-                // ---- C5 bitshuffle in registers: row c = tid/8 of A, lanes k = tid%8 ----
-                uint32_t w4[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) w4[i] = __byte_perm(code[2 * i], code[2 * i + 1], 0x5410);
-                transpose32_group8(w4, lane & 7);
-                const int c = tid >> 3, kk = tid & 7;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) Obuf[(4 * kk + i) * 33 + c] = w4[i];
-            }
-            const int any_out = __syncthreads_or((dmask | vmask) != 0);
-
-            // ---- outlier records (rare; R7, R20): ascending element index ----
-            if (any_out) {
-                const int cd = __popc(dmask), cv = __popc(vmask);
-                const int wd = __reduce_add_sync(kFull, cd), wv = __reduce_add_sync(kFull, cv);
-                if (lane == 0) { s_cd[warp] = wd; s_cv[warp] = wv; }
-                __syncthreads();
-                uint32_t tnd = 0, tnv = 0, wpre_d = 0, wpre_v = 0;
-#pragma unroll
-                for (int w = 0; w < 8; ++w) {
-                    tnd += s_cd[w]; tnv += s_cv[w];
-                    if (w < warp) { wpre_d += s_cd[w]; wpre_v += s_cv[w]; }
-                }
-                if (tid == 0) {
-                    if (a.rescan) {
-                        const uint2 o = a.opre[t];
-                        s_ob[0] = o.x; s_ob[1] = o.y;
-                    } else {
-                        s_ob[0] = tnd ? atomicAdd(&ctrl->dcount, (unsigned long long)tnd) : 0ull;
-                        s_ob[1] = tnv ? atomicAdd(&ctrl->vcount, (unsigned long long)tnv) : 0ull;
-                        a.ocnt[t] = make_uint2(tnd, tnv);
-                        a.obase[t] = make_uint2((uint32_t)s_ob[0], (uint32_t)s_ob[1]);
-                    }
-                }
-                int id = cd, iv = cv;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int yd = __shfl_up_sync(kFull, id, o), yv = __shfl_up_sync(kFull, iv, o);
-                    if (lane >= o) { id += yd; iv += yv; }
-                }
-                __syncthreads();
-                uint64_t pd = s_ob[0] + wpre_d + (id - cd), pv = s_ob[1] + wpre_v + (iv - cv);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const uint32_t gi = g0 + e;
-                    if (dmask & (1u << e)) {
-                        if (pd < a.dcap) {
-                            if (a.o_didx) { a.o_didx[pd] = gi; a.o_dval[pd] = dl[e]; }
-                            else a.dstage[pd] = make_uint2(gi, (uint32_t)dl[e]);
-                        } else {
-                            atomicOr(&ctrl->stage_overflow, 1u);
-                        }
-                        ++pd;
-                    }
-                    if (vmask & (1u << e)) {
-                        if (pv < a.vcap) {
-                            if (a.o_vidx) { a.o_vidx[pv] = gi; a.o_vbits[pv] = __float_as_uint(dv[e]); }
-                            else a.vstage[pv] = make_uint2(gi, __float_as_uint(dv[e]));
-                        } else {
-                            atomicOr(&ctrl->stage_overflow, 1u);
-                        }
-                        ++pv;
-                    }
-                }
-                __syncthreads();
-            }
-            if (a.rescan) continue;
-
-            // ---- C6 block flags: thread b owns block b = 8r + x of the shuffled tile ----
-            const uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
-            const uint4 blk = make_uint4(row[0], row[1], row[2], row[3]);
-            const bool nz = (blk.x | blk.y | blk.z | blk.w) != 0;
-            const uint32_t F = __ballot_sync(kFull, nz);
-            if (lane == 0) s_F[warp] = F;
-            // the pending unit's look-back overlaps the other warps' flag work
-            if (t == t_first && pu != NONE && warp == 0) {
-                unsigned long long ex = 0;
-                if (pu != 0) {
-                    ex = lookback_wide<8, false>(a.status, pu, 0, kStAgg - 1, &ctrl->err);
-                    if (lane == 0) st_relaxed_u64(&a.status[pu], kStInc | (ex + pcnt));
-                }
-                if (lane == 0) s_off = ex;
-            }
-            __syncthreads();
-            uint32_t tn = 0, wpre = 0;
-#pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                const uint32_t pc = __popc(s_F[w]);
-                tn += pc;
-                if (w < warp) wpre += pc;
-            }
-            if (tid < 8) {
-                const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * tid;
-                if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = s_F[tid];
-            }
-            // ---- C8 (local): compact the tile's nonzero blocks into the unit stage ----
-            if (nz) st[cnt + wpre + __popc(F & ((1u << lane) - 1u))] = blk;
-            cnt += tn;
-            if (t == t_first && pu != NONE) {
-                // ---- C8 (global): the pending unit's stage goes to its final offset ----
-                const uint4* ps = stage + (buf ^ 1) * kStageBlocks;
-                const unsigned long long off = s_off;
-                for (uint32_t i = tid; i < pcnt; i += kCta) {
-                    const uint64_t bo = 16 * (off + i);
-                    if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = ps[i];
-                }
-                if (tid == 0 && pu == nunits - 1) ctrl->nnz = off + pcnt;
-                pu = NONE;
-            }
+            uint32_t vmask, vm;
+            float dv[8];
+            if (VEC) front_vec<NDIM>(a, P, smem, rmask, t, t == t_first, dl, vmask, dv, vm);
+            else front_gen<NDIM>(a, P, smem, t, dl, vmask, dv, vm);
+            tile_tail(a, sh, Obuf, stage, us, t, t == t_first, lbt, (uint32_t)t * kTileCodes + 8u * tid, vm,
+                      dl, vmask, dv, use_pre ? pre : nullptr);
         }
-        if (a.rescan) {
-            __syncthreads();
-            continue;
+        if (!a.rescan) {
+            // ---- C7: publish the unit's aggregate (inclusive for unit 0) ----
+            if (tid == 0) st_relaxed_u64(&a.status[u], (u == 0 ? kStInc : kStAgg) | us.cnt);
+            us.pu = u;
+            us.pcnt = us.cnt;
+            us.buf ^= 1;
         }
-        // ---- C7: publish the unit's aggregate (inclusive for unit 0) ----
-        if (tid == 0) st_relaxed_u64(&a.status[u], (u == 0 ? kStInc : kStAgg) | cnt);
-        pu = u;
-        pcnt = cnt;
-        buf ^= 1;
         __syncthreads();
     }
 }
 
-// The margin/fallback mode (R2) is known only on the device when fz_compress derives the
-// parameters there, so the kernel dispatches on it (block-uniform branch).
-template <int NDIM>
+// One kernel per (ndim, front end); the margin/fallback choice (R2) only changes the
+// fast-path threshold hU (k_params / k_init set hU = -1 in fallback mode).
+template <int NDIM, bool VEC>
 __global__ void __launch_bounds__(kCta, 2) k_compress(CompressArgs a)
 {
-    if (a.ctrl->p.fallback) compress_body<NDIM, true>(a);
-    else compress_body<NDIM, false>(a);
+    compress_body<NDIM, VEC>(a);
+}
+
+// ------------------------------------------------------------------------------------
+// Warp-specialized vector kernel (k_compress_ws): 8 compute warps + 1 scanner warp.
+//   compute warps : TMA-fed front (own tile and previous-plane tile arrive by
+//                   cp.async.bulk into a 2-stage shared buffer while the previous tile is
+//                   processed), Lorenzo, codes, bitshuffle, flags, local compaction into a
+//                   unit stage; at a unit's end they publish its aggregate and hand the
+//                   stage to the scanner (named barrier READY_b).
+//   scanner warp  : decoupled look-back of the unit (C7), inclusive publication, copy of
+//                   the stage to the payload (C8), then releases the stage (FREE_b).
+// The compute warps never wait for the look-back unless they are two units ahead.
+// Named barriers: 0 = whole CTA (start only), 1/2 = READY_0/1, 3/4 = FREE_0/1,
+// 5 = compute warps only.
+// ------------------------------------------------------------------------------------
+constexpr int kWsThreads = kCta + 32;
+constexpr int kBarCompute = 5;
+
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ int bar_or(int id, int n, int pred)
+{
+    int r;
+    asm volatile("{ .reg .pred p, q; setp.ne.s32 p, %1, 0; bar.red.or.pred q, %2, %3, p; selp.s32 %0, 1, 0, q; }"
+                 : "=r"(r) : "r"(pred), "r"(id), "r"(n) : "memory");
+    return r;
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* m, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(smem_u32(m)), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* m)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
+}
+
+struct WsShared {
+    uint64_t mbar[2];              // TMA input stages
+    uint32_t tma_bits[2];          // bit0: own tile loaded by TMA, bit1: previous-plane tile
+    uint32_t unit[2];
+    uint32_t ready_unit[2], ready_cnt[2];
+    uint32_t F[8];
+    uint32_t cd[8], cv[8];
+    unsigned long long ob[2];
+};
+
+// Issue the TMA loads of tile t into input stage `stg` (thread 0 of the compute group).
+template <int NDIM>
+__device__ __forceinline__ void ws_issue(const CompressArgs& a, WsShared& sh, float* inbuf, int stg, uint32_t t)
+{
+    const int64_t s = (int64_t)t * kTileCodes, base = (int64_t)a.base;
+    const bool full = s + kTileCodes <= (int64_t)a.g.n;
+    uint32_t bits = 0, bytes = 0;
+    if (full && s >= base) { bits |= 1; bytes += kTileCodes * 4; }
+    if (NDIM == 3 && full && s - (int64_t)a.g.P >= base) { bits |= 2; bytes += kTileCodes * 4; }
+    sh.tma_bits[stg] = bits;
+    if (bytes) {
+        uint64_t* m = &sh.mbar[stg];
+        mbar_expect_tx(m, bytes);
+        float* dst = inbuf + stg * 2 * kTileCodes;
+        if (bits & 1) tma_load_1d(dst, a.field + (s - base), kTileCodes * 4, m);
+        if (bits & 2) tma_load_1d(dst + kTileCodes, a.field + (s - (int64_t)a.g.P - base), kTileCodes * 4, m);
+    }
+}
+
+template <int NDIM>
+__device__ __forceinline__ void front_ws(const CompressArgs& a, const QuantP& P, int* smem, uint32_t rmask,
+                                         uint32_t t, bool first, const float* in_own, const float* in_b,
+                                         int32_t (&dl)[8], uint32_t& vmask, float (&dv)[8], uint32_t& vm)
+{
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t n = a.g.n, nx = a.g.nx, PL = a.g.P;
+    const int RB = (int)rmask + 1;
+    const int64_t s = (int64_t)t * kTileCodes;
+    const uint32_t g0 = (uint32_t)s + 8u * tid;
+    const int64_t H = NDIM >= 2 ? (int64_t)nx + 1 : 1;
+    const bool full = s + kTileCodes <= (int64_t)n;
+    float bz[8];
+    if (in_own) {
+        const float4 x = *reinterpret_cast<const float4*>(in_own + 8 * tid);
+        const float4 y = *reinterpret_cast<const float4*>(in_own + 8 * tid + 4);
+        dv[0] = x.x; dv[1] = x.y; dv[2] = x.z; dv[3] = x.w; dv[4] = y.x; dv[5] = y.y; dv[6] = y.z; dv[7] = y.w;
+    } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dv[u] = load1(a, (int64_t)g0 + u);
+    }
+    if (NDIM == 3) {
+        if (in_b) {
+            const float4 x = *reinterpret_cast<const float4*>(in_b + 8 * tid);
+            const float4 y = *reinterpret_cast<const float4*>(in_b + 8 * tid + 4);
+            bz[0] = x.x; bz[1] = x.y; bz[2] = x.z; bz[3] = x.w; bz[4] = y.x; bz[5] = y.y; bz[6] = y.z; bz[7] = y.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) bz[u] = load1(a, (int64_t)g0 - PL + u);
+        }
+    }
+    if (first) {
+        fill_ring(a, P, smem, 0, rmask, (s - H) & ~(int64_t)3, s);
+        if (NDIM == 3) fill_ring(a, P, smem, RB, rmask, (s - (int64_t)PL - H) & ~(int64_t)3, s - (int64_t)PL);
+    }
+    int qo[8], qz[8];
+    pq_own(dv, qo, vmask, P);
+    if (NDIM == 3) pq_many<8>(bz, qz, P);
+    *reinterpret_cast<int4*>(smem + (g0 & rmask)) = make_int4(qo[0], qo[1], qo[2], qo[3]);
+    *reinterpret_cast<int4*>(smem + ((g0 + 4) & rmask)) = make_int4(qo[4], qo[5], qo[6], qo[7]);
+    if (NDIM == 3) {
+        const uint32_t gb = g0 - PL;
+        *reinterpret_cast<int4*>(smem + RB + (gb & rmask)) = make_int4(qz[0], qz[1], qz[2], qz[3]);
+        *reinterpret_cast<int4*>(smem + RB + ((gb + 4) & rmask)) = make_int4(qz[4], qz[5], qz[6], qz[7]);
+    }
+    vm = 0xFFu;
+    if (!full) vm = (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
+    bar_sync(kBarCompute, kCta);
+
+    uint32_t xm, ym, zm;
+    bool fast_yz;
+    lorenzo_masks<NDIM>(a, g0, xm, ym, zm, fast_yz);
+    uint32_t S[9];
+    if (NDIM == 1) {
+#pragma unroll
+        for (int j = 1; j < 9; ++j) S[j] = (uint32_t)qo[j - 1];
+    } else if (fast_yz) {
+        uint32_t y[8], yz[8];
+        {
+            const int4 p = *reinterpret_cast<const int4*>(smem + ((g0 - nx) & rmask));
+            const int4 q = *reinterpret_cast<const int4*>(smem + ((g0 - nx + 4) & rmask));
+            y[0] = p.x; y[1] = p.y; y[2] = p.z; y[3] = p.w; y[4] = q.x; y[5] = q.y; y[6] = q.z; y[7] = q.w;
+        }
+        if (NDIM == 3) {
+            const uint32_t gb = g0 - PL - nx;
+            const int4 p = *reinterpret_cast<const int4*>(smem + RB + (gb & rmask));
+            const int4 q = *reinterpret_cast<const int4*>(smem + RB + ((gb + 4) & rmask));
+            yz[0] = p.x; yz[1] = p.y; yz[2] = p.z; yz[3] = p.w; yz[4] = q.x; yz[5] = q.y; yz[6] = q.z; yz[7] = q.w;
+        }
+#pragma unroll
+        for (int j = 1; j < 9; ++j) {
+            uint32_t v = (uint32_t)qo[j - 1] - y[j - 1];
+            if (NDIM == 3) v -= (uint32_t)qz[j - 1] - yz[j - 1];
+            S[j] = v;
+        }
+    } else {
+#pragma unroll
+        for (int j = 1; j < 9; ++j) {
+            const uint32_t pos = g0 + j - 1;
+            const int e = j - 1;
+            const uint32_t Y = (ym >> e) & 1u ? 0xFFFFFFFFu : 0u;
+            const uint32_t Z = (zm >> e) & 1u ? 0xFFFFFFFFu : 0u;
+            const uint32_t qy = (uint32_t)smem[(pos - nx) & rmask];
+            uint32_t v = (uint32_t)qo[e] - (qy & Y);
+            if (NDIM == 3) {
+                const uint32_t qzz = (uint32_t)smem[RB + ((pos - PL) & rmask)];
+                const uint32_t qyz = (uint32_t)smem[RB + ((pos - PL - nx) & rmask)];
+                v -= (qzz - (qyz & Y)) & Z;
+            }
+            S[j] = v;
+        }
+    }
+    S[0] = __shfl_up_sync(kFull, S[8], 1);
+    if (lane == 0 || !fast_yz) {
+        const uint32_t pos = g0 - 1;
+        const uint32_t Y = (ym & 1u) ? 0xFFFFFFFFu : 0u;
+        const uint32_t Z = (zm & 1u) ? 0xFFFFFFFFu : 0u;
+        uint32_t v = (uint32_t)smem[pos & rmask];
+        if (NDIM >= 2) v -= (uint32_t)smem[(pos - nx) & rmask] & Y;
+        if (NDIM == 3)
+            v -= ((uint32_t)smem[RB + ((pos - PL) & rmask)] - ((uint32_t)smem[RB + ((pos - PL - nx) & rmask)] & Y)) & Z;
+        S[0] = v;
+    }
+    residuals(S, xm, dl);
+}
+
+// Tail of a tile on the compute warps (no look-back): codes, bitshuffle, outliers, flags,
+// local compaction.  Returns the tile's nonzero block count.
+__device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh, uint32_t* Obuf, uint4* st,
+                                            uint32_t cnt, uint32_t t, uint32_t g0, uint32_t vm,
+                                            const int32_t (&dl)[8], uint32_t vmask, const float (&dv)[8])
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Ctrl* ctrl = a.ctrl;
+    const uint32_t n = a.g.n;
+    uint32_t code[8];
+    uint32_t dmask = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const uint32_t dd = (uint32_t)dl[e];
+        const uint32_t mag = (uint32_t)abs(dl[e]);
+        const bool outl = mag > 32767u;
+        code[e] = outl ? 0u : (((dd >> 16) & 0x8000u) | mag);
+        if (outl) dmask |= 1u << e;
+    }
+    if (vm != 0xFFu) {
+        dmask &= vm;
+        vmask &= vm;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (!((vm >> e) & 1u)) code[e] = 0u;
+    }
+    if (a.codes_out != nullptr) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (g0 + e < n) a.codes_out[g0 + e] = (uint16_t)code[e];
+    }
+    if (!a.rescan) {
+        uint32_t w4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w4[i] = __byte_perm(code[2 * i], code[2 * i + 1], 0x5410);
+        transpose32_group8(w4, lane & 7);
+        const int c = tid >> 3, kk = tid & 7;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Obuf[(4 * kk + i) * 33 + c] = w4[i];
+    }
+    const int any_out = bar_or(kBarCompute, kCta, (dmask | vmask) != 0);
+    if (any_out) {
+        const int cd = __popc(dmask), cv = __popc(vmask);
+        const int wd = __reduce_add_sync(kFull, cd), wv = __reduce_add_sync(kFull, cv);
+        if (lane == 0) { sh.cd[warp] = wd; sh.cv[warp] = wv; }
+        bar_sync(kBarCompute, kCta);
+        uint32_t tnd = 0, tnv = 0, wpre_d = 0, wpre_v = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            tnd += sh.cd[w]; tnv += sh.cv[w];
+            if (w < warp) { wpre_d += sh.cd[w]; wpre_v += sh.cv[w]; }
+        }
+        if (tid == 0) {
+            if (a.rescan) {
+                const uint2 o = a.opre[t];
+                sh.ob[0] = o.x; sh.ob[1] = o.y;
+            } else {
+                sh.ob[0] = tnd ? atomicAdd(&ctrl->dcount, (unsigned long long)tnd) : 0ull;
+                sh.ob[1] = tnv ? atomicAdd(&ctrl->vcount, (unsigned long long)tnv) : 0ull;
+                a.ocnt[t] = make_uint2(tnd, tnv);
+                a.obase[t] = make_uint2((uint32_t)sh.ob[0], (uint32_t)sh.ob[1]);
+            }
+        }
+        int id = cd, iv = cv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yd = __shfl_up_sync(kFull, id, o), yv = __shfl_up_sync(kFull, iv, o);
+            if (lane >= o) { id += yd; iv += yv; }
+        }
+        bar_sync(kBarCompute, kCta);
+        uint64_t pd = sh.ob[0] + wpre_d + (id - cd), pv = sh.ob[1] + wpre_v + (iv - cv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint32_t gi = g0 + e;
+            if (dmask & (1u << e)) {
+                if (pd < a.dcap) {
+                    if (a.o_didx) { a.o_didx[pd] = gi; a.o_dval[pd] = dl[e]; }
+                    else a.dstage[pd] = make_uint2(gi, (uint32_t)dl[e]);
+                } else {
+                    atomicOr(&ctrl->stage_overflow, 1u);
+                }
+                ++pd;
+            }
+            if (vmask & (1u << e)) {
+                if (pv < a.vcap) {
+                    if (a.o_vidx) { a.o_vidx[pv] = gi; a.o_vbits[pv] = __float_as_uint(dv[e]); }
+                    else a.vstage[pv] = make_uint2(gi, __float_as_uint(dv[e]));
+                } else {
+                    atomicOr(&ctrl->stage_overflow, 1u);
+                }
+                ++pv;
+            }
+        }
+        bar_sync(kBarCompute, kCta);
+    }
+    if (a.rescan) return 0;
+    const uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+    const uint4 blk = make_uint4(row[0], row[1], row[2], row[3]);
+    const bool nz = (blk.x | blk.y | blk.z | blk.w) != 0;
+    const uint32_t F = __ballot_sync(kFull, nz);
+    if (lane == 0) sh.F[warp] = F;
+    bar_sync(kBarCompute, kCta);
+    uint32_t tn = 0, wpre = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const uint32_t pc = __popc(sh.F[w]);
+        tn += pc;
+        if (w < warp) wpre += pc;
+    }
+    if (tid < 8) {
+        const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * tid;
+        if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = sh.F[tid];
+    }
+    if (nz) st[cnt + wpre + __popc(F & ((1u << lane) - 1u))] = blk;
+    return tn;
+}
+
+template <int NDIM>
+__global__ void __launch_bounds__(kWsThreads, 2) k_compress_ws(CompressArgs a)
+{
+    extern __shared__ __align__(16) int smem[];
+    __shared__ WsShared sh;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    Ctrl* ctrl = a.ctrl;
+    if (ctrl->err != 0) return;
+    const uint32_t rmask = a.qstride - 1;
+    uint32_t* Obuf = reinterpret_cast<uint32_t*>(smem + a.qwords);           // 32 x 33
+    uint4* stage = reinterpret_cast<uint4*>(smem + a.qwords + 32 * 33 + 4);   // 2 x kStageBlocks
+    float* inbuf = reinterpret_cast<float*>(stage + 2 * kStageBlocks);        // 2 stages x (own, prev)
+    const uint32_t nunits = (a.tile_end - a.tile_begin + kUnitTiles - 1) / kUnitTiles;
+
+    if (tid == 0) {
+        mbar_init(&sh.mbar[0], 1);
+        mbar_init(&sh.mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sh.unit[0] = atomicAdd(&ctrl->ticket, 1u);
+        sh.tma_bits[0] = sh.tma_bits[1] = 0;
+        if (sh.unit[0] < nunits) ws_issue<NDIM>(a, sh, inbuf, 0, a.tile_begin + sh.unit[0] * kUnitTiles);
+    }
+    __syncthreads();
+
+    if (warp == kCta / 32) {
+        // ================= scanner warp =================
+        if (a.rescan) return;
+        for (int k = 0;; ++k) {
+            const int b = k & 1;
+            bar_sync(1 + b, kWsThreads);
+            const uint32_t u = sh.ready_unit[b];
+            if (u == kNone) break;
+            const uint32_t cnt = sh.ready_cnt[b];
+            unsigned long long ex = 0;
+            if (u != 0) {
+                long long t0 = clock64();
+                ex = lookback_wide<kLbLane, false>(a.status, u, 0, kStAgg - 1, &ctrl->err, nullptr,
+                                                   (a.exp & 8) ? &ctrl->dbg[0] : nullptr);
+                if (lane == 0) st_relaxed_u64(&a.status[u], kStInc | (ex + cnt));
+                if ((a.exp & 8) && lane == 0) {
+                    atomicAdd(&ctrl->dbg[1], 1ull);
+                    atomicAdd(&ctrl->dbg[2], (unsigned long long)(clock64() - t0));
+                }
+            }
+            const uint4* ps = stage + b * kStageBlocks;
+            for (uint32_t i = lane; i < cnt; i += 32) {
+                const uint64_t bo = 16 * (ex + i);
+                if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = ps[i];
+            }
+            if (lane == 0 && u == nunits - 1) ctrl->nnz = ex + cnt;
+            __syncwarp();
+            bar_arrive(3 + b, kWsThreads);
+        }
+        return;
+    }
+
+    // ================= compute warps =================
+    QuantP P;
+    P.w = ctrl->p.w; P.r = ctrl->p.r; P.h = ctrl->h; P.eb32 = ctrl->p.eb32; P.hU = ctrl->hU;
+    uint32_t phase = 0;     // bit s: parity of the next wait on input stage s
+    int stg = 0;            // input stage of the current tile
+    int k = 0;              // units processed by this CTA
+    for (int it = 0;; ++it) {
+        const uint32_t u = sh.unit[it & 1];
+        const int b = k & 1;
+        if (u >= nunits) {
+            if (!a.rescan) {
+                if (k >= 2) bar_sync(3 + b, kWsThreads);     // stage b released by the scanner
+                if (tid == 0) sh.ready_unit[b] = kNone;
+                bar_arrive(1 + b, kWsThreads);
+            }
+            break;
+        }
+        if (!a.rescan && k >= 2) bar_sync(3 + b, kWsThreads);
+        const uint32_t t_first = a.tile_begin + u * kUnitTiles;
+        const uint32_t t_last = min(a.tile_end, t_first + kUnitTiles);
+        uint32_t cnt = 0;
+        for (uint32_t t = t_first; t < t_last; ++t) {
+            const bool first = t == t_first;
+            // wait for this tile's TMA input
+            const uint32_t bits = sh.tma_bits[stg];
+            if (bits) {
+                while (!mbar_try_wait(&sh.mbar[stg], (phase >> stg) & 1u)) {
+                }
+                phase ^= 1u << stg;
+            }
+            const float* ib = inbuf + stg * 2 * kTileCodes;
+            int32_t dl[8];
+            uint32_t vmask, vm;
+            float dv[8];
+            front_ws<NDIM>(a, P, smem, rmask, t, first, (bits & 1) ? ib : nullptr,
+                           (bits & 2) ? ib + kTileCodes : nullptr, dl, vmask, dv, vm);
+            // every compute thread has consumed input stage `stg`: prefetch the next tile
+            if (tid == 0) {
+                if (first) sh.unit[(it & 1) ^ 1] = atomicAdd(&ctrl->ticket, 1u);
+                uint32_t nt = kNone;
+                if (t + 1 < t_last) nt = t + 1;
+                else if (sh.unit[(it & 1) ^ 1] < nunits) nt = a.tile_begin + sh.unit[(it & 1) ^ 1] * kUnitTiles;
+                if (nt != kNone) {
+                    ws_issue<NDIM>(a, sh, inbuf, stg ^ 1, nt);
+                    if (first && nt != t + 1 && sh.unit[(it & 1) ^ 1] + 1 < nunits) {
+                    }
+                } else {
+                    sh.tma_bits[stg ^ 1] = 0;
+                }
+                if (first) {
+                    const uint32_t nu = sh.unit[(it & 1) ^ 1];
+                    if (nu < nunits)   // L2 prefetch of the next unit beyond the TMA stage
+                        prefetch_l2_range(a, (uint64_t)(a.tile_begin + nu * kUnitTiles) * kTileCodes,
+                                          (uint64_t)kUnitTiles * kTileCodes);
+                }
+            }
+            cnt += tail_ws(a, sh, Obuf, stage + b * kStageBlocks, cnt, t, (uint32_t)t * kTileCodes + 8u * tid, vm,
+                           dl, vmask, dv);
+            stg ^= 1;
+        }
+        if (!a.rescan) {
+            if (tid == 0) {
+                st_relaxed_u64(&a.status[u], (u == 0 ? kStInc : kStAgg) | cnt);
+                sh.ready_unit[b] = u;
+                sh.ready_cnt[b] = cnt;
+            }
+            bar_arrive(1 + b, kWsThreads);
+        }
+        ++k;
+        bar_sync(kBarCompute, kCta);
+    }
 }
 
 // ------------------------------------------------------------------------------------
@@ -637,55 +1384,96 @@ int num_sms()
     return g_sms;
 }
 
-// Shared q arrays for a shape: fills a.union_mode / a.qstride; returns dynamic smem bytes.
-static size_t plan_smem(CompressArgs& a)
+// Shared q storage for a shape; fills a.union_mode / a.qstride / a.qwords and returns the
+// dynamic shared memory bytes.  vec: rings of R = 2^k >= 2048 + halo + 4 elements.
+static size_t plan_smem(CompressArgs& a, bool& vec)
 {
-    const uint32_t ndim = a.g.ndim;
-    uint32_t narr, len;
-    if (ndim == 1) {
-        narr = 1;
-        len = kTileCodes + 1;
-        a.union_mode = 0;
-    } else if (a.g.nx + 1 <= kUnionHaloMax) {
+    const uint32_t ndim = a.g.ndim, nx = a.g.nx;
+    const uint32_t halo = ndim >= 2 ? nx + 1 : 1;
+    vec = (ndim == 1 || (nx % 4) == 0) && (a.base % 4) == 0 && halo + kTileCodes + 4 <= 8192;
+    if (vec) {
+        uint32_t R = 1;
+        while (R < halo + kTileCodes + 4) R <<= 1;
         a.union_mode = 1;
-        narr = ndim == 3 ? 2 : 1;
-        len = kTileCodes + a.g.nx + 1;
+        a.qstride = R;
+        a.qwords = (ndim == 3 ? 2 : 1) * R;
     } else {
-        a.union_mode = 0;
-        narr = ndim == 3 ? 4 : 2;
-        len = kTileCodes + 1;
+        uint32_t narr, len;
+        if (ndim == 1) {
+            narr = 1;
+            len = kTileCodes + 1;
+            a.union_mode = 0;
+        } else if (nx + 1 <= kUnionHaloMax) {
+            a.union_mode = 1;
+            narr = ndim == 3 ? 2 : 1;
+            len = kTileCodes + nx + 1;
+        } else {
+            a.union_mode = 0;
+            narr = ndim == 3 ? 4 : 2;
+            len = kTileCodes + 1;
+        }
+        a.qstride = (pad_words(len) + 31) & ~31u;
+        a.qwords = narr * a.qstride;
     }
-    a.qstride = (pad_words(len) + 31) & ~31u;
-    return sizeof(int) * ((size_t)narr * a.qstride + 32 * 33 + 8) + 2 * 16 * (size_t)kUnitTiles * kTileBlocks;
+    a.qwords = (a.qwords + 3) & ~3u;
+    return sizeof(int) * ((size_t)a.qwords + 32 * 33 + 8) + 2 * 16 * (size_t)kStageBlocks;
 }
 
-template <int NDIM>
+template <int NDIM, bool VEC>
 static cudaError_t launch_compress_t(const CompressArgs& a, size_t sm, uint32_t ntiles, cudaStream_t st)
 {
-    cudaFuncSetAttribute(k_compress<NDIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_compress<NDIM, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compress<NDIM>, kCta, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compress<NDIM, VEC>, kCta, sm);
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)per_sm * num_sms();
     const uint32_t nunits = (ntiles + kUnitTiles - 1) / kUnitTiles;
     if (grid > nunits) grid = nunits;
     if (grid == 0) return cudaSuccess;
-    k_compress<NDIM><<<(unsigned)grid, kCta, sm, st>>>(a);
+    k_compress<NDIM, VEC><<<(unsigned)grid, kCta, sm, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int NDIM>
+static cudaError_t launch_compress_ws(const CompressArgs& a, size_t sm, uint32_t ntiles, cudaStream_t st)
+{
+    cudaFuncSetAttribute(k_compress_ws<NDIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compress_ws<NDIM>, kWsThreads, sm);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)per_sm * num_sms();
+    const uint32_t nunits = (ntiles + kUnitTiles - 1) / kUnitTiles;
+    if (grid > nunits) grid = nunits;
+    if (grid == 0) return cudaSuccess;
+    k_compress_ws<NDIM><<<(unsigned)grid, kWsThreads, sm, st>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_compress(const CompressArgs& a_in, cudaStream_t st)
 {
     CompressArgs a = a_in;
+    if (const char* e = getenv("FZ_EXP")) a.exp = atoi(e);
     a.dnx = make_fastdiv(a.g.nx);
     a.dP = make_fastdiv(a.g.P);
-    const size_t sm = plan_smem(a);
+    bool vec = false;
+    size_t sm = plan_smem(a, vec);
     const uint32_t ntiles = a.tile_end - a.tile_begin;
     LaunchProf lp(K_COMPRESS, st);
-    switch (a.g.ndim) {
-        case 1: return launch_compress_t<1>(a, sm, ntiles, st);
-        case 2: return launch_compress_t<2>(a, sm, ntiles, st);
-        default: return launch_compress_t<3>(a, sm, ntiles, st);
+    if (vec && !(a.exp & 16)) {
+        sm += 2 * 2 * kTileCodes * sizeof(float);   // TMA input stages
+        switch (a.g.ndim) {
+            case 1: return launch_compress_ws<1>(a, sm, ntiles, st);
+            case 2: return launch_compress_ws<2>(a, sm, ntiles, st);
+            default: return launch_compress_ws<3>(a, sm, ntiles, st);
+        }
+    }
+    switch (a.g.ndim * 2 + (vec ? 1 : 0)) {
+        case 2: return launch_compress_t<1, false>(a, sm, ntiles, st);
+        case 3: return launch_compress_t<1, true>(a, sm, ntiles, st);
+        case 4: return launch_compress_t<2, false>(a, sm, ntiles, st);
+        case 5: return launch_compress_t<2, true>(a, sm, ntiles, st);
+        case 6: return launch_compress_t<3, false>(a, sm, ntiles, st);
+        default: return launch_compress_t<3, true>(a, sm, ntiles, st);
     }
 }
 

@@ -28,12 +28,14 @@ struct Ctrl {
     // parameters (Appendix A), written by k_params or k_init
     fz_params p;
     float h;                         // w / 2
+    float hU;                        // fast-path threshold (see pq_fast)
     int32_t err;                     // fz_status of the device-side steps
     uint32_t ticket;                 // persistent-tile ticket
     uint32_t stage_overflow;         // outlier staging overflowed -> rescan pass
     // results (written by the last tile / k_finalize)
     unsigned long long nnz, nd, nv, total;
     unsigned long long dcount, vcount;   // outlier staging allocation counters (= totals)
+    unsigned long long dbg[4];           // FZ_EXP & 8: look-back tries / failures / blocking
 };
 static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 
@@ -163,61 +165,115 @@ constexpr unsigned long long kStTerm = 1ull << 61;
 // logic error can never hang the device (the caller reports FZ_ERR_CUDA).
 constexpr int32_t kErrStall = 100;
 
+// Window layout: entry (k, lane) is tile t-1-(32k + lane), i.e. distance 32k + lane: each
+// load instruction reads 32 consecutive status words (two 128-byte lines).
+template <int PER_LANE>
+__device__ __forceinline__ void lookback_load(const unsigned long long* st, int64_t hi, int64_t first,
+                                              unsigned long long (&v)[PER_LANE])
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < PER_LANE; ++k) {
+        const int64_t idx = hi - 32 * k - lane;
+        v[k] = idx >= first ? ld_relaxed_u64(st + idx) : kStInc;
+    }
+}
+
+// Evaluates one loaded window: returns 0 = an entry nearer than the nearest terminal is
+// unpublished (retry), 1 = terminal found (sum complete), 2 = no terminal (sum of the whole
+// window, continue with the next window).
+template <int PER_LANE, bool SEG>
+__device__ __forceinline__ int lookback_eval(const unsigned long long (&v)[PER_LANE], unsigned long long vmask,
+                                             unsigned long long& sum)
+{
+    const int lane = threadIdx.x & 31;
+    // nearest terminal: smallest k with one, lowest lane within it
+    int kt = PER_LANE;
+    uint32_t tmask = 0;
+#pragma unroll
+    for (int k = PER_LANE - 1; k >= 0; --k) {
+        const bool term = (v[k] >> 62) == 2 || (SEG && (v[k] & kStTerm));
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, term);
+        if (m) { kt = k; tmask = m; }
+    }
+    const int tl = kt < PER_LANE ? __ffs(tmask) - 1 : 0;
+    // every entry nearer than the terminal must be published
+    bool missing = false;
+#pragma unroll
+    for (int k = 0; k < PER_LANE; ++k) {
+        const bool nearer = k < kt || (k == kt && lane < tl);
+        if (nearer && (v[k] >> 62) == 0) missing = true;
+    }
+    if (__any_sync(0xFFFFFFFFu, missing)) return 0;
+    unsigned long long part = 0;
+#pragma unroll
+    for (int k = 0; k < PER_LANE; ++k) {
+        const bool take = k < kt || (k == kt && lane <= tl);
+        if (take) part += v[k] & vmask;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
+    sum = part;
+    return kt < PER_LANE ? 1 : 2;
+}
+
+// `pre` (optional) is the first window, loaded earlier by lookback_load(st, t-1, first, pre)
+// so that its latency overlaps other work.
 template <int PER_LANE, bool SEG>
 __device__ __forceinline__ unsigned long long lookback_wide(const unsigned long long* st, int64_t t,
                                                             int64_t first, unsigned long long vmask,
-                                                            int32_t* err)
+                                                            int32_t* err,
+                                                            const unsigned long long* pre = nullptr,
+                                                            unsigned long long* dbg = nullptr)
 {
     const int lane = threadIdx.x & 31;
     unsigned long long sum = 0;
     int64_t hi = t - 1;
     uint32_t spins = 0;
+    bool use_pre = pre != nullptr;
     while (hi >= first) {
         unsigned long long v[PER_LANE];
-        uint32_t termbits, zerobits;
         for (;;) {
             if (++spins > (1u << 22)) {
                 if (lane == 0) atomicExch(err, kErrStall);
                 return sum;
             }
-            termbits = 0;
-            zerobits = 0;
+            if (use_pre) {
 #pragma unroll
-            for (int k = 0; k < PER_LANE; ++k) {
-                const int64_t idx = hi - (int64_t)lane * PER_LANE - k;   // k = 0 nearest
-                unsigned long long s = kStInc;
-                if (idx >= first) s = ld_relaxed_u64(st + idx);
-                v[k] = s;
-                const bool term = (s >> 62) == 2 || (SEG && (s & kStTerm));
-                termbits |= (uint32_t)term << k;
-                zerobits |= (uint32_t)((s >> 62) == 0) << k;
+                for (int k = 0; k < PER_LANE; ++k) v[k] = pre[k];
+                use_pre = false;
+            } else {
+                lookback_load<PER_LANE>(st, hi, first, v);
+                if (dbg && lane == 0) atomicAdd(dbg, 1ull);
             }
-            // nearest terminal: lowest lane having one, lowest k inside that lane
-            const uint32_t lanes_t = __ballot_sync(0xFFFFFFFFu, termbits != 0);
-            const int tl = lanes_t ? __ffs(lanes_t) - 1 : 32;
-            // all entries nearer than the terminal must be published
-            uint32_t need = 0;
-            if (lane < tl) need = zerobits;
-            else if (lane == tl) need = zerobits & ((termbits & (0u - termbits)) - 1u);
-            if (__ballot_sync(0xFFFFFFFFu, need != 0) == 0) {
-                unsigned long long part = 0;
-                if (lane <= tl) {
-                    const int kmax = (lane == tl) ? __ffs(termbits) - 1 : PER_LANE - 1;
-#pragma unroll
-                    for (int k = 0; k < PER_LANE; ++k)
-                        if (k <= kmax) part += v[k] & vmask;
-                }
-#pragma unroll
-                for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
-                sum += part;
-                if (lanes_t) return sum;
-                break;
-            }
+            unsigned long long part;
+            const int r = lookback_eval<PER_LANE, SEG>(v, vmask, part);
+            if (r == 0) continue;
+            sum += part;
+            if (r == 1) return sum;
+            break;
         }
         hi -= 32 * PER_LANE;
+        use_pre = false;
     }
     return sum;
 }
+
+// Non-blocking attempt on a window loaded earlier (lookback_load(st, t-1, first, v)).
+template <int PER_LANE>
+__device__ __forceinline__ bool lookback_try(const unsigned long long* st, int64_t t, int64_t first,
+                                             unsigned long long vmask, int32_t* err,
+                                             const unsigned long long (&v)[PER_LANE], unsigned long long& out,
+                                             unsigned long long* dbg = nullptr)
+{
+    unsigned long long part;
+    const int r = lookback_eval<PER_LANE, false>(v, vmask, part);
+    if (r == 0) return false;
+    if (r == 2) part += lookback_wide<PER_LANE, false>(st, t - 32 * PER_LANE, first, vmask, err);
+    out = part;
+    return true;
+}
+
 
 // 16-byte streaming load of the read-only field.
 __device__ __forceinline__ float4 ldg_f4(const float* p)
@@ -273,7 +329,7 @@ __device__ __forceinline__ void transpose32_group8(uint32_t (&a)[4], int k)
 // Returns q; *vout = value outlier.
 // ------------------------------------------------------------------------------------
 struct QuantP {
-    float w, r, h, eb32;
+    float w, r, h, eb32, hU;
 };
 
 __device__ __forceinline__ int prequant(float d, const QuantP& P, bool& vout)
@@ -394,7 +450,8 @@ struct CompressArgs {
     // neighbour streams (SV §7 hard part 3): q of the element and of its y-1, z-1, (y-1,z-1)
     // neighbours live in shared arrays; union = [s-nx-1, e) and [s-P-nx-1, e-P)
     int union_mode;           // 1: one array per plane; 0: one 2049-element array per stream
-    uint32_t qstride;         // padded words per shared q array
+    uint32_t qstride;         // padded words per shared q array (vec: ring size, a power of 2)
+    uint32_t qwords;          // words of shared q storage before the shuffle buffer
     uint8_t* flags_out;       // 32 B per tile, tile t at (t - tile_begin) * 32
     uint8_t* payload_out;     // 16 B blocks
     uint64_t flags_cap;       // bytes writable at flags_out
@@ -413,6 +470,7 @@ struct CompressArgs {
     uint32_t* o_vidx;
     uint32_t* o_vbits;
     int rescan;               // 1: outliers only, straight to final offsets via opre
+    int exp;                  // performance experiments (FZ_EXP env var; 0 in production)
 };
 
 }  // namespace fz
