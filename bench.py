@@ -118,6 +118,7 @@ def algorithmic_bytes(kernel: str, n: int, stream_bytes: int, ndim: int):
         "k_decode_tiles": payload + 4 * n,
         "k_scan_sums": 4 * n,
         "k_scan_apply": 8 * n,
+        "k_scan_walk": 8 * n,
     }.get(kernel)
 
 

@@ -342,6 +342,36 @@ __global__ void k_scan_apply(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
     }
 }
 
+// Single-pass inclusive scan along L when there are many independent columns: one thread
+// per column walks L with 8 loads in flight (8 B/element of traffic instead of 12).
+__global__ void __launch_bounds__(256) k_scan_walk(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
+                                                   float dequant_w)
+{
+    const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= outer * W) return;
+    const uint64_t w = gid % W, o = gid / W;
+    int32_t* p = v + o * L * W + w;
+    uint32_t acc = 0;
+    uint64_t l = 0;
+    for (; l + 8 <= L; l += 8) {
+        uint32_t x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = (uint32_t)__ldcs(p + k * W);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            acc += x[k];
+            if (dequant_w > 0.0f) __stcs(reinterpret_cast<float*>(p + k * W), __fmul_rn(__int2float_rn((int32_t)acc), dequant_w));
+            else __stcs(p + k * W, (int32_t)acc);
+        }
+        p += 8 * W;
+    }
+    for (; l < L; ++l, p += W) {
+        acc += (uint32_t)*p;
+        if (dequant_w > 0.0f) *reinterpret_cast<float*>(p) = __fmul_rn(__int2float_rn((int32_t)acc), dequant_w);
+        else *p = (int32_t)acc;
+    }
+}
+
 __global__ void k_value_patch(float* out, const uint2* rec, uint64_t cnt, uint64_t n)
 {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
@@ -406,6 +436,11 @@ cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st)
 cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t W, uint32_t* sums,
                              float dequant_w, cudaStream_t st)
 {
+    if (outer * W >= 32768) {
+        LaunchProf lp(K_SCAN_APPLY, st);
+        k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, dequant_w);
+        return cudaGetLastError();
+    }
     const uint64_t nch = (L + kScanChunk - 1) / kScanChunk;
     const uint64_t work = outer * nch * W;
     {
