@@ -392,8 +392,11 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     if (work_bytes < L.total) return FZ_ERR_WORKSPACE;
     uint8_t* wb = static_cast<uint8_t*>(d_work);
     Ctrl* ctrl = reinterpret_cast<Ctrl*>(wb + L.ctrl);
-    auto* st_nnz = reinterpret_cast<unsigned long long*>(wb + L.st_nnz);
-    auto* st_x = reinterpret_cast<unsigned long long*>(wb + L.st_x);
+    auto* loc = reinterpret_cast<uint32_t*>(wb + L.loc);
+    auto* bsum = reinterpret_cast<uint32_t*>(wb + L.bsum);
+    auto* xagg = reinterpret_cast<uint2*>(wb + L.xagg);
+    auto* xloc = reinterpret_cast<uint2*>(wb + L.xloc);
+    auto* xbagg = reinterpret_cast<uint2*>(wb + L.xbagg);
     auto* sums = reinterpret_cast<uint32_t*>(wb + L.sums);
     const uint8_t* in = static_cast<const uint8_t*>(d_in);
     const uint64_t T = I.tiles;
@@ -405,9 +408,10 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     int32_t* q = d_q ? d_q : reinterpret_cast<int32_t*>(d_field);
     const bool deq = d_q == nullptr;
 
-    FZ_CUDA(launch_decode_init(ctrl, st_nnz, st_x, (uint32_t)T, st));
+    FZ_CUDA(launch_decode_init(ctrl, st));
     FZ_CUDA(launch_validate_outliers(drec, I.counts.n_delta, n, ctrl, st));
     FZ_CUDA(launch_validate_outliers(vrec, I.counts.n_value, n, ctrl, st));
+    FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st));
     DecodeArgs a{};
     a.flags = in + kHeaderBytes;
     a.payload = in + pbase;
@@ -416,13 +420,21 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     a.nd = I.counts.n_delta;
     a.g = g;
     a.tiles = (uint32_t)T;
-    a.w = I.params.w;
+    a.w = deq ? I.params.w : 0.0f;
     a.q_out = q;
-    a.x_out = (deq && I.shape.ndim == 1) ? d_field : nullptr;
-    a.st_nnz = st_nnz;
-    a.st_x = st_x;
+    a.loc = loc;
+    a.bpre = bsum;
+    a.xagg = xagg;
     a.ctrl = ctrl;
     FZ_CUDA(launch_decode_tiles(a, st));
+    // x carries exist when some tile starts inside a row (always for 1-D fields)
+    const bool carries = T > 1 && (g.ndim == 1 || !(g.nx <= kTileCodes && kTileCodes % g.nx == 0));
+    if (g.ndim == 1 && !deq) a.w = 0.0f;
+    if (g.ndim == 1 && !deq) {
+        if (carries) FZ_CUDA(launch_xcarry(a, xloc, xbagg, true, st));
+    } else {
+        FZ_CUDA(launch_xcarry(a, xloc, xbagg, carries, st));
+    }
     const float wq = deq ? I.params.w : 0.0f;
     if (I.shape.ndim == 2) {
         FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1], sums, wq, st));
@@ -549,7 +561,7 @@ const char* fz_kernel_name(int id)
     static const char* names[] = {"k_init", "k_range", "k_params", "k_compress", "k_finalize",
                                   "k_decode_init", "k_validate_outliers", "k_decode_tiles",
                                   "k_scan_sums", "k_scan_chunks", "k_scan_apply", "k_value_patch",
-                                  "k_outliers"};
+                                  "k_outliers", "k_tile_offsets", "k_xcarry"};
     return (id >= 0 && id < fz::K_COUNT) ? names[id] : "?";
 }
 

@@ -15,6 +15,8 @@ namespace fz {
 
 constexpr int kScanChunk = 32;
 
+// Decode workspace: control block, per-tile block offsets (two-level exclusive scan of the
+// flag popcounts), per-tile x-scan aggregates and carries, chunk sums of the axis scans.
 DecodeLayout decode_layout(const fz_shape& s)
 {
     DecodeLayout L{};
@@ -25,6 +27,7 @@ DecodeLayout decode_layout(const fz_shape& s)
     else if (s.ndim == 2) { ny = d[0]; nx = d[1]; }
     else { nz = d[0]; ny = d[1]; nx = d[2]; }
     const uint64_t n = nz * ny * nx, T = (n + kTileCodes - 1) / kTileCodes;
+    const uint64_t nb = (T + 1023) / 1024;
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const uint64_t ych = (ny + kScanChunk - 1) / kScanChunk, zch = (nz + kScanChunk - 1) / kScanChunk;
     uint64_t sums = 0;
@@ -32,22 +35,21 @@ DecodeLayout decode_layout(const fz_shape& s)
     if (s.ndim == 3 && zch * ny * nx > sums) sums = zch * ny * nx;
     size_t off = 0;
     L.ctrl = off;   off += 512;
-    L.st_nnz = off; off = al(off + 8 * T);
-    L.st_x = off;   off = al(off + 8 * T);
+    L.loc = off;    off = al(off + 4 * T);
+    L.bsum = off;   off = al(off + 4 * nb);
+    L.xagg = off;   off = al(off + 8 * T);
+    L.xloc = off;   off = al(off + 8 * T);
+    L.xbagg = off;  off = al(off + 8 * nb);
     L.sums = off;   off = al(off + 4 * sums);
     L.sums_elems = sums;
     L.total = off;
     return L;
 }
 
-__global__ void k_decode_init(Ctrl* ctrl, unsigned long long* st_nnz, unsigned long long* st_x,
-                              uint32_t ntiles)
+__global__ void k_decode_init(Ctrl* ctrl)
 {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    for (uint32_t k = i; k < ntiles; k += gridDim.x * blockDim.x) { st_nnz[k] = 0; st_x[k] = 0; }
-    if (i == 0) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
         ctrl->err = 0;
-        ctrl->ticket = 0;
         ctrl->nnz = 0;
     }
 }
@@ -71,222 +73,334 @@ __device__ __forceinline__ Seg seg_combine(Seg e, Seg l)
     return l.f ? l : Seg{e.f, e.v + l.v};
 }
 
+// Block-wide (1024 threads) exclusive scans: plain sums and segmented sums.
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t x, uint32_t& total, uint32_t* wsum)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = wsum[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, wi, o);
+            if (lane >= o) wi += y;
+        }
+        wsum[lane] = wi - w;          // exclusive warp prefix
+        if (lane == 31) wsum[32] = wi;
+    }
+    __syncthreads();
+    total = wsum[32];
+    const uint32_t r = wsum[warp] + inc - x;
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ Seg block_excl_seg(Seg x, Seg& total, uint32_t* wf, uint32_t* wv)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Seg inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const Seg y{__shfl_up_sync(kFull, inc.f, o), __shfl_up_sync(kFull, inc.v, o)};
+        if (lane >= o) inc = seg_combine(y, inc);
+    }
+    Seg ex{__shfl_up_sync(kFull, inc.f, 1), __shfl_up_sync(kFull, inc.v, 1)};
+    if (lane == 0) ex = Seg{0, 0};
+    if (lane == 31) { wf[warp] = inc.f; wv[warp] = inc.v; }
+    __syncthreads();
+    if (warp == 0) {
+        const Seg w{wf[lane], wv[lane]};
+        Seg wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const Seg y{__shfl_up_sync(kFull, wi.f, o), __shfl_up_sync(kFull, wi.v, o)};
+            if (lane >= o) wi = seg_combine(y, wi);
+        }
+        Seg we{__shfl_up_sync(kFull, wi.f, 1), __shfl_up_sync(kFull, wi.v, 1)};
+        if (lane == 0) we = Seg{0, 0};
+        __syncwarp();
+        wf[lane] = we.f;
+        wv[lane] = we.v;
+        if (lane == 31) { wf[32] = wi.f; wv[32] = wi.v; }
+    }
+    __syncthreads();
+    total = Seg{wf[32], wv[32]};
+    const Seg r = seg_combine(Seg{wf[warp], wv[warp]}, ex);
+    __syncthreads();
+    return r;
+}
+
+// D1 part 1: per-tile nonzero-block counts (popcount of the 8 flag words), exclusive scan
+// inside blocks of 1024 tiles; block totals in bsum.
+__global__ void __launch_bounds__(1024) k_nnz_block(const uint32_t* __restrict__ flags, uint32_t ntiles,
+                                                    uint32_t* loc, uint32_t* bsum)
+{
+    __shared__ uint32_t wsum[33];
+    const uint32_t t = blockIdx.x * 1024 + threadIdx.x;
+    uint32_t c = 0;
+    if (t < ntiles) {
+        const uint4 a = reinterpret_cast<const uint4*>(flags)[2 * (uint64_t)t];
+        const uint4 b = reinterpret_cast<const uint4*>(flags)[2 * (uint64_t)t + 1];
+        c = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) + __popc(b.z) +
+            __popc(b.w);
+    }
+    uint32_t total;
+    const uint32_t ex = block_excl_sum(c, total, wsum);
+    if (t < ntiles) loc[t] = ex;
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+// D1 part 2: exclusive scan of the block totals (one block), grand total -> ctrl->nnz.
+__global__ void __launch_bounds__(1024) k_nnz_top(uint32_t* bsum, uint32_t nb, Ctrl* ctrl)
+{
+    __shared__ uint32_t wsum[33];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < nb; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t x = i < nb ? bsum[i] : 0u;
+        uint32_t total;
+        const uint32_t ex = block_excl_sum(x, total, wsum);
+        if (i < nb) bsum[i] = (uint32_t)(carry + ex);
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ctrl->nnz = carry;
+}
+
+// x carries: segmented exclusive scan of the per-tile x aggregates (only when some tile
+// starts inside a row).
+__global__ void __launch_bounds__(1024) k_xseg_block(const uint2* xagg, uint32_t ntiles, uint2* xloc, uint2* xbagg)
+{
+    __shared__ uint32_t wf[33], wv[33];
+    const uint32_t t = blockIdx.x * 1024 + threadIdx.x;
+    const uint2 g = t < ntiles ? xagg[t] : make_uint2(0, 0);
+    Seg total;
+    const Seg ex = block_excl_seg(Seg{g.x, g.y}, total, wf, wv);
+    if (t < ntiles) xloc[t] = make_uint2(ex.f, ex.v);
+    if (threadIdx.x == 0) xbagg[blockIdx.x] = make_uint2(total.f, total.v);
+}
+
+__global__ void __launch_bounds__(1024) k_xseg_top(uint2* xbagg, uint32_t nb)
+{
+    __shared__ uint32_t wf[33], wv[33];
+    __shared__ uint32_t cf, cv;
+    if (threadIdx.x == 0) { cf = 0; cv = 0; }
+    __syncthreads();
+    for (uint32_t base = 0; base < nb; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint2 g = i < nb ? xbagg[i] : make_uint2(0, 0);
+        Seg total;
+        const Seg ex = block_excl_seg(Seg{g.x, g.y}, total, wf, wv);
+        const Seg c{cf, cv};
+        if (i < nb) {
+            const Seg r = seg_combine(c, ex);
+            xbagg[i] = make_uint2(r.f, r.v);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const Seg r = seg_combine(c, total);
+            cf = r.f;
+            cv = r.v;
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------------------------
-// Tile decoder, a 3-stage software pipeline per CTA (tiles from a ticket):
-//   stage 1 (tile t)  : read its 8 flag words, publish its block count (aggregate);
-//   stage 2 (tile t1) : payload offset by wide look-back, gather the 16-byte blocks (D2),
-//                       un-shuffle (D3), unpack + delta patch (D4), local segmented x-scan,
-//                       publish the x aggregate (a tile holding a row start is terminal);
-//   stage 3 (tile t2) : x carry by wide look-back, final x-scanned q written (D5 along x;
-//                       1-D fields are dequantized here, D6).
-// Each look-back targets a tile whose predecessors have had a whole iteration to publish.
+// Tile decoder (D2-D4 + the local part of D5 along x).  Tiles are independent: the payload
+// offset of tile t is bsum[t/1024] + loc[t].  Per tile: gather the nonzero 16-byte blocks,
+// un-shuffle (same 32x32 bit transpose), unpack (0x8000 -> 0), delta patch, segmented
+// inclusive x-scan inside the tile (resets at row starts), write q, publish the tile's
+// aggregate (row start seen, sum since the last row start) for the x carries.
 // ------------------------------------------------------------------------------------
 template <int NDIM>
 __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
 {
     __shared__ uint32_t Obuf[32 * 33];
     __shared__ int32_t D[kTileCodes];
-    __shared__ uint32_t s_tile[2], s_F[2][8], s_tnnz[2], s_wf[8], s_wv[8];
-    __shared__ unsigned long long s_off;
-    __shared__ uint32_t s_carry;
-    __shared__ uint32_t s_tagf[2], s_tagv[2];
+    __shared__ uint32_t s_F[8], s_wf[8], s_wv[8];
     __shared__ uint64_t s_lo, s_hi;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    Ctrl* ctrl = a.ctrl;
-    if (ctrl->err != 0) return;
     const uint32_t n = a.g.n, nx = a.g.nx;
-    constexpr uint32_t NONE = 0xFFFFFFFFu;
-
-    if (tid == 0) s_tile[0] = atomicAdd(&ctrl->ticket, 1u);
-    __syncthreads();
-    uint32_t t1 = NONE, t2 = NONE;
-    // stage-3 state of tile t2, per thread
-    uint32_t loc2[8];
-    uint32_t rmask2 = 0;
-    Seg wp2{0, 0}, lx2{0, 0};
-#pragma unroll
-    for (int u = 0; u < 8; ++u) loc2[u] = 0;
-
-    for (int it = 0;; ++it) {
-        const int cur = it & 1;
-        const uint32_t t = s_tile[cur];
-        const bool work = t < a.tiles;
-        if (!work && t1 == NONE && t2 == NONE) break;
-
-        // ---- stage 1: flags of tile t ----
-        if (work && lane == 0) s_F[cur][warp] = reinterpret_cast<const uint32_t*>(a.flags)[8 * (uint64_t)t + warp];
-        __syncthreads();
-        if (tid == 0) s_tile[cur ^ 1] = work ? atomicAdd(&ctrl->ticket, 1u) : NONE;
-        if (warp == 0) {
-            if (work) {
-                uint32_t tn = 0;
-#pragma unroll
-                for (int w = 0; w < 8; ++w) tn += __popc(s_F[cur][w]);
-                if (lane == 0) {
-                    s_tnnz[cur] = tn;
-                    st_relaxed_u64(&a.st_nnz[t], (t == 0 ? kStInc : kStAgg) | tn);
-                }
-            }
-            if (t1 != NONE) {
-                unsigned long long ex = 0;
-                if (t1 != 0) {
-                    ex = lookback_wide<8, false>(a.st_nnz, t1, 0, kStAgg - 1, &ctrl->err);
-                    if (lane == 0) st_relaxed_u64(&a.st_nnz[t1], kStInc | (ex + s_tnnz[cur ^ 1]));
-                }
-                if (lane == 0) {
-                    s_off = ex;
-                    if (t1 == a.tiles - 1) ctrl->nnz = ex + s_tnnz[cur ^ 1];
-                }
-            }
-        }
-        if (tid == 32 && t1 != NONE) {
+    for (uint32_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+        const int64_t s = (int64_t)t * kTileCodes;
+        const uint32_t g0 = (uint32_t)s + 8u * tid;
+        // ---- D1/D2: offsets, gather block b = tid into the shuffled tile O ----
+        const uint32_t F = reinterpret_cast<const uint32_t*>(a.flags)[8 * (uint64_t)t + warp];
+        if (lane == 0) s_F[warp] = F;
+        if (tid == 32) {
             uint64_t lo = 0, hi = 0;
             if (a.nd > 0) {
-                const int64_t s1 = (int64_t)t1 * kTileCodes;
                 uint64_t l = 0, h = a.nd;
-                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < s1) l = m + 1; else h = m; }
+                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < s) l = m + 1; else h = m; }
                 lo = l;
                 h = a.nd;
-                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < s1 + kTileCodes) l = m + 1; else h = m; }
+                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < s + kTileCodes) l = m + 1; else h = m; }
                 hi = l;
             }
             s_lo = lo;
             s_hi = hi;
         }
         __syncthreads();
-
-        // ---- stage 2: decode tile t1 ----
-        uint32_t loc[8];
-        uint32_t rmask = 0;
-        Seg wp{0, 0}, lex{0, 0};
-        if (t1 != NONE) {
-            const int64_t s1 = (int64_t)t1 * kTileCodes;
-            const uint32_t g0 = (uint32_t)s1 + 8u * tid;
-            {
-                const uint32_t F = s_F[cur ^ 1][warp];
-                uint32_t wpre = 0;
+        {
+            uint32_t wpre = 0;
 #pragma unroll
-                for (int w = 0; w < 8; ++w)
-                    if (w < warp) wpre += __popc(s_F[cur ^ 1][w]);
-                uint4 blk = make_uint4(0, 0, 0, 0);
-                if ((F >> lane) & 1u) {
-                    const uint64_t bi = s_off + wpre + __popc(F & ((1u << lane) - 1u));
-                    if (bi < a.nnz_total) blk = reinterpret_cast<const uint4*>(a.payload)[bi];
-                    else atomicExch(&ctrl->err, (int)FZ_ERR_CORRUPT);
-                }
-                uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
-                row[0] = blk.x; row[1] = blk.y; row[2] = blk.z; row[3] = blk.w;
+            for (int w = 0; w < 8; ++w)
+                if (w < warp) wpre += __popc(s_F[w]);
+            uint4 blk = make_uint4(0, 0, 0, 0);
+            if ((F >> lane) & 1u) {
+                const uint64_t bi = (uint64_t)a.bpre[t >> 10] + a.loc[t] + wpre + __popc(F & ((1u << lane) - 1u));
+                if (bi < a.nnz_total) blk = reinterpret_cast<const uint4*>(a.payload)[bi];
+                else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
+            }
+            uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+            row[0] = blk.x; row[1] = blk.y; row[2] = blk.z; row[3] = blk.w;
+        }
+        __syncthreads();
+        // ---- D3: column c of O -> row c of A ----
+        uint32_t w4[4];
+        {
+            const int c = tid >> 3, kk = tid & 7;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w4[i] = Obuf[(4 * kk + i) * 33 + c];
+            transpose32_group8(w4, lane & 7);
+        }
+        // ---- D4: unpack, delta outliers ----
+        int32_t dl[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t lo16 = w4[i] & 0xFFFFu, hi16 = w4[i] >> 16;
+            dl[2 * i] = (lo16 & 0x8000u) ? -(int32_t)(lo16 & 0x7FFFu) : (int32_t)lo16;
+            dl[2 * i + 1] = (hi16 & 0x8000u) ? -(int32_t)(hi16 & 0x7FFFu) : (int32_t)hi16;
+        }
+        if (s_hi > s_lo) {   // rare, block-uniform
+#pragma unroll
+            for (int u = 0; u < 8; ++u) D[8 * tid + u] = dl[u];
+            __syncthreads();
+            for (uint64_t k = s_lo + tid; k < s_hi; k += kCta) {
+                const uint2 r = a.drec[k];
+                D[r.x - (uint32_t)s] = (int32_t)r.y;
             }
             __syncthreads();
-            // D3: column c of O -> row c of A (the same 32x32 bit transpose)
-            uint32_t w4[4];
-            {
-                const int c = tid >> 3, kk = tid & 7;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) w4[i] = Obuf[(4 * kk + i) * 33 + c];
-                transpose32_group8(w4, lane & 7);
+            for (int u = 0; u < 8; ++u) dl[u] = D[8 * tid + u];
+        }
+        // ---- D5 (x, local): segmented inclusive scan, resets at row starts ----
+        uint32_t loc[8];
+        Seg me{0, 0};
+        if (nx >= 8) {
+            uint32_t x = fmod_(g0, a.dnx);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (x == 0) { me.f = 1; me.v = 0; }
+                me.v += (uint32_t)dl[u];
+                loc[u] = me.v;
+                if (++x == nx) x = 0;
             }
-            // D4: unpack (0x8000 -> 0, R8), delta outliers
-            int32_t dl[8];
+        } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t lo16 = w4[i] & 0xFFFFu, hi16 = w4[i] >> 16;
-                dl[2 * i] = (lo16 & 0x8000u) ? -(int32_t)(lo16 & 0x7FFFu) : (int32_t)lo16;
-                dl[2 * i + 1] = (hi16 & 0x8000u) ? -(int32_t)(hi16 & 0x7FFFu) : (int32_t)hi16;
+            for (int u = 0; u < 8; ++u) {
+                if (fmod_(g0 + u, a.dnx) == 0) { me.f = 1; me.v = 0; }
+                me.v += (uint32_t)dl[u];
+                loc[u] = me.v;
             }
-            if (s_hi > s_lo) {   // rare, block-uniform
+        }
+        Seg inc = me;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) D[8 * tid + u] = dl[u];
-                __syncthreads();
-                for (uint64_t k = s_lo + tid; k < s_hi; k += kCta) {
-                    const uint2 r = a.drec[k];
-                    D[r.x - (uint32_t)s1] = (int32_t)r.y;
-                }
-                __syncthreads();
+        for (int o = 1; o < 32; o <<= 1) {
+            const Seg up{__shfl_up_sync(kFull, inc.f, o), __shfl_up_sync(kFull, inc.v, o)};
+            if (lane >= o) inc = seg_combine(up, inc);
+        }
+        Seg lex{__shfl_up_sync(kFull, inc.f, 1), __shfl_up_sync(kFull, inc.v, 1)};
+        if (lane == 0) lex = Seg{0, 0};
+        if (lane == 31) { s_wf[warp] = inc.f; s_wv[warp] = inc.v; }
+        __syncthreads();
+        Seg wp{0, 0}, tagg{0, 0};
 #pragma unroll
-                for (int u = 0; u < 8; ++u) dl[u] = D[8 * tid + u];
-            }
-            // local segmented inclusive x-scan, resets at row starts (x == 0)
-            Seg me{0, 0};
+        for (int w = 0; w < 8; ++w) {
+            const Seg sw{s_wf[w], s_wv[w]};
+            if (w < warp) wp = seg_combine(wp, sw);
+            tagg = seg_combine(tagg, sw);
+        }
+        if (tid == 0) a.xagg[t] = make_uint2(tagg.f, tagg.v);
+        // values before the thread's first row start get the in-tile prefix (the carry from
+        // earlier tiles is added by k_xfix where needed)
+        const Seg acc = seg_combine(wp, lex);
+        uint32_t q[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) q[u] = loc[u];
+        {
+            // recompute "row start at or before u inside this thread"
+            uint32_t rs = 0;
             if (nx >= 8) {
                 uint32_t x = fmod_(g0, a.dnx);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    if (x == 0) { me.f = 1; me.v = 0; }
-                    me.v += (uint32_t)dl[u];
-                    loc[u] = me.v;
-                    if (me.f) rmask |= 1u << u;
+                    if (x == 0) rs = 1;
+                    if (!rs) q[u] = acc.v + loc[u];
                     if (++x == nx) x = 0;
                 }
             } else {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    if (fmod_(g0 + u, a.dnx) == 0) { me.f = 1; me.v = 0; }
-                    me.v += (uint32_t)dl[u];
-                    loc[u] = me.v;
-                    if (me.f) rmask |= 1u << u;
+                    if (fmod_(g0 + u, a.dnx) == 0) rs = 1;
+                    if (!rs) q[u] = acc.v + loc[u];
                 }
             }
-            Seg inc = me;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const Seg up{__shfl_up_sync(kFull, inc.f, o), __shfl_up_sync(kFull, inc.v, o)};
-                if (lane >= o) inc = seg_combine(up, inc);
-            }
-            lex = Seg{__shfl_up_sync(kFull, inc.f, 1), __shfl_up_sync(kFull, inc.v, 1)};
-            if (lane == 0) lex = Seg{0, 0};
-            if (lane == 31) { s_wf[warp] = inc.f; s_wv[warp] = inc.v; }
-            __syncthreads();
-            Seg tagg{0, 0};
-#pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                const Seg sw{s_wf[w], s_wv[w]};
-                if (w < warp) wp = seg_combine(wp, sw);
-                tagg = seg_combine(tagg, sw);
-            }
-            if (tid == 0) {
-                s_tagf[cur] = tagg.f;
-                s_tagv[cur] = tagg.v;
-                // a row start inside the tile makes its value carry-independent: terminal
-                st_relaxed_u64(&a.st_x[t1], ((tagg.f || t1 == 0) ? kStInc : kStAgg) | tagg.v);
-            }
         }
-
-        // ---- stage 3: x carry of tile t2 ----
-        if (warp == 0 && t2 != NONE) {
-            uint32_t carry = 0;
-            if (t2 != 0) {
-                carry = (uint32_t)lookback_wide<8, false>(a.st_x, t2, 0, 0xFFFFFFFFull, &ctrl->err);
-                if (lane == 0 && !s_tagf[cur ^ 1])
-                    st_relaxed_u64(&a.st_x[t2], kStInc | (uint32_t)(carry + s_tagv[cur ^ 1]));
-            }
-            if (lane == 0) s_carry = carry;
+        if (s + kTileCodes <= (int64_t)n) {
+            int4* o = reinterpret_cast<int4*>(a.q_out + g0);
+            o[0] = make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]);
+            o[1] = make_int4((int)q[4], (int)q[5], (int)q[6], (int)q[7]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (g0 + u < n) a.q_out[g0 + u] = (int32_t)q[u];
         }
         __syncthreads();
-        if (t2 != NONE) {
-            const int64_t s2 = (int64_t)t2 * kTileCodes;
-            Seg acc{0, s_carry};
-            acc = seg_combine(acc, wp2);
-            acc = seg_combine(acc, lx2);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int64_t g = s2 + 8 * tid + u;
-                if (g < (int64_t)n) {
-                    const uint32_t qv = ((rmask2 >> u) & 1u) ? loc2[u] : acc.v + loc2[u];
-                    if (NDIM == 1 && a.x_out != nullptr) a.x_out[g] = __fmul_rn(__int2float_rn((int32_t)qv), a.w);
-                    else a.q_out[g] = (int32_t)qv;
-                }
+    }
+}
+
+// x carries into the elements of a tile whose row began in an earlier tile; 1-D fields are
+// dequantized here (D6).  One CTA per tile.
+template <int NDIM>
+__global__ void __launch_bounds__(kCta) k_xfix(int32_t* q, const uint2* xloc, const uint2* xbpre, uint32_t ntiles,
+                                               uint32_t n, uint32_t nx, float w, int carries)
+{
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t s = (uint64_t)t * kTileCodes;
+        uint32_t carry = 0;
+        if (carries) {
+            const uint2 b = xbpre[t >> 10], l = xloc[t];
+            carry = seg_combine(Seg{b.x, b.y}, Seg{l.x, l.y}).v;
+        }
+        uint64_t e = s + kTileCodes;
+        if (e > n) e = n;
+        uint64_t r0 = e;           // first row start at or after s
+        if (NDIM != 1) {
+            const uint64_t rr = (s + nx - 1) / nx * nx;
+            if (rr < r0) r0 = rr;
+        } else if (s == 0) {
+            r0 = 0;
+        }
+        if (NDIM == 1 && w > 0.0f) {
+            for (uint64_t g = s + threadIdx.x; g < e; g += kCta) {
+                const uint32_t v = (uint32_t)q[g] + (g < r0 ? carry : 0u);
+                reinterpret_cast<float*>(q)[g] = __fmul_rn(__int2float_rn((int32_t)v), w);
             }
+        } else if (carry != 0) {
+            for (uint64_t g = s + threadIdx.x; g < r0; g += kCta) q[g] = (int32_t)((uint32_t)q[g] + carry);
         }
-        t2 = t1;
-        if (t1 != NONE) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) loc2[u] = loc[u];
-            rmask2 = rmask;
-            wp2 = wp;
-            lx2 = lex;
-        }
-        t1 = work ? t : NONE;
     }
 }
 
@@ -391,11 +505,10 @@ static unsigned grid_for(uint64_t work, int per_thread = 1)
     return (unsigned)g;
 }
 
-cudaError_t launch_decode_init(Ctrl* ctrl, unsigned long long* st_nnz, unsigned long long* st_x,
-                               uint32_t ntiles, cudaStream_t st)
+cudaError_t launch_decode_init(Ctrl* ctrl, cudaStream_t st)
 {
     LaunchProf lp(K_DINIT, st);
-    k_decode_init<<<grid_for(ntiles), 256, 0, st>>>(ctrl, st_nnz, st_x, ntiles);
+    k_decode_init<<<1, 32, 0, st>>>(ctrl);
     return cudaGetLastError();
 }
 
@@ -405,6 +518,21 @@ cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n,
     if (cnt == 0) return cudaSuccess;
     LaunchProf lp(K_VALIDATE, st);
     k_validate_outliers<<<grid_for(cnt), 256, 0, st>>>(rec, cnt, n, ctrl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum, Ctrl* ctrl,
+                                cudaStream_t st)
+{
+    const uint32_t nb = (ntiles + 1023) / 1024;
+    {
+        LaunchProf lp(K_OFFSETS, st);
+        k_nnz_block<<<nb, 1024, 0, st>>>(reinterpret_cast<const uint32_t*>(flags), ntiles, loc, bsum);
+    }
+    {
+        LaunchProf lp(K_OFFSETS, st);
+        k_nnz_top<<<1, 1024, 0, st>>>(bsum, nb, ctrl);
+    }
     return cudaGetLastError();
 }
 
@@ -431,6 +559,30 @@ cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st)
         case 2: return launch_decode_t<2>(a, st);
         default: return launch_decode_t<3>(a, st);
     }
+}
+
+cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool carries, cudaStream_t st)
+{
+    const uint32_t nb = (a.tiles + 1023) / 1024;
+    if (carries) {
+        {
+            LaunchProf lp(K_XCARRY, st);
+            k_xseg_block<<<nb, 1024, 0, st>>>(a.xagg, a.tiles, xloc, xbagg);
+        }
+        {
+            LaunchProf lp(K_XCARRY, st);
+            k_xseg_top<<<1, 1024, 0, st>>>(xbagg, nb);
+        }
+    }
+    if (!carries && a.g.ndim != 1) return cudaGetLastError();
+    unsigned grid = a.tiles < (uint32_t)num_sms() * 8 ? a.tiles : num_sms() * 8;
+    LaunchProf lp(K_XCARRY, st);
+    switch (a.g.ndim) {
+        case 1: k_xfix<1><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries); break;
+        case 2: k_xfix<2><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries); break;
+        default: k_xfix<3><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries); break;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t W, uint32_t* sums,

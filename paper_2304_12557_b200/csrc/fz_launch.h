@@ -12,7 +12,7 @@ int num_sms();
 // Kernel kinds for launch accounting and per-kernel CUDA-event timing (fz_profile_*).
 enum KernelId {
     K_INIT = 0, K_RANGE, K_PARAMS, K_COMPRESS, K_FINALIZE, K_DINIT, K_VALIDATE, K_DECODE,
-    K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_COUNT
+    K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_COUNT
 };
 
 // Counts one launch of `id` and, when profiling is on, brackets it with CUDA events on the
@@ -50,24 +50,26 @@ struct DecodeArgs {
     FastDiv dnx;
     uint32_t tiles;
     float w;
-    int32_t* q_out;             // integer codes (2-D/3-D), aliases the output field
-    float* x_out;               // 1-D: dequantized directly
-    unsigned long long* st_nnz; // look-back status, payload offsets
-    unsigned long long* st_x;   // look-back status, segmented x-scan carry
+    int32_t* q_out;             // integer codes (aliases the output field)
+    const uint32_t* loc;        // per-tile block offset inside its group of 1024 tiles
+    const uint32_t* bpre;       // exclusive block offset of each group of 1024 tiles
+    uint2* xagg;                // per-tile x-scan aggregate (row start seen, sum)
     Ctrl* ctrl;
 };
 
 struct DecodeLayout {
-    size_t ctrl, st_nnz, st_x, sums, total;
+    size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, total;
     uint64_t sums_elems;
 };
 DecodeLayout decode_layout(const fz_shape& s);
 
-cudaError_t launch_decode_init(Ctrl* ctrl, unsigned long long* st_nnz, unsigned long long* st_x,
-                               uint32_t ntiles, cudaStream_t st);
+cudaError_t launch_decode_init(Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, Ctrl* ctrl,
                                      cudaStream_t st);
+cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum,
+                                Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st);
+cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool carries, cudaStream_t st);
 // inclusive prefix sum along an axis of a [outer][L][W] int32 array (mod 2^32); when
 // dequant_w > 0 the final values are written as fl32(fl32(q) * w) floats in place.
 cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t W,
