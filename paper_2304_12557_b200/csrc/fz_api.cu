@@ -561,7 +561,7 @@ const char* fz_kernel_name(int id)
     static const char* names[] = {"k_init", "k_range", "k_params", "k_compress", "k_finalize",
                                   "k_decode_init", "k_validate_outliers", "k_decode_tiles",
                                   "k_scan_sums", "k_scan_chunks", "k_scan_apply", "k_value_patch",
-                                  "k_outliers", "k_tile_offsets", "k_xcarry"};
+                                  "k_outliers", "k_tile_offsets", "k_xcarry", "k_slab"};
     return (id >= 0 && id < fz::K_COUNT) ? names[id] : "?";
 }
 
@@ -706,6 +706,132 @@ fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_pa
     d.vidx = d_vidx;
     d.vbits = d_vbits;
     return place_outliers(W, a, h, d, st);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// Slab decompression (multi-GPU, plane-aligned z-slabs)
+// ---------------------------------------------------------------------------------------
+namespace {
+struct SlabGeo {
+    fz_shape local;     // the slab as a standalone field
+    uint64_t n, g0;     // local elements, global index of local element 0
+    uint64_t L, W;      // slowest-axis length and the aggregate width
+};
+
+fz_status slab_geo(const fz_shape* global, uint64_t tb, uint64_t te, SlabGeo* sg)
+{
+    uint64_t n;
+    if (!shape_n(global, &n)) return FZ_ERR_ARG;
+    const uint64_t T = tiles_of(n);
+    if (te <= tb || te > T) return FZ_ERR_ARG;
+    const uint64_t g0 = tb * kTileCodes, g1 = te * kTileCodes < n ? te * kTileCodes : n;
+    const Geom g = geom_of(*global, n);
+    const uint64_t unit = global->ndim == 3 ? g.P : (global->ndim == 2 ? g.nx : 1);
+    if (g0 % unit != 0 || (g1 != n && g1 % unit != 0)) return FZ_ERR_ARG;   // not plane-aligned
+    SlabGeo r{};
+    r.n = g1 - g0;
+    r.g0 = g0;
+    r.local = *global;
+    r.local.dims[0] = r.n / unit;
+    r.L = r.local.dims[0];
+    r.W = unit;
+    *sg = r;
+    return FZ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+uint64_t fz_slab_agg_elems(const fz_shape* global)
+{
+    uint64_t n;
+    if (!shape_n(global, &n)) return 0;
+    const Geom g = geom_of(*global, n);
+    return global->ndim == 3 ? g.P : (global->ndim == 2 ? g.nx : 1);
+}
+
+fz_status fz_slab_decode(const void* d_stage, const fz_counts* local, const fz_shape* global, uint64_t tb,
+                         uint64_t te, int32_t* d_q, int32_t* d_agg, void* d_work, size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    SlabGeo sg;
+    if (d_stage == nullptr || local == nullptr || d_q == nullptr || d_agg == nullptr || d_work == nullptr ||
+        !aligned16(d_stage) || !aligned16(d_q) || !aligned16(d_work))
+        return FZ_ERR_ARG;
+    fz_status rs = slab_geo(global, tb, te, &sg);
+    if (rs != FZ_OK) return rs;
+    const DecodeLayout L = decode_layout(sg.local);
+    if (work_bytes < L.total) return FZ_ERR_WORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* wb = static_cast<uint8_t*>(d_work);
+    Ctrl* ctrl = reinterpret_cast<Ctrl*>(wb + L.ctrl);
+    const uint64_t nt = te - tb;
+    const uint8_t* in = static_cast<const uint8_t*>(d_stage);
+    const uint64_t pbase = 32 * nt, dbase = pbase + 16 * local->nnz;
+    const Geom g = geom_of(sg.local, sg.n);
+    FZ_CUDA(launch_decode_init(ctrl, st));
+    FZ_CUDA(launch_tile_offsets(in, (uint32_t)nt, reinterpret_cast<uint32_t*>(wb + L.loc),
+                                reinterpret_cast<uint32_t*>(wb + L.bsum), ctrl, st));
+    DecodeArgs a{};
+    a.flags = in;
+    a.payload = in + pbase;
+    a.drec = reinterpret_cast<const uint2*>(in + dbase);
+    a.nnz_total = local->nnz;
+    a.nd = local->n_delta;
+    a.g = g;
+    a.tiles = (uint32_t)nt;
+    a.w = 0.0f;
+    a.q_out = d_q;
+    a.gbase = sg.g0;
+    a.loc = reinterpret_cast<const uint32_t*>(wb + L.loc);
+    a.bpre = reinterpret_cast<const uint32_t*>(wb + L.bsum);
+    a.xagg = reinterpret_cast<uint2*>(wb + L.xagg);
+    a.ctrl = ctrl;
+    FZ_CUDA(launch_decode_tiles(a, st));
+    const bool carries = nt > 1 && (g.ndim == 1 || !(g.nx <= kTileCodes && kTileCodes % g.nx == 0));
+    if (carries)
+        FZ_CUDA(launch_xcarry(a, reinterpret_cast<uint2*>(wb + L.xloc), reinterpret_cast<uint2*>(wb + L.xbagg), true, st));
+    if (sg.local.ndim == 3)
+        FZ_CUDA(launch_scan_axis(d_q, sg.local.dims[0], sg.local.dims[1], sg.local.dims[2],
+                                 reinterpret_cast<uint32_t*>(wb + L.sums), 0.0f, st));
+    if (sg.local.ndim >= 2) FZ_CUDA(launch_axis_sum(d_q, sg.L, sg.W, d_agg, st));
+    else FZ_CUDA(cudaMemcpyAsync(d_agg, d_q + (sg.n - 1), 4, cudaMemcpyDeviceToDevice, st));
+    Ctrl h;
+    FZ_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    FZ_CUDA(cudaStreamSynchronize(st));
+    if (h.err != 0) return err_status(h.err);
+    if (h.nnz != local->nnz) return FZ_ERR_CORRUPT;
+    return FZ_OK;
+}
+
+fz_status fz_slab_carry(const int32_t* d_aggs, uint32_t nbefore, uint64_t elems, int32_t* d_carry, void* stream)
+{
+    LaunchScope ls;
+    if (d_carry == nullptr || (nbefore > 0 && d_aggs == nullptr) || elems == 0) return FZ_ERR_ARG;
+    FZ_CUDA(launch_slab_carry(d_aggs, nbefore, elems, d_carry, static_cast<cudaStream_t>(stream)));
+    return FZ_OK;
+}
+
+fz_status fz_slab_finish(int32_t* d_q, const int32_t* d_carry, const void* d_stage, const fz_counts* local,
+                         const fz_shape* global, uint64_t tb, uint64_t te, const fz_params* p, void* stream)
+{
+    LaunchScope ls;
+    SlabGeo sg;
+    if (d_q == nullptr || d_carry == nullptr || d_stage == nullptr || local == nullptr || p == nullptr)
+        return FZ_ERR_ARG;
+    fz_status rs = slab_geo(global, tb, te, &sg);
+    if (rs != FZ_OK) return rs;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (sg.local.ndim >= 2) FZ_CUDA(launch_walk_carry(d_q, sg.L, sg.W, p->w, d_carry, st));
+    else FZ_CUDA(launch_add_dequant(d_q, sg.n, d_carry, p->w, st));
+    const uint64_t nt = te - tb;
+    const uint8_t* in = static_cast<const uint8_t*>(d_stage);
+    const uint2* vrec = reinterpret_cast<const uint2*>(in + 32 * nt + 16 * local->nnz + 8 * local->n_delta);
+    FZ_CUDA(launch_value_patch(reinterpret_cast<float*>(d_q), vrec, local->n_value, sg.n, st, sg.g0));
+    FZ_CUDA(cudaStreamSynchronize(st));
+    return FZ_OK;
 }
 
 }  // extern "C"

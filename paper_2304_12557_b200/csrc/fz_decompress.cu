@@ -242,10 +242,11 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
             uint64_t lo = 0, hi = 0;
             if (a.nd > 0) {
                 uint64_t l = 0, h = a.nd;
-                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < s) l = m + 1; else h = m; }
+                const int64_t gs = s + (int64_t)a.gbase;   // records hold global indices
+                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs) l = m + 1; else h = m; }
                 lo = l;
                 h = a.nd;
-                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < s + kTileCodes) l = m + 1; else h = m; }
+                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs + kTileCodes) l = m + 1; else h = m; }
                 hi = l;
             }
             s_lo = lo;
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
             __syncthreads();
             for (uint64_t k = s_lo + tid; k < s_hi; k += kCta) {
                 const uint2 r = a.drec[k];
-                D[r.x - (uint32_t)s] = (int32_t)r.y;
+                D[(uint32_t)(r.x - a.gbase - (uint64_t)s)] = (int32_t)r.y;
             }
             __syncthreads();
 #pragma unroll
@@ -459,13 +460,13 @@ __global__ void k_scan_apply(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
 // Single-pass inclusive scan along L when there are many independent columns: one thread
 // per column walks L with 8 loads in flight (8 B/element of traffic instead of 12).
 __global__ void __launch_bounds__(256) k_scan_walk(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
-                                                   float dequant_w)
+                                                   float dequant_w, const int32_t* __restrict__ carry)
 {
     const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= outer * W) return;
     const uint64_t w = gid % W, o = gid / W;
     int32_t* p = v + o * L * W + w;
-    uint32_t acc = 0;
+    uint32_t acc = carry ? (uint32_t)carry[w] : 0u;
     uint64_t l = 0;
     for (; l + 8 <= L; l += 8) {
         uint32_t x[8];
@@ -486,13 +487,54 @@ __global__ void __launch_bounds__(256) k_scan_walk(int32_t* v, uint64_t outer, u
     }
 }
 
-__global__ void k_value_patch(float* out, const uint2* rec, uint64_t cnt, uint64_t n)
+__global__ void k_value_patch(float* out, const uint2* rec, uint64_t cnt, uint64_t n, uint64_t base)
 {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint2 r = rec[k];
-        if (r.x < n) out[r.x] = __uint_as_float(r.y);
+        if (r.x >= base && r.x - base < n) out[r.x - base] = __uint_as_float(r.y);
     }
+}
+
+// ---- multi-GPU slab decode helpers ----
+// agg[w] = sum over l of v[l][w] (mod 2^32): a slab's aggregate along its slowest axis.
+__global__ void __launch_bounds__(256) k_axis_sum(const int32_t* __restrict__ v, uint64_t L, uint64_t W,
+                                                  int32_t* __restrict__ agg)
+{
+    const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= W) return;
+    const int32_t* p = v + w;
+    uint32_t acc = 0;
+    uint64_t l = 0;
+    for (; l + 8 <= L; l += 8) {
+        uint32_t x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = (uint32_t)__ldcs(p + k * W);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += x[k];
+        p += 8 * W;
+    }
+    for (; l < L; ++l, p += W) acc += (uint32_t)*p;
+    agg[w] = (int32_t)acc;
+}
+
+// carry[w] = sum over the lower ranks j < nbefore of aggs[j][w] (mod 2^32).
+__global__ void k_slab_carry(const int32_t* __restrict__ aggs, uint32_t nbefore, uint64_t elems, int32_t* carry)
+{
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < elems;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t acc = 0;
+        for (uint32_t j = 0; j < nbefore; ++j) acc += (uint32_t)aggs[(uint64_t)j * elems + w];
+        carry[w] = (int32_t)acc;
+    }
+}
+
+// 1-D slab finish: x = fl32(fl32(q + carry) * w).
+__global__ void k_add_dequant(int32_t* q, uint64_t n, const int32_t* carry, float w)
+{
+    const uint32_t c = (uint32_t)carry[0];
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (uint64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<float*>(q)[g] = __fmul_rn(__int2float_rn((int32_t)((uint32_t)q[g] + c)), w);
 }
 
 // ------------------------------------------------------------------------------------
@@ -590,7 +632,7 @@ cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t
 {
     if (outer * W >= 32768) {
         LaunchProf lp(K_SCAN_APPLY, st);
-        k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, dequant_w);
+        k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, dequant_w, nullptr);
         return cudaGetLastError();
     }
     const uint64_t nch = (L + kScanChunk - 1) / kScanChunk;
@@ -610,11 +652,40 @@ cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint64_t n, cudaStream_t st)
+cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint64_t n, cudaStream_t st,
+                               uint64_t base)
 {
     if (cnt == 0) return cudaSuccess;
     LaunchProf lp(K_VPATCH, st);
-    k_value_patch<<<grid_for(cnt), 256, 0, st>>>(out, vrec, cnt, n);
+    k_value_patch<<<grid_for(cnt), 256, 0, st>>>(out, vrec, cnt, n, base);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_axis_sum(const int32_t* v, uint64_t L, uint64_t W, int32_t* agg, cudaStream_t st)
+{
+    LaunchProf lp(K_SLAB, st);
+    k_axis_sum<<<(unsigned)((W + 255) / 256), 256, 0, st>>>(v, L, W, agg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t elems, int32_t* carry, cudaStream_t st)
+{
+    LaunchProf lp(K_SLAB, st);
+    k_slab_carry<<<grid_for(elems), 256, 0, st>>>(aggs, nbefore, elems, carry);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_walk_carry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* carry, cudaStream_t st)
+{
+    LaunchProf lp(K_SCAN_APPLY, st);
+    k_scan_walk<<<(unsigned)((W + 255) / 256), 256, 0, st>>>(data, 1, L, W, w, carry);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_add_dequant(int32_t* q, uint64_t n, const int32_t* carry, float w, cudaStream_t st)
+{
+    LaunchProf lp(K_SLAB, st);
+    k_add_dequant<<<grid_for(n), 256, 0, st>>>(q, n, carry, w);
     return cudaGetLastError();
 }
 

@@ -12,7 +12,7 @@ int num_sms();
 // Kernel kinds for launch accounting and per-kernel CUDA-event timing (fz_profile_*).
 enum KernelId {
     K_INIT = 0, K_RANGE, K_PARAMS, K_COMPRESS, K_FINALIZE, K_DINIT, K_VALIDATE, K_DECODE,
-    K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_COUNT
+    K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_SLAB, K_COUNT
 };
 
 // Counts one launch of `id` and, when profiling is on, brackets it with CUDA events on the
@@ -51,6 +51,7 @@ struct DecodeArgs {
     uint32_t tiles;
     float w;
     int32_t* q_out;             // integer codes (aliases the output field)
+    uint64_t gbase;             // global element index of local element 0 (slab decode)
     const uint32_t* loc;        // per-tile block offset inside its group of 1024 tiles
     const uint32_t* bpre;       // exclusive block offset of each group of 1024 tiles
     uint2* xagg;                // per-tile x-scan aggregate (row start seen, sum)
@@ -75,6 +76,12 @@ cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool c
 cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t W,
                              uint32_t* sums, float dequant_w, cudaStream_t st);
 cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint64_t n,
-                               cudaStream_t st);
+                               cudaStream_t st, uint64_t base = 0);
+cudaError_t launch_axis_sum(const int32_t* v, uint64_t L, uint64_t W, int32_t* agg, cudaStream_t st);
+cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t elems, int32_t* carry,
+                              cudaStream_t st);
+cudaError_t launch_walk_carry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* carry,
+                              cudaStream_t st);
+cudaError_t launch_add_dequant(int32_t* q, uint64_t n, const int32_t* carry, float w, cudaStream_t st);
 
 }  // namespace fz

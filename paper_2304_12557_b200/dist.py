@@ -9,6 +9,11 @@ The path has exactly two exchange steps, both tiny all_gathers:
   2. (nnz, n_delta, n_value) of every rank -> exclusive prefixes = where each rank's share of
      every section goes in the global stream.
 The concatenated stream is byte-identical to the 1-GPU stream for any rank count (R19).
+
+Decompression of plane-aligned slabs (3-D: slab starts at multiples of P = ny*nx) has one
+more exchange: each rank decodes its share locally (x and y prefix sums), reduces it to one
+int32 plane (its z aggregate), the planes are all_gathered, and rank k seeds its z prefix sum
+with the sum of the k lower planes (fz_slab_carry) before dequantizing (fz_slab_finish).
 """
 from __future__ import annotations
 
@@ -49,7 +54,8 @@ def geometry(dims):
 
 
 def plan(dims, world: int, rank: int) -> SlabPlan:
-    """Tile-aligned z-slabs: rank k starts at the tile containing plane floor(k*nz/world)."""
+    """Tile-aligned z-slabs: rank k starts at the tile containing plane floor(k*nz/world)
+    (plane-aligned whenever P % 2048 == 0)."""
     dims = tuple(int(x) for x in dims)
     n, nx, P, halo = geometry(dims)
     T = -(-n // TILE)
@@ -97,6 +103,15 @@ def exchange_range(mn: float, mx: float, device="cpu"):
     return combine_ranges(vals[:, 0].tolist(), vals[:, 1].tolist())
 
 
+def exchange_planes(agg, device=None):
+    """all_gather of the per-rank aggregate planes (int32 tensors, same length)."""
+    import torch
+    import torch.distributed as dist
+    out = [torch.empty_like(agg) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, agg)
+    return torch.stack(out)
+
+
 def exchange_counts(counts, device="cpu"):
     import torch
     import torch.distributed as dist
@@ -138,6 +153,14 @@ class SlabCompressor:
         pl = self.pl
         return self.fz.slab_compress(slab, pl.slab_first, self.dims, pl.tb, pl.te, params, self.stage, self.work)
 
+    def decode_local(self, counts, q, agg, dwork):
+        pl = self.pl
+        self.fz.slab_decode(self.stage, counts, self.dims, pl.tb, pl.te, q, agg, dwork)
+
+    def finish(self, q, carry, counts, params):
+        pl = self.pl
+        self.fz.slab_finish(q, carry, self.stage, counts, self.dims, pl.tb, pl.te, params)
+
     def place(self, counts, before, totals, params, out):
         fz = self.fz
         pl = self.pl
@@ -176,3 +199,49 @@ def compress_sharded_single_process(d: np.ndarray, mode, eb, ranks: int, device=
         c.place(cnt, b, totals, params, out)
     torch.cuda.synchronize()
     return out.cpu().numpy()
+
+
+def roundtrip_sharded_single_process(d: np.ndarray, mode, eb, ranks: int, device="cuda:0"):
+    """Compress and decompress through the k-rank slab protocol sequentially on one GPU.
+    Returns (stream bytes, decompressed field).  Requires plane-aligned slabs."""
+    import torch
+
+    from . import fz
+    dims = d.shape
+    flat = np.ascontiguousarray(d).reshape(-1)
+    plans = [p for p in (plan(dims, ranks, k) for k in range(ranks)) if p.te > p.tb]
+    comps, slabs, mins, maxs = [], [], [], []
+    for p in plans:
+        slab = torch.from_numpy(flat[p.slab_first: p.slab_hi].copy()).to(device)
+        c = SlabCompressor(dims, p, device)
+        mn, mx = c.local_range(slab)
+        mins.append(mn)
+        maxs.append(mx)
+        comps.append(c)
+        slabs.append(slab)
+    params = fz.derive_params(*combine_ranges(mins, maxs), mode, eb)
+    counts = [c.compress_local(s, params) for c, s in zip(comps, slabs)]
+    before, totals = prefix_counts([(c.nnz, c.n_delta, c.n_value) for c in counts])
+    T = plans[0].tiles
+    out = torch.zeros(128 + 32 * T + 16 * totals[0] + 8 * totals[1] + 8 * totals[2], dtype=torch.uint8,
+                      device=device)
+    for c, cnt, b in zip(comps, counts, before):
+        c.place(cnt, b, totals, params, out)
+    # decode: local decode -> aggregates -> carries -> finish
+    E = fz.slab_agg_elems(dims)
+    aggs = torch.empty((len(plans), E), dtype=torch.int32, device=device)
+    qs = []
+    for k, (c, cnt, p) in enumerate(zip(comps, counts, plans)):
+        q = torch.empty(p.own_hi - p.own_lo, dtype=torch.int32, device=device)
+        local_dims = (int((p.own_hi - p.own_lo) // E),) + tuple(dims[1:]) if len(dims) > 1 else (p.own_hi - p.own_lo,)
+        dwork = torch.empty(max(16, fz.decompress_workspace_bytes(local_dims)), dtype=torch.uint8, device=device)
+        c.decode_local(cnt, q, aggs[k], dwork)
+        qs.append(q)
+    xhat = np.empty(flat.size, dtype=np.float32)
+    for k, (c, cnt, p, q) in enumerate(zip(comps, counts, plans, qs)):
+        carry = torch.empty(E, dtype=torch.int32, device=device)
+        fz.slab_carry(aggs, k, E, carry)
+        c.finish(q, carry, cnt, params)
+        xhat[p.own_lo: p.own_hi] = q.view(torch.float32).cpu().numpy()
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), xhat

@@ -85,6 +85,10 @@ def lib():
         "fz_profile_enable": ([i], None),
         "fz_profile_read": ([C.POINTER(C.c_double), C.POINTER(C.c_int), i], i),
         "fz_kernel_name": ([i], C.c_char_p),
+        "fz_slab_agg_elems": ([pS], u64),
+        "fz_slab_decode": ([P, pC, pS, u64, u64, P, P, P, S, P], i),
+        "fz_slab_carry": ([P, C.c_uint32, u64, P, P], i),
+        "fz_slab_finish": ([P, P, P, pC, pS, u64, u64, pP, P], i),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -302,3 +306,24 @@ def slab_place(stage, dims, tb, te, local: Counts, before: Counts, totals: Count
                              C.byref(totals), C.byref(params), int(write_header), _ptr(out), out.numel(),
                              _stream(stream))
     _check(st, "fz_slab_place")
+
+
+def slab_agg_elems(dims) -> int:
+    return lib().fz_slab_agg_elems(C.byref(make_shape(dims)))
+
+
+def slab_decode(stage, counts: Counts, dims, tb, te, q, agg, work, stream=None):
+    st = lib().fz_slab_decode(_ptr(stage), C.byref(counts), C.byref(make_shape(dims)), tb, te, _ptr(q), _ptr(agg),
+                              _ptr(work), work.numel(), _stream(stream))
+    _check(st, "fz_slab_decode")
+
+
+def slab_carry(aggs, nbefore: int, elems: int, carry, stream=None):
+    st = lib().fz_slab_carry(_ptr(aggs) if aggs is not None else None, nbefore, elems, _ptr(carry), _stream(stream))
+    _check(st, "fz_slab_carry")
+
+
+def slab_finish(q, carry, stage, counts: Counts, dims, tb, te, params: Params, stream=None):
+    st = lib().fz_slab_finish(_ptr(q), _ptr(carry), _ptr(stage), C.byref(counts), C.byref(make_shape(dims)), tb, te,
+                              C.byref(params), _stream(stream))
+    _check(st, "fz_slab_finish")

@@ -197,3 +197,27 @@ def test_host_buffer_entry_points():
     fz.decompress_host(h_out, size, h_x, d_out, d_field, dwork)
     st, xref = O.decompress(ref, d.size)
     assert np.array_equal(h_x.reshape(-1).view(np.uint32), xref.view(np.uint32))
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 4, 8])
+def test_fake_multirank_roundtrip(ranks):
+    """Slab decompression with the carry-plane exchange (SV §8.e) reproduces the oracle's
+    decompressed field bit for bit; the assembled stream equals the oracle's."""
+    from paper_2304_12557_b200 import dist
+    d = synth.generate("nyx_rho", (64, 32, 64))           # P = 2048: plane-aligned slabs
+    st, ref = O.compress(d, O.REL, 1e-3)
+    st, xref = O.decompress(ref, d.size)
+    stream, xh = dist.roundtrip_sharded_single_process(d, fz.REL, 1e-3, ranks, DEV)
+    _assert_stream_equal(stream, ref, f"ranks={ranks}")
+    assert np.array_equal(xh.view(np.uint32), xref.view(np.uint32))
+
+
+@pytest.mark.parametrize("shape", [(300, 2048), (6000,), (4, 64, 64)])
+def test_fake_multirank_roundtrip_2d_1d(shape):
+    from paper_2304_12557_b200 import dist
+    d = synth.adversarial("noise", int(np.prod(shape))).reshape(shape) + np.float32(3)
+    st, ref = O.compress(d, O.ABS, 1e-2)
+    st, xref = O.decompress(ref, d.size)
+    stream, xh = dist.roundtrip_sharded_single_process(d, fz.ABS, 1e-2, 3, DEV)
+    _assert_stream_equal(stream, ref, f"{shape}")
+    assert np.array_equal(xh.view(np.uint32), xref.view(np.uint32))
