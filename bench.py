@@ -54,9 +54,13 @@ def ncu_traffic(workload: str, kernel: str):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f)[workload][kernel]
+            t = json.load(f)[workload]
+        for k in (kernel, kernel + "_ws"):
+            if k in t:
+                return t[k]
     except Exception:
-        return None
+        pass
+    return None
 
 
 class ClockSampler:
