@@ -198,39 +198,45 @@ __device__ __forceinline__ int pq_fast(float d, const QuantP& P, bool& hard)
 template <int K>
 __device__ __forceinline__ void pq_many(const float (&v)[K], int (&q)[K], const QuantP& P)
 {
-    uint32_t hard = 0;
+    bool any = false;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         bool h;
         q[i] = pq_fast(v[i], P, h);
-        hard |= (uint32_t)h << i;
+        any |= h;
     }
-    if (__any_sync(kFull, hard != 0)) {
+    if (__any_sync(kFull, any) && any) {
 #pragma unroll
-        for (int i = 0; i < K; ++i)
-            if ((hard >> i) & 1u) q[i] = prequant_q(v[i], P);
+        for (int i = 0; i < K; ++i) {
+            bool h;
+            pq_fast(v[i], P, h);
+            if (h) q[i] = prequant_q(v[i], P);
+        }
     }
 }
 
 // Own elements: q plus the exact rule + bound check where the fast path does not apply.
 __device__ __forceinline__ void pq_own(const float (&v)[8], int (&q)[8], uint32_t& vmask, const QuantP& P)
 {
-    uint32_t hard = 0;
+    bool any = false;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         bool h;
         q[i] = pq_fast(v[i], P, h);
-        hard |= (uint32_t)h << i;
+        any |= h;
     }
     vmask = 0;
-    if (__any_sync(kFull, hard != 0)) {
+    if (__any_sync(kFull, any) && any) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if ((hard >> i) & 1u) {
+        for (int i = 0; i < 8; ++i) {
+            bool h;
+            pq_fast(v[i], P, h);
+            if (h) {
                 bool vo;
                 q[i] = prequant(v[i], P, vo);
                 if (vo) vmask |= 1u << i;
             }
+        }
     }
 }
 
@@ -492,9 +498,11 @@ __device__ __forceinline__ void lorenzo_masks(const CompressArgs& a, uint32_t g0
 __device__ __forceinline__ void residuals(const uint32_t (&S)[9], uint32_t xm, int32_t (&dl)[8])
 {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const uint32_t X = (xm >> e) & 1u ? 0xFFFFFFFFu : 0u;
-        dl[e] = (int32_t)(S[e + 1] - (S[e] & X));
+    for (int e = 0; e < 8; ++e) dl[e] = (int32_t)(S[e + 1] - S[e]);
+    if (xm != 0xFFu) {   // a row start among the 8 elements: its x-1 neighbour is outside
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (!((xm >> e) & 1u)) dl[e] = (int32_t)S[e + 1];
     }
 }
 
@@ -1023,12 +1031,17 @@ __device__ __forceinline__ void front_ws(const CompressArgs& a, const QuantP& P,
     S[0] = __shfl_up_sync(kFull, S[8], 1);
     if (lane == 0 || !fast_yz) {
         const uint32_t pos = g0 - 1;
-        const uint32_t Y = (ym & 1u) ? 0xFFFFFFFFu : 0u;
-        const uint32_t Z = (zm & 1u) ? 0xFFFFFFFFu : 0u;
         uint32_t v = (uint32_t)smem[pos & rmask];
-        if (NDIM >= 2) v -= (uint32_t)smem[(pos - nx) & rmask] & Y;
-        if (NDIM == 3)
-            v -= ((uint32_t)smem[RB + ((pos - PL) & rmask)] - ((uint32_t)smem[RB + ((pos - PL - nx) & rmask)] & Y)) & Z;
+        if (fast_yz) {
+            if (NDIM >= 2) v -= (uint32_t)smem[(pos - nx) & rmask];
+            if (NDIM == 3) v -= (uint32_t)smem[RB + ((pos - PL) & rmask)] - (uint32_t)smem[RB + ((pos - PL - nx) & rmask)];
+        } else {
+            const uint32_t Y = (ym & 1u) ? 0xFFFFFFFFu : 0u;
+            const uint32_t Z = (zm & 1u) ? 0xFFFFFFFFu : 0u;
+            if (NDIM >= 2) v -= (uint32_t)smem[(pos - nx) & rmask] & Y;
+            if (NDIM == 3)
+                v -= ((uint32_t)smem[RB + ((pos - PL) & rmask)] - ((uint32_t)smem[RB + ((pos - PL - nx) & rmask)] & Y)) & Z;
+        }
         S[0] = v;
     }
     residuals(S, xm, dl);
@@ -1043,15 +1056,20 @@ __device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh,
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Ctrl* ctrl = a.ctrl;
     const uint32_t n = a.g.n;
+    // ---- C3 codes; |delta| > 32767 (rare) -> code 0 + delta outlier (R7) ----
     uint32_t code[8];
-    uint32_t dmask = 0;
+    uint32_t magor = 0;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-        const uint32_t dd = (uint32_t)dl[e];
         const uint32_t mag = (uint32_t)abs(dl[e]);
-        const bool outl = mag > 32767u;
-        code[e] = outl ? 0u : (((dd >> 16) & 0x8000u) | mag);
-        if (outl) dmask |= 1u << e;
+        code[e] = (((uint32_t)dl[e] >> 16) & 0x8000u) | mag;
+        magor |= mag;
+    }
+    uint32_t dmask = 0;
+    if (magor > 32767u) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if ((uint32_t)abs(dl[e]) > 32767u) { dmask |= 1u << e; code[e] = 0u; }
     }
     if (vm != 0xFFu) {
         dmask &= vm;
@@ -1136,16 +1154,14 @@ __device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh,
     const uint32_t F = __ballot_sync(kFull, nz);
     if (lane == 0) sh.F[warp] = F;
     bar_sync(kBarCompute, kCta);
-    uint32_t tn = 0, wpre = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-        const uint32_t pc = __popc(sh.F[w]);
-        tn += pc;
-        if (w < warp) wpre += pc;
-    }
+    // block counts of the 8 flag words: lane l < 8 holds word l; warp prefix by reductions
+    const uint32_t fw = lane < 8 ? sh.F[lane] : 0u;
+    const uint32_t pc = __popc(fw);
+    const uint32_t tn = __reduce_add_sync(kFull, pc);
+    const uint32_t wpre = __reduce_add_sync(kFull, lane < warp ? pc : 0u);
     if (tid < 8) {
         const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * tid;
-        if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = sh.F[tid];
+        if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = fw;
     }
     if (nz) st[cnt + wpre + __popc(F & ((1u << lane) - 1u))] = blk;
     return tn;

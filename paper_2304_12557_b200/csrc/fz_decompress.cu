@@ -232,143 +232,121 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
     __shared__ uint64_t s_lo, s_hi;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t n = a.g.n, nx = a.g.nx;
-    for (uint32_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
-        const int64_t s = (int64_t)t * kTileCodes;
-        const uint32_t g0 = (uint32_t)s + 8u * tid;
-        // ---- D1/D2: offsets, gather block b = tid into the shuffled tile O ----
-        const uint32_t F = reinterpret_cast<const uint32_t*>(a.flags)[8 * (uint64_t)t + warp];
-        if (lane == 0) s_F[warp] = F;
-        if (tid == 32) {
-            uint64_t lo = 0, hi = 0;
-            if (a.nd > 0) {
-                uint64_t l = 0, h = a.nd;
-                const int64_t gs = s + (int64_t)a.gbase;   // records hold global indices
-                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs) l = m + 1; else h = m; }
-                lo = l;
-                h = a.nd;
-                while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs + kTileCodes) l = m + 1; else h = m; }
-                hi = l;
-            }
-            s_lo = lo;
-            s_hi = hi;
+    const uint32_t t = blockIdx.x;          // one CTA per tile: many tiles in flight per SM
+    const int64_t s = (int64_t)t * kTileCodes;
+    const uint32_t g0 = (uint32_t)s + 8u * tid;
+    // ---- D1/D2: all independent loads first (flags word, offsets) ----
+    const uint32_t F = reinterpret_cast<const uint32_t*>(a.flags)[8 * (uint64_t)t + warp];
+    const uint64_t tbase = (uint64_t)a.bpre[t >> 10] + a.loc[t];
+    uint32_t xm_rs = 0;                      // row-start bit per element
+    if (nx >= 8) {
+        const uint32_t x0 = fmod_(g0, a.dnx);
+        const uint32_t us = x0 == 0 ? 0u : nx - x0;
+        if (us < 8) xm_rs = 1u << us;
+    } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (fmod_(g0 + u, a.dnx) == 0) xm_rs |= 1u << u;
+    }
+    if (lane == 0) s_F[warp] = F;
+    if (tid == 32) {
+        uint64_t lo = 0, hi = 0;
+        if (a.nd > 0) {
+            const int64_t gs = s + (int64_t)a.gbase;   // records hold global indices
+            uint64_t l = 0, h = a.nd;
+            while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs) l = m + 1; else h = m; }
+            lo = l;
+            h = a.nd;
+            while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs + kTileCodes) l = m + 1; else h = m; }
+            hi = l;
+        }
+        s_lo = lo;
+        s_hi = hi;
+    }
+    __syncthreads();
+    {
+        const uint32_t fw = lane < 8 ? s_F[lane] : 0u;
+        const uint32_t wpre = __reduce_add_sync(kFull, lane < warp ? __popc(fw) : 0u);
+        uint4 blk = make_uint4(0, 0, 0, 0);
+        if ((F >> lane) & 1u) {
+            const uint64_t bi = tbase + wpre + __popc(F & ((1u << lane) - 1u));
+            if (bi < a.nnz_total) blk = __ldcs(reinterpret_cast<const uint4*>(a.payload) + bi);
+            else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
+        }
+        uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+        row[0] = blk.x; row[1] = blk.y; row[2] = blk.z; row[3] = blk.w;
+    }
+    __syncthreads();
+    // ---- D3: column c of O -> row c of A ----
+    uint32_t w4[4];
+    {
+        const int c = tid >> 3, kk = tid & 7;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w4[i] = Obuf[(4 * kk + i) * 33 + c];
+        transpose32_group8(w4, lane & 7);
+    }
+    // ---- D4: unpack, delta outliers ----
+    int32_t dl[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t lo16 = w4[i] & 0xFFFFu, hi16 = w4[i] >> 16;
+        dl[2 * i] = (lo16 & 0x8000u) ? -(int32_t)(lo16 & 0x7FFFu) : (int32_t)lo16;
+        dl[2 * i + 1] = (hi16 & 0x8000u) ? -(int32_t)(hi16 & 0x7FFFu) : (int32_t)hi16;
+    }
+    if (s_hi > s_lo) {   // rare, block-uniform
+#pragma unroll
+        for (int u = 0; u < 8; ++u) D[8 * tid + u] = dl[u];
+        __syncthreads();
+        for (uint64_t k = s_lo + tid; k < s_hi; k += kCta) {
+            const uint2 r = a.drec[k];
+            D[(uint32_t)(r.x - a.gbase - (uint64_t)s)] = (int32_t)r.y;
         }
         __syncthreads();
-        {
-            uint32_t wpre = 0;
 #pragma unroll
-            for (int w = 0; w < 8; ++w)
-                if (w < warp) wpre += __popc(s_F[w]);
-            uint4 blk = make_uint4(0, 0, 0, 0);
-            if ((F >> lane) & 1u) {
-                const uint64_t bi = (uint64_t)a.bpre[t >> 10] + a.loc[t] + wpre + __popc(F & ((1u << lane) - 1u));
-                if (bi < a.nnz_total) blk = reinterpret_cast<const uint4*>(a.payload)[bi];
-                else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
-            }
-            uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
-            row[0] = blk.x; row[1] = blk.y; row[2] = blk.z; row[3] = blk.w;
-        }
-        __syncthreads();
-        // ---- D3: column c of O -> row c of A ----
-        uint32_t w4[4];
-        {
-            const int c = tid >> 3, kk = tid & 7;
+        for (int u = 0; u < 8; ++u) dl[u] = D[8 * tid + u];
+    }
+    // ---- D5 (x, local): segmented inclusive scan, resets at row starts ----
+    uint32_t loc[8];
+    Seg me{0, 0};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) w4[i] = Obuf[(4 * kk + i) * 33 + c];
-            transpose32_group8(w4, lane & 7);
-        }
-        // ---- D4: unpack, delta outliers ----
-        int32_t dl[8];
+    for (int u = 0; u < 8; ++u) {
+        if ((xm_rs >> u) & 1u) { me.f = 1; me.v = 0; }
+        me.v += (uint32_t)dl[u];
+        loc[u] = me.v;
+    }
+    Seg inc = me;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t lo16 = w4[i] & 0xFFFFu, hi16 = w4[i] >> 16;
-            dl[2 * i] = (lo16 & 0x8000u) ? -(int32_t)(lo16 & 0x7FFFu) : (int32_t)lo16;
-            dl[2 * i + 1] = (hi16 & 0x8000u) ? -(int32_t)(hi16 & 0x7FFFu) : (int32_t)hi16;
-        }
-        if (s_hi > s_lo) {   // rare, block-uniform
+    for (int o = 1; o < 32; o <<= 1) {
+        const Seg up{__shfl_up_sync(kFull, inc.f, o), __shfl_up_sync(kFull, inc.v, o)};
+        if (lane >= o) inc = seg_combine(up, inc);
+    }
+    Seg lex{__shfl_up_sync(kFull, inc.f, 1), __shfl_up_sync(kFull, inc.v, 1)};
+    if (lane == 0) lex = Seg{0, 0};
+    if (lane == 31) { s_wf[warp] = inc.f; s_wv[warp] = inc.v; }
+    __syncthreads();
+    Seg wp{0, 0}, tagg{0, 0};
 #pragma unroll
-            for (int u = 0; u < 8; ++u) D[8 * tid + u] = dl[u];
-            __syncthreads();
-            for (uint64_t k = s_lo + tid; k < s_hi; k += kCta) {
-                const uint2 r = a.drec[k];
-                D[(uint32_t)(r.x - a.gbase - (uint64_t)s)] = (int32_t)r.y;
-            }
-            __syncthreads();
+    for (int w = 0; w < 8; ++w) {
+        const Seg sw{s_wf[w], s_wv[w]};
+        if (w < warp) wp = seg_combine(wp, sw);
+        tagg = seg_combine(tagg, sw);
+    }
+    if (tid == 0) a.xagg[t] = make_uint2(tagg.f, tagg.v);
+    // elements before the thread's first row start get the in-tile prefix; the carry from
+    // earlier tiles is added by k_xfix where needed
+    const Seg acc = seg_combine(wp, lex);
+    uint32_t q[8];
+    const uint32_t pre = xm_rs ? ((xm_rs & (0u - xm_rs)) - 1u) : 0xFFu;   // elements before it
 #pragma unroll
-            for (int u = 0; u < 8; ++u) dl[u] = D[8 * tid + u];
-        }
-        // ---- D5 (x, local): segmented inclusive scan, resets at row starts ----
-        uint32_t loc[8];
-        Seg me{0, 0};
-        if (nx >= 8) {
-            uint32_t x = fmod_(g0, a.dnx);
+    for (int u = 0; u < 8; ++u) q[u] = ((pre >> u) & 1u) ? acc.v + loc[u] : loc[u];
+    if (s + kTileCodes <= (int64_t)n) {
+        int4* o = reinterpret_cast<int4*>(a.q_out + g0);
+        __stcs(o, make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]));
+        __stcs(o + 1, make_int4((int)q[4], (int)q[5], (int)q[6], (int)q[7]));
+    } else {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (x == 0) { me.f = 1; me.v = 0; }
-                me.v += (uint32_t)dl[u];
-                loc[u] = me.v;
-                if (++x == nx) x = 0;
-            }
-        } else {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (fmod_(g0 + u, a.dnx) == 0) { me.f = 1; me.v = 0; }
-                me.v += (uint32_t)dl[u];
-                loc[u] = me.v;
-            }
-        }
-        Seg inc = me;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const Seg up{__shfl_up_sync(kFull, inc.f, o), __shfl_up_sync(kFull, inc.v, o)};
-            if (lane >= o) inc = seg_combine(up, inc);
-        }
-        Seg lex{__shfl_up_sync(kFull, inc.f, 1), __shfl_up_sync(kFull, inc.v, 1)};
-        if (lane == 0) lex = Seg{0, 0};
-        if (lane == 31) { s_wf[warp] = inc.f; s_wv[warp] = inc.v; }
-        __syncthreads();
-        Seg wp{0, 0}, tagg{0, 0};
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const Seg sw{s_wf[w], s_wv[w]};
-            if (w < warp) wp = seg_combine(wp, sw);
-            tagg = seg_combine(tagg, sw);
-        }
-        if (tid == 0) a.xagg[t] = make_uint2(tagg.f, tagg.v);
-        // values before the thread's first row start get the in-tile prefix (the carry from
-        // earlier tiles is added by k_xfix where needed)
-        const Seg acc = seg_combine(wp, lex);
-        uint32_t q[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) q[u] = loc[u];
-        {
-            // recompute "row start at or before u inside this thread"
-            uint32_t rs = 0;
-            if (nx >= 8) {
-                uint32_t x = fmod_(g0, a.dnx);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (x == 0) rs = 1;
-                    if (!rs) q[u] = acc.v + loc[u];
-                    if (++x == nx) x = 0;
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (fmod_(g0 + u, a.dnx) == 0) rs = 1;
-                    if (!rs) q[u] = acc.v + loc[u];
-                }
-            }
-        }
-        if (s + kTileCodes <= (int64_t)n) {
-            int4* o = reinterpret_cast<int4*>(a.q_out + g0);
-            o[0] = make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]);
-            o[1] = make_int4((int)q[4], (int)q[5], (int)q[6], (int)q[7]);
-        } else {
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (g0 + u < n) a.q_out[g0 + u] = (int32_t)q[u];
-        }
-        __syncthreads();
+        for (int u = 0; u < 8; ++u)
+            if (g0 + u < n) a.q_out[g0 + u] = (int32_t)q[u];
     }
 }
 
@@ -583,13 +561,8 @@ static cudaError_t launch_decode_t(const DecodeArgs& a_in, cudaStream_t st)
 {
     DecodeArgs a = a_in;
     a.dnx = make_fastdiv(a.g.nx);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_tiles<NDIM>, kCta, 0);
-    if (per_sm < 1) per_sm = 1;
-    uint64_t grid = (uint64_t)per_sm * num_sms();
-    if (grid > a.tiles) grid = a.tiles;
-    if (grid == 0) return cudaSuccess;
-    k_decode_tiles<NDIM><<<(unsigned)grid, kCta, 0, st>>>(a);
+    if (a.tiles == 0) return cudaSuccess;
+    k_decode_tiles<NDIM><<<a.tiles, kCta, 0, st>>>(a);
     return cudaGetLastError();
 }
 
