@@ -714,8 +714,14 @@ __device__ __forceinline__ void front_vec(const CompressArgs& a, const QuantP& P
         if (NDIM == 3) fill_ring(a, P, smem, RB, rmask, (s - (int64_t)PL - H) & ~(int64_t)3, s - (int64_t)PL);
     }
     int qo[8], qz[8];
-    pq_own(dv, qo, vmask, P);
-    if (NDIM == 3) pq_many<8>(bz, qz, P);
+    if (a.exp & 64) {
+        vmask = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { qo[u] = __float_as_int(dv[u]) >> 12; qz[u] = __float_as_int(bz[u]) >> 12; }
+    } else {
+        pq_own(dv, qo, vmask, P);
+        if (NDIM == 3) pq_many<8>(bz, qz, P);
+    }
     *reinterpret_cast<int4*>(smem + (g0 & rmask)) = make_int4(qo[0], qo[1], qo[2], qo[3]);
     *reinterpret_cast<int4*>(smem + ((g0 + 4) & rmask)) = make_int4(qo[4], qo[5], qo[6], qo[7]);
     if (NDIM == 3) {
@@ -907,32 +913,40 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
 }
 
+constexpr int kRingBlocks = 1024;   // 16 KB elastic payload ring (per-tile allocation)
+constexpr int kDescQ = 8;          // unit descriptors in flight to the scanner
+
+struct WsDesc {
+    uint32_t unit, start, cnt, pad;
+};
+
 struct WsShared {
-    uint64_t mbar[2];              // TMA input stages
-    uint32_t tma_bits[2];          // bit0: own tile loaded by TMA, bit1: previous-plane tile
+    uint64_t mbar;                 // TMA input stage
+    uint32_t tma_bits;             // bit0: own tile loaded by TMA, bit1: previous-plane tile
     uint32_t unit[2];
-    uint32_t ready_unit[2], ready_cnt[2];
     uint32_t F[8];
     uint32_t cd[8], cv[8];
     unsigned long long ob[2];
+    volatile uint32_t ring_tail;   // payload ring blocks released by the scanner
+    volatile uint32_t desc_head;   // descriptors published by the compute warps
+    volatile uint32_t desc_tail;   // descriptors consumed by the scanner
+    WsDesc desc[kDescQ];
 };
 
-// Issue the TMA loads of tile t into input stage `stg` (thread 0 of the compute group).
+// Issue the TMA loads of tile t into the input stage (thread 0 of the compute group).
 template <int NDIM>
-__device__ __forceinline__ void ws_issue(const CompressArgs& a, WsShared& sh, float* inbuf, int stg, uint32_t t)
+__device__ __forceinline__ void ws_issue(const CompressArgs& a, WsShared& sh, float* inbuf, uint32_t t)
 {
     const int64_t s = (int64_t)t * kTileCodes, base = (int64_t)a.base;
     const bool full = s + kTileCodes <= (int64_t)a.g.n;
     uint32_t bits = 0, bytes = 0;
     if (full && s >= base) { bits |= 1; bytes += kTileCodes * 4; }
     if (NDIM == 3 && full && s - (int64_t)a.g.P >= base) { bits |= 2; bytes += kTileCodes * 4; }
-    sh.tma_bits[stg] = bits;
+    sh.tma_bits = bits;
     if (bytes) {
-        uint64_t* m = &sh.mbar[stg];
-        mbar_expect_tx(m, bytes);
-        float* dst = inbuf + stg * 2 * kTileCodes;
-        if (bits & 1) tma_load_1d(dst, a.field + (s - base), kTileCodes * 4, m);
-        if (bits & 2) tma_load_1d(dst + kTileCodes, a.field + (s - (int64_t)a.g.P - base), kTileCodes * 4, m);
+        mbar_expect_tx(&sh.mbar, bytes);
+        if (bits & 1) tma_load_1d(inbuf, a.field + (s - base), kTileCodes * 4, &sh.mbar);
+        if (bits & 2) tma_load_1d(inbuf + kTileCodes, a.field + (s - (int64_t)a.g.P - base), kTileCodes * 4, &sh.mbar);
     }
 }
 
@@ -972,8 +986,14 @@ __device__ __forceinline__ void front_ws(const CompressArgs& a, const QuantP& P,
         if (NDIM == 3) fill_ring(a, P, smem, RB, rmask, (s - (int64_t)PL - H) & ~(int64_t)3, s - (int64_t)PL);
     }
     int qo[8], qz[8];
-    pq_own(dv, qo, vmask, P);
-    if (NDIM == 3) pq_many<8>(bz, qz, P);
+    if (a.exp & 64) {
+        vmask = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { qo[u] = __float_as_int(dv[u]) >> 12; qz[u] = __float_as_int(bz[u]) >> 12; }
+    } else {
+        pq_own(dv, qo, vmask, P);
+        if (NDIM == 3) pq_many<8>(bz, qz, P);
+    }
     *reinterpret_cast<int4*>(smem + (g0 & rmask)) = make_int4(qo[0], qo[1], qo[2], qo[3]);
     *reinterpret_cast<int4*>(smem + ((g0 + 4) & rmask)) = make_int4(qo[4], qo[5], qo[6], qo[7]);
     if (NDIM == 3) {
@@ -1049,8 +1069,8 @@ __device__ __forceinline__ void front_ws(const CompressArgs& a, const QuantP& P,
 
 // Tail of a tile on the compute warps (no look-back): codes, bitshuffle, outliers, flags,
 // local compaction.  Returns the tile's nonzero block count.
-__device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh, uint32_t* Obuf, uint4* st,
-                                            uint32_t cnt, uint32_t t, uint32_t g0, uint32_t vm,
+__device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh, uint32_t* Obuf, uint4* ring,
+                                            uint32_t head, uint32_t t, uint32_t g0, uint32_t vm,
                                             const int32_t (&dl)[8], uint32_t vmask, const float (&dv)[8])
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1087,7 +1107,7 @@ __device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh,
         uint32_t w4[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) w4[i] = __byte_perm(code[2 * i], code[2 * i + 1], 0x5410);
-        transpose32_group8(w4, lane & 7);
+        if (!(a.exp & 32)) transpose32_group8(w4, lane & 7);
         const int c = tid >> 3, kk = tid & 7;
 #pragma unroll
         for (int i = 0; i < 4; ++i) Obuf[(4 * kk + i) * 33 + c] = w4[i];
@@ -1153,6 +1173,11 @@ __device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh,
     const bool nz = (blk.x | blk.y | blk.z | blk.w) != 0;
     const uint32_t F = __ballot_sync(kFull, nz);
     if (lane == 0) sh.F[warp] = F;
+    if (tid == 0) {
+        // room for a whole tile (worst case 256 blocks) in the payload ring
+        while (head + kTileBlocks - sh.ring_tail > (uint32_t)kRingBlocks) __nanosleep(32);
+        __threadfence_block();
+    }
     bar_sync(kBarCompute, kCta);
     // block counts of the 8 flag words: lane l < 8 holds word l; warp prefix by reductions
     const uint32_t fw = lane < 8 ? sh.F[lane] : 0u;
@@ -1163,12 +1188,12 @@ __device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh,
         const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * tid;
         if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = fw;
     }
-    if (nz) st[cnt + wpre + __popc(F & ((1u << lane) - 1u))] = blk;
+    if (nz) ring[(head + wpre + __popc(F & ((1u << lane) - 1u))) & (kRingBlocks - 1)] = blk;
     return tn;
 }
 
 template <int NDIM>
-__global__ void __launch_bounds__(kWsThreads, 2) k_compress_ws(CompressArgs a)
+__global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
 {
     extern __shared__ __align__(16) int smem[];
     __shared__ WsShared sh;
@@ -1177,48 +1202,48 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_compress_ws(CompressArgs a)
     if (ctrl->err != 0) return;
     const uint32_t rmask = a.qstride - 1;
     uint32_t* Obuf = reinterpret_cast<uint32_t*>(smem + a.qwords);           // 32 x 33
-    uint4* stage = reinterpret_cast<uint4*>(smem + a.qwords + 32 * 33 + 4);   // 2 x kStageBlocks
-    float* inbuf = reinterpret_cast<float*>(stage + 2 * kStageBlocks);        // 2 stages x (own, prev)
+    uint4* ring = reinterpret_cast<uint4*>(smem + a.qwords + 32 * 33 + 4);    // kRingBlocks
+    float* inbuf = reinterpret_cast<float*>(ring + kRingBlocks);              // own, previous plane
     const uint32_t nunits = (a.tile_end - a.tile_begin + kUnitTiles - 1) / kUnitTiles;
 
     if (tid == 0) {
-        mbar_init(&sh.mbar[0], 1);
-        mbar_init(&sh.mbar[1], 1);
+        mbar_init(&sh.mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sh.ring_tail = 0;
+        sh.desc_head = 0;
+        sh.desc_tail = 0;
         sh.unit[0] = atomicAdd(&ctrl->ticket, 1u);
-        sh.tma_bits[0] = sh.tma_bits[1] = 0;
-        if (sh.unit[0] < nunits) ws_issue<NDIM>(a, sh, inbuf, 0, a.tile_begin + sh.unit[0] * kUnitTiles);
+        sh.tma_bits = 0;
+        if (sh.unit[0] < nunits) ws_issue<NDIM>(a, sh, inbuf, a.tile_begin + sh.unit[0] * kUnitTiles);
     }
     __syncthreads();
 
     if (warp == kCta / 32) {
         // ================= scanner warp =================
         if (a.rescan) return;
-        for (int k = 0;; ++k) {
-            const int b = k & 1;
-            bar_sync(1 + b, kWsThreads);
-            const uint32_t u = sh.ready_unit[b];
-            if (u == kNone) break;
-            const uint32_t cnt = sh.ready_cnt[b];
+        for (uint32_t dt = 0;; ++dt) {
+            while (sh.desc_head == dt) __nanosleep(64);
+            __threadfence_block();
+            const WsDesc d = sh.desc[dt % kDescQ];
+            if (d.unit == kNone) break;
             unsigned long long ex = 0;
-            if (u != 0) {
-                long long t0 = clock64();
-                ex = lookback_wide<kLbLane, false>(a.status, u, 0, kStAgg - 1, &ctrl->err, nullptr,
-                                                   (a.exp & 8) ? &ctrl->dbg[0] : nullptr);
-                if (lane == 0) st_relaxed_u64(&a.status[u], kStInc | (ex + cnt));
-                if ((a.exp & 8) && lane == 0) {
-                    atomicAdd(&ctrl->dbg[1], 1ull);
-                    atomicAdd(&ctrl->dbg[2], (unsigned long long)(clock64() - t0));
-                }
+            if (d.unit != 0) {
+                ex = lookback_wide<kLbLane, false>(a.status, d.unit, 0, kStAgg - 1, &ctrl->err);
+                if (lane == 0) st_relaxed_u64(&a.status[d.unit], kStInc | (ex + d.cnt));
             }
-            const uint4* ps = stage + b * kStageBlocks;
-            for (uint32_t i = lane; i < cnt; i += 32) {
+            for (uint32_t i = lane; i < d.cnt; i += 32) {
                 const uint64_t bo = 16 * (ex + i);
-                if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = ps[i];
+                if (bo + 16 <= a.payload_cap)
+                    *reinterpret_cast<uint4*>(a.payload_out + bo) = ring[(d.start + i) & (kRingBlocks - 1)];
             }
-            if (lane == 0 && u == nunits - 1) ctrl->nnz = ex + cnt;
+            if (lane == 0 && d.unit == nunits - 1) ctrl->nnz = ex + d.cnt;
             __syncwarp();
-            bar_arrive(3 + b, kWsThreads);
+            if (lane == 0) {
+                __threadfence_block();
+                sh.ring_tail = d.start + d.cnt;
+                sh.desc_tail = dt + 1;
+            }
+            __syncwarp();
         }
         return;
     }
@@ -1226,73 +1251,60 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_compress_ws(CompressArgs a)
     // ================= compute warps =================
     QuantP P;
     P.w = ctrl->p.w; P.r = ctrl->p.r; P.h = ctrl->h; P.eb32 = ctrl->p.eb32; P.hU = ctrl->hU;
-    uint32_t phase = 0;     // bit s: parity of the next wait on input stage s
-    int stg = 0;            // input stage of the current tile
-    int k = 0;              // units processed by this CTA
+    uint32_t phase = 0;      // parity of the next wait on the input stage
+    uint32_t head = 0;       // payload ring blocks written so far
     for (int it = 0;; ++it) {
         const uint32_t u = sh.unit[it & 1];
-        const int b = k & 1;
         if (u >= nunits) {
-            if (!a.rescan) {
-                if (k >= 2) bar_sync(3 + b, kWsThreads);     // stage b released by the scanner
-                if (tid == 0) sh.ready_unit[b] = kNone;
-                bar_arrive(1 + b, kWsThreads);
+            if (!a.rescan && tid == 0) {
+                while (sh.desc_head - sh.desc_tail >= (uint32_t)kDescQ) __nanosleep(32);
+                const uint32_t dh = sh.desc_head;
+                sh.desc[dh % kDescQ].unit = kNone;
+                __threadfence_block();
+                sh.desc_head = dh + 1;
             }
             break;
         }
-        if (!a.rescan && k >= 2) bar_sync(3 + b, kWsThreads);
         const uint32_t t_first = a.tile_begin + u * kUnitTiles;
         const uint32_t t_last = min(a.tile_end, t_first + kUnitTiles);
-        uint32_t cnt = 0;
+        const uint32_t start = head;
         for (uint32_t t = t_first; t < t_last; ++t) {
             const bool first = t == t_first;
-            // wait for this tile's TMA input
-            const uint32_t bits = sh.tma_bits[stg];
+            const uint32_t bits = sh.tma_bits;
             if (bits) {
-                while (!mbar_try_wait(&sh.mbar[stg], (phase >> stg) & 1u)) {
+                while (!mbar_try_wait(&sh.mbar, phase)) {
                 }
-                phase ^= 1u << stg;
+                phase ^= 1u;
             }
-            const float* ib = inbuf + stg * 2 * kTileCodes;
             int32_t dl[8];
             uint32_t vmask, vm;
             float dv[8];
-            front_ws<NDIM>(a, P, smem, rmask, t, first, (bits & 1) ? ib : nullptr,
-                           (bits & 2) ? ib + kTileCodes : nullptr, dl, vmask, dv, vm);
-            // every compute thread has consumed input stage `stg`: prefetch the next tile
+            front_ws<NDIM>(a, P, smem, rmask, t, first, (bits & 1) ? inbuf : nullptr,
+                           (bits & 2) ? inbuf + kTileCodes : nullptr, dl, vmask, dv, vm);
+            // every compute thread has consumed the input stage: prefetch the next tile
             if (tid == 0) {
                 if (first) sh.unit[(it & 1) ^ 1] = atomicAdd(&ctrl->ticket, 1u);
+                const uint32_t nu = sh.unit[(it & 1) ^ 1];
                 uint32_t nt = kNone;
                 if (t + 1 < t_last) nt = t + 1;
-                else if (sh.unit[(it & 1) ^ 1] < nunits) nt = a.tile_begin + sh.unit[(it & 1) ^ 1] * kUnitTiles;
-                if (nt != kNone) {
-                    ws_issue<NDIM>(a, sh, inbuf, stg ^ 1, nt);
-                    if (first && nt != t + 1 && sh.unit[(it & 1) ^ 1] + 1 < nunits) {
-                    }
-                } else {
-                    sh.tma_bits[stg ^ 1] = 0;
-                }
-                if (first) {
-                    const uint32_t nu = sh.unit[(it & 1) ^ 1];
-                    if (nu < nunits)   // L2 prefetch of the next unit beyond the TMA stage
-                        prefetch_l2_range(a, (uint64_t)(a.tile_begin + nu * kUnitTiles) * kTileCodes,
-                                          (uint64_t)kUnitTiles * kTileCodes);
-                }
+                else if (nu < nunits) nt = a.tile_begin + nu * kUnitTiles;
+                if (nt != kNone) ws_issue<NDIM>(a, sh, inbuf, nt);
+                else sh.tma_bits = 0;
+                if (first && nu < nunits)   // L2 prefetch of the next unit beyond the TMA stage
+                    prefetch_l2_range(a, (uint64_t)(a.tile_begin + nu * kUnitTiles) * kTileCodes,
+                                      (uint64_t)kUnitTiles * kTileCodes);
             }
-            cnt += tail_ws(a, sh, Obuf, stage + b * kStageBlocks, cnt, t, (uint32_t)t * kTileCodes + 8u * tid, vm,
-                           dl, vmask, dv);
-            stg ^= 1;
+            head += tail_ws(a, sh, Obuf, ring, head, t, (uint32_t)t * kTileCodes + 8u * tid, vm, dl, vmask, dv);
         }
-        if (!a.rescan) {
-            if (tid == 0) {
-                st_relaxed_u64(&a.status[u], (u == 0 ? kStInc : kStAgg) | cnt);
-                sh.ready_unit[b] = u;
-                sh.ready_cnt[b] = cnt;
-            }
-            bar_arrive(1 + b, kWsThreads);
+        bar_sync(kBarCompute, kCta);   // all ring writes of the unit are done
+        if (!a.rescan && tid == 0) {
+            st_relaxed_u64(&a.status[u], (u == 0 ? kStInc : kStAgg) | (head - start));
+            while (sh.desc_head - sh.desc_tail >= (uint32_t)kDescQ) __nanosleep(32);
+            const uint32_t dh = sh.desc_head;
+            sh.desc[dh % kDescQ] = WsDesc{u, start, head - start, 0};
+            __threadfence_block();
+            sh.desc_head = dh + 1;
         }
-        ++k;
-        bar_sync(kBarCompute, kCta);
     }
 }
 
@@ -1476,7 +1488,9 @@ cudaError_t launch_compress(const CompressArgs& a_in, cudaStream_t st)
     const uint32_t ntiles = a.tile_end - a.tile_begin;
     LaunchProf lp(K_COMPRESS, st);
     if (vec && !(a.exp & 16)) {
-        sm += 2 * 2 * kTileCodes * sizeof(float);   // TMA input stages
+        // ws kernel: q storage + shuffle buffer + payload ring + one TMA input stage
+        sm = sizeof(int) * ((size_t)a.qwords + 32 * 33 + 8) + 16 * (size_t)kRingBlocks +
+             2 * kTileCodes * sizeof(float);
         switch (a.g.ndim) {
             case 1: return launch_compress_ws<1>(a, sm, ntiles, st);
             case 2: return launch_compress_ws<2>(a, sm, ntiles, st);

@@ -12,6 +12,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     d = np.load(cache) if os.path.exists(cache) else synth.generate(field, shape)
     if not os.path.exists(cache):
         np.save(cache, d)
+    if os.environ.get("AS2D"):
+        d = d.reshape(-1, shape[-1])
+        shape = d.shape
     x = torch.from_numpy(d).cuda()
     c = fz.Codec(shape, "cuda")
     for _ in range(3):
