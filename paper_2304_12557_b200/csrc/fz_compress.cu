@@ -1222,13 +1222,13 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
         // ================= scanner warp =================
         if (a.rescan) return;
         for (uint32_t dt = 0;; ++dt) {
-            while (sh.desc_head == dt) __nanosleep(64);
+            while (sh.desc_head == dt) __nanosleep(500);
             __threadfence_block();
             const WsDesc d = sh.desc[dt % kDescQ];
             if (d.unit == kNone) break;
             unsigned long long ex = 0;
             if (d.unit != 0) {
-                ex = lookback_wide<kLbLane, false>(a.status, d.unit, 0, kStAgg - 1, &ctrl->err);
+                ex = lookback_adaptive<kLbLane>(a.status, d.unit, kStAgg - 1, &ctrl->err);
                 if (lane == 0) st_relaxed_u64(&a.status[d.unit], kStInc | (ex + d.cnt));
             }
             for (uint32_t i = lane; i < d.cnt; i += 32) {

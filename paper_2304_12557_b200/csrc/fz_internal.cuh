@@ -259,6 +259,26 @@ __device__ __forceinline__ unsigned long long lookback_wide(const unsigned long 
     return sum;
 }
 
+// Look-back that first polls the nearest 32 predecessors (one status word per lane, backing
+// off while one is unpublished) and widens to WIDE words per lane only past them.
+template <int WIDE>
+__device__ __forceinline__ unsigned long long lookback_adaptive(const unsigned long long* st, int64_t t,
+                                                                unsigned long long vmask, int32_t* err)
+{
+    for (uint32_t spins = 0;; ++spins) {
+        if (spins > (1u << 22)) {
+            if ((threadIdx.x & 31) == 0) atomicExch(err, kErrStall);
+            return 0;
+        }
+        unsigned long long v[1], part;
+        lookback_load<1>(st, t - 1, 0, v);
+        const int r = lookback_eval<1, false>(v, vmask, part);
+        if (r == 1) return part;
+        if (r == 2) return part + lookback_wide<WIDE, false>(st, t - 32, 0, vmask, err);
+        __nanosleep(128);
+    }
+}
+
 // Non-blocking attempt on a window loaded earlier (lookback_load(st, t-1, first, v)).
 template <int PER_LANE>
 __device__ __forceinline__ bool lookback_try(const unsigned long long* st, int64_t t, int64_t first,
