@@ -9,6 +9,7 @@
 //   k_outlier_scan / k_outlier_place: outlier sections (only launched when outliers exist)
 //
 // Citation key: P:n = PAPER.md line n; R# = DESIGN.md §3 readings; SV = SURVEY.md.
+#include <cfloat>
 #include <cstdlib>
 
 #include "fz_internal.cuh"
@@ -71,34 +72,61 @@ __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint
 }
 
 // ------------------------------------------------------------------------------------
-// C0 range: grid-stride, 16-byte loads, warp reductions, one atomic per warp.
+// C0 range: grid-stride, four 16-byte loads in flight per thread, float min/max with one
+// finiteness test per element (the index of the first non-finite value is recovered on a
+// rare path), -0.0 canonicalized to +0.0 once per warp (R18), one atomic per warp.
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_range(const float* __restrict__ d, uint64_t n, Ctrl* ctrl)
 {
-    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+    constexpr int U = 4;
+    float lo = INFINITY, hi = -INFINITY;
     unsigned long long bad = ~0ull;
     const uint64_t nv4 = n / 4;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    auto take = [&](float v, uint64_t idx) {
-        if (!isfinite(v)) { bad = min(bad, (unsigned long long)idx); return; }
-        v = __fadd_rn(v, 0.0f);   // -0.0 -> +0.0 (R18)
-        uint32_t e = f2ord(v);
-        lo = min(lo, e);
-        hi = max(hi, e);
+    auto first_bad = [&](uint64_t i0, int cnt) {
+        for (int u = 0; u < cnt; ++u)
+            if (!(fabsf(__ldg(d + i0 + u)) <= FLT_MAX)) { bad = min(bad, (unsigned long long)(i0 + u)); return; }
     };
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nv4; k += stride) {
-        float4 v = ldg_f4(d + 4 * k);
-        take(v.x, 4 * k); take(v.y, 4 * k + 1); take(v.z, 4 * k + 2); take(v.w, 4 * k + 3);
+    uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; k + (U - 1) * stride < nv4; k += U * stride) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ldg_f4(d + 4 * (k + u * stride));
+        bool ok = true;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            lo = fminf(lo, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+            hi = fmaxf(hi, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+            ok &= fabsf(v[u].x) <= FLT_MAX && fabsf(v[u].y) <= FLT_MAX && fabsf(v[u].z) <= FLT_MAX &&
+                  fabsf(v[u].w) <= FLT_MAX;
+        }
+        if (!ok)
+            for (int u = 0; u < U; ++u) first_bad(4 * (k + u * stride), 4);
     }
-    for (uint64_t k = 4 * nv4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
-        take(__ldg(d + k), k);
-    lo = __reduce_min_sync(kFull, lo);
-    hi = __reduce_max_sync(kFull, hi);
+    for (; k < nv4; k += stride) {
+        const float4 v = ldg_f4(d + 4 * k);
+        lo = fminf(lo, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+        hi = fmaxf(hi, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+        if (!(fabsf(v.x) <= FLT_MAX && fabsf(v.y) <= FLT_MAX && fabsf(v.z) <= FLT_MAX && fabsf(v.w) <= FLT_MAX))
+            first_bad(4 * k, 4);
+    }
+    for (uint64_t j = 4 * nv4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const float v = __ldg(d + j);
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+        if (!(fabsf(v) <= FLT_MAX)) bad = min(bad, (unsigned long long)j);
+    }
+    // fminf/fmaxf skip NaN; non-finite inputs are reported through first_bad anyway
+    uint32_t elo = f2ord(__fadd_rn(lo, 0.0f)), ehi = f2ord(__fadd_rn(hi, 0.0f));
+    if (lo == INFINITY) elo = 0xFFFFFFFFu;   // no element seen by this thread
+    if (hi == -INFINITY) ehi = 0u;
+    elo = __reduce_min_sync(kFull, elo);
+    ehi = __reduce_max_sync(kFull, ehi);
     unsigned long long b = bad;
     for (int o = 16; o; o >>= 1) b = min(b, __shfl_xor_sync(kFull, b, o));
     if ((threadIdx.x & 31) == 0) {
-        atomicMin(&ctrl->mn_enc, lo);
-        atomicMax(&ctrl->mx_enc, hi);
+        atomicMin(&ctrl->mn_enc, elo);
+        atomicMax(&ctrl->mx_enc, ehi);
         if (b != ~0ull) atomicMin(&ctrl->first_bad, b);
     }
 }

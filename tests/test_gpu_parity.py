@@ -221,3 +221,29 @@ def test_fake_multirank_roundtrip_2d_1d(shape):
     stream, xh = dist.roundtrip_sharded_single_process(d, fz.ABS, 1e-2, 3, DEV)
     _assert_stream_equal(stream, ref, f"{shape}")
     assert np.array_equal(xh.view(np.uint32), xref.view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 7, 1000, 4 * 148 * 8 * 256 * 4 + 13, 5_000_003])
+def test_range_kernel_vs_oracle(n):
+    """C0: (min, max) with -0.0 canonicalized and the first non-finite index (R18), on sizes
+    that hit the scalar tail, the single-load loop and the 4-deep unrolled loop."""
+    rng = np.random.default_rng(n)
+    d = rng.normal(size=n).astype(np.float32) * np.float32(3.0)
+    work = torch.empty(fz.workspace_bytes((n,)), dtype=torch.uint8, device=DEV)
+    for case in range(4):
+        x = d.copy()
+        if case == 1:
+            x[:] = np.float32(-0.0)
+            x[n // 2] = np.float32(0.0)
+        if case == 2 and n > 2:
+            x[[n - 1, n // 3]] = [np.inf, np.nan]
+        if case == 3:
+            x[n - 1] = np.float32(-1e30)
+        mn, mx, bad = fz.slab_range(torch.from_numpy(x).to(DEV), work)
+        st, omn, omx, obad = O.field_range(x)
+        if st == O.ERR_NONFINITE:
+            assert bad == obad
+        else:
+            assert bad == -1
+            assert np.float32(mn).tobytes() == np.float32(omn).tobytes()
+            assert np.float32(mx).tobytes() == np.float32(omx).tobytes()
