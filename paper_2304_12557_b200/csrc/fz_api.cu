@@ -1,5 +1,6 @@
 // fz_api.cu -- the C ABI of libfz (include/fz.h): validation, workspace carving, launch
 // sequences, host<->device control-block round trips, status mapping.
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -62,6 +63,16 @@ static thread_local char g_cuda_err[256] = "";
 static thread_local int g_last_launches = 0;
 
 namespace {
+
+// FZ_EXP: experiment bits for A/B timing (128: unfused y scan in the decoder).
+int exp_bits()
+{
+    static const int v = [] {
+        const char* e = getenv("FZ_EXP");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
 
 struct LaunchScope {
     LaunchScope() { fz::t_launches = 0; }
@@ -408,6 +419,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     int32_t* q = d_q ? d_q : reinterpret_cast<int32_t*>(d_field);
     const bool deq = d_q == nullptr;
 
+    const bool fuse_y = decode_fuses_y(I.shape) && !(exp_bits() & 128);
     FZ_CUDA(launch_decode_init(ctrl, st));
     FZ_CUDA(launch_validate_outliers(drec, I.counts.n_delta, n, ctrl, st));
     FZ_CUDA(launch_validate_outliers(vrec, I.counts.n_value, n, ctrl, st));
@@ -426,7 +438,8 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     a.bpre = bsum;
     a.xagg = xagg;
     a.ctrl = ctrl;
-    FZ_CUDA(launch_decode_tiles(a, st));
+    if (fuse_y) a.tpp = (uint32_t)(I.shape.dims[1] * I.shape.dims[2] / kTileCodes);
+    FZ_CUDA(launch_decode_tiles(a, st, fuse_y));
     // x carries exist when some tile starts inside a row (always for 1-D fields)
     const bool carries = T > 1 && (g.ndim == 1 || !(g.nx <= kTileCodes && kTileCodes % g.nx == 0));
     if (g.ndim == 1 && !deq) a.w = 0.0f;
@@ -437,9 +450,10 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     }
     const float wq = deq ? I.params.w : 0.0f;
     if (I.shape.ndim == 2) {
-        FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1], sums, wq, st));
+        if (!fuse_y) FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1], sums, wq, st));
     } else if (I.shape.ndim == 3) {
-        FZ_CUDA(launch_scan_axis(q, I.shape.dims[0], I.shape.dims[1], I.shape.dims[2], sums, 0.0f, st));
+        if (!fuse_y)
+            FZ_CUDA(launch_scan_axis(q, I.shape.dims[0], I.shape.dims[1], I.shape.dims[2], sums, 0.0f, st));
         FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], sums, wq, st));
     }
     if (deq) FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));

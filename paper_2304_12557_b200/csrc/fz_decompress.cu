@@ -15,6 +15,17 @@ namespace fz {
 
 constexpr int kScanChunk = 32;
 
+// The y prefix sum is fused into the tile decode when every tile holds whole rows
+// (nx | 2048, nx >= 256 so a tile has at most 8 rows) and no tile straddles two planes.
+bool decode_fuses_y(const fz_shape& s)
+{
+    if (s.ndim != 3) return false;
+    const uint64_t nx = s.dims[2];
+    if (nx < 256 || nx > (uint64_t)kTileCodes || kTileCodes % nx != 0) return false;
+    if ((s.dims[1] * nx) % kTileCodes != 0) return false;
+    return s.dims[0] >= 2 * 148;    // one CTA per plane: enough planes to fill the GPU
+}
+
 // Decode workspace: control block, per-tile block offsets (two-level exclusive scan of the
 // flag popcounts), per-tile x-scan aggregates and carries, chunk sums of the axis scans.
 DecodeLayout decode_layout(const fz_shape& s)
@@ -217,22 +228,25 @@ __global__ void __launch_bounds__(1024) k_xseg_top(uint2* xbagg, uint32_t nb)
 }
 
 // ------------------------------------------------------------------------------------
-// Tile decoder (D2-D4 + the local part of D5 along x).  Tiles are independent: the payload
-// offset of tile t is bsum[t/1024] + loc[t].  Per tile: gather the nonzero 16-byte blocks,
-// un-shuffle (same 32x32 bit transpose), unpack (0x8000 -> 0), delta patch, segmented
-// inclusive x-scan inside the tile (resets at row starts), write q, publish the tile's
-// aggregate (row start seen, sum since the last row start) for the x carries.
+// D1-D5(x) for one tile: payload offsets from the flags, gather of the 16-byte blocks,
+// register un-shuffle, unpack, delta-outlier patch, segmented inclusive x-scan inside the
+// tile.  Returns the thread's 8 x-prefixed values (elements 8*tid .. 8*tid+7 of the tile);
+// elements before the thread's first row start carry only the in-tile prefix (the carry
+// from earlier tiles is added by k_xfix where a row spans tiles).  (lo, hi): the tile's
+// delta-outlier records, found by the caller.
 // ------------------------------------------------------------------------------------
+struct DecSmem {
+    uint32_t Obuf[32 * 33];
+    __align__(16) int32_t D[kTileCodes];
+    uint32_t F[8], wf[8], wv[8];
+    uint64_t lo, hi;
+};
+
 template <int NDIM>
-__global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
+__device__ __forceinline__ Seg decode_tile_x(const DecodeArgs& a, DecSmem& sm, uint32_t t, uint32_t (&q)[8])
 {
-    __shared__ uint32_t Obuf[32 * 33];
-    __shared__ int32_t D[kTileCodes];
-    __shared__ uint32_t s_F[8], s_wf[8], s_wv[8];
-    __shared__ uint64_t s_lo, s_hi;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t n = a.g.n, nx = a.g.nx;
-    const uint32_t t = blockIdx.x;          // one CTA per tile: many tiles in flight per SM
+    const uint32_t nx = a.g.nx;
     const int64_t s = (int64_t)t * kTileCodes;
     const uint32_t g0 = (uint32_t)s + 8u * tid;
     // ---- D1/D2: all independent loads first (flags word, offsets) ----
@@ -248,24 +262,10 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
         for (int u = 0; u < 8; ++u)
             if (fmod_(g0 + u, a.dnx) == 0) xm_rs |= 1u << u;
     }
-    if (lane == 0) s_F[warp] = F;
-    if (tid == 32) {
-        uint64_t lo = 0, hi = 0;
-        if (a.nd > 0) {
-            const int64_t gs = s + (int64_t)a.gbase;   // records hold global indices
-            uint64_t l = 0, h = a.nd;
-            while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs) l = m + 1; else h = m; }
-            lo = l;
-            h = a.nd;
-            while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs + kTileCodes) l = m + 1; else h = m; }
-            hi = l;
-        }
-        s_lo = lo;
-        s_hi = hi;
-    }
+    if (lane == 0) sm.F[warp] = F;
     __syncthreads();
     {
-        const uint32_t fw = lane < 8 ? s_F[lane] : 0u;
+        const uint32_t fw = lane < 8 ? sm.F[lane] : 0u;
         const uint32_t wpre = __reduce_add_sync(kFull, lane < warp ? __popc(fw) : 0u);
         uint4 blk = make_uint4(0, 0, 0, 0);
         if ((F >> lane) & 1u) {
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
             if (bi < a.nnz_total) blk = __ldcs(reinterpret_cast<const uint4*>(a.payload) + bi);
             else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
         }
-        uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+        uint32_t* row = sm.Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
         row[0] = blk.x; row[1] = blk.y; row[2] = blk.z; row[3] = blk.w;
     }
     __syncthreads();
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
     {
         const int c = tid >> 3, kk = tid & 7;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) w4[i] = Obuf[(4 * kk + i) * 33 + c];
+        for (int i = 0; i < 4; ++i) w4[i] = sm.Obuf[(4 * kk + i) * 33 + c];
         transpose32_group8(w4, lane & 7);
     }
     // ---- D4: unpack, delta outliers ----
@@ -293,17 +293,18 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
         dl[2 * i] = (lo16 & 0x8000u) ? -(int32_t)(lo16 & 0x7FFFu) : (int32_t)lo16;
         dl[2 * i + 1] = (hi16 & 0x8000u) ? -(int32_t)(hi16 & 0x7FFFu) : (int32_t)hi16;
     }
-    if (s_hi > s_lo) {   // rare, block-uniform
+    const uint64_t rlo = sm.lo, rhi = sm.hi;
+    if (rhi > rlo) {   // rare, block-uniform
 #pragma unroll
-        for (int u = 0; u < 8; ++u) D[8 * tid + u] = dl[u];
+        for (int u = 0; u < 8; ++u) sm.D[8 * tid + u] = dl[u];
         __syncthreads();
-        for (uint64_t k = s_lo + tid; k < s_hi; k += kCta) {
+        for (uint64_t k = rlo + tid; k < rhi; k += kCta) {
             const uint2 r = a.drec[k];
-            D[(uint32_t)(r.x - a.gbase - (uint64_t)s)] = (int32_t)r.y;
+            sm.D[(uint32_t)(r.x - a.gbase - (uint64_t)s)] = (int32_t)r.y;
         }
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 8; ++u) dl[u] = D[8 * tid + u];
+        for (int u = 0; u < 8; ++u) dl[u] = sm.D[8 * tid + u];
     }
     // ---- D5 (x, local): segmented inclusive scan, resets at row starts ----
     uint32_t loc[8];
@@ -322,23 +323,58 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
     }
     Seg lex{__shfl_up_sync(kFull, inc.f, 1), __shfl_up_sync(kFull, inc.v, 1)};
     if (lane == 0) lex = Seg{0, 0};
-    if (lane == 31) { s_wf[warp] = inc.f; s_wv[warp] = inc.v; }
+    if (lane == 31) { sm.wf[warp] = inc.f; sm.wv[warp] = inc.v; }
     __syncthreads();
     Seg wp{0, 0}, tagg{0, 0};
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-        const Seg sw{s_wf[w], s_wv[w]};
+        const Seg sw{sm.wf[w], sm.wv[w]};
         if (w < warp) wp = seg_combine(wp, sw);
         tagg = seg_combine(tagg, sw);
     }
-    if (tid == 0) a.xagg[t] = make_uint2(tagg.f, tagg.v);
-    // elements before the thread's first row start get the in-tile prefix; the carry from
-    // earlier tiles is added by k_xfix where needed
     const Seg acc = seg_combine(wp, lex);
-    uint32_t q[8];
     const uint32_t pre = xm_rs ? ((xm_rs & (0u - xm_rs)) - 1u) : 0xFFu;   // elements before it
 #pragma unroll
     for (int u = 0; u < 8; ++u) q[u] = ((pre >> u) & 1u) ? acc.v + loc[u] : loc[u];
+    return tagg;
+}
+
+// [lo, hi) of the delta-outlier records of the elements [gs, ge) (global indices), searched
+// from `from` on (records ascend): galloping then binary search.
+__device__ __forceinline__ uint64_t records_before(const uint2* rec, uint64_t nd, uint64_t from, int64_t ge)
+{
+    uint64_t l = from, step = 1;
+    while (l + step <= nd && (int64_t)rec[l + step - 1].x < ge) { l += step; step *= 2; }
+    uint64_t h = l + step <= nd ? l + step : nd;
+    while (l < h) { const uint64_t m = (l + h) / 2; if ((int64_t)rec[m].x < ge) l = m + 1; else h = m; }
+    return l;
+}
+
+// One CTA per tile: many tiles in flight per SM.
+template <int NDIM>
+__global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
+{
+    __shared__ DecSmem sm;
+    const int tid = threadIdx.x;
+    const uint32_t n = a.g.n;
+    const uint32_t t = blockIdx.x;
+    const int64_t s = (int64_t)t * kTileCodes;
+    const uint32_t g0 = (uint32_t)s + 8u * tid;
+    if (tid == 32) {
+        uint64_t lo = 0, hi = 0;
+        if (a.nd > 0) {
+            const int64_t gs = s + (int64_t)a.gbase;   // records hold global indices
+            uint64_t l = 0, h = a.nd;
+            while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs) l = m + 1; else h = m; }
+            lo = l;
+            hi = records_before(a.drec, a.nd, lo, gs + kTileCodes);
+        }
+        sm.lo = lo;
+        sm.hi = hi;
+    }
+    uint32_t q[8];
+    const Seg tagg = decode_tile_x<NDIM>(a, sm, t, q);
+    if (tid == 0) a.xagg[t] = make_uint2(tagg.f, tagg.v);
     if (s + kTileCodes <= (int64_t)n) {
         int4* o = reinterpret_cast<int4*>(a.q_out + g0);
         __stcs(o, make_int4((int)q[0], (int)q[1], (int)q[2], (int)q[3]));
@@ -347,6 +383,72 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
 #pragma unroll
         for (int u = 0; u < 8; ++u)
             if (g0 + u < n) a.q_out[g0 + u] = (int32_t)q[u];
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// D1-D5(x, y) for 3-D fields whose tiles hold R = 2048/nx whole rows of one plane
+// (R in {1, 2, 4, 8}): one CTA per plane walks the plane's tiles in order.  After the x scan
+// each thread takes C = 8/R whole columns of the tile (all R rows) from shared memory and
+// runs the y prefix sum down them with its running column carries in registers, so the y
+// scan costs no extra pass over HBM and no inter-CTA communication.  The z scan follows.
+// ------------------------------------------------------------------------------------
+template <int R>
+__global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
+{
+    constexpr int C = 8 / R;
+    __shared__ DecSmem sm;
+    const int tid = threadIdx.x;
+    const uint32_t nx = a.g.nx, z = blockIdx.x;
+    uint32_t carry[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) carry[c] = 0;
+    uint64_t rec = 0;       // delta-outlier cursor (records ascend)
+    if (tid == 32 && a.nd > 0) {
+        const int64_t gs = (int64_t)z * a.tpp * kTileCodes;
+        uint64_t l = 0, h = a.nd;
+        while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs) l = m + 1; else h = m; }
+        rec = l;
+    }
+    for (uint32_t k = 0; k < a.tpp; ++k) {
+        const uint32_t t = z * a.tpp + k;
+        const int64_t s = (int64_t)t * kTileCodes;
+        if (tid == 32) {
+            uint64_t hi = rec;
+            if (a.nd > 0) hi = records_before(a.drec, a.nd, rec, s + kTileCodes);
+            sm.lo = rec;
+            sm.hi = hi;
+            rec = hi;
+        }
+        uint32_t q[8];
+        decode_tile_x<3>(a, sm, t, q);
+        *reinterpret_cast<uint4*>(sm.D + 8 * tid) = make_uint4(q[0], q[1], q[2], q[3]);
+        *reinterpret_cast<uint4*>(sm.D + 8 * tid + 4) = make_uint4(q[4], q[5], q[6], q[7]);
+        __syncthreads();
+        uint32_t v[R][C];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                carry[c] += (uint32_t)sm.D[r * nx + C * tid + c];
+                v[r][c] = carry[c];
+            }
+        }
+        int32_t* o = a.q_out + s + C * tid;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if constexpr (C == 1) {
+                __stcs(o + r * nx, (int32_t)v[r][0]);
+            } else if constexpr (C == 2) {
+                __stcs(reinterpret_cast<int2*>(o + r * nx), make_int2((int)v[r][0], (int)v[r][1]));
+            } else {
+#pragma unroll
+                for (int c = 0; c < C; c += 4)
+                    __stcs(reinterpret_cast<int4*>(o + r * nx + c),
+                           make_int4((int)v[r][c], (int)v[r][c + 1], (int)v[r][c + 2], (int)v[r][c + 3]));
+            }
+        }
+        __syncthreads();    // sm.D and sm.Obuf are reused by the next tile
     }
 }
 
@@ -566,13 +668,25 @@ static cudaError_t launch_decode_t(const DecodeArgs& a_in, cudaStream_t st)
     return cudaGetLastError();
 }
 
-cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st)
+cudaError_t launch_decode_tiles(const DecodeArgs& a_in, cudaStream_t st, bool fuse_y)
 {
     LaunchProf lp(K_DECODE, st);
-    switch (a.g.ndim) {
-        case 1: return launch_decode_t<1>(a, st);
-        case 2: return launch_decode_t<2>(a, st);
-        default: return launch_decode_t<3>(a, st);
+    if (fuse_y) {
+        DecodeArgs a = a_in;
+        a.dnx = make_fastdiv(a.g.nx);
+        const uint32_t planes = a.g.n / a.g.P;
+        switch (kTileCodes / a.g.nx) {
+            case 1: k_decode_planes<1><<<planes, kCta, 0, st>>>(a); break;
+            case 2: k_decode_planes<2><<<planes, kCta, 0, st>>>(a); break;
+            case 4: k_decode_planes<4><<<planes, kCta, 0, st>>>(a); break;
+            default: k_decode_planes<8><<<planes, kCta, 0, st>>>(a); break;
+        }
+        return cudaGetLastError();
+    }
+    switch (a_in.g.ndim) {
+        case 1: return launch_decode_t<1>(a_in, st);
+        case 2: return launch_decode_t<2>(a_in, st);
+        default: return launch_decode_t<3>(a_in, st);
     }
 }
 

@@ -56,7 +56,12 @@ struct DecodeArgs {
     const uint32_t* bpre;       // exclusive block offset of each group of 1024 tiles
     uint2* xagg;                // per-tile x-scan aggregate (row start seen, sum)
     Ctrl* ctrl;
+    uint32_t tpp;               // tiles per plane (fused y scan)
 };
+
+// The y scan runs inside the decode (one CTA per plane) when every tile holds whole rows of
+// one plane and there are enough planes to fill the GPU.
+bool decode_fuses_y(const fz_shape& s);
 
 struct DecodeLayout {
     size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, total;
@@ -69,7 +74,7 @@ cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n,
                                      cudaStream_t st);
 cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum,
                                 Ctrl* ctrl, cudaStream_t st);
-cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st);
+cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st, bool fuse_y = false);
 cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool carries, cudaStream_t st);
 // inclusive prefix sum along an axis of a [outer][L][W] int32 array (mod 2^32); when
 // dequant_w > 0 the final values are written as fl32(fl32(q) * w) floats in place.

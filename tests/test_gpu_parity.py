@@ -247,3 +247,36 @@ def test_range_kernel_vs_oracle(n):
             assert bad == -1
             assert np.float32(mn).tobytes() == np.float32(omn).tobytes()
             assert np.float32(mx).tobytes() == np.float32(omx).tobytes()
+
+
+# Shapes on the decoder's fused-y path (k_decode_planes: 3-D, nz >= 296, nx in
+# {256..2048} dividing the tile, tiles inside planes): R = 8, 4, 2, 1 rows per tile with two
+# or more tiles per plane, one tile per plane, and delta outliers inside fused planes.
+FUSED_Y = [
+    ("r8", lambda: synth.generate("nyx_rho", (296, 16, 256))),
+    ("r4", lambda: synth.generate("nyx_v", (296, 8, 512))),
+    ("r2", lambda: synth.generate("hurr_u", (300, 4, 1024))),
+    ("r1", lambda: synth.generate("rtm", (300, 2, 2048))),
+    ("one_tile_per_plane", lambda: synth.generate("sines3d", (300, 8, 256))),
+    ("tpp4", lambda: synth.generate("sines3d", (300, 32, 256))),
+]
+
+
+@pytest.mark.parametrize("name,gen", FUSED_Y, ids=[s[0] for s in FUSED_Y])
+@pytest.mark.parametrize("rel", [1e-2, 1e-4])
+def test_fused_y_decode_parity(name, gen, rel):
+    _check_full(gen(), O.REL, rel, f"{name}@{rel}")
+
+
+def test_fused_y_decode_with_outliers():
+    d = synth.generate("nyx_rho", (296, 8, 512)).copy()
+    eb = float(d.max() - d.min()) * 1e-4
+    rng = np.random.default_rng(11)
+    idx = rng.choice(d.size, 300, replace=False)
+    d.reshape(-1)[idx] += np.float32(50.0) * np.float32(d.max() - d.min())
+    ref = _check_full(d, O.ABS, eb, "fused_y_outliers")
+    assert int.from_bytes(ref[96:104].tobytes(), "little") > 0      # delta outliers present
+    st, qref = O.decode_q(ref, d.size)
+    assert st == O.OK
+    q = fz.debug_decode_q(torch.from_numpy(ref).to(DEV), d.shape)
+    assert np.array_equal(q.cpu().numpy(), qref)
