@@ -424,6 +424,8 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     FZ_CUDA(launch_validate_outliers(drec, I.counts.n_delta, n, ctrl, st));
     FZ_CUDA(launch_validate_outliers(vrec, I.counts.n_value, n, ctrl, st));
     FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st));
+    auto* drange = reinterpret_cast<uint32_t*>(wb + L.drange);
+    FZ_CUDA(launch_record_tiles(drec, I.counts.n_delta, (uint32_t)T, 0, drange, st));
     DecodeArgs a{};
     a.flags = in + kHeaderBytes;
     a.payload = in + pbase;
@@ -438,6 +440,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     a.bpre = bsum;
     a.xagg = xagg;
     a.ctrl = ctrl;
+    a.drange = drange;
     if (fuse_y) a.tpp = (uint32_t)(I.shape.dims[1] * I.shape.dims[2] / kTileCodes);
     FZ_CUDA(launch_decode_tiles(a, st, fuse_y));
     // x carries exist when some tile starts inside a row (always for 1-D fields)
@@ -788,10 +791,13 @@ fz_status fz_slab_decode(const void* d_stage, const fz_counts* local, const fz_s
     FZ_CUDA(launch_decode_init(ctrl, st));
     FZ_CUDA(launch_tile_offsets(in, (uint32_t)nt, reinterpret_cast<uint32_t*>(wb + L.loc),
                                 reinterpret_cast<uint32_t*>(wb + L.bsum), ctrl, st));
+    FZ_CUDA(launch_record_tiles(reinterpret_cast<const uint2*>(in + dbase), local->n_delta, (uint32_t)nt, sg.g0,
+                                reinterpret_cast<uint32_t*>(wb + L.drange), st));
     DecodeArgs a{};
     a.flags = in;
     a.payload = in + pbase;
     a.drec = reinterpret_cast<const uint2*>(in + dbase);
+    a.drange = reinterpret_cast<const uint32_t*>(wb + L.drange);
     a.nnz_total = local->nnz;
     a.nd = local->n_delta;
     a.g = g;

@@ -52,6 +52,7 @@ DecodeLayout decode_layout(const fz_shape& s)
     L.xloc = off;   off = al(off + 8 * T);
     L.xbagg = off;  off = al(off + 8 * nb);
     L.sums = off;   off = al(off + 4 * sums);
+    L.drange = off; off = al(off + 4 * (T + 1));
     L.sums_elems = sums;
     L.total = off;
     return L;
@@ -72,6 +73,24 @@ __global__ void k_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, 
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t idx = rec[k].x;
         if (idx >= n || (k > 0 && rec[k - 1].x >= idx)) atomicExch(&ctrl->err, (int)FZ_ERR_CORRUPT);
+    }
+}
+
+// Per-tile delta-outlier ranges: records [drange[t], drange[t+1]) fall in tile t (records
+// ascend; entries are clamped by the reader, so a corrupt list cannot index out of range).
+__global__ void k_record_tiles(const uint2* __restrict__ rec, uint64_t nd, uint32_t ntiles, uint64_t gbase,
+                               uint32_t* __restrict__ drange)
+{
+    auto tile_of = [&](uint64_t k) -> int64_t {
+        const int64_t rel = (int64_t)rec[k].x - (int64_t)gbase;
+        const int64_t tk = rel < 0 ? 0 : rel / kTileCodes;
+        return tk < (int64_t)ntiles ? tk : (int64_t)ntiles;
+    };
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nd;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t tk = k < nd ? tile_of(k) : (int64_t)ntiles;
+        const int64_t tp = k > 0 ? tile_of(k - 1) : -1;
+        for (int64_t t = tp + 1; t <= tk; ++t) drange[t] = (uint32_t)k;
     }
 }
 
@@ -238,20 +257,54 @@ __global__ void __launch_bounds__(1024) k_xseg_top(uint2* xbagg, uint32_t nb)
 struct DecSmem {
     uint32_t Obuf[32 * 33];
     __align__(16) int32_t D[kTileCodes];
-    uint32_t F[8], wf[8], wv[8];
-    uint64_t lo, hi;
+    uint32_t wf[8], wv[8];
 };
 
+// Independent loads of a tile: lanes 0-7 of every warp hold the tile's 8 flag words, every
+// lane its payload base and delta-outlier record range.
+struct TileIn {
+    uint32_t fw;
+    uint64_t tbase;
+    uint32_t rlo, rhi;
+};
+
+__device__ __forceinline__ TileIn tile_in(const DecodeArgs& a, uint32_t t)
+{
+    const int lane = threadIdx.x & 31;
+    TileIn in;
+    in.fw = lane < 8 ? __ldg(reinterpret_cast<const uint32_t*>(a.flags) + 8 * (uint64_t)t + lane) : 0u;
+    in.tbase = (uint64_t)__ldg(a.bpre + (t >> 10)) + __ldg(a.loc + t);
+    in.rlo = in.rhi = 0;
+    if (a.nd > 0) {
+        in.rlo = __ldg(a.drange + t);
+        in.rhi = __ldg(a.drange + t + 1);
+    }
+    return in;
+}
+
+// The thread's 16-byte payload block of the tile (zero when its flag bit is clear).
+__device__ __forceinline__ uint4 tile_blk(const DecodeArgs& a, const TileIn& in)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t F = __shfl_sync(kFull, in.fw, warp);
+    const uint32_t wpre = __reduce_add_sync(kFull, lane < warp ? __popc(in.fw) : 0u);
+    uint4 blk = make_uint4(0, 0, 0, 0);
+    if ((F >> lane) & 1u) {
+        const uint64_t bi = in.tbase + wpre + __popc(F & ((1u << lane) - 1u));
+        if (bi < a.nnz_total) blk = __ldcs(reinterpret_cast<const uint4*>(a.payload) + bi);
+        else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
+    }
+    return blk;
+}
+
 template <int NDIM>
-__device__ __forceinline__ Seg decode_tile_x(const DecodeArgs& a, DecSmem& sm, uint32_t t, uint32_t (&q)[8])
+__device__ __forceinline__ Seg decode_tile_x(const DecodeArgs& a, DecSmem& sm, uint32_t t, const uint4& blk,
+                                             uint32_t rlo, uint32_t rhi, uint32_t (&q)[8])
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t nx = a.g.nx;
     const int64_t s = (int64_t)t * kTileCodes;
     const uint32_t g0 = (uint32_t)s + 8u * tid;
-    // ---- D1/D2: all independent loads first (flags word, offsets) ----
-    const uint32_t F = reinterpret_cast<const uint32_t*>(a.flags)[8 * (uint64_t)t + warp];
-    const uint64_t tbase = (uint64_t)a.bpre[t >> 10] + a.loc[t];
     uint32_t xm_rs = 0;                      // row-start bit per element
     if (nx >= 8) {
         const uint32_t x0 = fmod_(g0, a.dnx);
@@ -262,17 +315,7 @@ __device__ __forceinline__ Seg decode_tile_x(const DecodeArgs& a, DecSmem& sm, u
         for (int u = 0; u < 8; ++u)
             if (fmod_(g0 + u, a.dnx) == 0) xm_rs |= 1u << u;
     }
-    if (lane == 0) sm.F[warp] = F;
-    __syncthreads();
     {
-        const uint32_t fw = lane < 8 ? sm.F[lane] : 0u;
-        const uint32_t wpre = __reduce_add_sync(kFull, lane < warp ? __popc(fw) : 0u);
-        uint4 blk = make_uint4(0, 0, 0, 0);
-        if ((F >> lane) & 1u) {
-            const uint64_t bi = tbase + wpre + __popc(F & ((1u << lane) - 1u));
-            if (bi < a.nnz_total) blk = __ldcs(reinterpret_cast<const uint4*>(a.payload) + bi);
-            else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
-        }
         uint32_t* row = sm.Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
         row[0] = blk.x; row[1] = blk.y; row[2] = blk.z; row[3] = blk.w;
     }
@@ -293,14 +336,18 @@ __device__ __forceinline__ Seg decode_tile_x(const DecodeArgs& a, DecSmem& sm, u
         dl[2 * i] = (lo16 & 0x8000u) ? -(int32_t)(lo16 & 0x7FFFu) : (int32_t)lo16;
         dl[2 * i + 1] = (hi16 & 0x8000u) ? -(int32_t)(hi16 & 0x7FFFu) : (int32_t)hi16;
     }
-    const uint64_t rlo = sm.lo, rhi = sm.hi;
+    const uint32_t nd32 = (uint32_t)a.nd;
+    rlo = rlo < nd32 ? rlo : nd32;
+    rhi = rhi < rlo ? rlo : (rhi < nd32 ? rhi : nd32);
     if (rhi > rlo) {   // rare, block-uniform
 #pragma unroll
         for (int u = 0; u < 8; ++u) sm.D[8 * tid + u] = dl[u];
         __syncthreads();
-        for (uint64_t k = rlo + tid; k < rhi; k += kCta) {
+        for (uint32_t k = rlo + tid; k < rhi; k += kCta) {
             const uint2 r = a.drec[k];
-            sm.D[(uint32_t)(r.x - a.gbase - (uint64_t)s)] = (int32_t)r.y;
+            const uint64_t e = (uint64_t)r.x - a.gbase - (uint64_t)s;
+            if (e < (uint64_t)kTileCodes) sm.D[e] = (int32_t)r.y;
+            else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
         }
         __syncthreads();
 #pragma unroll
@@ -339,17 +386,6 @@ __device__ __forceinline__ Seg decode_tile_x(const DecodeArgs& a, DecSmem& sm, u
     return tagg;
 }
 
-// [lo, hi) of the delta-outlier records of the elements [gs, ge) (global indices), searched
-// from `from` on (records ascend): galloping then binary search.
-__device__ __forceinline__ uint64_t records_before(const uint2* rec, uint64_t nd, uint64_t from, int64_t ge)
-{
-    uint64_t l = from, step = 1;
-    while (l + step <= nd && (int64_t)rec[l + step - 1].x < ge) { l += step; step *= 2; }
-    uint64_t h = l + step <= nd ? l + step : nd;
-    while (l < h) { const uint64_t m = (l + h) / 2; if ((int64_t)rec[m].x < ge) l = m + 1; else h = m; }
-    return l;
-}
-
 // One CTA per tile: many tiles in flight per SM.
 template <int NDIM>
 __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
@@ -360,20 +396,10 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
     const uint32_t t = blockIdx.x;
     const int64_t s = (int64_t)t * kTileCodes;
     const uint32_t g0 = (uint32_t)s + 8u * tid;
-    if (tid == 32) {
-        uint64_t lo = 0, hi = 0;
-        if (a.nd > 0) {
-            const int64_t gs = s + (int64_t)a.gbase;   // records hold global indices
-            uint64_t l = 0, h = a.nd;
-            while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs) l = m + 1; else h = m; }
-            lo = l;
-            hi = records_before(a.drec, a.nd, lo, gs + kTileCodes);
-        }
-        sm.lo = lo;
-        sm.hi = hi;
-    }
+    const TileIn in = tile_in(a, t);
+    const uint4 blk = tile_blk(a, in);
     uint32_t q[8];
-    const Seg tagg = decode_tile_x<NDIM>(a, sm, t, q);
+    const Seg tagg = decode_tile_x<NDIM>(a, sm, t, blk, in.rlo, in.rhi, q);
     if (tid == 0) a.xagg[t] = make_uint2(tagg.f, tagg.v);
     if (s + kTileCodes <= (int64_t)n) {
         int4* o = reinterpret_cast<int4*>(a.q_out + g0);
@@ -399,29 +425,26 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
     constexpr int C = 8 / R;
     __shared__ DecSmem sm;
     const int tid = threadIdx.x;
-    const uint32_t nx = a.g.nx, z = blockIdx.x;
+    const uint32_t nx = a.g.nx, z = blockIdx.x, t0 = z * a.tpp;
     uint32_t carry[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) carry[c] = 0;
-    uint64_t rec = 0;       // delta-outlier cursor (records ascend)
-    if (tid == 32 && a.nd > 0) {
-        const int64_t gs = (int64_t)z * a.tpp * kTileCodes;
-        uint64_t l = 0, h = a.nd;
-        while (l < h) { uint64_t m = (l + h) / 2; if ((int64_t)a.drec[m].x < gs) l = m + 1; else h = m; }
-        rec = l;
-    }
+    // two-stage software pipeline: payload block of tile k+1, flags/offsets of tile k+2
+    TileIn in_cur = tile_in(a, t0);
+    uint4 blk_next = tile_blk(a, in_cur);
+    TileIn in_next = a.tpp > 1 ? tile_in(a, t0 + 1) : in_cur;
     for (uint32_t k = 0; k < a.tpp; ++k) {
-        const uint32_t t = z * a.tpp + k;
+        const uint32_t t = t0 + k;
         const int64_t s = (int64_t)t * kTileCodes;
-        if (tid == 32) {
-            uint64_t hi = rec;
-            if (a.nd > 0) hi = records_before(a.drec, a.nd, rec, s + kTileCodes);
-            sm.lo = rec;
-            sm.hi = hi;
-            rec = hi;
+        const uint4 blk = blk_next;
+        const uint32_t rlo = in_cur.rlo, rhi = in_cur.rhi;
+        if (k + 1 < a.tpp) {
+            blk_next = tile_blk(a, in_next);
+            in_cur = in_next;
+            if (k + 2 < a.tpp) in_next = tile_in(a, t + 2);
         }
         uint32_t q[8];
-        decode_tile_x<3>(a, sm, t, q);
+        decode_tile_x<3>(a, sm, t, blk, rlo, rhi, q);
         *reinterpret_cast<uint4*>(sm.D + 8 * tid) = make_uint4(q[0], q[1], q[2], q[3]);
         *reinterpret_cast<uint4*>(sm.D + 8 * tid + 4) = make_uint4(q[4], q[5], q[6], q[7]);
         __syncthreads();
@@ -640,6 +663,15 @@ cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n,
     if (cnt == 0) return cudaSuccess;
     LaunchProf lp(K_VALIDATE, st);
     k_validate_outliers<<<grid_for(cnt), 256, 0, st>>>(rec, cnt, n, ctrl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,
+                                cudaStream_t st)
+{
+    if (nd == 0) return cudaSuccess;
+    LaunchProf lp(K_OFFSETS, st);
+    k_record_tiles<<<grid_for(nd + 1), 256, 0, st>>>(drec, nd, ntiles, gbase, drange);
     return cudaGetLastError();
 }
 

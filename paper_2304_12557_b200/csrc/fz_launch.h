@@ -57,6 +57,7 @@ struct DecodeArgs {
     uint2* xagg;                // per-tile x-scan aggregate (row start seen, sum)
     Ctrl* ctrl;
     uint32_t tpp;               // tiles per plane (fused y scan)
+    const uint32_t* drange;     // per-tile delta-outlier record ranges (k_record_tiles)
 };
 
 // The y scan runs inside the decode (one CTA per plane) when every tile holds whole rows of
@@ -64,7 +65,7 @@ struct DecodeArgs {
 bool decode_fuses_y(const fz_shape& s);
 
 struct DecodeLayout {
-    size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, total;
+    size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, drange, total;
     uint64_t sums_elems;
 };
 DecodeLayout decode_layout(const fz_shape& s);
@@ -74,6 +75,8 @@ cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n,
                                      cudaStream_t st);
 cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum,
                                 Ctrl* ctrl, cudaStream_t st);
+cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,
+                                cudaStream_t st);
 cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st, bool fuse_y = false);
 cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool carries, cudaStream_t st);
 // inclusive prefix sum along an axis of a [outer][L][W] int32 array (mod 2^32); when
