@@ -8,6 +8,9 @@
 //   k_scan_*        D5(y, z): inclusive prefix sums along y and z (reduce-then-scan in
 //                   chunks of 32 rows), D6 dequantization fused into the last axis.
 //   k_value_patch   D6: value outliers get their raw bits back.
+#include <cstdlib>
+#include <type_traits>
+
 #include "fz_internal.cuh"
 #include "fz_launch.h"
 
@@ -590,6 +593,54 @@ __global__ void __launch_bounds__(256) k_scan_walk(int32_t* v, uint64_t outer, u
     }
 }
 
+// Vector walk: V adjacent columns per thread (W % V == 0, rows 16-byte aligned for V = 4),
+// U rows in flight; same arithmetic as k_scan_walk.
+template <int V, int U>
+__global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
+                                                     float dequant_w, const int32_t* __restrict__ carry)
+{
+    using VT = typename std::conditional<V == 4, int4, int2>::type;
+    const uint64_t Wv = W / V;
+    const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= outer * Wv) return;
+    const uint64_t w = (gid % Wv) * V, o = gid / Wv;
+    int32_t* p = v + o * L * W + w;
+    uint32_t acc[V];
+#pragma unroll
+    for (int c = 0; c < V; ++c) acc[c] = carry ? (uint32_t)carry[w + c] : 0u;
+    auto emit = [&](int32_t* q, const uint32_t (&x)[V]) {
+        uint32_t y[V];
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+            acc[c] += x[c];
+            y[c] = dequant_w > 0.0f ? __float_as_uint(__fmul_rn(__int2float_rn((int32_t)acc[c]), dequant_w)) : acc[c];
+        }
+        if constexpr (V == 4) __stcs(reinterpret_cast<int4*>(q), make_int4((int)y[0], (int)y[1], (int)y[2], (int)y[3]));
+        else __stcs(reinterpret_cast<int2*>(q), make_int2((int)y[0], (int)y[1]));
+    };
+    uint64_t l = 0;
+    for (; l + U <= L; l += U) {
+        VT x[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) x[k] = __ldcs(reinterpret_cast<const VT*>(p + k * W));
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            uint32_t e[V];
+            if constexpr (V == 4) { e[0] = x[k].x; e[1] = x[k].y; e[2] = x[k].z; e[3] = x[k].w; }
+            else { e[0] = x[k].x; e[1] = x[k].y; }
+            emit(p + k * W, e);
+        }
+        p += U * W;
+    }
+    for (; l < L; ++l, p += W) {
+        const VT x = *reinterpret_cast<const VT*>(p);
+        uint32_t e[V];
+        if constexpr (V == 4) { e[0] = x.x; e[1] = x.y; e[2] = x.z; e[3] = x.w; }
+        else { e[0] = x.x; e[1] = x.y; }
+        emit(p, e);
+    }
+}
+
 __global__ void k_value_patch(float* out, const uint2* rec, uint64_t cnt, uint64_t n, uint64_t base)
 {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
@@ -746,12 +797,38 @@ cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool c
     return cudaGetLastError();
 }
 
+static int walk_mode()
+{
+    static const int v = [] {
+        const char* e = getenv("FZ_EXP");
+        return e ? (atoi(e) >> 8) & 3 : 0;
+    }();
+    return v;
+}
+
+// Column walk along L (stride W): vector columns when the rows allow it.
+static void launch_walk(int32_t* data, uint64_t outer, uint64_t L, uint64_t W, float w, const int32_t* carry,
+                        cudaStream_t st)
+{
+    const int m = walk_mode();
+    const bool a16 = (reinterpret_cast<uintptr_t>(data) & 15) == 0;
+    if (m != 3 && W % 4 == 0 && a16 && m != 1) {
+        const uint64_t thr = outer * W / 4;
+        k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry);
+    } else if (m != 3 && W % 2 == 0 && a16) {
+        const uint64_t thr = outer * W / 2;
+        k_scan_walk_v<2, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry);
+    } else {
+        k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry);
+    }
+}
+
 cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t W, uint32_t* sums,
                              float dequant_w, cudaStream_t st)
 {
     if (outer * W >= 32768) {
         LaunchProf lp(K_SCAN_APPLY, st);
-        k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, dequant_w, nullptr);
+        launch_walk(data, outer, L, W, dequant_w, nullptr, st);
         return cudaGetLastError();
     }
     const uint64_t nch = (L + kScanChunk - 1) / kScanChunk;
@@ -797,7 +874,7 @@ cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t el
 cudaError_t launch_walk_carry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* carry, cudaStream_t st)
 {
     LaunchProf lp(K_SCAN_APPLY, st);
-    k_scan_walk<<<(unsigned)((W + 255) / 256), 256, 0, st>>>(data, 1, L, W, w, carry);
+    launch_walk(data, 1, L, W, w, carry, st);
     return cudaGetLastError();
 }
 
