@@ -522,6 +522,36 @@ __device__ __forceinline__ void lorenzo_masks(const CompressArgs& a, uint32_t g0
     if (NDIM == 2) zm = 0;
 }
 
+// Same masks from the thread's precomputed in-row (x0) and in-plane (p0) positions.
+template <int NDIM>
+__device__ __forceinline__ void lorenzo_masks_xp(const CompressArgs& a, uint32_t g0, uint32_t x0, uint32_t p0,
+                                                 uint32_t& xm, uint32_t& ym, uint32_t& zm, bool& fast_yz)
+{
+    const uint32_t nx = a.g.nx, PL = a.g.P;
+    if (nx < 8) {
+        lorenzo_masks<NDIM>(a, g0, xm, ym, zm, fast_yz);
+        return;
+    }
+    xm = 0xFFu; ym = 0xFFu; zm = 0xFFu;
+    fast_yz = true;
+    const uint32_t us = x0 == 0 ? 0u : nx - x0;
+    if (us < 8) xm &= ~(1u << us);
+    if (NDIM >= 2) {
+        fast_yz = p0 >= nx && p0 + 7 < PL && (NDIM == 2 || g0 >= PL);
+        if (!fast_yz) {
+            uint32_t pp = p0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (pp < nx) ym &= ~(1u << e);
+                if (g0 + e < PL) zm &= ~(1u << e);
+                if (++pp == PL) pp = 0;
+            }
+        }
+    }
+    if (NDIM == 1) { ym = 0; zm = 0; }
+    if (NDIM == 2) zm = 0;
+}
+
 // delta(e) = S(e+1) - [x>0] S(e), with S(j) the y/z combination at element g0-1+j (C2).
 __device__ __forceinline__ void residuals(const uint32_t (&S)[9], uint32_t xm, int32_t (&dl)[8])
 {
@@ -981,6 +1011,7 @@ __device__ __forceinline__ void ws_issue(const CompressArgs& a, WsShared& sh, fl
 template <int NDIM>
 __device__ __forceinline__ void front_ws(const CompressArgs& a, const QuantP& P, int* smem, uint32_t rmask,
                                          uint32_t t, bool first, const float* in_own, const float* in_b,
+                                         uint32_t x0, uint32_t p0,
                                          int32_t (&dl)[8], uint32_t& vmask, float (&dv)[8], uint32_t& vm)
 {
     const int tid = threadIdx.x, lane = tid & 31;
@@ -1035,7 +1066,7 @@ __device__ __forceinline__ void front_ws(const CompressArgs& a, const QuantP& P,
 
     uint32_t xm, ym, zm;
     bool fast_yz;
-    lorenzo_masks<NDIM>(a, g0, xm, ym, zm, fast_yz);
+    lorenzo_masks_xp<NDIM>(a, g0, x0, p0, xm, ym, zm, fast_yz);
     uint32_t S[9];
     if (NDIM == 1) {
 #pragma unroll
@@ -1296,6 +1327,15 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
         const uint32_t t_first = a.tile_begin + u * kUnitTiles;
         const uint32_t t_last = min(a.tile_end, t_first + kUnitTiles);
         const uint32_t start = head;
+        // thread's in-row / in-plane positions, advanced per tile without divisions
+        uint32_t x0 = 0, p0 = 0;
+        {
+            const uint32_t g = t_first * kTileCodes + 8u * tid;
+            if (a.g.nx >= 8) {
+                x0 = fmod_(g, a.dnx);
+                if (NDIM >= 2) p0 = fmod_(g, a.dP);
+            }
+        }
         for (uint32_t t = t_first; t < t_last; ++t) {
             const bool first = t == t_first;
             const uint32_t bits = sh.tma_bits;
@@ -1308,7 +1348,11 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
             uint32_t vmask, vm;
             float dv[8];
             front_ws<NDIM>(a, P, smem, rmask, t, first, (bits & 1) ? inbuf : nullptr,
-                           (bits & 2) ? inbuf + kTileCodes : nullptr, dl, vmask, dv, vm);
+                           (bits & 2) ? inbuf + kTileCodes : nullptr, x0, p0, dl, vmask, dv, vm);
+            x0 += a.sx;
+            if (x0 >= a.g.nx) x0 -= a.g.nx;
+            p0 += a.sp;
+            if (p0 >= a.g.P) p0 -= a.g.P;
             // every compute thread has consumed the input stage: prefetch the next tile
             if (tid == 0) {
                 if (first) sh.unit[(it & 1) ^ 1] = atomicAdd(&ctrl->ticket, 1u);
@@ -1511,6 +1555,8 @@ cudaError_t launch_compress(const CompressArgs& a_in, cudaStream_t st)
     if (const char* e = getenv("FZ_EXP")) a.exp = atoi(e);
     a.dnx = make_fastdiv(a.g.nx);
     a.dP = make_fastdiv(a.g.P);
+    a.sx = a.g.nx ? (uint32_t)(kTileCodes % a.g.nx) : 0u;
+    a.sp = a.g.P ? (uint32_t)(kTileCodes % a.g.P) : 0u;
     bool vec = false;
     size_t sm = plan_smem(a, vec);
     const uint32_t ntiles = a.tile_end - a.tile_begin;

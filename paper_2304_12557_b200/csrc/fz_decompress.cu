@@ -300,6 +300,89 @@ __device__ __forceinline__ uint4 tile_blk(const DecodeArgs& a, const TileIn& in)
     return blk;
 }
 
+// Sign-magnitude 16-bit codes (two per word) -> int32 (C3 inverse): with m = -sign,
+// v = ((c & 0x7FFF) ^ m) - m.
+__device__ __forceinline__ void unpack_codes(const uint32_t (&w4)[4], int32_t (&dl)[8])
+{
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t w = w4[i];
+        const uint32_t mlo = (uint32_t)((int32_t)(w << 16) >> 31), mhi = (uint32_t)((int32_t)w >> 31);
+        dl[2 * i] = (int32_t)(((w & 0x7FFFu) ^ mlo) - mlo);
+        dl[2 * i + 1] = (int32_t)((((w >> 16) & 0x7FFFu) ^ mhi) - mhi);
+    }
+}
+
+// Delta-outlier patch of the thread's 8 deltas (records [rlo, rhi) of tile starting at s).
+__device__ __forceinline__ void patch_deltas(const DecodeArgs& a, DecSmem& sm, int64_t s, uint32_t rlo, uint32_t rhi,
+                                             int32_t (&dl)[8])
+{
+    const int tid = threadIdx.x;
+    const uint32_t nd32 = (uint32_t)a.nd;
+    rlo = rlo < nd32 ? rlo : nd32;
+    rhi = rhi < rlo ? rlo : (rhi < nd32 ? rhi : nd32);
+    if (rhi > rlo) {   // rare, block-uniform
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sm.D[8 * tid + u] = dl[u];
+        __syncthreads();
+        for (uint32_t k = rlo + tid; k < rhi; k += kCta) {
+            const uint2 r = a.drec[k];
+            const uint64_t e = (uint64_t)r.x - a.gbase - (uint64_t)s;
+            if (e < (uint64_t)kTileCodes) sm.D[e] = (int32_t)r.y;
+            else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dl[u] = sm.D[8 * tid + u];
+    }
+}
+
+// D3-D5(x) for a tile of R whole rows (nx = 2048 / R >= 256, so every warp lies inside one
+// row and row starts fall on warp boundaries): plain scans, no segment flags.
+template <int R>
+__device__ __forceinline__ void decode_tile_rows(const DecodeArgs& a, DecSmem& sm, int64_t s, const uint4& blk,
+                                                 uint32_t rlo, uint32_t rhi, uint32_t (&q)[8])
+{
+    constexpr int WPR = 8 / R;    // warps per row
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    {
+        uint32_t* row = sm.Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+        row[0] = blk.x; row[1] = blk.y; row[2] = blk.z; row[3] = blk.w;
+    }
+    __syncthreads();
+    uint32_t w4[4];
+    {
+        const int c = tid >> 3, kk = tid & 7;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w4[i] = sm.Obuf[(4 * kk + i) * 33 + c];
+        transpose32_group8(w4, lane & 7);
+    }
+    int32_t dl[8];
+    unpack_codes(w4, dl);
+    patch_deltas(a, sm, s, rlo, rhi, dl);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { acc += (uint32_t)dl[u]; q[u] = acc; }
+    uint32_t inc = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t up = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += up;
+    }
+    if (lane == 31) sm.wv[warp] = inc;
+    uint32_t pre = inc - acc;      // exclusive prefix inside the warp
+    if (WPR > 1) {
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < WPR - 1; ++w) {
+            const int ww = (warp & ~(WPR - 1)) + w;
+            if (ww < warp) pre += sm.wv[ww];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] += pre;
+}
+
 template <int NDIM>
 __device__ __forceinline__ Seg decode_tile_x(const DecodeArgs& a, DecSmem& sm, uint32_t t, const uint4& blk,
                                              uint32_t rlo, uint32_t rhi, uint32_t (&q)[8])
@@ -333,29 +416,8 @@ __device__ __forceinline__ Seg decode_tile_x(const DecodeArgs& a, DecSmem& sm, u
     }
     // ---- D4: unpack, delta outliers ----
     int32_t dl[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t lo16 = w4[i] & 0xFFFFu, hi16 = w4[i] >> 16;
-        dl[2 * i] = (lo16 & 0x8000u) ? -(int32_t)(lo16 & 0x7FFFu) : (int32_t)lo16;
-        dl[2 * i + 1] = (hi16 & 0x8000u) ? -(int32_t)(hi16 & 0x7FFFu) : (int32_t)hi16;
-    }
-    const uint32_t nd32 = (uint32_t)a.nd;
-    rlo = rlo < nd32 ? rlo : nd32;
-    rhi = rhi < rlo ? rlo : (rhi < nd32 ? rhi : nd32);
-    if (rhi > rlo) {   // rare, block-uniform
-#pragma unroll
-        for (int u = 0; u < 8; ++u) sm.D[8 * tid + u] = dl[u];
-        __syncthreads();
-        for (uint32_t k = rlo + tid; k < rhi; k += kCta) {
-            const uint2 r = a.drec[k];
-            const uint64_t e = (uint64_t)r.x - a.gbase - (uint64_t)s;
-            if (e < (uint64_t)kTileCodes) sm.D[e] = (int32_t)r.y;
-            else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < 8; ++u) dl[u] = sm.D[8 * tid + u];
-    }
+    unpack_codes(w4, dl);
+    patch_deltas(a, sm, s, rlo, rhi, dl);
     // ---- D5 (x, local): segmented inclusive scan, resets at row starts ----
     uint32_t loc[8];
     Seg me{0, 0};
@@ -447,7 +509,7 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
             if (k + 2 < a.tpp) in_next = tile_in(a, t + 2);
         }
         uint32_t q[8];
-        decode_tile_x<3>(a, sm, t, blk, rlo, rhi, q);
+        decode_tile_rows<R>(a, sm, s, blk, rlo, rhi, q);
         *reinterpret_cast<uint4*>(sm.D + 8 * tid) = make_uint4(q[0], q[1], q[2], q[3]);
         *reinterpret_cast<uint4*>(sm.D + 8 * tid + 4) = make_uint4(q[4], q[5], q[6], q[7]);
         __syncthreads();

@@ -476,6 +476,7 @@ struct CompressArgs {
     uint64_t base;
     Geom g;
     FastDiv dnx, dP;          // x extent, plane size
+    uint32_t sx, sp;          // 2048 mod nx, 2048 mod P: per-tile position increments
     uint32_t tile_begin, tile_end;
     // neighbour streams (SV §7 hard part 3): q of the element and of its y-1, z-1, (y-1,z-1)
     // neighbours live in shared arrays; union = [s-nx-1, e) and [s-P-nx-1, e-P)
