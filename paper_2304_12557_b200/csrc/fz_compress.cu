@@ -958,6 +958,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes)
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* m)
+{
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* m, uint32_t parity)
 {
     uint32_t ok;
@@ -986,6 +990,7 @@ struct WsShared {
     uint32_t cd[8], cv[8];
     unsigned long long ob[2];
     volatile uint32_t ring_tail;   // payload ring blocks released by the scanner
+    uint64_t desc_full[kDescQ];    // mbarrier per descriptor slot: completes when it is written
     volatile uint32_t desc_head;   // descriptors published by the compute warps
     volatile uint32_t desc_tail;   // descriptors consumed by the scanner
     WsDesc desc[kDescQ];
@@ -1008,11 +1013,12 @@ __device__ __forceinline__ void ws_issue(const CompressArgs& a, WsShared& sh, fl
     }
 }
 
-template <int NDIM>
+template <int NDIM, class OnFree>
 __device__ __forceinline__ void front_ws(const CompressArgs& a, const QuantP& P, int* smem, uint32_t rmask,
                                          uint32_t t, bool first, const float* in_own, const float* in_b,
                                          uint32_t x0, uint32_t p0,
-                                         int32_t (&dl)[8], uint32_t& vmask, float (&dv)[8], uint32_t& vm)
+                                         int32_t (&dl)[8], uint32_t& vmask, float (&dv)[8], uint32_t& vm,
+                                         OnFree&& on_input_free)
 {
     const int tid = threadIdx.x, lane = tid & 31;
     const uint32_t n = a.g.n, nx = a.g.nx, PL = a.g.P;
@@ -1063,6 +1069,7 @@ __device__ __forceinline__ void front_ws(const CompressArgs& a, const QuantP& P,
     vm = 0xFFu;
     if (!full) vm = (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
     bar_sync(kBarCompute, kCta);
+    on_input_free();   // every compute thread has read the TMA input stage
 
     uint32_t xm, ym, zm;
     bool fast_yz;
@@ -1267,6 +1274,7 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
 
     if (tid == 0) {
         mbar_init(&sh.mbar, 1);
+        for (int k = 0; k < kDescQ; ++k) mbar_init(&sh.desc_full[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sh.ring_tail = 0;
         sh.desc_head = 0;
@@ -1281,8 +1289,9 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
         // ================= scanner warp =================
         if (a.rescan) return;
         for (uint32_t dt = 0;; ++dt) {
-            while (sh.desc_head == dt) __nanosleep(500);
-            __threadfence_block();
+            // sleeps in hardware until the compute warps publish descriptor dt
+            while (!mbar_try_wait(&sh.desc_full[dt % kDescQ], (dt / kDescQ) & 1u)) {
+            }
             const WsDesc d = sh.desc[dt % kDescQ];
             if (d.unit == kNone) break;
             unsigned long long ex = 0;
@@ -1319,8 +1328,8 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
                 while (sh.desc_head - sh.desc_tail >= (uint32_t)kDescQ) __nanosleep(32);
                 const uint32_t dh = sh.desc_head;
                 sh.desc[dh % kDescQ].unit = kNone;
-                __threadfence_block();
                 sh.desc_head = dh + 1;
+                mbar_arrive(&sh.desc_full[dh % kDescQ]);
             }
             break;
         }
@@ -1347,25 +1356,27 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
             int32_t dl[8];
             uint32_t vmask, vm;
             float dv[8];
+            // as soon as every compute thread has consumed the input stage: TMA of the next tile
+            auto issue_next = [&]() {
+                if (tid == 0) {
+                    if (first) sh.unit[(it & 1) ^ 1] = atomicAdd(&ctrl->ticket, 1u);
+                    const uint32_t nu = sh.unit[(it & 1) ^ 1];
+                    uint32_t nt = kNone;
+                    if (t + 1 < t_last) nt = t + 1;
+                    else if (nu < nunits) nt = a.tile_begin + nu * kUnitTiles;
+                    if (nt != kNone) ws_issue<NDIM>(a, sh, inbuf, nt);
+                    else sh.tma_bits = 0;
+                    if (first && nu < nunits)   // L2 prefetch of the next unit beyond the TMA stage
+                        prefetch_l2_range(a, (uint64_t)(a.tile_begin + nu * kUnitTiles) * kTileCodes,
+                                          (uint64_t)kUnitTiles * kTileCodes);
+                }
+            };
             front_ws<NDIM>(a, P, smem, rmask, t, first, (bits & 1) ? inbuf : nullptr,
-                           (bits & 2) ? inbuf + kTileCodes : nullptr, x0, p0, dl, vmask, dv, vm);
+                           (bits & 2) ? inbuf + kTileCodes : nullptr, x0, p0, dl, vmask, dv, vm, issue_next);
             x0 += a.sx;
             if (x0 >= a.g.nx) x0 -= a.g.nx;
             p0 += a.sp;
             if (p0 >= a.g.P) p0 -= a.g.P;
-            // every compute thread has consumed the input stage: prefetch the next tile
-            if (tid == 0) {
-                if (first) sh.unit[(it & 1) ^ 1] = atomicAdd(&ctrl->ticket, 1u);
-                const uint32_t nu = sh.unit[(it & 1) ^ 1];
-                uint32_t nt = kNone;
-                if (t + 1 < t_last) nt = t + 1;
-                else if (nu < nunits) nt = a.tile_begin + nu * kUnitTiles;
-                if (nt != kNone) ws_issue<NDIM>(a, sh, inbuf, nt);
-                else sh.tma_bits = 0;
-                if (first && nu < nunits)   // L2 prefetch of the next unit beyond the TMA stage
-                    prefetch_l2_range(a, (uint64_t)(a.tile_begin + nu * kUnitTiles) * kTileCodes,
-                                      (uint64_t)kUnitTiles * kTileCodes);
-            }
             head += tail_ws(a, sh, Obuf, ring, head, t, (uint32_t)t * kTileCodes + 8u * tid, vm, dl, vmask, dv);
         }
         bar_sync(kBarCompute, kCta);   // all ring writes of the unit are done
@@ -1374,8 +1385,8 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
             while (sh.desc_head - sh.desc_tail >= (uint32_t)kDescQ) __nanosleep(32);
             const uint32_t dh = sh.desc_head;
             sh.desc[dh % kDescQ] = WsDesc{u, start, head - start, 0};
-            __threadfence_block();
             sh.desc_head = dh + 1;
+            mbar_arrive(&sh.desc_full[dh % kDescQ]);
         }
     }
 }
