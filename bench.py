@@ -120,6 +120,7 @@ def algorithmic_bytes(kernel: str, n: int, stream_bytes: int, ndim: int):
         "k_range": 4 * n,
         "k_compress": 4 * n + payload,
         "k_decode_tiles": payload + 4 * n,
+        "k_decode_planes": payload + 4 * n,
         "k_scan_sums": 4 * n,
         "k_scan_apply": 8 * n,
         "k_scan_walk": 8 * n,

@@ -578,7 +578,8 @@ const char* fz_kernel_name(int id)
     static const char* names[] = {"k_init", "k_range", "k_params", "k_compress", "k_finalize",
                                   "k_decode_init", "k_validate_outliers", "k_decode_tiles",
                                   "k_scan_sums", "k_scan_chunks", "k_scan_apply", "k_value_patch",
-                                  "k_outliers", "k_tile_offsets", "k_xcarry", "k_slab"};
+                                  "k_outliers", "k_tile_offsets", "k_xcarry", "k_slab", "k_decode_planes",
+                                  "k_scan_walk"};
     return (id >= 0 && id < fz::K_COUNT) ? names[id] : "?";
 }
 

@@ -815,7 +815,7 @@ static cudaError_t launch_decode_t(const DecodeArgs& a_in, cudaStream_t st)
 
 cudaError_t launch_decode_tiles(const DecodeArgs& a_in, cudaStream_t st, bool fuse_y)
 {
-    LaunchProf lp(K_DECODE, st);
+    LaunchProf lp(fuse_y ? K_DECODE_PLANES : K_DECODE, st);
     if (fuse_y) {
         DecodeArgs a = a_in;
         a.dnx = make_fastdiv(a.g.nx);
@@ -889,7 +889,7 @@ cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t
                              float dequant_w, cudaStream_t st)
 {
     if (outer * W >= 32768) {
-        LaunchProf lp(K_SCAN_APPLY, st);
+        LaunchProf lp(K_SCAN_WALK, st);
         launch_walk(data, outer, L, W, dequant_w, nullptr, st);
         return cudaGetLastError();
     }
@@ -935,7 +935,7 @@ cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t el
 
 cudaError_t launch_walk_carry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* carry, cudaStream_t st)
 {
-    LaunchProf lp(K_SCAN_APPLY, st);
+    LaunchProf lp(K_SCAN_WALK, st);
     launch_walk(data, 1, L, W, w, carry, st);
     return cudaGetLastError();
 }

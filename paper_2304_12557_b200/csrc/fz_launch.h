@@ -12,7 +12,7 @@ int num_sms();
 // Kernel kinds for launch accounting and per-kernel CUDA-event timing (fz_profile_*).
 enum KernelId {
     K_INIT = 0, K_RANGE, K_PARAMS, K_COMPRESS, K_FINALIZE, K_DINIT, K_VALIDATE, K_DECODE,
-    K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_SLAB, K_COUNT
+    K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_SLAB, K_DECODE_PLANES, K_SCAN_WALK, K_COUNT
 };
 
 // Counts one launch of `id` and, when profiling is on, brackets it with CUDA events on the
