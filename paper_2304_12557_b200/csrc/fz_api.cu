@@ -441,7 +441,12 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     a.xagg = xagg;
     a.ctrl = ctrl;
     a.drange = drange;
-    if (fuse_y) a.tpp = (uint32_t)(I.shape.dims[1] * I.shape.dims[2] / kTileCodes);
+    if (fuse_y) {
+        a.tpp = (uint32_t)(I.shape.dims[1] * I.shape.dims[2] / kTileCodes);
+        // two CTAs per plane unless the planes alone fill the GPU several times over
+        a.yseg = (a.tpp % 2 == 0 && I.shape.dims[0] < 4 * 148 && !(exp_bits() & 512)) ? 2 : 1;
+        a.ycarry = reinterpret_cast<int32_t*>(wb + L.ycarry);
+    }
     FZ_CUDA(launch_decode_tiles(a, st, fuse_y));
     // x carries exist when some tile starts inside a row (always for 1-D fields)
     const bool carries = T > 1 && (g.ndim == 1 || !(g.nx <= kTileCodes && kTileCodes % g.nx == 0));
@@ -457,7 +462,11 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     } else if (I.shape.ndim == 3) {
         if (!fuse_y)
             FZ_CUDA(launch_scan_axis(q, I.shape.dims[0], I.shape.dims[1], I.shape.dims[2], sums, 0.0f, st));
-        FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], sums, wq, st));
+        if (fuse_y && a.yseg == 2)
+            FZ_CUDA(launch_zwalk_ycarry(q, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], wq, a.ycarry,
+                                        (uint32_t)I.shape.dims[2], st));
+        else
+            FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], sums, wq, st));
     }
     if (deq) FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
     Ctrl h;

@@ -26,7 +26,7 @@ bool decode_fuses_y(const fz_shape& s)
     const uint64_t nx = s.dims[2];
     if (nx < 256 || nx > (uint64_t)kTileCodes || kTileCodes % nx != 0) return false;
     if ((s.dims[1] * nx) % kTileCodes != 0) return false;
-    return s.dims[0] >= 2 * 148;    // one CTA per plane: enough planes to fill the GPU
+    return s.dims[0] >= 148;        // one or two CTAs per plane: enough planes to fill the GPU
 }
 
 // Decode workspace: control block, per-tile block offsets (two-level exclusive scan of the
@@ -56,6 +56,7 @@ DecodeLayout decode_layout(const fz_shape& s)
     L.xbagg = off;  off = al(off + 8 * nb);
     L.sums = off;   off = al(off + 4 * sums);
     L.drange = off; off = al(off + 4 * (T + 1));
+    L.ycarry = off; off = al(off + (decode_fuses_y(s) ? 4 * nz * nx : 0));
     L.sums_elems = sums;
     L.total = off;
     return L;
@@ -490,23 +491,25 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
     constexpr int C = 8 / R;
     __shared__ DecSmem sm;
     const int tid = threadIdx.x;
-    const uint32_t nx = a.g.nx, z = blockIdx.x, t0 = z * a.tpp;
+    // CTA = segment (blockIdx % yseg) of plane (blockIdx / yseg): tiles [k0, k0 + nk)
+    const uint32_t nx = a.g.nx, z = blockIdx.x / a.yseg, seg = blockIdx.x % a.yseg;
+    const uint32_t nk = a.tpp / a.yseg, t0 = z * a.tpp + seg * nk;
     uint32_t carry[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) carry[c] = 0;
     // two-stage software pipeline: payload block of tile k+1, flags/offsets of tile k+2
     TileIn in_cur = tile_in(a, t0);
     uint4 blk_next = tile_blk(a, in_cur);
-    TileIn in_next = a.tpp > 1 ? tile_in(a, t0 + 1) : in_cur;
-    for (uint32_t k = 0; k < a.tpp; ++k) {
+    TileIn in_next = nk > 1 ? tile_in(a, t0 + 1) : in_cur;
+    for (uint32_t k = 0; k < nk; ++k) {
         const uint32_t t = t0 + k;
         const int64_t s = (int64_t)t * kTileCodes;
         const uint4 blk = blk_next;
         const uint32_t rlo = in_cur.rlo, rhi = in_cur.rhi;
-        if (k + 1 < a.tpp) {
+        if (k + 1 < nk) {
             blk_next = tile_blk(a, in_next);
             in_cur = in_next;
-            if (k + 2 < a.tpp) in_next = tile_in(a, t + 2);
+            if (k + 2 < nk) in_next = tile_in(a, t + 2);
         }
         uint32_t q[8];
         decode_tile_rows<R>(a, sm, s, blk, rlo, rhi, q);
@@ -537,6 +540,12 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
             }
         }
         __syncthreads();    // sm.D and sm.Obuf are reused by the next tile
+    }
+    // lower segment of a split plane: its column totals are the upper segment's y carry,
+    // added by the z walk
+    if (a.yseg == 2 && seg == 0) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) a.ycarry[(size_t)z * nx + C * tid + c] = (int32_t)carry[c];
     }
 }
 
@@ -657,9 +666,12 @@ __global__ void __launch_bounds__(256) k_scan_walk(int32_t* v, uint64_t outer, u
 
 // Vector walk: V adjacent columns per thread (W % V == 0, rows 16-byte aligned for V = 4),
 // U rows in flight; same arithmetic as k_scan_walk.
+// ycarry (optional): columns w >= W/2 of step l also add ycarry[l * ynx + w % ynx] (the y carry
+// of the upper half of a plane decoded as two segments by k_decode_planes).
 template <int V, int U>
 __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
-                                                     float dequant_w, const int32_t* __restrict__ carry)
+                                                     float dequant_w, const int32_t* __restrict__ carry,
+                                                     const int32_t* __restrict__ ycarry, uint32_t ynx)
 {
     using VT = typename std::conditional<V == 4, int4, int2>::type;
     const uint64_t Wv = W / V;
@@ -680,11 +692,20 @@ __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer,
         if constexpr (V == 4) __stcs(reinterpret_cast<int4*>(q), make_int4((int)y[0], (int)y[1], (int)y[2], (int)y[3]));
         else __stcs(reinterpret_cast<int2*>(q), make_int2((int)y[0], (int)y[1]));
     };
+    const int32_t* yc = (ycarry != nullptr && w >= W / 2) ? ycarry + w % ynx : nullptr;
     uint64_t l = 0;
     for (; l + U <= L; l += U) {
         VT x[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) x[k] = __ldcs(reinterpret_cast<const VT*>(p + k * W));
+        if (yc != nullptr) {
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const VT c = __ldg(reinterpret_cast<const VT*>(yc + (l + k) * ynx));
+                if constexpr (V == 4) { x[k].x += c.x; x[k].y += c.y; x[k].z += c.z; x[k].w += c.w; }
+                else { x[k].x += c.x; x[k].y += c.y; }
+            }
+        }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             uint32_t e[V];
@@ -695,7 +716,12 @@ __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer,
         p += U * W;
     }
     for (; l < L; ++l, p += W) {
-        const VT x = *reinterpret_cast<const VT*>(p);
+        VT x = *reinterpret_cast<const VT*>(p);
+        if (yc != nullptr) {
+            const VT c = __ldg(reinterpret_cast<const VT*>(yc + l * ynx));
+            if constexpr (V == 4) { x.x += c.x; x.y += c.y; x.z += c.z; x.w += c.w; }
+            else { x.x += c.x; x.y += c.y; }
+        }
         uint32_t e[V];
         if constexpr (V == 4) { e[0] = x.x; e[1] = x.y; e[2] = x.z; e[3] = x.w; }
         else { e[0] = x.x; e[1] = x.y; }
@@ -819,12 +845,12 @@ cudaError_t launch_decode_tiles(const DecodeArgs& a_in, cudaStream_t st, bool fu
     if (fuse_y) {
         DecodeArgs a = a_in;
         a.dnx = make_fastdiv(a.g.nx);
-        const uint32_t planes = a.g.n / a.g.P;
+        const uint32_t ctas = a.g.n / a.g.P * a.yseg;
         switch (kTileCodes / a.g.nx) {
-            case 1: k_decode_planes<1><<<planes, kCta, 0, st>>>(a); break;
-            case 2: k_decode_planes<2><<<planes, kCta, 0, st>>>(a); break;
-            case 4: k_decode_planes<4><<<planes, kCta, 0, st>>>(a); break;
-            default: k_decode_planes<8><<<planes, kCta, 0, st>>>(a); break;
+            case 1: k_decode_planes<1><<<ctas, kCta, 0, st>>>(a); break;
+            case 2: k_decode_planes<2><<<ctas, kCta, 0, st>>>(a); break;
+            case 4: k_decode_planes<4><<<ctas, kCta, 0, st>>>(a); break;
+            default: k_decode_planes<8><<<ctas, kCta, 0, st>>>(a); break;
         }
         return cudaGetLastError();
     }
@@ -870,16 +896,16 @@ static int walk_mode()
 
 // Column walk along L (stride W): vector columns when the rows allow it.
 static void launch_walk(int32_t* data, uint64_t outer, uint64_t L, uint64_t W, float w, const int32_t* carry,
-                        cudaStream_t st)
+                        cudaStream_t st, const int32_t* ycarry = nullptr, uint32_t ynx = 0)
 {
     const int m = walk_mode();
     const bool a16 = (reinterpret_cast<uintptr_t>(data) & 15) == 0;
     if (m != 3 && W % 4 == 0 && a16 && m != 1) {
         const uint64_t thr = outer * W / 4;
-        k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry);
+        k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx);
     } else if (m != 3 && W % 2 == 0 && a16) {
         const uint64_t thr = outer * W / 2;
-        k_scan_walk_v<2, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry);
+        k_scan_walk_v<2, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx);
     } else {
         k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry);
     }
@@ -930,6 +956,16 @@ cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t el
 {
     LaunchProf lp(K_SLAB, st);
     k_slab_carry<<<grid_for(elems), 256, 0, st>>>(aggs, nbefore, elems, carry);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zwalk_ycarry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* ycarry, uint32_t nx,
+                               cudaStream_t st)
+{
+    LaunchProf lp(K_SCAN_WALK, st);
+    if (W % 4 != 0 || (reinterpret_cast<uintptr_t>(data) & 15) != 0) return cudaErrorInvalidValue;
+    const uint64_t thr = W / 4;
+    k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, 1, L, W, w, nullptr, ycarry, nx);
     return cudaGetLastError();
 }
 

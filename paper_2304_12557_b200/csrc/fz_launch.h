@@ -57,6 +57,8 @@ struct DecodeArgs {
     uint2* xagg;                // per-tile x-scan aggregate (row start seen, sum)
     Ctrl* ctrl;
     uint32_t tpp;               // tiles per plane (fused y scan)
+    uint32_t yseg;              // CTAs (segments) per plane: 1, or 2 with the carry in ycarry
+    int32_t* ycarry;            // [nz][nx] column totals of the lower segment (yseg == 2)
     const uint32_t* drange;     // per-tile delta-outlier record ranges (k_record_tiles)
 };
 
@@ -65,7 +67,7 @@ struct DecodeArgs {
 bool decode_fuses_y(const fz_shape& s);
 
 struct DecodeLayout {
-    size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, drange, total;
+    size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, drange, ycarry, total;
     uint64_t sums_elems;
 };
 DecodeLayout decode_layout(const fz_shape& s);
@@ -88,6 +90,8 @@ cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint
 cudaError_t launch_axis_sum(const int32_t* v, uint64_t L, uint64_t W, int32_t* agg, cudaStream_t st);
 cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t elems, int32_t* carry,
                               cudaStream_t st);
+cudaError_t launch_zwalk_ycarry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* ycarry, uint32_t nx,
+                               cudaStream_t st);
 cudaError_t launch_walk_carry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* carry,
                               cudaStream_t st);
 cudaError_t launch_add_dequant(int32_t* q, uint64_t n, const int32_t* carry, float w, cudaStream_t st);

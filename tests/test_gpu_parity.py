@@ -249,7 +249,7 @@ def test_range_kernel_vs_oracle(n):
             assert np.float32(mx).tobytes() == np.float32(omx).tobytes()
 
 
-# Shapes on the decoder's fused-y path (k_decode_planes: 3-D, nz >= 296, nx in
+# Shapes on the decoder's fused-y path (k_decode_planes: 3-D, nz >= 148, nx in
 # {256..2048} dividing the tile, tiles inside planes): R = 8, 4, 2, 1 rows per tile with two
 # or more tiles per plane, one tile per plane, and delta outliers inside fused planes.
 FUSED_Y = [
@@ -259,6 +259,9 @@ FUSED_Y = [
     ("r1", lambda: synth.generate("rtm", (300, 2, 2048))),
     ("one_tile_per_plane", lambda: synth.generate("sines3d", (300, 8, 256))),
     ("tpp4", lambda: synth.generate("sines3d", (300, 32, 256))),
+    ("split_150", lambda: synth.generate("nyx_v", (150, 16, 512))),      # two CTAs per plane
+    ("unsplit_600", lambda: synth.generate("nyx_rho", (600, 8, 512))),   # one CTA per plane
+    ("odd_tpp", lambda: synth.generate("hurr_u", (160, 24, 256))),       # 3 tiles per plane
 ]
 
 
