@@ -121,6 +121,18 @@ fz_status fz_compress_with_params(const float* d_field, const fz_shape* s,
 fz_status fz_decompress(const void* d_in, size_t in_size, float* d_field, uint64_t n,
                         void* d_work, size_t work_bytes, void* stream);
 
+/* Same, with the 128-byte header supplied from host memory (h_hdr, e.g. from fz_last_header
+ * after the fz_compress that produced d_in): no blocking header read before the launches;
+ * blocks once at the end for the status.  h_hdr must be the header of d_in -- the section
+ * bounds it implies are checked against in_size, and every device read stays inside them,
+ * but a header that does not belong to the stream decodes to garbage. */
+fz_status fz_decompress_hdr(const void* d_in, size_t in_size, const void* h_hdr, float* d_field,
+                            uint64_t n, void* d_work, size_t work_bytes, void* stream);
+
+/* Copies the header of the last successful fz_compress / fz_compress_with_params on this
+ * thread (128 bytes, the same bytes as the stream's header) to h_hdr.  FZ_ERR_ARG if none. */
+fz_status fz_last_header(void* h_hdr);
+
 /* Host-buffer variants (end-to-end path): H2D of the input, the device call, D2H of the
  * result, all on `stream`.  The caller passes device scratch of the stated sizes.
  *   compress  : d_field_scratch >= 4N bytes, d_out_scratch >= d_out_cap bytes.

@@ -61,6 +61,8 @@ using namespace fz;
 
 static thread_local char g_cuda_err[256] = "";
 static thread_local int g_last_launches = 0;
+static thread_local uint8_t g_last_hdr[128];
+static thread_local bool g_have_hdr = false;
 
 namespace {
 
@@ -278,7 +280,13 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     OutDest d;
     d.drec = reinterpret_cast<uint2*>(out + pbase + 16 * h.nnz);
     d.vrec = reinterpret_cast<uint2*>(out + pbase + 16 * h.nnz + 8 * h.nd);
-    return place_outliers(W, a, h, d, st);
+    rs = place_outliers(W, a, h, d, st);
+    if (rs == FZ_OK) {
+        // the same bytes k_finalize wrote to the stream's header
+        write_header_host(g_last_hdr, *s, n, T, h.p, fz_counts{h.nnz, h.nd, h.nv}, h.total);
+        g_have_hdr = true;
+    }
+    return rs;
 }
 
 }  // namespace
@@ -386,14 +394,18 @@ fz_status fz_peek_header(const void* h_hdr, size_t nbytes, fz_info* info)
 namespace {
 
 fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int32_t* d_q, uint64_t n,
-                          void* d_work, size_t work_bytes, cudaStream_t st)
+                          void* d_work, size_t work_bytes, cudaStream_t st, const void* h_hdr = nullptr)
 {
     if (d_in == nullptr || (d_field == nullptr && d_q == nullptr) || d_work == nullptr ||
         !aligned16(d_in) || !aligned16(d_work) || in_size < kHeaderBytes)
         return FZ_ERR_ARG;
     uint8_t hdr[128];
-    FZ_CUDA(cudaMemcpyAsync(hdr, d_in, 128, cudaMemcpyDeviceToHost, st));
-    FZ_CUDA(cudaStreamSynchronize(st));
+    if (h_hdr != nullptr) {
+        memcpy(hdr, h_hdr, 128);
+    } else {
+        FZ_CUDA(cudaMemcpyAsync(hdr, d_in, 128, cudaMemcpyDeviceToHost, st));
+        FZ_CUDA(cudaStreamSynchronize(st));
+    }
     fz_info I;
     fz_status rs = fz_peek_header(hdr, 128, &I);
     if (rs != FZ_OK) return rs;
@@ -488,6 +500,22 @@ fz_status fz_decompress(const void* d_in, size_t in_size, float* d_field, uint64
     if (d_field == nullptr || !aligned16(d_field)) return FZ_ERR_ARG;
     return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
                            static_cast<cudaStream_t>(stream));
+}
+
+fz_status fz_decompress_hdr(const void* d_in, size_t in_size, const void* h_hdr, float* d_field, uint64_t n,
+                            void* d_work, size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    if (d_field == nullptr || !aligned16(d_field) || h_hdr == nullptr) return FZ_ERR_ARG;
+    return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
+                           static_cast<cudaStream_t>(stream), h_hdr);
+}
+
+fz_status fz_last_header(void* h_hdr)
+{
+    if (h_hdr == nullptr || !g_have_hdr) return FZ_ERR_ARG;
+    memcpy(h_hdr, g_last_hdr, 128);
+    return FZ_OK;
 }
 
 fz_status fz_debug_decode_q(const void* d_in, size_t in_size, int32_t* d_q, uint64_t n, void* d_work,

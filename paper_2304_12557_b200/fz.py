@@ -70,6 +70,8 @@ def lib():
         "fz_compress": ([P, pS, i, C.c_double, P, S, C.POINTER(S), P, S, P], i),
         "fz_compress_with_params": ([P, pS, pP, P, S, C.POINTER(S), P, S, P], i),
         "fz_decompress": ([P, S, P, u64, P, S, P], i),
+        "fz_decompress_hdr": ([P, S, P, P, u64, P, S, P], i),
+        "fz_last_header": ([P], i),
         "fz_compress_host": ([P, pS, i, C.c_double, P, S, C.POINTER(S), P, P, S, P, S, P], i),
         "fz_decompress_host": ([P, S, P, u64, P, P, P, S, P], i),
         "fz_peek_header": ([P, S, C.POINTER(Info)], i),
@@ -176,6 +178,8 @@ class Codec:
         self.out = _u8(self.cap, device)
         self.work = _u8(workspace_bytes(self.dims), device)
         self.dwork = _u8(decompress_workspace_bytes(self.dims), device)
+        self.hdr = (C.c_uint8 * 128)()   # host copy of the last stream's header
+        self.hdr_size = None             # size of the stream it belongs to (None: no header)
 
     def compress(self, field, mode=REL, eb=1e-3, params: Params | None = None, stream=None):
         """Returns (uint8 view of the stream, size)."""
@@ -188,14 +192,24 @@ class Codec:
                                                _ptr(self.out), self.cap, C.byref(size), _ptr(self.work),
                                                self.work.numel(), _stream(stream))
         _check(st, "fz_compress")
+        _check(lib().fz_last_header(self.hdr), "fz_last_header")
+        self.hdr_size = size.value
         return self.out[: size.value], size.value
 
     def decompress(self, buf, out=None, stream=None):
+        """Decompresses `buf`; when it is this codec's last output, the header comes from the
+        host copy kept by compress (fz_decompress_hdr: no blocking header read)."""
         import torch
         if out is None:
             out = torch.empty(self.dims, dtype=torch.float32, device=self.device)
-        st = lib().fz_decompress(_ptr(buf), buf.numel(), _ptr(out), self.n, _ptr(self.dwork),
-                                 self.dwork.numel(), _stream(stream))
+        own = (self.hdr_size is not None and buf.data_ptr() == self.out.data_ptr()
+               and buf.numel() == self.hdr_size)
+        if own:
+            st = lib().fz_decompress_hdr(_ptr(buf), buf.numel(), self.hdr, _ptr(out), self.n, _ptr(self.dwork),
+                                         self.dwork.numel(), _stream(stream))
+        else:
+            st = lib().fz_decompress(_ptr(buf), buf.numel(), _ptr(out), self.n, _ptr(self.dwork),
+                                     self.dwork.numel(), _stream(stream))
         _check(st, "fz_decompress")
         return out
 

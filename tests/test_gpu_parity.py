@@ -283,3 +283,19 @@ def test_fused_y_decode_with_outliers():
     assert st == O.OK
     q = fz.debug_decode_q(torch.from_numpy(ref).to(DEV), d.shape)
     assert np.array_equal(q.cpu().numpy(), qref)
+
+
+def test_host_header_decompress_matches():
+    """fz_last_header returns the stream's own header bytes, and fz_decompress_hdr (no
+    blocking header read) decodes bit-identically to fz_decompress."""
+    import ctypes as C
+    d = synth.generate("nyx_v", (300, 8, 512))
+    codec = fz.Codec(d.shape, DEV)
+    buf, size = codec.compress(torch.from_numpy(d).to(DEV), fz.REL, 1e-3)
+    assert bytes(codec.hdr) == buf[:128].cpu().numpy().tobytes()
+    a = codec.decompress(buf)                                     # header from the host copy
+    b = torch.empty_like(a)
+    st = fz.lib().fz_decompress(C.c_void_p(buf.data_ptr()), size, C.c_void_p(b.data_ptr()), d.size,
+                                C.c_void_p(codec.dwork.data_ptr()), codec.dwork.numel(), None)
+    assert st == fz.OK
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
