@@ -63,7 +63,6 @@ __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint
         ctrl->stage_overflow = 0;
         ctrl->nnz = ctrl->nd = ctrl->nv = ctrl->total = 0;
         ctrl->dcount = ctrl->vcount = 0;
-        ctrl->dbg[0] = ctrl->dbg[1] = ctrl->dbg[2] = ctrl->dbg[3] = 0;
         if (set_params) {
             ctrl->p = p;
             set_quant_consts(ctrl);
@@ -293,7 +292,6 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 __device__ __forceinline__ void flush_unit(const CompressArgs& a, CompShared& sh, const uint4* ps,
                                            const UnitState& us, unsigned long long off)
 {
-    if (a.exp & 2) return;
     for (uint32_t i = threadIdx.x; i < us.pcnt; i += kCta) {
         const uint64_t bo = 16 * (off + i);
         if (bo + 16 <= a.payload_cap) *reinterpret_cast<uint4*>(a.payload_out + bo) = ps[i];
@@ -428,7 +426,6 @@ __device__ __forceinline__ void tile_tail(const CompressArgs& a, CompShared& sh,
     }
     if (a.rescan) return;
 
-    if (a.exp & 4) { us.cnt += 1; __syncthreads(); return; }
     // ---- C6 block flags: thread b owns block b = 8r + x of the shuffled tile ----
     const uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
     const uint4 blk = make_uint4(row[0], row[1], row[2], row[3]);
@@ -440,14 +437,11 @@ __device__ __forceinline__ void tile_tail(const CompressArgs& a, CompShared& sh,
     if (us.pu != kNone && warp == 0) {
         unsigned long long ex = 0;
         bool ok = true;
-        if (us.pu != 0 && !(a.exp & 1)) {
-            if (pre != nullptr) ok = lookback_try<kLbLane>(a.status, us.pu, 0, kStAgg - 1, &ctrl->err, *reinterpret_cast<const unsigned long long (*)[kLbLane]>(pre), ex, (a.exp & 8) ? &ctrl->dbg[3] : nullptr);
+        if (us.pu != 0) {
+            if (pre != nullptr)
+                ok = lookback_try<kLbLane>(a.status, us.pu, 0, kStAgg - 1, &ctrl->err,
+                                           *reinterpret_cast<const unsigned long long (*)[kLbLane]>(pre), ex);
             else ok = false;
-            if ((a.exp & 8) && lane == 0) {
-                atomicAdd(&ctrl->dbg[0], 1ull);
-                if (!ok) atomicAdd(&ctrl->dbg[1], 1ull);
-                if (!ok && lbt) atomicAdd(&ctrl->dbg[2], 1ull);
-            }
             if (!ok && lbt) {
                 ex = lookback_wide<kLbLane, false>(a.status, us.pu, 0, kStAgg - 1, &ctrl->err);
                 ok = true;
@@ -772,14 +766,8 @@ __device__ __forceinline__ void front_vec(const CompressArgs& a, const QuantP& P
         if (NDIM == 3) fill_ring(a, P, smem, RB, rmask, (s - (int64_t)PL - H) & ~(int64_t)3, s - (int64_t)PL);
     }
     int qo[8], qz[8];
-    if (a.exp & 64) {
-        vmask = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) { qo[u] = __float_as_int(dv[u]) >> 12; qz[u] = __float_as_int(bz[u]) >> 12; }
-    } else {
-        pq_own(dv, qo, vmask, P);
-        if (NDIM == 3) pq_many<8>(bz, qz, P);
-    }
+    pq_own(dv, qo, vmask, P);
+    if (NDIM == 3) pq_many<8>(bz, qz, P);
     *reinterpret_cast<int4*>(smem + (g0 & rmask)) = make_int4(qo[0], qo[1], qo[2], qo[3]);
     *reinterpret_cast<int4*>(smem + ((g0 + 4) & rmask)) = make_int4(qo[4], qo[5], qo[6], qo[7]);
     if (NDIM == 3) {
@@ -1051,14 +1039,8 @@ __device__ __forceinline__ void front_ws(const CompressArgs& a, const QuantP& P,
         if (NDIM == 3) fill_ring(a, P, smem, RB, rmask, (s - (int64_t)PL - H) & ~(int64_t)3, s - (int64_t)PL);
     }
     int qo[8], qz[8];
-    if (a.exp & 64) {
-        vmask = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) { qo[u] = __float_as_int(dv[u]) >> 12; qz[u] = __float_as_int(bz[u]) >> 12; }
-    } else {
-        pq_own(dv, qo, vmask, P);
-        if (NDIM == 3) pq_many<8>(bz, qz, P);
-    }
+    pq_own(dv, qo, vmask, P);
+    if (NDIM == 3) pq_many<8>(bz, qz, P);
     *reinterpret_cast<int4*>(smem + (g0 & rmask)) = make_int4(qo[0], qo[1], qo[2], qo[3]);
     *reinterpret_cast<int4*>(smem + ((g0 + 4) & rmask)) = make_int4(qo[4], qo[5], qo[6], qo[7]);
     if (NDIM == 3) {
@@ -1173,7 +1155,7 @@ __device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh,
         uint32_t w4[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) w4[i] = __byte_perm(code[2 * i], code[2 * i + 1], 0x5410);
-        if (!(a.exp & 32)) transpose32_group8(w4, lane & 7);
+        transpose32_group8(w4, lane & 7);
         const int c = tid >> 3, kk = tid & 7;
 #pragma unroll
         for (int i = 0; i < 4; ++i) Obuf[(4 * kk + i) * 33 + c] = w4[i];

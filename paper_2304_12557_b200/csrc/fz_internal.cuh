@@ -35,7 +35,6 @@ struct Ctrl {
     // results (written by the last tile / k_finalize)
     unsigned long long nnz, nd, nv, total;
     unsigned long long dcount, vcount;   // outlier staging allocation counters (= totals)
-    unsigned long long dbg[4];           // FZ_EXP & 8: look-back tries / failures / blocking
 };
 static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 
@@ -501,7 +500,7 @@ struct CompressArgs {
     uint32_t* o_vidx;
     uint32_t* o_vbits;
     int rescan;               // 1: outliers only, straight to final offsets via opre
-    int exp;                  // performance experiments (FZ_EXP env var; 0 in production)
+    int exp;                  // FZ_EXP env var, bit 16: generic kernel instead of the warp-specialized one
 };
 
 }  // namespace fz

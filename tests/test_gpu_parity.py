@@ -299,3 +299,12 @@ def test_host_header_decompress_matches():
                                 C.c_void_p(codec.dwork.data_ptr()), codec.dwork.numel(), None)
     assert st == fz.OK
     assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+
+
+def test_generic_vector_kernel_parity(monkeypatch):
+    """FZ_EXP=16 routes compression through the generic padded-halo kernel (k_compress<NDIM,
+    VEC>) instead of the warp-specialized one; its stream must be byte-identical too."""
+    monkeypatch.setenv("FZ_EXP", "16")
+    for d in (synth.generate("nyx_v", (24, 40, 64)), synth.generate("cesm_t", (90, 256)),
+              synth.adversarial("spike", 30000)):
+        _check_full(d, O.REL, 1e-3, f"generic{d.shape}")

@@ -1,4 +1,5 @@
-"""Times k_compress alone (CUDA-event profiling) for the c4 workload under FZ_EXP variants."""
+"""Times k_compress alone (CUDA-event profiling) for a workload; FZ_EXP=16 selects the generic
+kernel instead of the warp-specialized one.  AS2D=1 reshapes the field to 2-D."""
 import os, sys, subprocess
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if len(sys.argv) > 1 and sys.argv[1] == "child":
@@ -25,15 +26,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     p = fz.profile_read()
     ms, k = p["k_compress"]
     print(f"FZ_EXP={os.environ.get('FZ_EXP','0')} k_compress {ms/k*1000:.1f} us")
-    if int(os.environ.get('FZ_EXP', '0')) & 8:
-        import ctypes
-        h = c.work[:512].cpu().numpy()
-        # Ctrl.dbg sits after dcount/vcount: read via the known struct layout (offset printed by test)
-        off = int(os.environ.get('FZ_DBG_OFF', '0'))
-        if off:
-            v = h[off:off + 32].view(np.uint64)
-            print("loads", v[0], "lookbacks", v[1], "cycles/lookback", v[2] / max(1, v[1]), "units", (d.size // 2048 + 3) // 4)
 else:
-    for e in sys.argv[1:] or ["0", "1", "3", "7"]:
+    for e in sys.argv[1:] or ["0", "16"]:
         env = dict(os.environ, FZ_EXP=e)
         subprocess.run([sys.executable, __file__, "child"], env=env)
