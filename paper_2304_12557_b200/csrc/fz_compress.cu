@@ -946,6 +946,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes)
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint (ns): the thread stays parked until the phase completes
+// or the hint elapses, instead of returning after the default short timeout.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* m, uint32_t parity, uint32_t ns)
+{
+    uint32_t ok;
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(smem_u32(m)), "r"(parity), "r"(ns) : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* m)
 {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
@@ -1272,7 +1281,7 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
         if (a.rescan) return;
         for (uint32_t dt = 0;; ++dt) {
             // sleeps in hardware until the compute warps publish descriptor dt
-            while (!mbar_try_wait(&sh.desc_full[dt % kDescQ], (dt / kDescQ) & 1u)) {
+            while (!mbar_try_wait_sleep(&sh.desc_full[dt % kDescQ], (dt / kDescQ) & 1u, 20000)) {
             }
             const WsDesc d = sh.desc[dt % kDescQ];
             if (d.unit == kNone) break;
