@@ -1,0 +1,39 @@
+"""Ablations of the fused design (analogous to the paper's Fig. 8).
+
+Runs bench.py (c4 512^3 REL 1e-3, 1 GPU) once per variant, selected by FZ_EXP bits read by
+libfz, and writes profiles/<round>_ablation.md with the step, compress and decompress
+throughput and the per-kernel times:
+  base          warp-specialized fused compressor, plane decoder (x+y fused), 2 CTAs per plane
+  generic_comp  FZ_EXP=16   generic fused compressor (no warp specialization / TMA / scanner warp)
+  unfused_dec   FZ_EXP=128  tile decoder (x only) + separate y and z walks
+  one_cta_plane FZ_EXP=512  plane decoder with one CTA per plane (no y-carry split)
+Usage (GPU box): python tools/ablation.py [round] [steps]
+"""
+import json, os, subprocess, sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+steps = sys.argv[2] if len(sys.argv) > 2 else "10"
+variants = [("base", "0"), ("generic_comp", "16"), ("unfused_dec", "128"), ("one_cta_plane", "512")]
+rows = []
+for name, e in variants:
+    env = dict(os.environ, FZ_EXP=e)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", steps, "--warmup", "3",
+                          "--no-cpu-baseline"], env=env, capture_output=True, text=True, cwd=ROOT)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    k = {n: round(v["ms_per_launch"] * 1e3, 1) for n, v in line["kernels"].items() if v["ms_per_launch"] > 0.02}
+    rows.append((name, e, line["value"], line["ms_per_step"], line["compress_gbs"], line["decompress_gbs"],
+                 line.get("parity_vs_oracle"), k))
+    print(name, line["value"], line["ms_per_step"], k, flush=True)
+md = [f"# {rnd} ablations (c4 512^3 REL 1e-3, 1 B200, `python tools/ablation.py`)", "",
+      "Each variant is `bench.py --steps %s --warmup 3` with the FZ_EXP bits shown (read by libfz)." % steps,
+      "Kernel times are CUDA-event means per launch (us).", "",
+      "| variant | FZ_EXP | step GB/s | ms/step | compress GB/s | decompress GB/s | kernels (us/launch) |",
+      "|---|---|---|---|---|---|---|"]
+for name, e, v, ms, c, d, par, k in rows:
+    ks = ", ".join(f"{n} {t}" for n, t in sorted(k.items(), key=lambda kv: -kv[1]))
+    md.append(f"| {name} | {e} | {v} | {ms} | {c} | {d} | {ks} |")
+os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+with open(os.path.join(ROOT, "profiles", f"{rnd}_ablation.md"), "w") as f:
+    f.write("\n".join(md) + "\n")
+print("\n".join(md))
