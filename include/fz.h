@@ -129,6 +129,14 @@ fz_status fz_decompress(const void* d_in, size_t in_size, float* d_field, uint64
 fz_status fz_decompress_hdr(const void* d_in, size_t in_size, const void* h_hdr, float* d_field,
                             uint64_t n, void* d_work, size_t work_bytes, void* stream);
 
+/* Asynchronous form of fz_decompress_hdr: enqueues the decode on `stream` and returns without
+ * waiting; argument errors are returned at once, stream errors (corrupt input, a popcount that
+ * disagrees with nnz) are recorded in d_work and returned by fz_decompress_result, which waits
+ * for `stream`.  d_field is valid only once fz_decompress_result returns FZ_OK. */
+fz_status fz_decompress_hdr_async(const void* d_in, size_t in_size, const void* h_hdr, float* d_field,
+                                  uint64_t n, void* d_work, size_t work_bytes, void* stream);
+fz_status fz_decompress_result(const void* d_work, void* stream);
+
 /* Copies the header of the last successful fz_compress / fz_compress_with_params on this
  * thread (128 bytes, the same bytes as the stream's header) to h_hdr.  FZ_ERR_ARG if none. */
 fz_status fz_last_header(void* h_hdr);
@@ -227,6 +235,11 @@ int fz_last_launch_count(void);
  * (indices 0..n-1, names from fz_kernel_name) and resets the totals; returns n. */
 void fz_profile_enable(int on);
 int fz_profile_read(double* h_ms, int* h_launches, int max_kernels);
+
+/* Timeline of the launches recorded since the last fz_profile_read (profiling on): kernel id,
+ * start and end of each launch's event pair in ms relative to the first one.  Does not clear.
+ * Returns the number of records written (<= max_records). */
+int fz_profile_timeline(int* h_ids, float* h_start_ms, float* h_end_ms, int max_records);
 const char* fz_kernel_name(int id);
 
 #ifdef __cplusplus

@@ -394,7 +394,8 @@ fz_status fz_peek_header(const void* h_hdr, size_t nbytes, fz_info* info)
 namespace {
 
 fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int32_t* d_q, uint64_t n,
-                          void* d_work, size_t work_bytes, cudaStream_t st, const void* h_hdr = nullptr)
+                          void* d_work, size_t work_bytes, cudaStream_t st, const void* h_hdr = nullptr,
+                          bool async = false)
 {
     if (d_in == nullptr || (d_field == nullptr && d_q == nullptr) || d_work == nullptr ||
         !aligned16(d_in) || !aligned16(d_work) || in_size < kHeaderBytes)
@@ -435,7 +436,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     FZ_CUDA(launch_decode_init(ctrl, st));
     FZ_CUDA(launch_validate_outliers(drec, I.counts.n_delta, n, ctrl, st));
     FZ_CUDA(launch_validate_outliers(vrec, I.counts.n_value, n, ctrl, st));
-    FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st));
+    FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st, I.counts.nnz));
     auto* drange = reinterpret_cast<uint32_t*>(wb + L.drange);
     FZ_CUDA(launch_record_tiles(drec, I.counts.n_delta, (uint32_t)T, 0, drange, st));
     DecodeArgs a{};
@@ -481,6 +482,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
             FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], sums, wq, st));
     }
     if (deq) FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+    if (async) return FZ_OK;     // status later: fz_decompress_result
     Ctrl h;
     FZ_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     FZ_CUDA(cudaStreamSynchronize(st));
@@ -509,6 +511,25 @@ fz_status fz_decompress_hdr(const void* d_in, size_t in_size, const void* h_hdr,
     if (d_field == nullptr || !aligned16(d_field) || h_hdr == nullptr) return FZ_ERR_ARG;
     return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
                            static_cast<cudaStream_t>(stream), h_hdr);
+}
+
+fz_status fz_decompress_hdr_async(const void* d_in, size_t in_size, const void* h_hdr, float* d_field, uint64_t n,
+                                  void* d_work, size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    if (d_field == nullptr || !aligned16(d_field) || h_hdr == nullptr) return FZ_ERR_ARG;
+    return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
+                           static_cast<cudaStream_t>(stream), h_hdr, true);
+}
+
+fz_status fz_decompress_result(const void* d_work, void* stream)
+{
+    if (d_work == nullptr) return FZ_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Ctrl h;
+    FZ_CUDA(cudaMemcpyAsync(&h, d_work, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));   // decode ctrl at offset 0
+    FZ_CUDA(cudaStreamSynchronize(st));
+    return h.err != 0 ? err_status(h.err) : FZ_OK;
 }
 
 fz_status fz_last_header(void* h_hdr)
@@ -585,6 +606,25 @@ void fz_profile_enable(int on)
 {
     std::lock_guard<std::mutex> g(fz::g_prof_mu);
     fz::g_prof_on = on != 0;
+}
+
+int fz_profile_timeline(int* h_ids, float* h_start_ms, float* h_end_ms, int max_records)
+{
+    std::lock_guard<std::mutex> g(fz::g_prof_mu);
+    const int n = (int)fz::g_prof_pending.size() < max_records ? (int)fz::g_prof_pending.size() : max_records;
+    if (n == 0) return 0;
+    const cudaEvent_t t0 = fz::g_prof_pending[0].a;
+    for (int k = 0; k < n; ++k) {
+        const auto& r = fz::g_prof_pending[k];
+        cudaEventSynchronize(r.b);
+        float a = 0.0f, b = 0.0f;
+        cudaEventElapsedTime(&a, t0, r.a);
+        cudaEventElapsedTime(&b, t0, r.b);
+        if (h_ids) h_ids[k] = r.id;
+        if (h_start_ms) h_start_ms[k] = a;
+        if (h_end_ms) h_end_ms[k] = b;
+    }
+    return n;
 }
 
 int fz_profile_read(double* h_ms, int* h_launches, int max_kernels)
@@ -828,7 +868,7 @@ fz_status fz_slab_decode(const void* d_stage, const fz_counts* local, const fz_s
     const Geom g = geom_of(sg.local, sg.n);
     FZ_CUDA(launch_decode_init(ctrl, st));
     FZ_CUDA(launch_tile_offsets(in, (uint32_t)nt, reinterpret_cast<uint32_t*>(wb + L.loc),
-                                reinterpret_cast<uint32_t*>(wb + L.bsum), ctrl, st));
+                                reinterpret_cast<uint32_t*>(wb + L.bsum), ctrl, st, local->nnz));
     FZ_CUDA(launch_record_tiles(reinterpret_cast<const uint2*>(in + dbase), local->n_delta, (uint32_t)nt, sg.g0,
                                 reinterpret_cast<uint32_t*>(wb + L.drange), st));
     DecodeArgs a{};

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(1024) k_nnz_block(const uint32_t* __restrict__
 }
 
 // D1 part 2: exclusive scan of the block totals (one block), grand total -> ctrl->nnz.
-__global__ void __launch_bounds__(1024) k_nnz_top(uint32_t* bsum, uint32_t nb, Ctrl* ctrl)
+__global__ void __launch_bounds__(1024) k_nnz_top(uint32_t* bsum, uint32_t nb, Ctrl* ctrl, uint64_t expect_nnz)
 {
     __shared__ uint32_t wsum[33];
     __shared__ unsigned long long carry;
@@ -208,7 +208,10 @@ __global__ void __launch_bounds__(1024) k_nnz_top(uint32_t* bsum, uint32_t nb, C
         if (threadIdx.x == 0) carry += total;
         __syncthreads();
     }
-    if (threadIdx.x == 0) ctrl->nnz = carry;
+    if (threadIdx.x == 0) {
+        ctrl->nnz = carry;
+        if (carry != expect_nnz) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_CORRUPT);   // popcount(flags) != nnz
+    }
 }
 
 // x carries: segmented exclusive scan of the per-tile x aggregates (only when some tile
@@ -815,7 +818,7 @@ cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles,
 }
 
 cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum, Ctrl* ctrl,
-                                cudaStream_t st)
+                                cudaStream_t st, uint64_t expect_nnz)
 {
     const uint32_t nb = (ntiles + 1023) / 1024;
     {
@@ -824,7 +827,7 @@ cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t*
     }
     {
         LaunchProf lp(K_OFFSETS, st);
-        k_nnz_top<<<1, 1024, 0, st>>>(bsum, nb, ctrl);
+        k_nnz_top<<<1, 1024, 0, st>>>(bsum, nb, ctrl, expect_nnz);
     }
     return cudaGetLastError();
 }

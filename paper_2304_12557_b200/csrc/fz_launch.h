@@ -76,7 +76,7 @@ cudaError_t launch_decode_init(Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, Ctrl* ctrl,
                                      cudaStream_t st);
 cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum,
-                                Ctrl* ctrl, cudaStream_t st);
+                                Ctrl* ctrl, cudaStream_t st, uint64_t expect_nnz);
 cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,
                                 cudaStream_t st);
 cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st, bool fuse_y = false);

@@ -72,6 +72,8 @@ def lib():
         "fz_decompress": ([P, S, P, u64, P, S, P], i),
         "fz_decompress_hdr": ([P, S, P, P, u64, P, S, P], i),
         "fz_last_header": ([P], i),
+        "fz_decompress_hdr_async": ([P, S, P, P, u64, P, S, P], i),
+        "fz_decompress_result": ([P, P], i),
         "fz_compress_host": ([P, pS, i, C.c_double, P, S, C.POINTER(S), P, P, S, P, S, P], i),
         "fz_decompress_host": ([P, S, P, u64, P, P, P, S, P], i),
         "fz_peek_header": ([P, S, C.POINTER(Info)], i),
@@ -87,6 +89,7 @@ def lib():
         "fz_profile_enable": ([i], None),
         "fz_profile_read": ([C.POINTER(C.c_double), C.POINTER(C.c_int), i], i),
         "fz_kernel_name": ([i], C.c_char_p),
+        "fz_profile_timeline": ([C.POINTER(C.c_int), C.POINTER(C.c_float), C.POINTER(C.c_float), i], i),
         "fz_slab_agg_elems": ([pS], u64),
         "fz_slab_decode": ([P, pC, pS, u64, u64, P, P, P, S, P], i),
         "fz_slab_carry": ([P, C.c_uint32, u64, P, P], i),
@@ -151,6 +154,16 @@ def profile_enable(on: bool = True):
     lib().fz_profile_enable(int(on))
 
 
+def profile_timeline(max_records: int = 4096) -> list:
+    """[(kernel name, start ms, end ms)] of the launches recorded since the last profile_read,
+    relative to the first one (profiling on)."""
+    ids = (C.c_int * max_records)()
+    a = (C.c_float * max_records)()
+    b = (C.c_float * max_records)()
+    k = lib().fz_profile_timeline(ids, a, b, max_records)
+    return [(lib().fz_kernel_name(ids[i]).decode(), a[i], b[i]) for i in range(k)]
+
+
 def profile_read() -> dict:
     """{kernel name: (total ms, launches)} since the last read (CUDA events per launch)."""
     ms = (C.c_double * 32)()
@@ -196,14 +209,21 @@ class Codec:
         self.hdr_size = size.value
         return self.out[: size.value], size.value
 
-    def decompress(self, buf, out=None, stream=None):
+    def decompress(self, buf, out=None, stream=None, sync=True):
         """Decompresses `buf`; when it is this codec's last output, the header comes from the
-        host copy kept by compress (fz_decompress_hdr: no blocking header read)."""
+        host copy kept by compress (fz_decompress_hdr: no blocking header read).  With
+        sync=False (own output only) the decode is only enqueued; call result() before using
+        `out`."""
         import torch
         if out is None:
             out = torch.empty(self.dims, dtype=torch.float32, device=self.device)
         own = (self.hdr_size is not None and buf.data_ptr() == self.out.data_ptr()
                and buf.numel() == self.hdr_size)
+        if own and not sync:
+            st = lib().fz_decompress_hdr_async(_ptr(buf), buf.numel(), self.hdr, _ptr(out), self.n,
+                                               _ptr(self.dwork), self.dwork.numel(), _stream(stream))
+            _check(st, "fz_decompress_hdr_async")
+            return out
         if own:
             st = lib().fz_decompress_hdr(_ptr(buf), buf.numel(), self.hdr, _ptr(out), self.n, _ptr(self.dwork),
                                          self.dwork.numel(), _stream(stream))
@@ -212,6 +232,14 @@ class Codec:
                                      self.dwork.numel(), _stream(stream))
         _check(st, "fz_decompress")
         return out
+
+
+def _codec_result(self, stream=None):
+    """Waits for an asynchronous decompress and raises on a recorded stream error."""
+    _check(lib().fz_decompress_result(_ptr(self.dwork), _stream(stream)), "fz_decompress_result")
+
+
+Codec.result = _codec_result
 
 
 def compress(field, mode=REL, eb=1e-3, params: Params | None = None, stream=None):

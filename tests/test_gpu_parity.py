@@ -299,6 +299,19 @@ def test_host_header_decompress_matches():
                                 C.c_void_p(codec.dwork.data_ptr()), codec.dwork.numel(), None)
     assert st == fz.OK
     assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    # asynchronous form: same result once fz_decompress_result returns OK
+    c = torch.full_like(a, float("nan"))
+    codec.decompress(buf, out=c, sync=False)
+    codec.result()
+    assert torch.equal(a.view(torch.int32), c.view(torch.int32))
+    # a flipped flag bit makes popcount(flags) disagree with nnz: reported by the result call
+    bad = buf.clone()
+    bad[200] ^= 1
+    codec.out[:size].copy_(bad)
+    codec.decompress(codec.out[:size], out=c, sync=False)
+    with pytest.raises(fz.FZError) as e:
+        codec.result()
+    assert e.value.status == fz.ERR_CORRUPT
 
 
 def test_generic_vector_kernel_parity(monkeypatch):
