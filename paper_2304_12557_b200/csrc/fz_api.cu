@@ -188,12 +188,28 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
     const uint32_t tb = a.tile_begin, nt = a.tile_end - a.tile_begin;
     // status words are per scan unit, indexed from the range start; outlier counts per tile
     FZ_CUDA(launch_init(W.ctrl(), W.status(), W.ocnt() + tb, nt, hp, st));
+    // the warp-specialized kernel derives the parameters in its prologue and its last CTA
+    // writes totals + header, so k_params and k_finalize are not launched for it
+    const bool fused = compress_uses_ws(a);
     if (hp == nullptr) {
         FZ_CUDA(launch_range(a.field, n, W.ctrl(), st));
-        FZ_CUDA(launch_params(W.ctrl(), mode, eb, n, st));
+        if (!fused) FZ_CUDA(launch_params(W.ctrl(), mode, eb, n, st));
     }
-    FZ_CUDA(launch_compress(a, st));
-    FZ_CUDA(launch_finalize(hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
+    CompressArgs b = a;
+    if (fused) {
+        b.derive = hp == nullptr;
+        b.finalize = 1;
+        b.eb_mode = mode;
+        b.eb = eb;
+        b.hdr_out = hdr_out;
+        b.hdr_cap = out_cap;
+        b.ndim = s.ndim;
+        for (uint32_t k = 0; k < 3; ++k) b.dims[k] = k < s.ndim ? s.dims[k] : 1;
+        b.n_hdr = n;
+        b.T_hdr = tiles_of(n);
+    }
+    FZ_CUDA(launch_compress(b, st));
+    if (!fused) FZ_CUDA(launch_finalize(hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
     return read_ctrl(W, h, st);
 }
 

@@ -26,12 +26,12 @@ constexpr uint32_t kUnionHaloMax = 4097;   // union arrays when the row halo nx+
 // h = w/2; hU = RD32(w/2 - U) with U = 2^(e-23), M = max|d| = m 2^e (Appendix A): the
 // fast-path threshold of pq_fast.  Fallback mode: hU = -1 (every element takes the exact
 // rule and the bound check).
-__device__ void set_quant_consts(Ctrl* ctrl)
+// h = w/2 and the fast-path threshold hU = RD32(w/2 - U) (-1: fast path off, fallback mode).
+__device__ void quant_consts(const fz_params& p, float& h, float& hU)
 {
-    const fz_params& p = ctrl->p;
-    ctrl->h = 0.5f * p.w;
+    h = 0.5f * p.w;
     if (p.fallback) {
-        ctrl->hU = -1.0f;
+        hU = -1.0f;
         return;
     }
     const float M = fmaxf(fabsf(p.mn), fabsf(p.mx));
@@ -41,8 +41,22 @@ __device__ void set_quant_consts(Ctrl* ctrl)
         frexp((double)M, &e);
         U = ldexp(1.0, e - 23);
     }
-    const double t = (double)ctrl->h - U;
-    ctrl->hU = t > 0.0 ? rd32(t) : -1.0f;
+    const double t = (double)h - U;
+    hU = t > 0.0 ? rd32(t) : -1.0f;
+}
+
+__device__ void set_quant_consts(Ctrl* ctrl)
+{
+    quant_consts(ctrl->p, ctrl->h, ctrl->hU);
+}
+
+// Appendix-A parameters from the range pass's result (k_params and the ws-kernel prologue).
+__device__ int params_from_range(const Ctrl* ctrl, int mode, double eb, uint64_t n, fz_params* p)
+{
+    if (ctrl->first_bad != ~0ull) return FZ_ERR_NONFINITE;
+    const float mn = n ? ord2f(ctrl->mn_enc) : 0.0f;
+    const float mx = n ? ord2f(ctrl->mx_enc) : 0.0f;
+    return derive_params(mn, mx, mode, eb, p);
 }
 
 // ------------------------------------------------------------------------------------
@@ -63,6 +77,7 @@ __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint
         ctrl->stage_overflow = 0;
         ctrl->nnz = ctrl->nd = ctrl->nv = ctrl->total = 0;
         ctrl->dcount = ctrl->vcount = 0;
+        ctrl->done = 0;
         if (set_params) {
             ctrl->p = p;
             set_quant_consts(ctrl);
@@ -133,11 +148,8 @@ __global__ void __launch_bounds__(256) k_range(const float* __restrict__ d, uint
 __global__ void k_params(Ctrl* ctrl, int mode, double eb, uint64_t n)
 {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (ctrl->first_bad != ~0ull) { ctrl->err = FZ_ERR_NONFINITE; return; }
-    float mn = n ? ord2f(ctrl->mn_enc) : 0.0f;
-    float mx = n ? ord2f(ctrl->mx_enc) : 0.0f;
     fz_params p;
-    int st = derive_params(mn, mx, mode, eb, &p);
+    const int st = params_from_range(ctrl, mode, eb, n, &p);
     if (st != FZ_OK) { ctrl->err = st; return; }
     ctrl->p = p;
     set_quant_consts(ctrl);
@@ -988,6 +1000,9 @@ struct WsShared {
     unsigned long long ob[2];
     volatile uint32_t ring_tail;   // payload ring blocks released by the scanner
     uint64_t desc_full[kDescQ];    // mbarrier per descriptor slot: completes when it is written
+    fz_params p;                   // parameters (derived in the prologue when a.derive)
+    QuantP P;
+    int perr;
     volatile uint32_t desc_head;   // descriptors published by the compute warps
     volatile uint32_t desc_tail;   // descriptors consumed by the scanner
     WsDesc desc[kDescQ];
@@ -1249,6 +1264,9 @@ __device__ __forceinline__ uint32_t tail_ws(const CompressArgs& a, WsShared& sh,
     return tn;
 }
 
+__device__ void finalize_stream(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64_t d0, uint64_t d1,
+                                uint64_t d2, uint64_t n, uint64_t T, Ctrl* ctrl, const fz_params& p);
+
 template <int NDIM>
 __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
 {
@@ -1264,22 +1282,44 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
     const uint32_t nunits = (a.tile_end - a.tile_begin + kUnitTiles - 1) / kUnitTiles;
 
     if (tid == 0) {
-        mbar_init(&sh.mbar, 1);
-        for (int k = 0; k < kDescQ; ++k) mbar_init(&sh.desc_full[k], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        sh.ring_tail = 0;
-        sh.desc_head = 0;
-        sh.desc_tail = 0;
-        sh.unit[0] = atomicAdd(&ctrl->ticket, 1u);
-        sh.tma_bits = 0;
-        if (sh.unit[0] < nunits) ws_issue<NDIM>(a, sh, inbuf, a.tile_begin + sh.unit[0] * kUnitTiles);
+        sh.perr = 0;
+        if (a.derive) {
+            // C0 parameters from k_range's result (every CTA derives the same values; CTA 0
+            // publishes them for the host and the header)
+            fz_params p;
+            const int st = params_from_range(ctrl, a.eb_mode, a.eb, a.n_hdr, &p);
+            sh.perr = st;
+            if (st == FZ_OK) {
+                float h, hU;
+                quant_consts(p, h, hU);
+                sh.p = p;
+                sh.P = QuantP{p.w, p.r, h, p.eb32, hU};
+                if (blockIdx.x == 0) { ctrl->p = p; ctrl->h = h; ctrl->hU = hU; }
+            } else if (blockIdx.x == 0) {
+                ctrl->err = st;
+            }
+        } else {
+            sh.p = ctrl->p;
+            sh.P = QuantP{ctrl->p.w, ctrl->p.r, ctrl->h, ctrl->p.eb32, ctrl->hU};
+        }
+        if (sh.perr == 0) {
+            mbar_init(&sh.mbar, 1);
+            for (int k = 0; k < kDescQ; ++k) mbar_init(&sh.desc_full[k], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            sh.ring_tail = 0;
+            sh.desc_head = 0;
+            sh.desc_tail = 0;
+            sh.unit[0] = atomicAdd(&ctrl->ticket, 1u);
+            sh.tma_bits = 0;
+            if (sh.unit[0] < nunits) ws_issue<NDIM>(a, sh, inbuf, a.tile_begin + sh.unit[0] * kUnitTiles);
+        }
     }
     __syncthreads();
+    if (sh.perr != 0) return;
 
     if (warp == kCta / 32) {
         // ================= scanner warp =================
-        if (a.rescan) return;
-        for (uint32_t dt = 0;; ++dt) {
+        for (uint32_t dt = 0; !a.rescan; ++dt) {
             // sleeps in hardware until the compute warps publish descriptor dt
             while (!mbar_try_wait_sleep(&sh.desc_full[dt % kDescQ], (dt / kDescQ) & 1u, 20000)) {
             }
@@ -1304,12 +1344,9 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
             }
             __syncwarp();
         }
-        return;
-    }
-
+    } else {
     // ================= compute warps =================
-    QuantP P;
-    P.w = ctrl->p.w; P.r = ctrl->p.r; P.h = ctrl->h; P.eb32 = ctrl->p.eb32; P.hU = ctrl->hU;
+    const QuantP P = sh.P;
     uint32_t phase = 0;      // parity of the next wait on the input stage
     uint32_t head = 0;       // payload ring blocks written so far
     for (int it = 0;; ++it) {
@@ -1380,22 +1417,36 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
             mbar_arrive(&sh.desc_full[dh % kDescQ]);
         }
     }
+    }
+    // C9: the last CTA to finish writes the totals and the header (replaces k_finalize)
+    __syncthreads();
+    if (a.finalize && tid == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(&ctrl->done, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence();
+            if (*(volatile int32_t*)&ctrl->err == 0)
+                finalize_stream(a.hdr_out, a.hdr_cap, a.ndim, a.dims[0], a.dims[1], a.dims[2], a.n_hdr, a.T_hdr,
+                                ctrl, sh.p);
+        }
+    }
 }
 
 // ------------------------------------------------------------------------------------
 // C9: header (outlier sections are placed by k_outlier_place when there are any).
 // ------------------------------------------------------------------------------------
-__global__ void k_finalize(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64_t d0, uint64_t d1,
-                           uint64_t d2, uint64_t n, uint64_t T, Ctrl* ctrl)
+// C9 totals and header (one thread): k_finalize, or the last CTA of the ws kernel.
+__device__ void finalize_stream(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64_t d0, uint64_t d1,
+                                uint64_t d2, uint64_t n, uint64_t T, Ctrl* ctrl, const fz_params& p)
 {
-    if (ctrl->err != 0 || threadIdx.x != 0) return;
-    const uint64_t nnz = ctrl->nnz, nd = ctrl->dcount, nv = ctrl->vcount;
+    const uint64_t nnz = *(volatile unsigned long long*)&ctrl->nnz;
+    const uint64_t nd = *(volatile unsigned long long*)&ctrl->dcount;
+    const uint64_t nv = *(volatile unsigned long long*)&ctrl->vcount;
     const uint64_t total = kHeaderBytes + 32 * T + 16 * nnz + 8 * nd + 8 * nv;
     ctrl->nd = nd;
     ctrl->nv = nv;
     ctrl->total = total;
     if (total > out_cap || out == nullptr) return;
-    const fz_params& p = ctrl->p;
     uint8_t h[128];
     for (int i = 0; i < 128; ++i) h[i] = 0;
     h[0] = 'F'; h[1] = 'Z'; h[2] = 'B'; h[3] = '2';
@@ -1417,6 +1468,13 @@ __global__ void k_finalize(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64
     uint4* o = reinterpret_cast<uint4*>(out);
     const uint4* hs = reinterpret_cast<const uint4*>(h);
     for (int i = 0; i < 8; ++i) o[i] = hs[i];
+}
+
+__global__ void k_finalize(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64_t d0, uint64_t d1,
+                           uint64_t d2, uint64_t n, uint64_t T, Ctrl* ctrl)
+{
+    if (ctrl->err != 0 || threadIdx.x != 0) return;
+    finalize_stream(out, out_cap, ndim, d0, d1, d2, n, T, ctrl, ctrl->p);
 }
 
 // Exclusive scan of the per-tile outlier counts (one block; only when outliers exist).
@@ -1549,6 +1607,15 @@ static cudaError_t launch_compress_ws(const CompressArgs& a, size_t sm, uint32_t
     if (grid == 0) return cudaSuccess;
     k_compress_ws<NDIM><<<(unsigned)grid, kWsThreads, sm, st>>>(a);
     return cudaGetLastError();
+}
+
+bool compress_uses_ws(const CompressArgs& a_in)
+{
+    CompressArgs a = a_in;
+    if (const char* e = getenv("FZ_EXP")) a.exp = atoi(e);
+    bool vec = false;
+    plan_smem(a, vec);
+    return vec && !(a.exp & 16);
 }
 
 cudaError_t launch_compress(const CompressArgs& a_in, cudaStream_t st)

@@ -35,6 +35,7 @@ struct Ctrl {
     // results (written by the last tile / k_finalize)
     unsigned long long nnz, nd, nv, total;
     unsigned long long dcount, vcount;   // outlier staging allocation counters (= totals)
+    uint32_t done;                       // CTAs finished (last one finalizes)
 };
 static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 
@@ -500,6 +501,16 @@ struct CompressArgs {
     uint32_t* o_vidx;
     uint32_t* o_vbits;
     int rescan;               // 1: outliers only, straight to final offsets via opre
+    // ws kernel only: parameters derived in the prologue from k_range's result (replaces
+    // k_params) and totals + header written by the last CTA to finish (replaces k_finalize)
+    int derive, finalize;
+    int eb_mode;
+    double eb;
+    uint8_t* hdr_out;         // 128-byte header destination (null: totals only)
+    uint64_t hdr_cap;         // bytes writable at hdr_out (whole stream capacity)
+    uint64_t dims[3];
+    uint32_t ndim;
+    uint64_t n_hdr, T_hdr;    // field size and tiles for the totals / header
     int exp;                  // FZ_EXP env var, bit 16: generic kernel instead of the warp-specialized one
 };
 

@@ -31,6 +31,7 @@ cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uin
 cudaError_t launch_range(const float* d, uint64_t n, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_params(Ctrl* ctrl, int mode, double eb, uint64_t n, cudaStream_t st);
 cudaError_t launch_compress(const CompressArgs& a, cudaStream_t st);
+bool compress_uses_ws(const CompressArgs& a);   // the warp-specialized kernel takes this launch
 cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint64_t n,
                             uint64_t T, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st);
