@@ -129,6 +129,15 @@ fz_status fz_decompress(const void* d_in, size_t in_size, float* d_field, uint64
 fz_status fz_decompress_hdr(const void* d_in, size_t in_size, const void* h_hdr, float* d_field,
                             uint64_t n, void* d_work, size_t work_bytes, void* stream);
 
+/* Asynchronous compression: the whole pipeline (range, parameters, fused kernel, outlier
+ * placement) is enqueued on `stream` with no host round trip.  fz_compress_result waits for
+ * `stream` and returns the status and the stream size (FZ_ERR_CAPACITY if it exceeds
+ * out_cap).  A staging overflow (more than N/64 + 1024 outliers of one kind; the synchronous
+ * fz_compress handles it with a second pass) is reported as FZ_ERR_WORKSPACE. */
+fz_status fz_compress_async(const float* d_field, const fz_shape* s, int eb_mode, double eb,
+                            void* d_out, size_t out_cap, void* d_work, size_t work_bytes, void* stream);
+fz_status fz_compress_result(const void* d_work, size_t out_cap, size_t* h_out_size, void* stream);
+
 /* Asynchronous form of fz_decompress_hdr: enqueues the decode on `stream` and returns without
  * waiting; argument errors are returned at once, stream errors (corrupt input, a popcount that
  * disagrees with nnz) are recorded in d_work and returned by fz_decompress_result, which waits
@@ -136,6 +145,15 @@ fz_status fz_decompress_hdr(const void* d_in, size_t in_size, const void* h_hdr,
 fz_status fz_decompress_hdr_async(const void* d_in, size_t in_size, const void* h_hdr, float* d_field,
                                   uint64_t n, void* d_work, size_t work_bytes, void* stream);
 fz_status fz_decompress_result(const void* d_work, void* stream);
+
+/* Fully device-driven asynchronous decompression: the host supplies only the expected shape
+ * (launch configuration); the stream header is parsed and checked on the device (magic,
+ * version, shape, N, tile count, size law against in_size) and every kernel takes the section
+ * counts and the bin width from the workspace.  Nothing blocks; the status comes from
+ * fz_decompress_result.  Lets a compress -> decompress pipeline run without host round trips
+ * (and be captured in a CUDA graph). */
+fz_status fz_decompress_async(const void* d_in, size_t in_size, const fz_shape* s, float* d_field,
+                              void* d_work, size_t work_bytes, void* stream);
 
 /* Copies the header of the last successful fz_compress / fz_compress_with_params on this
  * thread (128 bytes, the same bytes as the stream's header) to h_hdr.  FZ_ERR_ARG if none. */
@@ -234,6 +252,10 @@ int fz_last_launch_count(void);
  * the pending events, writes the summed milliseconds and launch counts per kernel kind
  * (indices 0..n-1, names from fz_kernel_name) and resets the totals; returns n. */
 void fz_profile_enable(int on);
+/* Restrict profiling to the kernels whose ids (fz_kernel_name order) are set in `mask`; the
+ * others launch without event records.  fz_profile_enable resets the mask to all kernels. */
+void fz_profile_mask(unsigned long long mask);
+
 int fz_profile_read(double* h_ms, int* h_launches, int max_kernels);
 
 /* Timeline of the launches recorded since the last fz_profile_read (profiling on): kernel id,

@@ -20,6 +20,7 @@ struct ProfRec {
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
+uint64_t g_prof_mask = ~0ull;     // kernels recorded (bit = KernelId)
 std::vector<ProfRec> g_prof_pending;
 std::vector<cudaEvent_t> g_prof_pool;
 double g_prof_ms[K_COUNT];
@@ -42,7 +43,7 @@ LaunchProf::LaunchProf(KernelId id_, cudaStream_t st_) : id(id_), st(st_), slot(
 {
     ++t_launches;
     std::lock_guard<std::mutex> g(g_prof_mu);
-    if (!g_prof_on) return;
+    if (!g_prof_on || !((g_prof_mask >> id) & 1)) return;
     ProfRec r{id, prof_event(), prof_event()};
     cudaEventRecord(r.a, st);
     g_prof_pending.push_back(r);
@@ -210,6 +211,7 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
     }
     FZ_CUDA(launch_compress(b, st));
     if (!fused) FZ_CUDA(launch_finalize(hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
+    if (h == nullptr) return FZ_OK;    // asynchronous: the caller reads ctrl later
     return read_ctrl(W, h, st);
 }
 
@@ -409,25 +411,37 @@ fz_status fz_peek_header(const void* h_hdr, size_t nbytes, fz_info* info)
 
 namespace {
 
+// dev_shape != nullptr: device-driven decode.  The host uses only the caller's shape (launch
+// configuration); k_decode_hdr parses the stream header on the device and every kernel takes
+// the section counts and the bin width from ctrl, so nothing waits for the host.
 fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int32_t* d_q, uint64_t n,
                           void* d_work, size_t work_bytes, cudaStream_t st, const void* h_hdr = nullptr,
-                          bool async = false)
+                          bool async = false, const fz_shape* dev_shape = nullptr)
 {
     if (d_in == nullptr || (d_field == nullptr && d_q == nullptr) || d_work == nullptr ||
         !aligned16(d_in) || !aligned16(d_work) || in_size < kHeaderBytes)
         return FZ_ERR_ARG;
-    uint8_t hdr[128];
-    if (h_hdr != nullptr) {
-        memcpy(hdr, h_hdr, 128);
+    const bool dev = dev_shape != nullptr;
+    fz_info I{};
+    if (dev) {
+        uint64_t nn;
+        if (!shape_n(dev_shape, &nn) || nn != n) return FZ_ERR_ARG;
+        I.shape = *dev_shape;
+        I.n = n;
+        I.tiles = tiles_of(n);
     } else {
-        FZ_CUDA(cudaMemcpyAsync(hdr, d_in, 128, cudaMemcpyDeviceToHost, st));
-        FZ_CUDA(cudaStreamSynchronize(st));
+        uint8_t hdr[128];
+        if (h_hdr != nullptr) {
+            memcpy(hdr, h_hdr, 128);
+        } else {
+            FZ_CUDA(cudaMemcpyAsync(hdr, d_in, 128, cudaMemcpyDeviceToHost, st));
+            FZ_CUDA(cudaStreamSynchronize(st));
+        }
+        fz_status rs = fz_peek_header(hdr, 128, &I);
+        if (rs != FZ_OK) return rs;
+        if (I.n != n) return FZ_ERR_ARG;
+        if (in_size < I.total_size) return FZ_ERR_CORRUPT;
     }
-    fz_info I;
-    fz_status rs = fz_peek_header(hdr, 128, &I);
-    if (rs != FZ_OK) return rs;
-    if (I.n != n) return FZ_ERR_ARG;
-    if (in_size < I.total_size) return FZ_ERR_CORRUPT;
     const DecodeLayout L = decode_layout(I.shape);
     if (work_bytes < L.total) return FZ_ERR_WORKSPACE;
     uint8_t* wb = static_cast<uint8_t*>(d_work);
@@ -449,18 +463,28 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     const bool deq = d_q == nullptr;
 
     const bool fuse_y = decode_fuses_y(I.shape) && !(exp_bits() & 128);
-    FZ_CUDA(launch_decode_init(ctrl, st));
-    FZ_CUDA(launch_validate_outliers(drec, I.counts.n_delta, n, ctrl, st));
-    FZ_CUDA(launch_validate_outliers(vrec, I.counts.n_value, n, ctrl, st));
-    FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st, I.counts.nnz));
     auto* drange = reinterpret_cast<uint32_t*>(wb + L.drange);
-    FZ_CUDA(launch_record_tiles(drec, I.counts.n_delta, (uint32_t)T, 0, drange, st));
+    const float* wp = (dev && deq) ? &ctrl->dec_w : nullptr;   // device bin width (dev mode)
+    if (dev) {
+        FZ_CUDA(launch_decode_hdr(ctrl, in, in_size, I.shape, n, T, st));
+        FZ_CUDA(launch_validate_dev(in + pbase, n, ctrl, st));
+        FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st, ~0ull));
+        FZ_CUDA(launch_record_tiles_dev(in + pbase, ctrl, (uint32_t)T, drange, st));
+    } else {
+        FZ_CUDA(launch_decode_init(ctrl, st));
+        FZ_CUDA(launch_validate_outliers(drec, I.counts.n_delta, n, ctrl, st));
+        FZ_CUDA(launch_validate_outliers(vrec, I.counts.n_value, n, ctrl, st));
+        FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st, I.counts.nnz));
+        FZ_CUDA(launch_record_tiles(drec, I.counts.n_delta, (uint32_t)T, 0, drange, st));
+    }
     DecodeArgs a{};
     a.flags = in + kHeaderBytes;
     a.payload = in + pbase;
     a.drec = drec;
     a.nnz_total = I.counts.nnz;
     a.nd = I.counts.n_delta;
+    a.dev = dev ? 1 : 0;
+    a.wp = wp;
     a.g = g;
     a.tiles = (uint32_t)T;
     a.w = deq ? I.params.w : 0.0f;
@@ -479,7 +503,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     FZ_CUDA(launch_decode_tiles(a, st, fuse_y));
     // x carries exist when some tile starts inside a row (always for 1-D fields)
     const bool carries = T > 1 && (g.ndim == 1 || !(g.nx <= kTileCodes && kTileCodes % g.nx == 0));
-    if (g.ndim == 1 && !deq) a.w = 0.0f;
+    if (g.ndim == 1 && !deq) { a.w = 0.0f; a.wp = nullptr; }
     if (g.ndim == 1 && !deq) {
         if (carries) FZ_CUDA(launch_xcarry(a, xloc, xbagg, true, st));
     } else {
@@ -487,23 +511,26 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     }
     const float wq = deq ? I.params.w : 0.0f;
     if (I.shape.ndim == 2) {
-        if (!fuse_y) FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1], sums, wq, st));
+        if (!fuse_y) FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1], sums, wq, st, wp));
     } else if (I.shape.ndim == 3) {
         if (!fuse_y)
             FZ_CUDA(launch_scan_axis(q, I.shape.dims[0], I.shape.dims[1], I.shape.dims[2], sums, 0.0f, st));
         if (fuse_y && a.yseg == 2)
             FZ_CUDA(launch_zwalk_ycarry(q, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], wq, a.ycarry,
-                                        (uint32_t)I.shape.dims[2], st));
+                                        (uint32_t)I.shape.dims[2], st, wp));
         else
-            FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], sums, wq, st));
+            FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], sums, wq, st, wp));
     }
-    if (deq) FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+    if (deq) {
+        if (dev) FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
+        else FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+    }
     if (async) return FZ_OK;     // status later: fz_decompress_result
     Ctrl h;
     FZ_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     FZ_CUDA(cudaStreamSynchronize(st));
     if (h.err != 0) return err_status(h.err);
-    if (h.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;   // sum of popcount(flags) == nnz
+    if (!dev && h.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;   // sum of popcount(flags) == nnz
     return FZ_OK;
 }
 
@@ -529,6 +556,48 @@ fz_status fz_decompress_hdr(const void* d_in, size_t in_size, const void* h_hdr,
                            static_cast<cudaStream_t>(stream), h_hdr);
 }
 
+fz_status fz_compress_async(const float* d_field, const fz_shape* s, int eb_mode, double eb, void* d_out,
+                            size_t out_cap, void* d_work, size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    uint64_t n;
+    if (!shape_n(s, &n) || d_field == nullptr || d_out == nullptr || d_work == nullptr || !aligned16(d_field) ||
+        !aligned16(d_out) || !aligned16(d_work))
+        return FZ_ERR_ARG;
+    if (!(eb > 0.0) || !std::isfinite(eb) || (eb_mode != FZ_EB_ABS && eb_mode != FZ_EB_REL)) return FZ_ERR_ARG;
+    const uint64_t T = tiles_of(n);
+    Work W{compress_layout(n, T), static_cast<uint8_t*>(d_work)};
+    if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const Geom g = geom_of(*s, n);
+    uint8_t* out = static_cast<uint8_t*>(d_out);
+    CompressArgs a = make_args(W, d_field, 0, g, 0, (uint32_t)T);
+    const uint64_t pbase = kHeaderBytes + 32 * T;
+    a.flags_out = out + kHeaderBytes;
+    a.flags_cap = out_cap > kHeaderBytes ? out_cap - kHeaderBytes : 0;
+    a.payload_out = out + pbase;
+    a.payload_cap = out_cap > pbase ? out_cap - pbase : 0;
+    fz_status rs = compress_run(W, a, nullptr, eb_mode, eb, out, out_cap, *s, n, nullptr, st);
+    if (rs != FZ_OK) return rs;
+    FZ_CUDA(launch_outlier_scan(W.ocnt(), W.opre(), (uint32_t)T, st, W.ctrl()));
+    FZ_CUDA(launch_outlier_place_dev(W.ocnt(), W.obase(), W.opre(), (uint32_t)T, W.dstage(), W.vstage(),
+                                     a.payload_out, a.payload_cap, W.ctrl(), st));
+    return FZ_OK;
+}
+
+fz_status fz_compress_result(const void* d_work, size_t out_cap, size_t* out_size, void* stream)
+{
+    if (d_work == nullptr || out_size == nullptr) return FZ_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Ctrl h;
+    FZ_CUDA(cudaMemcpyAsync(&h, d_work, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));   // compress ctrl at offset 0
+    FZ_CUDA(cudaStreamSynchronize(st));
+    if (h.err != 0) return err_status(h.err);
+    *out_size = (size_t)h.total;
+    if (h.total > out_cap) return FZ_ERR_CAPACITY;
+    return FZ_OK;
+}
+
 fz_status fz_decompress_hdr_async(const void* d_in, size_t in_size, const void* h_hdr, float* d_field, uint64_t n,
                                   void* d_work, size_t work_bytes, void* stream)
 {
@@ -536,6 +605,16 @@ fz_status fz_decompress_hdr_async(const void* d_in, size_t in_size, const void* 
     if (d_field == nullptr || !aligned16(d_field) || h_hdr == nullptr) return FZ_ERR_ARG;
     return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
                            static_cast<cudaStream_t>(stream), h_hdr, true);
+}
+
+fz_status fz_decompress_async(const void* d_in, size_t in_size, const fz_shape* s, float* d_field, void* d_work,
+                              size_t work_bytes, void* stream)
+{
+    LaunchScope ls;
+    uint64_t n;
+    if (d_field == nullptr || !aligned16(d_field) || !shape_n(s, &n)) return FZ_ERR_ARG;
+    return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
+                           static_cast<cudaStream_t>(stream), nullptr, true, s);
 }
 
 fz_status fz_decompress_result(const void* d_work, void* stream)
@@ -622,6 +701,13 @@ void fz_profile_enable(int on)
 {
     std::lock_guard<std::mutex> g(fz::g_prof_mu);
     fz::g_prof_on = on != 0;
+    fz::g_prof_mask = ~0ull;
+}
+
+void fz_profile_mask(unsigned long long mask)
+{
+    std::lock_guard<std::mutex> g(fz::g_prof_mu);
+    fz::g_prof_mask = mask;
 }
 
 int fz_profile_timeline(int* h_ids, float* h_start_ms, float* h_end_ms, int max_records)

@@ -1478,11 +1478,14 @@ __global__ void k_finalize(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64
 }
 
 // Exclusive scan of the per-tile outlier counts (one block; only when outliers exist).
-__global__ void __launch_bounds__(1024) k_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles)
+__global__ void __launch_bounds__(1024) k_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles,
+                                                       const Ctrl* ctrl)
 {
     __shared__ uint32_t wd[32], wv[32];
     __shared__ uint32_t carry_d, carry_v;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // device-driven mode: nothing to do without outliers (ctrl == null: the host checked)
+    if (ctrl != nullptr && (ctrl->err != 0 || ctrl->dcount + ctrl->vcount == 0)) return;
     if (tid == 0) { carry_d = 0; carry_v = 0; }
     __syncthreads();
     for (uint32_t base = 0; base < ntiles; base += 1024) {
@@ -1526,6 +1529,34 @@ __global__ void k_outlier_place(const uint2* ocnt, const uint2* obase, const uin
             if (vidx) { vidx[p.y + k] = r.x; vbits[p.y + k] = r.y; }
             else vout[p.y + k] = r;
         }
+    }
+}
+
+// Device-driven placement (asynchronous compression): destinations from the totals in ctrl;
+// a staging overflow (the rescan needs the host) is reported as FZ_ERR_WORKSPACE.
+__global__ void k_outlier_place_dev(const uint2* ocnt, const uint2* obase, const uint2* opre, uint32_t ntiles,
+                                    const uint2* dstage, const uint2* vstage, uint8_t* payload_out,
+                                    uint64_t payload_cap, Ctrl* ctrl)
+{
+    if (ctrl->err != 0) return;
+    const uint64_t nd = ctrl->dcount, nv = ctrl->vcount, nnz = ctrl->nnz;
+    if (nd + nv == 0) return;
+    if (ctrl->stage_overflow) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_WORKSPACE);
+        return;
+    }
+    if (16 * nnz + 8 * (nd + nv) > payload_cap) return;   // capacity: reported by the result call
+    uint2* dout = reinterpret_cast<uint2*>(payload_out + 16 * nnz);
+    uint2* vout = dout + nd;
+    const int lane = threadIdx.x & 31;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t t = wid; t < ntiles; t += nw) {
+        const uint2 c = ocnt[t];
+        if ((c.x | c.y) == 0) continue;
+        const uint2 b = obase[t], p = opre[t];
+        for (uint32_t k = lane; k < c.x; k += 32) dout[p.x + k] = dstage[b.x + k];
+        for (uint32_t k = lane; k < c.y; k += 32) vout[p.y + k] = vstage[b.y + k];
     }
 }
 
@@ -1690,10 +1721,23 @@ cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint6
     return cudaGetLastError();
 }
 
-cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st)
+cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st, const Ctrl* ctrl)
 {
     LaunchProf lp(K_OUTLIERS, st);
-    k_outlier_scan<<<1, 1024, 0, st>>>(ocnt, opre, ntiles);
+    k_outlier_scan<<<1, 1024, 0, st>>>(ocnt, opre, ntiles, ctrl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_outlier_place_dev(const uint2* ocnt, const uint2* obase, const uint2* opre, uint32_t ntiles,
+                                     const uint2* dstage, const uint2* vstage, uint8_t* payload_out,
+                                     uint64_t payload_cap, Ctrl* ctrl, cudaStream_t st)
+{
+    LaunchProf lp(K_OUTLIERS, st);
+    unsigned grid = (unsigned)((ntiles + 7) / 8);
+    if (grid > (unsigned)num_sms() * 8) grid = num_sms() * 8;
+    if (grid < 1) grid = 1;
+    k_outlier_place_dev<<<grid, 256, 0, st>>>(ocnt, obase, opre, ntiles, dstage, vstage, payload_out, payload_cap,
+                                              ctrl);
     return cudaGetLastError();
 }
 

@@ -70,6 +70,46 @@ __global__ void k_decode_init(Ctrl* ctrl)
     }
 }
 
+// Device-driven decode: the stream header is parsed on the device (thread 0); the section
+// counts and the bin width go to ctrl, where every later kernel reads them, so the host needs
+// nothing from the stream.  A header that does not match (magic, version, shape, N, T, size
+// law, capacity, bin width) sets FZ_ERR_CORRUPT and zero counts (the kernels then read nothing
+// outside the flags).
+__global__ void k_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, uint32_t ndim, uint64_t d0,
+                             uint64_t d1, uint64_t d2, uint64_t n, uint64_t T)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    ctrl->err = 0;
+    ctrl->nnz = 0;
+    auto u64 = [&](int off) {
+        uint64_t v;
+        memcpy(&v, in + off, 8);
+        return v;
+    };
+    uint32_t magic;
+    uint16_t ver;
+    float w;
+    memcpy(&magic, in, 4);
+    memcpy(&ver, in + 4, 2);
+    memcpy(&w, in + 64, 4);
+    const uint64_t cT = u64(80), nnz = u64(88), nd = u64(96), nv = u64(104), total = u64(112);
+    const uint64_t dm[3] = {d0, d1, d2};
+    bool ok = magic == 0x32425A46u /* "FZB2" */ && ver == 1 && in[8] == ndim && u64(40) == n && cT == T &&
+              total <= in_size && nnz <= 256 * T && nd <= n && nv <= n &&
+              total == kHeaderBytes + 32 * T + 16 * nnz + 8 * nd + 8 * nv && w > 0.0f && isfinite(w);
+    for (uint32_t k = 0; k < 3; ++k) ok = ok && u64(16 + 8 * k) == (k < ndim ? dm[k] : 1);
+    if (!ok) {
+        ctrl->err = FZ_ERR_CORRUPT;
+        ctrl->dec_nnz = ctrl->dec_nd = ctrl->dec_nv = 0;
+        ctrl->dec_w = 0.0f;
+        return;
+    }
+    ctrl->dec_nnz = nnz;
+    ctrl->dec_nd = nd;
+    ctrl->dec_nv = nv;
+    ctrl->dec_w = w;
+}
+
 // Outlier lists must be strictly increasing and inside the field.
 __global__ void k_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, Ctrl* ctrl)
 {
@@ -82,19 +122,54 @@ __global__ void k_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, 
 
 // Per-tile delta-outlier ranges: records [drange[t], drange[t+1]) fall in tile t (records
 // ascend; entries are clamped by the reader, so a corrupt list cannot index out of range).
-__global__ void k_record_tiles(const uint2* __restrict__ rec, uint64_t nd, uint32_t ntiles, uint64_t gbase,
-                               uint32_t* __restrict__ drange)
+// Device-driven forms: records and counts located from ctrl (payload = the stream's payload
+// section; which = 0 delta records, 1 value records).
+// Both record lists in one launch: index k < nd checks the delta list, the rest the value list.
+__global__ void k_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl)
 {
-    auto tile_of = [&](uint64_t k) -> int64_t {
-        const int64_t rel = (int64_t)rec[k].x - (int64_t)gbase;
-        const int64_t tk = rel < 0 ? 0 : rel / kTileCodes;
-        return tk < (int64_t)ntiles ? tk : (int64_t)ntiles;
-    };
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nd;
+    const uint64_t nnz = ctrl->dec_nnz, nd = ctrl->dec_nd, nv = ctrl->dec_nv;
+    const uint2* drec = reinterpret_cast<const uint2*>(payload + 16 * nnz);
+    const uint2* vrec = drec + nd;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nd + nv;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        const int64_t tk = k < nd ? tile_of(k) : (int64_t)ntiles;
-        const int64_t tp = k > 0 ? tile_of(k - 1) : -1;
-        for (int64_t t = tp + 1; t <= tk; ++t) drange[t] = (uint32_t)k;
+        const uint2* rec = k < nd ? drec : vrec;
+        const uint64_t j = k < nd ? k : k - nd;
+        const uint32_t idx = rec[j].x;
+        if (idx >= n || (j > 0 && rec[j - 1].x >= idx)) atomicExch(&ctrl->err, (int)FZ_ERR_CORRUPT);
+    }
+}
+
+__global__ void k_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n)
+{
+    const uint64_t cnt = ctrl->dec_nv;
+    const uint2* rec = reinterpret_cast<const uint2*>(payload + 16 * ctrl->dec_nnz + 8 * ctrl->dec_nd);
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint2 r = rec[k];
+        if (r.x < n) out[r.x] = __uint_as_float(r.y);
+    }
+}
+
+__global__ void k_record_tiles(const uint2* __restrict__ rec, uint64_t nd, uint32_t ntiles, uint64_t gbase,
+                               uint32_t* __restrict__ drange, const uint8_t* payload = nullptr,
+                               const Ctrl* ctrl = nullptr)
+{
+    if (ctrl != nullptr) {   // device-driven: records and count from the parsed header
+        nd = ctrl->dec_nd;
+        rec = reinterpret_cast<const uint2*>(payload + 16 * ctrl->dec_nnz);
+    }
+    if (nd == 0) return;     // readers skip the ranges without records
+    // one tile boundary per thread: drange[t] = first record at or after element 2048 t
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= ntiles;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t e = (int64_t)(t * kTileCodes);
+        uint64_t l = 0, h = nd;
+        while (l < h) {
+            const uint64_t m = (l + h) / 2;
+            if ((int64_t)rec[m].x - (int64_t)gbase < e) l = m + 1;
+            else h = m;
+        }
+        drange[t] = (uint32_t)l;
     }
 }
 
@@ -210,7 +285,8 @@ __global__ void __launch_bounds__(1024) k_nnz_top(uint32_t* bsum, uint32_t nb, C
     }
     if (threadIdx.x == 0) {
         ctrl->nnz = carry;
-        if (carry != expect_nnz) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_CORRUPT);   // popcount(flags) != nnz
+        const uint64_t want = expect_nnz == ~0ull ? ctrl->dec_nnz : expect_nnz;
+        if (carry != want) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_CORRUPT);   // popcount(flags) != nnz
     }
 }
 
@@ -282,7 +358,7 @@ __device__ __forceinline__ TileIn tile_in(const DecodeArgs& a, uint32_t t)
     in.fw = lane < 8 ? __ldg(reinterpret_cast<const uint32_t*>(a.flags) + 8 * (uint64_t)t + lane) : 0u;
     in.tbase = (uint64_t)__ldg(a.bpre + (t >> 10)) + __ldg(a.loc + t);
     in.rlo = in.rhi = 0;
-    if (a.nd > 0) {
+    if ((a.dev ? a.ctrl->dec_nd : a.nd) > 0) {
         in.rlo = __ldg(a.drange + t);
         in.rhi = __ldg(a.drange + t + 1);
     }
@@ -298,7 +374,7 @@ __device__ __forceinline__ uint4 tile_blk(const DecodeArgs& a, const TileIn& in)
     uint4 blk = make_uint4(0, 0, 0, 0);
     if ((F >> lane) & 1u) {
         const uint64_t bi = in.tbase + wpre + __popc(F & ((1u << lane) - 1u));
-        if (bi < a.nnz_total) blk = __ldcs(reinterpret_cast<const uint4*>(a.payload) + bi);
+        if (bi < (a.dev ? a.ctrl->dec_nnz : a.nnz_total)) blk = __ldcs(reinterpret_cast<const uint4*>(a.payload) + bi);
         else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
     }
     return blk;
@@ -322,7 +398,8 @@ __device__ __forceinline__ void patch_deltas(const DecodeArgs& a, DecSmem& sm, i
                                              int32_t (&dl)[8])
 {
     const int tid = threadIdx.x;
-    const uint32_t nd32 = (uint32_t)a.nd;
+    const uint32_t nd32 = (uint32_t)(a.dev ? a.ctrl->dec_nd : a.nd);
+    const uint2* drec = a.dev ? reinterpret_cast<const uint2*>(a.payload + 16 * a.ctrl->dec_nnz) : a.drec;
     rlo = rlo < nd32 ? rlo : nd32;
     rhi = rhi < rlo ? rlo : (rhi < nd32 ? rhi : nd32);
     if (rhi > rlo) {   // rare, block-uniform
@@ -330,7 +407,7 @@ __device__ __forceinline__ void patch_deltas(const DecodeArgs& a, DecSmem& sm, i
         for (int u = 0; u < 8; ++u) sm.D[8 * tid + u] = dl[u];
         __syncthreads();
         for (uint32_t k = rlo + tid; k < rhi; k += kCta) {
-            const uint2 r = a.drec[k];
+            const uint2 r = drec[k];
             const uint64_t e = (uint64_t)r.x - a.gbase - (uint64_t)s;
             if (e < (uint64_t)kTileCodes) sm.D[e] = (int32_t)r.y;
             else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
@@ -455,10 +532,22 @@ __device__ __forceinline__ Seg decode_tile_x(const DecodeArgs& a, DecSmem& sm, u
     return tagg;
 }
 
+// Device-driven mode: the parsed counts are read once per CTA into the CTA's copy of the
+// arguments (uniform registers), off every tile's critical path.
+__device__ __forceinline__ void resolve_dev(DecodeArgs& a)
+{
+    if (!a.dev) return;
+    a.nnz_total = a.ctrl->dec_nnz;
+    a.nd = a.ctrl->dec_nd;
+    a.drec = reinterpret_cast<const uint2*>(a.payload + 16 * a.nnz_total);
+    a.dev = 0;
+}
+
 // One CTA per tile: many tiles in flight per SM.
 template <int NDIM>
 __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
 {
+    resolve_dev(a);
     __shared__ DecSmem sm;
     const int tid = threadIdx.x;
     const uint32_t n = a.g.n;
@@ -491,6 +580,7 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
 template <int R>
 __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
 {
+    resolve_dev(a);
     constexpr int C = 8 / R;
     __shared__ DecSmem sm;
     const int tid = threadIdx.x;
@@ -556,8 +646,9 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
 // dequantized here (D6).  One CTA per tile.
 template <int NDIM>
 __global__ void __launch_bounds__(kCta) k_xfix(int32_t* q, const uint2* xloc, const uint2* xbpre, uint32_t ntiles,
-                                               uint32_t n, uint32_t nx, float w, int carries)
+                                               uint32_t n, uint32_t nx, float w_in, int carries, const float* wp)
 {
+    const float w = wp ? *wp : w_in;
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t s = (uint64_t)t * kTileCodes;
         uint32_t carry = 0;
@@ -620,8 +711,9 @@ __global__ void k_scan_chunks(uint64_t outer, uint64_t W, uint64_t nch, uint32_t
 }
 
 __global__ void k_scan_apply(int32_t* v, uint64_t outer, uint64_t L, uint64_t W, uint64_t nch,
-                             const uint32_t* __restrict__ sums, float dequant_w)
+                             const uint32_t* __restrict__ sums, float dequant_w_in, const float* wp)
 {
+    const float dequant_w = wp ? *wp : dequant_w_in;
     const uint64_t total = outer * nch * W;
     for (uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
          gid += (uint64_t)gridDim.x * blockDim.x) {
@@ -640,8 +732,10 @@ __global__ void k_scan_apply(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
 // Single-pass inclusive scan along L when there are many independent columns: one thread
 // per column walks L with 8 loads in flight (8 B/element of traffic instead of 12).
 __global__ void __launch_bounds__(256) k_scan_walk(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
-                                                   float dequant_w, const int32_t* __restrict__ carry)
+                                                   float dequant_w_in, const int32_t* __restrict__ carry,
+                                                   const float* wp)
 {
+    const float dequant_w = wp ? *wp : dequant_w_in;
     const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= outer * W) return;
     const uint64_t w = gid % W, o = gid / W;
@@ -673,9 +767,11 @@ __global__ void __launch_bounds__(256) k_scan_walk(int32_t* v, uint64_t outer, u
 // of the upper half of a plane decoded as two segments by k_decode_planes).
 template <int V, int U>
 __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
-                                                     float dequant_w, const int32_t* __restrict__ carry,
-                                                     const int32_t* __restrict__ ycarry, uint32_t ynx)
+                                                     float dequant_w_in, const int32_t* __restrict__ carry,
+                                                     const int32_t* __restrict__ ycarry, uint32_t ynx,
+                                                     const float* wp)
 {
+    const float dequant_w = wp ? *wp : dequant_w_in;
     using VT = typename std::conditional<V == 4, int4, int2>::type;
     const uint64_t Wv = W / V;
     const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -808,12 +904,45 @@ cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n,
     return cudaGetLastError();
 }
 
+cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, const fz_shape& s, uint64_t n,
+                              uint64_t T, cudaStream_t st)
+{
+    uint64_t d[3] = {1, 1, 1};
+    for (uint32_t k = 0; k < s.ndim && k < 3; ++k) d[k] = s.dims[k];
+    LaunchProf lp(K_DINIT, st);
+    k_decode_hdr<<<1, 32, 0, st>>>(ctrl, in, in_size, s.ndim, d[0], d[1], d[2], n, T);
+    return cudaGetLastError();
+}
+
+// fixed grids: the record counts are only known on the device
+cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, cudaStream_t st)
+{
+    LaunchProf lp(K_VALIDATE, st);
+    k_validate_dev<<<num_sms(), 256, 0, st>>>(payload, n, ctrl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_record_tiles_dev(const uint8_t* payload, const Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
+                                    cudaStream_t st)
+{
+    LaunchProf lp(K_OFFSETS, st);
+    k_record_tiles<<<grid_for((uint64_t)ntiles + 1), 256, 0, st>>>(nullptr, 0, ntiles, 0, drange, payload, ctrl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st)
+{
+    LaunchProf lp(K_VPATCH, st);
+    k_value_patch_dev<<<num_sms(), 256, 0, st>>>(out, payload, ctrl, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,
                                 cudaStream_t st)
 {
     if (nd == 0) return cudaSuccess;
     LaunchProf lp(K_OFFSETS, st);
-    k_record_tiles<<<grid_for(nd + 1), 256, 0, st>>>(drec, nd, ntiles, gbase, drange);
+    k_record_tiles<<<grid_for((uint64_t)ntiles + 1), 256, 0, st>>>(drec, nd, ntiles, gbase, drange);
     return cudaGetLastError();
 }
 
@@ -881,9 +1010,9 @@ cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool c
     unsigned grid = a.tiles < (uint32_t)num_sms() * 8 ? a.tiles : num_sms() * 8;
     LaunchProf lp(K_XCARRY, st);
     switch (a.g.ndim) {
-        case 1: k_xfix<1><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries); break;
-        case 2: k_xfix<2><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries); break;
-        default: k_xfix<3><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries); break;
+        case 1: k_xfix<1><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries, a.wp); break;
+        case 2: k_xfix<2><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries, nullptr); break;
+        default: k_xfix<3><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries, nullptr); break;
     }
     return cudaGetLastError();
 }
@@ -899,27 +1028,28 @@ static int walk_mode()
 
 // Column walk along L (stride W): vector columns when the rows allow it.
 static void launch_walk(int32_t* data, uint64_t outer, uint64_t L, uint64_t W, float w, const int32_t* carry,
-                        cudaStream_t st, const int32_t* ycarry = nullptr, uint32_t ynx = 0)
+                        cudaStream_t st, const int32_t* ycarry = nullptr, uint32_t ynx = 0,
+                        const float* wp = nullptr)
 {
     const int m = walk_mode();
     const bool a16 = (reinterpret_cast<uintptr_t>(data) & 15) == 0;
     if (m != 3 && W % 4 == 0 && a16 && m != 1) {
         const uint64_t thr = outer * W / 4;
-        k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx);
+        k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx, wp);
     } else if (m != 3 && W % 2 == 0 && a16) {
         const uint64_t thr = outer * W / 2;
-        k_scan_walk_v<2, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx);
+        k_scan_walk_v<2, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx, wp);
     } else {
-        k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry);
+        k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, wp);
     }
 }
 
 cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t W, uint32_t* sums,
-                             float dequant_w, cudaStream_t st)
+                             float dequant_w, cudaStream_t st, const float* wp)
 {
     if (outer * W >= 32768) {
         LaunchProf lp(K_SCAN_WALK, st);
-        launch_walk(data, outer, L, W, dequant_w, nullptr, st);
+        launch_walk(data, outer, L, W, dequant_w, nullptr, st, nullptr, 0, wp);
         return cudaGetLastError();
     }
     const uint64_t nch = (L + kScanChunk - 1) / kScanChunk;
@@ -934,7 +1064,7 @@ cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t
     }
     {
         LaunchProf lp(K_SCAN_APPLY, st);
-        k_scan_apply<<<grid_for(work), 256, 0, st>>>(data, outer, L, W, nch, sums, dequant_w);
+        k_scan_apply<<<grid_for(work), 256, 0, st>>>(data, outer, L, W, nch, sums, dequant_w, wp);
     }
     return cudaGetLastError();
 }
@@ -963,12 +1093,12 @@ cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t el
 }
 
 cudaError_t launch_zwalk_ycarry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* ycarry, uint32_t nx,
-                               cudaStream_t st)
+                               cudaStream_t st, const float* wp)
 {
     LaunchProf lp(K_SCAN_WALK, st);
     if (W % 4 != 0 || (reinterpret_cast<uintptr_t>(data) & 15) != 0) return cudaErrorInvalidValue;
     const uint64_t thr = W / 4;
-    k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, 1, L, W, w, nullptr, ycarry, nx);
+    k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, 1, L, W, w, nullptr, ycarry, nx, wp);
     return cudaGetLastError();
 }
 

@@ -36,6 +36,9 @@ struct Ctrl {
     unsigned long long nnz, nd, nv, total;
     unsigned long long dcount, vcount;   // outlier staging allocation counters (= totals)
     uint32_t done;                       // CTAs finished (last one finalizes)
+    // decoder, device-driven mode (k_decode_hdr parses the stream header on the device)
+    unsigned long long dec_nnz, dec_nd, dec_nv;
+    float dec_w;
 };
 static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 

@@ -34,7 +34,11 @@ cudaError_t launch_compress(const CompressArgs& a, cudaStream_t st);
 bool compress_uses_ws(const CompressArgs& a);   // the warp-specialized kernel takes this launch
 cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint64_t n,
                             uint64_t T, Ctrl* ctrl, cudaStream_t st);
-cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st);
+cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st,
+                                const Ctrl* ctrl = nullptr);
+cudaError_t launch_outlier_place_dev(const uint2* ocnt, const uint2* obase, const uint2* opre, uint32_t ntiles,
+                                     const uint2* dstage, const uint2* vstage, uint8_t* payload_out,
+                                     uint64_t payload_cap, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_outlier_place(const uint2* ocnt, const uint2* obase, const uint2* opre,
                                  uint32_t ntiles, const uint2* dstage, const uint2* vstage,
                                  uint2* dout, uint2* vout, uint32_t* didx, int32_t* dval,
@@ -61,6 +65,8 @@ struct DecodeArgs {
     uint32_t yseg;              // CTAs (segments) per plane: 1, or 2 with the carry in ycarry
     int32_t* ycarry;            // [nz][nx] column totals of the lower segment (yseg == 2)
     const uint32_t* drange;     // per-tile delta-outlier record ranges (k_record_tiles)
+    int dev;                    // 1: nnz / n_delta / delta records come from ctrl (k_decode_hdr)
+    const float* wp;            // device bin width for dequantization (dev mode), else null
 };
 
 // The y scan runs inside the decode (one CTA per plane) when every tile holds whole rows of
@@ -78,21 +84,29 @@ cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n,
                                      cudaStream_t st);
 cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum,
                                 Ctrl* ctrl, cudaStream_t st, uint64_t expect_nnz);
+// device-driven decode (counts parsed from the stream header on the device)
+cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, const fz_shape& s, uint64_t n,
+                              uint64_t T, cudaStream_t st);
+cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, cudaStream_t st);
+cudaError_t launch_record_tiles_dev(const uint8_t* payload, const Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
+                                    cudaStream_t st);
+cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st);
 cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,
                                 cudaStream_t st);
 cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st, bool fuse_y = false);
 cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool carries, cudaStream_t st);
 // inclusive prefix sum along an axis of a [outer][L][W] int32 array (mod 2^32); when
 // dequant_w > 0 the final values are written as fl32(fl32(q) * w) floats in place.
+// wp (device, optional) supplies the bin width instead of dequant_w (device-driven decode).
 cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t W,
-                             uint32_t* sums, float dequant_w, cudaStream_t st);
+                             uint32_t* sums, float dequant_w, cudaStream_t st, const float* wp = nullptr);
 cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint64_t n,
                                cudaStream_t st, uint64_t base = 0);
 cudaError_t launch_axis_sum(const int32_t* v, uint64_t L, uint64_t W, int32_t* agg, cudaStream_t st);
 cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t elems, int32_t* carry,
                               cudaStream_t st);
 cudaError_t launch_zwalk_ycarry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* ycarry, uint32_t nx,
-                               cudaStream_t st);
+                               cudaStream_t st, const float* wp = nullptr);
 cudaError_t launch_walk_carry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* carry,
                               cudaStream_t st);
 cudaError_t launch_add_dequant(int32_t* q, uint64_t n, const int32_t* carry, float w, cudaStream_t st);

@@ -74,6 +74,9 @@ def lib():
         "fz_last_header": ([P], i),
         "fz_decompress_hdr_async": ([P, S, P, P, u64, P, S, P], i),
         "fz_decompress_result": ([P, P], i),
+        "fz_decompress_async": ([P, S, pS, P, P, S, P], i),
+        "fz_compress_async": ([P, pS, i, C.c_double, P, S, P, S, P], i),
+        "fz_compress_result": ([P, S, C.POINTER(S), P], i),
         "fz_compress_host": ([P, pS, i, C.c_double, P, S, C.POINTER(S), P, P, S, P, S, P], i),
         "fz_decompress_host": ([P, S, P, u64, P, P, P, S, P], i),
         "fz_peek_header": ([P, S, C.POINTER(Info)], i),
@@ -87,6 +90,7 @@ def lib():
         "fz_debug_decode_q": ([P, S, P, u64, P, S, P], i),
         "fz_last_launch_count": ([], i),
         "fz_profile_enable": ([i], None),
+        "fz_profile_mask": ([C.c_ulonglong], None),
         "fz_profile_read": ([C.POINTER(C.c_double), C.POINTER(C.c_int), i], i),
         "fz_kernel_name": ([i], C.c_char_p),
         "fz_profile_timeline": ([C.POINTER(C.c_int), C.POINTER(C.c_float), C.POINTER(C.c_float), i], i),
@@ -164,6 +168,15 @@ def profile_timeline(max_records: int = 4096) -> list:
     return [(lib().fz_kernel_name(ids[i]).decode(), a[i], b[i]) for i in range(k)]
 
 
+def profile_only(names):
+    """Record events only for the named kernels (others launch without event records)."""
+    ids = {lib().fz_kernel_name(i).decode(): i for i in range(64) if lib().fz_kernel_name(i) != b"?"}
+    mask = 0
+    for n in names:
+        mask |= 1 << ids[n]
+    lib().fz_profile_mask(mask)
+
+
 def profile_read() -> dict:
     """{kernel name: (total ms, launches)} since the last read (CUDA events per launch)."""
     ms = (C.c_double * 32)()
@@ -194,8 +207,17 @@ class Codec:
         self.hdr = (C.c_uint8 * 128)()   # host copy of the last stream's header
         self.hdr_size = None             # size of the stream it belongs to (None: no header)
 
-    def compress(self, field, mode=REL, eb=1e-3, params: Params | None = None, stream=None):
-        """Returns (uint8 view of the stream, size)."""
+    def compress(self, field, mode=REL, eb=1e-3, params: Params | None = None, stream=None, sync=True):
+        """Returns (uint8 view of the stream, size).  With sync=False the whole compression is
+        only enqueued (fz_compress_async) and (the output buffer, None) is returned; the size
+        comes from compress_result()."""
+        if not sync:
+            assert params is None
+            st = lib().fz_compress_async(_ptr(field), C.byref(self.shape), mode, eb, _ptr(self.out), self.cap,
+                                         _ptr(self.work), self.work.numel(), _stream(stream))
+            _check(st, "fz_compress_async")
+            self.hdr_size = None
+            return self.out, None
         size = C.c_size_t()
         if params is None:
             st = lib().fz_compress(_ptr(field), C.byref(self.shape), mode, eb, _ptr(self.out), self.cap,
@@ -239,7 +261,29 @@ def _codec_result(self, stream=None):
     _check(lib().fz_decompress_result(_ptr(self.dwork), _stream(stream)), "fz_decompress_result")
 
 
+def _codec_compress_result(self, stream=None) -> int:
+    """Waits for an asynchronous compress; returns the stream size."""
+    size = C.c_size_t()
+    _check(lib().fz_compress_result(_ptr(self.work), self.cap, C.byref(size), _stream(stream)),
+           "fz_compress_result")
+    return size.value
+
+
+def _codec_decompress_device(self, buf, out=None, stream=None):
+    """Fully device-driven asynchronous decompress (fz_decompress_async): the header is parsed
+    on the device, nothing waits for the host; call result() before using `out`."""
+    import torch
+    if out is None:
+        out = torch.empty(self.dims, dtype=torch.float32, device=self.device)
+    st = lib().fz_decompress_async(_ptr(buf), buf.numel(), C.byref(self.shape), _ptr(out), _ptr(self.dwork),
+                                   self.dwork.numel(), _stream(stream))
+    _check(st, "fz_decompress_async")
+    return out
+
+
 Codec.result = _codec_result
+Codec.compress_result = _codec_compress_result
+Codec.decompress_device = _codec_decompress_device
 
 
 def compress(field, mode=REL, eb=1e-3, params: Params | None = None, stream=None):

@@ -321,3 +321,57 @@ def test_generic_vector_kernel_parity(monkeypatch):
     for d in (synth.generate("nyx_v", (24, 40, 64)), synth.generate("cesm_t", (90, 256)),
               synth.adversarial("spike", 30000)):
         _check_full(d, O.REL, 1e-3, f"generic{d.shape}")
+
+
+ASYNC_SHAPES = [
+    ("plane", lambda: synth.generate("nyx_v", (296, 8, 512))),         # k_decode_planes
+    ("tiles3d", lambda: synth.generate("hurr_u", (20, 50, 52))),       # k_decode_tiles + walks
+    ("ragged3d", lambda: synth.generate("sines3d", (33, 47, 61))),     # generic compressor (nx % 4)
+    ("cesm2d", lambda: synth.generate("cesm_t", (180, 360))),          # chunked y scan
+    ("wide2d", lambda: synth.generate("cesm_t", (7, 5000))),
+    ("noise1d", lambda: synth.adversarial("noise", 10007)),            # x carries + 1-D dequant
+    ("spike1d", lambda: synth.adversarial("spike", 50000)),            # delta outliers
+    ("offset1d", lambda: synth.adversarial("offset", 30000)),          # staging overflow (reported)
+    ("vout1d", lambda: synth.adversarial("offset", 1000)),             # value outliers below the cap
+]
+
+
+@pytest.mark.parametrize("name,gen", ASYNC_SHAPES, ids=[a[0] for a in ASYNC_SHAPES])
+def test_async_pipeline_parity(name, gen):
+    """fz_compress_async + fz_decompress_async (no host round trip, header parsed on the
+    device): byte-identical stream and bit-identical field vs the oracle."""
+    d = gen()
+    mode, eb = (O.REL, 1e-6) if name in ("offset1d", "vout1d") else ((O.ABS, 1e-3) if name == "spike1d" else (O.REL, 1e-3))
+    st, ref = O.compress(d, mode, eb)
+    assert st == O.OK
+    codec = fz.Codec(d.shape, DEV)
+    buf, _ = codec.compress(torch.from_numpy(np.ascontiguousarray(d)).to(DEV), mode, eb, sync=False)
+    if name == "offset1d":
+        # more value outliers than the staging area holds: the asynchronous path cannot run the
+        # rescan pass and says so (the synchronous fz_compress handles it)
+        with pytest.raises(fz.FZError) as e:
+            codec.compress_result()
+        assert e.value.status == fz.ERR_WORKSPACE
+        return
+    xh = codec.decompress_device(buf)
+    size = codec.compress_result()
+    codec.result()
+    _assert_stream_equal(buf[:size].cpu().numpy(), ref, name)
+    st, xref = O.decompress(ref, d.size)
+    assert np.array_equal(xh.cpu().numpy().reshape(-1).view(np.uint32), xref.view(np.uint32))
+
+
+def test_async_decompress_rejects_bad_headers():
+    d = synth.generate("nyx_v", (24, 30, 32))
+    codec = fz.Codec(d.shape, DEV)
+    buf, size = codec.compress(torch.from_numpy(d).to(DEV), fz.REL, 1e-3)
+    good = buf.clone()
+    for off, val in ((0, 0x00), (40, 0x07), (88, 0x7F), (67, 0x80)):   # magic, N, nnz, sign of w
+        bad = good.clone()
+        bad[off] = val if bad[off].item() != val else (val ^ 1)
+        codec.decompress_device(bad)
+        with pytest.raises(fz.FZError) as e:
+            codec.result()
+        assert e.value.status == fz.ERR_CORRUPT
+    codec.decompress_device(good)
+    codec.result()
