@@ -69,8 +69,13 @@ def run(args, wl, metric):
         launches[0] += fz.last_launch_count()
         return total
 
+    # warm-up mirrors the timed loop (barriers included: the first NCCL barrier is expensive)
     for _ in range(max(3, args.warmup)):
+        tdist.barrier()
+        torch.cuda.synchronize()
         total = step()
+        torch.cuda.synchronize()
+        tdist.barrier()
     torch.cuda.synchronize()
     times = []
     launches[0] = 0
@@ -84,6 +89,8 @@ def run(args, wl, metric):
         torch.cuda.synchronize()
         tdist.barrier()
         times.append(e0.elapsed_time(e1))
+    if os.environ.get("FZ_DIST_DEBUG"):
+        print(f"rank {rank} step ms {[round(x, 3) for x in times]}", flush=True)
     t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
@@ -119,7 +126,10 @@ def run(args, wl, metric):
         return total
 
     for _ in range(max(3, args.warmup)):
+        tdist.barrier()
         step_e2e()
+        torch.cuda.synchronize()
+    tdist.barrier()
     torch.cuda.synchronize()
     etimes = []
     for _ in range(args.steps):

@@ -132,7 +132,15 @@ struct Work {
     uint2* opre() const { return reinterpret_cast<uint2*>(base + L.opre); }
     uint2* dstage() const { return reinterpret_cast<uint2*>(base + L.dstage); }
     uint2* vstage() const { return reinterpret_cast<uint2*>(base + L.vstage); }
+    uint4* tstage() const { return L.tstage ? reinterpret_cast<uint4*>(base + L.tstage) : nullptr; }
+    uint32_t* zloc() const { return reinterpret_cast<uint32_t*>(base + L.zloc); }
+    uint32_t* zbsum() const { return reinterpret_cast<uint32_t*>(base + L.zbsum); }
 };
+
+bool zb_layout(const fz_shape& s)
+{
+    return s.ndim == 3 && zb_shape(3, s.dims[1], s.dims[2], s.dims[0]);
+}
 
 CompressArgs make_args(const Work& W, const float* field, uint64_t base, const Geom& g,
                        uint32_t tb, uint32_t te)
@@ -152,6 +160,7 @@ CompressArgs make_args(const Work& W, const float* field, uint64_t base, const G
     a.obase = W.obase();
     a.opre = W.opre();
     a.ctrl = W.ctrl();
+    a.tstage = W.tstage();
     return a;
 }
 
@@ -189,6 +198,24 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
     const uint32_t tb = a.tile_begin, nt = a.tile_end - a.tile_begin;
     // status words are per scan unit, indexed from the range start; outlier counts per tile
     FZ_CUDA(launch_init(W.ctrl(), W.status(), W.ocnt() + tb, nt, hp, st));
+    if (compress_uses_zb(a)) {
+        // z-band two-pass compressor: pass 1 derives the parameters in its prologue, writes
+        // the flags and stages each tile's blocks; the popcount scan of the flags gives the
+        // offsets, k_compact moves the blocks, k_finalize writes totals + header
+        if (hp == nullptr) FZ_CUDA(launch_range(a.field, n, W.ctrl(), st));
+        CompressArgs b = a;
+        b.derive = hp == nullptr;
+        b.eb_mode = mode;
+        b.eb = eb;
+        b.n_hdr = n;
+        FZ_CUDA(launch_compress_zb(b, st));
+        const uint32_t T = a.tile_end - a.tile_begin;
+        FZ_CUDA(launch_tile_offsets(a.flags_out, T, W.zloc(), W.zbsum(), W.ctrl(), st, ~1ull));
+        FZ_CUDA(launch_compact(a.flags_out, W.zloc(), W.zbsum(), W.tstage(), a.payload_out, a.payload_cap, T, st));
+        FZ_CUDA(launch_finalize(hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
+        if (h == nullptr) return FZ_OK;
+        return read_ctrl(W, h, st);
+    }
     // the warp-specialized kernel derives the parameters in its prologue and its last CTA
     // writes totals + header, so k_params and k_finalize are not launched for it
     const bool fused = compress_uses_ws(a);
@@ -278,7 +305,7 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     if (hp == nullptr && (!(eb > 0.0) || !std::isfinite(eb) || (mode != FZ_EB_ABS && mode != FZ_EB_REL)))
         return FZ_ERR_ARG;
     const uint64_t T = tiles_of(n);
-    Work W{compress_layout(n, T), static_cast<uint8_t*>(d_work)};
+    Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
     if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
     const Geom g = geom_of(*s, n);
     uint8_t* out = static_cast<uint8_t*>(d_out);
@@ -323,7 +350,7 @@ size_t fz_workspace_bytes(const fz_shape* s)
 {
     uint64_t n;
     if (!shape_n(s, &n)) return 0;
-    return compress_layout(n, tiles_of(n)).total;
+    return compress_layout(n, tiles_of(n), zb_layout(*s)).total;
 }
 
 size_t fz_decompress_workspace_bytes(const fz_shape* s)
@@ -566,7 +593,7 @@ fz_status fz_compress_async(const float* d_field, const fz_shape* s, int eb_mode
         return FZ_ERR_ARG;
     if (!(eb > 0.0) || !std::isfinite(eb) || (eb_mode != FZ_EB_ABS && eb_mode != FZ_EB_REL)) return FZ_ERR_ARG;
     const uint64_t T = tiles_of(n);
-    Work W{compress_layout(n, T), static_cast<uint8_t*>(d_work)};
+    Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
     if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const Geom g = geom_of(*s, n);
@@ -758,7 +785,7 @@ const char* fz_kernel_name(int id)
                                   "k_decode_init", "k_validate_outliers", "k_decode_tiles",
                                   "k_scan_sums", "k_scan_chunks", "k_scan_apply", "k_value_patch",
                                   "k_outliers", "k_tile_offsets", "k_xcarry", "k_slab", "k_decode_planes",
-                                  "k_scan_walk"};
+                                  "k_scan_walk", "k_compact"};
     return (id >= 0 && id < fz::K_COUNT) ? names[id] : "?";
 }
 
@@ -885,7 +912,7 @@ fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_pa
         h_nv == nullptr || !aligned16(d_field) || !aligned16(d_work))
         return FZ_ERR_ARG;
     const uint64_t T = tiles_of(n);
-    Work W{compress_layout(n, T), static_cast<uint8_t*>(d_work)};
+    Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
     if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CompressArgs a = make_args(W, d_field, 0, geom_of(*s, n), 0, (uint32_t)T);

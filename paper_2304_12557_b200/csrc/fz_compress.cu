@@ -1433,6 +1433,361 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
 }
 
 // ------------------------------------------------------------------------------------
+// z-band compression, pass 1 (3-D fields with whole tiles per plane, P % 2048 == 0).
+// A work item is a column of tiles: tile position p of the planes [z0, z0 + Zc).  The CTA
+// walks it plane by plane, so the previous plane's quantized values are still in its shared
+// ring from the step before (the two rings swap roles every step) -- no re-quantization of
+// the previous plane, no previous-plane TMA.  Only the row halo (the nx+1 elements before the
+// tile, from the neighbouring tile of the same plane) is quantized again, from the TMA
+// stage.  Each tile's flags go straight to the stream; its nonzero blocks go to a staging
+// slot of 256 blocks (pass 2, k_compact, moves them to their final offsets), so no ordering
+// between CTAs is needed: no look-back, no scanner warp, any work order.
+// ------------------------------------------------------------------------------------
+constexpr int kZbChunk = 16;       // planes per work item
+
+struct ZbShared {
+    uint64_t mbar;
+    uint32_t tma_bits;             // bit0 own tile, bit1 own row halo staged by TMA
+    uint32_t item;
+    uint32_t F[8];
+    uint32_t cd[8], cv[8];
+    unsigned long long ob[2];
+    QuantP P;
+    fz_params p;
+    int perr;
+};
+
+__device__ __forceinline__ void zb_issue(const CompressArgs& a, ZbShared& sh, float* inbuf, uint32_t t)
+{
+    const int64_t s = (int64_t)t * kTileCodes, base = (int64_t)a.base;
+    const int64_t hw = (int64_t)a.hwords;
+    const bool full = s + kTileCodes <= (int64_t)a.g.n;
+    uint32_t bits = 0, bytes = 0;
+    if (full && s >= base) { bits |= 1; bytes += kTileCodes * 4; }
+    if (hw > 0 && s - hw >= base) { bits |= 2; bytes += (uint32_t)hw * 4; }
+    sh.tma_bits = bits;
+    if (bytes) {
+        mbar_expect_tx(&sh.mbar, bytes);
+        if (bits & 1) tma_load_1d(inbuf, a.field + (s - base), kTileCodes * 4, &sh.mbar);
+        if (bits & 2) tma_load_1d(inbuf + kTileCodes, a.field + (s - hw - base), (uint32_t)hw * 4, &sh.mbar);
+    }
+}
+
+// Quantize the hw floats staged in shared memory (field elements [g_lo, g_lo + hw)) into ring
+// `ro` (positions & rmask); warp-uniform trip count (pq_many votes across the warp).
+__device__ __forceinline__ void zb_fill_halo(const QuantP& P, int* smem, int ro, uint32_t rmask, const float* src,
+                                             int64_t g_lo, int hw)
+{
+    for (int b0 = 0; b0 < hw; b0 += 8 * kCta) {
+        const int c0 = b0 + 8 * (int)threadIdx.x;
+        float v[8];
+        int q[8];
+        float4 x = make_float4(0, 0, 0, 0), y = make_float4(0, 0, 0, 0);
+        if (c0 < hw) x = *reinterpret_cast<const float4*>(src + c0);
+        if (c0 + 4 < hw) y = *reinterpret_cast<const float4*>(src + c0 + 4);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+        pq_many<8>(v, q, P);
+        const uint32_t g = (uint32_t)(g_lo + c0);
+        if (c0 < hw) *reinterpret_cast<int4*>(smem + ro + (g & rmask)) = make_int4(q[0], q[1], q[2], q[3]);
+        if (c0 + 4 < hw) *reinterpret_cast<int4*>(smem + ro + ((g + 4) & rmask)) = make_int4(q[4], q[5], q[6], q[7]);
+    }
+}
+
+// Front half of a z-band step: own tile (+ halo) quantized into ring ra; the previous plane is
+// already in ring rb (or, at a chunk start, quantized into it here); Lorenzo residuals.
+template <class OnFree>
+__device__ __forceinline__ void front_zb(const CompressArgs& a, const QuantP& P, int* smem, uint32_t rmask, int ra,
+                                         int rb, uint32_t t, bool bstart, const float* in_own, const float* in_halo,
+                                         uint32_t x0, uint32_t p0, int32_t (&dl)[8], uint32_t& vmask, float (&dv)[8],
+                                         uint32_t& vm, OnFree&& on_input_free)
+{
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t n = a.g.n, nx = a.g.nx, PL = a.g.P;
+    const int64_t s = (int64_t)t * kTileCodes;
+    const uint32_t g0 = (uint32_t)s + 8u * tid;
+    const int64_t H = (int64_t)nx + 1;
+    const bool full = s + kTileCodes <= (int64_t)n;
+    if (in_own) {
+        const float4 x = *reinterpret_cast<const float4*>(in_own + 8 * tid);
+        const float4 y = *reinterpret_cast<const float4*>(in_own + 8 * tid + 4);
+        dv[0] = x.x; dv[1] = x.y; dv[2] = x.z; dv[3] = x.w; dv[4] = y.x; dv[5] = y.y; dv[6] = y.z; dv[7] = y.w;
+    } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dv[u] = load1(a, (int64_t)g0 + u);
+    }
+    if (in_halo) zb_fill_halo(P, smem, ra, rmask, in_halo, s - (int64_t)a.hwords, (int)a.hwords);
+    else fill_ring(a, P, smem, ra, rmask, (s - H) & ~(int64_t)3, s);
+    if (bstart)   // first step of a chunk: the previous plane's tile and halo, once
+        fill_ring(a, P, smem, rb, rmask, (s - (int64_t)PL - H) & ~(int64_t)3, s - (int64_t)PL + kTileCodes);
+    int qo[8];
+    pq_own(dv, qo, vmask, P);
+    *reinterpret_cast<int4*>(smem + ra + (g0 & rmask)) = make_int4(qo[0], qo[1], qo[2], qo[3]);
+    *reinterpret_cast<int4*>(smem + ra + ((g0 + 4) & rmask)) = make_int4(qo[4], qo[5], qo[6], qo[7]);
+    vm = 0xFFu;
+    if (!full) vm = (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
+    bar_sync(kBarCompute, kCta);
+    on_input_free();   // every thread has read the TMA stage
+
+    uint32_t xm, ym, zm;
+    bool fast_yz;
+    lorenzo_masks_xp<3>(a, g0, x0, p0, xm, ym, zm, fast_yz);
+    uint32_t S[9];
+    if (fast_yz) {
+        uint32_t y[8], z[8], yz[8];
+        {
+            const int4 p = *reinterpret_cast<const int4*>(smem + ra + ((g0 - nx) & rmask));
+            const int4 q = *reinterpret_cast<const int4*>(smem + ra + ((g0 - nx + 4) & rmask));
+            y[0] = p.x; y[1] = p.y; y[2] = p.z; y[3] = p.w; y[4] = q.x; y[5] = q.y; y[6] = q.z; y[7] = q.w;
+        }
+        {
+            const uint32_t gb = g0 - PL;
+            const int4 p = *reinterpret_cast<const int4*>(smem + rb + (gb & rmask));
+            const int4 q = *reinterpret_cast<const int4*>(smem + rb + ((gb + 4) & rmask));
+            z[0] = p.x; z[1] = p.y; z[2] = p.z; z[3] = p.w; z[4] = q.x; z[5] = q.y; z[6] = q.z; z[7] = q.w;
+        }
+        {
+            const uint32_t gb = g0 - PL - nx;
+            const int4 p = *reinterpret_cast<const int4*>(smem + rb + (gb & rmask));
+            const int4 q = *reinterpret_cast<const int4*>(smem + rb + ((gb + 4) & rmask));
+            yz[0] = p.x; yz[1] = p.y; yz[2] = p.z; yz[3] = p.w; yz[4] = q.x; yz[5] = q.y; yz[6] = q.z; yz[7] = q.w;
+        }
+#pragma unroll
+        for (int j = 1; j < 9; ++j) S[j] = ((uint32_t)qo[j - 1] - y[j - 1]) - (z[j - 1] - yz[j - 1]);
+    } else {
+#pragma unroll
+        for (int j = 1; j < 9; ++j) {
+            const uint32_t pos = g0 + j - 1;
+            const int e = j - 1;
+            const uint32_t Y = (ym >> e) & 1u ? 0xFFFFFFFFu : 0u;
+            const uint32_t Z = (zm >> e) & 1u ? 0xFFFFFFFFu : 0u;
+            const uint32_t qy = (uint32_t)smem[ra + ((pos - nx) & rmask)];
+            uint32_t v = (uint32_t)qo[e] - (qy & Y);
+            const uint32_t qzz = (uint32_t)smem[rb + ((pos - PL) & rmask)];
+            const uint32_t qyz = (uint32_t)smem[rb + ((pos - PL - nx) & rmask)];
+            v -= (qzz - (qyz & Y)) & Z;
+            S[j] = v;
+        }
+    }
+    S[0] = __shfl_up_sync(kFull, S[8], 1);
+    if (lane == 0 || !fast_yz) {
+        const uint32_t pos = g0 - 1;
+        uint32_t v = (uint32_t)smem[ra + (pos & rmask)];
+        if (fast_yz) {
+            v -= (uint32_t)smem[ra + ((pos - nx) & rmask)];
+            v -= (uint32_t)smem[rb + ((pos - PL) & rmask)] - (uint32_t)smem[rb + ((pos - PL - nx) & rmask)];
+        } else {
+            const uint32_t Y = (ym & 1u) ? 0xFFFFFFFFu : 0u;
+            const uint32_t Z = (zm & 1u) ? 0xFFFFFFFFu : 0u;
+            v -= (uint32_t)smem[ra + ((pos - nx) & rmask)] & Y;
+            v -= ((uint32_t)smem[rb + ((pos - PL) & rmask)] - ((uint32_t)smem[rb + ((pos - PL - nx) & rmask)] & Y)) & Z;
+        }
+        S[0] = v;
+    }
+    residuals(S, xm, dl);
+}
+
+// Tail of a z-band step: codes, bitshuffle, outliers, flags to the stream, nonzero blocks
+// to the tile's staging slot.
+__device__ __forceinline__ void tail_zb(const CompressArgs& a, ZbShared& sh, uint32_t* Obuf, uint32_t t, uint32_t g0,
+                                        uint32_t vm, const int32_t (&dl)[8], uint32_t vmask, const float (&dv)[8])
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Ctrl* ctrl = a.ctrl;
+    const uint32_t n = a.g.n;
+    uint32_t code[8];
+    uint32_t magor = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const uint32_t mag = (uint32_t)abs(dl[e]);
+        code[e] = (((uint32_t)dl[e] >> 16) & 0x8000u) | mag;
+        magor |= mag;
+    }
+    uint32_t dmask = 0;
+    if (magor > 32767u) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if ((uint32_t)abs(dl[e]) > 32767u) { dmask |= 1u << e; code[e] = 0u; }
+    }
+    if (vm != 0xFFu) {
+        dmask &= vm;
+        vmask &= vm;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (!((vm >> e) & 1u)) code[e] = 0u;
+    }
+    if (a.codes_out != nullptr) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (g0 + e < n) a.codes_out[g0 + e] = (uint16_t)code[e];
+    }
+    {
+        uint32_t w4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w4[i] = __byte_perm(code[2 * i], code[2 * i + 1], 0x5410);
+        transpose32_group8(w4, lane & 7);
+        const int c = tid >> 3, kk = tid & 7;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Obuf[(4 * kk + i) * 33 + c] = w4[i];
+    }
+    const int any_out = bar_or(kBarCompute, kCta, (dmask | vmask) != 0);
+    if (any_out) {
+        const int cd = __popc(dmask), cv = __popc(vmask);
+        const int wd = __reduce_add_sync(kFull, cd), wv = __reduce_add_sync(kFull, cv);
+        if (lane == 0) { sh.cd[warp] = wd; sh.cv[warp] = wv; }
+        bar_sync(kBarCompute, kCta);
+        uint32_t tnd = 0, tnv = 0, wpre_d = 0, wpre_v = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            tnd += sh.cd[w]; tnv += sh.cv[w];
+            if (w < warp) { wpre_d += sh.cd[w]; wpre_v += sh.cv[w]; }
+        }
+        if (tid == 0) {
+            sh.ob[0] = tnd ? atomicAdd(&ctrl->dcount, (unsigned long long)tnd) : 0ull;
+            sh.ob[1] = tnv ? atomicAdd(&ctrl->vcount, (unsigned long long)tnv) : 0ull;
+            a.ocnt[t] = make_uint2(tnd, tnv);
+            a.obase[t] = make_uint2((uint32_t)sh.ob[0], (uint32_t)sh.ob[1]);
+        }
+        int id = cd, iv = cv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yd = __shfl_up_sync(kFull, id, o), yv = __shfl_up_sync(kFull, iv, o);
+            if (lane >= o) { id += yd; iv += yv; }
+        }
+        bar_sync(kBarCompute, kCta);
+        uint64_t pd = sh.ob[0] + wpre_d + (id - cd), pv = sh.ob[1] + wpre_v + (iv - cv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint32_t gi = g0 + e;
+            if (dmask & (1u << e)) {
+                if (pd < a.dcap) a.dstage[pd] = make_uint2(gi, (uint32_t)dl[e]);
+                else atomicOr(&ctrl->stage_overflow, 1u);
+                ++pd;
+            }
+            if (vmask & (1u << e)) {
+                if (pv < a.vcap) a.vstage[pv] = make_uint2(gi, __float_as_uint(dv[e]));
+                else atomicOr(&ctrl->stage_overflow, 1u);
+                ++pv;
+            }
+        }
+        bar_sync(kBarCompute, kCta);
+    }
+    const uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
+    const uint4 blk = make_uint4(row[0], row[1], row[2], row[3]);
+    const bool nz = (blk.x | blk.y | blk.z | blk.w) != 0;
+    const uint32_t F = __ballot_sync(kFull, nz);
+    if (lane == 0) sh.F[warp] = F;
+    bar_sync(kBarCompute, kCta);
+    const uint32_t fw = lane < 8 ? sh.F[lane] : 0u;
+    const uint32_t pc = __popc(fw);
+    const uint32_t wpre = __reduce_add_sync(kFull, lane < warp ? pc : 0u);
+    if (tid < 8) {
+        const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * tid;
+        if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = fw;
+    }
+    if (nz) a.tstage[(uint64_t)t * kTileBlocks + wpre + __popc(F & ((1u << lane) - 1u))] = blk;
+}
+
+__global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
+{
+    extern __shared__ __align__(16) int smem[];
+    __shared__ ZbShared sh;
+    const int tid = threadIdx.x;
+    Ctrl* ctrl = a.ctrl;
+    if (ctrl->err != 0) return;
+    const uint32_t rmask = a.qstride - 1;
+    const int RB = (int)a.qstride;
+    uint32_t* Obuf = reinterpret_cast<uint32_t*>(smem + a.qwords);              // 32 x 33
+    float* inbuf = reinterpret_cast<float*>(smem + a.qwords + 32 * 33 + 4);    // own tile + row halo
+    const uint32_t tpp = a.g.P / kTileCodes, nz = a.g.n / a.g.P;
+    const uint32_t nchunks = (nz + kZbChunk - 1) / kZbChunk, nwork = tpp * nchunks;
+    if (tid == 0) {
+        sh.perr = 0;
+        if (a.derive) {
+            fz_params p;
+            const int st = params_from_range(ctrl, a.eb_mode, a.eb, a.n_hdr, &p);
+            sh.perr = st;
+            if (st == FZ_OK) {
+                float h, hU;
+                quant_consts(p, h, hU);
+                sh.p = p;
+                sh.P = QuantP{p.w, p.r, h, p.eb32, hU};
+                if (blockIdx.x == 0) { ctrl->p = p; ctrl->h = h; ctrl->hU = hU; }
+            } else if (blockIdx.x == 0) {
+                ctrl->err = st;
+            }
+        } else {
+            sh.P = QuantP{ctrl->p.w, ctrl->p.r, ctrl->h, ctrl->p.eb32, ctrl->hU};
+        }
+        mbar_init(&sh.mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sh.tma_bits = 0;
+    }
+    __syncthreads();
+    if (sh.perr != 0) return;
+    const QuantP P = sh.P;
+    uint32_t phase = 0;
+    for (;;) {
+        if (tid == 0) sh.item = atomicAdd(&ctrl->ticket, 1u);
+        __syncthreads();
+        const uint32_t w = sh.item;
+        if (w >= nwork) break;
+        const uint32_t c = w / tpp, p = w - c * tpp;
+        const uint32_t z0 = c * kZbChunk, z1 = min(nz, z0 + kZbChunk);
+        // the thread's in-row / in-plane positions are the same in every plane of the column
+        const uint32_t pp = p * kTileCodes + 8u * tid;
+        const uint32_t x0 = fmod_(pp, a.dnx), p0 = pp;
+        if (tid == 0) zb_issue(a, sh, inbuf, z0 * tpp + p);
+        int ra = 0, rb = RB;
+        for (uint32_t z = z0; z < z1; ++z) {
+            const uint32_t t = z * tpp + p;
+            __syncthreads();                      // sh.tma_bits written by thread 0
+            const uint32_t bits = sh.tma_bits;
+            if (bits) {
+                while (!mbar_try_wait(&sh.mbar, phase)) {
+                }
+                phase ^= 1u;
+            }
+            int32_t dl[8];
+            uint32_t vmask, vm;
+            float dv[8];
+            auto issue_next = [&]() {
+                if (tid == 0) {
+                    if (z + 1 < z1) zb_issue(a, sh, inbuf, t + tpp);
+                    else sh.tma_bits = 0;
+                }
+            };
+            front_zb(a, P, smem, rmask, ra, rb, t, z == z0 && z > 0, (bits & 1) ? inbuf : nullptr,
+                     (bits & 2) ? inbuf + kTileCodes : nullptr, x0, p0, dl, vmask, dv, vm, issue_next);
+            tail_zb(a, sh, Obuf, t, (uint32_t)t * kTileCodes + 8u * tid, vm, dl, vmask, dv);
+            const int tmp = ra;
+            ra = rb;
+            rb = tmp;
+        }
+    }
+}
+
+// Pass 2: each tile's staged blocks to their final offsets (exclusive scan of the flag
+// popcounts by k_nnz_block/k_nnz_top).  One warp per tile.
+__global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ loc,
+                                                 const uint32_t* __restrict__ bpre, const uint4* __restrict__ tstage,
+                                                 uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles)
+{
+    const int lane = threadIdx.x & 31;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t t = wid; t < ntiles; t += nw) {
+        const uint32_t fw = lane < 8 ? __ldg(flags + 8 * (uint64_t)t + lane) : 0u;
+        const uint32_t cnt = __reduce_add_sync(kFull, __popc(fw));
+        const uint64_t off = (uint64_t)__ldg(bpre + (t >> 10)) + __ldg(loc + t);
+        const uint4* src = tstage + (uint64_t)t * kTileBlocks;
+        for (uint32_t i = lane; i < cnt; i += 32) {
+            const uint64_t bo = 16 * (off + i);
+            if (bo + 16 <= payload_cap) __stcs(reinterpret_cast<uint4*>(payload_out + bo), __ldcs(src + i));
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // C9: header (outlier sections are placed by k_outlier_place when there are any).
 // ------------------------------------------------------------------------------------
 // C9 totals and header (one thread): k_finalize, or the last CTA of the ws kernel.
@@ -1637,6 +1992,58 @@ static cudaError_t launch_compress_ws(const CompressArgs& a, size_t sm, uint32_t
     if (grid > nunits) grid = nunits;
     if (grid == 0) return cudaSuccess;
     k_compress_ws<NDIM><<<(unsigned)grid, kWsThreads, sm, st>>>(a);
+    return cudaGetLastError();
+}
+
+// z-band two-pass compression applies to 3-D fields with whole tiles per plane on the vector
+// path (FZ_EXP bit 1024 turns it off for A/B timing).
+bool compress_uses_zb(const CompressArgs& a_in)
+{
+    CompressArgs a = a_in;
+    if (const char* e = getenv("FZ_EXP")) a.exp = atoi(e);
+    if (a.g.ndim != 3 || (a.exp & (16 | 1024)) || a.rescan || a.tstage == nullptr) return false;
+    if (a.g.P % kTileCodes != 0 || a.base != 0 || a.tile_begin != 0) return false;
+    if (a.g.n / a.g.P < 2) return false;
+    bool vec = false;
+    plan_smem(a, vec);
+    return vec;
+}
+
+cudaError_t launch_compress_zb(const CompressArgs& a_in, cudaStream_t st)
+{
+    CompressArgs a = a_in;
+    a.dnx = make_fastdiv(a.g.nx);
+    a.dP = make_fastdiv(a.g.P);
+    a.sx = a.g.nx ? (uint32_t)(kTileCodes % a.g.nx) : 0u;
+    a.sp = a.g.P ? (uint32_t)(kTileCodes % a.g.P) : 0u;
+    bool vec = false;
+    plan_smem(a, vec);
+    const uint32_t H = a.g.nx + 1;
+    const uint32_t hw = (H + 3) & ~3u;
+    a.hwords = hw * 4 <= 8192 ? hw : 0;
+    const size_t sm = sizeof(int) * ((size_t)a.qwords + 32 * 33 + 4) + sizeof(float) * (kTileCodes + (size_t)a.hwords);
+    cudaFuncSetAttribute(k_compress_zb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compress_zb, kCta, sm);
+    if (per_sm < 1) per_sm = 1;
+    const uint32_t tpp = a.g.P / kTileCodes, nz = a.g.n / a.g.P;
+    const uint64_t nwork = (uint64_t)tpp * ((nz + kZbChunk - 1) / kZbChunk);
+    uint64_t grid = (uint64_t)per_sm * num_sms();
+    if (grid > nwork) grid = nwork;
+    LaunchProf lp(K_COMPRESS, st);
+    k_compress_zb<<<(unsigned)grid, kCta, sm, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const uint8_t* flags, const uint32_t* loc, const uint32_t* bpre, const uint4* tstage,
+                           uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles, cudaStream_t st)
+{
+    LaunchProf lp(K_COMPACT, st);
+    unsigned grid = (unsigned)((ntiles + 7) / 8);
+    if (grid > (unsigned)num_sms() * 16) grid = num_sms() * 16;
+    if (grid < 1) grid = 1;
+    k_compact<<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(flags), loc, bpre, tstage, payload_out,
+                                    payload_cap, ntiles);
     return cudaGetLastError();
 }
 

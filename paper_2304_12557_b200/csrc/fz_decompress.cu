@@ -285,8 +285,12 @@ __global__ void __launch_bounds__(1024) k_nnz_top(uint32_t* bsum, uint32_t nb, C
     }
     if (threadIdx.x == 0) {
         ctrl->nnz = carry;
-        const uint64_t want = expect_nnz == ~0ull ? ctrl->dec_nnz : expect_nnz;
-        if (carry != want) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_CORRUPT);   // popcount(flags) != nnz
+        // expect_nnz: the header's nnz, ~0 = the device-parsed one, ~1 = no check (the z-band
+        // compressor uses this scan to produce nnz)
+        if (expect_nnz != ~1ull) {
+            const uint64_t want = expect_nnz == ~0ull ? ctrl->dec_nnz : expect_nnz;
+            if (carry != want) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_CORRUPT);   // popcount(flags) != nnz
+        }
     }
 }
 

@@ -47,11 +47,13 @@ static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 //   ocnt   : per-tile (n_delta, n_value); obase: staging offsets of the tile's records;
 //   opre   : per-tile exclusive outlier offsets (filled only when outliers exist)
 struct Layout {
-    size_t ctrl, status, ocnt, obase, opre, dstage, vstage, total;
+    size_t ctrl, status, ocnt, obase, opre, dstage, vstage, tstage, zloc, zbsum, total;
     uint64_t dcap, vcap;             // staging capacities in records
 };
 
-inline Layout compress_layout(uint64_t n, uint64_t tiles)
+// zb: room for the z-band two-pass compressor (a 4 KB staging slot per tile + the offsets
+// of its compaction pass).
+inline Layout compress_layout(uint64_t n, uint64_t tiles, bool zb = false)
 {
     Layout L{};
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -65,8 +67,20 @@ inline Layout compress_layout(uint64_t n, uint64_t tiles)
     L.vcap = n / 64 + 1024;
     L.dstage = off; off = al(off + 8 * L.dcap);
     L.vstage = off; off = al(off + 8 * L.vcap);
+    L.tstage = L.zloc = L.zbsum = 0;
+    if (zb) {
+        L.tstage = off; off = al(off + 16 * 256 * tiles);
+        L.zloc = off;   off = al(off + 4 * tiles);
+        L.zbsum = off;  off = al(off + 4 * ((tiles + 1023) / 1024));
+    }
     L.total = off;
     return L;
+}
+
+// 3-D, nx % 4 == 0 and whole tiles per plane: the shapes the z-band compressor may take.
+inline bool zb_shape(uint32_t ndim, uint64_t ny, uint64_t nx, uint64_t nz)
+{
+    return ndim == 3 && nz >= 2 && nx % 4 == 0 && (ny * nx) % 2048 == 0 && nx + 1 + 2048 + 4 <= 8192;
 }
 
 // ------------------------------------------------------------------------------------
@@ -514,6 +528,8 @@ struct CompressArgs {
     uint64_t dims[3];
     uint32_t ndim;
     uint64_t n_hdr, T_hdr;    // field size and tiles for the totals / header
+    uint4* tstage;            // z-band pass 1: 256-block staging slot per tile (null: not available)
+    uint32_t hwords;          // z-band: floats of the TMA-staged row halo (0: quantized from global)
     int exp;                  // FZ_EXP env var, bit 16: generic kernel instead of the warp-specialized one
 };
 

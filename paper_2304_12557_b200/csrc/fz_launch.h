@@ -12,7 +12,8 @@ int num_sms();
 // Kernel kinds for launch accounting and per-kernel CUDA-event timing (fz_profile_*).
 enum KernelId {
     K_INIT = 0, K_RANGE, K_PARAMS, K_COMPRESS, K_FINALIZE, K_DINIT, K_VALIDATE, K_DECODE,
-    K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_SLAB, K_DECODE_PLANES, K_SCAN_WALK, K_COUNT
+    K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_SLAB, K_DECODE_PLANES, K_SCAN_WALK,
+    K_COMPACT, K_COUNT
 };
 
 // Counts one launch of `id` and, when profiling is on, brackets it with CUDA events on the
@@ -32,6 +33,10 @@ cudaError_t launch_range(const float* d, uint64_t n, Ctrl* ctrl, cudaStream_t st
 cudaError_t launch_params(Ctrl* ctrl, int mode, double eb, uint64_t n, cudaStream_t st);
 cudaError_t launch_compress(const CompressArgs& a, cudaStream_t st);
 bool compress_uses_ws(const CompressArgs& a);   // the warp-specialized kernel takes this launch
+bool compress_uses_zb(const CompressArgs& a);   // the z-band two-pass compressor takes it
+cudaError_t launch_compress_zb(const CompressArgs& a, cudaStream_t st);
+cudaError_t launch_compact(const uint8_t* flags, const uint32_t* loc, const uint32_t* bpre, const uint4* tstage,
+                           uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles, cudaStream_t st);
 cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint64_t n,
                             uint64_t T, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st,
