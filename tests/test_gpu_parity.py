@@ -375,3 +375,30 @@ def test_async_decompress_rejects_bad_headers():
         assert e.value.status == fz.ERR_CORRUPT
     codec.decompress_device(good)
     codec.result()
+
+
+# z-band two-pass compressor (3-D, P % 2048 == 0): chunk remainders, the smallest nz, a chunk
+# boundary inside a field with outliers, and equality with the single-kernel path.
+ZB_SHAPES = [
+    ("nz2", lambda: synth.generate("nyx_v", (2, 32, 64))),
+    ("nz17", lambda: synth.generate("sines3d", (17, 16, 128))),     # one full chunk + 1 plane
+    ("nz33_r4", lambda: synth.generate("hurr_u", (33, 8, 512))),
+    ("nz40_tpp3", lambda: synth.generate("rtm", (40, 24, 256))),    # 3 tiles per plane
+]
+
+
+@pytest.mark.parametrize("name,gen", ZB_SHAPES, ids=[z[0] for z in ZB_SHAPES])
+def test_zband_compressor_parity(name, gen):
+    _check_full(gen(), O.REL, 1e-3, name)
+
+
+def test_zband_with_outliers_and_single_kernel_equality(monkeypatch):
+    d = synth.generate("nyx_rho", (36, 16, 256)).copy()
+    eb = float(d.max() - d.min()) * 1e-4
+    rng = np.random.default_rng(5)
+    d.reshape(-1)[rng.choice(d.size, 400, replace=False)] += np.float32(80.0) * np.float32(d.max() - d.min())
+    ref = _check_full(d, O.ABS, eb, "zband_outliers")
+    assert int.from_bytes(ref[96:104].tobytes(), "little") > 0
+    monkeypatch.setenv("FZ_EXP", "1024")            # warp-specialized single kernel instead
+    got, _, _ = _gpu_stream(d, O.ABS, eb)
+    _assert_stream_equal(got, ref, "single_kernel")
