@@ -55,7 +55,9 @@ def ncu_traffic(workload: str, kernel: str):
     try:
         with open(p) as f:
             t = json.load(f)[workload]
-        for k in (kernel, kernel + "_ws"):
+        # the profiler id k_compress covers the z-band pass 1 (k_compress_zb) or the
+        # warp-specialized kernel (k_compress_ws), whichever the shape takes
+        for k in (kernel, kernel + "_zb", kernel + "_ws"):
             if k in t:
                 return t[k]
     except Exception:
