@@ -1479,6 +1479,7 @@ __device__ __forceinline__ void zb_fill_halo(const QuantP& P, int* smem, int ro,
                                              int64_t g_lo, int hw)
 {
     for (int b0 = 0; b0 < hw; b0 += 8 * kCta) {
+        if (b0 + 256 * (int)(threadIdx.x >> 5) >= hw) break;   // warp-uniform: no element left for this warp
         const int c0 = b0 + 8 * (int)threadIdx.x;
         float v[8];
         int q[8];
@@ -1493,20 +1494,25 @@ __device__ __forceinline__ void zb_fill_halo(const QuantP& P, int* smem, int ro,
     }
 }
 
-// Front half of a z-band step: own tile (+ halo) quantized into ring ra; the previous plane is
-// already in ring rb (or, at a chunk start, quantized into it here); Lorenzo residuals.
+// Front half of a z-band step.  The thread's 8 elements sit at the same in-plane positions
+// in every plane of the work item, so the Lorenzo residual is built from the y-difference
+// D(z, e) = q(z, e) - [y>0] q(z, e - nx): S(e) = D(z, e) - [z>0] D(z-1, e) and
+// delta(e) = S(e) - [x>0] S(e-1) (C2).  D(z-1, .) is carried in registers (Dp, and
+// Dp0 for element g0-1 on lane 0), so the previous plane is neither re-quantized nor
+// re-read; only at a chunk start (z0 > 0) is the previous plane's tile (+ row halo)
+// quantized once into ring rb to seed the carry.  Own tile + row halo go to ring ra.
+// xm / ym (x-1 / y-1 neighbour exists, bit e) are per work item.
 template <class OnFree>
 __device__ __forceinline__ void front_zb(const CompressArgs& a, const QuantP& P, int* smem, uint32_t rmask, int ra,
                                          int rb, uint32_t t, bool bstart, const float* in_own, const float* in_halo,
-                                         uint32_t x0, uint32_t p0, int32_t (&dl)[8], uint32_t& vmask, float (&dv)[8],
-                                         uint32_t& vm, OnFree&& on_input_free)
+                                         uint32_t xm, uint32_t ym, uint32_t (&Dp)[8], uint32_t& Dp0,
+                                         int32_t (&dl)[8], uint32_t& vmask, float (&dv)[8], OnFree&& on_input_free)
 {
     const int tid = threadIdx.x, lane = tid & 31;
-    const uint32_t n = a.g.n, nx = a.g.nx, PL = a.g.P;
+    const uint32_t nx = a.g.nx, PL = a.g.P;
     const int64_t s = (int64_t)t * kTileCodes;
     const uint32_t g0 = (uint32_t)s + 8u * tid;
     const int64_t H = (int64_t)nx + 1;
-    const bool full = s + kTileCodes <= (int64_t)n;
     if (in_own) {
         const float4 x = *reinterpret_cast<const float4*>(in_own + 8 * tid);
         const float4 y = *reinterpret_cast<const float4*>(in_own + 8 * tid + 4);
@@ -1523,65 +1529,53 @@ __device__ __forceinline__ void front_zb(const CompressArgs& a, const QuantP& P,
     pq_own(dv, qo, vmask, P);
     *reinterpret_cast<int4*>(smem + ra + (g0 & rmask)) = make_int4(qo[0], qo[1], qo[2], qo[3]);
     *reinterpret_cast<int4*>(smem + ra + ((g0 + 4) & rmask)) = make_int4(qo[4], qo[5], qo[6], qo[7]);
-    vm = 0xFFu;
-    if (!full) vm = (g0 >= n) ? 0u : ((n - g0 >= 8) ? 0xFFu : ((1u << (n - g0)) - 1u));
     bar_sync(kBarCompute, kCta);
     on_input_free();   // every thread has read the TMA stage
 
-    uint32_t xm, ym, zm;
-    bool fast_yz;
-    lorenzo_masks_xp<3>(a, g0, x0, p0, xm, ym, zm, fast_yz);
-    uint32_t S[9];
-    if (fast_yz) {
-        uint32_t y[8], z[8], yz[8];
+    if (bstart) {      // seed the carry with D(z0-1, .)
+        const uint32_t gb = g0 - PL;
+        uint32_t zz[8], zy[8];
         {
-            const int4 p = *reinterpret_cast<const int4*>(smem + ra + ((g0 - nx) & rmask));
-            const int4 q = *reinterpret_cast<const int4*>(smem + ra + ((g0 - nx + 4) & rmask));
-            y[0] = p.x; y[1] = p.y; y[2] = p.z; y[3] = p.w; y[4] = q.x; y[5] = q.y; y[6] = q.z; y[7] = q.w;
-        }
-        {
-            const uint32_t gb = g0 - PL;
             const int4 p = *reinterpret_cast<const int4*>(smem + rb + (gb & rmask));
             const int4 q = *reinterpret_cast<const int4*>(smem + rb + ((gb + 4) & rmask));
-            z[0] = p.x; z[1] = p.y; z[2] = p.z; z[3] = p.w; z[4] = q.x; z[5] = q.y; z[6] = q.z; z[7] = q.w;
+            zz[0] = p.x; zz[1] = p.y; zz[2] = p.z; zz[3] = p.w; zz[4] = q.x; zz[5] = q.y; zz[6] = q.z; zz[7] = q.w;
         }
         {
-            const uint32_t gb = g0 - PL - nx;
-            const int4 p = *reinterpret_cast<const int4*>(smem + rb + (gb & rmask));
-            const int4 q = *reinterpret_cast<const int4*>(smem + rb + ((gb + 4) & rmask));
-            yz[0] = p.x; yz[1] = p.y; yz[2] = p.z; yz[3] = p.w; yz[4] = q.x; yz[5] = q.y; yz[6] = q.z; yz[7] = q.w;
+            const int4 p = *reinterpret_cast<const int4*>(smem + rb + ((gb - nx) & rmask));
+            const int4 q = *reinterpret_cast<const int4*>(smem + rb + ((gb - nx + 4) & rmask));
+            zy[0] = p.x; zy[1] = p.y; zy[2] = p.z; zy[3] = p.w; zy[4] = q.x; zy[5] = q.y; zy[6] = q.z; zy[7] = q.w;
         }
 #pragma unroll
-        for (int j = 1; j < 9; ++j) S[j] = ((uint32_t)qo[j - 1] - y[j - 1]) - (z[j - 1] - yz[j - 1]);
-    } else {
-#pragma unroll
-        for (int j = 1; j < 9; ++j) {
-            const uint32_t pos = g0 + j - 1;
-            const int e = j - 1;
-            const uint32_t Y = (ym >> e) & 1u ? 0xFFFFFFFFu : 0u;
-            const uint32_t Z = (zm >> e) & 1u ? 0xFFFFFFFFu : 0u;
-            const uint32_t qy = (uint32_t)smem[ra + ((pos - nx) & rmask)];
-            uint32_t v = (uint32_t)qo[e] - (qy & Y);
-            const uint32_t qzz = (uint32_t)smem[rb + ((pos - PL) & rmask)];
-            const uint32_t qyz = (uint32_t)smem[rb + ((pos - PL - nx) & rmask)];
-            v -= (qzz - (qyz & Y)) & Z;
-            S[j] = v;
+        for (int e = 0; e < 8; ++e) Dp[e] = zz[e] - (((ym >> e) & 1u) ? zy[e] : 0u);
+        if (lane == 0 && (xm & 1u)) {
+            Dp0 = (uint32_t)smem[rb + ((gb - 1) & rmask)];
+            if (ym & 1u) Dp0 -= (uint32_t)smem[rb + ((gb - 1 - nx) & rmask)];
         }
     }
+    uint32_t y[8];
+    {
+        const int4 p = *reinterpret_cast<const int4*>(smem + ra + ((g0 - nx) & rmask));
+        const int4 q = *reinterpret_cast<const int4*>(smem + ra + ((g0 - nx + 4) & rmask));
+        y[0] = p.x; y[1] = p.y; y[2] = p.z; y[3] = p.w; y[4] = q.x; y[5] = q.y; y[6] = q.z; y[7] = q.w;
+    }
+    if (ym != 0xFFu) {   // first row of the plane among the 8 elements: no y-1 neighbour
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (!((ym >> e) & 1u)) y[e] = 0u;
+    }
+    uint32_t S[9];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const uint32_t D = (uint32_t)qo[e] - y[e];
+        S[e + 1] = D - Dp[e];
+        Dp[e] = D;
+    }
     S[0] = __shfl_up_sync(kFull, S[8], 1);
-    if (lane == 0 || !fast_yz) {
-        const uint32_t pos = g0 - 1;
-        uint32_t v = (uint32_t)smem[ra + (pos & rmask)];
-        if (fast_yz) {
-            v -= (uint32_t)smem[ra + ((pos - nx) & rmask)];
-            v -= (uint32_t)smem[rb + ((pos - PL) & rmask)] - (uint32_t)smem[rb + ((pos - PL - nx) & rmask)];
-        } else {
-            const uint32_t Y = (ym & 1u) ? 0xFFFFFFFFu : 0u;
-            const uint32_t Z = (zm & 1u) ? 0xFFFFFFFFu : 0u;
-            v -= (uint32_t)smem[ra + ((pos - nx) & rmask)] & Y;
-            v -= ((uint32_t)smem[rb + ((pos - PL) & rmask)] - ((uint32_t)smem[rb + ((pos - PL - nx) & rmask)] & Y)) & Z;
-        }
-        S[0] = v;
+    if (lane == 0 && (xm & 1u)) {   // element g0-1 (same row) belongs to the previous warp
+        uint32_t D = (uint32_t)smem[ra + ((g0 - 1) & rmask)];
+        if (ym & 1u) D -= (uint32_t)smem[ra + ((g0 - 1 - nx) & rmask)];
+        S[0] = D - Dp0;
+        Dp0 = D;
     }
     residuals(S, xm, dl);
 }
@@ -1594,36 +1588,38 @@ __device__ __forceinline__ void tail_zb(const CompressArgs& a, ZbShared& sh, uin
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Ctrl* ctrl = a.ctrl;
     const uint32_t n = a.g.n;
-    uint32_t code[8];
+    // C3/C4: two sign-magnitude codes per word, built pairwise: magnitudes by PRMT, both
+    // sign bits (bit 31 of each delta -> bits 15 and 31) by a second PRMT, merged by LOP3.
+    uint32_t w4[4];
     uint32_t magor = 0;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const uint32_t mag = (uint32_t)abs(dl[e]);
-        code[e] = (((uint32_t)dl[e] >> 16) & 0x8000u) | mag;
-        magor |= mag;
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t m0 = (uint32_t)abs(dl[2 * i]), m1 = (uint32_t)abs(dl[2 * i + 1]);
+        magor |= m0 | m1;
+        w4[i] = bitsel(__byte_perm((uint32_t)dl[2 * i], (uint32_t)dl[2 * i + 1], 0x7030u), __byte_perm(m0, m1, 0x5410u),
+                       0x80008000u);
     }
     uint32_t dmask = 0;
-    if (magor > 32767u) {
+    if (magor > 32767u || vm != 0xFFu) {   // delta-outliers (R7) or a partial tile: code 0
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if ((uint32_t)abs(dl[e]) > 32767u) { dmask |= 1u << e; code[e] = 0u; }
-    }
-    if (vm != 0xFFu) {
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int e = 2 * i + h;
+                const bool drop = (uint32_t)abs(dl[e]) > 32767u;
+                if (drop) dmask |= 1u << e;
+                if (drop || !((vm >> e) & 1u)) w4[i] &= h ? 0x0000FFFFu : 0xFFFF0000u;
+            }
+        }
         dmask &= vm;
         vmask &= vm;
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if (!((vm >> e) & 1u)) code[e] = 0u;
     }
     if (a.codes_out != nullptr) {
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-            if (g0 + e < n) a.codes_out[g0 + e] = (uint16_t)code[e];
+            if (g0 + e < n) a.codes_out[g0 + e] = (uint16_t)(w4[e >> 1] >> (16 * (e & 1)));
     }
     {
-        uint32_t w4[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) w4[i] = __byte_perm(code[2 * i], code[2 * i + 1], 0x5410);
         transpose32_group8(w4, lane & 7);
         const int c = tid >> 3, kk = tid & 7;
 #pragma unroll
@@ -1735,9 +1731,14 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
         const uint32_t z0 = c * kZbChunk, z1 = min(nz, z0 + kZbChunk);
         // the thread's in-row / in-plane positions are the same in every plane of the column
         const uint32_t pp = p * kTileCodes + 8u * tid;
-        const uint32_t x0 = fmod_(pp, a.dnx), p0 = pp;
+        uint32_t xm = 0xFFu, ym = 0xFFu;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {   // pp + e < P: no plane wrap inside a thread's 8 elements
+            if (fmod_(pp + e, a.dnx) == 0) xm &= ~(1u << e);
+            if (pp + e < a.g.nx) ym &= ~(1u << e);
+        }
+        uint32_t Dp[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, Dp0 = 0u;
         if (tid == 0) zb_issue(a, sh, inbuf, z0 * tpp + p);
-        int ra = 0, rb = RB;
         for (uint32_t z = z0; z < z1; ++z) {
             const uint32_t t = z * tpp + p;
             __syncthreads();                      // sh.tma_bits written by thread 0
@@ -1748,7 +1749,7 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
                 phase ^= 1u;
             }
             int32_t dl[8];
-            uint32_t vmask, vm;
+            uint32_t vmask;
             float dv[8];
             auto issue_next = [&]() {
                 if (tid == 0) {
@@ -1756,12 +1757,9 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
                     else sh.tma_bits = 0;
                 }
             };
-            front_zb(a, P, smem, rmask, ra, rb, t, z == z0 && z > 0, (bits & 1) ? inbuf : nullptr,
-                     (bits & 2) ? inbuf + kTileCodes : nullptr, x0, p0, dl, vmask, dv, vm, issue_next);
-            tail_zb(a, sh, Obuf, t, (uint32_t)t * kTileCodes + 8u * tid, vm, dl, vmask, dv);
-            const int tmp = ra;
-            ra = rb;
-            rb = tmp;
+            front_zb(a, P, smem, rmask, 0, RB, t, z == z0 && z > 0, (bits & 1) ? inbuf : nullptr,
+                     (bits & 2) ? inbuf + kTileCodes : nullptr, xm, ym, Dp, Dp0, dl, vmask, dv, issue_next);
+            tail_zb(a, sh, Obuf, t, (uint32_t)t * kTileCodes + 8u * tid, 0xFFu, dl, vmask, dv);
         }
     }
 }

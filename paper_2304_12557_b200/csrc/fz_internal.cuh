@@ -343,6 +343,14 @@ __device__ __forceinline__ void xpose_pair(uint32_t& lo, uint32_t& hi, int s, ui
     lo ^= t << s;
 }
 
+// (a & c) | (b & ~c) as one LOP3 (the compiler splits it when c is lane-dependent).
+__device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b, uint32_t c)
+{
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 __device__ __forceinline__ void transpose32_group8(uint32_t (&a)[4], int k)
 {
 #pragma unroll
@@ -359,7 +367,7 @@ __device__ __forceinline__ void transpose32_group8(uint32_t (&a)[4], int k)
             // lower: (a & m) | ((p << s) & ~m); upper: (a & ~m) | ((p >> s) & m).
             // A rotate puts the wanted bits in place; wrapped bits fall in the kept field.
             uint32_t r = __funnelshift_l(p, p, rot);
-            a[i] = (a[i] & keep) | (r & ~keep);
+            a[i] = bitsel(a[i], r, keep);
         }
     }
     xpose_pair(a[0], a[2], 2, 0x33333333u);
