@@ -1583,7 +1583,7 @@ __device__ __forceinline__ void front_zb(const CompressArgs& a, const QuantP& P,
 // Tail of a z-band step: codes, bitshuffle, outliers, flags to the stream, nonzero blocks
 // to the tile's staging slot.
 __device__ __forceinline__ void tail_zb(const CompressArgs& a, ZbShared& sh, uint32_t* Obuf, uint32_t t, uint32_t g0,
-                                        uint32_t vm, const int32_t (&dl)[8], uint32_t vmask, const float (&dv)[8])
+                                        uint32_t vm, const int32_t (&dl)[8], uint32_t vmask)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Ctrl* ctrl = a.ctrl;
@@ -1660,7 +1660,8 @@ __device__ __forceinline__ void tail_zb(const CompressArgs& a, ZbShared& sh, uin
                 ++pd;
             }
             if (vmask & (1u << e)) {
-                if (pv < a.vcap) a.vstage[pv] = make_uint2(gi, __float_as_uint(dv[e]));
+                // raw bits re-read from the field (rare path; keeps the 8 inputs out of registers)
+                if (pv < a.vcap) a.vstage[pv] = make_uint2(gi, __float_as_uint(__ldg(a.field + (gi - a.base))));
                 else atomicOr(&ctrl->stage_overflow, 1u);
                 ++pv;
             }
@@ -1731,11 +1732,17 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
         const uint32_t z0 = c * kZbChunk, z1 = min(nz, z0 + kZbChunk);
         // the thread's in-row / in-plane positions are the same in every plane of the column
         const uint32_t pp = p * kTileCodes + 8u * tid;
+        // pp + e < P: no plane wrap inside a thread's 8 elements.  nx >= 4, so x0 + e < 3 nx and
+        // a row starts at element e iff x0 + e is 0, nx or 2 nx.
         uint32_t xm = 0xFFu, ym = 0xFFu;
+        {
+            const uint32_t x0 = fmod_(pp, a.dnx), nx = a.g.nx;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {   // pp + e < P: no plane wrap inside a thread's 8 elements
-            if (fmod_(pp + e, a.dnx) == 0) xm &= ~(1u << e);
-            if (pp + e < a.g.nx) ym &= ~(1u << e);
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t xe = x0 + e;
+                if (xe == 0 || xe == nx || xe == 2 * nx) xm &= ~(1u << e);
+                if (pp + e < nx) ym &= ~(1u << e);
+            }
         }
         uint32_t Dp[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, Dp0 = 0u;
         if (tid == 0) zb_issue(a, sh, inbuf, z0 * tpp + p);
@@ -1757,9 +1764,14 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
                     else sh.tma_bits = 0;
                 }
             };
+            // opaque per-step copies: keeps the compiler from hoisting 16 per-element mask
+            // registers out of the z loop (they spill at 64 registers)
+            uint32_t xmv, ymv;
+            asm volatile("mov.b32 %0, %1;" : "=r"(xmv) : "r"(xm));
+            asm volatile("mov.b32 %0, %1;" : "=r"(ymv) : "r"(ym));
             front_zb(a, P, smem, rmask, 0, RB, t, z == z0 && z > 0, (bits & 1) ? inbuf : nullptr,
-                     (bits & 2) ? inbuf + kTileCodes : nullptr, xm, ym, Dp, Dp0, dl, vmask, dv, issue_next);
-            tail_zb(a, sh, Obuf, t, (uint32_t)t * kTileCodes + 8u * tid, 0xFFu, dl, vmask, dv);
+                     (bits & 2) ? inbuf + kTileCodes : nullptr, xmv, ymv, Dp, Dp0, dl, vmask, dv, issue_next);
+            tail_zb(a, sh, Obuf, t, (uint32_t)t * kTileCodes + 8u * tid, 0xFFu, dl, vmask);
         }
     }
 }

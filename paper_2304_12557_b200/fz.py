@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libfz.so")
+LIB_PATH = os.environ.get("FZ_LIB") or os.path.join(PKG, "libfz.so")  # FZ_LIB: A/B builds
 
 ABS, REL = 0, 1
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_EB_TOO_SMALL", 4: "ERR_CAPACITY",
