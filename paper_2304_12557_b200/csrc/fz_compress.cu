@@ -1668,20 +1668,19 @@ __device__ __forceinline__ void tail_zb(const CompressArgs& a, ZbShared& sh, uin
         }
         bar_sync(kBarCompute, kCta);
     }
+    // C6: thread tid holds block b = tid (O[r][4x..4x+3], r = tid/8, x = tid%8), so warp w's
+    // ballot is flag word w.  Its nonzero blocks go to sub-slot w (32 blocks) of the tile's
+    // staging slot in lane order; k_compact concatenates the sub-slots (C8 order b).  No
+    // cross-warp exchange, no barrier.
     const uint32_t* row = Obuf + (tid >> 3) * 33 + 4 * (tid & 7);
     const uint4 blk = make_uint4(row[0], row[1], row[2], row[3]);
     const bool nz = (blk.x | blk.y | blk.z | blk.w) != 0;
     const uint32_t F = __ballot_sync(kFull, nz);
-    if (lane == 0) sh.F[warp] = F;
-    bar_sync(kBarCompute, kCta);
-    const uint32_t fw = lane < 8 ? sh.F[lane] : 0u;
-    const uint32_t pc = __popc(fw);
-    const uint32_t wpre = __reduce_add_sync(kFull, lane < warp ? pc : 0u);
-    if (tid < 8) {
-        const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * tid;
-        if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = fw;
+    if (lane == 0) {
+        const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * warp;
+        if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = F;
     }
-    if (nz) a.tstage[(uint64_t)t * kTileBlocks + wpre + __popc(F & ((1u << lane) - 1u))] = blk;
+    if (nz) a.tstage[(uint64_t)t * kTileBlocks + 32 * warp + __popc(F & ((1u << lane) - 1u))] = blk;
 }
 
 __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
@@ -1748,7 +1747,9 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
         if (tid == 0) zb_issue(a, sh, inbuf, z0 * tpp + p);
         for (uint32_t z = z0; z < z1; ++z) {
             const uint32_t t = z * tpp + p;
-            __syncthreads();                      // sh.tma_bits written by thread 0
+            // sh.tma_bits: at z0 written by thread 0 just above; later by issue_next in the
+            // previous step's front, ordered by that step's tail barrier (bar_or)
+            if (z == z0) __syncthreads();
             const uint32_t bits = sh.tma_bits;
             if (bits) {
                 while (!mbar_try_wait(&sh.mbar, phase)) {
@@ -1787,12 +1788,24 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ fl
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t t = wid; t < ntiles; t += nw) {
         const uint32_t fw = lane < 8 ? __ldg(flags + 8 * (uint64_t)t + lane) : 0u;
-        const uint32_t cnt = __reduce_add_sync(kFull, __popc(fw));
+        const uint32_t pc = __popc(fw);
+        uint32_t pre = pc;   // inclusive prefix over the 8 flag words (lanes 0..7)
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, pre, o);
+            if (lane >= o) pre += y;
+        }
+        pre -= pc;
         const uint64_t off = (uint64_t)__ldg(bpre + (t >> 10)) + __ldg(loc + t);
         const uint4* src = tstage + (uint64_t)t * kTileBlocks;
-        for (uint32_t i = lane; i < cnt; i += 32) {
-            const uint64_t bo = 16 * (off + i);
-            if (bo + 16 <= payload_cap) __stcs(reinterpret_cast<uint4*>(payload_out + bo), __ldcs(src + i));
+        // sub-slot w holds flag word w's nonzero blocks (k_compress_zb), in block order
+#pragma unroll 2
+        for (int w = 0; w < 8; ++w) {
+            const uint32_t cw = __shfl_sync(kFull, pc, w), pw = __shfl_sync(kFull, pre, w);
+            if ((uint32_t)lane < cw) {
+                const uint64_t bo = 16 * (off + pw + lane);
+                if (bo + 16 <= payload_cap) __stcs(reinterpret_cast<uint4*>(payload_out + bo), __ldcs(src + 32 * w + lane));
+            }
         }
     }
 }
