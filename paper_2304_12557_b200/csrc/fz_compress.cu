@@ -1474,23 +1474,31 @@ __device__ __forceinline__ void zb_issue(const CompressArgs& a, ZbShared& sh, fl
 }
 
 // Quantize the hw floats staged in shared memory (field elements [g_lo, g_lo + hw)) into ring
-// `ro` (positions & rmask); warp-uniform trip count (pq_many votes across the warp).
+// `ro` (positions & rmask).  Element-strided over the whole CTA so every warp does about the
+// same share (the front barrier follows); warp-uniform trip count (pq_many votes per warp).
 __device__ __forceinline__ void zb_fill_halo(const QuantP& P, int* smem, int ro, uint32_t rmask, const float* src,
                                              int64_t g_lo, int hw)
 {
-    for (int b0 = 0; b0 < hw; b0 += 8 * kCta) {
-        if (b0 + 256 * (int)(threadIdx.x >> 5) >= hw) break;   // warp-uniform: no element left for this warp
-        const int c0 = b0 + 8 * (int)threadIdx.x;
-        float v[8];
-        int q[8];
-        float4 x = make_float4(0, 0, 0, 0), y = make_float4(0, 0, 0, 0);
-        if (c0 < hw) x = *reinterpret_cast<const float4*>(src + c0);
-        if (c0 + 4 < hw) y = *reinterpret_cast<const float4*>(src + c0 + 4);
-        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
-        pq_many<8>(v, q, P);
+    const int wbase = (int)(threadIdx.x & ~31u);
+    for (int b0 = 0; b0 < hw; b0 += 2 * kCta) {
+        if (b0 + wbase >= hw) break;   // warp-uniform: no element left for this warp
+        const int c0 = b0 + (int)threadIdx.x, c1 = c0 + kCta;
+        const bool has1 = b0 + kCta + wbase < hw;   // warp-uniform
+        float v[2];
+        int q[2];
+        v[0] = c0 < hw ? src[c0] : 0.0f;
+        v[1] = (has1 && c1 < hw) ? src[c1] : 0.0f;
+        if (has1) {
+            pq_many<2>(v, q, P);
+        } else {
+            float v1[1] = {v[0]};
+            int q1[1];
+            pq_many<1>(v1, q1, P);
+            q[0] = q1[0];
+        }
         const uint32_t g = (uint32_t)(g_lo + c0);
-        if (c0 < hw) *reinterpret_cast<int4*>(smem + ro + (g & rmask)) = make_int4(q[0], q[1], q[2], q[3]);
-        if (c0 + 4 < hw) *reinterpret_cast<int4*>(smem + ro + ((g + 4) & rmask)) = make_int4(q[4], q[5], q[6], q[7]);
+        if (c0 < hw) smem[ro + (g & rmask)] = q[0];
+        if (has1 && c1 < hw) smem[ro + ((g + kCta) & rmask)] = q[1];
     }
 }
 
