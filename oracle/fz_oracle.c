@@ -186,7 +186,17 @@ int fzo_prequantize_one(float d, const fzo_params* p, int32_t* q)
 /*     neighbours outside the field are 0 (field-global boundary, reading R5),           */
 /*     arithmetic modulo 2^32 (reading R6).                                              */
 /* ------------------------------------------------------------------------------------ */
-void fzo_lorenzo(const int32_t* q, int ndim, const uint64_t* dims, int32_t* delta)
+/* f1 ("chunked data blocks can be compressed independently"):  */
+/* the chunk-local variant treats a neighbour in another chunk like one outside the     */
+/* field.  A chunk is cz planes x cy rows x the whole row of a 3-D field; cz = cy = 0    */
+/* means no chunking (the paper's field-global predictor, reading R5).                  */
+static int no_nb(uint64_t i, uint64_t c)
+{
+    return i == 0 || (c != 0 && i % c == 0);
+}
+
+static void lorenzo_cc(const int32_t* q, int ndim, const uint64_t* dims, uint64_t cz, uint64_t cy,
+                       int32_t* delta)
 {
     uint64_t nz, ny, nx, z, y, x;
     dims3(ndim, dims, &nz, &ny, &nx);
@@ -199,11 +209,21 @@ void fzo_lorenzo(const int32_t* q, int ndim, const uint64_t* dims, int32_t* delt
                     for (b = 0; b <= 1; ++b)
                         for (c = 0; c <= 1; ++c) {
                             int sign = ((a + b + c) & 1) ? -1 : 1;
-                            if ((a && z == 0) || (b && y == 0) || (c && x == 0)) continue;
+                            if ((a && no_nb(z, cz)) || (b && no_nb(y, cy)) || (c && x == 0)) continue;
                             s += sign * (int64_t)q[((z - a) * ny + (y - b)) * nx + (x - c)];
                         }
                 delta[(z * ny + y) * nx + x] = (int32_t)(uint32_t)(uint64_t)s;
             }
+}
+
+void fzo_lorenzo(const int32_t* q, int ndim, const uint64_t* dims, int32_t* delta)
+{
+    lorenzo_cc(q, ndim, dims, 0, 0, delta);
+}
+
+void fzo_lorenzo_chunked(const int32_t* q, const uint64_t* dims, uint64_t cz, uint64_t cy, int32_t* delta)
+{
+    lorenzo_cc(q, 3, dims, cz, cy, delta);
 }
 
 /* ------------------------------------------------------------------------------------ */
@@ -271,6 +291,7 @@ int fzo_flags_tile(const uint32_t* O, uint32_t* F)
 /* Field-level quantization stage (C1 -> C2 -> C3).                                      */
 /* ------------------------------------------------------------------------------------ */
 static int quantize_all(const float* d, int ndim, const uint64_t* dims, const fzo_params* p,
+                        uint64_t cz, uint64_t cy,
                         uint64_t n, uint16_t* codes, uint8_t* dflag, int32_t* dval,
                         uint8_t* vflag)
 {
@@ -278,7 +299,7 @@ static int quantize_all(const float* d, int ndim, const uint64_t* dims, const fz
     uint64_t i;
     if (q == NULL) return FZO_ERR_ARG;
     for (i = 0; i < n; ++i) vflag[i] = (uint8_t)fzo_prequantize_one(d[i], p, &q[i]);
-    fzo_lorenzo(q, ndim, dims, dval);
+    lorenzo_cc(q, ndim, dims, cz, cy, dval);
     free(q);
     for (i = 0; i < n; ++i) dflag[i] = (uint8_t)fzo_pack(dval[i], &codes[i]);
     return FZO_OK;
@@ -298,7 +319,7 @@ int fzo_quantize_field(const float* d, int ndim, const uint64_t* dims, const fzo
     vflag = (uint8_t*)malloc(n);
     dval = (int32_t*)malloc(n * sizeof(int32_t));
     if (!dflag || !vflag || !dval) { free(dflag); free(vflag); free(dval); return FZO_ERR_ARG; }
-    quantize_all(d, ndim, dims, p, n, codes, dflag, dval, vflag);
+    quantize_all(d, ndim, dims, p, 0, 0, n, codes, dflag, dval, vflag);
     for (i = 0; i < n; ++i) {
         if (dflag[i]) {
             if (kd < dcap) { didx[kd] = (uint32_t)i; dval_out[kd] = dval[i]; }
@@ -330,9 +351,8 @@ uint64_t fzo_compress_bound(int ndim, const uint64_t* dims)
 /* (a block is written iff its offset differs from the previous one),  */
 /* C8 compaction, C9 container.                                                          */
 /* ------------------------------------------------------------------------------------ */
-int fzo_compress_with_params(const float* d, int ndim, const uint64_t* dims,
-                             const fzo_params* p, uint8_t* out, uint64_t cap,
-                             uint64_t* size)
+static int compress_cc(const float* d, int ndim, const uint64_t* dims, const fzo_params* p,
+                       uint64_t cz, uint64_t cy, uint8_t* out, uint64_t cap, uint64_t* size)
 {
     uint64_t n, T, t, i, k, nnz = 0, nd = 0, nv = 0, total, pos;
     uint16_t* codes;
@@ -360,7 +380,7 @@ int fzo_compress_with_params(const float* d, int ndim, const uint64_t* dims,
     }
 
     /* C1-C3 */
-    quantize_all(d, ndim, dims, p, n, codes, dflag, dval, vflag);
+    quantize_all(d, ndim, dims, p, cz, cy, n, codes, dflag, dval, vflag);
     for (i = 0; i < n; ++i) { nd += dflag[i]; nv += vflag[i]; }
 
     /* C4 + C5 + C6 per tile: word k = code[2k] | code[2k+1] << 16 (reading R9) */
@@ -389,8 +409,13 @@ int fzo_compress_with_params(const float* d, int ndim, const uint64_t* dims,
     memset(out, 0, HDR_BYTES);
     memcpy(out, "FZB2", 4);
     put_u16(out + 4, 1);
-    put_u16(out + 6, (uint16_t)((p->mode == FZO_REL ? 1u : 0u) | (p->fallback ? 2u : 0u)));
+    put_u16(out + 6, (uint16_t)((p->mode == FZO_REL ? 1u : 0u) | (p->fallback ? 2u : 0u) |
+                                (cz ? 4u : 0u)));
     out[8] = (uint8_t)ndim;
+    if (cz) {                 /* f1: chunk depth and height (bytes 10-13, zero otherwise) */
+        put_u16(out + 10, (uint16_t)cz);
+        put_u16(out + 12, (uint16_t)cy);
+    }
     for (k = 0; k < 3; ++k) put_u64(out + 16 + 8 * k, k < (uint64_t)ndim ? dims[k] : 1u);
     put_u64(out + 40, n);
     put_f64(out + 48, p->eb_input);
@@ -440,6 +465,31 @@ done:
     return st;
 }
 
+int fzo_compress_with_params(const float* d, int ndim, const uint64_t* dims,
+                             const fzo_params* p, uint8_t* out, uint64_t cap,
+                             uint64_t* size)
+{
+    return compress_cc(d, ndim, dims, p, 0, 0, out, cap, size);
+}
+
+/* f1: chunk-local compressor (3-D only; 1 <= cz, cy <= 65535). */
+int fzo_compress_chunked(const float* d, const uint64_t* dims, int mode, double eb, uint64_t cz,
+                         uint64_t cy, uint8_t* out, uint64_t cap, uint64_t* size)
+{
+    uint64_t n;
+    float mn, mx;
+    int64_t bad;
+    fzo_params p;
+    int st = check_shape(3, dims, &n);
+    if (st != FZO_OK) return st;
+    if (d == NULL || size == NULL || cz < 1 || cy < 1 || cz > 65535 || cy > 65535) return FZO_ERR_ARG;
+    st = fzo_range(d, n, &mn, &mx, &bad);
+    if (st != FZO_OK) return st;
+    st = fzo_derive_params(mn, mx, mode, eb, &p);
+    if (st != FZO_OK) return st;
+    return compress_cc(d, 3, dims, &p, cz, cy, out, cap, size);
+}
+
 int fzo_compress(const float* d, int ndim, const uint64_t* dims, int mode, double eb,
                  uint8_t* out, uint64_t cap, uint64_t* size)
 {
@@ -464,6 +514,7 @@ int fzo_compress(const float* d, int ndim, const uint64_t* dims, int mode, doubl
 /* ------------------------------------------------------------------------------------ */
 typedef struct {
     int ndim;
+    uint64_t cz, cy;          /* f1 chunk depth / height, 0 = field-global Lorenzo */
     uint64_t dims[3], n, T, nnz, nd, nv, total;
     float w;
     const uint8_t *flags, *payload, *dsec, *vsec;
@@ -483,6 +534,12 @@ static int parse(const uint8_t* in, uint64_t size, parsed_t* h)
     if (memcmp(in, "FZB2", 4) != 0 || get_u16(in + 4) != 1) return FZO_ERR_CORRUPT;
     h->ndim = in[8];
     if (h->ndim < 1 || h->ndim > 3) return FZO_ERR_CORRUPT;
+    h->cz = h->cy = 0;
+    if (get_u16(in + 6) & 4u) {
+        h->cz = get_u16(in + 10);
+        h->cy = get_u16(in + 12);
+        if (h->ndim != 3 || h->cz == 0 || h->cy == 0) return FZO_ERR_CORRUPT;
+    }
     for (k = 0; k < 3; ++k) {
         h->dims[k] = get_u64(in + 16 + 8 * k);
         if (h->dims[k] == 0 || h->dims[k] > 0xFFFFFFFFull) return FZO_ERR_CORRUPT;
@@ -566,7 +623,7 @@ static int decode_q(const parsed_t* h, int32_t* q)
                         for (c = 0; c <= 1; ++c) {
                             uint32_t v;
                             if (a + b + c == 0) continue;
-                            if ((a && z == 0) || (b && y == 0) || (c && x == 0)) continue;
+                            if ((a && no_nb(z, h->cz)) || (b && no_nb(y, h->cy)) || (c && x == 0)) continue;
                             v = (uint32_t)q[((z - a) * ny + (y - b)) * nx + (x - c)];
                             /* pred = -sum_{(a,b,c) != 0} (-1)^(a+b+c) q(...) */
                             if ((a + b + c) & 1) s += v; else s -= v;

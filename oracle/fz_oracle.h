@@ -75,6 +75,10 @@ int fzo_prequantize_one(float d, const fzo_params* p, int32_t* q);
  * outside the field, int32 wrap-around.  dims slowest first, ndim in {1,2,3}. */
 void fzo_lorenzo(const int32_t* q, int ndim, const uint64_t* dims, int32_t* delta);
 
+/* f1 chunk-local Lorenzo: as fzo_lorenzo on a 3-D field, but a
+ * neighbour in another chunk (cz planes x cy rows x the whole row) counts as 0. */
+void fzo_lorenzo_chunked(const int32_t* q, const uint64_t* dims, uint64_t cz, uint64_t cy, int32_t* delta);
+
 /* C3 sign-magnitude packing: returns 1 if |delta| > 32767 (delta outlier,
  * code 0), else 0. */
 int fzo_pack(int32_t delta, uint16_t* code);
@@ -107,6 +111,11 @@ int fzo_compress(const float* d, int ndim, const uint64_t* dims, int mode, doubl
 int fzo_compress_with_params(const float* d, int ndim, const uint64_t* dims,
                              const fzo_params* p, uint8_t* out, uint64_t cap,
                              uint64_t* size);
+
+/* f1 chunk-local compressor (3-D): header flag bit 2, chunk depth/height at bytes 10-13;
+ * the decompressors below read both variants. */
+int fzo_compress_chunked(const float* d, const uint64_t* dims, int mode, double eb, uint64_t cz,
+                         uint64_t cy, uint8_t* out, uint64_t cap, uint64_t* size);
 
 /* Full decompressor.  out: n floats, n must equal the header's element count. */
 int fzo_decompress(const uint8_t* in, uint64_t size, float* out, uint64_t n);

@@ -59,6 +59,8 @@ def lib():
         L.fzo_compress_with_params.argtypes = [P, C.c_int, P, C.POINTER(Params), P, u64, P]
         L.fzo_decompress.argtypes = [P, u64, P, u64]
         L.fzo_decode_q.argtypes = [P, u64, P, u64]
+        L.fzo_lorenzo_chunked.argtypes = [P, P, u64, u64, P]
+        L.fzo_compress_chunked.argtypes = [P, P, C.c_int, C.c_double, u64, u64, P, u64, P]
         _lib = L
     return _lib
 
@@ -181,6 +183,29 @@ def compress(d: np.ndarray, mode: int, eb: float, params: Params | None = None):
     else:
         st = lib().fzo_compress_with_params(_ptr(d), d.ndim, _ptr(dims), C.byref(params),
                                             _ptr(out), cap, C.byref(size))
+    if st != OK:
+        return st, None
+    return st, out[: size.value].copy()
+
+
+def lorenzo_chunked(q: np.ndarray, cz: int, cy: int) -> np.ndarray:
+    """f1: chunk-local Lorenzo of a 3-D array (chunks of cz planes x cy rows x full rows)."""
+    q = np.ascontiguousarray(q, dtype=np.int32)
+    assert q.ndim == 3
+    out = np.empty_like(q)
+    dims = _dims(q.shape)
+    lib().fzo_lorenzo_chunked(_ptr(q), _ptr(dims), cz, cy, _ptr(out))
+    return out
+
+
+def compress_chunked(d: np.ndarray, mode: int, eb: float, cz: int, cy: int):
+    """f1 chunk-local compressor (3-D).  Returns (status, bytes)."""
+    d = np.ascontiguousarray(d, dtype=np.float32)
+    dims = _dims(d.shape)
+    cap = compress_bound(d.shape)
+    out = np.empty(cap, dtype=np.uint8)
+    size = C.c_uint64()
+    st = lib().fzo_compress_chunked(_ptr(d), _ptr(dims), mode, eb, cz, cy, _ptr(out), cap, C.byref(size))
     if st != OK:
         return st, None
     return st, out[: size.value].copy()

@@ -203,6 +203,70 @@ def test_lorenzo_annihilates_lower_dim_functions():
 
 
 # --------------------------------------------------------------------------------------
+# f1 chunk-local Lorenzo ("chunked data blocks can be compressed
+# independently"): each chunk's residuals are the field-global closed form applied to the
+# chunk alone, so chunks are independent (pinned with numpy, not with the oracle itself).
+# --------------------------------------------------------------------------------------
+
+def _np_lorenzo_chunked(q: np.ndarray, cz: int, cy: int) -> np.ndarray:
+    out = np.empty_like(q)
+    for z0 in range(0, q.shape[0], cz):
+        for y0 in range(0, q.shape[1], cy):
+            sub = q[z0:z0 + cz, y0:y0 + cy, :]
+            out[z0:z0 + cz, y0:y0 + cy, :] = _np_lorenzo(sub)
+    return out
+
+
+@pytest.mark.parametrize("shape,cz,cy", [((35, 12, 8), 16, 4), ((16, 8, 64), 16, 32), ((7, 9, 5), 3, 2),
+                                         ((5, 6, 7), 64, 64), ((33, 64, 64), 16, 32)])
+def test_lorenzo_chunked_closed_form(shape, cz, cy):
+    rng = np.random.default_rng(11)
+    q = rng.integers(-2 ** 31, 2 ** 31, size=shape, dtype=np.int64).astype(np.int32)
+    assert np.array_equal(O.lorenzo_chunked(q, cz, cy), _np_lorenzo_chunked(q, cz, cy))
+    if cz >= shape[0] and cy >= shape[1]:   # one chunk: the field-global predictor
+        assert np.array_equal(O.lorenzo_chunked(q, cz, cy), O.lorenzo(q))
+
+
+def test_chunked_stream_roundtrip_and_independence():
+    """Chunk-local stream: bound on every element, header bit 2 + chunk dims, and the codes
+    of each chunk equal the global-mode codes of that chunk compressed as its own field
+    with the same parameters (ABS: parameters do not depend on the rest of the field)."""
+    from paper_2304_12557_b200 import synth
+    d = synth.generate("sines3d", (40, 64, 64))
+    cz, cy = 16, 32
+    st, buf = O.compress_chunked(d, O.ABS, 1e-3, cz, cy)
+    assert st == O.OK
+    assert int.from_bytes(buf[6:8].tobytes(), "little") & 4
+    assert int.from_bytes(buf[10:12].tobytes(), "little") == cz
+    assert int.from_bytes(buf[12:14].tobytes(), "little") == cy
+    st, x = O.decompress(buf, d.size)
+    assert st == O.OK
+    assert np.all(np.abs(x.astype(np.float64) - d.reshape(-1).astype(np.float64)) <= 1e-3)
+    p = O.params_for(d, O.ABS, 1e-3)
+    q, _ = O.prequantize(d[:cz, :cy], p)
+    qz, _ = O.prequantize(d[cz:2 * cz, cy:2 * cy], p)
+    full = O.lorenzo_chunked(O.prequantize(d, p)[0].reshape(d.shape), cz, cy)
+    assert np.array_equal(full[:cz, :cy], _np_lorenzo(q.reshape(cz, cy, 64)))
+    assert np.array_equal(full[cz:2 * cz, cy:2 * cy], _np_lorenzo(qz.reshape(cz, cy, 64)))
+    st, qd = O.decode_q(buf, d.size)
+    assert st == O.OK and np.array_equal(qd, O.prequantize(d, p)[0])
+
+
+def test_chunked_single_chunk_equals_global_stream():
+    """When one chunk covers the field, the stream equals the global one except the header's
+    chunk fields."""
+    from paper_2304_12557_b200 import synth
+    d = synth.generate("sines3d", (8, 32, 64))
+    st, g = O.compress(d, O.REL, 1e-3)
+    st2, c = O.compress_chunked(d, O.REL, 1e-3, 8, 32)
+    assert st == st2 == O.OK and g.size == c.size
+    c2 = c.copy()
+    c2[6] &= 0xFB
+    c2[10:14] = 0
+    assert np.array_equal(g, c2)
+
+
+# --------------------------------------------------------------------------------------
 # C3 codes (P:188-205)
 # --------------------------------------------------------------------------------------
 
