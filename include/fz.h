@@ -30,6 +30,17 @@ extern "C" {
 
 typedef enum { FZ_EB_ABS = 0, FZ_EB_REL = 1 } fz_eb_mode;   /* REL = eb * (max-min) */
 
+/* f1 ("chunked data blocks can be compressed independently"): OR
+ * into eb_mode of fz_compress / fz_compress_async to select the chunk-local Lorenzo
+ * predictor.  Neighbours in another chunk count as zero, a chunk being 16 planes x one tile
+ * (2048 / nx whole rows) of a 3-D field, so each chunk decodes on its own in one pass.
+ * Shapes: 3-D, nz >= 2, nx % 4 == 0, nx divides 2048, (ny * nx) % 2048 == 0; otherwise
+ * FZ_ERR_ARG.  The stream sets header flag bit 2 and stores the chunk depth / height as
+ * u16 at bytes 10 / 12.  fz_decompress and fz_decompress_hdr read either variant;
+ * fz_decompress_async reports FZ_ERR_ARG for a chunk-local stream.  More than N/64 + 1024
+ * outliers of one kind return FZ_ERR_WORKSPACE in this mode (no rescan pass). */
+#define FZ_CHUNK_LOCAL 0x100
+
 typedef enum {
     FZ_OK = 0,
     FZ_ERR_ARG = 1,          /* ndim not in {1,2,3}, zero extent, N >= 2^32, eb <= 0 or

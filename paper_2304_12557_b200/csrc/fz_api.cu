@@ -142,6 +142,18 @@ bool zb_layout(const fz_shape& s)
     return s.ndim == 3 && zb_shape(3, s.dims[1], s.dims[2], s.dims[0]);
 }
 
+// f1 chunk-local Lorenzo: 3-D fields whose tiles hold whole rows of one plane;
+// chunk = 16 planes x one tile (2048 / nx rows).  Header word: cz | cy << 16.
+constexpr uint32_t kClDepth = 16;
+bool cl_shape(const fz_shape& s)
+{
+    return zb_layout(s) && s.dims[2] <= (uint64_t)kTileCodes && kTileCodes % s.dims[2] == 0;
+}
+uint32_t cl_chunk(const fz_shape& s)
+{
+    return kClDepth | (uint32_t)(kTileCodes / s.dims[2]) << 16;
+}
+
 CompressArgs make_args(const Work& W, const float* field, uint64_t base, const Geom& g,
                        uint32_t tb, uint32_t te)
 {
@@ -197,7 +209,8 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
 {
     const uint32_t tb = a.tile_begin, nt = a.tile_end - a.tile_begin;
     // status words are per scan unit, indexed from the range start; outlier counts per tile
-    FZ_CUDA(launch_init(W.ctrl(), W.status(), W.ocnt() + tb, nt, hp, st));
+    FZ_CUDA(launch_init(W.ctrl(), W.status(), W.ocnt() + tb, nt, hp, st, a.cl ? cl_chunk(s) : 0u));
+    if (a.cl && !compress_uses_zb(a)) return FZ_ERR_ARG;
     if (compress_uses_zb(a)) {
         // z-band two-pass compressor: pass 1 derives the parameters in its prologue, writes
         // the flags and stages each tile's blocks; the popcount scan of the flags gives the
@@ -250,6 +263,7 @@ fz_status place_outliers(const Work& W, CompressArgs a, const Ctrl& h, const Out
     if (h.nd + h.nv == 0) return FZ_OK;
     const uint32_t tb = a.tile_begin, nt = a.tile_end - a.tile_begin;
     FZ_CUDA(launch_outlier_scan(W.ocnt() + tb, W.opre() + tb, nt, st));
+    if (h.stage_overflow && a.cl) return FZ_ERR_WORKSPACE;   // the rescan kernels are field-global only
     if (!h.stage_overflow) {
         FZ_CUDA(launch_outlier_place(W.ocnt() + tb, W.obase() + tb, W.opre() + tb, nt, W.dstage(), W.vstage(),
                                      d.drec, d.vrec, d.didx, d.dval, d.vidx, d.vbits, st));
@@ -271,14 +285,16 @@ fz_status place_outliers(const Work& W, CompressArgs a, const Ctrl& h, const Out
 }
 
 void write_header_host(uint8_t* h, const fz_shape& s, uint64_t n, uint64_t T, const fz_params& p,
-                       const fz_counts& c, uint64_t total)
+                       const fz_counts& c, uint64_t total, uint32_t chunk = 0)
 {
     memset(h, 0, 128);
     memcpy(h, "FZB2", 4);
-    const uint16_t ver = 1, fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u));
+    const uint16_t ver = 1,
+                   fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u) | (chunk ? 4u : 0u));
     memcpy(h + 4, &ver, 2);
     memcpy(h + 6, &fl, 2);
     h[8] = (uint8_t)s.ndim;
+    memcpy(h + 10, &chunk, 4);
     for (uint32_t k = 0; k < 3; ++k) {
         uint64_t d = k < s.ndim ? s.dims[k] : 1;
         memcpy(h + 16 + 8 * k, &d, 8);
@@ -302,6 +318,9 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     if (!shape_n(s, &n) || d_field == nullptr || d_out == nullptr || out_size == nullptr ||
         d_work == nullptr || !aligned16(d_field) || !aligned16(d_out) || !aligned16(d_work))
         return FZ_ERR_ARG;
+    const bool cl = (mode & FZ_CHUNK_LOCAL) != 0;
+    mode &= ~FZ_CHUNK_LOCAL;
+    if (cl && !cl_shape(*s)) return FZ_ERR_ARG;
     if (hp == nullptr && (!(eb > 0.0) || !std::isfinite(eb) || (mode != FZ_EB_ABS && mode != FZ_EB_REL)))
         return FZ_ERR_ARG;
     const uint64_t T = tiles_of(n);
@@ -311,6 +330,7 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     uint8_t* out = static_cast<uint8_t*>(d_out);
 
     CompressArgs a = make_args(W, d_field, 0, g, 0, (uint32_t)T);
+    a.cl = cl ? 1u : 0u;
     const uint64_t fbase = kHeaderBytes, pbase = kHeaderBytes + 32 * T;
     a.flags_out = out + fbase;
     a.flags_cap = out_cap > fbase ? out_cap - fbase : 0;
@@ -328,7 +348,8 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     rs = place_outliers(W, a, h, d, st);
     if (rs == FZ_OK) {
         // the same bytes k_finalize wrote to the stream's header
-        write_header_host(g_last_hdr, *s, n, T, h.p, fz_counts{h.nnz, h.nd, h.nv}, h.total);
+        write_header_host(g_last_hdr, *s, n, T, h.p, fz_counts{h.nnz, h.nd, h.nv}, h.total,
+                          cl ? cl_chunk(*s) : 0u);
         g_have_hdr = true;
     }
     return rs;
@@ -450,6 +471,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         return FZ_ERR_ARG;
     const bool dev = dev_shape != nullptr;
     fz_info I{};
+    uint32_t chunk = 0;      // f1 chunk-local stream: cz | cy << 16 from header bytes 10-13
     if (dev) {
         uint64_t nn;
         if (!shape_n(dev_shape, &nn) || nn != n) return FZ_ERR_ARG;
@@ -467,6 +489,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         fz_status rs = fz_peek_header(hdr, 128, &I);
         if (rs != FZ_OK) return rs;
         if (I.n != n) return FZ_ERR_ARG;
+        if (I.flags & 4u) memcpy(&chunk, hdr + 10, 4);
         if (in_size < I.total_size) return FZ_ERR_CORRUPT;
     }
     const DecodeLayout L = decode_layout(I.shape);
@@ -489,7 +512,10 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     int32_t* q = d_q ? d_q : reinterpret_cast<int32_t*>(d_field);
     const bool deq = d_q == nullptr;
 
-    const bool fuse_y = decode_fuses_y(I.shape) && !(exp_bits() & 128);
+    // f1 chunk-local stream (header bit 2): one-pass chunk decode
+    if (chunk != 0 && (!cl_shape(I.shape) || (chunk >> 16) != kTileCodes / I.shape.dims[2] || (chunk & 0xFFFFu) == 0))
+        return FZ_ERR_ARG;   // a chunk geometry this decoder does not implement
+    const bool fuse_y = chunk == 0 && decode_fuses_y(I.shape) && !(exp_bits() & 128);
     auto* drange = reinterpret_cast<uint32_t*>(wb + L.drange);
     const float* wp = (dev && deq) ? &ctrl->dec_w : nullptr;   // device bin width (dev mode)
     if (dev) {
@@ -526,6 +552,18 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         // two CTAs per plane unless the planes alone fill the GPU several times over
         a.yseg = (a.tpp % 2 == 0 && I.shape.dims[0] < 4 * 148 && !(exp_bits() & 512)) ? 2 : 1;
         a.ycarry = reinterpret_cast<int32_t*>(wb + L.ycarry);
+    }
+    if (chunk != 0) {
+        a.w = deq ? I.params.w : 0.0f;
+        FZ_CUDA(launch_decode_cl(a, chunk & 0xFFFFu, st));
+        if (deq) FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+        if (async) return FZ_OK;
+        Ctrl hc;
+        FZ_CUDA(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+        FZ_CUDA(cudaStreamSynchronize(st));
+        if (hc.err != 0) return err_status(hc.err);
+        if (hc.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;
+        return FZ_OK;
     }
     FZ_CUDA(launch_decode_tiles(a, st, fuse_y));
     // x carries exist when some tile starts inside a row (always for 1-D fields)
@@ -591,6 +629,9 @@ fz_status fz_compress_async(const float* d_field, const fz_shape* s, int eb_mode
     if (!shape_n(s, &n) || d_field == nullptr || d_out == nullptr || d_work == nullptr || !aligned16(d_field) ||
         !aligned16(d_out) || !aligned16(d_work))
         return FZ_ERR_ARG;
+    const bool cl = (eb_mode & FZ_CHUNK_LOCAL) != 0;
+    eb_mode &= ~FZ_CHUNK_LOCAL;
+    if (cl && !cl_shape(*s)) return FZ_ERR_ARG;
     if (!(eb > 0.0) || !std::isfinite(eb) || (eb_mode != FZ_EB_ABS && eb_mode != FZ_EB_REL)) return FZ_ERR_ARG;
     const uint64_t T = tiles_of(n);
     Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
@@ -599,6 +640,7 @@ fz_status fz_compress_async(const float* d_field, const fz_shape* s, int eb_mode
     const Geom g = geom_of(*s, n);
     uint8_t* out = static_cast<uint8_t*>(d_out);
     CompressArgs a = make_args(W, d_field, 0, g, 0, (uint32_t)T);
+    a.cl = cl ? 1u : 0u;
     const uint64_t pbase = kHeaderBytes + 32 * T;
     a.flags_out = out + kHeaderBytes;
     a.flags_cap = out_cap > kHeaderBytes ? out_cap - kHeaderBytes : 0;

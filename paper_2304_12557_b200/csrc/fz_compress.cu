@@ -61,7 +61,7 @@ __device__ int params_from_range(const Ctrl* ctrl, int mode, double eb, uint64_t
 
 // ------------------------------------------------------------------------------------
 __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint32_t ntiles,
-                       int set_params, fz_params p)
+                       int set_params, fz_params p, uint32_t chunk)
 {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     for (uint32_t k = i; k < ntiles; k += gridDim.x * blockDim.x) {
@@ -78,6 +78,7 @@ __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint
         ctrl->nnz = ctrl->nd = ctrl->nv = ctrl->total = 0;
         ctrl->dcount = ctrl->vcount = 0;
         ctrl->done = 0;
+        ctrl->chunk = chunk;
         if (set_params) {
             ctrl->p = p;
             set_quant_consts(ctrl);
@@ -1529,8 +1530,9 @@ __device__ __forceinline__ void front_zb(const CompressArgs& a, const QuantP& P,
 #pragma unroll
         for (int u = 0; u < 8; ++u) dv[u] = load1(a, (int64_t)g0 + u);
     }
+    // row halo (the y-1 neighbours of the tile's first row); chunk-local mode (f1) has none
     if (in_halo) zb_fill_halo(P, smem, ra, rmask, in_halo, s - (int64_t)a.hwords, (int)a.hwords);
-    else fill_ring(a, P, smem, ra, rmask, (s - H) & ~(int64_t)3, s);
+    else if (!a.cl) fill_ring(a, P, smem, ra, rmask, (s - H) & ~(int64_t)3, s);
     if (bstart)   // first step of a chunk: the previous plane's tile and halo, once
         fill_ring(a, P, smem, rb, rmask, (s - (int64_t)PL - H) & ~(int64_t)3, s - (int64_t)PL + kTileCodes);
     int qo[8];
@@ -1744,11 +1746,13 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
         uint32_t xm = 0xFFu, ym = 0xFFu;
         {
             const uint32_t x0 = fmod_(pp, a.dnx), nx = a.g.nx;
+            // chunk-local (f1): a tile is one chunk plane, so its first row has no y-1 neighbour
+            const uint32_t yoff = a.cl ? 8u * tid : pp;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const uint32_t xe = x0 + e;
                 if (xe == 0 || xe == nx || xe == 2 * nx) xm &= ~(1u << e);
-                if (pp + e < nx) ym &= ~(1u << e);
+                if (yoff + e < nx) ym &= ~(1u << e);
             }
         }
         uint32_t Dp[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, Dp0 = 0u;
@@ -1778,7 +1782,8 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
             uint32_t xmv, ymv;
             asm volatile("mov.b32 %0, %1;" : "=r"(xmv) : "r"(xm));
             asm volatile("mov.b32 %0, %1;" : "=r"(ymv) : "r"(ym));
-            front_zb(a, P, smem, rmask, 0, RB, t, z == z0 && z > 0, (bits & 1) ? inbuf : nullptr,
+            // chunk-local (f1): items are whole chunks, the z carry starts from zero
+            front_zb(a, P, smem, rmask, 0, RB, t, z == z0 && z > 0 && !a.cl, (bits & 1) ? inbuf : nullptr,
                      (bits & 2) ? inbuf + kTileCodes : nullptr, xmv, ymv, Dp, Dp0, dl, vmask, dv, issue_next);
             tail_zb(a, sh, Obuf, t, (uint32_t)t * kTileCodes + 8u * tid, 0xFFu, dl, vmask);
         }
@@ -1836,10 +1841,13 @@ __device__ void finalize_stream(uint8_t* out, uint64_t out_cap, uint32_t ndim, u
     uint8_t h[128];
     for (int i = 0; i < 128; ++i) h[i] = 0;
     h[0] = 'F'; h[1] = 'Z'; h[2] = 'B'; h[3] = '2';
-    const uint16_t ver = 1, fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u));
+    const uint32_t chunk = ctrl->chunk;
+    const uint16_t ver = 1,
+                   fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u) | (chunk ? 4u : 0u));
     memcpy(h + 4, &ver, 2);
     memcpy(h + 6, &fl, 2);
     h[8] = (uint8_t)ndim;
+    memcpy(h + 10, &chunk, 4);     // f1: chunk depth (u16) and height (u16), zero otherwise
     uint64_t dims[3] = {d0, d1, d2};
     memcpy(h + 16, dims, 24);
     memcpy(h + 40, &n, 8);
@@ -2032,7 +2040,7 @@ bool compress_uses_zb(const CompressArgs& a_in)
 {
     CompressArgs a = a_in;
     if (const char* e = getenv("FZ_EXP")) a.exp = atoi(e);
-    if (a.g.ndim != 3 || (a.exp & (16 | 1024)) || a.rescan || a.tstage == nullptr) return false;
+    if (a.g.ndim != 3 || ((a.exp & (16 | 1024)) && !a.cl) || a.rescan || a.tstage == nullptr) return false;
     if (a.g.P % kTileCodes != 0 || a.base != 0 || a.tile_begin != 0) return false;
     if (a.g.n / a.g.P < 2) return false;
     bool vec = false;
@@ -2051,7 +2059,7 @@ cudaError_t launch_compress_zb(const CompressArgs& a_in, cudaStream_t st)
     plan_smem(a, vec);
     const uint32_t H = a.g.nx + 1;
     const uint32_t hw = (H + 3) & ~3u;
-    a.hwords = hw * 4 <= 8192 ? hw : 0;
+    a.hwords = (hw * 4 <= 8192 && !a.cl) ? hw : 0;
     const size_t sm = sizeof(int) * ((size_t)a.qwords + 32 * 33 + 4) + sizeof(float) * (kTileCodes + (size_t)a.hwords);
     cudaFuncSetAttribute(k_compress_zb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int per_sm = 0;
@@ -2120,7 +2128,7 @@ cudaError_t launch_compress(const CompressArgs& a_in, cudaStream_t st)
 }
 
 cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint32_t ntiles,
-                        const fz_params* p, cudaStream_t st)
+                        const fz_params* p, cudaStream_t st, uint32_t chunk)
 {
     fz_params pp{};
     if (p) pp = *p;
@@ -2128,7 +2136,7 @@ cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uin
     if (grid < 1) grid = 1;
     if (grid > 1024) grid = 1024;
     LaunchProf lp(K_INIT, st);
-    k_init<<<grid, 256, 0, st>>>(ctrl, status, ocnt, ntiles, p ? 1 : 0, pp);
+    k_init<<<grid, 256, 0, st>>>(ctrl, status, ocnt, ntiles, p ? 1 : 0, pp, chunk);
     return cudaGetLastError();
 }
 

@@ -98,8 +98,15 @@ __global__ void k_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, ui
               total <= in_size && nnz <= 256 * T && nd <= n && nv <= n &&
               total == kHeaderBytes + 32 * T + 16 * nnz + 8 * nd + 8 * nv && w > 0.0f && isfinite(w);
     for (uint32_t k = 0; k < 3; ++k) ok = ok && u64(16 + 8 * k) == (k < ndim ? dm[k] : 1);
-    if (!ok) {
+    uint16_t fl;
+    memcpy(&fl, in + 6, 2);
+    if (ok && (fl & 4u)) {   // f1 chunk-local stream: decoded by the blocking entry points only
+        ok = false;
+        ctrl->err = FZ_ERR_ARG;
+    } else if (!ok) {
         ctrl->err = FZ_ERR_CORRUPT;
+    }
+    if (!ok) {
         ctrl->dec_nnz = ctrl->dec_nd = ctrl->dec_nv = 0;
         ctrl->dec_w = 0.0f;
         return;
@@ -116,7 +123,7 @@ __global__ void k_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, 
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t idx = rec[k].x;
-        if (idx >= n || (k > 0 && rec[k - 1].x >= idx)) atomicExch(&ctrl->err, (int)FZ_ERR_CORRUPT);
+        if (idx >= n || (k > 0 && rec[k - 1].x >= idx)) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_CORRUPT);
     }
 }
 
@@ -135,7 +142,7 @@ __global__ void k_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl)
         const uint2* rec = k < nd ? drec : vrec;
         const uint64_t j = k < nd ? k : k - nd;
         const uint32_t idx = rec[j].x;
-        if (idx >= n || (j > 0 && rec[j - 1].x >= idx)) atomicExch(&ctrl->err, (int)FZ_ERR_CORRUPT);
+        if (idx >= n || (j > 0 && rec[j - 1].x >= idx)) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_CORRUPT);
     }
 }
 
@@ -379,7 +386,7 @@ __device__ __forceinline__ uint4 tile_blk(const DecodeArgs& a, const TileIn& in)
     if ((F >> lane) & 1u) {
         const uint64_t bi = in.tbase + wpre + __popc(F & ((1u << lane) - 1u));
         if (bi < (a.dev ? a.ctrl->dec_nnz : a.nnz_total)) blk = __ldcs(reinterpret_cast<const uint4*>(a.payload) + bi);
-        else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
+        else atomicCAS(&a.ctrl->err, 0, (int)FZ_ERR_CORRUPT);
     }
     return blk;
 }
@@ -414,7 +421,7 @@ __device__ __forceinline__ void patch_deltas(const DecodeArgs& a, DecSmem& sm, i
             const uint2 r = drec[k];
             const uint64_t e = (uint64_t)r.x - a.gbase - (uint64_t)s;
             if (e < (uint64_t)kTileCodes) sm.D[e] = (int32_t)r.y;
-            else atomicExch(&a.ctrl->err, (int)FZ_ERR_CORRUPT);
+            else atomicCAS(&a.ctrl->err, 0, (int)FZ_ERR_CORRUPT);
         }
         __syncthreads();
 #pragma unroll
@@ -643,6 +650,125 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
     if (a.yseg == 2 && seg == 0) {
 #pragma unroll
         for (int c = 0; c < C; ++c) a.ycarry[(size_t)z * nx + C * tid + c] = (int32_t)carry[c];
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// f1 chunk-local decode ("highly symmetrical"): with the Lorenzo
+// neighbours confined to chunks of cz planes x one tile (R whole rows), a chunk decodes on
+// its own -- one pass, no carries between CTAs.  CTA = one chunk column (tile position p,
+// planes [z0, z0 + cz)): per plane, gather + un-shuffle + unpack + delta patch + x scan
+// (decode_tile_rows), the y prefix down the tile's R rows from shared memory, the z prefix
+// in registers, then dequantization (D6) and a streaming store of the fp32 values.
+// ------------------------------------------------------------------------------------
+template <int R>
+__global__ void __launch_bounds__(kCta) k_decode_cl(DecodeArgs a, uint32_t cz)
+{
+    resolve_dev(a);
+    constexpr int C = 8 / R;
+    __shared__ DecSmem sm;
+    const int tid = threadIdx.x;
+    const uint32_t nx = a.g.nx, tpp = a.tpp, nz = a.g.n / a.g.P;
+    const uint32_t c = blockIdx.x / tpp, p = blockIdx.x - c * tpp;
+    const uint32_t z0 = c * cz, z1 = min(nz, z0 + cz);
+    const float w = a.wp ? *a.wp : a.w;
+    uint32_t zr[R][C];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int k = 0; k < C; ++k) zr[r][k] = 0u;
+    // two-stage software pipeline down z: payload block of plane z+1, flags/offsets of z+2
+    TileIn in_cur = tile_in(a, z0 * tpp + p);
+    uint4 blk_next = tile_blk(a, in_cur);
+    TileIn in_next = z0 + 1 < z1 ? tile_in(a, (z0 + 1) * tpp + p) : in_cur;
+    for (uint32_t z = z0; z < z1; ++z) {
+        const uint32_t t = z * tpp + p;
+        const int64_t s = (int64_t)t * kTileCodes;
+        const uint4 blk = blk_next;
+        const uint32_t rlo = in_cur.rlo, rhi = in_cur.rhi;
+        if (z + 1 < z1) {
+            blk_next = tile_blk(a, in_next);
+            in_cur = in_next;
+            if (z + 2 < z1) in_next = tile_in(a, t + 2 * tpp);
+        }
+        uint32_t q[8];
+        decode_tile_rows<R>(a, sm, s, blk, rlo, rhi, q);
+        *reinterpret_cast<uint4*>(sm.D + 8 * tid) = make_uint4(q[0], q[1], q[2], q[3]);
+        *reinterpret_cast<uint4*>(sm.D + 8 * tid + 4) = make_uint4(q[4], q[5], q[6], q[7]);
+        __syncthreads();
+        uint32_t ycar[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) ycar[k] = 0u;
+        int32_t* o = a.q_out + s + C * tid;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            uint32_t v[C];
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                ycar[k] += (uint32_t)sm.D[r * nx + C * tid + k];
+                zr[r][k] += ycar[k];
+                v[k] = w > 0.0f ? __float_as_uint(__fmul_rn(__int2float_rn((int32_t)zr[r][k]), w)) : zr[r][k];
+            }
+            if constexpr (C == 1) {
+                __stcs(o + r * nx, (int32_t)v[0]);
+            } else if constexpr (C == 2) {
+                __stcs(reinterpret_cast<int2*>(o + r * nx), make_int2((int)v[0], (int)v[1]));
+            } else {
+#pragma unroll
+                for (int k = 0; k < C; k += 4)
+                    __stcs(reinterpret_cast<int4*>(o + r * nx + k), make_int4((int)v[k], (int)v[k + 1], (int)v[k + 2], (int)v[k + 3]));
+            }
+        }
+        __syncthreads();    // sm.D and sm.Obuf are reused by the next plane
+    }
+}
+
+// Same for short rows (nx < 256, R = 2048 / nx > 8 rows per tile): segmented x scan
+// (decode_tile_x; the tile starts on a row), then thread t takes column x = t % nx, rows
+// 8g .. 8g+7 (g = t / nx): a local prefix down its 8 rows plus the totals of the groups
+// above it (shared memory), and the z prefix of those 8 elements in registers.
+__global__ void __launch_bounds__(kCta) k_decode_cl_short(DecodeArgs a, uint32_t cz)
+{
+    resolve_dev(a);
+    __shared__ DecSmem sm;
+    const int tid = threadIdx.x;
+    const uint32_t nx = a.g.nx, tpp = a.tpp, nz = a.g.n / a.g.P;
+    const uint32_t c = blockIdx.x / tpp, p = blockIdx.x - c * tpp;
+    const uint32_t z0 = c * cz, z1 = min(nz, z0 + cz);
+    const float w = a.wp ? *a.wp : a.w;
+    const uint32_t x = (uint32_t)tid % nx, g = (uint32_t)tid / nx;
+    uint32_t zr[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) zr[i] = 0u;
+    for (uint32_t z = z0; z < z1; ++z) {
+        const uint32_t t = z * tpp + p;
+        const int64_t s = (int64_t)t * kTileCodes;
+        const TileIn in = tile_in(a, t);
+        const uint4 blk = tile_blk(a, in);
+        uint32_t q[8];
+        decode_tile_x<3>(a, sm, t, blk, in.rlo, in.rhi, q);
+        __syncthreads();
+        *reinterpret_cast<uint4*>(sm.D + 8 * tid) = make_uint4(q[0], q[1], q[2], q[3]);
+        *reinterpret_cast<uint4*>(sm.D + 8 * tid + 4) = make_uint4(q[4], q[5], q[6], q[7]);
+        __syncthreads();
+        uint32_t v[8], acc = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            acc += (uint32_t)sm.D[(8 * g + i) * nx + x];
+            v[i] = acc;
+        }
+        sm.Obuf[tid] = acc;
+        __syncthreads();
+        uint32_t pre = 0;
+        for (uint32_t gg = 0; gg < g; ++gg) pre += sm.Obuf[gg * nx + x];
+        int32_t* o = a.q_out + s + (int64_t)(8 * g) * nx + x;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            zr[i] += v[i] + pre;
+            const uint32_t out = w > 0.0f ? __float_as_uint(__fmul_rn(__int2float_rn((int32_t)zr[i]), w)) : zr[i];
+            __stcs(o + (int64_t)i * nx, (int32_t)out);
+        }
+        __syncthreads();    // sm.D / sm.Obuf are reused by the next plane
     }
 }
 
@@ -995,6 +1121,25 @@ cudaError_t launch_decode_tiles(const DecodeArgs& a_in, cudaStream_t st, bool fu
         case 2: return launch_decode_t<2>(a_in, st);
         default: return launch_decode_t<3>(a_in, st);
     }
+}
+
+cudaError_t launch_decode_cl(const DecodeArgs& a_in, uint32_t cz, cudaStream_t st)
+{
+    DecodeArgs a = a_in;
+    a.dnx = make_fastdiv(a.g.nx);
+    a.tpp = (uint32_t)(a.g.P / kTileCodes);
+    const uint32_t nz = a.g.n / a.g.P;
+    const uint64_t ctas = (uint64_t)((nz + cz - 1) / cz) * a.tpp;
+    if (ctas == 0) return cudaSuccess;
+    LaunchProf lp(K_DECODE_PLANES, st);
+    switch (kTileCodes / a.g.nx) {
+        case 1: k_decode_cl<1><<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
+        case 2: k_decode_cl<2><<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
+        case 4: k_decode_cl<4><<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
+        case 8: k_decode_cl<8><<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
+        default: k_decode_cl_short<<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool carries, cudaStream_t st)

@@ -39,6 +39,7 @@ struct Ctrl {
     // decoder, device-driven mode (k_decode_hdr parses the stream header on the device)
     unsigned long long dec_nnz, dec_nd, dec_nv;
     float dec_w;
+    uint32_t chunk;                      // f1 chunk-local stream: cz | cy << 16 (0: field-global)
 };
 static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 
@@ -538,6 +539,7 @@ struct CompressArgs {
     uint64_t n_hdr, T_hdr;    // field size and tiles for the totals / header
     uint4* tstage;            // z-band pass 1: 256-block staging slot per tile (null: not available)
     uint32_t hwords;          // z-band: floats of the TMA-staged row halo (0: quantized from global)
+    uint32_t cl;              // f1 chunk-local Lorenzo (z-band kernel only): chunks of kZbChunk planes x one tile
     int exp;                  // FZ_EXP env var, bit 16: generic kernel instead of the warp-specialized one
 };
 

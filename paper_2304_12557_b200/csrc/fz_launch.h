@@ -28,7 +28,7 @@ struct LaunchProf {
 
 // compression (fz_compress.cu)
 cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint32_t ntiles,
-                        const fz_params* p, cudaStream_t st);
+                        const fz_params* p, cudaStream_t st, uint32_t chunk = 0);
 cudaError_t launch_range(const float* d, uint64_t n, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_params(Ctrl* ctrl, int mode, double eb, uint64_t n, cudaStream_t st);
 cudaError_t launch_compress(const CompressArgs& a, cudaStream_t st);
@@ -100,6 +100,8 @@ cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles,
                                 cudaStream_t st);
 cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st, bool fuse_y = false);
 cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool carries, cudaStream_t st);
+// f1 chunk-local decode (chunks of cz planes x one whole-row tile): one pass, dequantized
+cudaError_t launch_decode_cl(const DecodeArgs& a, uint32_t cz, cudaStream_t st);
 // inclusive prefix sum along an axis of a [outer][L][W] int32 array (mod 2^32); when
 // dequant_w > 0 the final values are written as fl32(fl32(q) * w) floats in place.
 // wp (device, optional) supplies the bin width instead of dequant_w (device-driven decode).

@@ -16,6 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FZ_LIB") or os.path.join(PKG, "libfz.so")  # FZ_LIB: A/B builds
 
 ABS, REL = 0, 1
+CHUNK_LOCAL = 0x100   # f1 chunk-local Lorenzo (fz.h FZ_CHUNK_LOCAL), OR into the mode
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_EB_TOO_SMALL", 4: "ERR_CAPACITY",
           5: "ERR_CORRUPT", 6: "ERR_WORKSPACE", 7: "ERR_CUDA"}
 OK, ERR_ARG, ERR_NONFINITE, ERR_EB_TOO_SMALL, ERR_CAPACITY, ERR_CORRUPT, ERR_WORKSPACE, ERR_CUDA = range(8)

@@ -402,3 +402,65 @@ def test_zband_with_outliers_and_single_kernel_equality(monkeypatch):
     monkeypatch.setenv("FZ_EXP", "1024")            # warp-specialized single kernel instead
     got, _, _ = _gpu_stream(d, O.ABS, eb)
     _assert_stream_equal(got, ref, "single_kernel")
+
+
+# f1 chunk-local Lorenzo: chunks of 16 planes x one whole-row tile,
+# bit-exact against the oracle's chunked compressor and decoder; partial last chunks, every
+# rows-per-tile count R = 2048 / nx, outliers, and each decode entry point.
+CL_SHAPES = [
+    ("c1_64", lambda: synth.generate("sines3d", (64, 64, 64))),
+    ("nz40_r4", lambda: synth.generate("nyx_v", (40, 16, 512))),       # 16 + 16 + 8 planes
+    ("nz33_r16", lambda: synth.generate("hurr_u", (33, 32, 128))),     # 2 tiles per plane
+    ("nz18_r8", lambda: synth.generate("rtm", (18, 16, 256))),
+    ("nz17_r2", lambda: synth.generate("sines3d", (17, 2, 1024))),     # 1 tile per plane
+    ("nz3_r1", lambda: synth.generate("nyx_rho", (3, 1, 2048))),
+]
+
+
+@pytest.mark.parametrize("name,gen", CL_SHAPES, ids=[c[0] for c in CL_SHAPES])
+@pytest.mark.parametrize("rel", [1e-2, 1e-4])
+def test_chunk_local_parity(name, gen, rel):
+    d = gen()
+    st, ref = O.compress_chunked(d, O.REL, rel, 16, 2048 // d.shape[2])
+    assert st == O.OK
+    got, xh, codec = _gpu_stream(d, O.REL | fz.CHUNK_LOCAL, rel)
+    _assert_stream_equal(got, ref, name)
+    st, xref = O.decompress(ref, d.size)
+    assert st == O.OK
+    assert np.array_equal(xh.view(np.uint32), xref.view(np.uint32)), name
+    # decoded from a foreign buffer (blocking header read) and into integer codes
+    buf = torch.from_numpy(ref).to(DEV)
+    x2 = fz.decompress(buf).cpu().numpy().reshape(-1)
+    assert np.array_equal(x2.view(np.uint32), xref.view(np.uint32))
+    st, qref = O.decode_q(ref, d.size)
+    assert np.array_equal(fz.debug_decode_q(buf, d.shape).cpu().numpy().reshape(-1), qref)
+
+
+def test_chunk_local_outliers_async_and_errors():
+    d = synth.generate("nyx_rho", (36, 16, 256)).copy()
+    eb = float(d.max() - d.min()) * 1e-4
+    rng = np.random.default_rng(7)
+    d.reshape(-1)[rng.choice(d.size, 300, replace=False)] += np.float32(80.0) * np.float32(d.max() - d.min())
+    st, ref = O.compress_chunked(d, O.ABS, eb, 16, 8)
+    assert st == O.OK and int.from_bytes(ref[96:104].tobytes(), "little") > 0
+    got, xh, codec = _gpu_stream(d, O.ABS | fz.CHUNK_LOCAL, eb)
+    _assert_stream_equal(got, ref, "cl_outliers")
+    st, xref = O.decompress(ref, d.size)
+    assert np.array_equal(xh.view(np.uint32), xref.view(np.uint32))
+    # asynchronous compress + host-header asynchronous decompress
+    field = torch.from_numpy(d).to(DEV)
+    codec.compress(field, O.ABS | fz.CHUNK_LOCAL, eb, sync=False)
+    size = codec.compress_result()
+    assert size == ref.size
+    assert np.array_equal(codec.out[:size].cpu().numpy(), ref)
+    # the device-parsed asynchronous decoder rejects chunk-local streams
+    buf = torch.from_numpy(ref).to(DEV)
+    codec.decompress_device(buf)
+    with pytest.raises(fz.FZError) as e:
+        codec.result()
+    assert e.value.status == fz.ERR_ARG
+    # shapes without whole-row tiles are refused
+    bad = synth.generate("sines3d", (20, 10, 100))
+    with pytest.raises(fz.FZError) as e:
+        _gpu_stream(bad, O.REL | fz.CHUNK_LOCAL, 1e-3)
+    assert e.value.status == fz.ERR_ARG
