@@ -179,6 +179,68 @@ def cpu_baseline(d: np.ndarray, rel: float):
             "decompress_gbs": round(d.nbytes / (t2 - t1) / 1e9, 6)}, buf
 
 
+def chunk_local_leg(args, gsize, field, flush, stream, rel, d, peak):
+    """f1: the chunk-local Lorenzo mode (FZ_CHUNK_LOCAL) on the same field: asynchronous
+    compress + host-header asynchronous decompress per step (the stream is identical every
+    step, so the header of the first call stays valid), CUDA events, L2 flushed."""
+    import ctypes as C
+    import torch
+    from paper_2304_12557_b200 import fz
+    mode = fz.REL | fz.CHUNK_LOCAL
+    c2 = fz.Codec(tuple(field.shape), field.device)
+    buf, size = c2.compress(field, mode, rel)
+    out = torch.empty_like(field)
+    c2.decompress(buf, out=out)
+    torch.cuda.synchronize()
+    p = fz.peek_header(bytes(c2.hdr))
+    err = float((out.double() - field.double()).abs().max().item())
+    L = fz.lib()
+
+    def dec():
+        st = L.fz_decompress_hdr_async(buf.data_ptr(), size, c2.hdr, out.data_ptr(), c2.n, c2.dwork.data_ptr(),
+                                       c2.dwork.numel(), C.c_void_p(stream.cuda_stream))
+        assert st == 0, st
+
+    for _ in range(3):
+        c2.compress(field, mode, rel, sync=False)
+        dec()
+    torch.cuda.synchronize()
+    fz.profile_enable(True)
+    fz.profile_only(["k_range", "k_compress", "k_compact", "k_decode_planes"])
+    fz.profile_read()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        c2.compress(field, mode, rel, sync=False)
+        ev[k][1].record(stream)
+        dec()
+        ev[k][2].record(stream)
+    torch.cuda.synchronize()
+    assert c2.compress_result() == size
+    c2.result()
+    prof = fz.profile_read()
+    fz.profile_enable(False)
+    ms_c = statistics.mean(ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps))
+    ms_d = statistics.mean(ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps))
+    gb = d.nbytes / 1e9
+    kern = {k: round(v[0] / v[1], 4) for k, v in prof.items()}
+    ab_dec = (size - 128) + 4 * d.size
+    ab_cmp = 4 * d.size + (size - 128)
+    res = {"mode": "FZ_CHUNK_LOCAL, chunks of 16 planes x one tile (2048/nx rows)",
+           "value": round(gb / ((ms_c + ms_d) / 1e3), 3), "unit": "GB/s", "ms_per_step": round(ms_c + ms_d, 4),
+           "compress_gbs": round(gb / (ms_c / 1e3), 2), "decompress_gbs": round(gb / (ms_d / 1e3), 2),
+           "cr": round(d.nbytes / size, 4), "cr_vs_global": round(gsize / size, 4),
+           "max_abs_err": err, "eb_abs": p.params.eb_abs, "kernels_ms": kern}
+    if "k_decode_planes" in kern:
+        a = ab_dec / (kern["k_decode_planes"] / 1e3) / 1e9
+        res["decode_roofline"] = {"kernel": "k_decode_cl", "achieved": round(a, 1), "frac": round(a / peak, 4)}
+    if "k_compress" in kern:
+        a = ab_cmp / (kern["k_compress"] / 1e3) / 1e9
+        res["compress_roofline"] = {"kernel": "k_compress_zb", "achieved": round(a, 1), "frac": round(a / peak, 4)}
+    return res
+
+
 def run_single(args, wl):
     import torch
 
@@ -262,6 +324,9 @@ def run_single(args, wl):
         comp_roof = {"kernel": "k_compress", "achieved": round(abk / (pk / 1e3) / 1e9, 1),
                      "frac": round(abk / (pk / 1e3) / 1e9 / peak, 4), "ms": round(pk, 4)}
 
+    # ---- f1 chunk-local variant: same field, same timing method ----
+    chunk_local = chunk_local_leg(args, stream_bytes, field, flush, stream, rel, d, peak)
+
     # ---- end to end through the public API with HOST buffers (pinned) ----
     # Every step: H2D of the field from pinned memory, fz_compress_host (kernels + D2H of the
     # stream), H2D of the stream back, fz_decompress_host (kernels + D2H of the field).  Two
@@ -343,6 +408,7 @@ def run_single(args, wl):
         "compress_ms": round(ms_c, 4), "decompress_ms": round(ms_d, 4),
         "cr": round(d.nbytes / stream_bytes, 4), "bits_per_value": round(32 * stream_bytes / d.nbytes, 4),
         "roofline": roof, "roofline_compress_kernel": comp_roof, "kernels": kernels,
+        "chunk_local": chunk_local,
         "clocks": sampler.summary(), "gpu_launches": launches,
         "e2e": {"value": round(gb / (ms_e2e / 1e3), 3), "unit": "GB/s", "ms_per_step": round(ms_e2e, 3),
                 "h2d_bytes_per_step": d.nbytes + stream_bytes, "d2h_bytes_per_step": stream_bytes + d.nbytes,
