@@ -34,42 +34,55 @@ with open(os.path.join(prof, f"{rnd}_launches.md"), "w") as f:
             f"({', '.join(sorted(set(k[:40] for k in other)))})\n")
 
 # ---- ncu --set full: key metrics per kernel ----
-raw = subprocess.run(["ncu", "-i", os.path.join(go, "full.ncu-rep"), "--page", "raw", "--csv"],
-                     capture_output=True, text=True).stdout
-rr = list(csv.reader(io.StringIO(raw)))
-hdr, units = rr[0], rr[1]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
-res = collections.OrderedDict()
-for r in rr[2:]:
-    name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
-    d = {}
-    for w in want:
-        if w in hdr:
-            i = hdr.index(w)
-            d[w] = (r[i], units[i])
-    res.setdefault(name, []).append(d)
+
 
 def to_bytes(v, u):
     v = float(v.replace(",", ""))
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
-traffic = {}
-with open(os.path.join(prof, f"{rnd}_ncu_full.md"), "w") as f:
-    f.write(f"# {rnd} ncu --set full (clock-control none), c4 512^3 REL 1e-3 via tools/prof_step.py\n\n")
-    for name, lst in res.items():
-        d = lst[-1]
-        f.write(f"## {name} ({len(lst)} captured launch(es), last shown)\n\n")
-        for k, (v, u) in d.items():
-            f.write(f"- {k}: {v} {u}\n")
-        rd = to_bytes(*d["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in d else 0
-        wr = to_bytes(*d["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in d else 0
-        short = name.split("::")[-1].split("<")[0]
-        traffic[short] = int(rd + wr)
-        f.write(f"- dram traffic per launch: {(rd + wr) / 1e6:.1f} MB\n\n")
+
+def summarize(rep, md, title):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rr[0], rr[1]
+    res = collections.OrderedDict()
+    for r in rr[2:]:
+        name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
+        d = {}
+        for w in want:
+            if w in hdr:
+                i = hdr.index(w)
+                d[w] = (r[i], units[i])
+        res.setdefault(name, []).append(d)
+    traffic = {}
+    with open(md, "w") as f:
+        f.write(title)
+        for name, lst in res.items():
+            d = lst[-1]
+            f.write(f"## {name} ({len(lst)} captured launch(es), last shown)\n\n")
+            for k, (v, u) in d.items():
+                f.write(f"- {k}: {v} {u}\n")
+            rd = to_bytes(*d["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in d else 0
+            wr = to_bytes(*d["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in d else 0
+            short = name.split("::")[-1].split("<")[0]
+            traffic[short] = int(rd + wr)
+            f.write(f"- dram traffic per launch: {(rd + wr) / 1e6:.1f} MB\n\n")
+    return traffic
+
+
+out = {"c4": summarize(os.path.join(go, "full.ncu-rep"), os.path.join(prof, f"{rnd}_ncu_full.md"),
+                       f"# {rnd} ncu --set full (clock-control none), c4 512^3 REL 1e-3 via tools/prof_step.py\n\n")}
+cl = os.path.join(go, "full_cl.ncu-rep")
+if os.path.exists(cl):
+    out["c4_chunk_local"] = summarize(cl, os.path.join(prof, f"{rnd}_ncu_full_cl.md"),
+                                      f"# {rnd} ncu --set full, c4 512^3 REL 1e-3, chunk-local mode (f1), "
+                                      f"tools/prof_step.py (launches after the field-global steps)\n\n")
+out["_source"] = f"profiles/{rnd}_ncu_full*.md (dram__bytes_read.sum + dram__bytes_write.sum)"
 with open(os.path.join(prof, "ncu_traffic.json"), "w") as f:
-    json.dump({"c4": traffic, "_source": f"profiles/{rnd}_ncu_full.md (dram__bytes_read.sum + dram__bytes_write.sum)"}, f, indent=1)
-print(json.dumps(traffic, indent=1))
+    json.dump(out, f, indent=1)
+print(json.dumps(out, indent=1))
