@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
 // in registers, then dequantization (D6) and a streaming store of the fp32 values.
 // ------------------------------------------------------------------------------------
 template <int R>
-__global__ void __launch_bounds__(kCta) k_decode_cl(DecodeArgs a, uint32_t cz)
+__global__ void __launch_bounds__(kCta, 5) k_decode_cl(DecodeArgs a, uint32_t cz)
 {
     resolve_dev(a);
     constexpr int C = 8 / R;
