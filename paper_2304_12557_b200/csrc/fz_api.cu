@@ -881,7 +881,7 @@ fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t sl
     const uint64_t need_lo = tb * kTileCodes > halo ? tb * kTileCodes - halo : 0;
     const uint64_t need_hi = te * kTileCodes < n ? te * kTileCodes : n;
     if (slab_first > need_lo || slab_first + slab_elems < need_hi) return FZ_ERR_ARG;
-    Work W{compress_layout(n, T), static_cast<uint8_t*>(d_work)};
+    Work W{compress_layout(n, T, zb_layout(*global)), static_cast<uint8_t*>(d_work)};
     if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const uint64_t nt = te - tb;

@@ -1690,7 +1690,7 @@ __device__ __forceinline__ void tail_zb(const CompressArgs& a, ZbShared& sh, uin
         const uint64_t fo = (uint64_t)(t - a.tile_begin) * 32 + 4 * warp;
         if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = F;
     }
-    if (nz) a.tstage[(uint64_t)t * kTileBlocks + 32 * warp + __popc(F & ((1u << lane) - 1u))] = blk;
+    if (nz) a.tstage[(uint64_t)(t - a.tile_begin) * kTileBlocks + 32 * warp + __popc(F & ((1u << lane) - 1u))] = blk;
 }
 
 __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
@@ -1704,8 +1704,9 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
     const int RB = (int)a.qstride;
     uint32_t* Obuf = reinterpret_cast<uint32_t*>(smem + a.qwords);              // 32 x 33
     float* inbuf = reinterpret_cast<float*>(smem + a.qwords + 32 * 33 + 4);    // own tile + row halo
-    const uint32_t tpp = a.g.P / kTileCodes, nz = a.g.n / a.g.P;
-    const uint32_t nchunks = (nz + kZbChunk - 1) / kZbChunk, nwork = tpp * nchunks;
+    // planes [zbeg, zend) of this call (a slab's tile range is plane-aligned; see compress_uses_zb)
+    const uint32_t tpp = a.g.P / kTileCodes, zbeg = a.tile_begin / tpp, zend = a.tile_end / tpp;
+    const uint32_t nchunks = (zend - zbeg + kZbChunk - 1) / kZbChunk, nwork = tpp * nchunks;
     if (tid == 0) {
         sh.perr = 0;
         if (a.derive) {
@@ -1738,7 +1739,7 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
         const uint32_t w = sh.item;
         if (w >= nwork) break;
         const uint32_t c = w / tpp, p = w - c * tpp;
-        const uint32_t z0 = c * kZbChunk, z1 = min(nz, z0 + kZbChunk);
+        const uint32_t z0 = zbeg + c * kZbChunk, z1 = min(zend, z0 + kZbChunk);
         // the thread's in-row / in-plane positions are the same in every plane of the column
         const uint32_t pp = p * kTileCodes + 8u * tid;
         // pp + e < P: no plane wrap inside a thread's 8 elements.  nx >= 4, so x0 + e < 3 nx and
@@ -2041,8 +2042,10 @@ bool compress_uses_zb(const CompressArgs& a_in)
     CompressArgs a = a_in;
     if (const char* e = getenv("FZ_EXP")) a.exp = atoi(e);
     if (a.g.ndim != 3 || ((a.exp & (16 | 1024)) && !a.cl) || a.rescan || a.tstage == nullptr) return false;
-    if (a.g.P % kTileCodes != 0 || a.base != 0 || a.tile_begin != 0) return false;
-    if (a.g.n / a.g.P < 2) return false;
+    if (a.g.P % kTileCodes != 0 || a.g.n / a.g.P < 2) return false;
+    // a slab (multi-GPU, SV 8.e) takes it when its tile range is whole planes
+    const uint32_t tpp = a.g.P / kTileCodes;
+    if (a.tile_begin % tpp != 0 || a.tile_end % tpp != 0 || (a.base & 3) != 0) return false;
     bool vec = false;
     plan_smem(a, vec);
     return vec;
@@ -2065,8 +2068,8 @@ cudaError_t launch_compress_zb(const CompressArgs& a_in, cudaStream_t st)
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compress_zb, kCta, sm);
     if (per_sm < 1) per_sm = 1;
-    const uint32_t tpp = a.g.P / kTileCodes, nz = a.g.n / a.g.P;
-    const uint64_t nwork = (uint64_t)tpp * ((nz + kZbChunk - 1) / kZbChunk);
+    const uint32_t tpp = a.g.P / kTileCodes, nzr = (a.tile_end - a.tile_begin) / tpp;
+    const uint64_t nwork = (uint64_t)tpp * ((nzr + kZbChunk - 1) / kZbChunk);
     uint64_t grid = (uint64_t)per_sm * num_sms();
     if (grid > nwork) grid = nwork;
     LaunchProf lp(K_COMPRESS, st);
