@@ -3,7 +3,8 @@
 Runs bench.py (c4 512^3 REL 1e-3, 1 GPU) once per variant, selected by FZ_EXP bits read by
 libfz, and writes profiles/<round>_ablation.md with the step, compress and decompress
 throughput and the per-kernel times:
-  base          warp-specialized fused compressor, plane decoder (x+y fused), 2 CTAs per plane
+  base          z-band compressor (k_compress_zb + k_compact), plane decoder (x+y fused), 2 CTAs per plane
+  ws_comp       FZ_EXP=1024 warp-specialized single-pass compressor (TMA + scanner warp look-back)
   generic_comp  FZ_EXP=16   generic fused compressor (no warp specialization / TMA / scanner warp)
   unfused_dec   FZ_EXP=128  tile decoder (x only) + separate y and z walks
   one_cta_plane FZ_EXP=512  plane decoder with one CTA per plane (no y-carry split)
@@ -14,7 +15,8 @@ import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
 steps = sys.argv[2] if len(sys.argv) > 2 else "10"
-variants = [("base", "0"), ("generic_comp", "16"), ("unfused_dec", "128"), ("one_cta_plane", "512")]
+variants = [("base", "0"), ("ws_comp", "1024"), ("generic_comp", "16"), ("unfused_dec", "128"),
+            ("one_cta_plane", "512")]
 rows = []
 for name, e in variants:
     env = dict(os.environ, FZ_EXP=e)
@@ -24,6 +26,10 @@ for name, e in variants:
     k = {n: round(v["ms_per_launch"] * 1e3, 1) for n, v in line["kernels"].items() if v["ms_per_launch"] > 0.02}
     rows.append((name, e, line["value"], line["ms_per_step"], line["compress_gbs"], line["decompress_gbs"],
                  line.get("parity_vs_oracle"), k))
+    if name == "base" and "chunk_local" in line:
+        c = line["chunk_local"]
+        rows.append(("chunk_local (f1)", "mode flag", c["value"], c["ms_per_step"], c["compress_gbs"],
+                     c["decompress_gbs"], None, {n: round(t * 1e3, 1) for n, t in c["kernels_ms"].items()}))
     print(name, line["value"], line["ms_per_step"], k, flush=True)
 md = [f"# {rnd} ablations (c4 512^3 REL 1e-3, 1 B200, `python tools/ablation.py`)", "",
       "Each variant is `bench.py --steps %s --warmup 3` with the FZ_EXP bits shown (read by libfz)." % steps,
