@@ -225,10 +225,33 @@ def chunk_local_leg(args, gsize, field, flush, stream, rel, d, peak):
     ms_d = statistics.mean(ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps))
     gb = d.nbytes / 1e9
     kern = {k: round(v[0] / v[1], 4) for k, v in prof.items()}
+    # the same step as one CUDA graph (see run_single)
+    gs = torch.cuda.Stream(field.device)
+    gs.wait_stream(stream)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(gs):
+        with torch.cuda.graph(graph, stream=gs):
+            c2.compress(field, mode, rel, sync=False, stream=gs)
+            st = L.fz_decompress_hdr_async(buf.data_ptr(), size, c2.hdr, out.data_ptr(), c2.n,
+                                           c2.dwork.data_ptr(), c2.dwork.numel(), C.c_void_p(gs.cuda_stream))
+            assert st == 0, st
+    torch.cuda.synchronize()
+    gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)
+        gev[k][0].record(stream)
+        graph.replay()
+        gev[k][1].record(stream)
+    torch.cuda.synchronize()
+    assert c2.compress_result() == size
+    c2.result()
+    ms_g = statistics.mean(gev[k][0].elapsed_time(gev[k][1]) for k in range(args.steps))
+    del graph
     ab_dec = (size - 128) + 4 * d.size
     ab_cmp = 4 * d.size + (size - 128)
     res = {"mode": "FZ_CHUNK_LOCAL, chunks of 16 planes x one tile (2048/nx rows)",
-           "value": round(gb / ((ms_c + ms_d) / 1e3), 3), "unit": "GB/s", "ms_per_step": round(ms_c + ms_d, 4),
+           "value": round(gb / (ms_g / 1e3), 3), "unit": "GB/s", "ms_per_step": round(ms_g, 4),
+           "value_stream_launch": round(gb / ((ms_c + ms_d) / 1e3), 3),
            "compress_gbs": round(gb / (ms_c / 1e3), 2), "decompress_gbs": round(gb / (ms_d / 1e3), 2),
            "cr": round(d.nbytes / size, 4), "cr_vs_global": round(gsize / size, 4),
            "max_abs_err": err, "eb_abs": p.params.eb_abs, "kernels_ms": kern}
@@ -291,6 +314,37 @@ def run_single(args, wl):
     codec.result()
     prof = fz.profile_read()
     fz.profile_enable(False)
+
+    # The same step captured once into a CUDA graph (the asynchronous entry points are
+    # device-driven, so the whole compress + decompress is capturable) and replayed: the
+    # kernels are identical, only the launch gaps between them go.  L2 flushed before every
+    # replay, outside the events.
+    gs = torch.cuda.Stream(dev)
+    gs.wait_stream(stream)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(gs):
+        codec.compress(field, fz.REL, rel, sync=False, stream=gs)
+        codec.decompress_device(codec.out, out=xh, stream=gs)   # warm-up on the capture stream
+        gs.synchronize()
+        with torch.cuda.graph(graph, stream=gs):
+            codec.compress(field, fz.REL, rel, sync=False, stream=gs)
+            codec.decompress_device(codec.out, out=xh, stream=gs)
+    torch.cuda.synchronize()
+    gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    sampler2 = ClockSampler(0)
+    with sampler2:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            gev[k][0].record(stream)
+            graph.replay()
+            gev[k][1].record(stream)
+        torch.cuda.synchronize()
+    sampler.samples += sampler2.samples
+    sampler.reasons |= sampler2.reasons
+    assert codec.compress_result() == size
+    codec.result()
+    ms_graph = statistics.mean(gev[k][0].elapsed_time(gev[k][1]) for k in range(args.steps))
+    del graph
     tc = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
     td = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
     ms_c, ms_d = statistics.mean(tc), statistics.mean(td)
@@ -399,8 +453,11 @@ def run_single(args, wl):
         assert np.array_equal(ln.h_x.view(np.uint32), xh.cpu().numpy().view(np.uint32))
 
     line = {
-        "metric": METRIC, "value": round(gb / (ms / 1e3), 3), "unit": "GB/s", "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "metric": METRIC, "value": round(gb / (ms_graph / 1e3), 3), "unit": "GB/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_graph, 4), "higher_is_better": True,
+        "timing": "CUDA-graph replay of one asynchronous compress + decompress step (value); "
+                  "value_stream_launch: the same step launched call by call",
+        "value_stream_launch": round(gb / (ms / 1e3), 3), "ms_per_step_stream_launch": round(ms, 4),
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": desc, "dims": list(shape), "rel_eb": rel, "field_bytes": d.nbytes,
                    "l2": "256 MiB flush before every timed step; field is 4.3x L2", "parallelism": "1 GPU"},
