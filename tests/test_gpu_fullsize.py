@@ -53,3 +53,33 @@ def test_fullsize_parity(cfg, field, shape, rel):
     assert bad == 0, f"{bad} decoded values differ"
     info = fz.peek_header(ref[:128].tobytes())
     assert np.abs(xh.astype(np.float64) - d.reshape(-1)).max() <= info.params.eb_abs
+
+
+# f1 chunk-local mode at the full shapes it applies to (3-D, nx | 2048): c1 and c4, in the
+# launch configuration bench.py's chunk-local leg times.
+CL_CASES = [
+    ("c1", "sines3d", (64, 64, 64), 1e-3),
+    ("c4", "nyx_v", (512, 512, 512), 1e-3),
+    ("c4", "nyx_rho", (512, 512, 512), 1e-4),
+]
+
+
+@pytest.mark.parametrize("cfg,field,shape,rel", CL_CASES, ids=[f"{c[0]}-{c[1]}-{c[3]}" for c in CL_CASES])
+def test_fullsize_chunk_local_parity(cfg, field, shape, rel):
+    d = synth.generate(field, shape)
+    st, ref = O.compress_chunked(d, O.REL, rel, 16, 2048 // shape[2])
+    assert st == O.OK
+    codec = fz.Codec(shape, "cuda:0")
+    x = torch.from_numpy(d).to("cuda:0")
+    buf, size = codec.compress(x, fz.REL | fz.CHUNK_LOCAL, rel)
+    got = buf.cpu().numpy()
+    assert size == ref.size, (size, ref.size)
+    if not np.array_equal(got, ref):
+        first = int(np.nonzero(got != ref)[0][0])
+        raise AssertionError(f"stream differs from the oracle at byte {first} of {size}")
+    del got
+    xh = codec.decompress(buf).cpu().numpy().reshape(-1)
+    del x, buf
+    st, xref = O.decompress(ref, d.size)
+    assert st == O.OK
+    assert np.count_nonzero(xh.view(np.uint32) != xref.view(np.uint32)) == 0
