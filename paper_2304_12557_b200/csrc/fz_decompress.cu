@@ -588,6 +588,21 @@ __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
 // runs the y prefix sum down them with its running column carries in registers, so the y
 // scan costs no extra pass over HBM and no inter-CTA communication.  The z scan follows.
 // ------------------------------------------------------------------------------------
+// C consecutive int32 (or float bits) of one row, streaming store.
+template <int C>
+__device__ __forceinline__ void store_row(int32_t* o, const uint32_t (&v)[C])
+{
+    if constexpr (C == 1) {
+        __stcs(o, (int32_t)v[0]);
+    } else if constexpr (C == 2) {
+        __stcs(reinterpret_cast<int2*>(o), make_int2((int)v[0], (int)v[1]));
+    } else {
+#pragma unroll
+        for (int k = 0; k < C; k += 4)
+            __stcs(reinterpret_cast<int4*>(o + k), make_int4((int)v[k], (int)v[k + 1], (int)v[k + 2], (int)v[k + 3]));
+    }
+}
+
 template <int R>
 __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
 {
@@ -631,18 +646,7 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
         }
         int32_t* o = a.q_out + s + C * tid;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            if constexpr (C == 1) {
-                __stcs(o + r * nx, (int32_t)v[r][0]);
-            } else if constexpr (C == 2) {
-                __stcs(reinterpret_cast<int2*>(o + r * nx), make_int2((int)v[r][0], (int)v[r][1]));
-            } else {
-#pragma unroll
-                for (int c = 0; c < C; c += 4)
-                    __stcs(reinterpret_cast<int4*>(o + r * nx + c),
-                           make_int4((int)v[r][c], (int)v[r][c + 1], (int)v[r][c + 2], (int)v[r][c + 3]));
-            }
-        }
+        for (int r = 0; r < R; ++r, o += nx) store_row<C>(o, v[r]);
         __syncthreads();    // sm.D and sm.Obuf are reused by the next tile
     }
     // lower segment of a split plane: its column totals are the upper segment's y carry,
@@ -699,25 +703,26 @@ __global__ void __launch_bounds__(kCta, 5) k_decode_cl(DecodeArgs a, uint32_t cz
         uint32_t ycar[C];
 #pragma unroll
         for (int k = 0; k < C; ++k) ycar[k] = 0u;
-        int32_t* o = a.q_out + s + C * tid;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            uint32_t v[C];
+        for (int r = 0; r < R; ++r)
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 ycar[k] += (uint32_t)sm.D[r * nx + C * tid + k];
                 zr[r][k] += ycar[k];
-                v[k] = w > 0.0f ? __float_as_uint(__fmul_rn(__int2float_rn((int32_t)zr[r][k]), w)) : zr[r][k];
             }
-            if constexpr (C == 1) {
-                __stcs(o + r * nx, (int32_t)v[0]);
-            } else if constexpr (C == 2) {
-                __stcs(reinterpret_cast<int2*>(o + r * nx), make_int2((int)v[0], (int)v[1]));
-            } else {
+        // D6 (or the integer codes for the decode_q hook), one row pointer stepped by nx
+        int32_t* o = a.q_out + s + C * tid;
+        if (w > 0.0f) {
 #pragma unroll
-                for (int k = 0; k < C; k += 4)
-                    __stcs(reinterpret_cast<int4*>(o + r * nx + k), make_int4((int)v[k], (int)v[k + 1], (int)v[k + 2], (int)v[k + 3]));
+            for (int r = 0; r < R; ++r, o += nx) {
+                uint32_t v[C];
+#pragma unroll
+                for (int k = 0; k < C; ++k) v[k] = __float_as_uint(__fmul_rn(__int2float_rn((int32_t)zr[r][k]), w));
+                store_row<C>(o, v);
             }
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r, o += nx) store_row<C>(o, zr[r]);
         }
         __syncthreads();    // sm.D and sm.Obuf are reused by the next plane
     }
