@@ -241,6 +241,17 @@ fz_status fz_slab_finish(int32_t* d_q, const int32_t* d_carry, const void* d_sta
                          const fz_counts* local, const fz_shape* global, uint64_t tile_begin,
                          uint64_t tile_end, const fz_params* h_params, void* stream);
 
+/* f1 chunk-local slabs ("multi-GPU decode needs no exchange").  OR
+ * FZ_CHUNK_LOCAL into h_params->mode for fz_slab_compress and fz_slab_place (the header then
+ * carries flag bit 2 and the chunk dims); the slab's planes must start on a chunk boundary
+ * (a multiple of 16 planes) and end on one or at nz, on a FZ_CHUNK_LOCAL shape, else
+ * FZ_ERR_ARG.  Such a slab decodes on its own, with no carry from other ranks:
+ *   d_out : the slab's own elements [2048*tile_begin, min(N, 2048*tile_end)) as fp32 x-hat,
+ *           value outliers patched.  d_work as for fz_slab_decode. */
+fz_status fz_slab_decode_cl(const void* d_stage, const fz_counts* local, const fz_shape* global,
+                            uint64_t tile_begin, uint64_t tile_end, const fz_params* h_params,
+                            float* d_out, void* d_work, size_t work_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * Stage hooks for parity tests (north star: codes and outlier lists match the oracle).
  * ------------------------------------------------------------------------------------- */

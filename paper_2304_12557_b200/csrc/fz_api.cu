@@ -153,6 +153,13 @@ uint32_t cl_chunk(const fz_shape& s)
 {
     return kClDepth | (uint32_t)(kTileCodes / s.dims[2]) << 16;
 }
+// a slab of a chunk-local field: whole chunks of planes (the last one may end at nz)
+bool cl_slab(const fz_shape& s, uint64_t n, uint64_t tb, uint64_t te)
+{
+    if (!cl_shape(s)) return false;
+    const uint64_t tpp = s.dims[1] * s.dims[2] / kTileCodes, T = tiles_of(n);
+    return tb % (tpp * kClDepth) == 0 && (te == T || te % (tpp * kClDepth) == 0);
+}
 
 CompressArgs make_args(const Work& W, const float* field, uint64_t base, const Geom& g,
                        uint32_t tb, uint32_t te)
@@ -886,8 +893,14 @@ fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t sl
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const uint64_t nt = te - tb;
     uint8_t* stage = static_cast<uint8_t*>(d_stage);
+    const bool cl = (p->mode & FZ_CHUNK_LOCAL) != 0;
+    if (cl && !cl_slab(*global, n, tb, te)) return FZ_ERR_ARG;
+    fz_params pm = *p;
+    pm.mode &= ~FZ_CHUNK_LOCAL;
+    p = &pm;
 
     CompressArgs a = make_args(W, d_slab, slab_first, g, (uint32_t)tb, (uint32_t)te);
+    a.cl = cl ? 1u : 0u;
     a.flags_out = stage;
     a.flags_cap = stage_cap < 32 * nt ? stage_cap : 32 * nt;
     a.payload_out = stage + 32 * nt;
@@ -936,7 +949,10 @@ fz_status fz_slab_place(const void* d_stage, const fz_shape* global, uint64_t tb
         FZ_CUDA(cudaMemcpyAsync(o + vbase + 8 * before->n_value, s8 + sv, 8 * local->n_value, cudaMemcpyDeviceToDevice, st));
     if (write_header) {
         uint8_t h[128];
-        write_header_host(h, *global, n, T, *p, *totals, total);
+        const bool cl = (p->mode & FZ_CHUNK_LOCAL) != 0;
+        fz_params pm = *p;
+        pm.mode &= ~FZ_CHUNK_LOCAL;
+        write_header_host(h, *global, n, T, pm, *totals, total, cl ? cl_chunk(*global) : 0u);
         FZ_CUDA(cudaMemcpyAsync(o, h, 128, cudaMemcpyHostToDevice, st));
     }
     FZ_CUDA(cudaStreamSynchronize(st));
@@ -1067,6 +1083,58 @@ fz_status fz_slab_decode(const void* d_stage, const fz_counts* local, const fz_s
                                  reinterpret_cast<uint32_t*>(wb + L.sums), 0.0f, st));
     if (sg.local.ndim >= 2) FZ_CUDA(launch_axis_sum(d_q, sg.L, sg.W, d_agg, st));
     else FZ_CUDA(cudaMemcpyAsync(d_agg, d_q + (sg.n - 1), 4, cudaMemcpyDeviceToDevice, st));
+    Ctrl h;
+    FZ_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    FZ_CUDA(cudaStreamSynchronize(st));
+    if (h.err != 0) return err_status(h.err);
+    if (h.nnz != local->nnz) return FZ_ERR_CORRUPT;
+    return FZ_OK;
+}
+
+fz_status fz_slab_decode_cl(const void* d_stage, const fz_counts* local, const fz_shape* global, uint64_t tb,
+                            uint64_t te, const fz_params* p, float* d_out, void* d_work, size_t work_bytes,
+                            void* stream)
+{
+    LaunchScope ls;
+    SlabGeo sg;
+    uint64_t n;
+    if (d_stage == nullptr || local == nullptr || p == nullptr || d_out == nullptr || d_work == nullptr ||
+        !aligned16(d_stage) || !aligned16(d_out) || !aligned16(d_work) || !shape_n(global, &n))
+        return FZ_ERR_ARG;
+    if (!cl_slab(*global, n, tb, te)) return FZ_ERR_ARG;
+    fz_status rs = slab_geo(global, tb, te, &sg);
+    if (rs != FZ_OK) return rs;
+    const DecodeLayout L = decode_layout(sg.local);
+    if (work_bytes < L.total) return FZ_ERR_WORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* wb = static_cast<uint8_t*>(d_work);
+    Ctrl* ctrl = reinterpret_cast<Ctrl*>(wb + L.ctrl);
+    const uint64_t nt = te - tb;
+    const uint8_t* in = static_cast<const uint8_t*>(d_stage);
+    const uint64_t pbase = 32 * nt, dbase = pbase + 16 * local->nnz, vbase = dbase + 8 * local->n_delta;
+    FZ_CUDA(launch_decode_init(ctrl, st));
+    FZ_CUDA(launch_tile_offsets(in, (uint32_t)nt, reinterpret_cast<uint32_t*>(wb + L.loc),
+                                reinterpret_cast<uint32_t*>(wb + L.bsum), ctrl, st, local->nnz));
+    FZ_CUDA(launch_record_tiles(reinterpret_cast<const uint2*>(in + dbase), local->n_delta, (uint32_t)nt, sg.g0,
+                                reinterpret_cast<uint32_t*>(wb + L.drange), st));
+    DecodeArgs a{};
+    a.flags = in;
+    a.payload = in + pbase;
+    a.drec = reinterpret_cast<const uint2*>(in + dbase);
+    a.drange = reinterpret_cast<const uint32_t*>(wb + L.drange);
+    a.nnz_total = local->nnz;
+    a.nd = local->n_delta;
+    a.g = geom_of(sg.local, sg.n);
+    a.tiles = (uint32_t)nt;
+    a.w = p->w;
+    a.q_out = reinterpret_cast<int32_t*>(d_out);
+    a.gbase = sg.g0;
+    a.loc = reinterpret_cast<const uint32_t*>(wb + L.loc);
+    a.bpre = reinterpret_cast<const uint32_t*>(wb + L.bsum);
+    a.ctrl = ctrl;
+    // the slab starts on a chunk boundary, so its local chunks are the global ones
+    FZ_CUDA(launch_decode_cl(a, kClDepth, st));
+    FZ_CUDA(launch_value_patch(d_out, reinterpret_cast<const uint2*>(in + vbase), local->n_value, sg.n, st, sg.g0));
     Ctrl h;
     FZ_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     FZ_CUDA(cudaStreamSynchronize(st));

@@ -53,9 +53,10 @@ def geometry(dims):
     return n, nx, P, halo
 
 
-def plan(dims, world: int, rank: int) -> SlabPlan:
+def plan(dims, world: int, rank: int, chunk: int = 1) -> SlabPlan:
     """Tile-aligned z-slabs: rank k starts at the tile containing plane floor(k*nz/world)
-    (plane-aligned whenever P % 2048 == 0)."""
+    (plane-aligned whenever P % 2048 == 0).  chunk > 1 (f1 chunk-local streams): slabs are
+    whole chunks of `chunk` planes, rank k starting at chunk floor(k * nchunks / world)."""
     dims = tuple(int(x) for x in dims)
     n, nx, P, halo = geometry(dims)
     T = -(-n // TILE)
@@ -64,7 +65,10 @@ def plan(dims, world: int, rank: int) -> SlabPlan:
         if k >= world:
             return T
         if len(dims) == 3:
-            z = k * dims[0] // world
+            if chunk > 1:
+                z = (k * (-(-dims[0] // chunk)) // world) * chunk
+            else:
+                z = k * dims[0] // world
             return (z * P) // TILE
         return (k * T) // world
 
@@ -243,5 +247,45 @@ def roundtrip_sharded_single_process(d: np.ndarray, mode, eb, ranks: int, device
         fz.slab_carry(aggs, k, E, carry)
         c.finish(q, carry, cnt, params)
         xhat[p.own_lo: p.own_hi] = q.view(torch.float32).cpu().numpy()
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), xhat
+
+
+def roundtrip_chunk_local_single_process(d: np.ndarray, mode, eb, ranks: int, device="cuda:0"):
+    """f1: the k-rank slab protocol for a chunk-local stream, sequentially on one GPU.  The
+    compress side is the usual one (range exchange, counts exchange, placement); the decode
+    side needs no exchange at all -- each rank decodes its whole chunks on its own
+    (fz_slab_decode_cl).  Returns (stream bytes, decompressed field)."""
+    import torch
+
+    from . import fz
+    dims = d.shape
+    flat = np.ascontiguousarray(d).reshape(-1)
+    plans = [p for p in (plan(dims, ranks, k, chunk=16) for k in range(ranks)) if p.te > p.tb]
+    comps, slabs, mins, maxs = [], [], [], []
+    for p in plans:
+        slab = torch.from_numpy(flat[p.slab_first: p.slab_hi].copy()).to(device)
+        c = SlabCompressor(dims, p, device)
+        mn, mx = c.local_range(slab)
+        mins.append(mn)
+        maxs.append(mx)
+        comps.append(c)
+        slabs.append(slab)
+    params = fz.derive_params(*combine_ranges(mins, maxs), mode, eb)
+    params.mode |= fz.CHUNK_LOCAL
+    counts = [c.compress_local(s, params) for c, s in zip(comps, slabs)]
+    before, totals = prefix_counts([(c.nnz, c.n_delta, c.n_value) for c in counts])
+    T = plans[0].tiles
+    out = torch.zeros(128 + 32 * T + 16 * totals[0] + 8 * totals[1] + 8 * totals[2], dtype=torch.uint8,
+                      device=device)
+    for c, cnt, b in zip(comps, counts, before):
+        c.place(cnt, b, totals, params, out)
+    xhat = np.empty(flat.size, dtype=np.float32)
+    for c, cnt, p in zip(comps, counts, plans):
+        local_dims = (int((p.own_hi - p.own_lo) // (dims[1] * dims[2])),) + tuple(dims[1:])
+        dwork = torch.empty(max(16, fz.decompress_workspace_bytes(local_dims)), dtype=torch.uint8, device=device)
+        x = torch.empty(p.own_hi - p.own_lo, dtype=torch.float32, device=device)
+        fz.slab_decode_cl(c.stage, cnt, dims, p.tb, p.te, params, x, dwork)
+        xhat[p.own_lo: p.own_hi] = x.cpu().numpy()
     torch.cuda.synchronize()
     return out.cpu().numpy(), xhat

@@ -99,6 +99,7 @@ def lib():
         "fz_slab_decode": ([P, pC, pS, u64, u64, P, P, P, S, P], i),
         "fz_slab_carry": ([P, C.c_uint32, u64, P, P], i),
         "fz_slab_finish": ([P, P, P, pC, pS, u64, u64, pP, P], i),
+        "fz_slab_decode_cl": ([P, pC, pS, u64, u64, pP, P, P, S, P], i),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -403,6 +404,13 @@ def slab_decode(stage, counts: Counts, dims, tb, te, q, agg, work, stream=None):
     st = lib().fz_slab_decode(_ptr(stage), C.byref(counts), C.byref(make_shape(dims)), tb, te, _ptr(q), _ptr(agg),
                               _ptr(work), work.numel(), _stream(stream))
     _check(st, "fz_slab_decode")
+
+
+def slab_decode_cl(stage, counts: Counts, dims, tb, te, params: Params, out, work, stream=None):
+    """f1: decode a chunk-local slab on its own (no carry from other ranks) into fp32 `out`."""
+    st = lib().fz_slab_decode_cl(_ptr(stage), C.byref(counts), C.byref(make_shape(dims)), tb, te, C.byref(params),
+                                 _ptr(out), _ptr(work), work.numel(), _stream(stream))
+    _check(st, "fz_slab_decode_cl")
 
 
 def slab_carry(aggs, nbefore: int, elems: int, carry, stream=None):

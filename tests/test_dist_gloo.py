@@ -81,3 +81,19 @@ def test_slab_plans_partition_and_halo(dims, world):
 def test_prefix_counts():
     before, totals = fzd.prefix_counts([(3, 1, 0), (0, 0, 0), (5, 2, 7)])
     assert before == [(0, 0, 0), (3, 1, 0), (3, 1, 0)] and totals == (8, 3, 7)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5, 8])
+def test_chunk_aligned_plan(world):
+    """f1: chunk-local slabs are whole chunks of 16 planes, cover every tile once, in order."""
+    from paper_2304_12557_b200 import dist
+    dims = (100, 64, 128)
+    P = dims[1] * dims[2]
+    plans = [dist.plan(dims, world, k, chunk=16) for k in range(world)]
+    assert plans[0].tb == 0 and plans[-1].te == plans[0].tiles
+    for a, b in zip(plans, plans[1:]):
+        assert a.te == b.tb
+    for p in plans:
+        if p.te > p.tb:
+            assert (p.tb * 2048) % (16 * P) == 0
+            assert p.te == p.tiles or (p.te * 2048) % (16 * P) == 0

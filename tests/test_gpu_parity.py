@@ -464,3 +464,18 @@ def test_chunk_local_outliers_async_and_errors():
     with pytest.raises(fz.FZError) as e:
         _gpu_stream(bad, O.REL | fz.CHUNK_LOCAL, 1e-3)
     assert e.value.status == fz.ERR_ARG
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 3, 4])
+def test_chunk_local_multirank_no_exchange_decode(ranks):
+    """f1 across ranks: chunk-aligned slabs compress to the oracle's chunk-local stream byte
+    for byte, and every rank decodes its slab alone (no carry exchange), bit-exact."""
+    from paper_2304_12557_b200 import dist
+    d = synth.generate("nyx_v", (64, 32, 128))
+    st, ref = O.compress_chunked(d, O.REL, 1e-3, 16, 2048 // 128)
+    assert st == O.OK
+    out, xh = dist.roundtrip_chunk_local_single_process(d, fz.REL, 1e-3, ranks, DEV)
+    _assert_stream_equal(out, ref, f"cl ranks={ranks}")
+    st, xref = O.decompress(ref, d.size)
+    assert np.array_equal(xh.view(np.uint32), xref.view(np.uint32))
+
