@@ -557,7 +557,13 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     if (fuse_y) {
         a.tpp = (uint32_t)(I.shape.dims[1] * I.shape.dims[2] / kTileCodes);
         // two CTAs per plane unless the planes alone fill the GPU several times over
-        a.yseg = (a.tpp % 2 == 0 && I.shape.dims[0] < 4 * 148 && !(exp_bits() & 512)) ? 2 : 1;
+        // several CTAs per plane (shorter tile chains) unless the planes alone fill the GPU
+        a.yseg = 1;
+        if (I.shape.dims[0] < 4 * 148 && !(exp_bits() & 512)) {
+            const uint32_t want = (exp_bits() & 4096) ? 2u : kMaxYseg;
+            for (uint32_t y = want; y >= 2; y /= 2)
+                if (a.tpp % y == 0) { a.yseg = y; break; }
+        }
         a.ycarry = reinterpret_cast<int32_t*>(wb + L.ycarry);
     }
     if (chunk != 0) {
@@ -587,9 +593,9 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     } else if (I.shape.ndim == 3) {
         if (!fuse_y)
             FZ_CUDA(launch_scan_axis(q, I.shape.dims[0], I.shape.dims[1], I.shape.dims[2], sums, 0.0f, st));
-        if (fuse_y && a.yseg == 2)
+        if (fuse_y && a.yseg >= 2)
             FZ_CUDA(launch_zwalk_ycarry(q, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], wq, a.ycarry,
-                                        (uint32_t)I.shape.dims[2], st, wp));
+                                        (uint32_t)I.shape.dims[2], a.yseg, st, wp));
         else
             FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], sums, wq, st, wp));
     }

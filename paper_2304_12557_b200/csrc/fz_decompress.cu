@@ -56,7 +56,7 @@ DecodeLayout decode_layout(const fz_shape& s)
     L.xbagg = off;  off = al(off + 8 * nb);
     L.sums = off;   off = al(off + 4 * sums);
     L.drange = off; off = al(off + 4 * (T + 1));
-    L.ycarry = off; off = al(off + (decode_fuses_y(s) ? 4 * nz * nx : 0));
+    L.ycarry = off; off = al(off + (decode_fuses_y(s) ? 4 * kMaxYseg * nz * nx : 0));
     L.sums_elems = sums;
     L.total = off;
     return L;
@@ -649,11 +649,12 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
         for (int r = 0; r < R; ++r, o += nx) store_row<C>(o, v[r]);
         __syncthreads();    // sm.D and sm.Obuf are reused by the next tile
     }
-    // lower segment of a split plane: its column totals are the upper segment's y carry,
-    // added by the z walk
-    if (a.yseg == 2 && seg == 0) {
+    // a plane split into yseg segments (CTAs): every segment but the last leaves its column
+    // totals; k_yprefix turns them into inclusive prefixes, the y carries the z walk adds to
+    // the rows of the segments below
+    if (seg + 1 < a.yseg) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) a.ycarry[(size_t)z * nx + C * tid + c] = (int32_t)carry[c];
+        for (int c = 0; c < C; ++c) a.ycarry[((size_t)z * a.yseg + seg) * nx + C * tid + c] = (int32_t)carry[c];
     }
 }
 
@@ -898,12 +899,14 @@ __global__ void __launch_bounds__(256) k_scan_walk(int32_t* v, uint64_t outer, u
 
 // Vector walk: V adjacent columns per thread (W % V == 0, rows 16-byte aligned for V = 4),
 // U rows in flight; same arithmetic as k_scan_walk.
-// ycarry (optional): columns w >= W/2 of step l also add ycarry[l * ynx + w % ynx] (the y carry
+// ycarry (optional): a column w in plane segment g = (w / ynx) / yrows > 0 also adds
+// ycarry[(l * ys + g - 1) * ynx + w % ynx] at step l (the y carry
 // of the upper half of a plane decoded as two segments by k_decode_planes).
 template <int V, int U>
 __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer, uint64_t L, uint64_t W,
                                                      float dequant_w_in, const int32_t* __restrict__ carry,
                                                      const int32_t* __restrict__ ycarry, uint32_t ynx,
+                                                     uint32_t yrows, uint32_t ys,
                                                      const float* wp)
 {
     const float dequant_w = wp ? *wp : dequant_w_in;
@@ -926,7 +929,9 @@ __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer,
         if constexpr (V == 4) __stcs(reinterpret_cast<int4*>(q), make_int4((int)y[0], (int)y[1], (int)y[2], (int)y[3]));
         else __stcs(reinterpret_cast<int2*>(q), make_int2((int)y[0], (int)y[1]));
     };
-    const int32_t* yc = (ycarry != nullptr && w >= W / 2) ? ycarry + w % ynx : nullptr;
+    const uint32_t yg = ycarry != nullptr ? (uint32_t)(w / ynx) / yrows : 0u;
+    const int32_t* yc = yg > 0 ? ycarry + (size_t)(yg - 1) * ynx + w % ynx : nullptr;
+    const uint64_t ystride = (uint64_t)ys * ynx;
     uint64_t l = 0;
     for (; l + U <= L; l += U) {
         VT x[U];
@@ -935,7 +940,7 @@ __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer,
         if (yc != nullptr) {
 #pragma unroll
             for (int k = 0; k < U; ++k) {
-                const VT c = __ldg(reinterpret_cast<const VT*>(yc + (l + k) * ynx));
+                const VT c = __ldg(reinterpret_cast<const VT*>(yc + (l + k) * ystride));
                 if constexpr (V == 4) { x[k].x += c.x; x[k].y += c.y; x[k].z += c.z; x[k].w += c.w; }
                 else { x[k].x += c.x; x[k].y += c.y; }
             }
@@ -952,7 +957,7 @@ __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer,
     for (; l < L; ++l, p += W) {
         VT x = *reinterpret_cast<const VT*>(p);
         if (yc != nullptr) {
-            const VT c = __ldg(reinterpret_cast<const VT*>(yc + l * ynx));
+            const VT c = __ldg(reinterpret_cast<const VT*>(yc + l * ystride));
             if constexpr (V == 4) { x.x += c.x; x.y += c.y; x.z += c.z; x.w += c.w; }
             else { x.x += c.x; x.y += c.y; }
         }
@@ -1189,10 +1194,10 @@ static void launch_walk(int32_t* data, uint64_t outer, uint64_t L, uint64_t W, f
     const bool a16 = (reinterpret_cast<uintptr_t>(data) & 15) == 0;
     if (m != 3 && W % 4 == 0 && a16 && m != 1) {
         const uint64_t thr = outer * W / 4;
-        k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx, wp);
+        k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx, 1u, 1u, wp);
     } else if (m != 3 && W % 2 == 0 && a16) {
         const uint64_t thr = outer * W / 2;
-        k_scan_walk_v<2, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx, wp);
+        k_scan_walk_v<2, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx, 1u, 1u, wp);
     } else {
         k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, wp);
     }
@@ -1246,13 +1251,32 @@ cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t el
     return cudaGetLastError();
 }
 
-cudaError_t launch_zwalk_ycarry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* ycarry, uint32_t nx,
-                               cudaStream_t st, const float* wp)
+// in place: the segments' column totals -> inclusive prefixes over the segments of a plane
+__global__ void k_yprefix(int32_t* ycarry, uint64_t nz, uint32_t nx, uint32_t ys)
 {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nz * nx) return;
+    const uint64_t z = i / nx, x = i - z * nx;
+    int32_t* p = ycarry + z * ys * nx + x;
+    uint32_t acc = (uint32_t)p[0];
+    for (uint32_t g = 1; g + 1 < ys; ++g) {
+        acc += (uint32_t)p[(size_t)g * nx];
+        p[(size_t)g * nx] = (int32_t)acc;
+    }
+}
+
+cudaError_t launch_zwalk_ycarry(int32_t* data, uint64_t L, uint64_t W, float w, int32_t* ycarry, uint32_t nx,
+                               uint32_t ys, cudaStream_t st, const float* wp)
+{
+    if (ys > 2) {
+        LaunchProf lp(K_OFFSETS, st);
+        k_yprefix<<<(unsigned)((L * nx + 255) / 256), 256, 0, st>>>(ycarry, L, nx, ys);
+    }
     LaunchProf lp(K_SCAN_WALK, st);
     if (W % 4 != 0 || (reinterpret_cast<uintptr_t>(data) & 15) != 0) return cudaErrorInvalidValue;
     const uint64_t thr = W / 4;
-    k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, 1, L, W, w, nullptr, ycarry, nx, wp);
+    k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, 1, L, W, w, nullptr, ycarry, nx,
+                                                                        (uint32_t)(W / nx / ys), ys, wp);
     return cudaGetLastError();
 }
 

@@ -78,6 +78,7 @@ struct DecodeArgs {
 // one plane and there are enough planes to fill the GPU.
 bool decode_fuses_y(const fz_shape& s);
 
+constexpr uint32_t kMaxYseg = 4;   // plane segments (CTAs) per plane in k_decode_planes
 struct DecodeLayout {
     size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, drange, ycarry, total;
     uint64_t sums_elems;
@@ -112,8 +113,8 @@ cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint
 cudaError_t launch_axis_sum(const int32_t* v, uint64_t L, uint64_t W, int32_t* agg, cudaStream_t st);
 cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t elems, int32_t* carry,
                               cudaStream_t st);
-cudaError_t launch_zwalk_ycarry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* ycarry, uint32_t nx,
-                               cudaStream_t st, const float* wp = nullptr);
+cudaError_t launch_zwalk_ycarry(int32_t* data, uint64_t L, uint64_t W, float w, int32_t* ycarry, uint32_t nx,
+                               uint32_t ys, cudaStream_t st, const float* wp = nullptr);
 cudaError_t launch_walk_carry(int32_t* data, uint64_t L, uint64_t W, float w, const int32_t* carry,
                               cudaStream_t st);
 cudaError_t launch_add_dequant(int32_t* q, uint64_t n, const int32_t* carry, float w, cudaStream_t st);

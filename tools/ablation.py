@@ -8,6 +8,7 @@ throughput and the per-kernel times:
   generic_comp  FZ_EXP=16   generic fused compressor (no warp specialization / TMA / scanner warp)
   unfused_dec   FZ_EXP=128  tile decoder (x only) + separate y and z walks
   one_cta_plane FZ_EXP=512  plane decoder with one CTA per plane (no y-carry split)
+  two_seg_plane FZ_EXP=4096 plane decoder with two CTAs per plane (default: four)
 Usage (GPU box): python tools/ablation.py [round] [steps]
 """
 import json, os, subprocess, sys
@@ -16,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
 steps = sys.argv[2] if len(sys.argv) > 2 else "10"
 variants = [("base", "0"), ("ws_comp", "1024"), ("generic_comp", "16"), ("unfused_dec", "128"),
-            ("one_cta_plane", "512")]
+            ("one_cta_plane", "512"), ("two_seg_plane", "4096")]
 rows = []
 for name, e in variants:
     env = dict(os.environ, FZ_EXP=e)
