@@ -78,7 +78,7 @@ struct DecodeArgs {
 // one plane and there are enough planes to fill the GPU.
 bool decode_fuses_y(const fz_shape& s);
 
-constexpr uint32_t kMaxYseg = 4;   // plane segments (CTAs) per plane in k_decode_planes
+constexpr uint32_t kMaxYseg = 8;   // plane segments (CTAs) per plane in k_decode_planes
 struct DecodeLayout {
     size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, drange, ycarry, total;
     uint64_t sums_elems;

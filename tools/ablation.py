@@ -8,7 +8,7 @@ throughput and the per-kernel times:
   generic_comp  FZ_EXP=16   generic fused compressor (no warp specialization / TMA / scanner warp)
   unfused_dec   FZ_EXP=128  tile decoder (x only) + separate y and z walks
   one_cta_plane FZ_EXP=512  plane decoder with one CTA per plane (no y-carry split)
-  two_seg_plane FZ_EXP=4096 plane decoder with two CTAs per plane (default: four)
+  two_seg_plane FZ_EXP=4096 plane decoder with two CTAs per plane (default: eight)
 Usage (GPU box): python tools/ablation.py [round] [steps]
 """
 import json, os, subprocess, sys
