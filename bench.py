@@ -378,6 +378,34 @@ def run_single(args, wl):
         comp_roof = {"kernel": "k_compress", "achieved": round(abk / (pk / 1e3) / 1e9, 1),
                      "frac": round(abk / (pk / 1e3) / 1e9 / peak, 4), "ms": round(pk, 4)}
 
+    # ---- the other REL bounds of SV 8.d on the same field (CR and throughput, same method) ----
+    by_rel = {}
+    for r2 in (1e-2, 1e-4):
+        for _ in range(3):
+            b2, _ = codec.compress(field, fz.REL, r2, sync=False)
+            codec.decompress_device(b2, out=xh)
+        ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(5)]
+        for k in range(5):
+            flush.fill_(k & 0xFF)
+            ev2[k][0].record(stream)
+            codec.compress(field, fz.REL, r2, sync=False)
+            ev2[k][1].record(stream)
+            codec.decompress_device(codec.out, out=xh)
+            ev2[k][2].record(stream)
+        torch.cuda.synchronize()
+        sz2 = codec.compress_result()
+        codec.result()
+        mc = statistics.mean(e[0].elapsed_time(e[1]) for e in ev2)
+        md = statistics.mean(e[1].elapsed_time(e[2]) for e in ev2)
+        by_rel[f"{r2:g}"] = {"cr": round(d.nbytes / sz2, 4), "compress_gbs": round(gb / (mc / 1e3), 2),
+                             "decompress_gbs": round(gb / (md / 1e3), 2),
+                             "step_gbs": round(gb / ((mc + md) / 1e3), 2)}
+    # restore the REL 1e-3 stream and field (checked below against the e2e lanes and the oracle)
+    codec.compress(field, fz.REL, rel, sync=False)
+    codec.decompress_device(codec.out, out=xh)
+    assert codec.compress_result() == stream_bytes
+    codec.result()
+
     # ---- f1 chunk-local variant: same field, same timing method ----
     chunk_local = chunk_local_leg(args, stream_bytes, field, flush, stream, rel, d, peak)
 
@@ -466,6 +494,7 @@ def run_single(args, wl):
         "cr": round(d.nbytes / stream_bytes, 4), "bits_per_value": round(32 * stream_bytes / d.nbytes, 4),
         "roofline": roof, "roofline_compress_kernel": comp_roof, "kernels": kernels,
         "chunk_local": chunk_local,
+        "by_rel": by_rel,
         "clocks": sampler.summary(), "gpu_launches": launches,
         "e2e": {"value": round(gb / (ms_e2e / 1e3), 3), "unit": "GB/s", "ms_per_step": round(ms_e2e, 3),
                 "h2d_bytes_per_step": d.nbytes + stream_bytes, "d2h_bytes_per_step": stream_bytes + d.nbytes,
