@@ -16,6 +16,16 @@ import statistics
 import numpy as np
 
 
+def _clock_sampler(index: int):
+    """bench.py's NVML sampler (SM clock + throttle reasons during the timed region)."""
+    import importlib
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    return importlib.import_module("bench").ClockSampler(index)
+
+
 def run(args, wl, metric):
     import torch
     import torch.distributed as tdist
@@ -25,9 +35,17 @@ def run(args, wl, metric):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FZ_DIST_BACKEND=gloo: a functional check of the multi-rank path with several ranks
+    # sharing one GPU (collectives through host memory); the bench itself runs NCCL.
+    backend = os.environ.get("FZ_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    tdist.init_process_group("nccl", device_id=dev)
+    if backend == "nccl":
+        tdist.init_process_group("nccl", device_id=dev)
+    else:
+        tdist.init_process_group(backend)
+    xdev = dev if backend == "nccl" else torch.device("cpu")
     field_name, shape, rel, desc = wl
     d = synth.generate(field_name, shape)
     flat = d.reshape(-1)
@@ -49,12 +67,12 @@ def run(args, wl, metric):
         nonlocal out
         mn, mx = comp.local_range(slab)
         launches[0] += fz.last_launch_count()
-        gmn, gmx = dist.exchange_range(mn, mx, device=dev)
+        gmn, gmx = dist.exchange_range(mn, mx, device=xdev)
         params = fz.derive_params(gmn, gmx, fz.REL, rel)
         last_params[0] = params
         counts = comp.compress_local(slab, params)
         launches[0] += fz.last_launch_count()
-        before_all, totals = dist.exchange_counts((counts.nnz, counts.n_delta, counts.n_value), device=dev)
+        before_all, totals = dist.exchange_counts((counts.nnz, counts.n_delta, counts.n_value), device=xdev)
         before = before_all[rank]
         total = 128 + 32 * pl.tiles + 16 * totals[0] + 8 * totals[1] + 8 * totals[2]
         if out is None or out.numel() < total:
@@ -62,7 +80,7 @@ def run(args, wl, metric):
         comp.place(counts, before, totals, params, out)
         comp.decode_local(counts, q, agg, dwork)
         launches[0] += fz.last_launch_count()
-        aggs = dist.exchange_planes(agg)
+        aggs = dist.exchange_planes(agg.to(xdev)).to(dev)
         fz.slab_carry(aggs, rank, E, carry)
         launches[0] += fz.last_launch_count()
         comp.finish(q, carry, counts, params)
@@ -79,19 +97,21 @@ def run(args, wl, metric):
     torch.cuda.synchronize()
     times = []
     launches[0] = 0
-    for _ in range(args.steps):
-        tdist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        total = step()
-        e1.record()
-        torch.cuda.synchronize()
-        tdist.barrier()
-        times.append(e0.elapsed_time(e1))
+    sampler = _clock_sampler(local)
+    with sampler:
+        for _ in range(args.steps):
+            tdist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            total = step()
+            e1.record()
+            torch.cuda.synchronize()
+            tdist.barrier()
+            times.append(e0.elapsed_time(e1))
     if os.environ.get("FZ_DIST_DEBUG"):
         print(f"rank {rank} step ms {[round(x, 3) for x in times]}", flush=True)
-    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=xdev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
 
@@ -107,17 +127,17 @@ def run(args, wl, metric):
     def step_e2e():
         slab.copy_(h_slab, non_blocking=True)
         mn, mx = comp.local_range(slab)
-        gmn, gmx = dist.exchange_range(mn, mx, device=dev)
+        gmn, gmx = dist.exchange_range(mn, mx, device=xdev)
         params = fz.derive_params(gmn, gmx, fz.REL, rel)
         counts = comp.compress_local(slab, params)
-        before_all, totals = dist.exchange_counts((counts.nnz, counts.n_delta, counts.n_value), device=dev)
+        before_all, totals = dist.exchange_counts((counts.nnz, counts.n_delta, counts.n_value), device=xdev)
         total = 128 + 32 * pl.tiles + 16 * totals[0] + 8 * totals[1] + 8 * totals[2]
         comp.place(counts, before_all[rank], totals, params, out)
         sb = 32 * (pl.te - pl.tb) + 16 * counts.nnz + 8 * counts.n_delta + 8 * counts.n_value
         h_stage[:sb].copy_(comp.stage[:sb], non_blocking=True)
         comp.stage[:sb].copy_(h_stage[:sb], non_blocking=True)
         comp.decode_local(counts, q, agg, dwork)
-        aggs = dist.exchange_planes(agg)
+        aggs = dist.exchange_planes(agg.to(xdev)).to(dev)
         fz.slab_carry(aggs, rank, E, carry)
         comp.finish(q, carry, counts, params)
         h_out[:nloc].copy_(q[:nloc].view(torch.float32), non_blocking=True)
@@ -142,9 +162,9 @@ def run(args, wl, metric):
         torch.cuda.synchronize()
         tdist.barrier()
         etimes.append(e0.elapsed_time(e1))
-    et = torch.tensor([statistics.mean(etimes)], dtype=torch.float64, device=dev)
+    et = torch.tensor([statistics.mean(etimes)], dtype=torch.float64, device=xdev)
     tdist.all_reduce(et, op=tdist.ReduceOp.MAX)
-    ebytes = torch.tensor([float(io[0]), float(io[1])], dtype=torch.float64, device=dev)
+    ebytes = torch.tensor([float(io[0]), float(io[1])], dtype=torch.float64, device=xdev)
     tdist.all_reduce(ebytes, op=tdist.ReduceOp.SUM)
     ems = float(et.item())
     # correctness spot check against the 1-GPU decode of the same stream: every rank's
@@ -152,9 +172,9 @@ def run(args, wl, metric):
     xh = q[:nloc].view(torch.float32)
     ref = torch.from_numpy(np.ascontiguousarray(flat[pl.own_lo: pl.own_hi])).to(dev)
     err = float((xh.double() - ref.double()).abs().max().item()) if nloc else 0.0
-    e = torch.tensor([err], dtype=torch.float64, device=dev)
+    e = torch.tensor([err], dtype=torch.float64, device=xdev)
     tdist.all_reduce(e, op=tdist.ReduceOp.MAX)
-    lt = torch.tensor([launches[0] / max(1, args.steps)], dtype=torch.float64, device=dev)
+    lt = torch.tensor([launches[0] / max(1, args.steps)], dtype=torch.float64, device=xdev)
     tdist.all_reduce(lt, op=tdist.ReduceOp.SUM)
     if rank == 0:
         gb = d.nbytes / 1e9
@@ -168,6 +188,7 @@ def run(args, wl, metric):
             "cr": round(d.nbytes / total, 4),
             "max_abs_err_over_eb_abs": round(err / last_params[0].eb_abs, 6),
             "gpu_launches": int(lt.item() * args.steps),
+            "clocks": sampler.summary(),
             "e2e": {"value": round(gb / (ems / 1e3), 3), "unit": "GB/s", "ms_per_step": round(ems, 4),
                     "h2d_bytes_per_step": int(ebytes[0].item()), "d2h_bytes_per_step": int(ebytes[1].item()),
                     "path": "slab API per rank: pinned H2D of the slab, compress, D2H + H2D of the rank's "
