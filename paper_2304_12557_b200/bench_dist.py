@@ -26,6 +26,15 @@ def _clock_sampler(index: int):
     return importlib.import_module("bench").ClockSampler(index)
 
 
+def _peak():
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
 def run(args, wl, metric):
     import torch
     import torch.distributed as tdist
@@ -98,6 +107,10 @@ def run(args, wl, metric):
     times = []
     launches[0] = 0
     sampler = _clock_sampler(local)
+    # per-kernel CUDA-event times of this rank's launches (the roofline of the compressor)
+    fz.profile_enable(True)
+    fz.profile_only(["k_range", "k_compress", "k_decode_tiles", "k_scan_walk", "k_scan_apply"])
+    fz.profile_read()
     with sampler:
         for _ in range(args.steps):
             tdist.barrier()
@@ -109,6 +122,8 @@ def run(args, wl, metric):
             torch.cuda.synchronize()
             tdist.barrier()
             times.append(e0.elapsed_time(e1))
+    prof = fz.profile_read()
+    fz.profile_enable(False)
     if os.environ.get("FZ_DIST_DEBUG"):
         print(f"rank {rank} step ms {[round(x, 3) for x in times]}", flush=True)
     t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=xdev)
@@ -178,6 +193,16 @@ def run(args, wl, metric):
     tdist.all_reduce(lt, op=tdist.ReduceOp.SUM)
     if rank == 0:
         gb = d.nbytes / 1e9
+        roof = None
+        if "k_compress" in prof:
+            pk = prof["k_compress"][0] / prof["k_compress"][1]
+            ab = 4 * nloc + (total - 128) * nloc / max(1, d.size)   # rank 0's share of the stream
+            peak = _peak()
+            ach = ab / (pk / 1e3) / 1e9
+            roof = {"kernel": "k_compress (rank 0 slab)", "bound": "hbm", "achieved": round(ach, 1),
+                    "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+                    "ms_per_launch": round(pk, 4),
+                    "kernels_ms": {k: round(v[0] / v[1], 4) for k, v in prof.items()}}
         line = {
             "metric": metric, "value": round(gb / (ms / 1e3), 3), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
@@ -189,6 +214,7 @@ def run(args, wl, metric):
             "max_abs_err_over_eb_abs": round(err / last_params[0].eb_abs, 6),
             "gpu_launches": int(lt.item() * args.steps),
             "clocks": sampler.summary(),
+            "roofline": roof,
             "e2e": {"value": round(gb / (ems / 1e3), 3), "unit": "GB/s", "ms_per_step": round(ems, 4),
                     "h2d_bytes_per_step": int(ebytes[0].item()), "d2h_bytes_per_step": int(ebytes[1].item()),
                     "path": "slab API per rank: pinned H2D of the slab, compress, D2H + H2D of the rank's "
