@@ -268,6 +268,8 @@ def run_single(args, wl):
     import torch
 
     from paper_2304_12557_b200 import fz
+    if os.environ.get("FZ_EXP"):   # A/B variants (tools/ablation.py); the library reads no env
+        fz.debug_set_variant(int(os.environ["FZ_EXP"]))
     field_name, shape, rel, desc = wl
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)

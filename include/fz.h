@@ -255,7 +255,12 @@ fz_status fz_slab_decode_cl(const void* d_stage, const fz_counts* local, const f
 /* ---------------------------------------------------------------------------------------
  * Stage hooks for parity tests (north star: codes and outlier lists match the oracle).
  * ------------------------------------------------------------------------------------- */
-/* C1-C3: uint16 codes of every element and both outlier lists (ascending index). */
+/* Workspace of fz_debug_quantize: the compression workspace plus scratch for the flag and
+ * payload sections the product kernels write (32 T + 4096 T bytes). */
+size_t fz_debug_workspace_bytes(const fz_shape* s);
+/* C1-C3: uint16 codes of every element and both outlier lists (ascending index), produced by
+ * the same kernels fz_compress launches for the shape (codes written as a side output).
+ * d_work: fz_debug_workspace_bytes(s) bytes, else FZ_ERR_WORKSPACE. */
 fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_params* h_params,
                             uint16_t* d_codes,
                             uint32_t* d_didx, int32_t* d_dval, uint64_t dcap, uint64_t* h_nd,
@@ -264,6 +269,12 @@ fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_pa
 /* D1-D5: reconstructed integer codes q (before dequantization), n int32 values. */
 fz_status fz_debug_decode_q(const void* d_in, size_t in_size, int32_t* d_q, uint64_t n,
                             void* d_work, size_t work_bytes, void* stream);
+
+/* Kernel variants for A/B experiments (tools/ablation.py): process-wide bits, 0 = the
+ * product configuration.  16: generic fused compressor; 1024: warp-specialized single-pass
+ * compressor instead of the z-band one; 128: unfused decoder y scan; 512 / 4096: plane decoder
+ * with one / two CTAs per plane.  Streams are byte-identical under every variant. */
+void fz_debug_set_variant(int bits);
 
 /* Number of kernel launches issued by the last fz_compress / fz_decompress on this thread
  * (bench accounting of "gpu_launches"). */

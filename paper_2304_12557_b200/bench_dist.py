@@ -59,6 +59,11 @@ def run(args, wl, metric):
     d = synth.generate(field_name, shape)
     flat = d.reshape(-1)
     pl = dist.plan(shape, world, rank)
+    # every rank needs a nonempty tile range (fz_slab_compress rejects an empty one, and a
+    # rank that skipped the all_gathers would hang the others)
+    nslabs = shape[0] if len(shape) == 3 else -(-int(np.prod(shape)) // 2048)
+    if world > nslabs or pl.te <= pl.tb:
+        raise SystemExit(f"bench_dist: {world} ranks but only {nslabs} slabs in {shape}")
     slab = torch.from_numpy(np.ascontiguousarray(flat[pl.slab_first: pl.slab_hi])).to(dev)
     comp = dist.SlabCompressor(shape, pl, dev)
     E = fz.slab_agg_elems(shape)
@@ -191,6 +196,10 @@ def run(args, wl, metric):
     tdist.all_reduce(e, op=tdist.ReduceOp.MAX)
     lt = torch.tensor([launches[0] / max(1, args.steps)], dtype=torch.float64, device=xdev)
     tdist.all_reduce(lt, op=tdist.ReduceOp.SUM)
+    # a wrong multi-GPU decode must not print a valid bench line
+    err = float(e.item())
+    if err > last_params[0].eb_abs:
+        raise SystemExit(f"bench_dist: max |x - x^| = {err} exceeds eb_abs = {last_params[0].eb_abs}")
     if rank == 0:
         gb = d.nbytes / 1e9
         roof = None

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -17,11 +18,12 @@ namespace {
 struct ProfRec {
     int id;
     cudaEvent_t a, b;
+    bool done;   // end event recorded (set by ~LaunchProf under g_prof_mu)
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 uint64_t g_prof_mask = ~0ull;     // kernels recorded (bit = KernelId)
-std::vector<ProfRec> g_prof_pending;
+std::vector<ProfRec*> g_prof_pending;   // heap records: stable while the vector grows
 std::vector<cudaEvent_t> g_prof_pool;
 double g_prof_ms[K_COUNT];
 int g_prof_n[K_COUNT];
@@ -39,22 +41,29 @@ cudaEvent_t prof_event()
 }
 }  // namespace
 
+static std::atomic<int> g_variant{0};
+int variant_bits() { return g_variant.load(std::memory_order_relaxed); }
+void set_variant_bits(int v) { g_variant.store(v, std::memory_order_relaxed); }
+
 LaunchProf::LaunchProf(KernelId id_, cudaStream_t st_) : id(id_), st(st_), slot(-1)
 {
     ++t_launches;
     std::lock_guard<std::mutex> g(g_prof_mu);
     if (!g_prof_on || !((g_prof_mask >> id) & 1)) return;
-    ProfRec r{id, prof_event(), prof_event()};
-    cudaEventRecord(r.a, st);
+    ProfRec* r = new ProfRec{id, prof_event(), prof_event(), false};
+    cudaEventRecord(r->a, st);
     g_prof_pending.push_back(r);
-    slot = (int)g_prof_pending.size() - 1;
+    rec = r;     // the record itself, not an index: another thread's fz_profile_read may
+    slot = 1;    // compact the pending vector meanwhile (it skips records not yet done)
 }
 
 LaunchProf::~LaunchProf()
 {
     if (slot < 0) return;
     std::lock_guard<std::mutex> g(g_prof_mu);
-    if (slot < (int)g_prof_pending.size()) cudaEventRecord(g_prof_pending[slot].b, st);
+    ProfRec* r = static_cast<ProfRec*>(rec);
+    cudaEventRecord(r->b, st);
+    r->done = true;
 }
 }  // namespace fz
 
@@ -67,15 +76,8 @@ static thread_local bool g_have_hdr = false;
 
 namespace {
 
-// FZ_EXP: experiment bits for A/B timing (128: unfused y scan in the decoder).
-int exp_bits()
-{
-    static const int v = [] {
-        const char* e = getenv("FZ_EXP");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
+// variant bits for A/B timing (128: unfused y scan in the decoder), fz_debug_set_variant
+int exp_bits() { return fz::variant_bits(); }
 
 struct LaunchScope {
     LaunchScope() { fz::t_launches = 0; }
@@ -381,6 +383,14 @@ size_t fz_workspace_bytes(const fz_shape* s)
     return compress_layout(n, tiles_of(n), zb_layout(*s)).total;
 }
 
+size_t fz_debug_workspace_bytes(const fz_shape* s)
+{
+    uint64_t n;
+    if (!shape_n(s, &n)) return 0;
+    const uint64_t T = tiles_of(n);
+    return compress_layout(n, T, zb_layout(*s)).total + 32 * T + 4096 * T;
+}
+
 size_t fz_decompress_workspace_bytes(const fz_shape* s)
 {
     uint64_t n;
@@ -408,7 +418,11 @@ fz_status fz_compress_with_params(const float* d_field, const fz_shape* s, const
 {
     LaunchScope ls;
     if (p == nullptr || !(p->w >= 1.17549435e-38f) || !std::isfinite(p->w)) return FZ_ERR_ARG;
-    return compress_impl(d_field, s, p, (int)p->mode, p->eb_input, d_out, out_cap, out_size, d_work,
+    // the chunk-local bit selects the Lorenzo variant; the params proper (and so the header's
+    // REL bit, which k_finalize derives from p.mode) never carry it
+    fz_params pm = *p;
+    pm.mode &= ~(uint32_t)FZ_CHUNK_LOCAL;
+    return compress_impl(d_field, s, &pm, (int)p->mode, p->eb_input, d_out, out_cap, out_size, d_work,
                          work_bytes, static_cast<cudaStream_t>(stream));
 }
 
@@ -442,6 +456,14 @@ fz_status fz_peek_header(const void* h_hdr, size_t nbytes, fz_info* info)
     memcpy(&I.params.r, h + 68, 4);
     memcpy(&I.params.mn, h + 72, 4);
     memcpy(&I.params.mx, h + 76, 4);
+    {
+        // f1 chunk-local streams (bit 2) carry nonzero chunk dims at bytes 10-13; other
+        // streams keep those bytes zero
+        uint16_t cz, cy;
+        memcpy(&cz, h + 10, 2);
+        memcpy(&cy, h + 12, 2);
+        if ((fl & 4u) ? (cz == 0 || cy == 0) : (cz != 0 || cy != 0)) return FZ_ERR_CORRUPT;
+    }
     I.params.mode = (fl & 1u) ? FZ_EB_REL : FZ_EB_ABS;
     I.params.fallback = (fl & 2u) ? 1u : 0u;
     if (!(I.params.w > 0.0f) || !std::isfinite(I.params.w)) return FZ_ERR_CORRUPT;
@@ -777,6 +799,8 @@ const char* fz_strerror(int status)
 
 const char* fz_last_cuda_error(void) { return g_cuda_err; }
 
+void fz_debug_set_variant(int bits) { fz::set_variant_bits(bits); }
+
 int fz_last_launch_count(void) { return g_last_launches; }
 
 void fz_profile_enable(int on)
@@ -797,13 +821,13 @@ int fz_profile_timeline(int* h_ids, float* h_start_ms, float* h_end_ms, int max_
     std::lock_guard<std::mutex> g(fz::g_prof_mu);
     const int n = (int)fz::g_prof_pending.size() < max_records ? (int)fz::g_prof_pending.size() : max_records;
     if (n == 0) return 0;
-    const cudaEvent_t t0 = fz::g_prof_pending[0].a;
+    const cudaEvent_t t0 = fz::g_prof_pending[0]->a;
     for (int k = 0; k < n; ++k) {
-        const auto& r = fz::g_prof_pending[k];
-        cudaEventSynchronize(r.b);
+        const fz::ProfRec& r = *fz::g_prof_pending[k];
+        if (r.done) cudaEventSynchronize(r.b);
         float a = 0.0f, b = 0.0f;
         cudaEventElapsedTime(&a, t0, r.a);
-        cudaEventElapsedTime(&b, t0, r.b);
+        if (r.done) cudaEventElapsedTime(&b, t0, r.b);
         if (h_ids) h_ids[k] = r.id;
         if (h_start_ms) h_start_ms[k] = a;
         if (h_end_ms) h_end_ms[k] = b;
@@ -814,17 +838,23 @@ int fz_profile_timeline(int* h_ids, float* h_start_ms, float* h_end_ms, int max_
 int fz_profile_read(double* h_ms, int* h_launches, int max_kernels)
 {
     std::lock_guard<std::mutex> g(fz::g_prof_mu);
-    for (auto& r : fz::g_prof_pending) {
-        cudaEventSynchronize(r.b);
-        float ms = 0.0f;
-        if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
-            fz::g_prof_ms[r.id] += ms;
-            fz::g_prof_n[r.id] += 1;
+    size_t keep = 0;
+    for (fz::ProfRec* r : fz::g_prof_pending) {
+        if (!r->done) {                       // launch still being issued by another thread
+            fz::g_prof_pending[keep++] = r;
+            continue;
         }
-        fz::g_prof_pool.push_back(r.a);
-        fz::g_prof_pool.push_back(r.b);
+        cudaEventSynchronize(r->b);
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, r->a, r->b) == cudaSuccess) {
+            fz::g_prof_ms[r->id] += ms;
+            fz::g_prof_n[r->id] += 1;
+        }
+        fz::g_prof_pool.push_back(r->a);
+        fz::g_prof_pool.push_back(r->b);
+        delete r;
     }
-    fz::g_prof_pending.clear();
+    fz::g_prof_pending.resize(keep);
     for (int k = 0; k < fz::K_COUNT && k < max_kernels; ++k) {
         if (h_ms) h_ms[k] = fz::g_prof_ms[k];
         if (h_launches) h_launches[k] = fz::g_prof_n[k];
@@ -977,10 +1007,16 @@ fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_pa
         return FZ_ERR_ARG;
     const uint64_t T = tiles_of(n);
     Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
-    if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
+    // the hook runs the product kernels, which write flags and payload: scratch for them
+    // follows the compression workspace (fz_debug_workspace_bytes)
+    if (work_bytes < W.L.total + 32 * T + 4096 * T) return FZ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CompressArgs a = make_args(W, d_field, 0, geom_of(*s, n), 0, (uint32_t)T);
     a.codes_out = d_codes;
+    a.flags_out = static_cast<uint8_t*>(d_work) + W.L.total;
+    a.flags_cap = 32 * T;
+    a.payload_out = a.flags_out + 32 * T;
+    a.payload_cap = 4096 * T;
     Ctrl h;
     fz_status rs = compress_run(W, a, p, (int)p->mode, p->eb_input, nullptr, 0, *s, n, &h, st);
     if (rs != FZ_OK) return rs;

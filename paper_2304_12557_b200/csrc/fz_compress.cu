@@ -2036,11 +2036,11 @@ static cudaError_t launch_compress_ws(const CompressArgs& a, size_t sm, uint32_t
 }
 
 // z-band two-pass compression applies to 3-D fields with whole tiles per plane on the vector
-// path (FZ_EXP bit 1024 turns it off for A/B timing).
+// path (variant bit 1024, fz_debug_set_variant, turns it off for A/B timing).
 bool compress_uses_zb(const CompressArgs& a_in)
 {
     CompressArgs a = a_in;
-    if (const char* e = getenv("FZ_EXP")) a.exp = atoi(e);
+    a.exp = variant_bits();
     if (a.g.ndim != 3 || ((a.exp & (16 | 1024)) && !a.cl) || a.rescan || a.tstage == nullptr) return false;
     if (a.g.P % kTileCodes != 0 || a.g.n / a.g.P < 2) return false;
     // a slab (multi-GPU, SV 8.e) takes it when its tile range is whole planes
@@ -2092,7 +2092,7 @@ cudaError_t launch_compact(const uint8_t* flags, const uint32_t* loc, const uint
 bool compress_uses_ws(const CompressArgs& a_in)
 {
     CompressArgs a = a_in;
-    if (const char* e = getenv("FZ_EXP")) a.exp = atoi(e);
+    a.exp = variant_bits();
     bool vec = false;
     plan_smem(a, vec);
     return vec && !(a.exp & 16);
@@ -2101,7 +2101,7 @@ bool compress_uses_ws(const CompressArgs& a_in)
 cudaError_t launch_compress(const CompressArgs& a_in, cudaStream_t st)
 {
     CompressArgs a = a_in;
-    if (const char* e = getenv("FZ_EXP")) a.exp = atoi(e);
+    a.exp = variant_bits();
     a.dnx = make_fastdiv(a.g.nx);
     a.dP = make_fastdiv(a.g.P);
     a.sx = a.g.nx ? (uint32_t)(kTileCodes % a.g.nx) : 0u;

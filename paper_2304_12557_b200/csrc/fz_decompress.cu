@@ -1178,11 +1178,7 @@ cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool c
 
 static int walk_mode()
 {
-    static const int v = [] {
-        const char* e = getenv("FZ_EXP");
-        return e ? (atoi(e) >> 8) & 3 : 0;
-    }();
-    return v;
+    return (variant_bits() >> 8) & 3;
 }
 
 // Column walk along L (stride W): vector columns when the rows allow it.

@@ -540,7 +540,7 @@ struct CompressArgs {
     uint4* tstage;            // z-band pass 1: 256-block staging slot per tile (null: not available)
     uint32_t hwords;          // z-band: floats of the TMA-staged row halo (0: quantized from global)
     uint32_t cl;              // f1 chunk-local Lorenzo (z-band kernel only): chunks of kZbChunk planes x one tile
-    int exp;                  // FZ_EXP env var, bit 16: generic kernel instead of the warp-specialized one
+    int exp;                  // variant bits (fz_debug_set_variant), bit 16: generic kernel instead of the warp-specialized one
 };
 
 }  // namespace fz

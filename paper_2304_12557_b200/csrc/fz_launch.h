@@ -9,6 +9,11 @@ namespace fz {
 
 int num_sms();
 
+// Kernel-variant bits for A/B experiments, set only through fz_debug_set_variant (0 = the
+// product configuration; never read from the environment).
+int variant_bits();
+void set_variant_bits(int v);
+
 // Kernel kinds for launch accounting and per-kernel CUDA-event timing (fz_profile_*).
 enum KernelId {
     K_INIT = 0, K_RANGE, K_PARAMS, K_COMPRESS, K_FINALIZE, K_DINIT, K_VALIDATE, K_DECODE,
@@ -23,7 +28,8 @@ struct LaunchProf {
     ~LaunchProf();
     KernelId id;
     cudaStream_t st;
-    int slot;
+    int slot;              // 1: events are being recorded for this launch
+    void* rec = nullptr;   // its pending record (fz_api.cu)
 };
 
 // compression (fz_compress.cu)

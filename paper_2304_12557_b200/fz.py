@@ -87,9 +87,11 @@ def lib():
         "fz_slab_stage_bound": ([pS, u64, u64], S),
         "fz_slab_compress": ([P, u64, u64, pS, u64, u64, pP, P, S, pC, P, S, P], i),
         "fz_slab_place": ([P, pS, u64, u64, pC, pC, pC, pP, i, P, S, P], i),
+        "fz_debug_workspace_bytes": ([pS], S),
         "fz_debug_quantize": ([P, pS, pP, P, P, P, u64, C.POINTER(u64), P, P, u64, C.POINTER(u64), P, S, P], i),
         "fz_debug_decode_q": ([P, S, P, u64, P, S, P], i),
         "fz_last_launch_count": ([], i),
+        "fz_debug_set_variant": ([i], None),
         "fz_profile_enable": ([i], None),
         "fz_profile_mask": ([C.c_ulonglong], None),
         "fz_profile_read": ([C.POINTER(C.c_double), C.POINTER(C.c_int), i], i),
@@ -327,13 +329,18 @@ def debug_quantize(field, params: Params, cap: int | None = None, stream=None):
     dval = torch.empty(max(cap, 4), dtype=torch.int32, device=dev)
     vidx = torch.empty(max(cap, 4), dtype=torch.int32, device=dev)
     vbits = torch.empty(max(cap, 4), dtype=torch.int32, device=dev)
-    work = _u8(workspace_bytes(dims), dev)
+    work = _u8(lib().fz_debug_workspace_bytes(C.byref(make_shape(dims))), dev)
     nd, nv = C.c_uint64(), C.c_uint64()
     st = lib().fz_debug_quantize(_ptr(field), C.byref(make_shape(dims)), C.byref(params), _ptr(codes),
                                  _ptr(didx), _ptr(dval), cap, C.byref(nd), _ptr(vidx), _ptr(vbits), cap,
                                  C.byref(nv), _ptr(work), work.numel(), _stream(stream))
     _check(st, "fz_debug_quantize")
     return codes, didx[: nd.value], dval[: nd.value], vidx[: nv.value], vbits[: nv.value]
+
+
+def debug_set_variant(bits: int) -> None:
+    """A/B experiments only: process-wide kernel-variant bits (0 = product configuration)."""
+    lib().fz_debug_set_variant(int(bits))
 
 
 def debug_decode_q(buf, dims, stream=None):

@@ -315,12 +315,15 @@ def test_host_header_decompress_matches():
 
 
 def test_generic_vector_kernel_parity(monkeypatch):
-    """FZ_EXP=16 routes compression through the generic padded-halo kernel (k_compress<NDIM,
+    """Variant 16 (fz_debug_set_variant) routes compression through the generic padded-halo kernel (k_compress<NDIM,
     VEC>) instead of the warp-specialized one; its stream must be byte-identical too."""
-    monkeypatch.setenv("FZ_EXP", "16")
-    for d in (synth.generate("nyx_v", (24, 40, 64)), synth.generate("cesm_t", (90, 256)),
-              synth.adversarial("spike", 30000)):
-        _check_full(d, O.REL, 1e-3, f"generic{d.shape}")
+    fz.debug_set_variant(16)
+    try:
+        for d in (synth.generate("nyx_v", (24, 40, 64)), synth.generate("cesm_t", (90, 256)),
+                  synth.adversarial("spike", 30000)):
+            _check_full(d, O.REL, 1e-3, f"generic{d.shape}")
+    finally:
+        fz.debug_set_variant(0)
 
 
 ASYNC_SHAPES = [
@@ -399,8 +402,11 @@ def test_zband_with_outliers_and_single_kernel_equality(monkeypatch):
     d.reshape(-1)[rng.choice(d.size, 400, replace=False)] += np.float32(80.0) * np.float32(d.max() - d.min())
     ref = _check_full(d, O.ABS, eb, "zband_outliers")
     assert int.from_bytes(ref[96:104].tobytes(), "little") > 0
-    monkeypatch.setenv("FZ_EXP", "1024")            # warp-specialized single kernel instead
-    got, _, _ = _gpu_stream(d, O.ABS, eb)
+    fz.debug_set_variant(1024)                     # warp-specialized single kernel instead
+    try:
+        got, _, _ = _gpu_stream(d, O.ABS, eb)
+    finally:
+        fz.debug_set_variant(0)
     _assert_stream_equal(got, ref, "single_kernel")
 
 

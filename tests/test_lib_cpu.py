@@ -31,7 +31,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol():
     syms = declared_symbols()
-    assert len(syms) == 36
+    assert len(syms) == 38
     L = C.CDLL(fz.LIB_PATH)
     for s in syms:
         assert hasattr(L, s), s
@@ -82,6 +82,26 @@ def test_peek_header_on_oracle_stream():
     bad[88] ^= 1                                   # nnz breaks the size law
     with pytest.raises(fz.FZError):
         fz.peek_header(bytes(bad))
+
+
+def test_peek_header_chunk_word_consistency():
+    """Header flag bit 2 (f1 chunk-local, R23) and the chunk dims at bytes 10-13 must agree:
+    bit 2 with a zero chunk word, or a nonzero word without bit 2, is a corrupt stream."""
+    d = synth.generate("nyx_v", (32, 32, 64))
+    st, g = O.compress(d, O.REL, 1e-3)
+    st, c = O.compress_chunked(d, O.REL, 1e-3, 16, 2048 // 64)
+    assert fz.peek_header(g[:128].tobytes()).flags & 4 == 0
+    assert fz.peek_header(c[:128].tobytes()).flags & 4 == 4
+    bad = bytearray(c[:128].tobytes())
+    bad[10:14] = b"\0\0\0\0"                    # bit 2 set, chunk word zero
+    with pytest.raises(fz.FZError) as e:
+        fz.peek_header(bytes(bad))
+    assert e.value.status == fz.ERR_CORRUPT
+    bad = bytearray(g[:128].tobytes())
+    bad[12] = 1                                    # chunk height without bit 2
+    with pytest.raises(fz.FZError) as e:
+        fz.peek_header(bytes(bad))
+    assert e.value.status == fz.ERR_CORRUPT
 
 
 def test_missing_library_fails_loudly(tmp_path, monkeypatch):

@@ -16,6 +16,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     if os.environ.get("AS2D"):
         d = d.reshape(-1, shape[-1])
         shape = d.shape
+    fz.debug_set_variant(int(os.environ.get("FZ_EXP", "0")))
     x = torch.from_numpy(d).cuda()
     c = fz.Codec(shape, "cuda")
     for _ in range(3):
