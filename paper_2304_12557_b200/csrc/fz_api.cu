@@ -219,8 +219,9 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
     const uint32_t tb = a.tile_begin, nt = a.tile_end - a.tile_begin;
     // status words are per scan unit, indexed from the range start; outlier counts per tile
     FZ_CUDA(launch_init(W.ctrl(), W.status(), W.ocnt() + tb, nt, hp, st, a.cl ? cl_chunk(s) : 0u));
-    if (a.cl && !compress_uses_zb(a)) return FZ_ERR_ARG;
-    if (compress_uses_zb(a)) {
+    const bool zr = compress_uses_zr(a);
+    if (a.cl && !zr && !compress_uses_zb(a)) return FZ_ERR_ARG;
+    if (zr || compress_uses_zb(a)) {
         // z-band two-pass compressor: pass 1 derives the parameters in its prologue, writes
         // the flags and stages each tile's blocks; the popcount scan of the flags gives the
         // offsets, k_compact moves the blocks, k_finalize writes totals + header
@@ -230,7 +231,7 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
         b.eb_mode = mode;
         b.eb = eb;
         b.n_hdr = n;
-        FZ_CUDA(launch_compress_zb(b, st));
+        FZ_CUDA(zr ? launch_compress_zr(b, st) : launch_compress_zb(b, st));
         const uint32_t T = a.tile_end - a.tile_begin;
         FZ_CUDA(launch_tile_offsets(a.flags_out, T, W.zloc(), W.zbsum(), W.ctrl(), st, ~1ull));
         FZ_CUDA(launch_compact(a.flags_out, W.zloc(), W.zbsum(), W.tstage(), a.payload_out, a.payload_cap, T, st));

@@ -23,42 +23,6 @@ __device__ __forceinline__ int pad(int m) { return m + (m >> 3); }
 inline uint32_t pad_words(uint32_t len) { return len + (len >> 3) + 8; }
 constexpr uint32_t kUnionHaloMax = 4097;   // union arrays when the row halo nx+1 fits
 
-// h = w/2; hU = RD32(w/2 - U) with U = 2^(e-23), M = max|d| = m 2^e (Appendix A): the
-// fast-path threshold of pq_fast.  Fallback mode: hU = -1 (every element takes the exact
-// rule and the bound check).
-// h = w/2 and the fast-path threshold hU = RD32(w/2 - U) (-1: fast path off, fallback mode).
-__device__ void quant_consts(const fz_params& p, float& h, float& hU)
-{
-    h = 0.5f * p.w;
-    if (p.fallback) {
-        hU = -1.0f;
-        return;
-    }
-    const float M = fmaxf(fabsf(p.mn), fabsf(p.mx));
-    double U = 0.0;
-    if (M > 0.0f) {
-        int e;
-        frexp((double)M, &e);
-        U = ldexp(1.0, e - 23);
-    }
-    const double t = (double)h - U;
-    hU = t > 0.0 ? rd32(t) : -1.0f;
-}
-
-__device__ void set_quant_consts(Ctrl* ctrl)
-{
-    quant_consts(ctrl->p, ctrl->h, ctrl->hU);
-}
-
-// Appendix-A parameters from the range pass's result (k_params and the ws-kernel prologue).
-__device__ int params_from_range(const Ctrl* ctrl, int mode, double eb, uint64_t n, fz_params* p)
-{
-    if (ctrl->first_bad != ~0ull) return FZ_ERR_NONFINITE;
-    const float mn = n ? ord2f(ctrl->mn_enc) : 0.0f;
-    const float mx = n ? ord2f(ctrl->mx_enc) : 0.0f;
-    return derive_params(mn, mx, mode, eb, p);
-}
-
 // ------------------------------------------------------------------------------------
 __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint32_t ntiles,
                        int set_params, fz_params p, uint32_t chunk)
@@ -937,56 +901,6 @@ __global__ void __launch_bounds__(kCta, 2) k_compress(CompressArgs a)
 // ------------------------------------------------------------------------------------
 constexpr int kWsThreads = kCta + 32;
 constexpr int kBarCompute = 5;
-
-__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ int bar_or(int id, int n, int pred)
-{
-    int r;
-    asm volatile("{ .reg .pred p, q; setp.ne.s32 p, %1, 0; bar.red.or.pred q, %2, %3, p; selp.s32 %0, 1, 0, q; }"
-                 : "=r"(r) : "r"(pred), "r"(id), "r"(n) : "memory");
-    return r;
-}
-__device__ __forceinline__ uint32_t smem_u32(const void* p)
-{
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
-}
-// try_wait with a suspend-time hint (ns): the thread stays parked until the phase completes
-// or the hint elapses, instead of returning after the default short timeout.
-__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* m, uint32_t parity, uint32_t ns)
-{
-    uint32_t ok;
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok) : "r"(smem_u32(m)), "r"(parity), "r"(ns) : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* m)
-{
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* m, uint32_t parity)
-{
-    uint32_t ok;
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok) : "r"(smem_u32(m)), "r"(parity) : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* m)
-{
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
-}
-
-constexpr int kRingBlocks = 1024;   // 16 KB elastic payload ring (per-tile allocation)
-constexpr int kDescQ = 8;          // unit descriptors in flight to the scanner
 
 struct WsDesc {
     uint32_t unit, start, cnt, pad;

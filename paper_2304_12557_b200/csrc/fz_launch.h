@@ -41,6 +41,8 @@ cudaError_t launch_compress(const CompressArgs& a, cudaStream_t st);
 bool compress_uses_ws(const CompressArgs& a);   // the warp-specialized kernel takes this launch
 bool compress_uses_zb(const CompressArgs& a);   // the z-band two-pass compressor takes it
 cudaError_t launch_compress_zb(const CompressArgs& a, cudaStream_t st);
+bool compress_uses_zr(const CompressArgs& a);   // the row-walking z-band compressor takes it (fz_zrow.cu)
+cudaError_t launch_compress_zr(const CompressArgs& a, cudaStream_t st);
 cudaError_t launch_compact(const uint8_t* flags, const uint32_t* loc, const uint32_t* bpre, const uint4* tstage,
                            uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles, cudaStream_t st);
 cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint64_t n,
