@@ -112,6 +112,23 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
                     "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
                  : "memory");
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld8(uint32_t (&v)[8])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
+                 :: "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+                 :: "r"(taddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st()
 {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -240,51 +257,85 @@ __device__ __forceinline__ ZrStep zr_next(ZrCursor& c, uint64_t u0, uint64_t u1,
 // A0: the t-bits of G stage rows r0..r0+G-1 (row 0 = halo), in place, exact: the fast path
 // for all, the exact rule (prequant) for the lanes of a group with a hard element (one warp
 // vote per group), value-outlier marks for own rows (1..16).
+// Out of line (cold, keeps the hot loop small for the instruction cache): the t-bits of G
+// stage rows from their floats with the exact rule (R1-R3, R20) wherever the fast path does
+// not apply, value-outlier marks for own rows (1..16).
+__device__ __noinline__ void zr_tgroup_slow(uint8_t* stg, uint8_t* msk, uint32_t RP, uint32_t spr, int r0, int G,
+                                            int tid, int lane, int warp, QuantP P)
+{
+    const float kMagic = 12582912.0f;
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+        uint32_t* row = reinterpret_cast<uint32_t*>(stg + (r0 + g) * RP + 16u * tid);
+        uint32_t vb = 0;
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+            const float d = __uint_as_float(row[k]);
+            const float tf = __fmaf_rn(d, P.r, kMagic);
+            const float qf = __fsub_rn(tf, kMagic);
+            uint32_t t = __float_as_uint(tf);
+            if (!(fabsf(__fmaf_rn(-qf, P.w, d)) < P.hU)) {
+                bool vo;
+                t = (uint32_t)prequant(d, P, vo) + kMagicBits;
+                if (vo) vb |= 1u << k;
+            }
+            row[k] = t;
+        }
+        const int r = r0 + g;
+        if (vb && r >= 1) {   // own rows only (row 0 is the halo)
+            const uint32_t seg = 2u * warp + (lane >> 4);
+            atomicOr(reinterpret_cast<unsigned long long*>(msk + 16 * ((r - 1) * spr + seg)),
+                     (unsigned long long)vb << (4 * (lane & 15)));
+        }
+    }
+}
+
+// A0: the t-bits of G stage rows r0..r0+G-1 (row 0 = halo), in place.  The fast path for all
+// (one FFMA + FADD + FFMA + FSETP per element).  A hard element (|e| >= hU) in margin mode
+// is corrected inline from its exact residual e = d - q0 w (|q0 - d/w| <= 1/2 + 1/8, so one
+// step reaches the nearest bin; |e| = w/2 is a tie -> even, R1); margin mode has no value
+// outliers (|fl(q w) - d| <= |e| + U/2 <= eb for |e| <= w/2, SV App. A) and |q| < 2^21.
+// Fallback mode (hU < 0) takes the full exact rule with the bound check out of line.
 template <int G>
 __device__ __forceinline__ void zr_tgroup(uint8_t* stg, uint8_t* msk, uint32_t RP, uint32_t spr, int r0, int tid,
                                           int lane, int warp, const QuantP& P)
 {
     const float kMagic = 12582912.0f;
-    float4 d[G];
+    float dv[G][4];
     uint32_t t[G][4];
     bool hard = false;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        d[g] = *reinterpret_cast<const float4*>(stg + (r0 + g) * RP + 16u * tid);
-        const float dv[4] = {d[g].x, d[g].y, d[g].z, d[g].w};
+        const float4 d = *reinterpret_cast<const float4*>(stg + (r0 + g) * RP + 16u * tid);
+        dv[g][0] = d.x; dv[g][1] = d.y; dv[g][2] = d.z; dv[g][3] = d.w;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             // q0 = rint(d r) by one rounding of d r + 1.5 2^23 (|d r| < 2^22 in margin mode);
             // the exact residual e = d - q0 w decides: |e| < hU => q0 is the unique nearest
             // bin and the bound holds (R3, SV App. A), however q0 was rounded
-            const float tf = __fmaf_rn(dv[k], P.r, kMagic);
+            const float tf = __fmaf_rn(dv[g][k], P.r, kMagic);
             const float qf = __fsub_rn(tf, kMagic);
-            const float e = __fmaf_rn(-qf, P.w, dv[k]);
+            const float e = __fmaf_rn(-qf, P.w, dv[g][k]);
             hard |= !(fabsf(e) < P.hU);
             t[g][k] = __float_as_uint(tf);
         }
     }
-    if (__any_sync(kFull, hard)) {   // rare: exact rule (R1-R3, R20) for this group
-        if (hard) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float dv[4] = {d[g].x, d[g].y, d[g].z, d[g].w};
-                uint32_t vb = 0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    bool vo;
-                    t[g][k] = (uint32_t)prequant(dv[k], P, vo) + kMagicBits;
-                    if (vo) vb |= 1u << k;
-                }
-                const int r = r0 + g;
-                if (vb && r >= 1) {   // own rows only (row 0 is the halo)
-                    const uint32_t seg = 2u * warp + (lane >> 4);
-                    atomicOr(reinterpret_cast<unsigned long long*>(msk + 16 * ((r - 1) * spr + seg)),
-                             (unsigned long long)vb << (4 * (lane & 15)));
-                }
-            }
+    if (__any_sync(kFull, hard)) {   // rare
+        if (P.hU < 0.0f) {           // fallback mode: exact rule + bound check for every element
+            zr_tgroup_slow(stg, msk, RP, spr, r0, G, tid, lane, warp, P);
+            __syncwarp();
+            return;
         }
-        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float qf = __fsub_rn(__uint_as_float(t[g][k]), kMagic);
+                const float e = __fmaf_rn(-qf, P.w, dv[g][k]);   // exact residual
+                const float ae = fabsf(e);
+                const bool step = ae > P.h || (ae == P.h && (t[g][k] & 1u));
+                t[g][k] += step ? (e > 0.0f ? 1u : 0xFFFFFFFFu) : 0u;
+            }
     }
 #pragma unroll
     for (int g = 0; g < G; ++g)
@@ -295,7 +346,7 @@ __device__ __forceinline__ void zr_tpass(uint8_t* stg, uint8_t* msk, uint32_t RP
                                          int lane, int warp, const QuantP& P)
 {
     if (halo) zr_tgroup<1>(stg, msk, RP, spr, 0, tid, lane, warp, P);
-#pragma unroll 1
+#pragma unroll
     for (int r0 = 1; r0 <= kZrRows; r0 += 4) zr_tgroup<4>(stg, msk, RP, spr, r0, tid, lane, warp, P);
 }
 
@@ -467,47 +518,47 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
             }
             // ---- A1: Lorenzo + codes, 16 rows in groups of 4; z carry in TMEM ----
             uint32_t magor = 0;
-            uint32_t tpn[16];
-            if (!zfirst) tmem_ld16(taddr, tpn);
-#pragma unroll 1
-            for (int g = 0; g < kZrRows / 4; ++g) {
-                uint32_t tp[16], tc[16];
-                if (!zfirst) {
-                    tmem_wait_ld(tpn);
+            // two carry buffers (the next group's load in flight while one is used)
+            uint32_t tpb[2][8];   // two rows of the carry per load, the next pair in flight
+            if (zfirst) {   // q(z-1) = 0: the carry starts as the t-bits of q = 0
+                uint32_t mg[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) tp[j] = tpn[j];
-                    if (g + 1 < kZrRows / 4) tmem_ld16(taddr + 16u * (g + 1), tpn);   // next group in flight
-                } else {
+                for (int j = 0; j < 16; ++j) mg[j] = kMagicBits;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) tp[j] = kMagicBits;
+                for (int g = 0; g < kZrRows / 4; ++g) tmem_st16(taddr + 16u * g, mg);
+                tmem_wait_st();
+            }
+            tmem_ld8(taddr, tpb[0]);
+#pragma unroll
+            for (int i = 0; i < kZrRows; ++i) {
+                uint32_t(&tpp)[8] = tpb[(i >> 1) & 1];
+                if ((i & 1) == 0) {
+                    tmem_wait_ld8(tpp);
+                    if (i + 2 < kZrRows) tmem_ld8(taddr + 4u * (i + 2), tpb[((i >> 1) + 1) & 1]);
                 }
+                const uint32_t* tp = tpp + 4 * (i & 1);
+                const uint4 tv = *reinterpret_cast<const uint4*>(stg + (i + 1) * RP + 16u * tid);
+                const uint32_t t[4] = {tv.x, tv.y, tv.z, tv.w};
+                tmem_st4(taddr + 4u * i, t[0], t[1], t[2], t[3]);
+                uint32_t Y[4];
+                const bool ystart = CL && ((y0 + i) % cy == 0);
 #pragma unroll
-                for (int ii = 0; ii < 4; ++ii) {
-                    const int i = 4 * g + ii;
-                    const uint4 tv = *reinterpret_cast<const uint4*>(stg + (i + 1) * RP + 16u * tid);
-                    const uint32_t t[4] = {tv.x, tv.y, tv.z, tv.w};
-                    uint32_t Y[4];
-                    const bool ystart = CL && ((y0 + i) % cy == 0);
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint32_t Z = t[kk] - tp[4 * ii + kk];
-                        tc[4 * ii + kk] = t[kk];
-                        Y[kk] = ystart ? Z : Z - Zup[kk];
-                        Zup[kk] = Z;
-                    }
-                    uint32_t Yl = __shfl_up_sync(kFull, Y[3], 1);
-                    const uint32_t ysh = __shfl_sync(kFull, Ysh, i + 1);
-                    if (lane == 0) Yl = ysh;          // warp 0: Ysh = 0 (x = 0, zero boundary)
-                    uint32_t mag = 0;
-                    const uint32_t w0 = zr_pack2((int32_t)(Y[0] - Yl), (int32_t)(Y[1] - Y[0]), mag);
-                    const uint32_t w1 = zr_pack2((int32_t)(Y[2] - Y[1]), (int32_t)(Y[3] - Y[2]), mag);
-                    magor |= mag;
-                    // codes of row i over row i - 1's t (read by this warp one row earlier)
-                    const uint32_t p = lane >> 4, seg = 2u * warp + p;
-                    uint8_t* sp = stg + i * RP + 512u * warp + 256u * p + 16u * ((i * spr + seg) & 7u);
-                    *reinterpret_cast<uint2*>(sp + 8 * (lane & 15)) = make_uint2(w0, w1);
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t Z = t[kk] - tp[kk];
+                    Y[kk] = ystart ? Z : Z - Zup[kk];
+                    Zup[kk] = Z;
                 }
-                tmem_st16(taddr + 16u * g, tc);
+                uint32_t Yl = __shfl_up_sync(kFull, Y[3], 1);
+                const uint32_t ysh = __shfl_sync(kFull, Ysh, i + 1);
+                if (lane == 0) Yl = ysh;          // warp 0: Ysh = 0 (x = 0, zero boundary)
+                uint32_t mag = 0;
+                const uint32_t w0 = zr_pack2((int32_t)(Y[0] - Yl), (int32_t)(Y[1] - Y[0]), mag);
+                const uint32_t w1 = zr_pack2((int32_t)(Y[2] - Y[1]), (int32_t)(Y[3] - Y[2]), mag);
+                magor |= mag;
+                // codes of row i over row i - 1's t (read by this warp one row earlier)
+                const uint32_t p = lane >> 4, seg = 2u * warp + p;
+                uint8_t* sp = stg + i * RP + 512u * warp + 256u * p + 16u * ((i * spr + seg) & 7u);
+                *reinterpret_cast<uint2*>(sp + 8 * (lane & 15)) = make_uint2(w0, w1);
             }
             tmem_wait_st();
             zfirst = false;
