@@ -291,7 +291,7 @@ __device__ __noinline__ void zr_tgroup_slow(uint8_t* stg, uint8_t* msk, uint32_t
 }
 
 // A0: the t-bits of G stage rows r0..r0+G-1 (row 0 = halo), in place.  The fast path for all
-// (one FFMA + FADD + FFMA + FSETP per element).  A hard element (|e| >= hU) in margin mode
+// (one FFMA + FADD + FFMA + FSETP per element).  A hard element (|e| >= w/2) in margin mode
 // is corrected inline from its exact residual e = d - q0 w (|q0 - d/w| <= 1/2 + 1/8, so one
 // step reaches the nearest bin; |e| = w/2 is a tie -> even, R1); margin mode has no value
 // outliers (|fl(q w) - d| <= |e| + U/2 <= eb for |e| <= w/2, SV App. A) and |q| < 2^21.
@@ -301,6 +301,10 @@ __device__ __forceinline__ void zr_tgroup(uint8_t* stg, uint8_t* msk, uint32_t R
                                           int lane, int warp, const QuantP& P)
 {
     const float kMagic = 12582912.0f;
+    // |e| < w/2 suffices in margin mode: q0 is then the unique nearest bin and
+    // |fl(q0 w) - d| < w/2 + U/2 <= eb (SV App. A), so the threshold is h, not h - U;
+    // fallback mode (hU < 0) sends every element to the exact rule
+    const float thr = P.hU < 0.0f ? -1.0f : P.h;
     float dv[G][4];
     uint32_t t[G][4];
     bool hard = false;
@@ -316,7 +320,7 @@ __device__ __forceinline__ void zr_tgroup(uint8_t* stg, uint8_t* msk, uint32_t R
             const float tf = __fmaf_rn(dv[g][k], P.r, kMagic);
             const float qf = __fsub_rn(tf, kMagic);
             const float e = __fmaf_rn(-qf, P.w, dv[g][k]);
-            hard |= !(fabsf(e) < P.hU);
+            hard |= !(fabsf(e) < thr);
             t[g][k] = __float_as_uint(tf);
         }
     }
@@ -346,8 +350,9 @@ __device__ __forceinline__ void zr_tpass(uint8_t* stg, uint8_t* msk, uint32_t RP
                                          int lane, int warp, const QuantP& P)
 {
     if (halo) zr_tgroup<1>(stg, msk, RP, spr, 0, tid, lane, warp, P);
+    // two groups of 4 rows per call: the compiler may then interleave their loads
 #pragma unroll
-    for (int r0 = 1; r0 <= kZrRows; r0 += 4) zr_tgroup<4>(stg, msk, RP, spr, r0, tid, lane, warp, P);
+    for (int r0 = 1; r0 <= kZrRows; r0 += 8) zr_tgroup<8>(stg, msk, RP, spr, r0, tid, lane, warp, P);
 }
 
 // NW = nx / 128 warps; at most ~170 registers per thread (12 warps per SM).
@@ -529,6 +534,11 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
                 tmem_wait_st();
             }
             tmem_ld8(taddr, tpb[0]);
+            // t of the next two rows loaded ahead: the compiler cannot move these loads above
+            // the code stores (it cannot prove the addresses distinct)
+            uint4 tvq[2];
+            tvq[0] = *reinterpret_cast<const uint4*>(stg + 1 * RP + 16u * tid);
+            tvq[1] = *reinterpret_cast<const uint4*>(stg + 2 * RP + 16u * tid);
 #pragma unroll
             for (int i = 0; i < kZrRows; ++i) {
                 uint32_t(&tpp)[8] = tpb[(i >> 1) & 1];
@@ -537,7 +547,8 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
                     if (i + 2 < kZrRows) tmem_ld8(taddr + 4u * (i + 2), tpb[((i >> 1) + 1) & 1]);
                 }
                 const uint32_t* tp = tpp + 4 * (i & 1);
-                const uint4 tv = *reinterpret_cast<const uint4*>(stg + (i + 1) * RP + 16u * tid);
+                const uint4 tv = tvq[i & 1];
+                if (i + 2 < kZrRows) tvq[i & 1] = *reinterpret_cast<const uint4*>(stg + (i + 3) * RP + 16u * tid);
                 const uint32_t t[4] = {tv.x, tv.y, tv.z, tv.w};
                 tmem_st4(taddr + 4u * i, t[0], t[1], t[2], t[3]);
                 uint32_t Y[4];
