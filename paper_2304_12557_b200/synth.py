@@ -23,6 +23,8 @@ Random numbers: splitmix64 (Steele et al.), u(idx, s) = ((mix(s*G + idx + G) >> 
 from __future__ import annotations
 
 import math
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -116,6 +118,17 @@ def _chunks(nz, per):
         z += per
 
 
+def _pmap(fn, chunks):
+    """fn over the chunks on a thread pool (numpy releases the GIL in its array loops);
+    results in chunk order, so reductions over them sum in the same order as a serial loop
+    and every element is the same f64 expression -- bit-identical to the serial evaluation."""
+    chunks = list(chunks)
+    if len(chunks) <= 1:
+        return [fn(*c) for c in chunks]
+    with ThreadPoolExecutor(max_workers=min(len(chunks), os.cpu_count() or 1, 32)) as ex:
+        return list(ex.map(lambda c: fn(*c), chunks))
+
+
 def _plane(shape):
     return int(np.prod(shape[1:])) if len(shape) > 1 else 1
 
@@ -123,15 +136,19 @@ def _plane(shape):
 def sines3d(shape=(64, 64, 64), seed=1, K=6, fmin=0.5, fmax=4.0, noise_rel=1e-3):
     terms = _sine_terms(shape, K, seed, fmin, fmax)
     clean = np.empty(shape, dtype=np.float64)
-    for z0, z1 in _chunks(shape[0], max(1, (1 << 23) // _plane(shape))):
+
+    def fill(z0, z1):
         clean[z0:z1] = _sines_chunk(terms, shape, z0, z1)
+    _pmap(fill, _chunks(shape[0], max(1, (1 << 23) // _plane(shape))))
     rng_ = float(clean.max() - clean.min())
     out = np.empty(shape, dtype=np.float32)
     P = _plane(shape)
-    for z0, z1 in _chunks(shape[0], max(1, (1 << 23) // P)):
+
+    def put(z0, z1):
         n = (z1 - z0) * P
         v = clean[z0:z1].reshape(-1) + _noise(noise_rel * rng_, z0 * P, n, seed)
         out[z0:z1] = v.reshape((z1 - z0,) + tuple(shape[1:])).astype(np.float32)
+    _pmap(put, _chunks(shape[0], max(1, (1 << 23) // P)))
     return out
 
 
@@ -203,17 +220,20 @@ def nyx_rho(shape=(512, 512, 512), seed=4):
     per = max(1, (1 << 23) // _plane(shape))
     n = float(np.prod(shape))
     s1 = 0.0
-    for z0, z1 in _chunks(shape[0], per):
-        s1 += float(_sines_chunk(terms, shape, z0, z1).sum())
+    for v in _pmap(lambda z0, z1: float(_sines_chunk(terms, shape, z0, z1).sum()), _chunks(shape[0], per)):
+        s1 += v
     mean = s1 / n
     s2 = 0.0
-    for z0, z1 in _chunks(shape[0], per):
-        s2 += float(((_sines_chunk(terms, shape, z0, z1) - mean) ** 2).sum())
+    for v in _pmap(lambda z0, z1: float(((_sines_chunk(terms, shape, z0, z1) - mean) ** 2).sum()),
+                   _chunks(shape[0], per)):
+        s2 += v
     std = math.sqrt(s2 / n)
     out = np.empty(shape, dtype=np.float32)
-    for z0, z1 in _chunks(shape[0], per):
+
+    def put(z0, z1):
         g = (_sines_chunk(terms, shape, z0, z1) - mean) / std
         out[z0:z1] = np.exp(1.5 * g).astype(np.float32)
+    _pmap(put, _chunks(shape[0], per))
     return out
 
 
@@ -221,16 +241,21 @@ def nyx_v(shape=(512, 512, 512), seed=44):
     terms = _sine_terms(shape, 6, seed, 0.5, 4.0)
     per = max(1, (1 << 23) // _plane(shape))
     lo, hi = math.inf, -math.inf
-    for z0, z1 in _chunks(shape[0], per):
+
+    def ext(z0, z1):
         c = _sines_chunk(terms, shape, z0, z1)
-        lo, hi = min(lo, float(c.min())), max(hi, float(c.max()))
+        return float(c.min()), float(c.max())
+    for a, b in _pmap(ext, _chunks(shape[0], per)):
+        lo, hi = min(lo, a), max(hi, b)
     amp = 2e-4 * 3e7 * (hi - lo)
     out = np.empty(shape, dtype=np.float32)
     P = _plane(shape)
-    for z0, z1 in _chunks(shape[0], per):
+
+    def put(z0, z1):
         v = 3e7 * _sines_chunk(terms, shape, z0, z1).reshape(-1)
         v = v + _noise(amp, z0 * P, (z1 - z0) * P, seed)
         out[z0:z1] = v.reshape((z1 - z0,) + tuple(shape[1:])).astype(np.float32)
+    _pmap(put, _chunks(shape[0], per))
     return out
 
 
@@ -242,15 +267,24 @@ def rtm(shape=(1008, 1008, 352), seed=5):
     out = np.empty(shape, dtype=np.float32)
     y = np.arange(ny, dtype=np.float64)[None, :, None]
     x = np.arange(nx, dtype=np.float64)[None, None, :]
-    for z0, z1 in _chunks(nz, max(1, (1 << 22) // _plane(shape))):
+    def put(z0, z1):
         z = np.arange(z0, z1, dtype=np.float64)[:, None, None]
-        rr = np.sqrt((z - 20 * sc) ** 2 + (y - ny / 2.0) ** 2 + (x - nx / 2.0) ** 2)
-        acc = np.zeros_like(rr)
+        rr = np.sqrt((z - 20 * sc) ** 2 + (y - ny / 2.0) ** 2 + (x - nx / 2.0) ** 2).reshape(-1)
+        # ricker(s) is exactly 0 for |s| >= 6: the shells are evaluated only where some shell
+        # is live (the same f64 expression per element; 0 / max(rr, 1) = +0 elsewhere)
+        live = np.zeros(rr.shape, dtype=bool)
         for m in range(5):
-            s = (rr - (150 + 60 * t) * sc + 45 * m * sc) / (6 * sc)
+            live |= np.abs((rr - (150 + 60 * t) * sc + 45 * m * sc) / (6 * sc)) < 6
+        r_l = rr[live]
+        acc = np.zeros_like(r_l)
+        for m in range(5):
+            s = (r_l - (150 + 60 * t) * sc + 45 * m * sc) / (6 * sc)
             rk = np.where(np.abs(s) < 6, (1 - 2 * s * s) * np.exp(-s * s), 0.0)
             acc += (0.6 ** m) * rk
-        out[z0:z1] = (acc / np.maximum(rr, 1.0)).astype(np.float32)
+        v = np.zeros(rr.shape, dtype=np.float32)
+        v[live] = (acc / np.maximum(r_l, 1.0)).astype(np.float32)
+        out[z0:z1] = v.reshape((z1 - z0, ny, nx))
+    _pmap(put, _chunks(nz, max(1, (1 << 22) // _plane(shape))))
     return out
 
 
