@@ -40,6 +40,20 @@ WORKLOADS = {
 }
 
 
+# the other BASELINE.json configs, measured at full size after the headline (line["configs"])
+CONFIG_LIST = [
+    ("c1", "sines3d", (64, 64, 64), 1e-3),
+    ("c2_t_1e-2", "cesm_t", (1800, 3600), 1e-2),
+    ("c2_t_1e-3", "cesm_t", (1800, 3600), 1e-3),
+    ("c2_t_1e-4", "cesm_t", (1800, 3600), 1e-4),
+    ("c2_cld_1e-3", "cesm_cld", (1800, 3600), 1e-3),
+    ("c3_u", "hurr_u", (100, 500, 500), 1e-3),
+    ("c3_qsnow", "hurr_qsnow", (100, 500, 500), 1e-3),
+    ("c4_rho_1e-3", "nyx_rho", (512, 512, 512), 1e-3),
+    ("c5_rtm_1e-4", "rtm", (1008, 1008, 352), 1e-4),
+]
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -116,67 +130,270 @@ class ClockSampler:
 
 
 def algorithmic_bytes(kernel: str, n: int, stream_bytes: int, ndim: int):
-    """Algorithmic HBM bytes per launch of each kernel."""
+    """Algorithmic HBM bytes per launch of each kernel: the method's bytes --
+    read the field (4N) and write the stream for compression, read the stream and write the
+    field (4N) for decompression -- attributed to the kernel that moves them.  Intermediates a
+    kernel pipeline keeps in HBM (the int32 x/y-scanned codes between k_decode_planes and the z
+    walk) are NOT algorithmic; they are reported separately (`intermediate_bytes`)."""
     payload = stream_bytes - 128
     return {
         "k_range": 4 * n,
         "k_compress": 4 * n + payload,
-        "k_decode_tiles": payload + 4 * n,
-        "k_decode_planes": payload + 4 * n,
-        "k_scan_sums": 4 * n,
-        "k_scan_apply": 8 * n,
-        "k_scan_walk": 8 * n,
+        "k_decode_tiles": payload,        # stream in; its int32 output is an intermediate
+        "k_decode_planes": payload,
+        "k_scan_walk": 4 * n,             # x^ out; its int32 input is an intermediate
+        "k_scan_apply": 0,
     }.get(kernel)
+
+
+def intermediate_bytes(kernel: str, n: int):
+    return {"k_decode_tiles": 4 * n, "k_decode_planes": 4 * n, "k_scan_walk": 4 * n,
+            "k_scan_apply": 8 * n}.get(kernel, 0)
+
+
+DECODE_IDS = ("k_decode_tiles", "k_decode_planes", "k_scan_walk", "k_scan_apply", "k_scan_sums", "k_xcarry",
+              "k_decode_init", "k_validate_outliers", "k_value_patch", "k_tile_offsets")
+PROF_IDS = ["k_range", "k_compress", "k_compact", "k_decode_tiles", "k_decode_planes", "k_scan_walk",
+            "k_scan_apply", "k_xcarry"]
+
+
+def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_for_parity=True):
+    """One BJ config at full size: asynchronous compress + device-parsed asynchronous decompress
+    per step, CUDA events on the launch stream, L2 flushed before every step; per-kernel CUDA-
+    event times from the library's profiler; CR, PSNR, bound check, rooflines, T_overall."""
+    import torch
+    from paper_2304_12557_b200 import fz
+    dev = torch.device("cuda", 0)
+    d = synth.generate(field_name, shape)
+    n = d.size
+    field = torch.from_numpy(d).to(dev)
+    codec = fz.Codec(shape, dev)
+    xh = torch.empty_like(field)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        codec.compress(field, fz.REL, rel, sync=False)
+        codec.decompress_device(codec.out, out=xh)
+    torch.cuda.synchronize()
+    fz.profile_enable(True)
+    fz.profile_only(PROF_IDS)
+    fz.profile_read()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    for k in range(steps):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        codec.compress(field, fz.REL, rel, sync=False)
+        ev[k][1].record(stream)
+        codec.decompress_device(codec.out, out=xh)
+        ev[k][2].record(stream)
+    torch.cuda.synchronize()
+    size = codec.compress_result()
+    codec.result()
+    prof = fz.profile_read()
+    fz.profile_enable(False)
+    ms_c = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    ms_d = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    gb = d.nbytes / 1e9
+    hdr = header_of(codec.out)
+    payload = size - 128
+    kern = {}
+    for kname, (tot, cnt) in prof.items():
+        kern[kname] = {"ms_per_launch": round(tot / cnt, 4), "launches_per_step": round(cnt / steps, 2)}
+    res = {"workload": f"{name}: {field_name} {'x'.join(map(str, shape))} REL {rel:g}", "dims": list(shape),
+           "rel_eb": rel, "compress_gbs": round(gb / (ms_c / 1e3), 2), "decompress_gbs": round(gb / (ms_d / 1e3), 2),
+           "step_gbs": round(gb / ((ms_c + ms_d) / 1e3), 2), "compress_ms": round(ms_c, 4),
+           "decompress_ms": round(ms_d, 4), "cr": round(d.nbytes / size, 4),
+           "bits_per_value": round(32 * size / d.nbytes, 4), "kernels": kern,
+           "quality": quality(field, xh, hdr.params.eb_abs)}
+    pk = prof.get("k_compress")
+    if pk:
+        t = pk[0] / pk[1]
+        a = (4 * n + payload) / (t / 1e3) / 1e9
+        res["roofline_compress"] = {"kernel": "k_compress", "achieved": round(a, 1), "frac": round(a / peak, 4),
+                                    "ms": round(t, 4)}
+    tdec = sum(v[0] / steps for k, v in prof.items() if k in DECODE_IDS)
+    if tdec > 0:
+        a = (payload + 4 * n) / (tdec / 1e3) / 1e9
+        res["roofline_decoder"] = {"kernels": sorted(k for k in prof if k in DECODE_IDS), "achieved": round(a, 1),
+                                   "frac": round(a / peak, 4), "ms": round(tdec, 4),
+                                   "bytes": "stream + 4N (method), intermediates excluded"}
+    if bw:
+        res["t_overall_gbs"] = {"compress_then_d2h": t_overall(bw["d2h"], d.nbytes / size, res["compress_gbs"]),
+                                "h2d_then_decompress": t_overall(bw["h2d"], d.nbytes / size,
+                                                                 res["decompress_gbs"])}
+    job = None
+    if keep_for_parity:
+        job = (name, d, rel, codec.out[:size].cpu().numpy().copy(), xh.cpu().numpy())
+    del field, xh, codec
+    torch.cuda.empty_cache()
+    return res, job
 
 
 # --------------------------------------------------------------------------------------
 def run_reference(args, wl):
-    """--impl reference: the CPU oracle as it stands, single-threaded, on a bounded sample."""
+    """--impl reference: the CPU oracle as it stands (single-threaded C, test infrastructure),
+    run as independent instances in parallel on the host cores, one per 16-plane z-slab of a
+    bounded sample of the workload (the first 16 x cores planes)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_lib as O
     field, shape, rel, desc = wl
     d = synth.generate(field, shape)
-    planes = min(shape[0], max(1, 16 * (512 * 512) // int(np.prod(shape[1:])))) if len(shape) == 3 else shape[0]
+    ci = cpu_info()
+    cores = max(1, min(ci["usable_cpus"], 64))
+    if len(shape) == 3:
+        per = max(1, 16 * (512 * 512) // int(np.prod(shape[1:])))
+        planes = min(shape[0], per * cores)
+    else:
+        planes = shape[0]
     sample = np.ascontiguousarray(d[:planes])
-    times, size = [], None
+    times, crs, k = [], [], 1
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        st, buf = O.compress(sample, O.REL, rel)
-        st2, xh = O.decompress(buf, sample.size)
-        dt = time.perf_counter() - t0
-        assert st == O.OK and st2 == O.OK
-        size = buf.size
+        v, wall, tc, td, cr, k = oracle_instances(sample, rel, cores)
         if i >= args.warmup:
-            times.append(dt)
+            times.append(wall)
+            crs.append(cr)
     ms = 1e3 * statistics.mean(times)
     v = sample.nbytes / (ms / 1e3) / 1e9
-    samp = f"first {planes} of {shape[0]} planes ({sample.nbytes / 1e6:.1f} MB) of the {args.workload} field"
+    samp = (f"first {planes} of {shape[0]} planes ({sample.nbytes / 1e6:.1f} MB) of the {args.workload} field as "
+            f"{k} independent z-slab instances in parallel")
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "sample": samp},
-            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": samp},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": k, "kind": "oracle", "sample": samp,
+                             **ci},
             "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "cr": round(sample.nbytes / size, 3)}
+            "cr": round(statistics.mean(crs), 3)}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(d: np.ndarray, rel: float):
+def cpu_info():
+    """CPU model, logical CPUs and the CPUs this process may run on."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model, "nproc": os.cpu_count() or 1, "usable_cpus": usable}
+
+
+def _slabs(shape, k):
+    """k z-slabs (whole planes, or whole rows for 2-D) covering the field, as index ranges."""
+    nz = shape[0]
+    k = max(1, min(k, nz))
+    return [(nz * i // k, nz * (i + 1) // k) for i in range(k)]
+
+
+def oracle_instances(d: np.ndarray, rel: float, cores: int):
+    """The CPU oracle as it stands (single-threaded C, test infrastructure) run as `cores`
+    independent instances in parallel, one per z-slab of `d` (one instance per
+    slab / field; ctypes releases the GIL, so the instances run on separate host cores).
+    Returns (GB/s of the whole field, wall s, compress s, decompress s per instance, CR)."""
+    from concurrent.futures import ThreadPoolExecutor
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib as O
+    parts = [np.ascontiguousarray(d[a:b]) for a, b in _slabs(d.shape, cores)]
+
+    def one(part):
+        t0 = time.perf_counter()
+        st, buf = O.compress(part, O.REL, rel)
+        t1 = time.perf_counter()
+        st2, _ = O.decompress(buf, part.size)
+        t2 = time.perf_counter()
+        assert st == O.OK and st2 == O.OK
+        return t1 - t0, t2 - t1, buf.size
+
     t0 = time.perf_counter()
-    st, buf = O.compress(d, O.REL, rel)
-    t1 = time.perf_counter()
-    st2, xh = O.decompress(buf, d.size)
-    t2 = time.perf_counter()
-    assert st == O.OK and st2 == O.OK
-    return {"value": round(d.nbytes / (t2 - t0) / 1e9, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"whole field, compress {t1 - t0:.1f} s + decompress {t2 - t1:.1f} s single-threaded",
-            "compress_gbs": round(d.nbytes / (t1 - t0) / 1e9, 6),
-            "decompress_gbs": round(d.nbytes / (t2 - t1) / 1e9, 6)}, buf
+    with ThreadPoolExecutor(max_workers=len(parts)) as ex:
+        res = list(ex.map(one, parts))
+    wall = time.perf_counter() - t0
+    return (d.nbytes / wall / 1e9, wall, statistics.mean(r[0] for r in res), statistics.mean(r[1] for r in res),
+            d.nbytes / sum(r[2] for r in res), len(parts))
+
+
+def cpu_baseline(d: np.ndarray, rel: float):
+    ci = cpu_info()
+    cores = max(1, min(ci["usable_cpus"], 64))
+    v, wall, tc, td, cr, k = oracle_instances(d, rel, cores)
+    return {"value": round(v, 6), "unit": "GB/s", "cores": k, "kind": "oracle",
+            "sample": f"whole field as {k} independent z-slab instances (one single-threaded oracle per "
+                      f"host core, in parallel): wall {wall:.1f} s; per instance compress {tc:.2f} s + "
+                      f"decompress {td:.2f} s",
+            "per_instance_gbs": round(d.nbytes / k / (tc + td) / 1e9, 6), "slab_cr": round(cr, 4), **ci}
+
+
+def oracle_parity_jobs(jobs, cores):
+    """Full-size parity of GPU results against the oracle, the jobs run in parallel on the host
+    (each job: field, REL bound, the GPU stream bytes, the GPU-decoded field)."""
+    from concurrent.futures import ThreadPoolExecutor
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+
+    def one(job):
+        name, d, rel, gstream, gx = job
+        st, ref = O.compress(d, O.REL, rel)
+        ok_s = st == O.OK and ref.size == gstream.size and np.array_equal(ref, gstream)
+        st2, xr = O.decompress(ref, d.size)
+        ok_x = st2 == O.OK and np.array_equal(xr.view(np.uint32), gx.reshape(-1).view(np.uint32))
+        return name, bool(ok_s), bool(ok_x)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=max(1, min(cores, len(jobs)))) as ex:
+        res = list(ex.map(one, jobs))
+    return {n: {"stream_bytes_equal": a, "field_bits_equal": b} for n, a, b in res}, time.perf_counter() - t0
+
+
+def pcie_bandwidth(dev, nbytes=256 << 20, reps=5):
+    """Pinned host <-> device copy bandwidth (GB/s), CUDA events: the BW of P:478's T_overall."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    g = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    res = {}
+    for name, fn in (("h2d", lambda: g.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(g, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        res[name] = round(nbytes / (min(ts) / 1e3) / 1e9, 2)
+    return res
+
+
+def t_overall(bw_gbs: float, cr: float, t_gbs: float):
+    """T_overall = ((BW x CR)^-1 + T_compr^-1)^-1 (GB/s of original data)."""
+    return round(1.0 / (1.0 / (bw_gbs * cr) + 1.0 / t_gbs), 2)
+
+
+def quality(field, xh, eb_abs: float):
+    """PSNR (20 log10(value range) - 10 log10(MSE)) and max |x - x^| / eb_abs, f64."""
+    x = field.double().reshape(-1)
+    y = xh.double().reshape(-1)
+    err = (x - y).abs()
+    mse = float((err * err).mean().item())
+    vr = float((x.max() - x.min()).item())
+    mx = float(err.max().item())
+    psnr = float("inf") if mse == 0 else 20 * np.log10(vr) - 10 * np.log10(mse)
+    return {"psnr_db": round(psnr, 3), "max_abs_err": mx, "eb_abs": eb_abs,
+            "max_err_over_eb": round(mx / eb_abs, 6) if eb_abs > 0 else None,
+            "bound_holds": bool(mx <= eb_abs)}
+
+
+def header_of(buf):
+    from paper_2304_12557_b200 import fz
+    return fz.peek_header(buf[:128].cpu().numpy().tobytes())
 
 
 def chunk_local_leg(args, gsize, field, flush, stream, rel, d, peak):
@@ -363,22 +580,41 @@ def run_single(args, wl):
         kernels[name] = {"ms_per_launch": round(per, 4), "launches": cnt,
                          "share_of_step": round(tot / (ms * args.steps), 4)}
         if ab is not None:
+            kernels[name]["algorithmic_bytes"] = ab
             kernels[name]["achieved_gbs"] = round(ab / (per / 1e3) / 1e9, 1)
             kernels[name]["frac"] = round(ab / (per / 1e3) / 1e9 / peak, 4)
+        ib = intermediate_bytes(name, n)
+        if ib:
+            kernels[name]["intermediate_bytes"] = ib
     dom = max(prof.items(), key=lambda kv: kv[1][0])[0]
     per = prof[dom][0] / prof[dom][1]
     ab = algorithmic_bytes(dom, n, stream_bytes, len(shape))
     achieved = ab / (per / 1e3) / 1e9
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, dom),
-            "algorithmic_bytes_per_launch": ab, "peak_source": peak_src}
+            "algorithmic_bytes_per_launch": ab, "peak_source": peak_src,
+            "note": "dominant kernel by CUDA-event time; algorithmic bytes = the method's bytes it moves "
+                    "(intermediates excluded)"}
     pc = prof.get("k_compress")
     comp_roof = None
     if pc:
         pk = pc[0] / pc[1]
         abk = algorithmic_bytes("k_compress", n, stream_bytes, len(shape))
         comp_roof = {"kernel": "k_compress", "achieved": round(abk / (pk / 1e3) / 1e9, 1),
-                     "frac": round(abk / (pk / 1e3) / 1e9 / peak, 4), "ms": round(pk, 4)}
+                     "frac": round(abk / (pk / 1e3) / 1e9 / peak, 4), "ms": round(pk, 4),
+                     "traffic": ncu_traffic(args.workload, "k_compress"), "algorithmic_bytes_per_launch": abk}
+    tdec = sum(v[0] / args.steps for k, v in prof.items() if k in DECODE_IDS)
+    dec_roof = None
+    if tdec > 0:
+        abd = (stream_bytes - 128) + 4 * n
+        dec_roof = {"kernels": sorted(k for k in prof if k in DECODE_IDS), "achieved": round(abd / (tdec / 1e3) / 1e9, 1),
+                    "frac": round(abd / (tdec / 1e3) / 1e9 / peak, 4), "ms": round(tdec, 4),
+                    "algorithmic_bytes_per_step": abd,
+                    "intermediate_bytes_per_step": sum(intermediate_bytes(k, n) for k in prof if k in DECODE_IDS)}
+    hdr = header_of(codec.out)
+    qual = quality(field, xh, hdr.params.eb_abs)
+    bw = pcie_bandwidth(dev)
+    parity_jobs = [("c4_v_1e-3 (main)", d, rel, buf[:stream_bytes].cpu().numpy().copy(), xh.cpu().numpy())]
 
     # ---- the other REL bounds of SV 8.d on the same field (CR and throughput, same method) ----
     by_rel = {}
@@ -399,9 +635,12 @@ def run_single(args, wl):
         codec.result()
         mc = statistics.mean(e[0].elapsed_time(e[1]) for e in ev2)
         md = statistics.mean(e[1].elapsed_time(e[2]) for e in ev2)
+        h2 = header_of(codec.out)
         by_rel[f"{r2:g}"] = {"cr": round(d.nbytes / sz2, 4), "compress_gbs": round(gb / (mc / 1e3), 2),
                              "decompress_gbs": round(gb / (md / 1e3), 2),
-                             "step_gbs": round(gb / ((mc + md) / 1e3), 2)}
+                             "step_gbs": round(gb / ((mc + md) / 1e3), 2),
+                             "quality": quality(field, xh, h2.params.eb_abs)}
+        parity_jobs.append((f"c4_v_{r2:g}", d, r2, codec.out[:sz2].cpu().numpy().copy(), xh.cpu().numpy()))
     # restore the REL 1e-3 stream and field (checked below against the e2e lanes and the oracle)
     codec.compress(field, fz.REL, rel, sync=False)
     codec.decompress_device(codec.out, out=xh)
@@ -494,7 +733,11 @@ def run_single(args, wl):
         "compress_gbs": round(gb / (ms_c / 1e3), 2), "decompress_gbs": round(gb / (ms_d / 1e3), 2),
         "compress_ms": round(ms_c, 4), "decompress_ms": round(ms_d, 4),
         "cr": round(d.nbytes / stream_bytes, 4), "bits_per_value": round(32 * stream_bytes / d.nbytes, 4),
-        "roofline": roof, "roofline_compress_kernel": comp_roof, "kernels": kernels,
+        "roofline": roof, "roofline_compress_kernel": comp_roof, "roofline_decoder": dec_roof, "kernels": kernels,
+        "quality": qual, "pcie_gbs": bw,
+        "t_overall_gbs": {"model": "P:478 T_overall = ((BW x CR)^-1 + T^-1)^-1, BW = measured pinned PCIe copy",
+                          "compress_then_d2h": t_overall(bw["d2h"], d.nbytes / stream_bytes, gb / (ms_c / 1e3)),
+                          "h2d_then_decompress": t_overall(bw["h2d"], d.nbytes / stream_bytes, gb / (ms_d / 1e3))},
         "chunk_local": chunk_local,
         "by_rel": by_rel,
         "clocks": sampler.summary(), "gpu_launches": launches,
@@ -505,10 +748,26 @@ def run_single(args, wl):
                         "three streams, staggered (copies in opposite directions overlap on the full-duplex "
                         "PCIe link); device span / steps"},
     }
+    # ---- the other BASELINE.json configs at full size (one entry each, same method) ----
+    if not args.no_configs:
+        del field, xh, codec, lanes
+        torch.cuda.empty_cache()
+        configs = {}
+        for cname, fname, cshape, crel in CONFIG_LIST:
+            res, job = measure_config(cname, fname, cshape, crel, flush, min(args.steps, 10), peak, bw,
+                                      keep_for_parity=not args.no_cpu_baseline)
+            configs[cname] = res
+            if job is not None:
+                parity_jobs.append(job)
+        line["configs"] = configs
     if not args.no_cpu_baseline:
-        cb, ref = cpu_baseline(d, rel)
-        line["cpu_baseline"] = cb
-        line["parity_vs_oracle"] = bool(ref.size == stream_bytes and np.array_equal(ref, buf[:stream_bytes].cpu().numpy()))
+        ci = cpu_info()
+        par, wall = oracle_parity_jobs(parity_jobs, ci["usable_cpus"])
+        line["parity_vs_oracle"] = all(v["stream_bytes_equal"] and v["field_bits_equal"] for v in par.values())
+        line["parity_detail"] = {"checked": par, "wall_s": round(wall, 1),
+                                 "how": "oracle compress + decompress of each full field on the host (parallel "
+                                        "instances); GPU stream byte-equal and decoded field bit-equal"}
+        line["cpu_baseline"] = cpu_baseline(d, rel)
     print(json.dumps(line), flush=True)
 
 
@@ -519,7 +778,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fz", choices=["fz", "reference"])
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU oracle (baseline and parity)")
+    ap.add_argument("--no-configs", action="store_true", help="only the c4 headline workload")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

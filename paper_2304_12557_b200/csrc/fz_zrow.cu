@@ -282,7 +282,9 @@ __device__ __noinline__ void zr_tgroup_slow(uint8_t* stg, uint8_t* msk, uint32_t
             row[k] = t;
         }
         const int r = r0 + g;
-        if (vb && r >= 1) {   // own rows only (row 0 is the halo)
+        // own rows only (row 0 is the halo); no marks in a seed step (msk == null): its plane
+        // is not encoded, and stale marks would reach the stage's next phase B
+        if (vb && r >= 1 && msk != nullptr) {
             const uint32_t seg = 2u * warp + (lane >> 4);
             atomicOr(reinterpret_cast<unsigned long long*>(msk + 16 * ((r - 1) * spr + seg)),
                      (unsigned long long)vb << (4 * (lane & 15)));
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
         }
         const bool halo = y0 > 0 && !(CL && y0 % cy == 0);
         // A0: t-bits in place (rows 1..16, and row 0 when the halo row is used)
-        zr_tpass(stg, msk, RP, spr, halo, tid, lane, warp, P);
+        zr_tpass(stg, st.seed ? nullptr : msk, RP, spr, halo, tid, lane, warp, P);
         __syncwarp();
         uint32_t tshn = kMagicBits;
         if (shv) {

@@ -518,3 +518,19 @@ def test_cuda_graph_step_matches_direct_calls():
         codec.result()
         _assert_stream_equal(codec.out[:ref_size].cpu().numpy(), ref, "graph")
         assert np.array_equal(out.cpu().numpy().reshape(-1).view(np.uint32), xref.view(np.uint32))
+
+
+def test_row_walker_fallback_value_outliers_across_runs():
+    """Row-walking compressor (nx % 128 == 0, ny % 16 == 0) in fallback mode (R2) with value
+    outliers (R20: |q| >= 2^21) spread over every plane, on a field whose band runs are long
+    enough that CTAs take seed steps and then reuse the seed's stage: the seed plane's outlier
+    marks must not reach a later plane's outlier lists."""
+    nz, ny, nx = 512, 32, 128
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    s = np.sin(0.02 * z + 0.03 * y + 0.025 * x + 1.0)
+    d = (2.0 ** 21 * 1.000001 * s).astype(np.float32)   # |d| >= 2^21 - 1/2 on ~0.1 % of elements
+    # (2112 value outliers, 16788 delta-outliers: both below the N/64 + 1024 staging size, so
+    # the single-pass path -- not the rescan -- produces the stream)
+    ref = _check_full(d, O.ABS, 0.5, "fallback-runs")
+    info = fz.peek_header(ref[:128].tobytes())
+    assert info.params.fallback == 1 and 0 < info.counts.n_value < d.size // 64
