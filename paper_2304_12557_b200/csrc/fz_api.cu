@@ -601,6 +601,45 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         if (hc.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;
         return FZ_OK;
     }
+    if (decode_uses_dzr(I.shape) && !(exp_bits() & 32768)) {
+        // row-walking decoder: no int32 intermediate field (fz_dzr.cu)
+        const DzrLayout Z = dzr_layout(I.shape);
+        DzrArgs z{};
+        z.flags = a.flags;
+        z.payload = a.payload;
+        z.drec = a.drec;
+        z.nnz_total = a.nnz_total;
+        z.nd = a.nd;
+        z.dev = a.dev;
+        z.wp = a.wp;
+        z.w = a.w;
+        z.ctrl = ctrl;
+        z.loc = loc;
+        z.bpre = bsum;
+        z.drange = drange;
+        z.q_out = q;
+        z.nx = (uint32_t)I.shape.dims[2];
+        z.nz = (uint32_t)I.shape.dims[0];
+        z.P = (uint32_t)(I.shape.dims[1] * I.shape.dims[2]);
+        z.tpp = z.P / kTileCodes;
+        z.nbands = Z.nbands;
+        z.nchunks = Z.nchunks;
+        z.cdelta = reinterpret_cast<int32_t*>(wb + L.dzr_cdelta);
+        z.dsum = reinterpret_cast<int32_t*>(wb + L.dzr_dsum);
+        z.cd = reinterpret_cast<int32_t*>(wb + L.dzr_cd);
+        FZ_CUDA(launch_decode_dzr(z, st));
+        if (deq) {
+            if (dev) FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
+            else FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+        }
+        if (async) return FZ_OK;
+        Ctrl hz;
+        FZ_CUDA(cudaMemcpyAsync(&hz, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+        FZ_CUDA(cudaStreamSynchronize(st));
+        if (hz.err != 0) return err_status(hz.err);
+        if (!dev && hz.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;
+        return FZ_OK;
+    }
     FZ_CUDA(launch_decode_tiles(a, st, fuse_y));
     // x carries exist when some tile starts inside a row (always for 1-D fields)
     const bool carries = T > 1 && (g.ndim == 1 || !(g.nx <= kTileCodes && kTileCodes % g.nx == 0));
@@ -871,7 +910,7 @@ const char* fz_kernel_name(int id)
                                   "k_decode_init", "k_validate_outliers", "k_decode_tiles",
                                   "k_scan_sums", "k_scan_chunks", "k_scan_apply", "k_value_patch",
                                   "k_outliers", "k_tile_offsets", "k_xcarry", "k_slab", "k_decode_planes",
-                                  "k_scan_walk", "k_compact"};
+                                  "k_scan_walk", "k_compact", "k_dzr_sum", "k_dzr_prep", "k_dzr_main"};
     return (id >= 0 && id < fz::K_COUNT) ? names[id] : "?";
 }
 

@@ -57,6 +57,12 @@ DecodeLayout decode_layout(const fz_shape& s)
     L.sums = off;   off = al(off + 4 * sums);
     L.drange = off; off = al(off + 4 * (T + 1));
     L.ycarry = off; off = al(off + (decode_fuses_y(s) ? 4 * kMaxYseg * nz * nx : 0));
+    {
+        const DzrLayout Z = dzr_layout(s);   // zero sizes unless the row-walking decoder applies
+        L.dzr_cdelta = off; off = al(off + 4 * Z.cdelta_elems);
+        L.dzr_dsum = off;   off = al(off + 4 * Z.dsum_elems);
+        L.dzr_cd = off;     off = al(off + 4 * Z.cd_elems);
+    }
     L.sums_elems = sums;
     L.total = off;
     return L;

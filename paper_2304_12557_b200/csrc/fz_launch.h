@@ -18,7 +18,7 @@ void set_variant_bits(int v);
 enum KernelId {
     K_INIT = 0, K_RANGE, K_PARAMS, K_COMPRESS, K_FINALIZE, K_DINIT, K_VALIDATE, K_DECODE,
     K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_SLAB, K_DECODE_PLANES, K_SCAN_WALK,
-    K_COMPACT, K_COUNT
+    K_COMPACT, K_DZR_SUM, K_DZR_PREP, K_DZR_MAIN, K_COUNT
 };
 
 // Counts one launch of `id` and, when profiling is on, brackets it with CUDA events on the
@@ -86,9 +86,36 @@ struct DecodeArgs {
 // one plane and there are enough planes to fill the GPU.
 bool decode_fuses_y(const fz_shape& s);
 
+// Row-walking decoder (fz_dzr.cu): 3-D, nx % 128 == 0, nx <= 1024, ny % 16 == 0.
+struct DzrArgs {
+    const uint8_t* flags;
+    const uint8_t* payload;
+    const uint2* drec;
+    uint64_t nnz_total, nd;
+    int dev;                    // 1: counts from ctrl (device-parsed header)
+    const float* wp;            // device bin width (dev mode), else null
+    float w;                    // > 0: dequantize; 0: integer codes out
+    Ctrl* ctrl;
+    const uint32_t* loc;
+    const uint32_t* bpre;
+    const uint32_t* drange;
+    int32_t* q_out;
+    uint32_t nx, nz, P, tpp, nbands, nchunks;
+    int32_t* cdelta;            // [nbands][nz][nx]  column delta sums -> V (y carries)
+    int32_t* dsum;              // [nbands][nchunks][16][nx] chunk delta sums -> prefixes
+    int32_t* cd;                // [nbands][nchunks][nx] chunk column sums -> G
+};
+struct DzrLayout {
+    uint32_t nbands, nchunks;
+    uint64_t cdelta_elems, dsum_elems, cd_elems;
+};
+bool decode_uses_dzr(const fz_shape& s);
+DzrLayout dzr_layout(const fz_shape& s);
+cudaError_t launch_decode_dzr(const DzrArgs& a, cudaStream_t st);
+
 constexpr uint32_t kMaxYseg = 8;   // plane segments (CTAs) per plane in k_decode_planes
 struct DecodeLayout {
-    size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, drange, ycarry, total;
+    size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, drange, ycarry, dzr_cdelta, dzr_dsum, dzr_cd, total;
     uint64_t sums_elems;
 };
 DecodeLayout decode_layout(const fz_shape& s);

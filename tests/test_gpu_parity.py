@@ -534,3 +534,53 @@ def test_row_walker_fallback_value_outliers_across_runs():
     ref = _check_full(d, O.ABS, 0.5, "fallback-runs")
     info = fz.peek_header(ref[:128].tobytes())
     assert info.params.fallback == 1 and 0 < info.counts.n_value < d.size // 64
+
+
+# Row-walking decoder (fz_dzr.cu): 3-D, nx in {128, 256, 512, 1024}, ny % 16 == 0 -- bands of
+# 16 rows, chunks of 16 planes (ragged last chunk), several bands and chunks, CTAs taking more
+# than one unit; checked against the oracle's sequential recurrence bit for bit.
+DZR = [
+    ("nx128", lambda: synth.generate("sines3d", (37, 48, 128))),
+    ("nx256", lambda: synth.generate("nyx_rho", (33, 32, 256))),
+    ("nx512", lambda: synth.generate("nyx_v", (40, 64, 512))),
+    ("nx1024", lambda: synth.generate("hurr_u", (18, 16, 1024))),
+    ("one_band", lambda: synth.generate("rtm", (70, 16, 512))),
+    ("many_units", lambda: synth.generate("nyx_v", (160, 128, 256))),
+    ("nz2", lambda: synth.generate("sines3d", (2, 32, 128))),
+]
+
+
+@pytest.mark.parametrize("name,gen", DZR, ids=[s[0] for s in DZR])
+@pytest.mark.parametrize("rel", [1e-2, 1e-4])
+def test_row_walking_decoder_parity(name, gen, rel):
+    d = gen()
+    ref = _check_full(d, O.REL, rel, f"dzr-{name}@{rel}")
+    # the device-parsed asynchronous decode and the integer-code hook take the same kernels
+    codec = fz.Codec(d.shape, DEV)
+    buf = torch.from_numpy(ref).to(DEV)
+    xh = codec.decompress_device(buf)
+    codec.result()
+    st, xref = O.decompress(ref, d.size)
+    assert np.array_equal(xh.cpu().numpy().reshape(-1).view(np.uint32), xref.view(np.uint32))
+    st, qref = O.decode_q(ref, d.size)
+    assert np.array_equal(fz.debug_decode_q(buf, d.shape).cpu().numpy().reshape(-1), qref)
+
+
+def test_row_walking_decoder_outliers_and_old_path_equal():
+    """delta- and value-outliers through the row-walking decoder, and the same stream decoded by
+    the tile decoder + z walk (variant bit 32768) gives the same bits."""
+    d = synth.generate("nyx_rho", (50, 32, 512)).copy()
+    eb = float(d.max() - d.min()) * 1e-4
+    rng = np.random.default_rng(12)
+    idx = rng.choice(d.size, 400, replace=False)
+    d.reshape(-1)[idx] += np.float32(50.0) * np.float32(d.max() - d.min())
+    ref = _check_full(d, O.ABS, eb, "dzr_outliers")
+    assert int.from_bytes(ref[96:104].tobytes(), "little") > 0      # delta outliers present
+    buf = torch.from_numpy(ref).to(DEV)
+    a = fz.decompress(buf)
+    fz.debug_set_variant(32768)
+    try:
+        b = fz.decompress(buf)
+    finally:
+        fz.debug_set_variant(0)
+    assert np.array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))

@@ -13,6 +13,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     d = np.load(cache) if os.path.exists(cache) else synth.generate(field, shape)
     if not os.path.exists(cache):
         np.save(cache, d)
+    fz.debug_set_variant(int(os.environ.get("FZ_EXP", "0")))
     x = torch.from_numpy(d).cuda()
     c = fz.Codec(shape, "cuda")
     buf, size = c.compress(x, fz.REL, rel)
