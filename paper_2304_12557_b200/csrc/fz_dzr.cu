@@ -454,10 +454,15 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_main(DzrArgs a)
     auto tile_of = [&](const DzrCur& q) { return q.z * tpp + q.b * NW + warp; };
     DzrCur nxt = cur;
     DzrIn in_next;
+    auto vrow = [&](const DzrCur& q) {   // the band's y carries at plane q.z
+        return *reinterpret_cast<const uint4*>(a.cdelta + ((uint64_t)q.b * nz + q.z) * nx + x0);
+    };
+    uint4 vy = make_uint4(0, 0, 0, 0);
     if (cur.valid) {
         dzr_gather(a, dzr_in(a, tile_of(cur)), dsm + trow, lane);
         nxt = dzr_next(a, cur);
         in_next = dzr_in(a, nxt.valid ? tile_of(nxt) : tile_of(cur));
+        vy = vrow(cur);
     }
     for (uint32_t k = 0; cur.valid; ++k) {
         const uint32_t b = cur.b, c = cur.c, z = cur.z;
@@ -518,17 +523,17 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_main(DzrArgs a)
             tmem_wait_st();
         }
         uint8_t* buf = dsm + (k & 1u) * S::buf;
-        // y carry of the band at plane z (issued before the tile decode)
-        const uint4 vy = *reinterpret_cast<const uint4*>(a.cdelta + ((uint64_t)b * nz + z) * nx + x0);
         dzr_tile<NW, true>(a, tile_of(cur), buf + trow, lane);
         __syncthreads();
-        // the next plane's gather into the other buffer (every warp is past its phase A)
+        uint32_t cy[4] = {vy.x, vy.y, vy.z, vy.w};
+        // the next plane's gather into the other buffer (every warp is past its phase A) and
+        // its y carries (a plane ahead)
         if (nxt.valid) {
             dzr_gather(a, in_next, dsm + ((k + 1) & 1u) * S::buf + trow, lane);
             const DzrCur n2 = dzr_next(a, nxt);
             if (n2.valid) in_next = dzr_in(a, tile_of(n2));
+            vy = vrow(nxt);
         }
-        uint32_t cy[4] = {vy.x, vy.y, vy.z, vy.w};
         uint32_t tpb[2][8];
         tmem_ld8(taddr, tpb[0]);
         int32_t* o = a.q_out + (uint64_t)z * PL + (uint64_t)(b * kDzrRows) * nx + x0;
@@ -593,6 +598,10 @@ static cudaError_t dzr_launch(const DzrArgs& a, cudaStream_t st)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total);
         uint64_t grid = (uint64_t)dzr_per_sm<NW>((const void*)kern, S::total, false) * num_sms();
         if (grid > U) grid = U;
+        if (variant_bits() & 65536) {
+            const uint64_t per = (U + grid - 1) / grid;
+            grid = (U + per - 1) / per;
+        }
         LaunchProf lp(K_DZR_SUM, st);
         kern<<<(unsigned)grid, 32 * NW, S::total, st>>>(a);
         cudaError_t e = cudaGetLastError();
@@ -626,6 +635,10 @@ static cudaError_t dzr_launch(const DzrArgs& a, cudaStream_t st)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total);
         uint64_t grid = (uint64_t)dzr_per_sm<NW>((const void*)kern, S::total, true) * num_sms();
         if (grid > U) grid = U;
+        if (variant_bits() & 65536) {   // A/B: every CTA the same number of units
+            const uint64_t per = (U + grid - 1) / grid;
+            grid = (U + per - 1) / per;
+        }
         LaunchProf lp(K_DZR_MAIN, st);
         kern<<<(unsigned)grid, 32 * NW, S::total, st>>>(a);
         return cudaGetLastError();
