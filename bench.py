@@ -51,6 +51,8 @@ CONFIG_LIST = [
     ("c3_qsnow", "hurr_qsnow", (100, 500, 500), 1e-3),
     ("c4_rho_1e-3", "nyx_rho", (512, 512, 512), 1e-3),
     ("c5_rtm_1e-4", "rtm", (1008, 1008, 352), 1e-4),
+    # f3 (SV 8.f): HACC-shaped 1-D field, point-wise relative bound via the log transform
+    ("f3_hacc_pwrel_1e-3", "hacc_x", (280953867,), 1e-3, "pwrel"),
 ]
 
 
@@ -143,27 +145,37 @@ def algorithmic_bytes(kernel: str, n: int, stream_bytes: int, ndim: int):
         "k_decode_planes": payload,
         "k_scan_walk": 4 * n,             # x^ out; its int32 input is an intermediate
         "k_scan_apply": 0,
+        # row-walking decoder: pass 2 reads the whole stream and writes x^ (the method's bytes);
+        # pass 1 re-reads the stream to build the carries (not algorithmic: 0)
+        "k_dzr_main": payload + 4 * n,
+        "k_dzr_sum": 0,
+        "k_dzr_prep": 0,
     }.get(kernel)
 
 
 def intermediate_bytes(kernel: str, n: int):
+    """HBM bytes of decoder intermediates per launch: the int32 field of the tile/plane decoders;
+    for the row-walking decoder the carry arrays (column sums N/16 x 4 B written by pass 1 and
+    read by pass 2, chunk sums N/16 x 4 B; 3-D shapes with 16-row bands and 16-plane chunks)."""
     return {"k_decode_tiles": 4 * n, "k_decode_planes": 4 * n, "k_scan_walk": 4 * n,
-            "k_scan_apply": 8 * n}.get(kernel, 0)
+            "k_scan_apply": 8 * n, "k_dzr_sum": n // 2, "k_dzr_prep": n, "k_dzr_main": n // 2}.get(kernel, 0)
 
 
 DECODE_IDS = ("k_decode_tiles", "k_decode_planes", "k_scan_walk", "k_scan_apply", "k_scan_sums", "k_xcarry",
-              "k_decode_init", "k_validate_outliers", "k_value_patch", "k_tile_offsets")
+              "k_decode_init", "k_validate_outliers", "k_value_patch", "k_tile_offsets", "k_dzr_sum",
+              "k_dzr_prep", "k_dzr_main")
 PROF_IDS = ["k_range", "k_compress", "k_compact", "k_decode_tiles", "k_decode_planes", "k_scan_walk",
-            "k_scan_apply", "k_xcarry"]
+            "k_scan_apply", "k_xcarry", "k_dzr_sum", "k_dzr_prep", "k_dzr_main"]
 
 
-def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_for_parity=True):
+def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_for_parity=True, mode_name="rel"):
     """One BJ config at full size: asynchronous compress + device-parsed asynchronous decompress
     per step, CUDA events on the launch stream, L2 flushed before every step; per-kernel CUDA-
     event times from the library's profiler; CR, PSNR, bound check, rooflines, T_overall."""
     import torch
     from paper_2304_12557_b200 import fz
     dev = torch.device("cuda", 0)
+    mode = fz.PWREL if mode_name == "pwrel" else fz.REL
     d = synth.generate(field_name, shape)
     n = d.size
     field = torch.from_numpy(d).to(dev)
@@ -171,7 +183,7 @@ def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_fo
     xh = torch.empty_like(field)
     stream = torch.cuda.current_stream()
     for _ in range(3):
-        codec.compress(field, fz.REL, rel, sync=False)
+        codec.compress(field, mode, rel, sync=False)
         codec.decompress_device(codec.out, out=xh)
     torch.cuda.synchronize()
     fz.profile_enable(True)
@@ -181,7 +193,7 @@ def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_fo
     for k in range(steps):
         flush.fill_(k & 0xFF)
         ev[k][0].record(stream)
-        codec.compress(field, fz.REL, rel, sync=False)
+        codec.compress(field, mode, rel, sync=False)
         ev[k][1].record(stream)
         codec.decompress_device(codec.out, out=xh)
         ev[k][2].record(stream)
@@ -198,12 +210,14 @@ def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_fo
     kern = {}
     for kname, (tot, cnt) in prof.items():
         kern[kname] = {"ms_per_launch": round(tot / cnt, 4), "launches_per_step": round(cnt / steps, 2)}
-    res = {"workload": f"{name}: {field_name} {'x'.join(map(str, shape))} REL {rel:g}", "dims": list(shape),
+    res = {"workload": f"{name}: {field_name} {'x'.join(map(str, shape))} {mode_name.upper()} {rel:g}", "dims": list(shape),
            "rel_eb": rel, "compress_gbs": round(gb / (ms_c / 1e3), 2), "decompress_gbs": round(gb / (ms_d / 1e3), 2),
            "step_gbs": round(gb / ((ms_c + ms_d) / 1e3), 2), "compress_ms": round(ms_c, 4),
            "decompress_ms": round(ms_d, 4), "cr": round(d.nbytes / size, 4),
            "bits_per_value": round(32 * size / d.nbytes, 4), "kernels": kern,
-           "quality": quality(field, xh, hdr.params.eb_abs)}
+           "quality": quality(field, xh, hdr.params.eb_abs) if mode_name != "pwrel" else quality_pwrel(field, xh, rel)}
+    if mode_name == "pwrel":
+        res["transform"] = "f3: y = log32(x) compressed with the ABS bound of R25 (eb_abs on y), x^ = exp32(y^)"
     pk = prof.get("k_compress")
     if pk:
         t = pk[0] / pk[1]
@@ -222,7 +236,7 @@ def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_fo
                                                                  res["decompress_gbs"])}
     job = None
     if keep_for_parity:
-        job = (name, d, rel, codec.out[:size].cpu().numpy().copy(), xh.cpu().numpy())
+        job = (name, d, rel, codec.out[:size].cpu().numpy().copy(), xh.cpu().numpy(), mode_name)
     del field, xh, codec
     torch.cuda.empty_cache()
     return res, job
@@ -338,8 +352,9 @@ def oracle_parity_jobs(jobs, cores):
     import oracle_lib as O
 
     def one(job):
-        name, d, rel, gstream, gx = job
-        st, ref = O.compress(d, O.REL, rel)
+        name, d, rel, gstream, gx = job[:5]
+        mode = O.PWREL if (len(job) > 5 and job[5] == "pwrel") else O.REL
+        st, ref = O.compress(d, mode, rel)
         ok_s = st == O.OK and ref.size == gstream.size and np.array_equal(ref, gstream)
         st2, xr = O.decompress(ref, d.size)
         ok_x = st2 == O.OK and np.array_equal(xr.view(np.uint32), gx.reshape(-1).view(np.uint32))
@@ -389,6 +404,19 @@ def quality(field, xh, eb_abs: float):
     return {"psnr_db": round(psnr, 3), "max_abs_err": mx, "eb_abs": eb_abs,
             "max_err_over_eb": round(mx / eb_abs, 6) if eb_abs > 0 else None,
             "bound_holds": bool(mx <= eb_abs)}
+
+
+def quality_pwrel(field, xh, eps: float):
+    """f3: max point-wise relative error |x^ - x| / |x| against eps, and PSNR."""
+    x = field.double().reshape(-1)
+    y = xh.double().reshape(-1)
+    rel = ((x - y).abs() / x.abs()).max().item()
+    err = (x - y).abs()
+    mse = float((err * err).mean().item())
+    vr = float((x.max() - x.min()).item())
+    psnr = float("inf") if mse == 0 else 20 * np.log10(vr) - 10 * np.log10(mse)
+    return {"psnr_db": round(psnr, 3), "max_rel_err": rel, "eps": eps, "max_rel_err_over_eps": round(rel / eps, 6),
+            "bound_holds": bool(rel <= eps)}
 
 
 def header_of(buf):
@@ -510,7 +538,7 @@ def run_single(args, wl):
     fz.profile_enable(True)
     # events only around the large kernels (the roofline's dominant kernel is one of them);
     # event records around every small launch would add host work inside the timed region
-    fz.profile_only(["k_range", "k_compress", "k_decode_tiles", "k_decode_planes", "k_scan_walk", "k_scan_apply"])
+    fz.profile_only(PROF_IDS)
     fz.profile_read()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     launches = 0
@@ -753,9 +781,11 @@ def run_single(args, wl):
         del field, xh, codec, lanes
         torch.cuda.empty_cache()
         configs = {}
-        for cname, fname, cshape, crel in CONFIG_LIST:
+        for cfg in CONFIG_LIST:
+            cname, fname, cshape, crel = cfg[:4]
             res, job = measure_config(cname, fname, cshape, crel, flush, min(args.steps, 10), peak, bw,
-                                      keep_for_parity=not args.no_cpu_baseline)
+                                      keep_for_parity=not args.no_cpu_baseline,
+                                      mode_name=cfg[4] if len(cfg) > 4 else "rel")
             configs[cname] = res
             if job is not None:
                 parity_jobs.append(job)

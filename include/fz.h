@@ -28,7 +28,16 @@
 extern "C" {
 #endif
 
-typedef enum { FZ_EB_ABS = 0, FZ_EB_REL = 1 } fz_eb_mode;   /* REL = eb * (max-min) */
+/* FZ_EB_ABS: |x^ - x| <= eb.  FZ_EB_REL: eb_abs = eb * (max - min).
+ * FZ_EB_PWREL (f3, "transform the original data using a logarithmic function and
+ * compress the log-transformed data with the corresponding absolute error bound"): the
+ * point-wise relative bound |x^ - x| <= eb |x|, 0 < eb < 1, for fields of positive normal
+ * floats (x >= FLT_MIN; zero, negative or subnormal -> FZ_ERR_ARG, NaN/Inf ->
+ * FZ_ERR_NONFINITE).  y = log x (reading R25: a fixed binary64 sequence rounded once) is
+ * compressed with the ABS bound of R25 and the decoder returns x^ = exp y^; header flag bit 3.
+ * Needs fz_workspace_bytes_mode(s, FZ_EB_PWREL) of compress workspace (the log field lives
+ * there); not combinable with FZ_CHUNK_LOCAL or the slab API (FZ_ERR_ARG). */
+typedef enum { FZ_EB_ABS = 0, FZ_EB_REL = 1, FZ_EB_PWREL = 2 } fz_eb_mode;
 
 /* f1 ("chunked data blocks can be compressed independently"): OR
  * into eb_mode of fz_compress / fz_compress_async to select the chunk-local Lorenzo
@@ -97,6 +106,8 @@ typedef struct {
 size_t fz_compress_bound(const fz_shape* s);
 /* Device workspace needed by fz_compress / fz_compress_with_params / slab calls. */
 size_t fz_workspace_bytes(const fz_shape* s);
+/* The same for a given eb_mode: FZ_EB_PWREL adds 4N bytes (the log field). */
+size_t fz_workspace_bytes_mode(const fz_shape* s, int eb_mode);
 /* Device workspace needed by fz_decompress. */
 size_t fz_decompress_workspace_bytes(const fz_shape* s);
 

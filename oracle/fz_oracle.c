@@ -84,6 +84,65 @@ int fzo_range(const float* d, uint64_t n, float* mn, float* mx, int64_t* first_b
     return FZO_OK;
 }
 
+/* ------------------------------------------------------------------------------------ */
+/* f3 log transform, reading R25: natural log and exp as fixed binary64 operation  */
+/* sequences (no libm, no FMA contraction), so the transform is a defined function.       */
+/* ------------------------------------------------------------------------------------ */
+/* ln 2 split (Cody-Waite): LN2_HI has 32 trailing zero bits, so k * LN2_HI is exact */
+#define FZO_LN2_HI 6.93147180369123816490e-01
+#define FZO_LN2_LO 1.90821492927058770002e-10
+#define FZO_INV_LN2 1.4426950408889634074
+#define FZO_SQRT_HALF 0.70710678118654752440
+
+/* log v = e ln2 + 2 atanh(s), v = m 2^e, m in [sqrt(1/2), sqrt(2)), s = (m - 1) / (m + 1):
+ * 2 atanh(s) = 2 s (1 + s^2/3 + s^4/5 + ... + s^22/23), |s| <= 0.1716 (truncation < 1e-20). */
+double fzo_log64(double v)
+{
+    int e, k;
+    double m = frexp(v, &e), s, z, p;
+    if (m < FZO_SQRT_HALF) { m = m * 2.0; e = e - 1; }
+    s = (m - 1.0) / (m + 1.0);
+    z = s * s;
+    p = 1.0 / 23.0;
+    for (k = 10; k >= 0; --k) p = p * z + 1.0 / (double)(2 * k + 1);
+    return (double)e * FZO_LN2_HI + ((double)e * FZO_LN2_LO + 2.0 * s * p);
+}
+
+/* exp t = 2^k e^r, k = rint(t / ln2), r = (t - k LN2_HI) - k LN2_LO (|r| <= 0.35):
+ * e^r = 1 + r (1 + r/2 (1 + r/3 (... (1 + r/17)))) (truncation < 1e-21). */
+double fzo_exp64(double t)
+{
+    int n;
+    double k = nearbyint(t * FZO_INV_LN2), r = (t - k * FZO_LN2_HI) - k * FZO_LN2_LO, p = 1.0;
+    for (n = 17; n >= 1; --n) p = 1.0 + p * r / (double)n;
+    return ldexp(p, (int)k);
+}
+
+float fzo_log32(float x) { return (float)fzo_log64((double)x); }
+
+float fzo_exp32(float y)
+{
+    double v = fzo_exp64((double)y);
+    if (v > (double)FLT_MAX) v = (double)FLT_MAX;
+    return (float)v;
+}
+
+double fzo_pwrel_eb(double eps, float M)
+{
+    const double k = ldexp(1.0, -24) + ldexp(1.0, -45);
+    double U = 0.0, up, lo, b;
+    int e;
+    if (!(eps > 0.0) || !(eps < 1.0)) return 0.0;
+    if (M > 0.0f) {
+        (void)frexp((double)M, &e);
+        U = ldexp(1.0, e - 23);
+    }
+    up = fzo_log64((1.0 + eps) / (1.0 + k));
+    lo = -fzo_log64((1.0 - eps) / (1.0 - k));
+    b = up < lo ? up : lo;
+    return b - U / 4.0 - ldexp(1.0, -40);
+}
+
 /* Largest float <= t (round toward -inf to binary32). */
 static float rd32(double t)
 {
@@ -105,19 +164,23 @@ int fzo_derive_params(float mn, float mx, int mode, double eb, fzo_params* p)
 
     if (p == NULL) return FZO_ERR_ARG;
     if (!(eb > 0.0) || !isfinite(eb)) return FZO_ERR_ARG;
-    if (mode != FZO_ABS && mode != FZO_REL) return FZO_ERR_ARG;
+    if (mode != FZO_ABS && mode != FZO_REL && mode != FZO_PWREL) return FZO_ERR_ARG;
+    if (mode == FZO_PWREL && !(eb < 1.0)) return FZO_ERR_ARG;
 
-    /* REL bound = eb * value range; a constant field keeps eb (reading R4) */
+    M = fabsf(mn);
+    if (fabsf(mx) > M) M = fabsf(mx);
+    /* REL bound = eb * value range; a constant field keeps eb (reading R4).
+     * P:314 (f3): the log field's ABS bound from the point-wise relative bound (R25). */
     if (mode == FZO_REL) {
         if (mx == mn) eb_abs = eb;
         else eb_abs = eb * ((double)mx - (double)mn);
+    } else if (mode == FZO_PWREL) {
+        eb_abs = fzo_pwrel_eb(eb, M);
     } else {
         eb_abs = eb;
     }
     if (!(eb_abs > 0.0) || !isfinite(eb_abs)) return FZO_ERR_EB_TOO_SMALL;
 
-    M = fabsf(mn);
-    if (fabsf(mx) > M) M = fabsf(mx);
     U = 0.0;
     if (M > 0.0f) {
         int e;
@@ -410,6 +473,7 @@ static int compress_cc(const float* d, int ndim, const uint64_t* dims, const fzo
     memcpy(out, "FZB2", 4);
     put_u16(out + 4, 1);
     put_u16(out + 6, (uint16_t)((p->mode == FZO_REL ? 1u : 0u) | (p->fallback ? 2u : 0u) |
+                                (p->mode == FZO_PWREL ? 8u : 0u) |
                                 (cz ? 4u : 0u)));
     out[8] = (uint8_t)ndim;
     if (cz) {                 /* f1: chunk depth and height (bytes 10-13, zero otherwise) */
@@ -490,6 +554,30 @@ int fzo_compress_chunked(const float* d, const uint64_t* dims, int mode, double 
     return compress_cc(d, 3, dims, &p, cz, cy, out, cap, size);
 }
 
+static int compress_pwrel(const float* d, int ndim, const uint64_t* dims, uint64_t n, double eps,
+                          uint8_t* out, uint64_t cap, uint64_t* size)
+{
+    /* f3: y = log(x) elementwise, then the ABS pipeline on y with the bound that
+     * guarantees |x^ - x| <= eps |x| after x^ = exp(y^) (reading R25) */
+    uint64_t i;
+    float mn, mx;
+    int64_t bad;
+    fzo_params p;
+    int st;
+    float* y = (float*)malloc(n * sizeof(float));
+    if (y == NULL) return FZO_ERR_ARG;
+    for (i = 0; i < n; ++i) {
+        if (!isfinite(d[i])) { free(y); return FZO_ERR_NONFINITE; }
+        if (!(d[i] >= FLT_MIN)) { free(y); return FZO_ERR_ARG; }   /* domain: normal x > 0 */
+        y[i] = fzo_log32(d[i]);
+    }
+    st = fzo_range(y, n, &mn, &mx, &bad);
+    if (st == FZO_OK) st = fzo_derive_params(mn, mx, FZO_PWREL, eps, &p);
+    if (st == FZO_OK) st = fzo_compress_with_params(y, ndim, dims, &p, out, cap, size);
+    free(y);
+    return st;
+}
+
 int fzo_compress(const float* d, int ndim, const uint64_t* dims, int mode, double eb,
                  uint8_t* out, uint64_t cap, uint64_t* size)
 {
@@ -500,6 +588,10 @@ int fzo_compress(const float* d, int ndim, const uint64_t* dims, int mode, doubl
     int st = check_shape(ndim, dims, &n);
     if (st != FZO_OK) return st;
     if (d == NULL || size == NULL) return FZO_ERR_ARG;
+    if (mode == FZO_PWREL) {
+        if (!(eb > 0.0) || !(eb < 1.0)) return FZO_ERR_ARG;
+        return compress_pwrel(d, ndim, dims, n, eb, out, cap, size);
+    }
     st = fzo_range(d, n, &mn, &mx, &bad);
     if (st != FZO_OK) return st;
     st = fzo_derive_params(mn, mx, mode, eb, &p);
@@ -515,6 +607,7 @@ int fzo_compress(const float* d, int ndim, const uint64_t* dims, int mode, doubl
 typedef struct {
     int ndim;
     uint64_t cz, cy;          /* f1 chunk depth / height, 0 = field-global Lorenzo */
+    int logt;                 /* f3: the stream holds log(x) (flag bit 3)          */
     uint64_t dims[3], n, T, nnz, nd, nv, total;
     float w;
     const uint8_t *flags, *payload, *dsec, *vsec;
@@ -535,6 +628,7 @@ static int parse(const uint8_t* in, uint64_t size, parsed_t* h)
     h->ndim = in[8];
     if (h->ndim < 1 || h->ndim > 3) return FZO_ERR_CORRUPT;
     h->cz = h->cy = 0;
+    h->logt = (get_u16(in + 6) & 8u) ? 1 : 0;
     if (get_u16(in + 6) & 4u) {
         h->cz = get_u16(in + 10);
         h->cy = get_u16(in + 12);
@@ -660,6 +754,8 @@ int fzo_decompress(const uint8_t* in, uint64_t size, float* out, uint64_t n)
             uint32_t bits = get_u32(h.vsec + 8 * k + 4);
             memcpy(&out[get_u32(h.vsec + 8 * k)], &bits, 4);
         }
+        if (h.logt)                                           /* f3: x^ = exp(y^) */
+            for (i = 0; i < n; ++i) out[i] = fzo_exp32(out[i]);
     }
     free(q);
     return st;

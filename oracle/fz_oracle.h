@@ -48,7 +48,7 @@ enum {
     FZO_ERR_CORRUPT = 5
 };
 
-enum { FZO_ABS = 0, FZO_REL = 1 };
+enum { FZO_ABS = 0, FZO_REL = 1, FZO_PWREL = 2 };
 
 typedef struct {
     double eb_input;  /* eb as given by the user                                  */
@@ -57,7 +57,7 @@ typedef struct {
     float  r;         /* (float)(1/(double)w), recorded in the header              */
     float  eb32;      /* largest float <= eb_abs                                   */
     float  mn, mx;    /* field range (canonical: -0.0 counted as +0.0)            */
-    int    mode;      /* FZO_ABS / FZO_REL                                         */
+    int    mode;      /* FZO_ABS / FZO_REL / FZO_PWREL (f3: log transform)         */
     int    fallback;  /* 1 when the margin ("fast") mode is infeasible             */
 } fzo_params;
 
@@ -119,6 +119,22 @@ int fzo_compress_chunked(const float* d, const uint64_t* dims, int mode, double 
 
 /* Full decompressor.  out: n floats, n must equal the header's element count. */
 int fzo_decompress(const uint8_t* in, uint64_t size, float* out, uint64_t n);
+
+/* f3 ("transform the original data using a logarithmic function and
+ * compress the log-transformed data with the corresponding absolute error bound (computed
+ * from the point-wise relative error bound)"), reading R25 in DESIGN.md.  The transform is a
+ * defined function: a fixed sequence of binary64 operations rounded once to binary32, so two
+ * independent implementations agree bit for bit.  Pins: tests/test_oracle_pins.py (numpy log /
+ * exp within half an ulp of binary32 plus the binary64 error, special values, the P:314
+ * guarantee |x^ - x| <= eps |x| on every element). */
+double fzo_log64(double v);            /* v > 0, finite                                     */
+double fzo_exp64(double t);            /* |t| < 700                                         */
+float fzo_log32(float x);              /* x >= FLT_MIN, finite                              */
+float fzo_exp32(float y);              /* fl32(min(exp64(y), FLT_MAX))                      */
+/* ABS bound on the log field that guarantees the point-wise relative bound eps (reading R25):
+ * min(log64((1+eps)/(1+k)), -log64((1-eps)/(1-k))) - U/4 - 2^-40, k = 2^-24 + 2^-45, U the
+ * binade-above ulp of M = max|y|.  <= 0 -> FZO_ERR_EB_TOO_SMALL. */
+double fzo_pwrel_eb(double eps, float M);
 
 /* Decoder stage hook: reconstructed integer codes q (before dequantization). */
 int fzo_decode_q(const uint8_t* in, uint64_t size, int32_t* q, uint64_t n);

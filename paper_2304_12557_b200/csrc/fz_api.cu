@@ -124,6 +124,9 @@ uint64_t tiles_of(uint64_t n) { return (n + kTileCodes - 1) / kTileCodes; }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// f3: bytes of the log field kept after the compress workspace's sections (FZ_EB_PWREL)
+size_t log_field_bytes(uint64_t n) { return (size_t)((4 * n + 255) & ~255ull); }
+
 struct Work {
     Layout L;
     uint8_t* base;
@@ -214,11 +217,13 @@ struct OutDest {
 // Phase 1: init (+ range + params on the device) -> fused kernel -> totals (+ header).
 fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp, int mode, double eb,
                        uint8_t* hdr_out, uint64_t out_cap, const fz_shape& s, uint64_t n, Ctrl* h,
-                       cudaStream_t st)
+                       cudaStream_t st, const float* log_src = nullptr)
 {
     const uint32_t tb = a.tile_begin, nt = a.tile_end - a.tile_begin;
     // status words are per scan unit, indexed from the range start; outlier counts per tile
     FZ_CUDA(launch_init(W.ctrl(), W.status(), W.ocnt() + tb, nt, hp, st, a.cl ? cl_chunk(s) : 0u));
+    // f3 (FZ_EB_PWREL): a.field is the log field y = log32(x) in the workspace (R25)
+    if (log_src != nullptr) FZ_CUDA(launch_log_fwd(log_src, const_cast<float*>(a.field), n, W.ctrl(), st));
     const bool zr = compress_uses_zr(a);
     if (a.cl && !zr && !compress_uses_zb(a)) return FZ_ERR_ARG;
     if (zr || compress_uses_zb(a)) {
@@ -300,7 +305,8 @@ void write_header_host(uint8_t* h, const fz_shape& s, uint64_t n, uint64_t T, co
     memset(h, 0, 128);
     memcpy(h, "FZB2", 4);
     const uint16_t ver = 1,
-                   fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u) | (chunk ? 4u : 0u));
+                   fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u) | (chunk ? 4u : 0u) |
+                                   (p.mode == FZ_EB_PWREL ? 8u : 0u));
     memcpy(h + 4, &ver, 2);
     memcpy(h + 6, &fl, 2);
     h[8] = (uint8_t)s.ndim;
@@ -331,15 +337,21 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     const bool cl = (mode & FZ_CHUNK_LOCAL) != 0;
     mode &= ~FZ_CHUNK_LOCAL;
     if (cl && !cl_shape(*s)) return FZ_ERR_ARG;
-    if (hp == nullptr && (!(eb > 0.0) || !std::isfinite(eb) || (mode != FZ_EB_ABS && mode != FZ_EB_REL)))
+    if (hp == nullptr && (!(eb > 0.0) || !std::isfinite(eb) ||
+                          (mode != FZ_EB_ABS && mode != FZ_EB_REL && mode != FZ_EB_PWREL) ||
+                          (mode == FZ_EB_PWREL && !(eb < 1.0))))
         return FZ_ERR_ARG;
+    const bool pw = (hp ? (int)(hp->mode & ~FZ_CHUNK_LOCAL) : mode) == FZ_EB_PWREL;
+    if (pw && cl) return FZ_ERR_ARG;
     const uint64_t T = tiles_of(n);
     Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
-    if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
+    if (work_bytes < W.L.total + (pw ? log_field_bytes(n) : 0)) return FZ_ERR_WORKSPACE;
     const Geom g = geom_of(*s, n);
     uint8_t* out = static_cast<uint8_t*>(d_out);
+    // f3: the pipeline compresses y = log32(x), kept after the workspace's other sections
+    const float* src = pw ? reinterpret_cast<const float*>(W.base + W.L.total) : d_field;
 
-    CompressArgs a = make_args(W, d_field, 0, g, 0, (uint32_t)T);
+    CompressArgs a = make_args(W, src, 0, g, 0, (uint32_t)T);
     a.cl = cl ? 1u : 0u;
     const uint64_t fbase = kHeaderBytes, pbase = kHeaderBytes + 32 * T;
     a.flags_out = out + fbase;
@@ -347,7 +359,7 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     a.payload_out = out + pbase;
     a.payload_cap = out_cap > pbase ? out_cap - pbase : 0;
     Ctrl h;
-    fz_status rs = compress_run(W, a, hp, mode, eb, out, out_cap, *s, n, &h, st);
+    fz_status rs = compress_run(W, a, hp, mode, eb, out, out_cap, *s, n, &h, st, pw ? d_field : nullptr);
     if (rs != FZ_OK) return rs;
     if (h.err != 0) return err_status(h.err);
     *out_size = (size_t)h.total;
@@ -382,6 +394,14 @@ size_t fz_workspace_bytes(const fz_shape* s)
     uint64_t n;
     if (!shape_n(s, &n)) return 0;
     return compress_layout(n, tiles_of(n), zb_layout(*s)).total;
+}
+
+size_t fz_workspace_bytes_mode(const fz_shape* s, int eb_mode)
+{
+    uint64_t n;
+    if (!shape_n(s, &n)) return 0;
+    const size_t base = compress_layout(n, tiles_of(n), zb_layout(*s)).total;
+    return (eb_mode & ~FZ_CHUNK_LOCAL) == FZ_EB_PWREL ? base + log_field_bytes(n) : base;
 }
 
 size_t fz_debug_workspace_bytes(const fz_shape* s)
@@ -465,7 +485,8 @@ fz_status fz_peek_header(const void* h_hdr, size_t nbytes, fz_info* info)
         memcpy(&cy, h + 12, 2);
         if ((fl & 4u) ? (cz == 0 || cy == 0) : (cz != 0 || cy != 0)) return FZ_ERR_CORRUPT;
     }
-    I.params.mode = (fl & 1u) ? FZ_EB_REL : FZ_EB_ABS;
+    if ((fl & 1u) && (fl & 8u)) return FZ_ERR_CORRUPT;   // REL and the f3 log transform exclude each other
+    I.params.mode = (fl & 8u) ? FZ_EB_PWREL : ((fl & 1u) ? FZ_EB_REL : FZ_EB_ABS);
     I.params.fallback = (fl & 2u) ? 1u : 0u;
     if (!(I.params.w > 0.0f) || !std::isfinite(I.params.w)) return FZ_ERR_CORRUPT;
     uint64_t cnt[5];
@@ -593,6 +614,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         a.w = deq ? I.params.w : 0.0f;
         FZ_CUDA(launch_decode_cl(a, chunk & 0xFFFFu, st));
         if (deq) FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+        if (deq && (I.flags & 8u)) FZ_CUDA(launch_exp_inv(d_field, n, nullptr, st));
         if (async) return FZ_OK;
         Ctrl hc;
         FZ_CUDA(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
@@ -631,6 +653,9 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         if (deq) {
             if (dev) FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
             else FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+            // f3 (header flag bit 3): x^ = exp32(y^); device-parsed: the kernel checks the flag
+            if (dev) FZ_CUDA(launch_exp_inv(d_field, n, ctrl, st));
+            else if (I.flags & 8u) FZ_CUDA(launch_exp_inv(d_field, n, nullptr, st));
         }
         if (async) return FZ_OK;
         Ctrl hz;
@@ -664,6 +689,8 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     if (deq) {
         if (dev) FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
         else FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+        if (dev) FZ_CUDA(launch_exp_inv(d_field, n, ctrl, st));
+        else if (I.flags & 8u) FZ_CUDA(launch_exp_inv(d_field, n, nullptr, st));
     }
     if (async) return FZ_OK;     // status later: fz_decompress_result
     Ctrl h;
@@ -707,21 +734,25 @@ fz_status fz_compress_async(const float* d_field, const fz_shape* s, int eb_mode
     const bool cl = (eb_mode & FZ_CHUNK_LOCAL) != 0;
     eb_mode &= ~FZ_CHUNK_LOCAL;
     if (cl && !cl_shape(*s)) return FZ_ERR_ARG;
-    if (!(eb > 0.0) || !std::isfinite(eb) || (eb_mode != FZ_EB_ABS && eb_mode != FZ_EB_REL)) return FZ_ERR_ARG;
+    if (!(eb > 0.0) || !std::isfinite(eb) || (eb_mode != FZ_EB_ABS && eb_mode != FZ_EB_REL && eb_mode != FZ_EB_PWREL) ||
+        (eb_mode == FZ_EB_PWREL && (cl || !(eb < 1.0))))
+        return FZ_ERR_ARG;
+    const bool pw = eb_mode == FZ_EB_PWREL;
     const uint64_t T = tiles_of(n);
     Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
-    if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
+    if (work_bytes < W.L.total + (pw ? log_field_bytes(n) : 0)) return FZ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const Geom g = geom_of(*s, n);
     uint8_t* out = static_cast<uint8_t*>(d_out);
-    CompressArgs a = make_args(W, d_field, 0, g, 0, (uint32_t)T);
+    const float* src = pw ? reinterpret_cast<const float*>(W.base + W.L.total) : d_field;
+    CompressArgs a = make_args(W, src, 0, g, 0, (uint32_t)T);
     a.cl = cl ? 1u : 0u;
     const uint64_t pbase = kHeaderBytes + 32 * T;
     a.flags_out = out + kHeaderBytes;
     a.flags_cap = out_cap > kHeaderBytes ? out_cap - kHeaderBytes : 0;
     a.payload_out = out + pbase;
     a.payload_cap = out_cap > pbase ? out_cap - pbase : 0;
-    fz_status rs = compress_run(W, a, nullptr, eb_mode, eb, out, out_cap, *s, n, nullptr, st);
+    fz_status rs = compress_run(W, a, nullptr, eb_mode, eb, out, out_cap, *s, n, nullptr, st, pw ? d_field : nullptr);
     if (rs != FZ_OK) return rs;
     FZ_CUDA(launch_outlier_scan(W.ocnt(), W.opre(), (uint32_t)T, st, W.ctrl()));
     FZ_CUDA(launch_outlier_place_dev(W.ocnt(), W.obase(), W.opre(), (uint32_t)T, W.dstage(), W.vstage(),
@@ -910,7 +941,7 @@ const char* fz_kernel_name(int id)
                                   "k_decode_init", "k_validate_outliers", "k_decode_tiles",
                                   "k_scan_sums", "k_scan_chunks", "k_scan_apply", "k_value_patch",
                                   "k_outliers", "k_tile_offsets", "k_xcarry", "k_slab", "k_decode_planes",
-                                  "k_scan_walk", "k_compact", "k_dzr_sum", "k_dzr_prep", "k_dzr_main"};
+                                  "k_scan_walk", "k_compact", "k_dzr_sum", "k_dzr_prep", "k_dzr_main", "k_logt"};
     return (id >= 0 && id < fz::K_COUNT) ? names[id] : "?";
 }
 
@@ -955,8 +986,8 @@ fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t sl
     uint64_t n;
     if (!shape_n(global, &n) || d_slab == nullptr || p == nullptr || d_stage == nullptr ||
         h_counts == nullptr || d_work == nullptr || !aligned16(d_slab) || !aligned16(d_stage) ||
-        !aligned16(d_work) || (slab_first & 3) != 0)
-        return FZ_ERR_ARG;
+        !aligned16(d_work) || (slab_first & 3) != 0 || (p->mode & ~FZ_CHUNK_LOCAL) == FZ_EB_PWREL)
+        return FZ_ERR_ARG;   // (f3's log transform is not part of the slab protocol)
     const uint64_t T = tiles_of(n);
     if (te <= tb || te > T) return FZ_ERR_ARG;
     const Geom g = geom_of(*global, n);

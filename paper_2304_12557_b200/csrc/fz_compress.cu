@@ -36,6 +36,7 @@ __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint
         ctrl->mn_enc = 0xFFFFFFFFu;
         ctrl->mx_enc = 0u;
         ctrl->first_bad = ~0ull;
+        ctrl->log_bad = ~0ull;
         ctrl->err = 0;
         ctrl->ticket = 0;
         ctrl->stage_overflow = 0;
@@ -114,6 +115,7 @@ __global__ void k_params(Ctrl* ctrl, int mode, double eb, uint64_t n)
 {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     fz_params p;
+    if (ctrl->err != 0) return;   // an earlier device step failed (e.g. the f3 log transform)
     const int st = params_from_range(ctrl, mode, eb, n, &p);
     if (st != FZ_OK) { ctrl->err = st; return; }
     ctrl->p = p;
@@ -1758,7 +1760,8 @@ __device__ void finalize_stream(uint8_t* out, uint64_t out_cap, uint32_t ndim, u
     h[0] = 'F'; h[1] = 'Z'; h[2] = 'B'; h[3] = '2';
     const uint32_t chunk = ctrl->chunk;
     const uint16_t ver = 1,
-                   fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u) | (chunk ? 4u : 0u));
+                   fl = (uint16_t)((p.mode == FZ_EB_REL ? 1u : 0u) | (p.fallback ? 2u : 0u) | (chunk ? 4u : 0u) |
+                                   (p.mode == FZ_EB_PWREL ? 8u : 0u));
     memcpy(h + 4, &ver, 2);
     memcpy(h + 6, &fl, 2);
     h[8] = (uint8_t)ndim;

@@ -115,12 +115,14 @@ __global__ void k_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, ui
     if (!ok) {
         ctrl->dec_nnz = ctrl->dec_nd = ctrl->dec_nv = 0;
         ctrl->dec_w = 0.0f;
+        ctrl->dec_flags = 0;
         return;
     }
     ctrl->dec_nnz = nnz;
     ctrl->dec_nd = nd;
     ctrl->dec_nv = nv;
     ctrl->dec_w = w;
+    ctrl->dec_flags = fl;
 }
 
 // Outlier lists must be strictly increasing and inside the field.

@@ -40,6 +40,8 @@ struct Ctrl {
     unsigned long long dec_nnz, dec_nd, dec_nv;
     float dec_w;
     uint32_t chunk;                      // f1 chunk-local stream: cz | cy << 16 (0: field-global)
+    uint32_t dec_flags;                  // header flags of the stream being decoded (dev mode)
+    unsigned long long log_bad;          // f3: first index outside the log domain, ~0 if none
 };
 static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 
@@ -453,15 +455,78 @@ __host__ __device__ inline float rd32(double t)
     return f;
 }
 
+// ------------------------------------------------------------------------------------
+// f3 log transform, reading R25: ln and exp as fixed binary64 operation sequences
+// (every op one IEEE rounding: --fmad=false on the device, -ffp-contract=off on the host),
+// rounded once to binary32 -- a defined function, so the decoder's exp and every rank's log
+// agree bit for bit.  ln 2 is split (Cody-Waite): k * kLn2Hi is exact for |k| < 2^11.
+// ------------------------------------------------------------------------------------
+constexpr double kLn2Hi = 6.93147180369123816490e-01;
+constexpr double kLn2Lo = 1.90821492927058770002e-10;
+constexpr double kInvLn2 = 1.4426950408889634074;
+
+// ln v (v > 0 finite) = e ln2 + 2 atanh(s): v = m 2^e, m in [sqrt(1/2), sqrt(2)),
+// s = (m - 1) / (m + 1), 2 atanh(s) = 2 s sum_{k=0}^{11} s^{2k} / (2k + 1) (Horner from k = 11)
+__host__ __device__ inline double log64(double v)
+{
+    int e;
+    double m = frexp(v, &e);
+    if (m < 0.70710678118654752440) { m = m * 2.0; e = e - 1; }
+    const double s = (m - 1.0) / (m + 1.0), z = s * s;
+    double p = 1.0 / 23.0;
+    for (int k = 10; k >= 0; --k) p = p * z + 1.0 / (double)(2 * k + 1);
+    return (double)e * kLn2Hi + ((double)e * kLn2Lo + 2.0 * s * p);
+}
+
+// exp t = 2^k e^r, k = rint(t / ln2), r = (t - k ln2_hi) - k ln2_lo, e^r by the nested
+// Taylor form 1 + r (1 + r/2 (1 + ... (1 + r/17))) evaluated inside out
+__host__ __device__ inline double exp64(double t)
+{
+    const double k = rint(t * kInvLn2);
+    const double r = (t - k * kLn2Hi) - k * kLn2Lo;
+    double p = 1.0;
+    for (int n = 17; n >= 1; --n) p = 1.0 + p * r / (double)n;
+    return ldexp(p, (int)k);
+}
+
+__host__ __device__ inline float log32(float x) { return (float)log64((double)x); }
+
+__host__ __device__ inline float exp32(float y)
+{
+    double v = exp64((double)y);
+    if (v > 3.4028234663852886e38) v = 3.4028234663852886e38;   // FLT_MAX (x^ stays finite)
+    return (float)v;
+}
+
+// R25: the ABS bound on y = log32(x) that keeps |exp32(y^) - x| <= eps |x|: with
+// |y^ - y| <= b, |y - ln x| <= U/4 (binary32 rounding of y, |y| <= M) and the binary32
+// rounding of exp (relative 2^-24, plus 2^-45 for the binary64 evaluations),
+// b = min(ln((1+eps)/(1+k)), -ln((1-eps)/(1-k))) - U/4 - 2^-40, k = 2^-24 + 2^-45.
+__host__ __device__ inline double pwrel_eb(double eps, float M)
+{
+    if (!(eps > 0.0) || !(eps < 1.0)) return 0.0;
+    const double k = ldexp(1.0, -24) + ldexp(1.0, -45);
+    double U = 0.0;
+    if (M > 0.0f) {
+        int e;
+        frexp((double)M, &e);
+        U = ldexp(1.0, e - 23);
+    }
+    const double up = log64((1.0 + eps) / (1.0 + k)), lo = -log64((1.0 - eps) / (1.0 - k));
+    return (up < lo ? up : lo) - U / 4.0 - ldexp(1.0, -40);
+}
+
 __host__ __device__ inline int derive_params(float mn, float mx, int mode, double eb,
                                              fz_params* p)
 {
     if (!(eb > 0.0) || !isfinite(eb)) return FZ_ERR_ARG;
-    if (mode != FZ_EB_ABS && mode != FZ_EB_REL) return FZ_ERR_ARG;
+    if (mode != FZ_EB_ABS && mode != FZ_EB_REL && mode != FZ_EB_PWREL) return FZ_ERR_ARG;
+    if (mode == FZ_EB_PWREL && !(eb < 1.0)) return FZ_ERR_ARG;
+    float M = fmaxf(fabsf(mn), fabsf(mx));
     double eb_abs = eb;
     if (mode == FZ_EB_REL && !(mx == mn)) eb_abs = eb * ((double)mx - (double)mn);
+    if (mode == FZ_EB_PWREL) eb_abs = pwrel_eb(eb, M);
     if (!(eb_abs > 0.0) || !isfinite(eb_abs)) return FZ_ERR_EB_TOO_SMALL;
-    float M = fmaxf(fabsf(mn), fabsf(mx));
     double U = 0.0;
     if (M > 0.0f) {
         int e;

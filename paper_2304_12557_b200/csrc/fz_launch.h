@@ -18,7 +18,7 @@ void set_variant_bits(int v);
 enum KernelId {
     K_INIT = 0, K_RANGE, K_PARAMS, K_COMPRESS, K_FINALIZE, K_DINIT, K_VALIDATE, K_DECODE,
     K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_SLAB, K_DECODE_PLANES, K_SCAN_WALK,
-    K_COMPACT, K_DZR_SUM, K_DZR_PREP, K_DZR_MAIN, K_COUNT
+    K_COMPACT, K_DZR_SUM, K_DZR_PREP, K_DZR_MAIN, K_LOGT, K_COUNT
 };
 
 // Counts one launch of `id` and, when profiling is on, brackets it with CUDA events on the
@@ -85,6 +85,11 @@ struct DecodeArgs {
 // The y scan runs inside the decode (one CTA per plane) when every tile holds whole rows of
 // one plane and there are enough planes to fill the GPU.
 bool decode_fuses_y(const fz_shape& s);
+
+// f3 log transform (fz_logt.cu): y = log32(x) with the domain check (first bad index and
+// status into ctrl), and x^ = exp32(y^) in place (dev_ctrl: only when its dec_flags bit 3)
+cudaError_t launch_log_fwd(const float* x, float* y, uint64_t n, Ctrl* ctrl, cudaStream_t st);
+cudaError_t launch_exp_inv(float* v, uint64_t n, const Ctrl* dev_ctrl, cudaStream_t st);
 
 // Row-walking decoder (fz_dzr.cu): 3-D, nx % 128 == 0, nx <= 1024, ny % 16 == 0.
 struct DzrArgs {

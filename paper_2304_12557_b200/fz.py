@@ -15,7 +15,7 @@ import numpy as np
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FZ_LIB") or os.path.join(PKG, "libfz.so")  # FZ_LIB: A/B builds
 
-ABS, REL = 0, 1
+ABS, REL, PWREL = 0, 1, 2   # PWREL: f3 point-wise relative bound via the log transform
 CHUNK_LOCAL = 0x100   # f1 chunk-local Lorenzo (fz.h FZ_CHUNK_LOCAL), OR into the mode
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_EB_TOO_SMALL", 4: "ERR_CAPACITY",
           5: "ERR_CORRUPT", 6: "ERR_WORKSPACE", 7: "ERR_CUDA"}
@@ -66,6 +66,7 @@ def lib():
     sig = {
         "fz_compress_bound": ([pS], S),
         "fz_workspace_bytes": ([pS], S),
+        "fz_workspace_bytes_mode": ([pS, i], S),
         "fz_decompress_workspace_bytes": ([pS], S),
         "fz_derive_params": ([C.c_float, C.c_float, i, C.c_double, pP], i),
         "fz_compress": ([P, pS, i, C.c_double, P, S, C.POINTER(S), P, S, P], i),
@@ -144,6 +145,11 @@ def workspace_bytes(dims) -> int:
     return lib().fz_workspace_bytes(C.byref(make_shape(dims)))
 
 
+def workspace_bytes_mode(dims, mode) -> int:
+    """Compress workspace for `mode` (FZ_EB_PWREL adds the 4N-byte log field)."""
+    return lib().fz_workspace_bytes_mode(C.byref(make_shape(dims)), int(mode))
+
+
 def decompress_workspace_bytes(dims) -> int:
     return lib().fz_decompress_workspace_bytes(C.byref(make_shape(dims)))
 
@@ -215,6 +221,9 @@ class Codec:
         """Returns (uint8 view of the stream, size).  With sync=False the whole compression is
         only enqueued (fz_compress_async) and (the output buffer, None) is returned; the size
         comes from compress_result()."""
+        need = workspace_bytes_mode(self.dims, (params.mode if params is not None else mode) & ~CHUNK_LOCAL)
+        if self.work.numel() < need:      # FZ_EB_PWREL: room for the log field
+            self.work = _u8(need, self.device)
         if not sync:
             assert params is None
             st = lib().fz_compress_async(_ptr(field), C.byref(self.shape), mode, eb, _ptr(self.out), self.cap,

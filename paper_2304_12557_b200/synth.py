@@ -15,6 +15,7 @@ Generators (dims slowest first, (z, y, x)):
   nyx_v       c4  512^3 velocity-like 3e7 * sines + noise
   rtm         c5  1008x1008x352 5 reflected Ricker shells over exact zeros
   qmc         alt 33120x69x69 oscillatory orbitals ("unsmooth")
+  hacc_x      f3  280,953,867 particle coordinates in (0, 256) (P:314 HACC, "unsmooth")
 Adversarial fields for parity edge cases live in `adversarial()`.
 
 Random numbers: splitmix64 (Steele et al.), u(idx, s) = ((mix(s*G + idx + G) >> 40) + .5)
@@ -43,6 +44,7 @@ FIELDS = {
     "nyx_v": ((512, 512, 512), 44),
     "rtm": ((1008, 1008, 352), 5),
     "qmc": ((33120, 69, 69), 6),
+    "hacc_x": ((280953867,), 8),
 }
 
 
@@ -307,9 +309,30 @@ def qmc(shape=(33120, 69, 69), seed=6):
     return out
 
 
+def hacc_x(shape=(280953867,), seed=8):
+    """HACC-like particle coordinate (1-D, SV 8.a: 280,953,867 particles): particles come in
+    halos of 1000 consecutive indices; halo h has centre c_h = 256 u(h) and radius
+    r_h = 0.05 + 2 u'(h); particle i sits at c_h + r_h (2 u(i) - 1), wrapped into the periodic
+    box [0, 256) and shifted by 1/64 so every value is strictly positive (the log transform's
+    domain).  Irregular within a halo, clustered across halos ("unsmooth")."""
+    n = int(np.prod(shape))
+    out = np.empty(n, dtype=np.float32)
+    per = 1 << 22
+
+    def put(a, b):
+        i = np.arange(a, b, dtype=np.uint64)
+        h = i // np.uint64(1000)
+        c = 256.0 * uniform01(h, seed)
+        r = 0.05 + 2.0 * uniform01(h, seed + 1)
+        v = np.mod(c + r * (2.0 * uniform01(i, seed + 2) - 1.0), 256.0) + 1.0 / 64.0
+        out[a:b] = v.astype(np.float32)
+    _pmap(put, _chunks(n, per))
+    return out.reshape(shape)
+
+
 _GEN = {
     "sines3d": sines3d, "cesm_t": cesm_t, "cesm_cld": cesm_cld, "hurr_qsnow": hurr_qsnow,
-    "hurr_u": hurr_u, "nyx_rho": nyx_rho, "nyx_v": nyx_v, "rtm": rtm, "qmc": qmc,
+    "hurr_u": hurr_u, "nyx_rho": nyx_rho, "nyx_v": nyx_v, "rtm": rtm, "qmc": qmc, "hacc_x": hacc_x,
 }
 
 

@@ -16,7 +16,7 @@ SRC = os.path.join(ROOT, "oracle", "fz_oracle.c")
 LIB = os.path.join(ROOT, "oracle", "liboracle.so")
 
 OK, ERR_ARG, ERR_NONFINITE, ERR_EB_TOO_SMALL, ERR_CAPACITY, ERR_CORRUPT = range(6)
-ABS, REL = 0, 1
+ABS, REL, PWREL = 0, 1, 2
 
 
 def build(force: bool = False) -> str:
@@ -61,6 +61,16 @@ def lib():
         L.fzo_decode_q.argtypes = [P, u64, P, u64]
         L.fzo_lorenzo_chunked.argtypes = [P, P, u64, u64, P]
         L.fzo_compress_chunked.argtypes = [P, P, C.c_int, C.c_double, u64, u64, P, u64, P]
+        L.fzo_log64.argtypes = [C.c_double]
+        L.fzo_log64.restype = C.c_double
+        L.fzo_exp64.argtypes = [C.c_double]
+        L.fzo_exp64.restype = C.c_double
+        L.fzo_log32.argtypes = [C.c_float]
+        L.fzo_log32.restype = C.c_float
+        L.fzo_exp32.argtypes = [C.c_float]
+        L.fzo_exp32.restype = C.c_float
+        L.fzo_pwrel_eb.argtypes = [C.c_double, C.c_float]
+        L.fzo_pwrel_eb.restype = C.c_double
         _lib = L
     return _lib
 

@@ -83,3 +83,21 @@ def test_fullsize_chunk_local_parity(cfg, field, shape, rel):
     st, xref = O.decompress(ref, d.size)
     assert st == O.OK
     assert np.count_nonzero(xh.view(np.uint32) != xref.view(np.uint32)) == 0
+
+
+# f3: the HACC-shaped 1-D field (280,953,867 particle coordinates) under the
+# point-wise relative bound, in the launch configuration bench.py times.
+@pytest.mark.parametrize("eps", [1e-3])
+def test_fullsize_hacc_pwrel_parity(eps):
+    d = synth.generate("hacc_x")
+    st, ref = O.compress(d, O.PWREL, eps)
+    assert st == O.OK
+    codec = fz.Codec(d.shape, "cuda:0")
+    x = torch.from_numpy(d).to("cuda:0")
+    buf, size = codec.compress(x, fz.PWREL, eps)
+    assert size == ref.size and np.array_equal(buf.cpu().numpy(), ref)
+    xh = codec.decompress(buf).cpu().numpy().reshape(-1)
+    del x, buf
+    st, xref = O.decompress(ref, d.size)
+    assert np.count_nonzero(xh.view(np.uint32) != xref.view(np.uint32)) == 0
+    assert np.all(np.abs(xh.astype(np.float64) - d) <= eps * d.astype(np.float64))

@@ -31,7 +31,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol():
     syms = declared_symbols()
-    assert len(syms) == 38
+    assert len(syms) == 39
     L = C.CDLL(fz.LIB_PATH)
     for s in syms:
         assert hasattr(L, s), s
@@ -46,10 +46,10 @@ def test_sizes():
     assert fz.slab_stage_bound((512, 512, 512), 0, 128) == 32 * 128 + 4096 * 128 + 16 * 128 * 2048
 
 
-@pytest.mark.parametrize("mode", [O.ABS, O.REL])
+@pytest.mark.parametrize("mode", [O.ABS, O.REL, O.PWREL])
 def test_host_params_match_oracle(mode):
     """libfz's host parameter derivation equals the oracle's (independent implementations of
-    Appendix A / R2)."""
+    Appendix A / R2; for PWREL also of R25's bound on the log field, incl. log64)."""
     rng = np.random.default_rng(0)
     for _ in range(2000):
         a = np.float32(rng.normal() * 10 ** rng.uniform(-5, 8))
