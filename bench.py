@@ -763,6 +763,12 @@ def run_single(args, wl):
         "cr": round(d.nbytes / stream_bytes, 4), "bits_per_value": round(32 * stream_bytes / d.nbytes, 4),
         "roofline": roof, "roofline_compress_kernel": comp_roof, "roofline_decoder": dec_roof, "kernels": kernels,
         "quality": qual, "pcie_gbs": bw,
+        "f4_model": {"model": "P:478 T_overall and the compress + transfer + decompress pipeline over NVLink 5 "
+                              "(900 GB/s per direction, nominal; measured exchanges are in the multi-GPU line)",
+                     "nvlink_gbs": 900.0,
+                     "t_overall_gbs": round(1.0 / (1.0 / (900.0 * d.nbytes / stream_bytes) + 1.0 / (gb / (ms_c / 1e3))), 2),
+                     "pipeline_gbs": round(1.0 / ((ms_c + ms_d) / 1e3 / gb + stream_bytes / d.nbytes / 900.0), 2),
+                     "raw_gbs": 900.0},
         "t_overall_gbs": {"model": "P:478 T_overall = ((BW x CR)^-1 + T^-1)^-1, BW = measured pinned PCIe copy",
                           "compress_then_d2h": t_overall(bw["d2h"], d.nbytes / stream_bytes, gb / (ms_c / 1e3)),
                           "h2d_then_decompress": t_overall(bw["h2d"], d.nbytes / stream_bytes, gb / (ms_d / 1e3))},
@@ -816,6 +822,17 @@ def main():
         run_reference(args, wl)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched bare (no torchrun): start N ranks over NCCL ourselves, rank 0 prints the line
+        import socket
+        import subprocess
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     if world > 1 or args.gpus > 1:
         from paper_2304_12557_b200 import bench_dist
         bench_dist.run(args, wl, METRIC)

@@ -77,16 +77,26 @@ def run(args, wl, metric):
     launches = [0]
     last_params = [None]
 
+    coll = []   # CUDA-event pairs around the three exchange steps of the timed steps
+
+    def timed(fn, *a, **k):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = fn(*a, **k)
+        e1.record()
+        coll.append((e0, e1))
+        return r
+
     def step():
         nonlocal out
         mn, mx = comp.local_range(slab)
         launches[0] += fz.last_launch_count()
-        gmn, gmx = dist.exchange_range(mn, mx, device=xdev)
+        gmn, gmx = timed(dist.exchange_range, mn, mx, device=xdev)
         params = fz.derive_params(gmn, gmx, fz.REL, rel)
         last_params[0] = params
         counts = comp.compress_local(slab, params)
         launches[0] += fz.last_launch_count()
-        before_all, totals = dist.exchange_counts((counts.nnz, counts.n_delta, counts.n_value), device=xdev)
+        before_all, totals = timed(dist.exchange_counts, (counts.nnz, counts.n_delta, counts.n_value), device=xdev)
         before = before_all[rank]
         total = 128 + 32 * pl.tiles + 16 * totals[0] + 8 * totals[1] + 8 * totals[2]
         if out is None or out.numel() < total:
@@ -94,7 +104,7 @@ def run(args, wl, metric):
         comp.place(counts, before, totals, params, out)
         comp.decode_local(counts, q, agg, dwork)
         launches[0] += fz.last_launch_count()
-        aggs = dist.exchange_planes(agg.to(xdev)).to(dev)
+        aggs = timed(dist.exchange_planes, agg.to(xdev)).to(dev)
         fz.slab_carry(aggs, rank, E, carry)
         launches[0] += fz.last_launch_count()
         comp.finish(q, carry, counts, params)
@@ -134,6 +144,12 @@ def run(args, wl, metric):
     t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=xdev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
+    # time inside the three exchange steps (range, counts, carry planes), max over ranks
+    nc = 3 * args.steps
+    ct = torch.tensor([sum(a.elapsed_time(b) for a, b in coll[-nc:]) / max(1, args.steps)], dtype=torch.float64,
+                      device=xdev)
+    tdist.all_reduce(ct, op=tdist.ReduceOp.MAX)
+    coll_ms = float(ct.item())
 
     # ---- end to end through the slab API with host buffers: per rank and step, H2D of the
     # slab (own + halo) from pinned memory, compress, D2H of the rank's compressed share (its
@@ -200,6 +216,7 @@ def run(args, wl, metric):
     err = float(e.item())
     if err > last_params[0].eb_abs:
         raise SystemExit(f"bench_dist: max |x - x^| = {err} exceeds eb_abs = {last_params[0].eb_abs}")
+    extra = _replica_and_link_legs(args, rank, world, dev, xdev, tdist, torch, fz, synth, d, shape, rel, pl)
     if rank == 0:
         gb = d.nbytes / 1e9
         roof = None
@@ -217,7 +234,8 @@ def run(args, wl, metric):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "dims": list(shape), "rel_eb": rel, "field_bytes": d.nbytes,
-                       "parallelism": f"z-slabs x{world}, NCCL all_gathers (range, counts, carry planes)",
+                       "parallelism": f"z-slabs x{world}, {'NCCL' if backend == 'nccl' else 'gloo (ranks sharing one GPU)'} "
+                                      "all_gathers (range, counts, carry planes)",
                        "l2": "field 4.3x L2"},
             "cr": round(d.nbytes / total, 4),
             "max_abs_err_over_eb_abs": round(err / last_params[0].eb_abs, 6),
@@ -228,7 +246,103 @@ def run(args, wl, metric):
                     "h2d_bytes_per_step": int(ebytes[0].item()), "d2h_bytes_per_step": int(ebytes[1].item()),
                     "path": "slab API per rank: pinned H2D of the slab, compress, D2H + H2D of the rank's "
                             "compressed share, decode, D2H of the decoded slab"},
+            "collectives_ms_per_step": round(coll_ms, 4),
+            "value_without_collectives": round(gb / (max(ms - coll_ms, 1e-6) / 1e3), 3),
+            **extra,
         }
         print(json.dumps(line), flush=True)
     tdist.barrier()
     tdist.destroy_process_group()
+
+
+def _replica_and_link_legs(args, rank, world, dev, xdev, tdist, torch, fz, synth, d, shape, rel, pl):
+    """c5 as replicas (SV 8.e: "c5 is replicas": every rank compresses + decompresses its own
+    RTM field t = rank, no collective; aggregate = sum of fields / max over ranks), and f4
+    (P:476-483): pairwise exchange of a field between ranks 2j and 2j+1 raw (the field's bytes
+    over NCCL) against compressed (compress, send the stream, decompress), CUDA events, max
+    over ranks.  Returns the keys for rank 0's JSON line."""
+    import statistics as st_
+
+    from . import link
+    out = {}
+    # ---- c5 replicas ----
+    if not os.environ.get("FZ_DIST_NO_REPLICAS"):
+        rshape = (1008, 1008, 352)
+        r = torch.from_numpy(synth.generate("rtm", rshape, seed=5 + rank % 8)).to(dev)
+        c = fz.Codec(rshape, dev)
+        xr = torch.empty_like(r)
+        for _ in range(3):
+            c.compress(r, fz.REL, 1e-4, sync=False)
+            c.decompress_device(c.out, out=xr)
+        torch.cuda.synchronize()
+        tdist.barrier()
+        evs = []
+        for _ in range(max(3, min(args.steps, 10))):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            c.compress(r, fz.REL, 1e-4, sync=False)
+            c.decompress_device(c.out, out=xr)
+            e1.record()
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        size = c.compress_result()
+        c.result()
+        tr = torch.tensor([st_.mean(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=xdev)
+        tdist.all_reduce(tr, op=tdist.ReduceOp.MAX)
+        out["c5_replicas"] = {"workload": f"c5 RTM-shaped 1008x1008x352 REL 1e-4, one field per rank (t = rank), "
+                                          f"{world} replicas, no collective",
+                              "value": round(world * r.numel() * 4 / 1e9 / (float(tr.item()) / 1e3), 3),
+                              "unit": "GB/s (sum over ranks)", "ms_per_step": round(float(tr.item()), 4),
+                              "cr_rank0": round(r.numel() * 4 / size, 4)}
+        del r, xr, c
+        torch.cuda.empty_cache()
+    # ---- f4: compressed vs raw pairwise exchange ----
+    if world >= 2 and world % 2 == 0:
+        peer = rank ^ 1
+        lshape = (max(1, (pl.own_hi - pl.own_lo) // (shape[1] * shape[2])),) + tuple(shape[1:])
+        nloc = int(np.prod(lshape))
+        flat = d.reshape(-1)
+        mine = torch.from_numpy(np.ascontiguousarray(flat[pl.own_lo: pl.own_lo + nloc])).to(dev).reshape(lshape)
+        got = torch.empty_like(mine)
+        transport = "cuda" if xdev.type == "cuda" else "cpu"
+        lk = link.CompressedLink(link.fz_codec(lshape, fz.REL, rel, dev), transport=transport)
+        raw_t = mine if transport == "cuda" else mine.cpu()
+        raw_o = torch.empty_like(raw_t)
+
+        def run(fn, k):
+            tdist.barrier()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(k):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            t = torch.tensor([st_.mean(ts)], dtype=torch.float64, device=xdev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            return float(t.item())
+
+        run(lambda: link.CompressedLink.exchange_raw(raw_t, peer, raw_o), 2)
+        run(lambda: lk.exchange(mine, peer, got), 2)
+        ms_raw = run(lambda: link.CompressedLink.exchange_raw(raw_t, peer, raw_o), max(3, min(args.steps, 10)))
+        ms_cmp = run(lambda: lk.exchange(mine, peer, got), max(3, min(args.steps, 10)))
+        # the received field decodes within the peer's REL bound (P:133, P:320)
+        from . import dist as fzd
+        ppl = fzd.plan(shape, world, peer)
+        pf = torch.from_numpy(np.ascontiguousarray(flat[ppl.own_lo: ppl.own_lo + nloc])).to(dev)
+        perr = float((got.reshape(-1).double() - pf.double()).abs().max().item())
+        pebs = rel * (float(pf.max().item()) - float(pf.min().item()))
+        if perr > pebs:
+            raise SystemExit(f"bench_dist f4: received field error {perr} exceeds the peer's bound {pebs}")
+        gb = world * nloc * 4 / 1e9
+        out["f4_compressed_link"] = {
+            "what": "pairwise exchange of each rank's slab (ranks 2j <-> 2j+1): raw field bytes over "
+                    f"{'NCCL' if transport == 'cuda' else 'gloo (host-staged)'} vs compress + send stream + decompress",
+            "raw_gbs": round(gb / (ms_raw / 1e3), 3), "compressed_gbs": round(gb / (ms_cmp / 1e3), 3),
+            "ms_raw": round(ms_raw, 4), "ms_compressed": round(ms_cmp, 4),
+            "stream_bytes_rank0": lk.last_sent, "field_bytes_per_rank": nloc * 4,
+            "max_err_over_eb_rank0": round(perr / pebs, 6) if pebs > 0 else None,
+            "unit": "GB/s of original data, all ranks"}
+    return out

@@ -97,3 +97,64 @@ def test_chunk_aligned_plan(world):
         if p.te > p.tb:
             assert (p.tb * 2048) % (16 * P) == 0
             assert p.te == p.tiles or (p.te * 2048) % (16 * P) == 0
+
+
+# ---- f4: compressed transfer between ranks, protocol checked with the oracle as
+# the codec (the CPU stand-in; the GPU test runs libfz through the same link) ----
+def _oracle_codec(shape, eb):
+    import oracle_lib as O
+    from paper_2304_12557_b200 import link
+
+    def compress(field):
+        st, buf = O.compress(field.numpy(), O.REL, eb)
+        assert st == O.OK
+        return torch.from_numpy(buf)
+
+    def decompress(stream, out):
+        st, x = O.decompress(stream.numpy(), out.numel())
+        assert st == O.OK
+        out.copy_(torch.from_numpy(x).reshape(out.shape))
+
+    return link.Codec(compress, decompress, O.compress_bound(shape))
+
+
+def _link_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2304_12557_b200 import link, synth
+        shape = (24, 40, 56)
+        mine = torch.from_numpy(synth.generate("sines3d", shape, seed=11 + rank))
+        lk = link.CompressedLink(_oracle_codec(shape, 1e-3), transport="cpu")
+        got = torch.empty(shape, dtype=torch.float32)
+        n = lk.exchange(mine, 1 - rank, got)
+        raw = torch.empty(shape, dtype=torch.float32)
+        link.CompressedLink.exchange_raw(mine, 1 - rank, raw)
+        q.put((rank, n, lk.last_sent, got.numpy().copy(), raw.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_compressed_link():
+    import oracle_lib as O
+    from paper_2304_12557_b200 import synth
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_link_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shape = (24, 40, 56)
+    for rank, n, sent, got, raw in res:
+        peer = synth.generate("sines3d", shape, seed=11 + (1 - rank))
+        st, ref = O.compress(peer, O.REL, 1e-3)
+        st, xr = O.decompress(ref, peer.size)
+        assert n == ref.size                       # only the stream's bytes crossed
+        assert np.array_equal(got.reshape(-1).view(np.uint32), xr.view(np.uint32))
+        assert np.array_equal(raw, peer)
+    assert res[0][2] == res[1][1] and res[1][2] == res[0][1]   # sizes agree both ways

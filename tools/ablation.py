@@ -3,21 +3,21 @@
 Runs bench.py (c4 512^3 REL 1e-3, 1 GPU) once per variant, selected by FZ_EXP bits read by
 libfz, and writes profiles/<round>_ablation.md with the step, compress and decompress
 throughput and the per-kernel times:
-  base          z-band compressor (k_compress_zb + k_compact), plane decoder (x+y fused), 2 CTAs per plane
-  ws_comp       FZ_EXP=1024 warp-specialized single-pass compressor (TMA + scanner warp look-back)
-  generic_comp  FZ_EXP=16   generic fused compressor (no warp specialization / TMA / scanner warp)
-  unfused_dec   FZ_EXP=128  tile decoder (x only) + separate y and z walks
-  one_cta_plane FZ_EXP=512  plane decoder with one CTA per plane (no y-carry split)
-  two_seg_plane FZ_EXP=4096 plane decoder with two CTAs per plane (default: eight)
+  base          row-walking compressor (k_compress_zr + k_compact), row-walking decoder (k_dzr_*)
+  zr_3stage     FZ_EXP=16384 row walker with three TMA stages (two CTAs per SM)
+  zband_comp    FZ_EXP=8192 z-band compressor (k_compress_zb, round 1's)
+  ws_comp       FZ_EXP=9216 warp-specialized single-pass compressor (TMA + scanner warp look-back)
+  plane_dec     FZ_EXP=32768 plane decoder (x+y fused, int32 field) + z walk (round 1's)
+  unfused_dec   FZ_EXP=32896 tile decoder (x only) + separate y and z walks
 Usage (GPU box): python tools/ablation.py [round] [steps]
 """
 import json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r02"
 steps = sys.argv[2] if len(sys.argv) > 2 else "10"
-variants = [("base", "0"), ("ws_comp", "1024"), ("generic_comp", "16"), ("unfused_dec", "128"),
-            ("one_cta_plane", "512"), ("two_seg_plane", "4096")]
+variants = [("base", "0"), ("zr_3stage", "16384"), ("zband_comp", "8192"), ("ws_comp", "9216"),
+            ("plane_dec", "32768"), ("unfused_dec", "32896")]
 rows = []
 for name, e in variants:
     env = dict(os.environ, FZ_EXP=e)
