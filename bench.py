@@ -165,7 +165,7 @@ DECODE_IDS = ("k_decode_tiles", "k_decode_planes", "k_scan_walk", "k_scan_apply"
               "k_decode_init", "k_validate_outliers", "k_value_patch", "k_tile_offsets", "k_dzr_sum",
               "k_dzr_prep", "k_dzr_main")
 PROF_IDS = ["k_range", "k_compress", "k_compact", "k_decode_tiles", "k_decode_planes", "k_scan_walk",
-            "k_scan_apply", "k_xcarry", "k_dzr_sum", "k_dzr_prep", "k_dzr_main"]
+            "k_scan_apply", "k_xcarry", "k_dzr_sum", "k_dzr_prep", "k_dzr_main", "k_rowtiles", "k_logt"]
 
 
 def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_for_parity=True, mode_name="rel"):

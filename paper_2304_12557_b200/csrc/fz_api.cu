@@ -147,6 +147,14 @@ bool zb_layout(const fz_shape& s)
     return s.ndim == 3 && zb_shape(3, s.dims[1], s.dims[2], s.dims[0]);
 }
 
+// the compress workspace of a shape: z-band / row-walker staging, or the row-codes path's
+// code field and masks (2-D and 3-D shapes whose planes are not whole tiles)
+Layout layout_of(const fz_shape& s, uint64_t n, uint64_t T)
+{
+    const bool zb = zb_layout(s);
+    return compress_layout(n, T, zb, !zb && rc_layout_shape(s));
+}
+
 // f1 chunk-local Lorenzo: 3-D fields whose tiles hold whole rows of one plane;
 // chunk = 16 planes x one tile (2048 / nx rows).  Header word: cz | cy << 16.
 constexpr uint32_t kClDepth = 16;
@@ -185,6 +193,11 @@ CompressArgs make_args(const Work& W, const float* field, uint64_t base, const G
     a.opre = W.opre();
     a.ctrl = W.ctrl();
     a.tstage = W.tstage();
+    if (W.L.rcodes) {
+        a.rc_codes = reinterpret_cast<uint16_t*>(W.base + W.L.rcodes);
+        a.rc_vmask = reinterpret_cast<uint32_t*>(W.base + W.L.rmask);
+        a.rc_dmask = a.rc_vmask + rc_mask_words(W.L.ntiles);
+    }
     return a;
 }
 
@@ -226,6 +239,24 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
     if (log_src != nullptr) FZ_CUDA(launch_log_fwd(log_src, const_cast<float*>(a.field), n, W.ctrl(), st));
     const bool zr = compress_uses_zr(a);
     if (a.cl && !zr && !compress_uses_zb(a)) return FZ_ERR_ARG;
+    if (!zr && !compress_uses_zb(a) && compress_uses_rc(a)) {
+        // row-codes two-pass path: pass A (row walk -> code field + outlier masks), pass B
+        // (tiles in stream order -> flags + staged blocks + outlier records), then the same
+        // popcount scan, compaction and finalize as the z-band path
+        if (hp == nullptr) FZ_CUDA(launch_range(a.field, n, W.ctrl(), st));
+        CompressArgs b = a;
+        b.derive = hp == nullptr;
+        b.eb_mode = mode;
+        b.eb = eb;
+        b.n_hdr = n;
+        FZ_CUDA(launch_compress_rc(b, st));
+        const uint32_t T = a.tile_end - a.tile_begin;
+        FZ_CUDA(launch_tile_offsets(a.flags_out, T, W.zloc(), W.zbsum(), W.ctrl(), st, ~1ull));
+        FZ_CUDA(launch_compact(a.flags_out, W.zloc(), W.zbsum(), W.tstage(), a.payload_out, a.payload_cap, T, st));
+        FZ_CUDA(launch_finalize(hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
+        if (h == nullptr) return FZ_OK;
+        return read_ctrl(W, h, st);
+    }
     if (zr || compress_uses_zb(a)) {
         // z-band two-pass compressor: pass 1 derives the parameters in its prologue, writes
         // the flags and stages each tile's blocks; the popcount scan of the flags gives the
@@ -344,7 +375,7 @@ fz_status compress_impl(const float* d_field, const fz_shape* s, const fz_params
     const bool pw = (hp ? (int)(hp->mode & ~FZ_CHUNK_LOCAL) : mode) == FZ_EB_PWREL;
     if (pw && cl) return FZ_ERR_ARG;
     const uint64_t T = tiles_of(n);
-    Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
+    Work W{layout_of(*s, n, T), static_cast<uint8_t*>(d_work)};
     if (work_bytes < W.L.total + (pw ? log_field_bytes(n) : 0)) return FZ_ERR_WORKSPACE;
     const Geom g = geom_of(*s, n);
     uint8_t* out = static_cast<uint8_t*>(d_out);
@@ -393,14 +424,14 @@ size_t fz_workspace_bytes(const fz_shape* s)
 {
     uint64_t n;
     if (!shape_n(s, &n)) return 0;
-    return compress_layout(n, tiles_of(n), zb_layout(*s)).total;
+    return layout_of(*s, n, tiles_of(n)).total;
 }
 
 size_t fz_workspace_bytes_mode(const fz_shape* s, int eb_mode)
 {
     uint64_t n;
     if (!shape_n(s, &n)) return 0;
-    const size_t base = compress_layout(n, tiles_of(n), zb_layout(*s)).total;
+    const size_t base = layout_of(*s, n, tiles_of(n)).total;
     return (eb_mode & ~FZ_CHUNK_LOCAL) == FZ_EB_PWREL ? base + log_field_bytes(n) : base;
 }
 
@@ -409,7 +440,7 @@ size_t fz_debug_workspace_bytes(const fz_shape* s)
     uint64_t n;
     if (!shape_n(s, &n)) return 0;
     const uint64_t T = tiles_of(n);
-    return compress_layout(n, T, zb_layout(*s)).total + 32 * T + 4096 * T;
+    return layout_of(*s, n, T).total + 32 * T + 4096 * T;
 }
 
 size_t fz_decompress_workspace_bytes(const fz_shape* s)
@@ -739,7 +770,7 @@ fz_status fz_compress_async(const float* d_field, const fz_shape* s, int eb_mode
         return FZ_ERR_ARG;
     const bool pw = eb_mode == FZ_EB_PWREL;
     const uint64_t T = tiles_of(n);
-    Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
+    Work W{layout_of(*s, n, T), static_cast<uint8_t*>(d_work)};
     if (work_bytes < W.L.total + (pw ? log_field_bytes(n) : 0)) return FZ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const Geom g = geom_of(*s, n);
@@ -941,7 +972,7 @@ const char* fz_kernel_name(int id)
                                   "k_decode_init", "k_validate_outliers", "k_decode_tiles",
                                   "k_scan_sums", "k_scan_chunks", "k_scan_apply", "k_value_patch",
                                   "k_outliers", "k_tile_offsets", "k_xcarry", "k_slab", "k_decode_planes",
-                                  "k_scan_walk", "k_compact", "k_dzr_sum", "k_dzr_prep", "k_dzr_main", "k_logt"};
+                                  "k_scan_walk", "k_compact", "k_dzr_sum", "k_dzr_prep", "k_dzr_main", "k_logt", "k_rowtiles"};
     return (id >= 0 && id < fz::K_COUNT) ? names[id] : "?";
 }
 
@@ -995,7 +1026,7 @@ fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t sl
     const uint64_t need_lo = tb * kTileCodes > halo ? tb * kTileCodes - halo : 0;
     const uint64_t need_hi = te * kTileCodes < n ? te * kTileCodes : n;
     if (slab_first > need_lo || slab_first + slab_elems < need_hi) return FZ_ERR_ARG;
-    Work W{compress_layout(n, T, zb_layout(*global)), static_cast<uint8_t*>(d_work)};
+    Work W{layout_of(*global, n, T), static_cast<uint8_t*>(d_work)};
     if (work_bytes < W.L.total) return FZ_ERR_WORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const uint64_t nt = te - tb;
@@ -1077,7 +1108,7 @@ fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_pa
         h_nv == nullptr || !aligned16(d_field) || !aligned16(d_work))
         return FZ_ERR_ARG;
     const uint64_t T = tiles_of(n);
-    Work W{compress_layout(n, T, zb_layout(*s)), static_cast<uint8_t*>(d_work)};
+    Work W{layout_of(*s, n, T), static_cast<uint8_t*>(d_work)};
     // the hook runs the product kernels, which write flags and payload: scratch for them
     // follows the compression workspace (fz_debug_workspace_bytes)
     if (work_bytes < W.L.total + 32 * T + 4096 * T) return FZ_ERR_WORKSPACE;

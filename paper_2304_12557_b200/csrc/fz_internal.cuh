@@ -50,17 +50,21 @@ static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 //   ocnt   : per-tile (n_delta, n_value); obase: staging offsets of the tile's records;
 //   opre   : per-tile exclusive outlier offsets (filled only when outliers exist)
 struct Layout {
-    size_t ctrl, status, ocnt, obase, opre, dstage, vstage, tstage, zloc, zbsum, total;
+    size_t ctrl, status, ocnt, obase, opre, dstage, vstage, tstage, zloc, zbsum, rcodes, rmask, total;
+    uint64_t ntiles;
     uint64_t dcap, vcap;             // staging capacities in records
 };
 
 // zb: room for the z-band two-pass compressor (a 4 KB staging slot per tile + the offsets
 // of its compaction pass).
-inline Layout compress_layout(uint64_t n, uint64_t tiles, bool zb = false)
+inline uint64_t rc_mask_words(uint64_t tiles) { return tiles * 64 + 2; }   // even: 8-byte aligned pairs
+
+inline Layout compress_layout(uint64_t n, uint64_t tiles, bool zb = false, bool rc = false)
 {
     Layout L{};
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     size_t off = 0;
+    L.ntiles = tiles;
     L.ctrl = off;   off += 512;
     L.status = off; off = al(off + 8 * tiles);
     L.ocnt = off;   off = al(off + 8 * tiles);
@@ -70,11 +74,15 @@ inline Layout compress_layout(uint64_t n, uint64_t tiles, bool zb = false)
     L.vcap = n / 64 + 1024;
     L.dstage = off; off = al(off + 8 * L.dcap);
     L.vstage = off; off = al(off + 8 * L.vcap);
-    L.tstage = L.zloc = L.zbsum = 0;
-    if (zb) {
+    L.tstage = L.zloc = L.zbsum = L.rcodes = L.rmask = 0;
+    if (zb || rc) {
         L.tstage = off; off = al(off + 16 * 256 * tiles);
         L.zloc = off;   off = al(off + 4 * tiles);
         L.zbsum = off;  off = al(off + 4 * ((tiles + 1023) / 1024));
+    }
+    if (rc) {
+        L.rcodes = off; off = al(off + 2 * 2048 * tiles);
+        L.rmask = off;  off = al(off + 2 * 4 * rc_mask_words(tiles));
     }
     L.total = off;
     return L;
@@ -696,6 +704,11 @@ struct CompressArgs {
     uint32_t hwords;          // z-band: floats of the TMA-staged row halo (0: quantized from global)
     uint32_t cl;              // f1 chunk-local Lorenzo (z-band kernel only): chunks of kZbChunk planes x one tile
     int exp;                  // variant bits (fz_debug_set_variant), bit 16: generic kernel instead of the warp-specialized one
+    // row-codes path (fz_rowcodes.cu): the code field (T x 2048 u16) and the two outlier bit
+    // masks (value, delta; one bit per element, rc_dmask = rc_vmask + rc_mask_words)
+    uint16_t* rc_codes;
+    uint32_t* rc_vmask;
+    uint32_t* rc_dmask;
 };
 
 }  // namespace fz

@@ -18,7 +18,7 @@ void set_variant_bits(int v);
 enum KernelId {
     K_INIT = 0, K_RANGE, K_PARAMS, K_COMPRESS, K_FINALIZE, K_DINIT, K_VALIDATE, K_DECODE,
     K_SCAN_SUMS, K_SCAN_CHUNKS, K_SCAN_APPLY, K_VPATCH, K_OUTLIERS, K_OFFSETS, K_XCARRY, K_SLAB, K_DECODE_PLANES, K_SCAN_WALK,
-    K_COMPACT, K_DZR_SUM, K_DZR_PREP, K_DZR_MAIN, K_LOGT, K_COUNT
+    K_COMPACT, K_DZR_SUM, K_DZR_PREP, K_DZR_MAIN, K_LOGT, K_ROWTILES, K_COUNT
 };
 
 // Counts one launch of `id` and, when profiling is on, brackets it with CUDA events on the
@@ -41,6 +41,9 @@ cudaError_t launch_compress(const CompressArgs& a, cudaStream_t st);
 bool compress_uses_ws(const CompressArgs& a);   // the warp-specialized kernel takes this launch
 bool compress_uses_zb(const CompressArgs& a);   // the z-band two-pass compressor takes it
 cudaError_t launch_compress_zb(const CompressArgs& a, cudaStream_t st);
+bool compress_uses_rc(const CompressArgs& a);   // the row-codes two-pass path takes it (fz_rowcodes.cu)
+bool rc_layout_shape(const fz_shape& s);
+cudaError_t launch_compress_rc(const CompressArgs& a, cudaStream_t st);
 bool compress_uses_zr(const CompressArgs& a);   // the row-walking z-band compressor takes it (fz_zrow.cu)
 cudaError_t launch_compress_zr(const CompressArgs& a, cudaStream_t st);
 cudaError_t launch_compact(const uint8_t* flags, const uint32_t* loc, const uint32_t* bpre, const uint4* tstage,

@@ -25,8 +25,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     for _ in range(10):
         c.compress(x, fz.REL, rel)
     p = fz.profile_read()
-    ms, k = p["k_compress"]
-    print(f"FZ_EXP={os.environ.get('FZ_EXP','0')} k_compress {ms/k*1000:.1f} us")
+    ks = " ".join(f"{name} {ms / k * 1000:.1f}" for name, (ms, k) in p.items() if ms / k > 0.002)
+    print(f"[{wl}] FZ_EXP={os.environ.get('FZ_EXP','0')} us/launch: {ks}")
 else:
     for e in sys.argv[1:] or ["0", "16"]:
         env = dict(os.environ, FZ_EXP=e)
