@@ -73,7 +73,7 @@ def ncu_traffic(workload: str, kernel: str):
             t = json.load(f)[workload]
         # the profiler id k_compress covers the z-band pass 1 (k_compress_zb) or the
         # warp-specialized kernel (k_compress_ws), whichever the shape takes
-        for k in (kernel, kernel + "_zb", kernel + "_ws"):
+        for k in (kernel, kernel + "_zr", kernel + "_zb", kernel + "_ws", kernel + "_rowcodes"):
             if k in t:
                 return t[k]
     except Exception:

@@ -35,6 +35,9 @@ bool compress_uses_rc(const CompressArgs& a)
     // step with no z carry to reuse, and a 3600-wide row needs per-row copies)
     if (a.g.ndim != 3 && !(a.g.ndim == 2 && (variant_bits() & 262144))) return false;
     const uint32_t nx = a.g.nx;
+    // runs of planes long enough to amortize the seed steps (c5: nz = 1008; c3's nz = 100
+    // measured slower than the single-pass kernel)
+    if (a.g.ndim == 3 && a.g.n / a.g.P < 256 && !(variant_bits() & 262144)) return false;
     // whole fields only (the slab API's tile ranges take the single-pass kernels)
     if (nx % 4 != 0 || nx < 64 || a.base != 0 || a.tile_begin != 0 ||
         (uint64_t)a.tile_end != ((uint64_t)a.g.n + kTileCodes - 1) / kTileCodes)
