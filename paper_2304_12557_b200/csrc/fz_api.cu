@@ -654,9 +654,11 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         if (hc.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;
         return FZ_OK;
     }
-    if (decode_uses_dzr(I.shape) && !(exp_bits() & 32768)) {
-        // row-walking decoder: no int32 intermediate field (fz_dzr.cu)
-        const DzrLayout Z = dzr_layout(I.shape);
+    const bool dzr = decode_uses_dzr(I.shape), dzg = !dzr && decode_uses_dzg(I.shape);
+    if ((dzr || dzg) && !(exp_bits() & 32768)) {
+        // row-walking decoders: no int32 intermediate field (fz_dzr.cu; fz_dzg.cu for rows
+        // that do not tile, through an un-shuffled code field)
+        const DzrLayout Z = dzr ? dzr_layout(I.shape) : dzg_layout(I.shape);
         DzrArgs z{};
         z.flags = a.flags;
         z.payload = a.payload;
@@ -680,7 +682,11 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         z.cdelta = reinterpret_cast<int32_t*>(wb + L.dzr_cdelta);
         z.dsum = reinterpret_cast<int32_t*>(wb + L.dzr_dsum);
         z.cd = reinterpret_cast<int32_t*>(wb + L.dzr_cd);
-        FZ_CUDA(launch_decode_dzr(z, st));
+        z.ny = (uint32_t)I.shape.dims[1];
+        z.cz = dzr ? 16u : Z.cz;
+        z.ntiles = (uint32_t)T;
+        if (dzg) z.codes = reinterpret_cast<uint16_t*>(wb + L.dzg_codes);
+        FZ_CUDA(dzr ? launch_decode_dzr(z, st) : launch_decode_dzg(z, st));
         if (deq) {
             if (dev) FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
             else FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));

@@ -33,6 +33,8 @@ __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint
         ocnt[k] = make_uint2(0, 0);
     }
     if (i == 0) {
+        // every byte of the control block defined (the host reads it back whole)
+        for (uint32_t w = 0; w < sizeof(Ctrl) / 4; ++w) reinterpret_cast<uint32_t*>(ctrl)[w] = 0u;
         ctrl->mn_enc = 0xFFFFFFFFu;
         ctrl->mx_enc = 0u;
         ctrl->first_bad = ~0ull;

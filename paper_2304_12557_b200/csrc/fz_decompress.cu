@@ -58,10 +58,12 @@ DecodeLayout decode_layout(const fz_shape& s)
     L.drange = off; off = al(off + 4 * (T + 1));
     L.ycarry = off; off = al(off + (decode_fuses_y(s) ? 4 * kMaxYseg * nz * nx : 0));
     {
-        const DzrLayout Z = dzr_layout(s);   // zero sizes unless the row-walking decoder applies
+        // zero sizes unless a row-walking decoder applies (dzg adds the code field)
+        const DzrLayout Z = decode_uses_dzr(s) ? dzr_layout(s) : dzg_layout(s);
         L.dzr_cdelta = off; off = al(off + 4 * Z.cdelta_elems);
         L.dzr_dsum = off;   off = al(off + 4 * Z.dsum_elems);
         L.dzr_cd = off;     off = al(off + 4 * Z.cd_elems);
+        L.dzg_codes = off;  off = al(off + Z.code_bytes);
     }
     L.sums_elems = sums;
     L.total = off;
@@ -71,6 +73,8 @@ DecodeLayout decode_layout(const fz_shape& s)
 __global__ void k_decode_init(Ctrl* ctrl)
 {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
+        // every byte of the control block defined (the host reads it back whole)
+        for (uint32_t w = 0; w < sizeof(Ctrl) / 4; ++w) reinterpret_cast<uint32_t*>(ctrl)[w] = 0u;
         ctrl->err = 0;
         ctrl->nnz = 0;
     }
@@ -85,6 +89,7 @@ __global__ void k_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, ui
                              uint64_t d1, uint64_t d2, uint64_t n, uint64_t T)
 {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (uint32_t w = 0; w < sizeof(Ctrl) / 4; ++w) reinterpret_cast<uint32_t*>(ctrl)[w] = 0u;
     ctrl->err = 0;
     ctrl->nnz = 0;
     auto u64 = [&](int off) {

@@ -315,8 +315,9 @@ __global__ void k_dzr_prep1(DzrArgs a, uint32_t dblocks)
 {
     __shared__ uint32_t wt8[8][8];   // [band of the round][warp] (nx / 4 <= 256 threads)
     const uint32_t nx = a.nx, nz = a.nz;
-    if (blockIdx.x < nz) {   // V(b, z, .) = S_x( sum_{b' < b} Cd(b', z, .) ), blockDim = nx / 4
+    if (blockIdx.x < nz) {   // V(b, z, .) = S_x( sum_{b' < b} Cd(b', z, .) ), blockDim >= nx / 4
         const uint32_t z = blockIdx.x, x0 = 4u * threadIdx.x;
+        const bool act = x0 < nx;   // (blockDim is nx / 4 rounded up to whole warps)
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
         uint32_t run[4] = {0u, 0u, 0u, 0u};
         for (uint32_t b0 = 0; b0 < a.nbands; b0 += 8) {   // 8 bands per round: loads in flight
@@ -324,7 +325,8 @@ __global__ void k_dzr_prep1(DzrArgs a, uint32_t dblocks)
             uint4 cv[8];
 #pragma unroll
             for (uint32_t j = 0; j < 8; ++j)
-                if (j < m) cv[j] = *reinterpret_cast<const uint4*>(a.cdelta + ((uint64_t)(b0 + j) * nz + z) * nx + x0);
+                cv[j] = (j < m && act) ? *reinterpret_cast<const uint4*>(a.cdelta + ((uint64_t)(b0 + j) * nz + z) * nx + x0)
+                                       : make_uint4(0, 0, 0, 0);
             uint32_t v[8][4];
 #pragma unroll
             for (uint32_t j = 0; j < 8; ++j) {
@@ -347,7 +349,7 @@ __global__ void k_dzr_prep1(DzrArgs a, uint32_t dblocks)
             for (uint32_t j = 0; j < 8; ++j) {
                 uint32_t pre = 0;
                 for (int w2 = 0; w2 < warp && w2 < nw; ++w2) pre += wt8[j][w2];
-                if (j < m)
+                if (j < m && act)
                     *reinterpret_cast<uint4*>(a.cdelta + ((uint64_t)(b0 + j) * nz + z) * nx + x0) =
                         make_uint4(v[j][0] + pre, v[j][1] + pre, v[j][2] + pre, v[j][3] + pre);
             }
@@ -431,7 +433,8 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_main(DzrArgs a)
 {
     dzr_resolve(a);
     extern __shared__ __align__(128) uint8_t dsm[];
-    __shared__ uint32_t tmem_base;
+    __shared__ __align__(16) uint32_t tsh[4];   // tsh[3]: TMEM base (kept off shared address 0)
+    uint32_t& tmem_base = tsh[3];
     using S = DzrSmem<NW>;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t nx = S::nx, tpp = a.tpp, nz = a.nz, PL = a.P;
@@ -587,6 +590,27 @@ static int dzr_per_sm(const void* kern, size_t sm, bool tmem)
     return per_sm < 1 ? 1 : per_sm;
 }
 
+// V, Dpre and G from pass 1's sums (shared by the row-walking decoders of fz_dzr.cu and
+// fz_dzg.cu).  One block size for the three parts of prep 1: nx / 4 rounded up to whole warps
+// (V takes one thread per x quad of a row); the Dpre and CD parts index by block * bs + thread.
+cudaError_t launch_dzr_prep(const DzrArgs& a, cudaStream_t st)
+{
+    const uint32_t bs = (a.nx / 4 + 31) / 32 * 32;
+    const uint64_t dq = (uint64_t)a.nbands * kDzrRows * (a.nx / 4);
+    const uint32_t dblocks = (uint32_t)((dq + bs - 1) / bs);
+    const uint32_t cblocks = (uint32_t)(((uint64_t)a.nchunks * (a.nx / 4) + bs - 1) / bs);
+    {
+        LaunchProf lp(K_DZR_PREP, st);
+        k_dzr_prep1<<<a.nz + dblocks + cblocks, bs, 0, st>>>(a, dblocks);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    LaunchProf lp(K_DZR_PREP, st);
+    const uint32_t g2 = (uint32_t)(((uint64_t)a.nbands * (a.nx / 4) + 127) / 128);
+    k_dzr_prep2<<<g2, 128, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 template <int NW>
 static cudaError_t dzr_launch(const DzrArgs& a, cudaStream_t st)
 {
@@ -609,24 +633,7 @@ static cudaError_t dzr_launch(const DzrArgs& a, cudaStream_t st)
     }
     // prep
     {
-        // one block size for all three parts of prep 1: nx / 4 threads (V needs one thread per
-        // x quad of a row); the Dpre and CD parts index by block * (nx / 4) + thread
-        const uint32_t bs = a.nx / 4;
-        const uint64_t dq = (uint64_t)a.nbands * kDzrRows * bs;
-        const uint32_t dblocks = (uint32_t)((dq + bs - 1) / bs);
-        const uint32_t cblocks = (uint32_t)(((uint64_t)a.nchunks * bs + bs - 1) / bs);
-        {
-            LaunchProf lp(K_DZR_PREP, st);
-            k_dzr_prep1<<<a.nz + dblocks + cblocks, bs, 0, st>>>(a, dblocks);
-        }
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        {
-            LaunchProf lp(K_DZR_PREP, st);
-            const uint32_t g2 = (uint32_t)(((uint64_t)a.nbands * (a.nx / 4) + 127) / 128);
-            k_dzr_prep2<<<g2, 128, 0, st>>>(a);
-        }
-        e = cudaGetLastError();
+        cudaError_t e = launch_dzr_prep(a, st);
         if (e != cudaSuccess) return e;
     }
     // pass 2

@@ -112,18 +112,28 @@ struct DzrArgs {
     int32_t* cdelta;            // [nbands][nz][nx]  column delta sums -> V (y carries)
     int32_t* dsum;              // [nbands][nchunks][16][nx] chunk delta sums -> prefixes
     int32_t* cd;                // [nbands][nchunks][nx] chunk column sums -> G
+    uint16_t* codes;            // dzg: the un-shuffled code field (tiles x 2048), else null
+    uint32_t ny, cz;            // dzg: rows (last band may be partial), planes per chunk
+    uint32_t ntiles;
 };
 struct DzrLayout {
-    uint32_t nbands, nchunks;
-    uint64_t cdelta_elems, dsum_elems, cd_elems;
+    uint32_t nbands, nchunks, cz;
+    uint64_t cdelta_elems, dsum_elems, cd_elems, code_bytes;
 };
 bool decode_uses_dzr(const fz_shape& s);
 DzrLayout dzr_layout(const fz_shape& s);
 cudaError_t launch_decode_dzr(const DzrArgs& a, cudaStream_t st);
+cudaError_t launch_dzr_prep(const DzrArgs& a, cudaStream_t st);
+// General row-walking decoder (fz_dzg.cu): 3-D, nx % 4 == 0, 64 <= nx <= 1024, nz >= 256;
+// the tiles are first un-shuffled into a code field (k_untile), then pass 1 / prep / pass 2
+// walk rows of that field.
+bool decode_uses_dzg(const fz_shape& s);
+DzrLayout dzg_layout(const fz_shape& s);
+cudaError_t launch_decode_dzg(const DzrArgs& a, cudaStream_t st);
 
 constexpr uint32_t kMaxYseg = 8;   // plane segments (CTAs) per plane in k_decode_planes
 struct DecodeLayout {
-    size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, drange, ycarry, dzr_cdelta, dzr_dsum, dzr_cd, total;
+    size_t ctrl, loc, bsum, xagg, xloc, xbagg, sums, drange, ycarry, dzr_cdelta, dzr_dsum, dzr_cd, dzg_codes, total;
     uint64_t sums_elems;
 };
 DecodeLayout decode_layout(const fz_shape& s);

@@ -584,3 +584,47 @@ def test_row_walking_decoder_outliers_and_old_path_equal():
     finally:
         fz.debug_set_variant(0)
     assert np.array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))
+
+
+# General row-walking decoder (fz_dzg.cu): 3-D, nx % 4 == 0, 64 <= nx <= 1024, nz >= 256,
+# rows that do not tile (partial bands, planes not whole tiles) -- un-shuffled code field, then
+# the carries' two passes.
+DZG = [
+    ("nx96", lambda: synth.generate("sines3d", (300, 20, 96))),
+    ("nx500_band9", lambda: synth.generate("hurr_u", (260, 9, 500))),
+    ("nx352", lambda: synth.generate("rtm", (256, 33, 352))),
+    ("nx1000", lambda: synth.generate("nyx_v", (257, 17, 1000))),
+]
+
+
+@pytest.mark.parametrize("name,gen", DZG, ids=[s[0] for s in DZG])
+@pytest.mark.parametrize("rel", [1e-2, 1e-4])
+def test_general_row_walking_decoder_parity(name, gen, rel):
+    d = gen()
+    ref = _check_full(d, O.REL, rel, f"dzg-{name}@{rel}")
+    codec = fz.Codec(d.shape, DEV)
+    buf = torch.from_numpy(ref).to(DEV)
+    xh = codec.decompress_device(buf)
+    codec.result()
+    st, xr = O.decompress(ref, d.size)
+    assert np.array_equal(xh.cpu().numpy().reshape(-1).view(np.uint32), xr.view(np.uint32))
+    st, qref = O.decode_q(ref, d.size)
+    assert np.array_equal(fz.debug_decode_q(buf, d.shape).cpu().numpy().reshape(-1), qref)
+
+
+def test_general_row_walking_decoder_outliers_and_old_path_equal():
+    d = synth.generate("hurr_u", (270, 12, 200)).copy()
+    eb = float(d.max() - d.min()) * 1e-4
+    rng = np.random.default_rng(13)
+    idx = rng.choice(d.size, 500, replace=False)
+    d.reshape(-1)[idx] += np.float32(50.0) * np.float32(d.max() - d.min())
+    ref = _check_full(d, O.ABS, eb, "dzg_outliers")
+    assert int.from_bytes(ref[96:104].tobytes(), "little") > 0      # delta outliers present
+    buf = torch.from_numpy(ref).to(DEV)
+    a = fz.decompress(buf)
+    fz.debug_set_variant(32768)
+    try:
+        b = fz.decompress(buf)
+    finally:
+        fz.debug_set_variant(0)
+    assert np.array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))
