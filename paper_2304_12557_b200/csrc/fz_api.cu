@@ -686,13 +686,17 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         z.cz = dzr ? 16u : Z.cz;
         z.ntiles = (uint32_t)T;
         if (dzg) z.codes = reinterpret_cast<uint16_t*>(wb + L.dzg_codes);
+        // f3 (header flag bit 3): exp32 fused into the dequantization and the value patch when
+        // the host knows the flag; device-parsed, a separate pass checks it
+        z.logt = (deq && !dev && (I.flags & 8u)) ? 1 : 0;
         FZ_CUDA(dzr ? launch_decode_dzr(z, st) : launch_decode_dzg(z, st));
         if (deq) {
-            if (dev) FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
-            else FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
-            // f3 (header flag bit 3): x^ = exp32(y^); device-parsed: the kernel checks the flag
-            if (dev) FZ_CUDA(launch_exp_inv(d_field, n, ctrl, st));
-            else if (I.flags & 8u) FZ_CUDA(launch_exp_inv(d_field, n, nullptr, st));
+            if (dev) {
+                FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
+                FZ_CUDA(launch_exp_inv(d_field, n, ctrl, st));
+            } else {
+                FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st, 0, z.logt));
+            }
         }
         if (async) return FZ_OK;
         Ctrl hz;

@@ -159,14 +159,18 @@ __global__ void k_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl)
     }
 }
 
-__global__ void k_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n)
+// logt (the row-walking decoders apply f3's exp in their dequantization): a value outlier of
+// a log-transformed stream holds y's bits, so its x^ is exp32 of them; -1: from the device-
+// parsed header flags (bit 3)
+__global__ void k_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, int logt)
 {
     const uint64_t cnt = ctrl->dec_nv;
+    const bool lt = logt < 0 ? (ctrl->dec_flags & 8u) != 0 : logt != 0;
     const uint2* rec = reinterpret_cast<const uint2*>(payload + 16 * ctrl->dec_nnz + 8 * ctrl->dec_nd);
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint2 r = rec[k];
-        if (r.x < n) out[r.x] = __uint_as_float(r.y);
+        if (r.x < n) out[r.x] = lt ? exp32(__uint_as_float(r.y)) : __uint_as_float(r.y);
     }
 }
 
@@ -981,12 +985,12 @@ __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer,
     }
 }
 
-__global__ void k_value_patch(float* out, const uint2* rec, uint64_t cnt, uint64_t n, uint64_t base)
+__global__ void k_value_patch(float* out, const uint2* rec, uint64_t cnt, uint64_t n, uint64_t base, int logt)
 {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint2 r = rec[k];
-        if (r.x >= base && r.x - base < n) out[r.x - base] = __uint_as_float(r.y);
+        if (r.x >= base && r.x - base < n) out[r.x - base] = logt ? exp32(__uint_as_float(r.y)) : __uint_as_float(r.y);
     }
 }
 
@@ -1083,10 +1087,11 @@ cudaError_t launch_record_tiles_dev(const uint8_t* payload, const Ctrl* ctrl, ui
     return cudaGetLastError();
 }
 
-cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st)
+cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st,
+                                  int logt)
 {
     LaunchProf lp(K_VPATCH, st);
-    k_value_patch_dev<<<num_sms(), 256, 0, st>>>(out, payload, ctrl, n);
+    k_value_patch_dev<<<num_sms(), 256, 0, st>>>(out, payload, ctrl, n, logt);
     return cudaGetLastError();
 }
 
@@ -1238,11 +1243,11 @@ cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t
 }
 
 cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint64_t n, cudaStream_t st,
-                               uint64_t base)
+                               uint64_t base, int logt)
 {
     if (cnt == 0) return cudaSuccess;
     LaunchProf lp(K_VPATCH, st);
-    k_value_patch<<<grid_for(cnt), 256, 0, st>>>(out, vrec, cnt, n, base);
+    k_value_patch<<<grid_for(cnt), 256, 0, st>>>(out, vrec, cnt, n, base, logt);
     return cudaGetLastError();
 }
 

@@ -292,7 +292,7 @@ __device__ __forceinline__ void dzg_rows_xscan(uint32_t (&v)[kDzgRows][4], uint3
 }
 
 // ---- pass 2 ----
-template <int NW>
+template <int NW, bool LOGT>
 __global__ void __launch_bounds__(32 * NW, 16 / NW) k_dzg_main(DzrArgs a)
 {
     dzg_resolve(a);
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) k_dzg_main(DzrArgs a)
                 for (int i = 0; i < kDzgRows; ++i) v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0u;
             } else {
                 uint4 gv = make_uint4(0, 0, 0, 0);
-                if (colv) gv = *reinterpret_cast<const uint4*>(a.cd + ((uint64_t)b * a.nchunks + c) * nx + x0);
+                if (colv) gv = dz_gsum(a.cd + x0, (uint64_t)b * a.nchunks, c, nx);
                 uint32_t run[4] = {gv.x, gv.y, gv.z, gv.w};
                 const int32_t* dp = a.dsum + ((uint64_t)b * a.nchunks + c) * kDzgRows * nx + x0;
 #pragma unroll
@@ -406,8 +406,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) k_dzg_main(DzrArgs a)
             if (colv && (uint32_t)i < cur.rows) {
                 if (w > 0.0f)
                     __stcs(reinterpret_cast<float4*>(o),
-                           make_float4(__fmul_rn(__int2float_rn((int32_t)q0), w), __fmul_rn(__int2float_rn((int32_t)q1), w),
-                                       __fmul_rn(__int2float_rn((int32_t)q2), w), __fmul_rn(__int2float_rn((int32_t)q3), w)));
+                           dzx<LOGT>(q0, q1, q2, q3, w));
                 else
                     __stcs(reinterpret_cast<int4*>(o), make_int4((int)q0, (int)q1, (int)q2, (int)q3));
             }
@@ -459,7 +458,7 @@ static cudaError_t dzg_launch(const DzrArgs& a, cudaStream_t st)
     }
     cudaError_t e = launch_dzr_prep(a, st);
     if (e != cudaSuccess) return e;
-    auto kern = k_dzg_main<NW>;
+    auto kern = a.logt > 0 ? k_dzg_main<NW, true> : k_dzg_main<NW, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     int per = dzg_per_sm<NW>((const void*)kern, sm2);
     const int tmem_cap = 512 / (NW > 4 ? 256 : 128);

@@ -20,7 +20,7 @@
 //
 //   k_dzr_sum   (pass 1) decodes every tile to delta: Cd per (band, plane), Dsum and CD per unit
 //   k_dzr_prep1 V = S_x exscan_b Cd (in place); Dpre = exscan_c Dsum (in place); CD exscan_b
-//   k_dzr_prep2 G = exscan_c (CD after exscan_b) (in place)
+//   (G = exscan_c of that, summed by pass 2 at each unit start)
 //   k_dzr_main  (pass 2) per unit: carry Q(16c - 1) from G and Dpre into tensor memory, then per
 //               plane: decode the band's tiles (gather, un-shuffle, unpack, delta patch, x scan)
 //               into shared memory, walk the 16 rows down y with the y carry from V, add the z
@@ -428,7 +428,7 @@ __global__ void k_dzr_prep2(DzrArgs a)
 }
 
 // ---- pass 2 ----
-template <int NW>
+template <int NW, bool LOGT>
 __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_main(DzrArgs a)
 {
     dzr_resolve(a);
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_main(DzrArgs a)
 #pragma unroll
                 for (int i = 0; i < kDzrRows; ++i) v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0u;
             } else {
-                const uint4 g = *reinterpret_cast<const uint4*>(a.cd + ((uint64_t)b * a.nchunks + c) * nx + x0);
+                const uint4 g = dz_gsum(a.cd + x0, (uint64_t)b * a.nchunks, c, nx);
                 uint32_t run[4] = {g.x, g.y, g.z, g.w};
                 const int32_t* dp = a.dsum + ((uint64_t)b * a.nchunks + c) * kDzrRows * nx + x0;
                 uint4 dv[kDzrRows];
@@ -554,8 +554,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_main(DzrArgs a)
             tmem_st4(taddr + 4u * i, q0, q1, q2, q3);
             if (w > 0.0f) {   // D6: x^ = fl32(fl32(q) w), one FMUL (R21)
                 __stcs(reinterpret_cast<float4*>(o),
-                       make_float4(__fmul_rn(__int2float_rn((int32_t)q0), w), __fmul_rn(__int2float_rn((int32_t)q1), w),
-                                   __fmul_rn(__int2float_rn((int32_t)q2), w), __fmul_rn(__int2float_rn((int32_t)q3), w)));
+                       dzx<LOGT>(q0, q1, q2, q3, w));
             } else {          // the integer codes (fz_debug_decode_q)
                 __stcs(reinterpret_cast<int4*>(o), make_int4((int)q0, (int)q1, (int)q2, (int)q3));
             }
@@ -603,11 +602,8 @@ cudaError_t launch_dzr_prep(const DzrArgs& a, cudaStream_t st)
         LaunchProf lp(K_DZR_PREP, st);
         k_dzr_prep1<<<a.nz + dblocks + cblocks, bs, 0, st>>>(a, dblocks);
     }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    LaunchProf lp(K_DZR_PREP, st);
-    const uint32_t g2 = (uint32_t)(((uint64_t)a.nbands * (a.nx / 4) + 127) / 128);
-    k_dzr_prep2<<<g2, 128, 0, st>>>(a);
+    // (G = the exclusive prefix over chunks of prep 1's CD scan is summed by pass 2 at each
+    // unit start: dz_gsum; k_dzr_prep2 below does it as a separate pass, kept for reference)
     return cudaGetLastError();
 }
 
@@ -638,7 +634,7 @@ static cudaError_t dzr_launch(const DzrArgs& a, cudaStream_t st)
     }
     // pass 2
     {
-        auto kern = k_dzr_main<NW>;
+        auto kern = a.logt > 0 ? k_dzr_main<NW, true> : k_dzr_main<NW, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total);
         uint64_t grid = (uint64_t)dzr_per_sm<NW>((const void*)kern, S::total, true) * num_sms();
         if (grid > U) grid = U;

@@ -115,6 +115,7 @@ struct DzrArgs {
     uint16_t* codes;            // dzg: the un-shuffled code field (tiles x 2048), else null
     uint32_t ny, cz;            // dzg: rows (last band may be partial), planes per chunk
     uint32_t ntiles;
+    int logt;                   // f3: x^ = exp32(fl32(q) w) (header flag bit 3); -1: from ctrl (dev)
 };
 struct DzrLayout {
     uint32_t nbands, nchunks, cz;
@@ -149,7 +150,10 @@ cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, c
 cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_record_tiles_dev(const uint8_t* payload, const Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
                                     cudaStream_t st);
-cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st);
+// logt: 1 / 0 (host-known f3 flag), -1 (device-parsed: the header's flag bit 3); value outliers
+// of a log-transformed stream become exp32 of their bits (the row-walking decoders fuse f3's exp)
+cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st,
+                                  int logt = 0);
 cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,
                                 cudaStream_t st);
 cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st, bool fuse_y = false);
@@ -162,7 +166,7 @@ cudaError_t launch_decode_cl(const DecodeArgs& a, uint32_t cz, cudaStream_t st);
 cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t W,
                              uint32_t* sums, float dequant_w, cudaStream_t st, const float* wp = nullptr);
 cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint64_t n,
-                               cudaStream_t st, uint64_t base = 0);
+                               cudaStream_t st, uint64_t base = 0, int logt = 0);
 cudaError_t launch_axis_sum(const int32_t* v, uint64_t L, uint64_t W, int32_t* agg, cudaStream_t st);
 cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t elems, int32_t* carry,
                               cudaStream_t st);

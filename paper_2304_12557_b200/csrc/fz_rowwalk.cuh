@@ -87,4 +87,36 @@ __device__ __forceinline__ void transpose32_regs(uint32_t (&A)[32])
     }
 }
 
+// G(b, c, x0..x0+3) = sum over chunks c' < c of R(b, c', .) (R: the chunk column sums after
+// k_dzr_prep1's exclusive scan over bands), summed at a unit start with the loads in flight
+__device__ __forceinline__ uint4 dz_gsum(const int32_t* cd, uint64_t row0, uint32_t c, uint32_t nx)
+{
+    uint4 g = make_uint4(0, 0, 0, 0);
+    for (uint32_t c0 = 0; c0 < c; c0 += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j)
+            v[j] = c0 + j < c ? *reinterpret_cast<const uint4*>(cd + (row0 + c0 + j) * nx) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) { g.x += v[j].x; g.y += v[j].y; g.z += v[j].z; g.w += v[j].w; }
+    }
+    return g;
+}
+
+// D6 (R21): x^ = fl32(fl32(q) w) for 4 codes; f3 (R25, header flag bit 3): then exp32 (the
+// decoder's exp fused into its dequantization)
+template <bool LOGT>
+__device__ __forceinline__ float4 dzx(uint32_t q0, uint32_t q1, uint32_t q2, uint32_t q3, float w)
+{
+    float4 v = make_float4(__fmul_rn(__int2float_rn((int32_t)q0), w), __fmul_rn(__int2float_rn((int32_t)q1), w),
+                           __fmul_rn(__int2float_rn((int32_t)q2), w), __fmul_rn(__int2float_rn((int32_t)q3), w));
+    if (LOGT) {
+        v.x = exp32(v.x);
+        v.y = exp32(v.y);
+        v.z = exp32(v.z);
+        v.w = exp32(v.w);
+    }
+    return v;
+}
+
 }  // namespace fz

@@ -16,6 +16,7 @@ CASES = [
     ("hurr_u", (12, 50, 52), fz.REL),                    # k_rowcodes + k_rowtiles, tile decoder
     ("cesm_t", (40, 300), fz.REL),                       # k_compress_ws (2-D)
     ("nyx_rho", (24, 32, 128), fz.PWREL),                # f3 log transform
+    ("rtm", (256, 20, 96), fz.REL),                      # k_rowcodes + k_rowtiles, k_untile + k_dzg_*
 ]
 for name, shape, mode in CASES:
     d = synth.generate(name, shape)
