@@ -2062,8 +2062,96 @@ cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uin
     return cudaGetLastError();
 }
 
+// C0 with the field streamed through shared memory by 1-D TMA bulk copies: a persistent CTA
+// owns chunks i, i + G, ... of 4096 floats; a ring of kRgStages chunks is in flight (thread 0
+// issues, an mbarrier per stage completes), every thread reduces 16 floats of the chunk.
+constexpr int kRgStages = 4;
+constexpr uint32_t kRgChunk = 4096;   // floats per chunk (16 KB)
+
+__global__ void __launch_bounds__(256) k_range_tma(const float* __restrict__ d, uint64_t n, Ctrl* ctrl)
+{
+    extern __shared__ __align__(128) float rgs[];
+    __shared__ __align__(8) uint64_t full[kRgStages];
+    const int tid = threadIdx.x;
+    const uint64_t nch = n / kRgChunk;   // whole chunks (the rest below)
+    if (tid == 0) {
+        for (int s = 0; s < kRgStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](uint64_t c, int s) {
+        mbar_expect_tx(&full[s], kRgChunk * 4);
+        tma_load_1d(rgs + (size_t)s * kRgChunk, d + c * kRgChunk, kRgChunk * 4, &full[s]);
+    };
+    uint64_t c = blockIdx.x;
+    if (tid == 0)
+        for (int s = 0; s < kRgStages; ++s)
+            if (c + (uint64_t)s * gridDim.x < nch) issue(c + (uint64_t)s * gridDim.x, s);
+    float lo = INFINITY, hi = -INFINITY;
+    unsigned long long bad = ~0ull;
+    for (uint32_t k = 0; c < nch; c += gridDim.x, ++k) {
+        const int s = k % kRgStages;
+        while (!mbar_try_wait(&full[s], (k / kRgStages) & 1u)) {
+        }
+        const float4* p = reinterpret_cast<const float4*>(rgs + (size_t)s * kRgChunk);
+        bool ok = true;
+#pragma unroll
+        for (int u = 0; u < (int)(kRgChunk / 4 / 256); ++u) {
+            const float4 v = p[tid + 256 * u];
+            lo = fminf(lo, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+            hi = fmaxf(hi, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+            ok &= fabsf(v.x) <= FLT_MAX && fabsf(v.y) <= FLT_MAX && fabsf(v.z) <= FLT_MAX && fabsf(v.w) <= FLT_MAX;
+        }
+        if (!ok) {   // rare: the first non-finite index of this thread's elements
+            for (int u = 0; u < (int)(kRgChunk / 4 / 256); ++u)
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t o = 4 * (tid + 256 * u) + e;
+                    if (!(fabsf(rgs[(size_t)s * kRgChunk + o]) <= FLT_MAX))
+                        bad = min(bad, (unsigned long long)(c * kRgChunk + o));
+                }
+        }
+        __syncthreads();   // the stage is consumed
+        if (tid == 0) {
+            const uint64_t nc = c + (uint64_t)kRgStages * gridDim.x;
+            if (nc < nch) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(nc, s);
+            }
+        }
+    }
+    // the tail past the whole chunks (CTA 0)
+    if (blockIdx.x == 0)
+        for (uint64_t j = nch * kRgChunk + tid; j < n; j += 256) {
+            const float v = __ldg(d + j);
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+            if (!(fabsf(v) <= FLT_MAX)) bad = min(bad, (unsigned long long)j);
+        }
+    uint32_t elo = f2ord(__fadd_rn(lo, 0.0f)), ehi = f2ord(__fadd_rn(hi, 0.0f));
+    if (lo == INFINITY) elo = 0xFFFFFFFFu;
+    if (hi == -INFINITY) ehi = 0u;
+    elo = __reduce_min_sync(kFull, elo);
+    ehi = __reduce_max_sync(kFull, ehi);
+    unsigned long long b = bad;
+    for (int o = 16; o; o >>= 1) b = min(b, __shfl_xor_sync(kFull, b, o));
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&ctrl->mn_enc, elo);
+        atomicMax(&ctrl->mx_enc, ehi);
+        if (b != ~0ull) atomicMin(&ctrl->first_bad, b);
+    }
+}
+
 cudaError_t launch_range(const float* d, uint64_t n, Ctrl* ctrl, cudaStream_t st)
 {
+    if (n >= (uint64_t)kRgChunk * 1184 && (reinterpret_cast<uintptr_t>(d) & 15) == 0 && !(variant_bits() & 1048576)) {
+        const size_t sm = (size_t)kRgStages * kRgChunk * 4;
+        cudaFuncSetAttribute(k_range_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        uint64_t nch = n / kRgChunk, grid = (uint64_t)num_sms() * 3;
+        if (grid > nch) grid = nch;
+        LaunchProf lp(K_RANGE, st);
+        k_range_tma<<<(unsigned)grid, 256, sm, st>>>(d, n, ctrl);
+        return cudaGetLastError();
+    }
     uint64_t want = (n / 4 + 255) / 256;
     uint64_t cap = (uint64_t)num_sms() * 8;
     unsigned grid = (unsigned)(want < 1 ? 1 : (want > cap ? cap : want));
