@@ -95,26 +95,55 @@ int fzo_range(const float* d, uint64_t n, float* mn, float* mx, int64_t* first_b
 #define FZO_SQRT_HALF 0.70710678118654752440
 
 /* log v = e ln2 + 2 atanh(s), v = m 2^e, m in [sqrt(1/2), sqrt(2)), s = (m - 1) / (m + 1):
- * 2 atanh(s) = 2 s (1 + s^2/3 + s^4/5 + ... + s^22/23), |s| <= 0.1716 (truncation < 1e-20). */
+ * 2 atanh(s) = 2 s (1 + s^2/3 + s^4/5 + ... + s^22/23), |s| <= 0.1716 (truncation < 1e-20);
+ * the polynomial in z = s^2 by Horner steps p = fma(p, z, 1/(2k+1)). */
 double fzo_log64(double v)
 {
-    int e, k;
+    int e;
     double m = frexp(v, &e), s, z, p;
     if (m < FZO_SQRT_HALF) { m = m * 2.0; e = e - 1; }
     s = (m - 1.0) / (m + 1.0);
     z = s * s;
+    /* Horner with fused multiply-adds, coefficients 1/(2k+1) rounded once (constant folding) */
     p = 1.0 / 23.0;
-    for (k = 10; k >= 0; --k) p = p * z + 1.0 / (double)(2 * k + 1);
+    p = fma(p, z, 1.0 / 21.0);
+    p = fma(p, z, 1.0 / 19.0);
+    p = fma(p, z, 1.0 / 17.0);
+    p = fma(p, z, 1.0 / 15.0);
+    p = fma(p, z, 1.0 / 13.0);
+    p = fma(p, z, 1.0 / 11.0);
+    p = fma(p, z, 1.0 / 9.0);
+    p = fma(p, z, 1.0 / 7.0);
+    p = fma(p, z, 1.0 / 5.0);
+    p = fma(p, z, 1.0 / 3.0);
+    p = fma(p, z, 1.0 / 1.0);
     return (double)e * FZO_LN2_HI + ((double)e * FZO_LN2_LO + 2.0 * s * p);
 }
 
 /* exp t = 2^k e^r, k = rint(t / ln2), r = (t - k LN2_HI) - k LN2_LO (|r| <= 0.35):
- * e^r = 1 + r (1 + r/2 (1 + r/3 (... (1 + r/17)))) (truncation < 1e-21). */
+ * e^r = sum_{n<=17} r^n / n! by Horner steps p = fma(p, r, 1/n!) (truncation < 1e-21). */
 double fzo_exp64(double t)
 {
-    int n;
-    double k = nearbyint(t * FZO_INV_LN2), r = (t - k * FZO_LN2_HI) - k * FZO_LN2_LO, p = 1.0;
-    for (n = 17; n >= 1; --n) p = 1.0 + p * r / (double)n;
+    double k = nearbyint(t * FZO_INV_LN2), r = (t - k * FZO_LN2_HI) - k * FZO_LN2_LO;
+    /* Horner with fused multiply-adds, coefficients 1/n! rounded once (constant folding) */
+    double p = 1.0 / 355687428096000.0;
+    p = fma(p, r, 1.0 / 20922789888000.0);
+    p = fma(p, r, 1.0 / 1307674368000.0);
+    p = fma(p, r, 1.0 / 87178291200.0);
+    p = fma(p, r, 1.0 / 6227020800.0);
+    p = fma(p, r, 1.0 / 479001600.0);
+    p = fma(p, r, 1.0 / 39916800.0);
+    p = fma(p, r, 1.0 / 3628800.0);
+    p = fma(p, r, 1.0 / 362880.0);
+    p = fma(p, r, 1.0 / 40320.0);
+    p = fma(p, r, 1.0 / 5040.0);
+    p = fma(p, r, 1.0 / 720.0);
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 1.0 / 2.0);
+    p = fma(p, r, 1.0 / 1.0);
+    p = fma(p, r, 1.0 / 1.0);
     return ldexp(p, (int)k);
 }
 

@@ -474,7 +474,8 @@ constexpr double kLn2Lo = 1.90821492927058770002e-10;
 constexpr double kInvLn2 = 1.4426950408889634074;
 
 // ln v (v > 0 finite) = e ln2 + 2 atanh(s): v = m 2^e, m in [sqrt(1/2), sqrt(2)),
-// s = (m - 1) / (m + 1), 2 atanh(s) = 2 s sum_{k=0}^{11} s^{2k} / (2k + 1) (Horner from k = 11)
+// s = (m - 1) / (m + 1), 2 atanh(s) = 2 s sum_{k=0}^{11} s^{2k} / (2k + 1) (Horner from k = 11
+// with fused multiply-adds, coefficients rounded once by constant folding)
 __host__ __device__ inline double log64(double v)
 {
     int e;
@@ -482,18 +483,44 @@ __host__ __device__ inline double log64(double v)
     if (m < 0.70710678118654752440) { m = m * 2.0; e = e - 1; }
     const double s = (m - 1.0) / (m + 1.0), z = s * s;
     double p = 1.0 / 23.0;
-    for (int k = 10; k >= 0; --k) p = p * z + 1.0 / (double)(2 * k + 1);
+    p = fma(p, z, 1.0 / 21.0);
+    p = fma(p, z, 1.0 / 19.0);
+    p = fma(p, z, 1.0 / 17.0);
+    p = fma(p, z, 1.0 / 15.0);
+    p = fma(p, z, 1.0 / 13.0);
+    p = fma(p, z, 1.0 / 11.0);
+    p = fma(p, z, 1.0 / 9.0);
+    p = fma(p, z, 1.0 / 7.0);
+    p = fma(p, z, 1.0 / 5.0);
+    p = fma(p, z, 1.0 / 3.0);
+    p = fma(p, z, 1.0 / 1.0);
     return (double)e * kLn2Hi + ((double)e * kLn2Lo + 2.0 * s * p);
 }
 
-// exp t = 2^k e^r, k = rint(t / ln2), r = (t - k ln2_hi) - k ln2_lo, e^r by the nested
-// Taylor form 1 + r (1 + r/2 (1 + ... (1 + r/17))) evaluated inside out
+// exp t = 2^k e^r, k = rint(t / ln2), r = (t - k ln2_hi) - k ln2_lo, e^r = sum_{n<=17} r^n/n!
+// by Horner steps p = fma(p, r, 1/n!) (coefficients rounded once by constant folding)
 __host__ __device__ inline double exp64(double t)
 {
     const double k = rint(t * kInvLn2);
     const double r = (t - k * kLn2Hi) - k * kLn2Lo;
-    double p = 1.0;
-    for (int n = 17; n >= 1; --n) p = 1.0 + p * r / (double)n;
+    double p = 1.0 / 355687428096000.0;
+    p = fma(p, r, 1.0 / 20922789888000.0);
+    p = fma(p, r, 1.0 / 1307674368000.0);
+    p = fma(p, r, 1.0 / 87178291200.0);
+    p = fma(p, r, 1.0 / 6227020800.0);
+    p = fma(p, r, 1.0 / 479001600.0);
+    p = fma(p, r, 1.0 / 39916800.0);
+    p = fma(p, r, 1.0 / 3628800.0);
+    p = fma(p, r, 1.0 / 362880.0);
+    p = fma(p, r, 1.0 / 40320.0);
+    p = fma(p, r, 1.0 / 5040.0);
+    p = fma(p, r, 1.0 / 720.0);
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 1.0 / 2.0);
+    p = fma(p, r, 1.0 / 1.0);
+    p = fma(p, r, 1.0 / 1.0);
     return ldexp(p, (int)k);
 }
 
