@@ -654,6 +654,45 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         if (hc.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;
         return FZ_OK;
     }
+    if (I.shape.ndim == 1 && !(exp_bits() & 32768)) {
+        // 1-D: tile sums, their scan, the decode with the carries -- no int32 field
+        DzrArgs z{};
+        z.flags = a.flags;
+        z.payload = a.payload;
+        z.drec = a.drec;
+        z.nnz_total = a.nnz_total;
+        z.nd = a.nd;
+        z.dev = a.dev;
+        z.wp = a.wp;
+        z.w = a.w;
+        z.ctrl = ctrl;
+        z.loc = loc;
+        z.bpre = bsum;
+        z.drange = drange;
+        z.q_out = q;
+        z.ntiles = (uint32_t)T;
+        // (f3's exp as its own pass here: fused into the decode it cost occupancy -- FP64
+        // latency chains at 148 registers -- and ran slower than the separate pass)
+        z.logt = 0;
+        uint32_t* tsum = reinterpret_cast<uint32_t*>(xagg);
+        FZ_CUDA(launch_decode_1d(z, n, tsum, tsum + T, reinterpret_cast<uint32_t*>(xbagg), st));
+        if (deq) {
+            if (dev) {
+                FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
+                FZ_CUDA(launch_exp_inv(d_field, n, ctrl, st));
+            } else {
+                FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+                if (I.flags & 8u) FZ_CUDA(launch_exp_inv(d_field, n, nullptr, st));
+            }
+        }
+        if (async) return FZ_OK;
+        Ctrl h1;
+        FZ_CUDA(cudaMemcpyAsync(&h1, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+        FZ_CUDA(cudaStreamSynchronize(st));
+        if (h1.err != 0) return err_status(h1.err);
+        if (!dev && h1.nnz != I.counts.nnz) return FZ_ERR_CORRUPT;
+        return FZ_OK;
+    }
     const bool dzr = decode_uses_dzr(I.shape), dzg = !dzr && decode_uses_dzg(I.shape);
     if ((dzr || dzg) && !(exp_bits() & 32768)) {
         // row-walking decoders: no int32 intermediate field (fz_dzr.cu; fz_dzg.cu for rows

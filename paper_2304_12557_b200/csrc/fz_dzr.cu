@@ -570,6 +570,233 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_main(DzrArgs a)
                      : "memory");
 }
 
+// ---------------------------------------------------------------------------------------
+// 1-D fields (f3's HACC-like particle arrays): the inverse Lorenzo is one prefix sum along the
+// field, q = S_x delta, so the carry into tile t is the sum of every delta before it.  Two
+// passes over the stream instead of an int32 field: k_dec1d<true> sums each tile's deltas
+// (gather by cp.async, register un-shuffle, unpack, delta patch), a two-level exclusive scan of
+// the tile sums gives the carries, and k_dec1d<false> decodes the tile again, scans it in the
+// lane (8 chains of 8) and across the warp, adds the carry, dequantizes (D6; f3's exp when the
+// header says so) and stores through a skewed shared staging as coalesced 16-byte stores.
+// ---------------------------------------------------------------------------------------
+template <bool SUM, bool LOGT>
+__global__ void __launch_bounds__(256) k_dec1d(DzrArgs a, uint64_t n, uint32_t* tsum, const uint32_t* loc,
+                                               const uint32_t* bpre)
+{
+    dzr_resolve(a);
+    extern __shared__ __align__(16) uint8_t dsm1[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* const B = dsm1 + (uint32_t)warp * (32 * 272);   // O (4 KB), then the output staging
+    const float w = a.wp ? *a.wp : a.w;
+    for (uint32_t t = blockIdx.x * 8 + warp; t < a.ntiles; t += gridDim.x * 8) {
+        dzr_gather(a, dzr_in(a, t), B, lane);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        uint32_t A[32];
+        {
+            const uint32_t* O = reinterpret_cast<const uint32_t*>(B);
+#pragma unroll
+            for (int r = 0; r < 32; ++r) A[r] = O[32 * r + lane];
+        }
+        __syncwarp();
+        transpose32_regs(A);
+        int32_t d[64];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t wd = A[j];
+            uint32_t mlo, mhi;
+            asm("prmt.b32 %0, %1, 0, 0x9999;" : "=r"(mlo) : "r"(wd));
+            asm("prmt.b32 %0, %1, 0, 0xBBBB;" : "=r"(mhi) : "r"(wd));
+            d[2 * j] = (int32_t)(((wd & 0x7FFFu) ^ mlo) - mlo);
+            d[2 * j + 1] = (int32_t)((((wd >> 16) & 0x7FFFu) ^ mhi) - mhi);
+        }
+        // delta-outliers (R7; rare): through the staging buffer (lane c's 64 at 272 c)
+        uint32_t rlo = 0, rhi = 0;
+        if (a.nd > 0) {
+            const uint32_t nd32 = (uint32_t)a.nd;
+            rlo = __ldg(a.drange + t);
+            rhi = __ldg(a.drange + t + 1);
+            rlo = rlo < nd32 ? rlo : nd32;
+            rhi = rhi < rlo ? rlo : (rhi < nd32 ? rhi : nd32);
+        }
+        if (rhi > rlo) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                *reinterpret_cast<int4*>(B + 272u * lane + 16u * k) = make_int4(d[4 * k], d[4 * k + 1], d[4 * k + 2], d[4 * k + 3]);
+            __syncwarp();
+            for (uint32_t k = rlo + lane; k < rhi; k += 32) {
+                const uint2 r = a.drec[k];
+                const uint64_t e = (uint64_t)r.x - (uint64_t)t * kTileCodes;
+                if (e < (uint64_t)kTileCodes)
+                    *reinterpret_cast<int32_t*>(B + 272u * (uint32_t)(e / 64) + 4u * (uint32_t)(e % 64)) = (int32_t)r.y;
+                else
+                    atomicCAS(&a.ctrl->err, 0, (int)FZ_ERR_CORRUPT);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int4 v = *reinterpret_cast<const int4*>(B + 272u * lane + 16u * k);
+                d[4 * k] = v.x; d[4 * k + 1] = v.y; d[4 * k + 2] = v.z; d[4 * k + 3] = v.w;
+            }
+            __syncwarp();
+        }
+        if (SUM) {
+            uint32_t sm = 0;
+#pragma unroll
+            for (int j = 0; j < 64; ++j) sm += (uint32_t)d[j];
+            sm = __reduce_add_sync(kFull, sm);
+            if (lane == 0) tsum[t] = sm;
+            continue;
+        }
+        // the lane's inclusive prefix (8 independent chains of 8), the warp's, the tile carry
+        uint32_t gt[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+#pragma unroll
+            for (int j = 1; j < 8; ++j) d[8 * g + j] = (int32_t)((uint32_t)d[8 * g + j] + (uint32_t)d[8 * g + j - 1]);
+            gt[g] = (uint32_t)d[8 * g + 7];
+        }
+#pragma unroll
+        for (int g = 1; g < 8; ++g) gt[g] += gt[g - 1];
+        uint32_t inc = gt[7];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t up = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += up;
+        }
+        const uint32_t carry = __ldg(bpre + (t >> 10)) + __ldg(loc + t);
+        const uint32_t ex = carry + inc - gt[7];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            float4 v;
+            const uint32_t a0 = ex + (k >= 2 ? gt[(k >> 1) - 1] : 0u);
+            v.x = __uint_as_float((uint32_t)d[4 * k] + a0);
+            v.y = __uint_as_float((uint32_t)d[4 * k + 1] + a0);
+            v.z = __uint_as_float((uint32_t)d[4 * k + 2] + a0);
+            v.w = __uint_as_float((uint32_t)d[4 * k + 3] + a0);
+            if (w > 0.0f) {
+                v = dzx<LOGT>(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w), w);
+            }
+            *reinterpret_cast<float4*>(B + 272u * lane + 16u * k) = v;
+        }
+        __syncwarp();
+        const uint64_t g = (uint64_t)t * kTileCodes;
+        if (g + kTileCodes <= n) {
+            float4* dst = reinterpret_cast<float4*>(a.q_out + g);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t c = (uint32_t)lane + 32u * j;   // 16-byte chunk = lane c / 16, part c % 16
+                __stcs(dst + c, *reinterpret_cast<const float4*>(B + 272u * (c >> 4) + 16u * (c & 15)));
+            }
+        } else {
+            for (uint32_t e = lane; e < (uint32_t)(n - g); e += 32)
+                a.q_out[g + e] = *reinterpret_cast<const int32_t*>(B + 272u * (e / 64) + 4u * (e % 64));
+        }
+        __syncwarp();
+    }
+}
+
+// two-level exclusive scan of the tile sums: loc = within blocks of 1024 tiles, bpre = of the
+// blocks (one block of 1024 threads for the second level)
+__global__ void __launch_bounds__(1024) k_tsum_block(const uint32_t* __restrict__ tsum, uint32_t ntiles, uint32_t* loc,
+                                                     uint32_t* bsum)
+{
+    __shared__ uint32_t ws[33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
+    const uint32_t x = i < ntiles ? tsum[i] : 0u;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t v = ws[lane];
+        uint32_t vi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, vi, o);
+            if (lane >= o) vi += y;
+        }
+        ws[lane] = vi - v;
+        if (lane == 31) ws[32] = vi;
+    }
+    __syncthreads();
+    if (i < ntiles) loc[i] = ws[warp] + inc - x;
+    if (threadIdx.x == 0) bsum[blockIdx.x] = ws[32];
+}
+
+__global__ void __launch_bounds__(1024) k_tsum_top(uint32_t* bsum, uint32_t nb)
+{
+    __shared__ uint32_t ws[33];
+    __shared__ uint32_t carry;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < nb; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t x = i < nb ? bsum[i] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) ws[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v = ws[lane];
+            uint32_t vi = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, vi, o);
+                if (lane >= o) vi += y;
+            }
+            ws[lane] = vi - v;
+            if (lane == 31) ws[32] = vi;
+        }
+        __syncthreads();
+        if (i < nb) bsum[i] = carry + ws[warp] + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += ws[32];
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_decode_1d(const DzrArgs& a, uint64_t n, uint32_t* tsum, uint32_t* loc, uint32_t* bsum,
+                             cudaStream_t st)
+{
+    const size_t sm = 8 * 32 * 272;
+    const uint64_t want = ((uint64_t)a.ntiles + 7) / 8, cap = (uint64_t)num_sms() * 3;
+    const unsigned grid = (unsigned)(want < cap ? want : cap);
+    {
+        cudaFuncSetAttribute(k_dec1d<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        LaunchProf lp(K_DZR_SUM, st);
+        k_dec1d<true, false><<<grid, 256, sm, st>>>(a, n, tsum, nullptr, nullptr);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const uint32_t nb = (a.ntiles + 1023) / 1024;
+    {
+        LaunchProf lp(K_DZR_PREP, st);
+        k_tsum_block<<<nb, 1024, 0, st>>>(tsum, a.ntiles, loc, bsum);
+    }
+    {
+        LaunchProf lp(K_DZR_PREP, st);
+        k_tsum_top<<<1, 1024, 0, st>>>(bsum, nb);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    auto kern = a.logt > 0 ? k_dec1d<false, true> : k_dec1d<false, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    LaunchProf lp(K_DZR_MAIN, st);
+    kern<<<grid, 256, sm, st>>>(a, n, nullptr, loc, bsum);
+    return cudaGetLastError();
+}
+
 template <int NW>
 static int dzr_per_sm(const void* kern, size_t sm, bool tmem)
 {

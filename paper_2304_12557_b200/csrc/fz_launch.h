@@ -125,6 +125,9 @@ bool decode_uses_dzr(const fz_shape& s);
 DzrLayout dzr_layout(const fz_shape& s);
 cudaError_t launch_decode_dzr(const DzrArgs& a, cudaStream_t st);
 cudaError_t launch_dzr_prep(const DzrArgs& a, cudaStream_t st);
+// 1-D fields: tile sums, their scan, then the decode with the carries (fz_dzr.cu)
+cudaError_t launch_decode_1d(const DzrArgs& a, uint64_t n, uint32_t* tsum, uint32_t* loc, uint32_t* bsum,
+                             cudaStream_t st);
 // General row-walking decoder (fz_dzg.cu): 3-D, nx % 4 == 0, 64 <= nx <= 1024, nz >= 256;
 // the tiles are first un-shuffled into a code field (k_untile), then pass 1 / prep / pass 2
 // walk rows of that field.
