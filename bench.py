@@ -234,6 +234,36 @@ def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_fo
         res["t_overall_gbs"] = {"compress_then_d2h": t_overall(bw["d2h"], d.nbytes / size, res["compress_gbs"]),
                                 "h2d_then_decompress": t_overall(bw["h2d"], d.nbytes / size,
                                                                  res["decompress_gbs"])}
+    # the same step captured once into a CUDA graph and replayed (as the headline value): the
+    # kernels are identical, the host launch gaps between them go
+    try:
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            codec.compress(field, mode, rel, sync=False, stream=gs)
+            codec.decompress_device(codec.out, out=xh, stream=gs)
+            gs.synchronize()
+            with torch.cuda.graph(graph, stream=gs):
+                codec.compress(field, mode, rel, sync=False, stream=gs)
+                codec.decompress_device(codec.out, out=xh, stream=gs)
+        torch.cuda.synchronize()
+        gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+        for k in range(steps):
+            flush.fill_(k & 0xFF)
+            gev[k][0].record(stream)
+            graph.replay()
+            gev[k][1].record(stream)
+        torch.cuda.synchronize()
+        assert codec.compress_result() == size
+        codec.result()
+        msg = statistics.mean(e[0].elapsed_time(e[1]) for e in gev)
+        res["step_gbs_graph"] = round(gb / (msg / 1e3), 2)
+        res["ms_per_step_graph"] = round(msg, 4)
+        del graph
+    except Exception as ex:   # graph capture is an extra measurement, never a blocker
+        res["step_gbs_graph"] = None
+        res["graph_error"] = str(ex)[:200]
     job = None
     if keep_for_parity:
         job = (name, d, rel, codec.out[:size].cpu().numpy().copy(), xh.cpu().numpy(), mode_name)
