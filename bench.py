@@ -131,16 +131,18 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def algorithmic_bytes(kernel: str, n: int, stream_bytes: int, ndim: int):
+def algorithmic_bytes(kernel: str, n: int, stream_bytes: int, ndim: int, range_fused: bool = False):
     """Algorithmic HBM bytes per launch of each kernel: the method's bytes --
     read the field (4N) and write the stream for compression, read the stream and write the
     field (4N) for decompression -- attributed to the kernel that moves them.  Intermediates a
     kernel pipeline keeps in HBM (the int32 x/y-scanned codes between k_decode_planes and the z
-    walk) are NOT algorithmic; they are reported separately (`intermediate_bytes`)."""
+    walk) are NOT algorithmic; they are reported separately (`intermediate_bytes`).  With C0
+    fused into the row walker (range_fused: no k_range launch) k_compress also reads the field
+    for the range (SV 8.d: "range pass: +4")."""
     payload = stream_bytes - 128
     return {
         "k_range": 4 * n,
-        "k_compress": 4 * n + payload,
+        "k_compress": (8 if range_fused else 4) * n + payload,
         "k_decode_tiles": payload,        # stream in; its int32 output is an intermediate
         "k_decode_planes": payload,
         "k_scan_walk": 4 * n,             # x^ out; its int32 input is an intermediate
@@ -221,9 +223,10 @@ def measure_config(name, field_name, shape, rel, flush, steps, peak, bw, keep_fo
     pk = prof.get("k_compress")
     if pk:
         t = pk[0] / pk[1]
-        a = (4 * n + payload) / (t / 1e3) / 1e9
+        fr = "k_range" not in prof   # C0 fused into the row walker: the kernel reads the field twice
+        a = ((8 if fr else 4) * n + payload) / (t / 1e3) / 1e9
         res["roofline_compress"] = {"kernel": "k_compress", "achieved": round(a, 1), "frac": round(a / peak, 4),
-                                    "ms": round(t, 4)}
+                                    "ms": round(t, 4), "range_fused": fr}
     tdec = sum(v[0] / steps for k, v in prof.items() if k in DECODE_IDS)
     if tdec > 0:
         a = (payload + 4 * n) / (tdec / 1e3) / 1e9
@@ -523,7 +526,7 @@ def chunk_local_leg(args, gsize, field, flush, stream, rel, d, peak):
     ms_g = statistics.mean(gev[k][0].elapsed_time(gev[k][1]) for k in range(args.steps))
     del graph
     ab_dec = (size - 128) + 4 * d.size
-    ab_cmp = 4 * d.size + (size - 128)
+    ab_cmp = (8 if "k_range" not in kern else 4) * d.size + (size - 128)   # C0 fused: +4 B/elem
     res = {"mode": "FZ_CHUNK_LOCAL, chunks of 16 planes x one tile (2048/nx rows)",
            "value": round(gb / (ms_g / 1e3), 3), "unit": "GB/s", "ms_per_step": round(ms_g, 4),
            "value_stream_launch": round(gb / ((ms_c + ms_d) / 1e3), 3),
@@ -535,7 +538,7 @@ def chunk_local_leg(args, gsize, field, flush, stream, rel, d, peak):
         res["decode_roofline"] = {"kernel": "k_decode_cl", "achieved": round(a, 1), "frac": round(a / peak, 4)}
     if "k_compress" in kern:
         a = ab_cmp / (kern["k_compress"] / 1e3) / 1e9
-        res["compress_roofline"] = {"kernel": "k_compress_zb", "achieved": round(a, 1), "frac": round(a / peak, 4)}
+        res["compress_roofline"] = {"kernel": "k_compress_zr", "achieved": round(a, 1), "frac": round(a / peak, 4)}
     return res
 
 
@@ -632,9 +635,10 @@ def run_single(args, wl):
     stream_bytes = size
     peak, peak_src = measured_peak()
     kernels = {}
+    fused_rng = "k_range" not in prof and "k_compress" in prof   # C0 inside the row walker
     for name, (tot, cnt) in prof.items():
         per = tot / cnt
-        ab = algorithmic_bytes(name, n, stream_bytes, len(shape))
+        ab = algorithmic_bytes(name, n, stream_bytes, len(shape), fused_rng)
         kernels[name] = {"ms_per_launch": round(per, 4), "launches": cnt,
                          "share_of_step": round(tot / (ms * args.steps), 4)}
         if ab is not None:
@@ -646,7 +650,7 @@ def run_single(args, wl):
             kernels[name]["intermediate_bytes"] = ib
     dom = max(prof.items(), key=lambda kv: kv[1][0])[0]
     per = prof[dom][0] / prof[dom][1]
-    ab = algorithmic_bytes(dom, n, stream_bytes, len(shape))
+    ab = algorithmic_bytes(dom, n, stream_bytes, len(shape), fused_rng)
     achieved = ab / (per / 1e3) / 1e9
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, dom),
@@ -657,7 +661,7 @@ def run_single(args, wl):
     comp_roof = None
     if pc:
         pk = pc[0] / pc[1]
-        abk = algorithmic_bytes("k_compress", n, stream_bytes, len(shape))
+        abk = algorithmic_bytes("k_compress", n, stream_bytes, len(shape), fused_rng)
         comp_roof = {"kernel": "k_compress", "achieved": round(abk / (pk / 1e3) / 1e9, 1),
                      "frac": round(abk / (pk / 1e3) / 1e9 / peak, 4), "ms": round(pk, 4),
                      "traffic": ncu_traffic(args.workload, "k_compress"), "algorithmic_bytes_per_launch": abk}

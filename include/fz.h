@@ -284,8 +284,17 @@ fz_status fz_debug_decode_q(const void* d_in, size_t in_size, int32_t* d_q, uint
 /* Kernel variants for A/B experiments (tools/ablation.py): process-wide bits, 0 = the
  * product configuration.  16: generic fused compressor; 1024: warp-specialized single-pass
  * compressor instead of the z-band one; 128: unfused decoder y scan; 512 / 4096: plane decoder
- * with one / two CTAs per plane.  Streams are byte-identical under every variant. */
+ * with one / two CTAs per plane; 2097152: k_range launched before the row walker instead of
+ * the walker's fused range phase (SV 8.f2); 4194304: the fused range phase reads its chunks in
+ * address order; 33554432: 16-plane units in the row-walking decoder instead of the balanced
+ * depth; 8388608: per-CTA residency trace of the row walker (fz_debug_zr_trace).  Streams are
+ * byte-identical under every variant. */
 void fz_debug_set_variant(int bits);
+
+/* Row-walker residency trace (variant 8388608): copies up to n (<= 8192) u64 to host_out,
+ * 4 per CTA of the last walker launch: globaltimer ns at start, SM id, end of the fused range
+ * phase (0 without it), end.  Returns the count copied, -1 on a CUDA error.  Debug only. */
+int fz_debug_zr_trace(unsigned long long* host_out, int n);
 
 /* Number of kernel launches issued by the last fz_compress / fz_decompress on this thread
  * (bench accounting of "gpu_launches"). */

@@ -261,9 +261,14 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
         // z-band two-pass compressor: pass 1 derives the parameters in its prologue, writes
         // the flags and stages each tile's blocks; the popcount scan of the flags gives the
         // offsets, k_compact moves the blocks, k_finalize writes totals + header
-        if (hp == nullptr) FZ_CUDA(launch_range(a.field, n, W.ctrl(), st));
+        // C0 fused into the row walker's first phase when it walks the whole field
+        // (variant bit 2097152: separate k_range launch, for A/B)
+        const bool fuse = zr && hp == nullptr && a.base == 0 && a.tile_begin == 0 && a.tile_end == tiles_of(n) &&
+                          !(exp_bits() & 2097152);
+        if (hp == nullptr && !fuse) FZ_CUDA(launch_range(a.field, n, W.ctrl(), st));
         CompressArgs b = a;
         b.derive = hp == nullptr;
+        b.fuse_range = fuse ? ((exp_bits() & 4194304) ? 2u : 1u) : 0u;
         b.eb_mode = mode;
         b.eb = eb;
         b.n_hdr = n;
@@ -722,7 +727,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         z.dsum = reinterpret_cast<int32_t*>(wb + L.dzr_dsum);
         z.cd = reinterpret_cast<int32_t*>(wb + L.dzr_cd);
         z.ny = (uint32_t)I.shape.dims[1];
-        z.cz = dzr ? 16u : Z.cz;
+        z.cz = Z.cz;
         z.ntiles = (uint32_t)T;
         if (dzg) z.codes = reinterpret_cast<uint16_t*>(wb + L.dzg_codes);
         // f3 (header flag bit 3): exp32 fused into the dequantization and the value patch when

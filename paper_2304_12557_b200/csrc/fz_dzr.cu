@@ -54,16 +54,43 @@ bool decode_uses_dzr(const fz_shape& s)
     return true;
 }
 
+static uint32_t dzr_grid_main(uint32_t nx);
+
+// Planes per unit.  Both passes hand units (band, chunk of cz planes) round-robin to a
+// persistent grid of G CTAs, so a pass lasts ceil(U / G) units: with 16-plane chunks c4
+// (32 bands x 32 chunks = 1024 units on 444 CTAs) ran 3 units where the mean is 2.3.  The
+// depth is picked per shape to minimize ceil(U / G) (cz + 2) (2 plane-equivalents for a
+// unit start: carry rebuild, first gather), cz in [8, 48]; c4 -> cz = 19, 2 units per CTA.
+// Variant 33554432 keeps cz = 16 (A/B).
+static uint32_t dzr_chunk_depth(uint64_t nz, uint32_t nbands, uint32_t nx)
+{
+    if (variant_bits() & 33554432) return (uint32_t)kDzrChunk;
+    const uint64_t G = dzr_grid_main(nx);
+    if (G == 0) return (uint32_t)kDzrChunk;   // no device (CPU-only process)
+    uint32_t best = kDzrChunk;
+    uint64_t bcost = ~0ull;
+    for (uint32_t cz = 8; cz <= 48; ++cz) {
+        const uint64_t U = (uint64_t)nbands * ((nz + cz - 1) / cz);
+        const uint64_t cost = (U + G - 1) / G * ((cz < nz ? cz : nz) + 2);
+        if (cost <= bcost) { bcost = cost; best = cz; }   // ties -> the deeper chunk (fewer starts)
+    }
+    return best;
+}
+
 DzrLayout dzr_layout(const fz_shape& s)
 {
     DzrLayout L{};
     if (!decode_uses_dzr(s)) return L;
     const uint64_t nz = s.dims[0], ny = s.dims[1], nx = s.dims[2];
     L.nbands = (uint32_t)(ny / kDzrRows);
-    L.nchunks = (uint32_t)((nz + kDzrChunk - 1) / kDzrChunk);
+    L.cz = dzr_chunk_depth(nz, L.nbands, (uint32_t)nx);
+    L.nchunks = (uint32_t)((nz + L.cz - 1) / L.cz);
+    // carry arrays sized for the larger of this depth and the A/B depth 16 (the workspace must
+    // not depend on the variant bits)
+    const uint64_t nch16 = (nz + kDzrChunk - 1) / kDzrChunk, nch_ws = L.nchunks > nch16 ? L.nchunks : nch16;
     L.cdelta_elems = (uint64_t)L.nbands * nz * nx;
-    L.dsum_elems = (uint64_t)L.nbands * L.nchunks * kDzrRows * nx;
-    L.cd_elems = (uint64_t)L.nbands * L.nchunks * nx;
+    L.dsum_elems = (uint64_t)L.nbands * nch_ws * kDzrRows * nx;
+    L.cd_elems = (uint64_t)L.nbands * nch_ws * nx;
     return L;
 }
 
@@ -234,8 +261,8 @@ __device__ __forceinline__ DzrCur dzr_unit(const DzrArgs& a, uint32_t u)
     q.valid = u < a.nbands * a.nchunks;
     q.b = u / a.nchunks;
     q.c = u - q.b * a.nchunks;
-    q.z = q.c * kDzrChunk;
-    q.z1 = min(a.nz, q.z + kDzrChunk);
+    q.z = q.c * a.cz;
+    q.z1 = min(a.nz, q.z + a.cz);
     return q;
 }
 __device__ __forceinline__ DzrCur dzr_next(const DzrArgs& a, DzrCur q)
@@ -273,7 +300,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_sum(DzrArgs a)
     uint32_t cdu[4];
     for (uint32_t k = 0; cur.valid; ++k) {
         uint8_t* buf = dsm + (k & 1u) * S::buf;
-        if (cur.z == cur.c * kDzrChunk) {
+        if (cur.z == cur.c * a.cz) {
 #pragma unroll
             for (int i = 0; i < kDzrRows; ++i) ds[i][0] = ds[i][1] = ds[i][2] = ds[i][3] = 0u;
             cdu[0] = cdu[1] = cdu[2] = cdu[3] = 0u;
@@ -470,7 +497,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_main(DzrArgs a)
     for (uint32_t k = 0; cur.valid; ++k) {
         const uint32_t b = cur.b, c = cur.c, z = cur.z;
         // ---- unit start: carry Q(16c - 1) of the band = S_x( G + S_y Dpre ) ----
-        if (z == c * kDzrChunk) {
+        if (z == c * a.cz) {
             uint32_t v[kDzrRows][4];
             if (c == 0) {
 #pragma unroll
@@ -873,6 +900,25 @@ static cudaError_t dzr_launch(const DzrArgs& a, cudaStream_t st)
         kern<<<(unsigned)grid, 32 * NW, S::total, st>>>(a);
         return cudaGetLastError();
     }
+}
+
+static uint32_t dzr_grid_main(uint32_t nx)
+{
+    static uint32_t cache[4] = {0, 0, 0, 0};   // per NW (device attributes: one device per process)
+    const int i = nx == 128 ? 0 : nx == 256 ? 1 : nx == 512 ? 2 : 3;
+    if (cache[i] == 0) {
+        int per = 1;
+        switch (i) {
+            case 0: per = dzr_per_sm<1>((const void*)k_dzr_main<1, false>, DzrSmem<1>::total, true); break;
+            case 1: per = dzr_per_sm<2>((const void*)k_dzr_main<2, false>, DzrSmem<2>::total, true); break;
+            case 2: per = dzr_per_sm<4>((const void*)k_dzr_main<4, false>, DzrSmem<4>::total, true); break;
+            default: per = dzr_per_sm<8>((const void*)k_dzr_main<8, false>, DzrSmem<8>::total, true); break;
+        }
+        const int sms = num_sms();
+        if (sms <= 0) return 0;
+        cache[i] = (uint32_t)per * (uint32_t)sms;
+    }
+    return cache[i];
 }
 
 cudaError_t launch_decode_dzr(const DzrArgs& a, cudaStream_t st)

@@ -42,6 +42,7 @@ struct Ctrl {
     uint32_t chunk;                      // f1 chunk-local stream: cz | cy << 16 (0: field-global)
     uint32_t dec_flags;                  // header flags of the stream being decoded (dev mode)
     unsigned long long log_bad;          // f3: first index outside the log domain, ~0 if none
+    uint32_t rclaim, rdone;              // fused range phase of the row walker: chunks claimed / done
 };
 static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 
@@ -730,6 +731,7 @@ struct CompressArgs {
     uint4* tstage;            // z-band pass 1: 256-block staging slot per tile (null: not available)
     uint32_t hwords;          // z-band: floats of the TMA-staged row halo (0: quantized from global)
     uint32_t cl;              // f1 chunk-local Lorenzo (z-band kernel only): chunks of kZbChunk planes x one tile
+    uint32_t fuse_range;      // row walker: C0 (range) as the kernel's first phase (no k_range launch)
     int exp;                  // variant bits (fz_debug_set_variant), bit 16: generic kernel instead of the warp-specialized one
     // row-codes path (fz_rowcodes.cu): the code field (T x 2048 u16) and the two outlier bit
     // masks (value, delta; one bit per element, rc_dmask = rc_vmask + rc_mask_words)

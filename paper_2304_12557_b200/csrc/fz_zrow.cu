@@ -38,6 +38,7 @@
 #include "fz_launch.h"
 #include "fz_rowwalk.cuh"
 
+#include <cfloat>
 #include <cstdio>
 #include <cstdlib>
 
@@ -278,6 +279,131 @@ __device__ __forceinline__ void zr_tpass(uint8_t* stg, uint8_t* msk, uint32_t RP
     for (int r0 = 1; r0 <= kZrRows; r0 += 8) zr_tgroup<8>(stg, msk, RP, spr, r0, tid, lane, warp, P);
 }
 
+// C0 (R4, R18) fused into the row walker as its first phase (SV §8.f2, "fusing
+// all GPU kernels into one"): the field's min / max and first non-finite index, then a
+// grid-wide wait, then the walk with the parameters every CTA derives from the result.
+// The unit of work is half a step's own rows (8 rows of a band in one plane: contiguous,
+// 32 nx bytes), copied by 1-D TMA into kZrRStages buffers carved from the walk's stages.
+// Chunks are CLAIMED from a global counter (batches of kZrRClaim) instead of being assigned
+// by blockIdx, so the wait cannot deadlock when fewer CTAs are resident than launched
+// (another stream's kernels on the SMs): every claimed chunk is held by a running CTA.
+// Claim order j -> chunk: position-major from the END of the compression runs (half-step
+// pos = 2L - 1 - j / G of run r = j % G), so the chunks read last -- the ones L2 still holds
+// at the wait -- are the first steps of every run of the walk.
+constexpr int kZrRStages = 4;
+
+// debug trace (variant 8388608): per CTA (start, smid, range-phase end, end) in globaltimer ns
+__device__ unsigned long long g_zr_trace[4 * 2048];
+constexpr uint32_t kZrRClaim = 8;
+
+__device__ __noinline__ void zr_range_phase(const float* field, Ctrl* ctrl, uint8_t* zsm, uint64_t* mbar,
+                                            int* ids, uint32_t nx, uint32_t PL, uint32_t nzr, uint32_t zbeg,
+                                            uint32_t U, bool natural)
+{
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const uint32_t G = gridDim.x, L2 = 2u * ((U + G - 1) / G), J = L2 * G;
+    const uint32_t cbytes = (kZrRows / 2) * 4u * nx;   // half a step's own rows
+    uint32_t jb = 0, je = 0;                          // thread 0: the claimed batch [jb, je)
+    // next valid chunk (half-step index 2u + h), or -1 when every chunk is claimed
+    auto claim = [&]() -> int {
+        for (;;) {
+            if (jb == je) {
+                jb = atomicAdd(&ctrl->rclaim, kZrRClaim);
+                je = jb + kZrRClaim;
+            }
+            if (jb >= J) return -1;
+            const uint32_t j = jb++;
+            if (natural) {   // A/B (variant 4194304): chunks in address order
+                if (j < 2u * U) {
+                    const uint32_t m = j >> 1, nb = U / nzr;
+                    return (int)(2u * ((m % nb) * nzr + m / nb) + (j & 1u));
+                }
+                continue;
+            }
+            const uint32_t pos = L2 - 1u - j / G, r = j % G;
+            const uint32_t a0 = (uint32_t)((uint64_t)U * r / G), a1 = (uint32_t)((uint64_t)U * (r + 1) / G);
+            if (a0 + pos / 2 < a1) return (int)(2u * (a0 + pos / 2) + (pos & 1u));
+        }
+    };
+    auto src_of = [&](int c) -> const float* {
+        const uint32_t u = (uint32_t)c >> 1, band = u / nzr, z = zbeg + u % nzr;
+        return field + (uint64_t)z * PL + ((uint64_t)band * kZrRows + (uint64_t)(c & 1) * (kZrRows / 2)) * nx;
+    };
+    auto issue = [&](int c, uint32_t s) {
+        mbar_expect_tx(&mbar[s], cbytes);
+        tma_load_1d(zsm + s * cbytes, src_of(c), cbytes, &mbar[s]);
+    };
+    if (tid == 0) {
+        for (uint32_t s = 0; s < (uint32_t)kZrRStages; ++s) {
+            const int c = claim();
+            ids[s] = c;
+            if (c >= 0) issue(c, s);
+        }
+    }
+    __syncthreads();
+    float lo = INFINITY, hi = -INFINITY;
+    unsigned long long bad = ~0ull;
+    uint32_t done = 0;
+    const uint32_t nv = cbytes / 16;
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t s = k % kZrRStages;
+        const int c = ids[s];   // written by thread 0 before the barrier of iteration k - 3
+        if (c < 0) break;
+        while (!mbar_try_wait(&mbar[s], (k / kZrRStages) & 1u)) {
+        }
+        const float4* p = reinterpret_cast<const float4*>(zsm + s * cbytes);
+        bool ok = true;
+        for (uint32_t i = tid; i < nv; i += nthr) {
+            const float4 v = p[i];
+            lo = fminf(lo, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+            hi = fmaxf(hi, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+            ok &= fabsf(v.x) <= FLT_MAX && fabsf(v.y) <= FLT_MAX && fabsf(v.z) <= FLT_MAX && fabsf(v.w) <= FLT_MAX;
+        }
+        if (!ok) {   // rare: the first non-finite index among this thread's elements
+            const uint64_t g0 = (uint64_t)(src_of(c) - field);
+            const float* f = reinterpret_cast<const float*>(zsm + s * cbytes);
+            for (uint32_t i = tid; i < nv; i += nthr)
+                for (uint32_t e = 0; e < 4; ++e)
+                    if (!(fabsf(f[4 * i + e]) <= FLT_MAX)) bad = min(bad, (unsigned long long)(g0 + 4 * i + e));
+        }
+        ++done;
+        __syncthreads();   // the buffer is consumed (and ids[s] read by every thread)
+        if (tid == 0) {
+            const int cn = claim();
+            ids[s] = cn;
+            if (cn >= 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(cn, s);
+            }
+        }
+    }
+    uint32_t elo = f2ord(__fadd_rn(lo, 0.0f)), ehi = f2ord(__fadd_rn(hi, 0.0f));
+    if (lo == INFINITY) elo = 0xFFFFFFFFu;
+    if (hi == -INFINITY) ehi = 0u;
+    elo = __reduce_min_sync(kFull, elo);
+    ehi = __reduce_max_sync(kFull, ehi);
+    unsigned long long b = bad;
+    for (int o = 16; o; o >>= 1) b = min(b, __shfl_xor_sync(kFull, b, o));
+    if ((tid & 31) == 0) {
+        atomicMin(&ctrl->mn_enc, elo);
+        atomicMax(&ctrl->mx_enc, ehi);
+        if (b != ~0ull) atomicMin(&ctrl->first_bad, b);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        atomicAdd(&ctrl->rdone, done);
+        uint32_t seen;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(&ctrl->rdone) : "memory");
+            if (seen >= 2u * U) break;
+            __nanosleep(64);
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // buffers go back to the walk's TMA
+    __syncthreads();
+}
+
 // NW = nx / 128 warps; at most ~170 registers per thread (12 warps per SM).
 // Shared memory per stage: 17 rows of the field (row 0 = the band's halo row y0 - 1, rows
 // 1..16 = the band) + the A-row outlier masks.  Codes of band row i are written over row i
@@ -300,11 +426,53 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
     const uint32_t PL = a.g.P;
     const uint32_t tpp = PL / kTileCodes, nbands = PL / nx / kZrRows;
     const uint32_t zbeg = a.tile_begin / tpp, zend = a.tile_end / tpp, nzr = zend - zbeg;
+    if ((a.exp & 8388608) && tid == 0 && blockIdx.x < 2048) {
+        unsigned long long ts;
+        uint32_t smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_zr_trace[4 * blockIdx.x] = ts;
+        g_zr_trace[4 * blockIdx.x + 1] = smid;
+    }
+    // TMEM for the z carry: warp 0 allocates (power-of-two columns) and frees it at the end.
+    // First thing: the SM launches its next CTA of this kernel only after this one relinquished
+    // the allocation permit (measured: a range phase before it left one CTA per SM resident)
+    constexpr uint32_t kTmemCols = NW > 4 ? 256u : 128u;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"(smem_u32(&sh.tmem)), "n"(kTmemCols) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (a.fuse_range) {
+        __shared__ __align__(8) uint64_t rbar[kZrRStages];
+        __shared__ int rids[kZrRStages];
+        static_assert(kZrRStages * (kZrRows / 2) <= NST * (kZrRows + 1), "range buffers exceed the stages");
+        if (tid == 0) {
+            for (int s = 0; s < kZrRStages; ++s) mbar_init(&rbar[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        zr_range_phase(a.field, ctrl, zsm, rbar, rids, nx, PL, nzr, zbeg, nbands * nzr, a.fuse_range == 2);
+        if ((a.exp & 8388608) && tid == 0 && blockIdx.x < 2048) {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            g_zr_trace[4 * blockIdx.x + 2] = t1;
+        }
+    }
     if (tid == 0) {
         sh.perr = 0;
         if (a.derive) {
             fz_params p;
-            const int st = params_from_range(ctrl, a.eb_mode, a.eb, a.n_hdr, &p);
+            int st;
+            if (a.fuse_range) {   // other CTAs' atomics: read from L2, not a stale L1 line
+                Ctrl rc;
+                rc.mn_enc = __ldcg(&ctrl->mn_enc);
+                rc.mx_enc = __ldcg(&ctrl->mx_enc);
+                rc.first_bad = __ldcg(&ctrl->first_bad);
+                st = params_from_range(&rc, a.eb_mode, a.eb, a.n_hdr, &p);
+            } else {
+                st = params_from_range(ctrl, a.eb_mode, a.eb, a.n_hdr, &p);
+            }
             sh.perr = st;
             if (st == FZ_OK) {
                 float h, hU;
@@ -320,13 +488,6 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
         }
         for (int s = 0; s < NST; ++s) mbar_init(&mbar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    // TMEM for the z carry: warp 0 allocates (power-of-two columns) and frees it at the end
-    constexpr uint32_t kTmemCols = NW > 4 ? 256u : 128u;
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     ::"r"(smem_u32(&sh.tmem)), "n"(kTmemCols) : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     // outlier masks start clear (phase B clears them after use)
     for (uint32_t s = 0; s < NST; ++s)
@@ -608,6 +769,11 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
             *reinterpret_cast<uint4*>(mym) = make_uint4(0, 0, 0, 0);   // clear for the stage's reuse
         }
     }
+    if ((a.exp & 8388608) && tid == 0 && blockIdx.x < 2048) {
+        unsigned long long t2;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+        g_zr_trace[4 * blockIdx.x + 3] = t2;
+    }
     tmem_free();
 }
 
@@ -655,6 +821,8 @@ cudaError_t launch_compress_zr(const CompressArgs& a, cudaStream_t st)
     if (variant_bits() & 16384) zr_pick<3>(nw, a.cl != 0, kern, sm);   // A/B: three TMA stages
     else zr_pick<kZrStages>(nw, a.cl != 0, kern, sm);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (!(variant_bits() & 16777216))   // the whole carveout as shared memory (3 CTAs per SM)
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     // residency from registers and shared memory (the occupancy API reports one CTA per SM
     // for kernels that allocate tensor memory)
     cudaFuncAttributes fa{};
@@ -676,8 +844,16 @@ cudaError_t launch_compress_zr(const CompressArgs& a, cudaStream_t st)
     if (grid > units) grid = units;
     if (grid == 0) return cudaSuccess;
     LaunchProf lp(K_COMPRESS, st);
-    kern<<<(unsigned)grid, 32 * nw, sm, st>>>(a, cz, cy);
+    CompressArgs ax = a;
+    ax.exp = variant_bits();
+    kern<<<(unsigned)grid, 32 * nw, sm, st>>>(ax, cz, cy);
     return cudaGetLastError();
 }
 
 }  // namespace fz
+
+extern "C" int fz_debug_zr_trace(unsigned long long* host, int n)
+{
+    if (n > 4 * 2048) n = 4 * 2048;
+    return cudaMemcpyFromSymbol(host, fz::g_zr_trace, sizeof(unsigned long long) * n) == cudaSuccess ? n : -1;
+}
