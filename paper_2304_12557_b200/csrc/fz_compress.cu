@@ -27,6 +27,7 @@ constexpr uint32_t kUnionHaloMax = 4097;   // union arrays when the row halo nx+
 __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint32_t ntiles,
                        int set_params, fz_params p, uint32_t chunk)
 {
+    pdl_begin();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     for (uint32_t k = i; k < ntiles; k += gridDim.x * blockDim.x) {
         status[k] = 0ull;   // per-unit look-back words (at most one per tile)
@@ -60,6 +61,7 @@ __global__ void k_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uint
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_range(const float* __restrict__ d, uint64_t n, Ctrl* ctrl)
 {
+    pdl_begin();
     constexpr int U = 4;
     float lo = INFINITY, hi = -INFINITY;
     unsigned long long bad = ~0ull;
@@ -115,6 +117,7 @@ __global__ void __launch_bounds__(256) k_range(const float* __restrict__ d, uint
 
 __global__ void k_params(Ctrl* ctrl, int mode, double eb, uint64_t n)
 {
+    pdl_begin();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     fz_params p;
     if (ctrl->err != 0) return;   // an earlier device step failed (e.g. the f3 log transform)
@@ -1715,6 +1718,7 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ fl
                                                  const uint32_t* __restrict__ bpre, const uint4* __restrict__ tstage,
                                                  uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles)
 {
+    pdl_begin();
     const int lane = threadIdx.x & 31;
     const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -1787,6 +1791,7 @@ __device__ void finalize_stream(uint8_t* out, uint64_t out_cap, uint32_t ndim, u
 __global__ void k_finalize(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64_t d0, uint64_t d1,
                            uint64_t d2, uint64_t n, uint64_t T, Ctrl* ctrl)
 {
+    pdl_begin();
     if (ctrl->err != 0 || threadIdx.x != 0) return;
     finalize_stream(out, out_cap, ndim, d0, d1, d2, n, T, ctrl, ctrl->p);
 }
@@ -1795,6 +1800,7 @@ __global__ void k_finalize(uint8_t* out, uint64_t out_cap, uint32_t ndim, uint64
 __global__ void __launch_bounds__(1024) k_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles,
                                                        const Ctrl* ctrl)
 {
+    pdl_begin();
     __shared__ uint32_t wd[32], wv[32];
     __shared__ uint32_t carry_d, carry_v;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1852,6 +1858,7 @@ __global__ void k_outlier_place_dev(const uint2* ocnt, const uint2* obase, const
                                     const uint2* dstage, const uint2* vstage, uint8_t* payload_out,
                                     uint64_t payload_cap, Ctrl* ctrl)
 {
+    pdl_begin();
     if (ctrl->err != 0) return;
     const uint64_t nd = ctrl->dcount, nv = ctrl->vcount, nnz = ctrl->nnz;
     if (nd + nv == 0) return;
@@ -2003,8 +2010,8 @@ cudaError_t launch_compact(const uint8_t* flags, const uint32_t* loc, const uint
     unsigned grid = (unsigned)((ntiles + 7) / 8);
     if (grid > (unsigned)num_sms() * 16) grid = num_sms() * 16;
     if (grid < 1) grid = 1;
-    k_compact<<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(flags), loc, bpre, tstage, payload_out,
-                                    payload_cap, ntiles);
+    { const cudaError_t e_ = launch_pdl(k_compact, dim3(grid), dim3(256), 0, st, reinterpret_cast<const uint32_t*>(flags), loc, bpre, tstage, payload_out,
+                                    payload_cap, ntiles); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -2058,7 +2065,7 @@ cudaError_t launch_init(Ctrl* ctrl, unsigned long long* status, uint2* ocnt, uin
     if (grid < 1) grid = 1;
     if (grid > 1024) grid = 1024;
     LaunchProf lp(K_INIT, st);
-    k_init<<<grid, 256, 0, st>>>(ctrl, status, ocnt, ntiles, p ? 1 : 0, pp, chunk);
+    { const cudaError_t e_ = launch_pdl(k_init, dim3(grid), dim3(256), 0, st, ctrl, status, ocnt, ntiles, p ? 1 : 0, pp, chunk); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -2070,6 +2077,7 @@ constexpr uint32_t kRgChunk = 4096;   // floats per chunk (16 KB)
 
 __global__ void __launch_bounds__(256) k_range_tma(const float* __restrict__ d, uint64_t n, Ctrl* ctrl)
 {
+    pdl_begin();
     extern __shared__ __align__(128) float rgs[];
     __shared__ __align__(8) uint64_t full[kRgStages];
     const int tid = threadIdx.x;
@@ -2149,21 +2157,21 @@ cudaError_t launch_range(const float* d, uint64_t n, Ctrl* ctrl, cudaStream_t st
         uint64_t nch = n / kRgChunk, grid = (uint64_t)num_sms() * 3;
         if (grid > nch) grid = nch;
         LaunchProf lp(K_RANGE, st);
-        k_range_tma<<<(unsigned)grid, 256, sm, st>>>(d, n, ctrl);
+        { const cudaError_t e_ = launch_pdl(k_range_tma, dim3((unsigned)grid), dim3(256), sm, st, d, n, ctrl); if (e_ != cudaSuccess) return e_; }
         return cudaGetLastError();
     }
     uint64_t want = (n / 4 + 255) / 256;
     uint64_t cap = (uint64_t)num_sms() * 8;
     unsigned grid = (unsigned)(want < 1 ? 1 : (want > cap ? cap : want));
     LaunchProf lp(K_RANGE, st);
-    k_range<<<grid, 256, 0, st>>>(d, n, ctrl);
+    { const cudaError_t e_ = launch_pdl(k_range, dim3(grid), dim3(256), 0, st, d, n, ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
 cudaError_t launch_params(Ctrl* ctrl, int mode, double eb, uint64_t n, cudaStream_t st)
 {
     LaunchProf lp(K_PARAMS, st);
-    k_params<<<1, 32, 0, st>>>(ctrl, mode, eb, n);
+    { const cudaError_t e_ = launch_pdl(k_params, dim3(1), dim3(32), 0, st, ctrl, mode, eb, n); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -2173,14 +2181,14 @@ cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint6
     uint64_t d[3] = {1, 1, 1};
     for (uint32_t k = 0; k < s.ndim; ++k) d[k] = s.dims[k];
     LaunchProf lp(K_FINALIZE, st);
-    k_finalize<<<1, 32, 0, st>>>(out, cap, s.ndim, d[0], d[1], d[2], n, T, ctrl);
+    { const cudaError_t e_ = launch_pdl(k_finalize, dim3(1), dim3(32), 0, st, out, cap, s.ndim, d[0], d[1], d[2], n, T, ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
 cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st, const Ctrl* ctrl)
 {
     LaunchProf lp(K_OUTLIERS, st);
-    k_outlier_scan<<<1, 1024, 0, st>>>(ocnt, opre, ntiles, ctrl);
+    { const cudaError_t e_ = launch_pdl(k_outlier_scan, dim3(1), dim3(1024), 0, st, ocnt, opre, ntiles, ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -2192,8 +2200,8 @@ cudaError_t launch_outlier_place_dev(const uint2* ocnt, const uint2* obase, cons
     unsigned grid = (unsigned)((ntiles + 7) / 8);
     if (grid > (unsigned)num_sms() * 8) grid = num_sms() * 8;
     if (grid < 1) grid = 1;
-    k_outlier_place_dev<<<grid, 256, 0, st>>>(ocnt, obase, opre, ntiles, dstage, vstage, payload_out, payload_cap,
-                                              ctrl);
+    { const cudaError_t e_ = launch_pdl(k_outlier_place_dev, dim3(grid), dim3(256), 0, st, ocnt, obase, opre, ntiles, dstage, vstage, payload_out, payload_cap,
+                                              ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 

@@ -72,6 +72,7 @@ DecodeLayout decode_layout(const fz_shape& s)
 
 __global__ void k_decode_init(Ctrl* ctrl)
 {
+    pdl_begin();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         // every byte of the control block defined (the host reads it back whole)
         for (uint32_t w = 0; w < sizeof(Ctrl) / 4; ++w) reinterpret_cast<uint32_t*>(ctrl)[w] = 0u;
@@ -88,6 +89,7 @@ __global__ void k_decode_init(Ctrl* ctrl)
 __global__ void k_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, uint32_t ndim, uint64_t d0,
                              uint64_t d1, uint64_t d2, uint64_t n, uint64_t T)
 {
+    pdl_begin();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (uint32_t w = 0; w < sizeof(Ctrl) / 4; ++w) reinterpret_cast<uint32_t*>(ctrl)[w] = 0u;
     ctrl->err = 0;
@@ -147,6 +149,7 @@ __global__ void k_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, 
 // Both record lists in one launch: index k < nd checks the delta list, the rest the value list.
 __global__ void k_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl)
 {
+    pdl_begin();
     const uint64_t nnz = ctrl->dec_nnz, nd = ctrl->dec_nd, nv = ctrl->dec_nv;
     const uint2* drec = reinterpret_cast<const uint2*>(payload + 16 * nnz);
     const uint2* vrec = drec + nd;
@@ -164,6 +167,7 @@ __global__ void k_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl)
 // parsed header flags (bit 3)
 __global__ void k_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, int logt)
 {
+    pdl_begin();
     const uint64_t cnt = ctrl->dec_nv;
     const bool lt = logt < 0 ? (ctrl->dec_flags & 8u) != 0 : logt != 0;
     const uint2* rec = reinterpret_cast<const uint2*>(payload + 16 * ctrl->dec_nnz + 8 * ctrl->dec_nd);
@@ -178,6 +182,7 @@ __global__ void k_record_tiles(const uint2* __restrict__ rec, uint64_t nd, uint3
                                uint32_t* __restrict__ drange, const uint8_t* payload = nullptr,
                                const Ctrl* ctrl = nullptr)
 {
+    pdl_begin();
     if (ctrl != nullptr) {   // device-driven: records and count from the parsed header
         nd = ctrl->dec_nd;
         rec = reinterpret_cast<const uint2*>(payload + 16 * ctrl->dec_nnz);
@@ -275,6 +280,7 @@ __device__ __forceinline__ Seg block_excl_seg(Seg x, Seg& total, uint32_t* wf, u
 __global__ void __launch_bounds__(1024) k_nnz_block(const uint32_t* __restrict__ flags, uint32_t ntiles,
                                                     uint32_t* loc, uint32_t* bsum)
 {
+    pdl_begin();
     __shared__ uint32_t wsum[33];
     const uint32_t t = blockIdx.x * 1024 + threadIdx.x;
     uint32_t c = 0;
@@ -293,6 +299,7 @@ __global__ void __launch_bounds__(1024) k_nnz_block(const uint32_t* __restrict__
 // D1 part 2: exclusive scan of the block totals (one block), grand total -> ctrl->nnz.
 __global__ void __launch_bounds__(1024) k_nnz_top(uint32_t* bsum, uint32_t nb, Ctrl* ctrl, uint64_t expect_nnz)
 {
+    pdl_begin();
     __shared__ uint32_t wsum[33];
     __shared__ unsigned long long carry;
     if (threadIdx.x == 0) carry = 0;
@@ -1048,7 +1055,7 @@ static unsigned grid_for(uint64_t work, int per_thread = 1)
 cudaError_t launch_decode_init(Ctrl* ctrl, cudaStream_t st)
 {
     LaunchProf lp(K_DINIT, st);
-    k_decode_init<<<1, 32, 0, st>>>(ctrl);
+    { const cudaError_t e_ = launch_pdl(k_decode_init, dim3(1), dim3(32), 0, st, ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1067,7 +1074,7 @@ cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, c
     uint64_t d[3] = {1, 1, 1};
     for (uint32_t k = 0; k < s.ndim && k < 3; ++k) d[k] = s.dims[k];
     LaunchProf lp(K_DINIT, st);
-    k_decode_hdr<<<1, 32, 0, st>>>(ctrl, in, in_size, s.ndim, d[0], d[1], d[2], n, T);
+    { const cudaError_t e_ = launch_pdl(k_decode_hdr, dim3(1), dim3(32), 0, st, ctrl, in, in_size, s.ndim, d[0], d[1], d[2], n, T); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1075,7 +1082,7 @@ cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, c
 cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, cudaStream_t st)
 {
     LaunchProf lp(K_VALIDATE, st);
-    k_validate_dev<<<num_sms(), 256, 0, st>>>(payload, n, ctrl);
+    { const cudaError_t e_ = launch_pdl(k_validate_dev, dim3(num_sms()), dim3(256), 0, st, payload, n, ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1083,7 +1090,7 @@ cudaError_t launch_record_tiles_dev(const uint8_t* payload, const Ctrl* ctrl, ui
                                     cudaStream_t st)
 {
     LaunchProf lp(K_OFFSETS, st);
-    k_record_tiles<<<grid_for((uint64_t)ntiles + 1), 256, 0, st>>>(nullptr, 0, ntiles, 0, drange, payload, ctrl);
+    { const cudaError_t e_ = launch_pdl(k_record_tiles, dim3(grid_for((uint64_t)ntiles + 1)), dim3(256), 0, st, nullptr, 0, ntiles, 0, drange, payload, ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1091,7 +1098,7 @@ cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctr
                                   int logt)
 {
     LaunchProf lp(K_VPATCH, st);
-    k_value_patch_dev<<<num_sms(), 256, 0, st>>>(out, payload, ctrl, n, logt);
+    { const cudaError_t e_ = launch_pdl(k_value_patch_dev, dim3(num_sms()), dim3(256), 0, st, out, payload, ctrl, n, logt); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1100,7 +1107,7 @@ cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles,
 {
     if (nd == 0) return cudaSuccess;
     LaunchProf lp(K_OFFSETS, st);
-    k_record_tiles<<<grid_for((uint64_t)ntiles + 1), 256, 0, st>>>(drec, nd, ntiles, gbase, drange);
+    { const cudaError_t e_ = launch_pdl(k_record_tiles, dim3(grid_for((uint64_t)ntiles + 1)), dim3(256), 0, st, drec, nd, ntiles, gbase, drange, (const uint8_t*)nullptr, (const Ctrl*)nullptr); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1110,11 +1117,11 @@ cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t*
     const uint32_t nb = (ntiles + 1023) / 1024;
     {
         LaunchProf lp(K_OFFSETS, st);
-        k_nnz_block<<<nb, 1024, 0, st>>>(reinterpret_cast<const uint32_t*>(flags), ntiles, loc, bsum);
+        { const cudaError_t e_ = launch_pdl(k_nnz_block, dim3(nb), dim3(1024), 0, st, reinterpret_cast<const uint32_t*>(flags), ntiles, loc, bsum); if (e_ != cudaSuccess) return e_; }
     }
     {
         LaunchProf lp(K_OFFSETS, st);
-        k_nnz_top<<<1, 1024, 0, st>>>(bsum, nb, ctrl, expect_nnz);
+        { const cudaError_t e_ = launch_pdl(k_nnz_top, dim3(1), dim3(1024), 0, st, bsum, nb, ctrl, expect_nnz); if (e_ != cudaSuccess) return e_; }
     }
     return cudaGetLastError();
 }

@@ -282,6 +282,7 @@ __device__ __forceinline__ uint32_t dzr_aoff(int warp, int lane)
 template <int NW>
 __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_sum(DzrArgs a)
 {
+    pdl_begin();
     dzr_resolve(a);
     extern __shared__ __align__(128) uint8_t dsm[];
     using S = DzrSmem<NW>;
@@ -340,6 +341,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_sum(DzrArgs a)
 // then CD exclusive over bands (in place) ----
 __global__ void k_dzr_prep1(DzrArgs a, uint32_t dblocks)
 {
+    pdl_begin();
     __shared__ uint32_t wt8[8][8];   // [band of the round][warp] (nx / 4 <= 256 threads)
     const uint32_t nx = a.nx, nz = a.nz;
     if (blockIdx.x < nz) {   // V(b, z, .) = S_x( sum_{b' < b} Cd(b', z, .) ), blockDim >= nx / 4
@@ -458,6 +460,7 @@ __global__ void k_dzr_prep2(DzrArgs a)
 template <int NW, bool LOGT>
 __global__ void __launch_bounds__(32 * NW, 12 / NW) k_dzr_main(DzrArgs a)
 {
+    pdl_begin();
     dzr_resolve(a);
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ __align__(16) uint32_t tsh[4];   // tsh[3]: TMEM base (kept off shared address 0)
@@ -854,7 +857,8 @@ cudaError_t launch_dzr_prep(const DzrArgs& a, cudaStream_t st)
     const uint32_t cblocks = (uint32_t)(((uint64_t)a.nchunks * (a.nx / 4) + bs - 1) / bs);
     {
         LaunchProf lp(K_DZR_PREP, st);
-        k_dzr_prep1<<<a.nz + dblocks + cblocks, bs, 0, st>>>(a, dblocks);
+        const cudaError_t e = launch_pdl(k_dzr_prep1, dim3(a.nz + dblocks + cblocks), dim3(bs), 0, st, a, dblocks);
+        if (e != cudaSuccess) return e;
     }
     // (G = the exclusive prefix over chunks of prep 1's CD scan is summed by pass 2 at each
     // unit start: dz_gsum; k_dzr_prep2 below does it as a separate pass, kept for reference)
@@ -877,8 +881,7 @@ static cudaError_t dzr_launch(const DzrArgs& a, cudaStream_t st)
             grid = (U + per - 1) / per;
         }
         LaunchProf lp(K_DZR_SUM, st);
-        kern<<<(unsigned)grid, 32 * NW, S::total, st>>>(a);
-        cudaError_t e = cudaGetLastError();
+        const cudaError_t e = launch_pdl(kern, dim3((unsigned)grid), dim3(32 * NW), S::total, st, a);
         if (e != cudaSuccess) return e;
     }
     // prep
@@ -897,8 +900,7 @@ static cudaError_t dzr_launch(const DzrArgs& a, cudaStream_t st)
             grid = (U + per - 1) / per;
         }
         LaunchProf lp(K_DZR_MAIN, st);
-        kern<<<(unsigned)grid, 32 * NW, S::total, st>>>(a);
-        return cudaGetLastError();
+        return launch_pdl(kern, dim3((unsigned)grid), dim3(32 * NW), S::total, st, a);
     }
 }
 

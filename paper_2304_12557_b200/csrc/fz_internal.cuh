@@ -637,6 +637,13 @@ __device__ __forceinline__ int bar_or(int id, int n, int pred)
                  : "=r"(r) : "r"(pred), "r"(id), "r"(n) : "memory");
     return r;
 }
+// PDL (launch_pdl): wait for the stream predecessors, then let the successor launch.  A no-op
+// for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_begin()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p)
 {
     return (uint32_t)__cvta_generic_to_shared(p);

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "fz_internal.cuh"
 
 namespace fz {
@@ -13,6 +15,29 @@ int num_sms();
 // product configuration; never read from the environment).
 int variant_bits();
 void set_variant_bits(int v);
+
+// Programmatic dependent launch (PDL, sm_90+): a kernel launched by launch_pdl may start
+// while its stream predecessor drains; it calls pdl_begin() (griddepcontrol.wait: every
+// predecessor grid complete and its memory visible, then launch_dependents) before touching
+// anything a predecessor wrote, so the launch latency and CTA ramp-up of each pipeline step
+// overlap the previous kernel's tail -- also inside a captured CUDA graph.  Variant bit
+// 67108864 launches without the attribute (A/B).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = (variant_bits() & 67108864) ? 0 : 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Kernel kinds for launch accounting and per-kernel CUDA-event timing (fz_profile_*).
 enum KernelId {

@@ -26,6 +26,7 @@ __device__ __forceinline__ float log_elem(float x, uint64_t i, unsigned long lon
 __global__ void __launch_bounds__(256) k_log_fwd(const float* __restrict__ x, float* __restrict__ y, uint64_t n,
                                                  Ctrl* ctrl)
 {
+    pdl_begin();
     unsigned long long bad = ~0ull;
     const uint64_t n4 = n / 4;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(256) k_log_fwd(const float* __restrict__ x, fl
 
 __global__ void k_log_check(const float* x, Ctrl* ctrl)
 {
+    pdl_begin();
     const unsigned long long b = ctrl->log_bad;
     if (b == ~0ull) return;
     atomicCAS(&ctrl->err, 0, isfinite(x[b]) ? (int)FZ_ERR_ARG : (int)FZ_ERR_NONFINITE);
@@ -53,6 +55,7 @@ __global__ void k_log_check(const float* x, Ctrl* ctrl)
 
 __global__ void __launch_bounds__(256) k_exp_inv(float* __restrict__ v, uint64_t n, const Ctrl* ctrl)
 {
+    pdl_begin();
     if (ctrl != nullptr && (!(ctrl->dec_flags & 8u) || ctrl->err != 0)) return;
     const uint64_t n4 = n / 4;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -78,19 +81,19 @@ cudaError_t launch_log_fwd(const float* x, float* y, uint64_t n, Ctrl* ctrl, cud
 {
     {
         LaunchProf lp(K_LOGT, st);
-        k_log_fwd<<<stream_grid(n), 256, 0, st>>>(x, y, n, ctrl);
+        { const cudaError_t e_ = launch_pdl(k_log_fwd, dim3(stream_grid(n)), dim3(256), 0, st, x, y, n, ctrl); if (e_ != cudaSuccess) return e_; }
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     LaunchProf lp(K_LOGT, st);
-    k_log_check<<<1, 1, 0, st>>>(x, ctrl);
+    { const cudaError_t e_ = launch_pdl(k_log_check, dim3(1), dim3(1), 0, st, x, ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
 cudaError_t launch_exp_inv(float* v, uint64_t n, const Ctrl* dev_ctrl, cudaStream_t st)
 {
     LaunchProf lp(K_LOGT, st);
-    k_exp_inv<<<stream_grid(n), 256, 0, st>>>(v, n, dev_ctrl);
+    { const cudaError_t e_ = launch_pdl(k_exp_inv, dim3(stream_grid(n)), dim3(256), 0, st, v, n, dev_ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 

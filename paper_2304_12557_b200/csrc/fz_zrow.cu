@@ -414,6 +414,7 @@ __device__ __noinline__ void zr_range_phase(const float* field, Ctrl* ctrl, uint
 template <int NW, bool CL, int NST>
 __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a, uint32_t cz, uint32_t cy)
 {
+    pdl_begin();
     extern __shared__ __align__(128) uint8_t zsm[];
     __shared__ ZrShared sh;
     __shared__ __align__(8) uint64_t mbar[NST];
@@ -846,7 +847,7 @@ cudaError_t launch_compress_zr(const CompressArgs& a, cudaStream_t st)
     LaunchProf lp(K_COMPRESS, st);
     CompressArgs ax = a;
     ax.exp = variant_bits();
-    kern<<<(unsigned)grid, 32 * nw, sm, st>>>(ax, cz, cy);
+    { const cudaError_t e_ = launch_pdl(kern, dim3((unsigned)grid), dim3(32 * nw), sm, st, ax, cz, cy); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
