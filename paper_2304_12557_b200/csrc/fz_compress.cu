@@ -1714,6 +1714,13 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
 
 // Pass 2: each tile's staged blocks to their final offsets (exclusive scan of the flag
 // popcounts by k_nnz_block/k_nnz_top).  One warp per tile.
+// C8: one warp per tile moves the tile's staged nonzero blocks to the payload at
+// offset bpre + loc (the popcount scan).  Sub-slot w of the staging slot holds flag word w's
+// nonzero blocks in block order, so the tile's k-th nonzero block is entry k - E[w] of
+// sub-slot w, w = #{i : I[i] <= k} (I / E = inclusive / exclusive prefixes of the 8 flag
+// words' popcounts).  Lanes take consecutive k (dense: a tile has ~50 of 256 blocks set on c4),
+// every load of the tile is issued before its stores, and the next tile's flags and offsets
+// are loaded while this tile's blocks move.
 __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ loc,
                                                  const uint32_t* __restrict__ bpre, const uint4* __restrict__ tstage,
                                                  uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles)
@@ -1722,27 +1729,56 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ fl
     const int lane = threadIdx.x & 31;
     const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t t = wid; t < ntiles; t += nw) {
-        const uint32_t fw = lane < 8 ? __ldg(flags + 8 * (uint64_t)t + lane) : 0u;
+    uint32_t t = wid;
+    if (t >= ntiles) return;
+    uint32_t fw = lane < 8 ? __ldg(flags + 8 * (uint64_t)t + lane) : 0u;
+    uint64_t off = (uint64_t)__ldg(bpre + (t >> 10)) + __ldg(loc + t);
+    for (;;) {
+        const uint32_t tn = t + nw;
+        // the next tile's metadata in flight while this one moves
+        uint32_t fwn = 0u;
+        uint64_t offn = 0;
+        if (tn < ntiles) {
+            fwn = lane < 8 ? __ldg(flags + 8 * (uint64_t)tn + lane) : 0u;
+            offn = (uint64_t)__ldg(bpre + (tn >> 10)) + __ldg(loc + tn);
+        }
         const uint32_t pc = __popc(fw);
-        uint32_t pre = pc;   // inclusive prefix over the 8 flag words (lanes 0..7)
+        uint32_t inc = pc;
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, pre, o);
-            if (lane >= o) pre += y;
+            const uint32_t y = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += y;
         }
-        pre -= pc;
-        const uint64_t off = (uint64_t)__ldg(bpre + (t >> 10)) + __ldg(loc + t);
+        uint32_t I[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) I[w] = __shfl_sync(kFull, inc, w);
+        const uint32_t total = I[7];
         const uint4* src = tstage + (uint64_t)t * kTileBlocks;
-        // sub-slot w holds flag word w's nonzero blocks (k_compress_zb), in block order
-#pragma unroll 2
-        for (int w = 0; w < 8; ++w) {
-            const uint32_t cw = __shfl_sync(kFull, pc, w), pw = __shfl_sync(kFull, pre, w);
-            if ((uint32_t)lane < cw) {
-                const uint64_t bo = 16 * (off + pw + lane);
-                if (bo + 16 <= payload_cap) __stcs(reinterpret_cast<uint4*>(payload_out + bo), __ldcs(src + 32 * w + lane));
+        constexpr int kMaxR = kTileBlocks / 32;
+        uint4 v[kMaxR];
+#pragma unroll
+        for (int r = 0; r < kMaxR; ++r) {
+            const uint32_t k = (uint32_t)lane + 32u * r;
+            if (32u * r < total && k < total) {
+                uint32_t w = 0, e = 0;
+#pragma unroll
+                for (int i = 0; i < 7; ++i)
+                    if (I[i] <= k) { w = i + 1; e = I[i]; }
+                v[r] = __ldcs(src + 32 * w + (k - e));
             }
         }
+#pragma unroll
+        for (int r = 0; r < kMaxR; ++r) {
+            const uint32_t k = (uint32_t)lane + 32u * r;
+            if (32u * r < total && k < total) {
+                const uint64_t bo = 16 * (off + k);
+                if (bo + 16 <= payload_cap) __stcs(reinterpret_cast<uint4*>(payload_out + bo), v[r]);
+            }
+        }
+        if (tn >= ntiles) break;
+        t = tn;
+        fw = fwn;
+        off = offn;
     }
 }
 
