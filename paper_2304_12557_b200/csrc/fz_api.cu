@@ -1,5 +1,6 @@
 // fz_api.cu -- the C ABI of libfz (include/fz.h): validation, workspace carving, launch
 // sequences, host<->device control-block round trips, status mapping.
+#include <nvtx3/nvToolsExt.h>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -79,9 +80,11 @@ namespace {
 // variant bits for A/B timing (128: unfused y scan in the decoder), fz_debug_set_variant
 int exp_bits() { return fz::variant_bits(); }
 
+// Per public call: launch accounting and an NVTX range named after the entry point (tracing:
+// visible in Nsight Systems / ncu --nvtx; header-only NVTX 3, a no-op without a tool attached).
 struct LaunchScope {
-    LaunchScope() { fz::t_launches = 0; }
-    ~LaunchScope() { g_last_launches = fz::t_launches; }
+    explicit LaunchScope(const char* name) { fz::t_launches = 0; nvtxRangePushA(name); }
+    ~LaunchScope() { g_last_launches = fz::t_launches; nvtxRangePop(); }
 };
 
 fz_status cuda_fail(cudaError_t e)
@@ -464,7 +467,7 @@ fz_status fz_derive_params(float mn, float mx, int eb_mode, double eb, fz_params
 fz_status fz_compress(const float* d_field, const fz_shape* s, int eb_mode, double eb, void* d_out,
                       size_t out_cap, size_t* out_size, void* d_work, size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     return compress_impl(d_field, s, nullptr, eb_mode, eb, d_out, out_cap, out_size, d_work,
                          work_bytes, static_cast<cudaStream_t>(stream));
 }
@@ -473,7 +476,7 @@ fz_status fz_compress_with_params(const float* d_field, const fz_shape* s, const
                                   void* d_out, size_t out_cap, size_t* out_size, void* d_work,
                                   size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     if (p == nullptr || !(p->w >= 1.17549435e-38f) || !std::isfinite(p->w)) return FZ_ERR_ARG;
     // the chunk-local bit selects the Lorenzo variant; the params proper (and so the header's
     // REL bit, which k_finalize derives from p.mode) never carry it
@@ -793,7 +796,7 @@ extern "C" {
 fz_status fz_decompress(const void* d_in, size_t in_size, float* d_field, uint64_t n, void* d_work,
                         size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     if (d_field == nullptr || !aligned16(d_field)) return FZ_ERR_ARG;
     return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
                            static_cast<cudaStream_t>(stream));
@@ -802,7 +805,7 @@ fz_status fz_decompress(const void* d_in, size_t in_size, float* d_field, uint64
 fz_status fz_decompress_hdr(const void* d_in, size_t in_size, const void* h_hdr, float* d_field, uint64_t n,
                             void* d_work, size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     if (d_field == nullptr || !aligned16(d_field) || h_hdr == nullptr) return FZ_ERR_ARG;
     return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
                            static_cast<cudaStream_t>(stream), h_hdr);
@@ -811,7 +814,7 @@ fz_status fz_decompress_hdr(const void* d_in, size_t in_size, const void* h_hdr,
 fz_status fz_compress_async(const float* d_field, const fz_shape* s, int eb_mode, double eb, void* d_out,
                             size_t out_cap, void* d_work, size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     uint64_t n;
     if (!shape_n(s, &n) || d_field == nullptr || d_out == nullptr || d_work == nullptr || !aligned16(d_field) ||
         !aligned16(d_out) || !aligned16(d_work))
@@ -861,7 +864,7 @@ fz_status fz_compress_result(const void* d_work, size_t out_cap, size_t* out_siz
 fz_status fz_decompress_hdr_async(const void* d_in, size_t in_size, const void* h_hdr, float* d_field, uint64_t n,
                                   void* d_work, size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     if (d_field == nullptr || !aligned16(d_field) || h_hdr == nullptr) return FZ_ERR_ARG;
     return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
                            static_cast<cudaStream_t>(stream), h_hdr, true);
@@ -870,7 +873,7 @@ fz_status fz_decompress_hdr_async(const void* d_in, size_t in_size, const void* 
 fz_status fz_decompress_async(const void* d_in, size_t in_size, const fz_shape* s, float* d_field, void* d_work,
                               size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     uint64_t n;
     if (d_field == nullptr || !aligned16(d_field) || !shape_n(s, &n)) return FZ_ERR_ARG;
     return decompress_impl(d_in, in_size, d_field, nullptr, n, d_work, work_bytes,
@@ -897,7 +900,7 @@ fz_status fz_last_header(void* h_hdr)
 fz_status fz_debug_decode_q(const void* d_in, size_t in_size, int32_t* d_q, uint64_t n, void* d_work,
                             size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     if (d_q == nullptr || !aligned16(d_q)) return FZ_ERR_ARG;
     return decompress_impl(d_in, in_size, nullptr, d_q, n, d_work, work_bytes,
                            static_cast<cudaStream_t>(stream));
@@ -907,7 +910,7 @@ fz_status fz_compress_host(const float* h_field, const fz_shape* s, int eb_mode,
                            size_t out_cap, size_t* out_size, float* d_field_scratch, void* d_out_scratch,
                            size_t d_out_cap, void* d_work, size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     uint64_t n;
     if (!shape_n(s, &n) || h_field == nullptr || h_out == nullptr || out_size == nullptr)
         return FZ_ERR_ARG;
@@ -926,7 +929,7 @@ fz_status fz_decompress_host(const void* h_in, size_t in_size, float* h_field, u
                              void* d_in_scratch, float* d_field_scratch, void* d_work, size_t work_bytes,
                              void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     if (h_in == nullptr || h_field == nullptr) return FZ_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     FZ_CUDA(cudaMemcpyAsync(d_in_scratch, h_in, in_size, cudaMemcpyHostToDevice, st));
@@ -1036,7 +1039,7 @@ const char* fz_kernel_name(int id)
 fz_status fz_slab_range(const float* d_slab, uint64_t n, float* h_min, float* h_max, int64_t* h_first_bad,
                         void* d_work, size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     if (d_slab == nullptr || !aligned16(d_slab) || d_work == nullptr || work_bytes < 512 || n == 0)
         return FZ_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1067,7 +1070,7 @@ fz_status fz_slab_compress(const float* d_slab, uint64_t slab_first, uint64_t sl
                            void* d_stage, size_t stage_cap, fz_counts* h_counts, void* d_work,
                            size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     uint64_t n;
     if (!shape_n(global, &n) || d_slab == nullptr || p == nullptr || d_stage == nullptr ||
         h_counts == nullptr || d_work == nullptr || !aligned16(d_slab) || !aligned16(d_stage) ||
@@ -1116,7 +1119,7 @@ fz_status fz_slab_place(const void* d_stage, const fz_shape* global, uint64_t tb
                         const fz_counts* local, const fz_counts* before, const fz_counts* totals,
                         const fz_params* p, int write_header, void* d_out, size_t out_cap, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     uint64_t n;
     if (!shape_n(global, &n) || d_stage == nullptr || local == nullptr || before == nullptr ||
         totals == nullptr || d_out == nullptr || (write_header && p == nullptr))
@@ -1156,7 +1159,7 @@ fz_status fz_debug_quantize(const float* d_field, const fz_shape* s, const fz_pa
                             uint32_t* d_vidx, uint32_t* d_vbits, uint64_t vcap, uint64_t* h_nv,
                             void* d_work, size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     uint64_t n;
     if (!shape_n(s, &n) || d_field == nullptr || p == nullptr || d_codes == nullptr || h_nd == nullptr ||
         h_nv == nullptr || !aligned16(d_field) || !aligned16(d_work))
@@ -1235,7 +1238,7 @@ uint64_t fz_slab_agg_elems(const fz_shape* global)
 fz_status fz_slab_decode(const void* d_stage, const fz_counts* local, const fz_shape* global, uint64_t tb,
                          uint64_t te, int32_t* d_q, int32_t* d_agg, void* d_work, size_t work_bytes, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     SlabGeo sg;
     if (d_stage == nullptr || local == nullptr || d_q == nullptr || d_agg == nullptr || d_work == nullptr ||
         !aligned16(d_stage) || !aligned16(d_q) || !aligned16(d_work))
@@ -1293,7 +1296,7 @@ fz_status fz_slab_decode_cl(const void* d_stage, const fz_counts* local, const f
                             uint64_t te, const fz_params* p, float* d_out, void* d_work, size_t work_bytes,
                             void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     SlabGeo sg;
     uint64_t n;
     if (d_stage == nullptr || local == nullptr || p == nullptr || d_out == nullptr || d_work == nullptr ||
@@ -1343,7 +1346,7 @@ fz_status fz_slab_decode_cl(const void* d_stage, const fz_counts* local, const f
 
 fz_status fz_slab_carry(const int32_t* d_aggs, uint32_t nbefore, uint64_t elems, int32_t* d_carry, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     if (d_carry == nullptr || (nbefore > 0 && d_aggs == nullptr) || elems == 0) return FZ_ERR_ARG;
     FZ_CUDA(launch_slab_carry(d_aggs, nbefore, elems, d_carry, static_cast<cudaStream_t>(stream)));
     return FZ_OK;
@@ -1352,7 +1355,7 @@ fz_status fz_slab_carry(const int32_t* d_aggs, uint32_t nbefore, uint64_t elems,
 fz_status fz_slab_finish(int32_t* d_q, const int32_t* d_carry, const void* d_stage, const fz_counts* local,
                          const fz_shape* global, uint64_t tb, uint64_t te, const fz_params* p, void* stream)
 {
-    LaunchScope ls;
+    LaunchScope ls(__func__);
     SlabGeo sg;
     if (d_q == nullptr || d_carry == nullptr || d_stage == nullptr || local == nullptr || p == nullptr)
         return FZ_ERR_ARG;

@@ -389,19 +389,23 @@ __device__ __noinline__ void zr_range_phase(const float* field, Ctrl* ctrl, uint
         atomicMax(&ctrl->mx_enc, ehi);
         if (b != ~0ull) atomicMin(&ctrl->first_bad, b);
     }
-    __syncthreads();
+    __syncthreads();   // every read of the buffers is done: they go back to the walk's TMA
     if (tid == 0) {
         __threadfence();
         atomicAdd(&ctrl->rdone, done);
-        uint32_t seen;
-        for (;;) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(&ctrl->rdone) : "memory");
-            if (seen >= 2u * U) break;
-            __nanosleep(64);
-        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // buffers go back to the walk's TMA
-    __syncthreads();
+}
+
+// The grid-wide wait of the fused range phase (thread 0): every chunk's min / max is in ctrl.
+__device__ __forceinline__ void zr_range_wait(Ctrl* ctrl, uint32_t U)
+{
+    uint32_t seen;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(&ctrl->rdone) : "memory");
+        if (seen >= 2u * U) break;
+        __nanosleep(64);
+    }
 }
 
 // NW = nx / 128 warps; at most ~170 registers per thread (12 warps per SM).
@@ -444,6 +448,33 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
                      ::"r"(smem_u32(&sh.tmem)), "n"(kTmemCols) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    const uint64_t U = (uint64_t)nbands * nzr;
+    const uint64_t u0 = U * blockIdx.x / gridDim.x, u1 = U * (blockIdx.x + 1) / gridDim.x;
+    const bool clm = CL;
+    // TMA issue of one step into its stage (thread 0): rows y0 - 1 .. y0 + 15 of plane z
+    auto issue = [&](const ZrStep& st, uint32_t k) {
+        const uint32_t s = k % NST;
+        uint8_t* dst = zsm + s * sbytes;
+        const uint32_t y0 = st.band * kZrRows;
+        const uint64_t g = (uint64_t)st.z * PL + (uint64_t)(y0 > 0 ? y0 - 1 : 0) * nx;
+        const uint32_t rows = y0 > 0 ? kZrRows + 1 : kZrRows;
+        mbar_expect_tx(&mbar[s], rows * RP);
+        tma_load_1d(dst + (y0 > 0 ? 0u : RP), a.field + (g - a.base), rows * RP, &mbar[s]);
+    };
+    ZrCursor ic = zr_cursor(u0, nzr);   // issue cursor (thread 0 only)
+    uint32_t kissue = 0;
+    // steps 0 .. NST-2 (thread 0); step k + NST - 1 once step k - 1 is done
+    auto issue_first = [&]() {
+        for (int s = 0; s + 1 < NST; ++s) {
+            const ZrStep st = zr_next(ic, u0, u1, nzr, zbeg, clm, cz);
+            if (!st.valid) break;
+            issue(st, kissue++);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) mbar_init(&mbar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     if (a.fuse_range) {
         __shared__ __align__(8) uint64_t rbar[kZrRStages];
         __shared__ int rids[kZrRStages];
@@ -454,6 +485,11 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
         }
         __syncthreads();
         zr_range_phase(a.field, ctrl, zsm, rbar, rids, nx, PL, nzr, zbeg, nbands * nzr, a.fuse_range == 2);
+        if (tid == 0) {
+            // the walk's first field rows do not depend on the range: in flight during the wait
+            issue_first();
+            zr_range_wait(ctrl, (uint32_t)U);
+        }
         if ((a.exp & 8388608) && tid == 0 && blockIdx.x < 2048) {
             unsigned long long t1;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -487,8 +523,6 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
         } else {
             sh.P = QuantP{ctrl->p.w, ctrl->p.r, ctrl->h, ctrl->p.eb32, ctrl->hU};
         }
-        for (int s = 0; s < NST; ++s) mbar_init(&mbar[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // outlier masks start clear (phase B clears them after use)
     for (uint32_t s = 0; s < NST; ++s)
@@ -506,33 +540,16 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_compress_zr(CompressArgs a
                          : "memory");
     };
     if (sh.perr != 0) {
+        // (fused range: the prefetched steps must land before the CTA exits)
+        if (tid == 0)
+            for (uint32_t k = 0; k < kissue; ++k)
+                while (!mbar_try_wait(&mbar[k % NST], (k / NST) & 1u)) {
+                }
         tmem_free();
         return;
     }
     const QuantP P = sh.P;
-
-    const uint64_t U = (uint64_t)nbands * nzr;
-    const uint64_t u0 = U * blockIdx.x / gridDim.x, u1 = U * (blockIdx.x + 1) / gridDim.x;
-    const bool clm = CL;
-    // TMA issue of one step into its stage (thread 0): rows y0 - 1 .. y0 + 15 of plane z
-    auto issue = [&](const ZrStep& st, uint32_t k) {
-        const uint32_t s = k % NST;
-        uint8_t* dst = zsm + s * sbytes;
-        const uint32_t y0 = st.band * kZrRows;
-        const uint64_t g = (uint64_t)st.z * PL + (uint64_t)(y0 > 0 ? y0 - 1 : 0) * nx;
-        const uint32_t rows = y0 > 0 ? kZrRows + 1 : kZrRows;
-        mbar_expect_tx(&mbar[s], rows * RP);
-        tma_load_1d(dst + (y0 > 0 ? 0u : RP), a.field + (g - a.base), rows * RP, &mbar[s]);
-    };
-    ZrCursor ic = zr_cursor(u0, nzr);   // issue cursor (thread 0 only)
-    uint32_t kissue = 0;
-    if (tid == 0) {   // steps 0 .. NST-2 now; step k + NST - 1 once step k - 1 is done
-        for (int s = 0; s + 1 < NST; ++s) {
-            const ZrStep st = zr_next(ic, u0, u1, nzr, zbeg, clm, cz);
-            if (!st.valid) break;
-            issue(st, kissue++);
-        }
-    }
+    if (tid == 0 && !a.fuse_range) issue_first();
     const uint32_t x0 = 128u * warp + 4u * lane;
     const bool has_shadow = warp > 0 && lane <= kZrRows;   // shadow column x = 128 w - 1
     ZrCursor pc = zr_cursor(u0, nzr);

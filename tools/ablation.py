@@ -1,9 +1,13 @@
 """Ablations of the fused design (analogous to the paper's Fig. 8).
 
-Runs bench.py (c4 512^3 REL 1e-3, 1 GPU) once per variant, selected by FZ_EXP bits read by
-libfz, and writes profiles/<round>_ablation.md with the step, compress and decompress
+Runs bench.py (c4 512^3 REL 1e-3, 1 GPU) once per variant, selected by FZ_EXP bits (bench.py
+passes them to fz_debug_set_variant; libfz reads no environment), and writes profiles/<round>_ablation.md with the step, compress and decompress
 throughput and the per-kernel times:
-  base          row-walking compressor (k_compress_zr + k_compact), row-walking decoder (k_dzr_*)
+  base          row-walking compressor with the fused range phase (k_compress_zr + k_compact),
+                row-walking decoder (k_dzr_*), programmatic dependent launch
+  range_unfused FZ_EXP=2097152 separate k_range launch before the row walker
+  no_pdl        FZ_EXP=67108864 kernels launched without programmatic dependent launch
+  dec_chunk16   FZ_EXP=33554432 decoder units of 16 planes instead of the balanced depth
   zr_3stage     FZ_EXP=16384 row walker with three TMA stages (two CTAs per SM)
   zband_comp    FZ_EXP=8192 z-band compressor (k_compress_zb, round 1's)
   ws_comp       FZ_EXP=9216 warp-specialized single-pass compressor (TMA + scanner warp look-back)
@@ -16,7 +20,8 @@ import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r02"
 steps = sys.argv[2] if len(sys.argv) > 2 else "10"
-variants = [("base", "0"), ("zr_3stage", "16384"), ("zband_comp", "8192"), ("ws_comp", "9216"),
+variants = [("base", "0"), ("range_unfused", "2097152"), ("no_pdl", "67108864"), ("dec_chunk16", "33554432"),
+            ("zr_3stage", "16384"), ("zband_comp", "8192"), ("ws_comp", "9216"),
             ("plane_dec", "32768"), ("unfused_dec", "32896")]
 rows = []
 for name, e in variants:
