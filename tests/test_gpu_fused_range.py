@@ -143,3 +143,34 @@ def test_fused_range_two_streams_concurrently():
         for c, r, s in ((ca, refs[0], s1), (cb, refs[1], s2)):
             size = c.compress_result(stream=s)
             assert size == r.size and np.array_equal(c.out[:size].cpu().numpy(), r)
+
+
+@pytest.mark.parametrize("variant", [0, SEPARATE_RANGE, 67108864])
+def test_fused_range_chunk_local_and_log_transform(variant):
+    """The fused phase under f1 (chunk-local Lorenzo: the range stays field-global) and f3
+    (FZ_EB_PWREL: the phase reads the log field in the workspace); variant 67108864 launches
+    every kernel without programmatic dependent launch -- the same bytes."""
+    d = synth.generate("nyx_v", (40, 32, 256))
+    st, ref = O.compress_chunked(d, O.REL, 1e-3, 16, 2048 // d.shape[2])
+    assert st == O.OK
+    r = synth.generate("nyx_rho", (40, 32, 256))   # positive (log-normal): log domain
+    st, ref_pw = O.compress(r, O.PWREL, 1e-3)
+    assert st == O.OK
+    fz.debug_set_variant(variant)
+    try:
+        codec = fz.Codec(d.shape, DEV)
+        buf, size = codec.compress(torch.from_numpy(d).to(DEV), fz.REL | fz.CHUNK_LOCAL, 1e-3)
+        got = buf.cpu().numpy().copy()
+        xh = codec.decompress(buf).cpu().numpy().reshape(-1)
+        buf2, size2 = codec.compress(torch.from_numpy(r).to(DEV), fz.PWREL, 1e-3)
+        got2 = buf2.cpu().numpy().copy()
+        xh2 = codec.decompress(buf2).cpu().numpy().reshape(-1)
+        torch.cuda.synchronize()
+    finally:
+        fz.debug_set_variant(0)
+    assert size == ref.size and np.array_equal(got, ref)
+    st, xref = O.decompress(ref, d.size)
+    assert np.array_equal(xh.view(np.uint32), xref.view(np.uint32))
+    assert size2 == ref_pw.size and np.array_equal(got2, ref_pw)
+    st, xref2 = O.decompress(ref_pw, r.size)
+    assert np.array_equal(xh2.view(np.uint32), xref2.view(np.uint32))
