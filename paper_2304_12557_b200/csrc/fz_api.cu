@@ -255,8 +255,8 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
         FZ_CUDA(launch_compress_rc(b, st));
         const uint32_t T = a.tile_end - a.tile_begin;
         FZ_CUDA(launch_tile_offsets(a.flags_out, T, W.zloc(), W.zbsum(), W.ctrl(), st, ~1ull));
-        FZ_CUDA(launch_compact(a.flags_out, W.zloc(), W.zbsum(), W.tstage(), a.payload_out, a.payload_cap, T, st));
-        FZ_CUDA(launch_finalize(hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
+        FZ_CUDA(launch_compact(a.flags_out, W.zloc(), W.zbsum(), W.tstage(), a.payload_out, a.payload_cap, T,
+                               hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
         if (h == nullptr) return FZ_OK;
         return read_ctrl(W, h, st);
     }
@@ -278,8 +278,8 @@ fz_status compress_run(const Work& W, const CompressArgs& a, const fz_params* hp
         FZ_CUDA(zr ? launch_compress_zr(b, st) : launch_compress_zb(b, st));
         const uint32_t T = a.tile_end - a.tile_begin;
         FZ_CUDA(launch_tile_offsets(a.flags_out, T, W.zloc(), W.zbsum(), W.ctrl(), st, ~1ull));
-        FZ_CUDA(launch_compact(a.flags_out, W.zloc(), W.zbsum(), W.tstage(), a.payload_out, a.payload_cap, T, st));
-        FZ_CUDA(launch_finalize(hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
+        FZ_CUDA(launch_compact(a.flags_out, W.zloc(), W.zbsum(), W.tstage(), a.payload_out, a.payload_cap, T,
+                               hdr_out, out_cap, s, n, tiles_of(n), W.ctrl(), st));
         if (h == nullptr) return FZ_OK;
         return read_ctrl(W, h, st);
     }
@@ -610,9 +610,8 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     const float* wp = (dev && deq) ? &ctrl->dec_w : nullptr;   // device bin width (dev mode)
     if (dev) {
         FZ_CUDA(launch_decode_hdr(ctrl, in, in_size, I.shape, n, T, st));
-        FZ_CUDA(launch_validate_dev(in + pbase, n, ctrl, st));
+        FZ_CUDA(launch_validate_dev(in + pbase, n, ctrl, (uint32_t)T, drange, st));
         FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st, ~0ull));
-        FZ_CUDA(launch_record_tiles_dev(in + pbase, ctrl, (uint32_t)T, drange, st));
     } else {
         FZ_CUDA(launch_decode_init(ctrl, st));
         FZ_CUDA(launch_validate_outliers(drec, I.counts.n_delta, n, ctrl, st));

@@ -1721,11 +1721,17 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
 // words' popcounts).  Lanes take consecutive k (dense: a tile has ~50 of 256 blocks set on c4),
 // every load of the tile is issued before its stores, and the next tile's flags and offsets
 // are loaded while this tile's blocks move.
+// C9 rides along: thread 0 of block 0 writes the totals and the header (k_finalize's work; the
+// scan's nnz and the walker's outlier counts are complete when this kernel starts).
 __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ loc,
                                                  const uint32_t* __restrict__ bpre, const uint4* __restrict__ tstage,
-                                                 uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles)
+                                                 uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles,
+                                                 uint8_t* hdr_out, uint64_t hdr_cap, uint32_t ndim, uint64_t d0,
+                                                 uint64_t d1, uint64_t d2, uint64_t n_hdr, uint64_t T_hdr, Ctrl* ctrl)
 {
     pdl_begin();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ctrl->err == 0)
+        finalize_stream(hdr_out, hdr_cap, ndim, d0, d1, d2, n_hdr, T_hdr, ctrl, ctrl->p);
     const int lane = threadIdx.x & 31;
     const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -2040,15 +2046,18 @@ cudaError_t launch_compress_zb(const CompressArgs& a_in, cudaStream_t st)
 }
 
 cudaError_t launch_compact(const uint8_t* flags, const uint32_t* loc, const uint32_t* bpre, const uint4* tstage,
-                           uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles, cudaStream_t st)
+                           uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles, uint8_t* hdr_out,
+                           uint64_t hdr_cap, const fz_shape& s, uint64_t n, uint64_t T, Ctrl* ctrl, cudaStream_t st)
 {
+    uint64_t d[3] = {1, 1, 1};
+    for (uint32_t k = 0; k < s.ndim; ++k) d[k] = s.dims[k];
     LaunchProf lp(K_COMPACT, st);
     unsigned grid = (unsigned)((ntiles + 7) / 8);
     if (grid > (unsigned)num_sms() * 16) grid = num_sms() * 16;
     if (grid < 1) grid = 1;
-    { const cudaError_t e_ = launch_pdl(k_compact, dim3(grid), dim3(256), 0, st, reinterpret_cast<const uint32_t*>(flags), loc, bpre, tstage, payload_out,
-                                    payload_cap, ntiles); if (e_ != cudaSuccess) return e_; }
-    return cudaGetLastError();
+    return launch_pdl(k_compact, dim3(grid), dim3(256), 0, st, reinterpret_cast<const uint32_t*>(flags), loc, bpre,
+                      tstage, payload_out, payload_cap, ntiles, hdr_out, hdr_cap, s.ndim, d[0], d[1], d[2], n, T,
+                      ctrl);
 }
 
 bool compress_uses_ws(const CompressArgs& a_in)

@@ -147,18 +147,31 @@ __global__ void k_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, 
 // Device-driven forms: records and counts located from ctrl (payload = the stream's payload
 // section; which = 0 delta records, 1 value records).
 // Both record lists in one launch: index k < nd checks the delta list, the rest the value list.
-__global__ void k_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl)
+// The same launch also records the per-tile delta-outlier ranges (k_record_tiles' device form:
+// drange[t] = first delta record at or after element 2048 t; readers clamp the entries).
+__global__ void k_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, uint32_t ntiles, uint32_t* drange)
 {
     pdl_begin();
     const uint64_t nnz = ctrl->dec_nnz, nd = ctrl->dec_nd, nv = ctrl->dec_nv;
     const uint2* drec = reinterpret_cast<const uint2*>(payload + 16 * nnz);
     const uint2* vrec = drec + nd;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nd + nv;
-         k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = i0; k < nd + nv; k += step) {
         const uint2* rec = k < nd ? drec : vrec;
         const uint64_t j = k < nd ? k : k - nd;
         const uint32_t idx = rec[j].x;
         if (idx >= n || (j > 0 && rec[j - 1].x >= idx)) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_CORRUPT);
+    }
+    if (nd == 0) return;   // readers skip the ranges without records
+    for (uint64_t t = i0; t <= ntiles; t += step) {
+        const int64_t e = (int64_t)(t * kTileCodes);
+        uint64_t l = 0, h = nd;
+        while (l < h) {
+            const uint64_t m = (l + h) / 2;
+            if ((int64_t)drec[m].x < e) l = m + 1;
+            else h = m;
+        }
+        drange[t] = (uint32_t)l;
     }
 }
 
@@ -277,11 +290,17 @@ __device__ __forceinline__ Seg block_excl_seg(Seg x, Seg& total, uint32_t* wf, u
 
 // D1 part 1: per-tile nonzero-block counts (popcount of the 8 flag words), exclusive scan
 // inside blocks of 1024 tiles; block totals in bsum.
+// D1 / C7: per-tile exclusive popcount prefixes of the flags inside blocks of
+// 1024 tiles (loc), block totals (bsum); the last block to finish (ticket in ctrl->scan_done,
+// zeroed with ctrl by k_init / k_decode_hdr / k_decode_init and reset here) scans the block
+// totals in place (exclusive) and writes the grand total to ctrl->nnz -- one launch.
 __global__ void __launch_bounds__(1024) k_nnz_block(const uint32_t* __restrict__ flags, uint32_t ntiles,
-                                                    uint32_t* loc, uint32_t* bsum)
+                                                    uint32_t* loc, uint32_t* bsum, Ctrl* ctrl, uint64_t expect_nnz)
 {
     pdl_begin();
     __shared__ uint32_t wsum[33];
+    __shared__ bool last;
+    __shared__ unsigned long long carry;
     const uint32_t t = blockIdx.x * 1024 + threadIdx.x;
     uint32_t c = 0;
     if (t < ntiles) {
@@ -293,33 +312,33 @@ __global__ void __launch_bounds__(1024) k_nnz_block(const uint32_t* __restrict__
     uint32_t total;
     const uint32_t ex = block_excl_sum(c, total, wsum);
     if (t < ntiles) loc[t] = ex;
-    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
-}
-
-// D1 part 2: exclusive scan of the block totals (one block), grand total -> ctrl->nnz.
-__global__ void __launch_bounds__(1024) k_nnz_top(uint32_t* bsum, uint32_t nb, Ctrl* ctrl, uint64_t expect_nnz)
-{
-    pdl_begin();
-    __shared__ uint32_t wsum[33];
-    __shared__ unsigned long long carry;
-    if (threadIdx.x == 0) carry = 0;
+    if (threadIdx.x == 0) {
+        bsum[blockIdx.x] = total;
+        __threadfence();
+        last = atomicAdd(&ctrl->scan_done, 1u) == gridDim.x - 1;
+        carry = 0;
+    }
     __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const uint32_t nb = gridDim.x;
     for (uint32_t base = 0; base < nb; base += 1024) {
         const uint32_t i = base + threadIdx.x;
-        const uint32_t x = i < nb ? bsum[i] : 0u;
-        uint32_t total;
-        const uint32_t ex = block_excl_sum(x, total, wsum);
-        if (i < nb) bsum[i] = (uint32_t)(carry + ex);
+        const uint32_t x = i < nb ? __ldcg(bsum + i) : 0u;
+        uint32_t tot;
+        const uint32_t e = block_excl_sum(x, tot, wsum);
+        if (i < nb) bsum[i] = (uint32_t)(carry + e);
         __syncthreads();
-        if (threadIdx.x == 0) carry += total;
+        if (threadIdx.x == 0) carry += tot;
         __syncthreads();
     }
     if (threadIdx.x == 0) {
+        ctrl->scan_done = 0;   // ready for the next scan on this workspace
         ctrl->nnz = carry;
-        // expect_nnz: the header's nnz, ~0 = the device-parsed one, ~1 = no check (the z-band
-        // compressor uses this scan to produce nnz)
+        // expect_nnz: the header's nnz, ~0 = the device-parsed one, ~1 = no check (the row-walking
+        // and z-band compressors use this scan to produce nnz)
         if (expect_nnz != ~1ull) {
-            const uint64_t want = expect_nnz == ~0ull ? ctrl->dec_nnz : expect_nnz;
+            const uint64_t want = expect_nnz == ~0ull ? __ldcg(&ctrl->dec_nnz) : expect_nnz;
             if (carry != want) atomicCAS(&ctrl->err, 0, (int)FZ_ERR_CORRUPT);   // popcount(flags) != nnz
         }
     }
@@ -1079,19 +1098,12 @@ cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, c
 }
 
 // fixed grids: the record counts are only known on the device
-cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, cudaStream_t st)
+cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
+                                cudaStream_t st)
 {
     LaunchProf lp(K_VALIDATE, st);
-    { const cudaError_t e_ = launch_pdl(k_validate_dev, dim3(num_sms()), dim3(256), 0, st, payload, n, ctrl); if (e_ != cudaSuccess) return e_; }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_record_tiles_dev(const uint8_t* payload, const Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
-                                    cudaStream_t st)
-{
-    LaunchProf lp(K_OFFSETS, st);
-    { const cudaError_t e_ = launch_pdl(k_record_tiles, dim3(grid_for((uint64_t)ntiles + 1)), dim3(256), 0, st, nullptr, 0, ntiles, 0, drange, payload, ctrl); if (e_ != cudaSuccess) return e_; }
-    return cudaGetLastError();
+    const unsigned g = grid_for((uint64_t)ntiles + 1), grid = g > (unsigned)num_sms() ? g : (unsigned)num_sms();
+    return launch_pdl(k_validate_dev, dim3(grid), dim3(256), 0, st, payload, n, ctrl, ntiles, drange);
 }
 
 cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st,
@@ -1114,16 +1126,10 @@ cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles,
 cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum, Ctrl* ctrl,
                                 cudaStream_t st, uint64_t expect_nnz)
 {
-    const uint32_t nb = (ntiles + 1023) / 1024;
-    {
-        LaunchProf lp(K_OFFSETS, st);
-        { const cudaError_t e_ = launch_pdl(k_nnz_block, dim3(nb), dim3(1024), 0, st, reinterpret_cast<const uint32_t*>(flags), ntiles, loc, bsum); if (e_ != cudaSuccess) return e_; }
-    }
-    {
-        LaunchProf lp(K_OFFSETS, st);
-        { const cudaError_t e_ = launch_pdl(k_nnz_top, dim3(1), dim3(1024), 0, st, bsum, nb, ctrl, expect_nnz); if (e_ != cudaSuccess) return e_; }
-    }
-    return cudaGetLastError();
+    const uint32_t nb = ntiles == 0 ? 1u : (ntiles + 1023) / 1024;   // one block even for no tiles (nnz = 0)
+    LaunchProf lp(K_OFFSETS, st);
+    return launch_pdl(k_nnz_block, dim3(nb), dim3(1024), 0, st, reinterpret_cast<const uint32_t*>(flags), ntiles, loc,
+                      bsum, ctrl, expect_nnz);
 }
 
 template <int NDIM>

@@ -43,6 +43,7 @@ struct Ctrl {
     uint32_t dec_flags;                  // header flags of the stream being decoded (dev mode)
     unsigned long long log_bad;          // f3: first index outside the log domain, ~0 if none
     uint32_t rclaim, rdone;              // fused range phase of the row walker: chunks claimed / done
+    uint32_t scan_done;                  // flag-popcount scan: blocks finished (the last one scans the totals)
 };
 static_assert(sizeof(Ctrl) <= 512, "Ctrl too large");
 

@@ -71,8 +71,10 @@ bool rc_layout_shape(const fz_shape& s);
 cudaError_t launch_compress_rc(const CompressArgs& a, cudaStream_t st);
 bool compress_uses_zr(const CompressArgs& a);   // the row-walking z-band compressor takes it (fz_zrow.cu)
 cudaError_t launch_compress_zr(const CompressArgs& a, cudaStream_t st);
+// C8 + C9: compaction of the staged blocks, and (thread 0) the totals + header of k_finalize
 cudaError_t launch_compact(const uint8_t* flags, const uint32_t* loc, const uint32_t* bpre, const uint4* tstage,
-                           uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles, cudaStream_t st);
+                           uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles, uint8_t* hdr_out,
+                           uint64_t hdr_cap, const fz_shape& s, uint64_t n, uint64_t T, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_finalize(uint8_t* out, uint64_t cap, const fz_shape& s, uint64_t n,
                             uint64_t T, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_outlier_scan(const uint2* ocnt, uint2* opre, uint32_t ntiles, cudaStream_t st,
@@ -175,9 +177,9 @@ cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t*
 // device-driven decode (counts parsed from the stream header on the device)
 cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, const fz_shape& s, uint64_t n,
                               uint64_t T, cudaStream_t st);
-cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, cudaStream_t st);
-cudaError_t launch_record_tiles_dev(const uint8_t* payload, const Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
-                                    cudaStream_t st);
+// validation of both outlier lists + the per-tile delta-record ranges, one launch (device-parsed)
+cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
+                                cudaStream_t st);
 // logt: 1 / 0 (host-known f3 flag), -1 (device-parsed: the header's flag bit 3); value outliers
 // of a log-transformed stream become exp32 of their bits (the row-walking decoders fuse f3's exp)
 cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st,
