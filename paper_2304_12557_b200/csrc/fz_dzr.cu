@@ -135,22 +135,25 @@ __device__ __forceinline__ void dzr_gather(const DzrArgs& a, const DzrIn& in, ui
 {
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t F[8] = {in.f0.x, in.f0.y, in.f0.z, in.f0.w, in.f1.x, in.f1.y, in.f1.z, in.f1.w};
-    const uint64_t base = (uint64_t)in.bpre + in.loc;
-    uint32_t pre = 0;
+    // 32-bit block indices: nnz <= 256 T < 2^29 for N < 2^32 (R16); a corrupt index (past the
+    // stream's nnz) zero-fills its block and reports FZ_ERR_CORRUPT once per lane
+    const uint32_t nnz = a.nnz_total < 0xFFFFFFFFull ? (uint32_t)a.nnz_total : 0xFFFFFFFFu;
+    uint32_t pre = in.bpre + in.loc;
+    bool bad = false;
     const uint4* pay = reinterpret_cast<const uint4*>(a.payload);
+    const uint32_t Ob = smem_u32(O) + 16u * lane;
 #pragma unroll
     for (int f = 0; f < 8; ++f) {
-        const uint64_t bi = base + pre + __popc(F[f] & lt);
-        uint32_t n = ((F[f] >> lane) & 1u) ? 16u : 0u;
-        if (n && bi >= a.nnz_total) {
-            atomicCAS(&a.ctrl->err, 0, (int)FZ_ERR_CORRUPT);
-            n = 0;
-        }
-        const uint4* src = n ? pay + bi : pay;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(O + 16u * (32u * f + lane))),
-                     "l"(src), "r"(n) : "memory");
+        const uint32_t bi = pre + __popc(F[f] & lt);
+        const bool set = (F[f] >> lane) & 1u;
+        const bool ok = bi < nnz;
+        bad |= set && !ok;
+        const uint32_t n = (set && ok) ? 16u : 0u;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(Ob + 512u * f),
+                     "l"(pay + (ok ? bi : 0u)), "r"(n) : "memory");
         pre += __popc(F[f]);
     }
+    if (bad) atomicCAS(&a.ctrl->err, 0, (int)FZ_ERR_CORRUPT);
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
