@@ -890,6 +890,7 @@ __device__ __forceinline__ void compress_body(const CompressArgs& a)
 template <int NDIM, bool VEC>
 __global__ void __launch_bounds__(kCta, 2) k_compress(CompressArgs a)
 {
+    pdl_begin();
     compress_body<NDIM, VEC>(a);
 }
 
@@ -1192,6 +1193,7 @@ __device__ void finalize_stream(uint8_t* out, uint64_t out_cap, uint32_t ndim, u
 template <int NDIM>
 __global__ void __launch_bounds__(kWsThreads, 3) k_compress_ws(CompressArgs a)
 {
+    pdl_begin();
     extern __shared__ __align__(16) int smem[];
     __shared__ WsShared sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1616,6 +1618,7 @@ __device__ __forceinline__ void tail_zb(const CompressArgs& a, ZbShared& sh, uin
 
 __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
 {
+    pdl_begin();
     extern __shared__ __align__(16) int smem[];
     __shared__ ZbShared sh;
     const int tid = threadIdx.x;
@@ -1874,6 +1877,7 @@ __global__ void k_outlier_place(const uint2* ocnt, const uint2* obase, const uin
                                 const uint2* dstage, const uint2* vstage, uint2* dout, uint2* vout,
                                 uint32_t* didx, int32_t* dval, uint32_t* vidx, uint32_t* vbits)
 {
+    pdl_begin();
     const int lane = threadIdx.x & 31;
     const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -1984,7 +1988,7 @@ static cudaError_t launch_compress_t(const CompressArgs& a, size_t sm, uint32_t 
     const uint32_t nunits = (ntiles + kUnitTiles - 1) / kUnitTiles;
     if (grid > nunits) grid = nunits;
     if (grid == 0) return cudaSuccess;
-    k_compress<NDIM, VEC><<<(unsigned)grid, kCta, sm, st>>>(a);
+    { const cudaError_t e_ = launch_pdl(k_compress<NDIM, VEC>, dim3((unsigned)grid), dim3(kCta), sm, st, a); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1999,7 +2003,7 @@ static cudaError_t launch_compress_ws(const CompressArgs& a, size_t sm, uint32_t
     const uint32_t nunits = (ntiles + kUnitTiles - 1) / kUnitTiles;
     if (grid > nunits) grid = nunits;
     if (grid == 0) return cudaSuccess;
-    k_compress_ws<NDIM><<<(unsigned)grid, kWsThreads, sm, st>>>(a);
+    { const cudaError_t e_ = launch_pdl(k_compress_ws<NDIM>, dim3((unsigned)grid), dim3(kWsThreads), sm, st, a); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -2041,7 +2045,7 @@ cudaError_t launch_compress_zb(const CompressArgs& a_in, cudaStream_t st)
     uint64_t grid = (uint64_t)per_sm * num_sms();
     if (grid > nwork) grid = nwork;
     LaunchProf lp(K_COMPRESS, st);
-    k_compress_zb<<<(unsigned)grid, kCta, sm, st>>>(a);
+    { const cudaError_t e_ = launch_pdl(k_compress_zb, dim3((unsigned)grid), dim3(kCta), sm, st, a); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -2258,8 +2262,8 @@ cudaError_t launch_outlier_place(const uint2* ocnt, const uint2* obase, const ui
     unsigned grid = (unsigned)((ntiles + 7) / 8);
     if (grid > (unsigned)num_sms() * 8) grid = num_sms() * 8;
     if (grid < 1) grid = 1;
-    k_outlier_place<<<grid, 256, 0, st>>>(ocnt, obase, opre, ntiles, dstage, vstage, dout, vout, didx, dval,
-                                          vidx, vbits);
+    { const cudaError_t e_ = launch_pdl(k_outlier_place, dim3(grid), dim3(256), 0, st, ocnt, obase, opre, ntiles, dstage, vstage, dout, vout, didx, dval,
+                                          vidx, vbits); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 

@@ -135,6 +135,7 @@ __global__ void k_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, ui
 // Outlier lists must be strictly increasing and inside the field.
 __global__ void k_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, Ctrl* ctrl)
 {
+    pdl_begin();
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t idx = rec[k].x;
@@ -348,6 +349,7 @@ __global__ void __launch_bounds__(1024) k_nnz_block(const uint32_t* __restrict__
 // starts inside a row).
 __global__ void __launch_bounds__(1024) k_xseg_block(const uint2* xagg, uint32_t ntiles, uint2* xloc, uint2* xbagg)
 {
+    pdl_begin();
     __shared__ uint32_t wf[33], wv[33];
     const uint32_t t = blockIdx.x * 1024 + threadIdx.x;
     const uint2 g = t < ntiles ? xagg[t] : make_uint2(0, 0);
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(1024) k_xseg_block(const uint2* xagg, uint32_t
 
 __global__ void __launch_bounds__(1024) k_xseg_top(uint2* xbagg, uint32_t nb)
 {
+    pdl_begin();
     __shared__ uint32_t wf[33], wv[33];
     __shared__ uint32_t cf, cv;
     if (threadIdx.x == 0) { cf = 0; cv = 0; }
@@ -601,6 +604,7 @@ __device__ __forceinline__ void resolve_dev(DecodeArgs& a)
 template <int NDIM>
 __global__ void __launch_bounds__(kCta) k_decode_tiles(DecodeArgs a)
 {
+    pdl_begin();
     resolve_dev(a);
     __shared__ DecSmem sm;
     const int tid = threadIdx.x;
@@ -649,6 +653,7 @@ __device__ __forceinline__ void store_row(int32_t* o, const uint32_t (&v)[C])
 template <int R>
 __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
 {
+    pdl_begin();
     resolve_dev(a);
     constexpr int C = 8 / R;
     __shared__ DecSmem sm;
@@ -712,6 +717,7 @@ __global__ void __launch_bounds__(kCta) k_decode_planes(DecodeArgs a)
 template <int R>
 __global__ void __launch_bounds__(kCta, 5) k_decode_cl(DecodeArgs a, uint32_t cz)
 {
+    pdl_begin();
     resolve_dev(a);
     constexpr int C = 8 / R;
     __shared__ DecSmem sm;
@@ -778,6 +784,7 @@ __global__ void __launch_bounds__(kCta, 5) k_decode_cl(DecodeArgs a, uint32_t cz
 // above it (shared memory), and the z prefix of those 8 elements in registers.
 __global__ void __launch_bounds__(kCta) k_decode_cl_short(DecodeArgs a, uint32_t cz)
 {
+    pdl_begin();
     resolve_dev(a);
     __shared__ DecSmem sm;
     const int tid = threadIdx.x;
@@ -827,6 +834,7 @@ template <int NDIM>
 __global__ void __launch_bounds__(kCta) k_xfix(int32_t* q, const uint2* xloc, const uint2* xbpre, uint32_t ntiles,
                                                uint32_t n, uint32_t nx, float w_in, int carries, const float* wp)
 {
+    pdl_begin();
     const float w = wp ? *wp : w_in;
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t s = (uint64_t)t * kTileCodes;
@@ -861,6 +869,7 @@ __global__ void __launch_bounds__(kCta) k_xfix(int32_t* q, const uint2* xloc, co
 __global__ void k_scan_sums(const int32_t* __restrict__ v, uint64_t outer, uint64_t L, uint64_t W,
                             uint64_t nch, uint32_t* __restrict__ sums)
 {
+    pdl_begin();
     const uint64_t total = outer * nch * W;
     for (uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
          gid += (uint64_t)gridDim.x * blockDim.x) {
@@ -875,6 +884,7 @@ __global__ void k_scan_sums(const int32_t* __restrict__ v, uint64_t outer, uint6
 
 __global__ void k_scan_chunks(uint64_t outer, uint64_t W, uint64_t nch, uint32_t* sums)
 {
+    pdl_begin();
     const uint64_t total = outer * W;
     for (uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
          gid += (uint64_t)gridDim.x * blockDim.x) {
@@ -892,6 +902,7 @@ __global__ void k_scan_chunks(uint64_t outer, uint64_t W, uint64_t nch, uint32_t
 __global__ void k_scan_apply(int32_t* v, uint64_t outer, uint64_t L, uint64_t W, uint64_t nch,
                              const uint32_t* __restrict__ sums, float dequant_w_in, const float* wp)
 {
+    pdl_begin();
     const float dequant_w = wp ? *wp : dequant_w_in;
     const uint64_t total = outer * nch * W;
     for (uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
@@ -914,6 +925,7 @@ __global__ void __launch_bounds__(256) k_scan_walk(int32_t* v, uint64_t outer, u
                                                    float dequant_w_in, const int32_t* __restrict__ carry,
                                                    const float* wp)
 {
+    pdl_begin();
     const float dequant_w = wp ? *wp : dequant_w_in;
     const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= outer * W) return;
@@ -952,6 +964,7 @@ __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer,
                                                      uint32_t yrows, uint32_t ys,
                                                      const float* wp)
 {
+    pdl_begin();
     const float dequant_w = wp ? *wp : dequant_w_in;
     using VT = typename std::conditional<V == 4, int4, int2>::type;
     const uint64_t Wv = W / V;
@@ -1013,6 +1026,7 @@ __global__ void __launch_bounds__(256) k_scan_walk_v(int32_t* v, uint64_t outer,
 
 __global__ void k_value_patch(float* out, const uint2* rec, uint64_t cnt, uint64_t n, uint64_t base, int logt)
 {
+    pdl_begin();
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint2 r = rec[k];
@@ -1025,6 +1039,7 @@ __global__ void k_value_patch(float* out, const uint2* rec, uint64_t cnt, uint64
 __global__ void __launch_bounds__(256) k_axis_sum(const int32_t* __restrict__ v, uint64_t L, uint64_t W,
                                                   int32_t* __restrict__ agg)
 {
+    pdl_begin();
     const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= W) return;
     const int32_t* p = v + w;
@@ -1045,6 +1060,7 @@ __global__ void __launch_bounds__(256) k_axis_sum(const int32_t* __restrict__ v,
 // carry[w] = sum over the lower ranks j < nbefore of aggs[j][w] (mod 2^32).
 __global__ void k_slab_carry(const int32_t* __restrict__ aggs, uint32_t nbefore, uint64_t elems, int32_t* carry)
 {
+    pdl_begin();
     for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < elems;
          w += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t acc = 0;
@@ -1056,6 +1072,7 @@ __global__ void k_slab_carry(const int32_t* __restrict__ aggs, uint32_t nbefore,
 // 1-D slab finish: x = fl32(fl32(q + carry) * w).
 __global__ void k_add_dequant(int32_t* q, uint64_t n, const int32_t* carry, float w)
 {
+    pdl_begin();
     const uint32_t c = (uint32_t)carry[0];
     for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (uint64_t)gridDim.x * blockDim.x)
         reinterpret_cast<float*>(q)[g] = __fmul_rn(__int2float_rn((int32_t)((uint32_t)q[g] + c)), w);
@@ -1083,7 +1100,7 @@ cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n,
 {
     if (cnt == 0) return cudaSuccess;
     LaunchProf lp(K_VALIDATE, st);
-    k_validate_outliers<<<grid_for(cnt), 256, 0, st>>>(rec, cnt, n, ctrl);
+    { const cudaError_t e_ = launch_pdl(k_validate_outliers, dim3(grid_for(cnt)), dim3(256), 0, st, rec, cnt, n, ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1138,7 +1155,7 @@ static cudaError_t launch_decode_t(const DecodeArgs& a_in, cudaStream_t st)
     DecodeArgs a = a_in;
     a.dnx = make_fastdiv(a.g.nx);
     if (a.tiles == 0) return cudaSuccess;
-    k_decode_tiles<NDIM><<<a.tiles, kCta, 0, st>>>(a);
+    { const cudaError_t e_ = launch_pdl(k_decode_tiles<NDIM>, dim3(a.tiles), dim3(kCta), 0, st, a); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1150,10 +1167,10 @@ cudaError_t launch_decode_tiles(const DecodeArgs& a_in, cudaStream_t st, bool fu
         a.dnx = make_fastdiv(a.g.nx);
         const uint32_t ctas = a.g.n / a.g.P * a.yseg;
         switch (kTileCodes / a.g.nx) {
-            case 1: k_decode_planes<1><<<ctas, kCta, 0, st>>>(a); break;
-            case 2: k_decode_planes<2><<<ctas, kCta, 0, st>>>(a); break;
-            case 4: k_decode_planes<4><<<ctas, kCta, 0, st>>>(a); break;
-            default: k_decode_planes<8><<<ctas, kCta, 0, st>>>(a); break;
+            case 1: { const cudaError_t e_ = launch_pdl(k_decode_planes<1>, dim3(ctas), dim3(kCta), 0, st, a); if (e_ != cudaSuccess) return e_; } break;
+            case 2: { const cudaError_t e_ = launch_pdl(k_decode_planes<2>, dim3(ctas), dim3(kCta), 0, st, a); if (e_ != cudaSuccess) return e_; } break;
+            case 4: { const cudaError_t e_ = launch_pdl(k_decode_planes<4>, dim3(ctas), dim3(kCta), 0, st, a); if (e_ != cudaSuccess) return e_; } break;
+            default: { const cudaError_t e_ = launch_pdl(k_decode_planes<8>, dim3(ctas), dim3(kCta), 0, st, a); if (e_ != cudaSuccess) return e_; } break;
         }
         return cudaGetLastError();
     }
@@ -1174,11 +1191,11 @@ cudaError_t launch_decode_cl(const DecodeArgs& a_in, uint32_t cz, cudaStream_t s
     if (ctas == 0) return cudaSuccess;
     LaunchProf lp(K_DECODE_PLANES, st);
     switch (kTileCodes / a.g.nx) {
-        case 1: k_decode_cl<1><<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
-        case 2: k_decode_cl<2><<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
-        case 4: k_decode_cl<4><<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
-        case 8: k_decode_cl<8><<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
-        default: k_decode_cl_short<<<(unsigned)ctas, kCta, 0, st>>>(a, cz); break;
+        case 1: { const cudaError_t e_ = launch_pdl(k_decode_cl<1>, dim3((unsigned)ctas), dim3(kCta), 0, st, a, cz); if (e_ != cudaSuccess) return e_; } break;
+        case 2: { const cudaError_t e_ = launch_pdl(k_decode_cl<2>, dim3((unsigned)ctas), dim3(kCta), 0, st, a, cz); if (e_ != cudaSuccess) return e_; } break;
+        case 4: { const cudaError_t e_ = launch_pdl(k_decode_cl<4>, dim3((unsigned)ctas), dim3(kCta), 0, st, a, cz); if (e_ != cudaSuccess) return e_; } break;
+        case 8: { const cudaError_t e_ = launch_pdl(k_decode_cl<8>, dim3((unsigned)ctas), dim3(kCta), 0, st, a, cz); if (e_ != cudaSuccess) return e_; } break;
+        default: { const cudaError_t e_ = launch_pdl(k_decode_cl_short, dim3((unsigned)ctas), dim3(kCta), 0, st, a, cz); if (e_ != cudaSuccess) return e_; } break;
     }
     return cudaGetLastError();
 }
@@ -1189,20 +1206,20 @@ cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool c
     if (carries) {
         {
             LaunchProf lp(K_XCARRY, st);
-            k_xseg_block<<<nb, 1024, 0, st>>>(a.xagg, a.tiles, xloc, xbagg);
+            { const cudaError_t e_ = launch_pdl(k_xseg_block, dim3(nb), dim3(1024), 0, st, a.xagg, a.tiles, xloc, xbagg); if (e_ != cudaSuccess) return e_; }
         }
         {
             LaunchProf lp(K_XCARRY, st);
-            k_xseg_top<<<1, 1024, 0, st>>>(xbagg, nb);
+            { const cudaError_t e_ = launch_pdl(k_xseg_top, dim3(1), dim3(1024), 0, st, xbagg, nb); if (e_ != cudaSuccess) return e_; }
         }
     }
     if (!carries && a.g.ndim != 1) return cudaGetLastError();
     unsigned grid = a.tiles < (uint32_t)num_sms() * 8 ? a.tiles : num_sms() * 8;
     LaunchProf lp(K_XCARRY, st);
     switch (a.g.ndim) {
-        case 1: k_xfix<1><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries, a.wp); break;
-        case 2: k_xfix<2><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries, nullptr); break;
-        default: k_xfix<3><<<grid, kCta, 0, st>>>(a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries, nullptr); break;
+        case 1: { const cudaError_t e_ = launch_pdl(k_xfix<1>, dim3(grid), dim3(kCta), 0, st, a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries, a.wp); if (e_ != cudaSuccess) return e_; } break;
+        case 2: { const cudaError_t e_ = launch_pdl(k_xfix<2>, dim3(grid), dim3(kCta), 0, st, a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries, nullptr); if (e_ != cudaSuccess) return e_; } break;
+        default: { const cudaError_t e_ = launch_pdl(k_xfix<3>, dim3(grid), dim3(kCta), 0, st, a.q_out, xloc, xbagg, a.tiles, a.g.n, a.g.nx, a.w, carries, nullptr); if (e_ != cudaSuccess) return e_; } break;
     }
     return cudaGetLastError();
 }
@@ -1221,12 +1238,12 @@ static void launch_walk(int32_t* data, uint64_t outer, uint64_t L, uint64_t W, f
     const bool a16 = (reinterpret_cast<uintptr_t>(data) & 15) == 0;
     if (m != 3 && W % 4 == 0 && a16 && m != 1) {
         const uint64_t thr = outer * W / 4;
-        k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx, 1u, 1u, wp);
+        { (void)launch_pdl(k_scan_walk_v<4, 8>, dim3((unsigned)((thr + 255) / 256)), dim3(256), 0, st, data, outer, L, W, w, carry, ycarry, ynx, 1u, 1u, wp);  /* errors: cudaGetLastError */ }
     } else if (m != 3 && W % 2 == 0 && a16) {
         const uint64_t thr = outer * W / 2;
-        k_scan_walk_v<2, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, ycarry, ynx, 1u, 1u, wp);
+        { (void)launch_pdl(k_scan_walk_v<2, 8>, dim3((unsigned)((thr + 255) / 256)), dim3(256), 0, st, data, outer, L, W, w, carry, ycarry, ynx, 1u, 1u, wp);  /* errors: cudaGetLastError */ }
     } else {
-        k_scan_walk<<<(unsigned)((outer * W + 255) / 256), 256, 0, st>>>(data, outer, L, W, w, carry, wp);
+        { (void)launch_pdl(k_scan_walk, dim3((unsigned)((outer * W + 255) / 256)), dim3(256), 0, st, data, outer, L, W, w, carry, wp);  /* errors: cudaGetLastError */ }
     }
 }
 
@@ -1242,15 +1259,15 @@ cudaError_t launch_scan_axis(int32_t* data, uint64_t outer, uint64_t L, uint64_t
     const uint64_t work = outer * nch * W;
     {
         LaunchProf lp(K_SCAN_SUMS, st);
-        k_scan_sums<<<grid_for(work), 256, 0, st>>>(data, outer, L, W, nch, sums);
+        { const cudaError_t e_ = launch_pdl(k_scan_sums, dim3(grid_for(work)), dim3(256), 0, st, data, outer, L, W, nch, sums); if (e_ != cudaSuccess) return e_; }
     }
     {
         LaunchProf lp(K_SCAN_CHUNKS, st);
-        k_scan_chunks<<<grid_for(outer * W), 256, 0, st>>>(outer, W, nch, sums);
+        { const cudaError_t e_ = launch_pdl(k_scan_chunks, dim3(grid_for(outer * W)), dim3(256), 0, st, outer, W, nch, sums); if (e_ != cudaSuccess) return e_; }
     }
     {
         LaunchProf lp(K_SCAN_APPLY, st);
-        k_scan_apply<<<grid_for(work), 256, 0, st>>>(data, outer, L, W, nch, sums, dequant_w, wp);
+        { const cudaError_t e_ = launch_pdl(k_scan_apply, dim3(grid_for(work)), dim3(256), 0, st, data, outer, L, W, nch, sums, dequant_w, wp); if (e_ != cudaSuccess) return e_; }
     }
     return cudaGetLastError();
 }
@@ -1260,27 +1277,28 @@ cudaError_t launch_value_patch(float* out, const uint2* vrec, uint64_t cnt, uint
 {
     if (cnt == 0) return cudaSuccess;
     LaunchProf lp(K_VPATCH, st);
-    k_value_patch<<<grid_for(cnt), 256, 0, st>>>(out, vrec, cnt, n, base, logt);
+    { const cudaError_t e_ = launch_pdl(k_value_patch, dim3(grid_for(cnt)), dim3(256), 0, st, out, vrec, cnt, n, base, logt); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
 cudaError_t launch_axis_sum(const int32_t* v, uint64_t L, uint64_t W, int32_t* agg, cudaStream_t st)
 {
     LaunchProf lp(K_SLAB, st);
-    k_axis_sum<<<(unsigned)((W + 255) / 256), 256, 0, st>>>(v, L, W, agg);
+    { const cudaError_t e_ = launch_pdl(k_axis_sum, dim3((unsigned)((W + 255) / 256)), dim3(256), 0, st, v, L, W, agg); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
 cudaError_t launch_slab_carry(const int32_t* aggs, uint32_t nbefore, uint64_t elems, int32_t* carry, cudaStream_t st)
 {
     LaunchProf lp(K_SLAB, st);
-    k_slab_carry<<<grid_for(elems), 256, 0, st>>>(aggs, nbefore, elems, carry);
+    { const cudaError_t e_ = launch_pdl(k_slab_carry, dim3(grid_for(elems)), dim3(256), 0, st, aggs, nbefore, elems, carry); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
 // in place: the segments' column totals -> inclusive prefixes over the segments of a plane
 __global__ void k_yprefix(int32_t* ycarry, uint64_t nz, uint32_t nx, uint32_t ys)
 {
+    pdl_begin();
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nz * nx) return;
     const uint64_t z = i / nx, x = i - z * nx;
@@ -1297,13 +1315,13 @@ cudaError_t launch_zwalk_ycarry(int32_t* data, uint64_t L, uint64_t W, float w, 
 {
     if (ys > 2) {
         LaunchProf lp(K_OFFSETS, st);
-        k_yprefix<<<(unsigned)((L * nx + 255) / 256), 256, 0, st>>>(ycarry, L, nx, ys);
+        { const cudaError_t e_ = launch_pdl(k_yprefix, dim3((unsigned)((L * nx + 255) / 256)), dim3(256), 0, st, ycarry, L, nx, ys); if (e_ != cudaSuccess) return e_; }
     }
     LaunchProf lp(K_SCAN_WALK, st);
     if (W % 4 != 0 || (reinterpret_cast<uintptr_t>(data) & 15) != 0) return cudaErrorInvalidValue;
     const uint64_t thr = W / 4;
-    k_scan_walk_v<4, 8><<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(data, 1, L, W, w, nullptr, ycarry, nx,
-                                                                        (uint32_t)(W / nx / ys), ys, wp);
+    { const cudaError_t e_ = launch_pdl(k_scan_walk_v<4, 8>, dim3((unsigned)((thr + 255) / 256)), dim3(256), 0, st, data, 1, L, W, w, nullptr, ycarry, nx,
+                                                                        (uint32_t)(W / nx / ys), ys, wp); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -1317,7 +1335,7 @@ cudaError_t launch_walk_carry(int32_t* data, uint64_t L, uint64_t W, float w, co
 cudaError_t launch_add_dequant(int32_t* q, uint64_t n, const int32_t* carry, float w, cudaStream_t st)
 {
     LaunchProf lp(K_SLAB, st);
-    k_add_dequant<<<grid_for(n), 256, 0, st>>>(q, n, carry, w);
+    { const cudaError_t e_ = launch_pdl(k_add_dequant, dim3(grid_for(n)), dim3(256), 0, st, q, n, carry, w); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 

@@ -64,6 +64,7 @@ __device__ __forceinline__ void dzg_resolve(DzrArgs& a)
 // ---- k_untile ----
 __global__ void __launch_bounds__(256) k_untile(DzrArgs a, uint64_t n)
 {
+    pdl_begin();
     dzg_resolve(a);
     __shared__ __align__(16) uint8_t Ush[8][32 * 144];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -211,6 +212,7 @@ __device__ __forceinline__ void dzg_load_async(const DzrArgs& a, const DzgCur& q
 template <int NW>
 __global__ void __launch_bounds__(32 * NW, 16 / NW) k_dzg_sum(DzrArgs a)
 {
+    pdl_begin();
     dzg_resolve(a);
     extern __shared__ __align__(16) uint8_t gsm[];
     uint2 (*slots)[kDzgRows * 32 * NW] = reinterpret_cast<uint2 (*)[kDzgRows * 32 * NW]>(gsm);   // codes of plane k, k + 1
@@ -295,6 +297,7 @@ __device__ __forceinline__ void dzg_rows_xscan(uint32_t (&v)[kDzgRows][4], uint3
 template <int NW, bool LOGT>
 __global__ void __launch_bounds__(32 * NW, 16 / NW) k_dzg_main(DzrArgs a)
 {
+    pdl_begin();
     dzg_resolve(a);
     __shared__ uint32_t wts[3][kDzgRows * NW];   // row-scan warp totals (unit start + 2 plane buffers)
     extern __shared__ __align__(16) uint8_t gsm[];
@@ -452,7 +455,7 @@ static cudaError_t dzg_launch(const DzrArgs& a, cudaStream_t st)
         uint64_t grid = (uint64_t)dzg_per_sm<NW>((const void*)kern, sm1) * num_sms();
         if (grid > U) grid = U;
         LaunchProf lp(K_DZR_SUM, st);
-        kern<<<(unsigned)grid, 32 * NW, sm1, st>>>(a);
+        { const cudaError_t e_ = launch_pdl(kern, dim3((unsigned)grid), dim3(32 * NW), sm1, st, a); if (e_ != cudaSuccess) return e_; }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -466,7 +469,7 @@ static cudaError_t dzg_launch(const DzrArgs& a, cudaStream_t st)
     uint64_t grid = (uint64_t)per * num_sms();
     if (grid > U) grid = U;
     LaunchProf lp(K_DZR_MAIN, st);
-    kern<<<(unsigned)grid, 32 * NW, sm2, st>>>(a);
+    { const cudaError_t e_ = launch_pdl(kern, dim3((unsigned)grid), dim3(32 * NW), sm2, st, a); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -476,7 +479,7 @@ cudaError_t launch_decode_dzg(const DzrArgs& a, cudaStream_t st)
     {
         const uint64_t want = ((uint64_t)a.ntiles + 7) / 8, cap = (uint64_t)num_sms() * 8;
         LaunchProf lp(K_DECODE, st);
-        k_untile<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(a, n);
+        { const cudaError_t e_ = launch_pdl(k_untile, dim3((unsigned)(want < cap ? want : cap)), dim3(256), 0, st, a, n); if (e_ != cudaSuccess) return e_; }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -438,6 +438,7 @@ __global__ void k_dzr_prep1(DzrArgs a, uint32_t dblocks)
 // ---- prep 2: G = exclusive over chunks of (CD exclusive over bands): thread = (band, x quad) ----
 __global__ void k_dzr_prep2(DzrArgs a)
 {
+    pdl_begin();
     const uint32_t nq = a.nx / 4;
     const uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gi >= (uint64_t)a.nbands * nq) return;
@@ -616,6 +617,7 @@ template <bool SUM, bool LOGT>
 __global__ void __launch_bounds__(256) k_dec1d(DzrArgs a, uint64_t n, uint32_t* tsum, const uint32_t* loc,
                                                const uint32_t* bpre)
 {
+    pdl_begin();
     dzr_resolve(a);
     extern __shared__ __align__(16) uint8_t dsm1[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -734,6 +736,7 @@ __global__ void __launch_bounds__(256) k_dec1d(DzrArgs a, uint64_t n, uint32_t* 
 __global__ void __launch_bounds__(1024) k_tsum_block(const uint32_t* __restrict__ tsum, uint32_t ntiles, uint32_t* loc,
                                                      uint32_t* bsum)
 {
+    pdl_begin();
     __shared__ uint32_t ws[33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
@@ -764,6 +767,7 @@ __global__ void __launch_bounds__(1024) k_tsum_block(const uint32_t* __restrict_
 
 __global__ void __launch_bounds__(1024) k_tsum_top(uint32_t* bsum, uint32_t nb)
 {
+    pdl_begin();
     __shared__ uint32_t ws[33];
     __shared__ uint32_t carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -808,25 +812,25 @@ cudaError_t launch_decode_1d(const DzrArgs& a, uint64_t n, uint32_t* tsum, uint3
     {
         cudaFuncSetAttribute(k_dec1d<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         LaunchProf lp(K_DZR_SUM, st);
-        k_dec1d<true, false><<<grid, 256, sm, st>>>(a, n, tsum, nullptr, nullptr);
+        { const cudaError_t e_ = launch_pdl(k_dec1d<true, false>, dim3(grid), dim3(256), sm, st, a, n, tsum, nullptr, nullptr); if (e_ != cudaSuccess) return e_; }
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const uint32_t nb = (a.ntiles + 1023) / 1024;
     {
         LaunchProf lp(K_DZR_PREP, st);
-        k_tsum_block<<<nb, 1024, 0, st>>>(tsum, a.ntiles, loc, bsum);
+        { const cudaError_t e_ = launch_pdl(k_tsum_block, dim3(nb), dim3(1024), 0, st, tsum, a.ntiles, loc, bsum); if (e_ != cudaSuccess) return e_; }
     }
     {
         LaunchProf lp(K_DZR_PREP, st);
-        k_tsum_top<<<1, 1024, 0, st>>>(bsum, nb);
+        { const cudaError_t e_ = launch_pdl(k_tsum_top, dim3(1), dim3(1024), 0, st, bsum, nb); if (e_ != cudaSuccess) return e_; }
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     auto kern = a.logt > 0 ? k_dec1d<false, true> : k_dec1d<false, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     LaunchProf lp(K_DZR_MAIN, st);
-    kern<<<grid, 256, sm, st>>>(a, n, nullptr, loc, bsum);
+    { const cudaError_t e_ = launch_pdl(kern, dim3(grid), dim3(256), sm, st, a, n, nullptr, loc, bsum); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 

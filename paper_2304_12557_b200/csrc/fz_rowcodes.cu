@@ -133,6 +133,7 @@ template <int NW>
 __global__ void __launch_bounds__(32 * NW, 12 / NW) k_rowcodes(CompressArgs a, uint32_t nseg, uint32_t ny,
                                                                uint32_t nz)
 {
+    pdl_begin();
     extern __shared__ __align__(128) uint8_t rsm[];
     __shared__ RcShared sh;
     __shared__ __align__(8) uint64_t mbar[2];
@@ -433,6 +434,7 @@ __global__ void __launch_bounds__(32 * NW, 12 / NW) k_rowcodes(CompressArgs a, u
 // per A-row: conflict-free), and lane c reads A-row c back (8 x 16 bytes).
 __global__ void __launch_bounds__(256) k_rowtiles(CompressArgs a, uint32_t ntiles)
 {
+    pdl_begin();
     __shared__ __align__(16) uint8_t Bsh[8][32 * 144];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Ctrl* ctrl = a.ctrl;
@@ -574,7 +576,7 @@ static cudaError_t rc_launch(const CompressArgs& a, uint32_t nseg, uint32_t ny, 
     uint64_t grid = (uint64_t)per_sm * num_sms();
     if (grid > units) grid = units;
     LaunchProf lp(K_COMPRESS, st);
-    kern<<<(unsigned)grid, 32 * NW, sm, st>>>(a, nseg, ny, nz);
+    { const cudaError_t e_ = launch_pdl(kern, dim3((unsigned)grid), dim3(32 * NW), sm, st, a, nseg, ny, nz); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
@@ -598,7 +600,7 @@ cudaError_t launch_compress_rc(const CompressArgs& a, cudaStream_t st)
     const uint64_t want = ((uint64_t)T + 7) / 8;
     const uint64_t cap = (uint64_t)num_sms() * 8;
     LaunchProf lp(K_ROWTILES, st);
-    k_rowtiles<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(a, T);
+    { const cudaError_t e_ = launch_pdl(k_rowtiles, dim3((unsigned)(want < cap ? want : cap)), dim3(256), 0, st, a, T); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
 }
 
