@@ -76,20 +76,22 @@ __global__ void __launch_bounds__(256) k_untile(DzrArgs a, uint64_t n)
         const uint4* fp = reinterpret_cast<const uint4*>(a.flags + 32ull * t);
         const uint4 f0 = __ldg(fp), f1 = __ldg(fp + 1);
         const uint32_t F[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-        const uint64_t base = (uint64_t)__ldg(a.bpre + (t >> 10)) + __ldg(a.loc + t);
-        uint32_t pre = 0;
+        // 32-bit block indices (nnz < 2^29, R16); one corrupt-index check per lane (fz_dzr.cu)
+        const uint32_t nnz = a.nnz_total < 0xFFFFFFFFull ? (uint32_t)a.nnz_total : 0xFFFFFFFFu;
+        uint32_t pre = __ldg(a.bpre + (t >> 10)) + __ldg(a.loc + t);
+        bool bad = false;
+        const uint32_t Bb = smem_u32(B) + 16u * lane;
 #pragma unroll
         for (int f = 0; f < 8; ++f) {
-            const uint64_t bi = base + pre + __popc(F[f] & lt);
-            uint32_t nb = ((F[f] >> lane) & 1u) ? 16u : 0u;
-            if (nb && bi >= a.nnz_total) {
-                atomicCAS(&a.ctrl->err, 0, (int)FZ_ERR_CORRUPT);
-                nb = 0;
-            }
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(B + 16u * (32u * f + lane))),
-                         "l"(nb ? pay + bi : pay), "r"(nb) : "memory");
+            const uint32_t bi = pre + __popc(F[f] & lt);
+            const bool set = (F[f] >> lane) & 1u;
+            const bool ok = bi < nnz;
+            bad |= set && !ok;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(Bb + 512u * f),
+                         "l"(pay + (ok ? bi : 0u)), "r"((set && ok) ? 16u : 0u) : "memory");
             pre += __popc(F[f]);
         }
+        if (bad) atomicCAS(&a.ctrl->err, 0, (int)FZ_ERR_CORRUPT);
         asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();
