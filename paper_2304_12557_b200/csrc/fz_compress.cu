@@ -1726,7 +1726,7 @@ __global__ void __launch_bounds__(kCta, 4) k_compress_zb(CompressArgs a)
 // are loaded while this tile's blocks move.
 // C9 rides along: thread 0 of block 0 writes the totals and the header (k_finalize's work; the
 // scan's nnz and the walker's outlier counts are complete when this kernel starts).
-__global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ loc,
+__global__ void __launch_bounds__(256, 6) k_compact(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ loc,
                                                  const uint32_t* __restrict__ bpre, const uint4* __restrict__ tstage,
                                                  uint8_t* payload_out, uint64_t payload_cap, uint32_t ntiles,
                                                  uint8_t* hdr_out, uint64_t hdr_cap, uint32_t ndim, uint64_t d0,
@@ -1763,25 +1763,29 @@ __global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ fl
         for (int w = 0; w < 8; ++w) I[w] = __shfl_sync(kFull, inc, w);
         const uint32_t total = I[7];
         const uint4* src = tstage + (uint64_t)t * kTileBlocks;
-        constexpr int kMaxR = kTileBlocks / 32;
-        uint4 v[kMaxR];
+        // two rounds of 32 blocks per pass (a c4 tile has ~50 nonzero blocks): both loads in
+        // flight before the stores, few registers (6 CTAs of 256 threads per SM)
+#pragma unroll 1
+        for (uint32_t r0 = 0; r0 < total; r0 += 64) {
+            uint4 v[2];
 #pragma unroll
-        for (int r = 0; r < kMaxR; ++r) {
-            const uint32_t k = (uint32_t)lane + 32u * r;
-            if (32u * r < total && k < total) {
-                uint32_t w = 0, e = 0;
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t k = (uint32_t)lane + r0 + 32u * r;
+                if (k < total) {
+                    uint32_t w = 0, e = 0;
 #pragma unroll
-                for (int i = 0; i < 7; ++i)
-                    if (I[i] <= k) { w = i + 1; e = I[i]; }
-                v[r] = __ldcs(src + 32 * w + (k - e));
+                    for (int i = 0; i < 7; ++i)
+                        if (I[i] <= k) { w = i + 1; e = I[i]; }
+                    v[r] = __ldcs(src + 32 * w + (k - e));
+                }
             }
-        }
 #pragma unroll
-        for (int r = 0; r < kMaxR; ++r) {
-            const uint32_t k = (uint32_t)lane + 32u * r;
-            if (32u * r < total && k < total) {
-                const uint64_t bo = 16 * (off + k);
-                if (bo + 16 <= payload_cap) __stcs(reinterpret_cast<uint4*>(payload_out + bo), v[r]);
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t k = (uint32_t)lane + r0 + 32u * r;
+                if (k < total) {
+                    const uint64_t bo = 16 * (off + k);
+                    if (bo + 16 <= payload_cap) __stcs(reinterpret_cast<uint4*>(payload_out + bo), v[r]);
+                }
             }
         }
         if (tn >= ntiles) break;
