@@ -76,6 +76,12 @@ __global__ void __launch_bounds__(256) k_untile(DzrArgs a, uint64_t n)
         const uint4* fp = reinterpret_cast<const uint4*>(a.flags + 32ull * t);
         const uint4 f0 = __ldg(fp), f1 = __ldg(fp + 1);
         const uint32_t F[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+        if (((f0.x | f0.y | f0.z | f0.w) | (f1.x | f1.y | f1.z | f1.w)) == 0u) {
+            // all 256 blocks zero: the tile's codes are 0 -- no gather, no transpose
+#pragma unroll
+            for (int j = 0; j < 8; ++j) *reinterpret_cast<uint4*>(B + 144u * lane + 16u * j) = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+        } else {
         // 32-bit block indices (nnz < 2^29, R16); one corrupt-index check per lane (fz_dzr.cu)
         const uint32_t nnz = a.nnz_total < 0xFFFFFFFFull ? (uint32_t)a.nnz_total : 0xFFFFFFFFu;
         uint32_t pre = __ldg(a.bpre + (t >> 10)) + __ldg(a.loc + t);
@@ -109,6 +115,7 @@ __global__ void __launch_bounds__(256) k_untile(DzrArgs a, uint64_t n)
         for (int j = 0; j < 8; ++j)
             *reinterpret_cast<uint4*>(B + 144u * lane + 16u * j) = make_uint4(A[4 * j], A[4 * j + 1], A[4 * j + 2], A[4 * j + 3]);
         __syncwarp();
+        }
         // delta-outliers of the tile (rare): code 0 -> 0x8000, the escape the walk resolves
         if (a.nd > 0) {
             const uint32_t nd32 = (uint32_t)a.nd;
@@ -240,6 +247,13 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) k_dzg_sum(DzrArgs a)
         const uint2* sl = slots[k % 3] + tid;
         const uint64_t g0 = (uint64_t)cur.z * a.P + (uint64_t)(cur.b * kDzgRows) * nx + x0;
         uint32_t cs[4] = {0u, 0u, 0u, 0u};
+        uint32_t orv = 0;   // all-zero codes (the warp's 16 rows): nothing to add
+#pragma unroll
+        for (int i = 0; i < kDzgRows; ++i) {
+            const uint2 cv = sl[i * blockDim.x];
+            orv |= cv.x | cv.y;
+        }
+        if (__any_sync(kFull, orv != 0u))
 #pragma unroll
         for (int i = 0; i < kDzgRows; ++i) {
             int32_t d[4];
@@ -372,6 +386,20 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) k_dzg_main(DzrArgs a)
         const uint64_t g0 = (uint64_t)z * PL + (uint64_t)(b * kDzgRows) * nx + x0;
         uint32_t* wt = wts[k & 1];
         uint4* xs = xsl + tid;
+        // a warp whose 16 rows x 128 columns of codes are all zero (RTM's exact-zero regions,
+        // P:372) has X = 0: no unpack, no scans, zero warp totals
+        uint32_t orv = 0;
+#pragma unroll
+        for (int i = 0; i < kDzgRows; ++i) {
+            const uint2 cv = sl[i * blockDim.x];
+            orv |= cv.x | cv.y;
+        }
+        const bool zw = !__any_sync(kFull, orv != 0u);
+        if (zw) {
+            if (lane == 31)
+#pragma unroll
+                for (int i = 0; i < kDzgRows; ++i) wt[i * NW + warp] = 0u;
+        } else
 #pragma unroll
         for (int i = 0; i < kDzgRows; ++i) {
             int32_t d[4];
@@ -404,7 +432,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) k_dzg_main(DzrArgs a)
 #pragma unroll
             for (int ww = 0; ww < NW; ++ww)
                 if (ww < warp) pre += wt[i * NW + ww];
-            const uint4 xv = xs[i * blockDim.x];
+            const uint4 xv = zw ? make_uint4(0u, 0u, 0u, 0u) : xs[i * blockDim.x];
             cy[0] += xv.x + pre; cy[1] += xv.y + pre; cy[2] += xv.z + pre; cy[3] += xv.w + pre;
             const uint32_t q0 = qp[0] + cy[0], q1 = qp[1] + cy[1], q2 = qp[2] + cy[2], q3 = qp[3] + cy[3];
             tmem_st4(taddr + 4u * i, q0, q1, q2, q3);
