@@ -463,8 +463,25 @@ __global__ void __launch_bounds__(256) k_rowtiles(CompressArgs a, uint32_t ntile
             mv = *reinterpret_cast<const uint2*>(a.rc_vmask + (g0 >> 5));
             md = *reinterpret_cast<const uint2*>(a.rc_dmask + (g0 >> 5));
         }
+        const bool whole = (uint64_t)t * kTileCodes + kTileCodes <= n;
+        // a tile of zero codes (RTM's exact-zero regions) has zero flags and no blocks:
+        // no staging, no transpose (its outlier marks below still count: a delta outlier's code is 0)
+        bool zt = false;
+        if (whole && a.codes_out == nullptr) {
+            uint32_t o = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o |= nxt[j].x | nxt[j].y | nxt[j].z | nxt[j].w;
+            zt = !__any_sync(kFull, o != 0u);
+        }
+        if (zt) {
+            load_tile(t + stride);
+            if (lane < 8) {
+                const uint64_t fo = (uint64_t)t * 32 + 4 * lane;
+                if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = 0u;
+            }
+        } else {
         uint32_t A[32];
-        if ((uint64_t)t * kTileCodes + kTileCodes <= n) {
+        if (whole) {
             // 16-byte chunk L + 32 j of the tile = A-row (L + 32 j) / 8, part (L + 32 j) % 8
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -513,6 +530,7 @@ __global__ void __launch_bounds__(256) k_rowtiles(CompressArgs a, uint32_t ntile
             if (fo + 4 <= a.flags_cap) *reinterpret_cast<uint32_t*>(a.flags_out + fo) = myF;
         }
         __syncwarp();   // the blocks are read: the next tile's codes may overwrite the buffer
+        }
         // outliers of this tile: the mask bits of A-row c are words (g0 >> 5) and +1
         const uint64_t vm = (uint64_t)mv.x | (uint64_t)mv.y << 32, dm = (uint64_t)md.x | (uint64_t)md.y << 32;
         if (__any_sync(kFull, (vm | dm) != 0)) {
