@@ -287,8 +287,10 @@ fz_status fz_debug_decode_q(const void* d_in, size_t in_size, int32_t* d_q, uint
  * with one / two CTAs per plane; 2097152: k_range launched before the row walker instead of
  * the walker's fused range phase (SV 8.f2); 4194304: the fused range phase reads its chunks in
  * address order; 33554432: 16-plane units in the row-walking decoder instead of the balanced
- * depth; 8388608: per-CTA residency trace of the row walker (fz_debug_zr_trace).  Streams are
- * byte-identical under every variant. */
+ * depth; 8388608: per-CTA residency trace of the row walker (fz_debug_zr_trace); 67108864:
+ * kernels launched without programmatic dependent launch; 268435456: the general row-walking
+ * decoder only for nz >= 256 (the tile decoder below; set before sizing the decompress
+ * workspace).  Streams are byte-identical under every variant. */
 void fz_debug_set_variant(int bits);
 
 /* Row-walker residency trace (variant 8388608): copies up to n (<= 8192) u64 to host_out,

@@ -32,9 +32,13 @@ bool decode_uses_dzg(const fz_shape& s)
 {
     if (s.ndim != 3 || decode_uses_dzr(s)) return false;
     const uint64_t nz = s.dims[0], ny = s.dims[1], nx = s.dims[2];
-    if (nx % 4 != 0 || nx < 64 || nx > 512 || ny < 1 || nz < 256) return false;
+    // nz >= 64: c3 (nz = 100) decodes 8 % faster than with the tile decoder + y / z walks
+    // (variant 268435456 restores the round-2 threshold of 256 for A/B)
+    if (nx % 4 != 0 || nx < 64 || nx > 512 || ny < 1 || nz < ((variant_bits() & 268435456) ? 256u : 64u)) return false;
     return nz * ny * nx < (1ull << 32);
 }
+
+static uint32_t dzg_grid_main(uint32_t nx);
 
 DzrLayout dzg_layout(const fz_shape& s)
 {
@@ -42,11 +46,12 @@ DzrLayout dzg_layout(const fz_shape& s)
     if (!decode_uses_dzg(s)) return L;
     const uint64_t nz = s.dims[0], ny = s.dims[1], nx = s.dims[2];
     L.nbands = (uint32_t)((ny + kDzgRows - 1) / kDzgRows);
-    L.cz = 16;
+    L.cz = dz_chunk_depth(nz, L.nbands, dzg_grid_main((uint32_t)nx));   // balanced units (fz_dzr.cu)
     L.nchunks = (uint32_t)((nz + L.cz - 1) / L.cz);
+    const uint64_t nch16 = (nz + 15) / 16, nch_ws = L.nchunks > nch16 ? L.nchunks : nch16;
     L.cdelta_elems = (uint64_t)L.nbands * nz * nx;
-    L.dsum_elems = (uint64_t)L.nbands * L.nchunks * kDzgRows * nx;
-    L.cd_elems = (uint64_t)L.nbands * L.nchunks * nx;
+    L.dsum_elems = (uint64_t)L.nbands * nch_ws * kDzgRows * nx;
+    L.cd_elems = (uint64_t)L.nbands * nch_ws * nx;
     const uint64_t T = (nz * ny * nx + kTileCodes - 1) / kTileCodes;
     L.code_bytes = 2 * kTileCodes * T;
     return L;
@@ -501,6 +506,31 @@ static cudaError_t dzg_launch(const DzrArgs& a, cudaStream_t st)
     LaunchProf lp(K_DZR_MAIN, st);
     { const cudaError_t e_ = launch_pdl(kern, dim3((unsigned)grid), dim3(32 * NW), sm2, st, a); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
+}
+
+template <int NW>
+static uint32_t dzg_grid_nw()
+{
+    int per = dzg_per_sm<NW>((const void*)k_dzg_main<NW, false>, 3 * 8 * kDzgRows * 32 * NW + 16 * kDzgRows * 32 * NW);
+    const int tmem_cap = 512 / (NW > 4 ? 256 : 128);
+    if (per > tmem_cap) per = tmem_cap;
+    return (uint32_t)per * (uint32_t)num_sms();
+}
+
+static uint32_t dzg_grid_main(uint32_t nx)
+{
+    static uint32_t cache[4] = {0, 0, 0, 0};
+    const uint32_t nw = (nx + 127) / 128;
+    if (nw < 1 || nw > 4) return 0;
+    if (cache[nw - 1] == 0) {
+        switch (nw) {
+            case 1: cache[0] = dzg_grid_nw<1>(); break;
+            case 2: cache[1] = dzg_grid_nw<2>(); break;
+            case 3: cache[2] = dzg_grid_nw<3>(); break;
+            default: cache[3] = dzg_grid_nw<4>(); break;
+        }
+    }
+    return cache[nw - 1];
 }
 
 cudaError_t launch_decode_dzg(const DzrArgs& a, cudaStream_t st)

@@ -62,11 +62,9 @@ static uint32_t dzr_grid_main(uint32_t nx);
 // depth is picked per shape to minimize ceil(U / G) (cz + 2) (2 plane-equivalents for a
 // unit start: carry rebuild, first gather), cz in [8, 48]; c4 -> cz = 19, 2 units per CTA.
 // Variant 33554432 keeps cz = 16 (A/B).
-static uint32_t dzr_chunk_depth(uint64_t nz, uint32_t nbands, uint32_t nx)
+uint32_t dz_chunk_depth(uint64_t nz, uint32_t nbands, uint64_t G)
 {
-    if (variant_bits() & 33554432) return (uint32_t)kDzrChunk;
-    const uint64_t G = dzr_grid_main(nx);
-    if (G == 0) return (uint32_t)kDzrChunk;   // no device (CPU-only process)
+    if ((variant_bits() & 33554432) || G == 0) return (uint32_t)kDzrChunk;   // A/B; no device
     uint32_t best = kDzrChunk;
     uint64_t bcost = ~0ull;
     for (uint32_t cz = 8; cz <= 48; ++cz) {
@@ -83,7 +81,7 @@ DzrLayout dzr_layout(const fz_shape& s)
     if (!decode_uses_dzr(s)) return L;
     const uint64_t nz = s.dims[0], ny = s.dims[1], nx = s.dims[2];
     L.nbands = (uint32_t)(ny / kDzrRows);
-    L.cz = dzr_chunk_depth(nz, L.nbands, (uint32_t)nx);
+    L.cz = dz_chunk_depth(nz, L.nbands, dzr_grid_main((uint32_t)nx));
     L.nchunks = (uint32_t)((nz + L.cz - 1) / L.cz);
     // carry arrays sized for the larger of this depth and the A/B depth 16 (the workspace must
     // not depend on the variant bits)

@@ -150,6 +150,8 @@ struct DzrLayout {
 };
 bool decode_uses_dzr(const fz_shape& s);
 DzrLayout dzr_layout(const fz_shape& s);
+// planes per unit of the row-walking decoders' persistent grids of G CTAs (fz_dzr.cu)
+uint32_t dz_chunk_depth(uint64_t nz, uint32_t nbands, uint64_t G);
 cudaError_t launch_decode_dzr(const DzrArgs& a, cudaStream_t st);
 cudaError_t launch_dzr_prep(const DzrArgs& a, cudaStream_t st);
 // 1-D fields: tile sums, their scan, then the decode with the carries (fz_dzr.cu)
