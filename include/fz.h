@@ -119,12 +119,16 @@ fz_status fz_derive_params(float mn, float mx, int eb_mode, double eb, fz_params
 
 /* ---------------------------------------------------------------------------------------
  * Compression: range -> prequantize -> Lorenzo -> codes -> bitshuffle -> block
- * flags -> exclusive scan -> compaction, fused in one persistent kernel after the range
- * pass.  Blocks once on `stream` to return *out_size (host).
+ * flags -> exclusive scan -> compaction.  3-D fields whose 16-row bands are whole tiles (c4):
+ * one persistent kernel takes the range (its first phase) through the flags and staged blocks,
+ * then one popcount-scan launch and one compaction launch (+ header); other shapes: a range
+ * launch, then a row-codes walk + tiling pass or a single-pass kernel with a decoupled
+ * look-back.  Blocks once on `stream` to return *out_size (host).
  *   d_field   : N fp32, device, row-major
  *   d_out     : device, out_cap bytes; receives header || flags || payload || outliers
  *   d_work    : device workspace of fz_workspace_bytes(s) bytes
- *   *h_first_bad (optional, may be NULL): first non-finite index on FZ_ERR_NONFINITE
+ * A NaN / Inf anywhere in the field returns FZ_ERR_NONFINITE (fz_slab_range reports the
+ * first such index).
  * ------------------------------------------------------------------------------------- */
 fz_status fz_compress(const float* d_field, const fz_shape* s, int eb_mode, double eb,
                       void* d_out, size_t out_cap, size_t* h_out_size,
