@@ -586,7 +586,8 @@ def test_row_walking_decoder_outliers_and_old_path_equal():
     assert np.array_equal(a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32))
 
 
-# General row-walking decoder (fz_dzg.cu): 3-D, nx % 4 == 0, 64 <= nx <= 1024, nz >= 256,
+# General row-walking decoder (fz_dzg.cu): 3-D, nx % 4 == 0, 64 <= nx <= 512, nz >= 256 (or >= 64
+# with N >= 2^22),
 # rows that do not tile (partial bands, planes not whole tiles) -- un-shuffled code field, then
 # the carries' two passes.
 DZG = [
@@ -594,6 +595,10 @@ DZG = [
     ("nx500_band9", lambda: synth.generate("hurr_u", (260, 9, 500))),
     ("nx352", lambda: synth.generate("rtm", (256, 33, 352))),
     ("nx1000", lambda: synth.generate("nyx_v", (257, 17, 1000))),
+    # nz in [64, 256) with N >= 2^22 (c3-like), and a mostly-zero field (QSNOW: exact zeros,
+    # the zero-tile / zero-warp fast paths next to dense warps)
+    ("nz72_mid", lambda: synth.generate("hurr_u", (72, 120, 500))),
+    ("qsnow_zero_paths", lambda: synth.generate("hurr_qsnow", (72, 120, 500))),
 ]
 
 
