@@ -60,7 +60,8 @@ static uint32_t dzr_grid_main(uint32_t nx);
 // persistent grid of G CTAs, so a pass lasts ceil(U / G) units: with 16-plane chunks c4
 // (32 bands x 32 chunks = 1024 units on 444 CTAs) ran 3 units where the mean is 2.3.  The
 // depth is picked per shape to minimize ceil(U / G) (cz + 2) (2 plane-equivalents for a
-// unit start: carry rebuild, first gather), cz in [8, 48]; c4 -> cz = 19, 2 units per CTA.
+// unit start: carry rebuild, first gather), cz in [8, 48]; c4 -> cz = 40 (ties with 19; the
+// deeper chunk measured faster: fewer chunk sums for the prep).
 // Variant 33554432 keeps cz = 16 (A/B).
 uint32_t dz_chunk_depth(uint64_t nz, uint32_t nbands, uint64_t G)
 {
