@@ -284,7 +284,8 @@ __device__ __forceinline__ void zr_tpass(uint8_t* stg, uint8_t* msk, uint32_t RP
 // grid-wide wait, then the walk with the parameters every CTA derives from the result.
 // The unit of work is half a step's own rows (8 rows of a band in one plane: contiguous,
 // 32 nx bytes), copied by 1-D TMA into kZrRStages buffers carved from the walk's stages.
-// Chunks are CLAIMED from a global counter (batches of kZrRClaim) instead of being assigned
+// Chunks are CLAIMED from a global counter (batches of kZrRClaim = 2: 8 left a longer tail at
+// the wait, 1 cost more atomic round trips) instead of being assigned
 // by blockIdx, so the wait cannot deadlock when fewer CTAs are resident than launched
 // (another stream's kernels on the SMs): every claimed chunk is held by a running CTA.
 // Claim order j -> chunk: position-major from the END of the compression runs (half-step
@@ -294,7 +295,7 @@ constexpr int kZrRStages = 4;
 
 // debug trace (variant 8388608): per CTA (start, smid, range-phase end, end) in globaltimer ns
 __device__ unsigned long long g_zr_trace[4 * 2048];
-constexpr uint32_t kZrRClaim = 8;
+constexpr uint32_t kZrRClaim = 2;
 
 __device__ __noinline__ void zr_range_phase(const float* field, Ctrl* ctrl, uint8_t* zsm, uint64_t* mbar,
                                             int* ids, uint32_t nx, uint32_t PL, uint32_t nzr, uint32_t zbeg,

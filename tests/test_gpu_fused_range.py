@@ -30,6 +30,10 @@ ZR_SHAPES = [
     ("sines3d", (20, 16, 512), 1e-4),
     ("rtm", (12, 16, 1024), 1e-3),
     ("nyx_v", (300, 64, 128), 1e-3),
+    # shapes on the warp-specialized single-pass kernel (2-D, short 3-D): k_range either way
+    ("cesm_t", (200, 400), 1e-3),
+    ("hurr_u", (12, 50, 52), 1e-3),
+    ("cesm_cld", (181, 359), 1e-4),
 ]
 
 
@@ -79,9 +83,10 @@ def test_fused_range_launches_one_kernel_fewer():
     assert n_fused == n_sep - 1
 
 
+@pytest.mark.parametrize("shape", [(40, 32, 256), (60, 333)])
 @pytest.mark.parametrize("where", ["first", "last", "middle", "two", "inf_neg"])
-def test_fused_range_nonfinite(where):
-    d = synth.generate("nyx_v", (40, 32, 256)).copy()
+def test_fused_range_nonfinite(where, shape):
+    d = synth.generate("nyx_v" if len(shape) == 3 else "cesm_t", shape).copy()
     flat = d.reshape(-1)
     n = flat.size
     if where == "first":
@@ -93,7 +98,7 @@ def test_fused_range_nonfinite(where):
     elif where == "two":
         flat[[n - 5, 1000]] = [np.nan, np.inf]
     else:
-        flat[12345] = -np.inf
+        flat[12345 % n] = -np.inf
     st, _ = O.compress(d, O.REL, 1e-3)
     assert st == O.ERR_NONFINITE
     codec = fz.Codec(d.shape, DEV)
@@ -101,7 +106,7 @@ def test_fused_range_nonfinite(where):
         codec.compress(torch.from_numpy(d).to(DEV), fz.REL, 1e-3)
     assert e.value.status == fz.ERR_NONFINITE
     # the same codec compresses a finite field afterwards (the claim counters are per call)
-    g = synth.generate("nyx_v", (40, 32, 256))
+    g = synth.generate("nyx_v" if len(shape) == 3 else "cesm_t", shape)
     st, ref = O.compress(g, O.REL, 1e-3)
     buf, size = codec.compress(torch.from_numpy(g).to(DEV), fz.REL, 1e-3)
     assert size == ref.size and np.array_equal(buf.cpu().numpy(), ref)
