@@ -347,28 +347,41 @@ __global__ void __launch_bounds__(1024) k_nnz_block(const uint32_t* __restrict__
 
 // x carries: segmented exclusive scan of the per-tile x aggregates (only when some tile
 // starts inside a row).
-__global__ void __launch_bounds__(1024) k_xseg_block(const uint2* xagg, uint32_t ntiles, uint2* xloc, uint2* xbagg)
+// One launch: the last block to finish (ticket in ctrl->scan_done, zero after the popcount scan
+// and reset here) scans the block aggregates in place (k_xseg_top's work).
+__device__ void xseg_top_block(uint2* xbagg, uint32_t nb, uint32_t* wf, uint32_t* wv);
+
+__global__ void __launch_bounds__(1024) k_xseg_block(const uint2* xagg, uint32_t ntiles, uint2* xloc, uint2* xbagg,
+                                                     Ctrl* ctrl)
 {
     pdl_begin();
     __shared__ uint32_t wf[33], wv[33];
+    __shared__ bool last;
     const uint32_t t = blockIdx.x * 1024 + threadIdx.x;
     const uint2 g = t < ntiles ? xagg[t] : make_uint2(0, 0);
     Seg total;
     const Seg ex = block_excl_seg(Seg{g.x, g.y}, total, wf, wv);
     if (t < ntiles) xloc[t] = make_uint2(ex.f, ex.v);
-    if (threadIdx.x == 0) xbagg[blockIdx.x] = make_uint2(total.f, total.v);
+    if (threadIdx.x == 0) {
+        xbagg[blockIdx.x] = make_uint2(total.f, total.v);
+        __threadfence();
+        last = atomicAdd(&ctrl->scan_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    xseg_top_block(xbagg, gridDim.x, wf, wv);
+    if (threadIdx.x == 0) ctrl->scan_done = 0;
 }
 
-__global__ void __launch_bounds__(1024) k_xseg_top(uint2* xbagg, uint32_t nb)
+__device__ void xseg_top_block(uint2* xbagg, uint32_t nb, uint32_t* wf, uint32_t* wv)
 {
-    pdl_begin();
-    __shared__ uint32_t wf[33], wv[33];
     __shared__ uint32_t cf, cv;
     if (threadIdx.x == 0) { cf = 0; cv = 0; }
     __syncthreads();
     for (uint32_t base = 0; base < nb; base += 1024) {
         const uint32_t i = base + threadIdx.x;
-        const uint2 g = i < nb ? xbagg[i] : make_uint2(0, 0);
+        const uint2 g = i < nb ? __ldcg(xbagg + i) : make_uint2(0, 0);
         Seg total;
         const Seg ex = block_excl_seg(Seg{g.x, g.y}, total, wf, wv);
         const Seg c{cf, cv};
@@ -1206,11 +1219,7 @@ cudaError_t launch_xcarry(const DecodeArgs& a, uint2* xloc, uint2* xbagg, bool c
     if (carries) {
         {
             LaunchProf lp(K_XCARRY, st);
-            { const cudaError_t e_ = launch_pdl(k_xseg_block, dim3(nb), dim3(1024), 0, st, a.xagg, a.tiles, xloc, xbagg); if (e_ != cudaSuccess) return e_; }
-        }
-        {
-            LaunchProf lp(K_XCARRY, st);
-            { const cudaError_t e_ = launch_pdl(k_xseg_top, dim3(1), dim3(1024), 0, st, xbagg, nb); if (e_ != cudaSuccess) return e_; }
+            { const cudaError_t e_ = launch_pdl(k_xseg_block, dim3(nb), dim3(1024), 0, st, a.xagg, a.tiles, xloc, xbagg, a.ctrl); if (e_ != cudaSuccess) return e_; }
         }
     }
     if (!carries && a.g.ndim != 1) return cudaGetLastError();
