@@ -685,8 +685,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         FZ_CUDA(launch_decode_1d(z, n, tsum, tsum + T, reinterpret_cast<uint32_t*>(xbagg), st));
         if (deq) {
             if (dev) {
-                FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
-                FZ_CUDA(launch_exp_inv(d_field, n, ctrl, st));
+                FZ_CUDA(launch_patch_exp_dev(d_field, in + pbase, ctrl, n, st));
             } else {
                 FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
                 if (I.flags & 8u) FZ_CUDA(launch_exp_inv(d_field, n, nullptr, st));
@@ -738,8 +737,7 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
         FZ_CUDA(dzr ? launch_decode_dzr(z, st) : launch_decode_dzg(z, st));
         if (deq) {
             if (dev) {
-                FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
-                FZ_CUDA(launch_exp_inv(d_field, n, ctrl, st));
+                FZ_CUDA(launch_patch_exp_dev(d_field, in + pbase, ctrl, n, st));
             } else {
                 FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st, 0, z.logt));
             }
@@ -774,10 +772,12 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
             FZ_CUDA(launch_scan_axis(q, 1, I.shape.dims[0], I.shape.dims[1] * I.shape.dims[2], sums, wq, st, wp));
     }
     if (deq) {
-        if (dev) FZ_CUDA(launch_value_patch_dev(d_field, in + pbase, ctrl, n, st));
-        else FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
-        if (dev) FZ_CUDA(launch_exp_inv(d_field, n, ctrl, st));
-        else if (I.flags & 8u) FZ_CUDA(launch_exp_inv(d_field, n, nullptr, st));
+        if (dev) {
+            FZ_CUDA(launch_patch_exp_dev(d_field, in + pbase, ctrl, n, st));
+        } else {
+            FZ_CUDA(launch_value_patch(d_field, vrec, I.counts.n_value, n, st));
+            if (I.flags & 8u) FZ_CUDA(launch_exp_inv(d_field, n, nullptr, st));
+        }
     }
     if (async) return FZ_OK;     // status later: fz_decompress_result
     Ctrl h;

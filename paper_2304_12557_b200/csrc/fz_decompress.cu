@@ -176,21 +176,6 @@ __global__ void k_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, u
     }
 }
 
-// logt (the row-walking decoders apply f3's exp in their dequantization): a value outlier of
-// a log-transformed stream holds y's bits, so its x^ is exp32 of them; -1: from the device-
-// parsed header flags (bit 3)
-__global__ void k_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, int logt)
-{
-    pdl_begin();
-    const uint64_t cnt = ctrl->dec_nv;
-    const bool lt = logt < 0 ? (ctrl->dec_flags & 8u) != 0 : logt != 0;
-    const uint2* rec = reinterpret_cast<const uint2*>(payload + 16 * ctrl->dec_nnz + 8 * ctrl->dec_nd);
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint2 r = rec[k];
-        if (r.x < n) out[r.x] = lt ? exp32(__uint_as_float(r.y)) : __uint_as_float(r.y);
-    }
-}
 
 __global__ void k_record_tiles(const uint2* __restrict__ rec, uint64_t nd, uint32_t ntiles, uint64_t gbase,
                                uint32_t* __restrict__ drange, const uint8_t* payload = nullptr,
@@ -1134,14 +1119,6 @@ cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, 
     LaunchProf lp(K_VALIDATE, st);
     const unsigned g = grid_for((uint64_t)ntiles + 1), grid = g > (unsigned)num_sms() ? g : (unsigned)num_sms();
     return launch_pdl(k_validate_dev, dim3(grid), dim3(256), 0, st, payload, n, ctrl, ntiles, drange);
-}
-
-cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st,
-                                  int logt)
-{
-    LaunchProf lp(K_VPATCH, st);
-    { const cudaError_t e_ = launch_pdl(k_value_patch_dev, dim3(num_sms()), dim3(256), 0, st, out, payload, ctrl, n, logt); if (e_ != cudaSuccess) return e_; }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,

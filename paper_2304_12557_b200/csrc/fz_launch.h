@@ -120,6 +120,8 @@ bool decode_fuses_y(const fz_shape& s);
 // status into ctrl), and x^ = exp32(y^) in place (dev_ctrl: only when its dec_flags bit 3)
 cudaError_t launch_log_fwd(const float* x, float* y, uint64_t n, Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_exp_inv(float* v, uint64_t n, const Ctrl* dev_ctrl, cudaStream_t st);
+// device-parsed decode: value patch + (header bit 3) exp32 in one launch (fz_logt.cu)
+cudaError_t launch_patch_exp_dev(float* v, const uint8_t* payload, Ctrl* ctrl, uint64_t n, cudaStream_t st);
 
 // Row-walking decoder (fz_dzr.cu): 3-D, nx % 128 == 0, nx <= 1024, ny % 16 == 0.
 struct DzrArgs {
@@ -182,10 +184,6 @@ cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, c
 // validation of both outlier lists + the per-tile delta-record ranges, one launch (device-parsed)
 cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
                                 cudaStream_t st);
-// logt: 1 / 0 (host-known f3 flag), -1 (device-parsed: the header's flag bit 3); value outliers
-// of a log-transformed stream become exp32 of their bits (the row-walking decoders fuse f3's exp)
-cudaError_t launch_value_patch_dev(float* out, const uint8_t* payload, const Ctrl* ctrl, uint64_t n, cudaStream_t st,
-                                  int logt = 0);
 cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,
                                 cudaStream_t st);
 cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st, bool fuse_y = false);

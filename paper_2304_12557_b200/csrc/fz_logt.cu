@@ -70,6 +70,53 @@ __global__ void __launch_bounds__(256) k_exp_inv(float* __restrict__ v, uint64_t
     for (uint64_t i = 4 * n4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) v[i] = exp32(v[i]);
 }
 
+// Device-parsed decode (fz_decompress_async): the value patch (R20) and, when the header has
+// bit 3 (f3), x^ = exp32(y^) in one launch.  Without the flag every block patches its share of
+// the value outliers (raw bits).  With it every block takes its share of the exp pass and the
+// last block to finish (ticket in ctrl->scan_done, zero after the popcount scan, reset here)
+// writes the value outliers as exp32 of their y bits -- the order of the separate patch + exp
+// launches.
+__global__ void __launch_bounds__(256) k_patch_exp_dev(float* __restrict__ v, const uint8_t* payload, Ctrl* ctrl,
+                                                       uint64_t n)
+{
+    pdl_begin();
+    __shared__ bool last;
+    const bool do_exp = (ctrl->dec_flags & 8u) && ctrl->err == 0;
+    const uint64_t cnt = ctrl->dec_nv;
+    const uint2* rec = reinterpret_cast<const uint2*>(payload + 16 * ctrl->dec_nnz + 8 * ctrl->dec_nd);
+    const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+    if (!do_exp) {
+        for (uint64_t k = i0; k < cnt; k += stride) {
+            const uint2 r = rec[k];
+            if (r.x < n) v[r.x] = __uint_as_float(r.y);
+        }
+        return;
+    }
+    const uint64_t n4 = n / 4;
+    for (uint64_t i = i0; i < n4; i += stride) {
+        float4 a = reinterpret_cast<float4*>(v)[i];
+        a.x = exp32(a.x);
+        a.y = exp32(a.y);
+        a.z = exp32(a.z);
+        a.w = exp32(a.w);
+        __stcs(reinterpret_cast<float4*>(v) + i, a);
+    }
+    for (uint64_t i = 4 * n4 + i0; i < n; i += stride) v[i] = exp32(v[i]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&ctrl->scan_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (uint64_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+        const uint2 r = rec[k];
+        if (r.x < n) v[r.x] = exp32(__uint_as_float(r.y));
+    }
+    if (threadIdx.x == 0) ctrl->scan_done = 0;
+}
+
 static unsigned stream_grid(uint64_t n)
 {
     const uint64_t want = (n / 4 + 255) / 256;
@@ -95,6 +142,12 @@ cudaError_t launch_exp_inv(float* v, uint64_t n, const Ctrl* dev_ctrl, cudaStrea
     LaunchProf lp(K_LOGT, st);
     { const cudaError_t e_ = launch_pdl(k_exp_inv, dim3(stream_grid(n)), dim3(256), 0, st, v, n, dev_ctrl); if (e_ != cudaSuccess) return e_; }
     return cudaGetLastError();
+}
+
+cudaError_t launch_patch_exp_dev(float* v, const uint8_t* payload, Ctrl* ctrl, uint64_t n, cudaStream_t st)
+{
+    LaunchProf lp(K_VPATCH, st);
+    return launch_pdl(k_patch_exp_dev, dim3(stream_grid(n)), dim3(256), 0, st, v, payload, ctrl, n);
 }
 
 }  // namespace fz
