@@ -610,8 +610,10 @@ fz_status decompress_impl(const void* d_in, size_t in_size, float* d_field, int3
     const float* wp = (dev && deq) ? &ctrl->dec_w : nullptr;   // device bin width (dev mode)
     if (dev) {
         FZ_CUDA(launch_decode_hdr(ctrl, in, in_size, I.shape, n, T, st));
-        FZ_CUDA(launch_validate_dev(in + pbase, n, ctrl, (uint32_t)T, drange, st));
-        FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st, ~0ull));
+        // the popcount scan's launch also validates the outlier lists and records the per-tile
+        // delta ranges (both need only the parsed header)
+        FZ_CUDA(launch_tile_offsets(in + kHeaderBytes, (uint32_t)T, loc, bsum, ctrl, st, ~0ull, in + pbase, n,
+                                    drange));
     } else {
         FZ_CUDA(launch_decode_init(ctrl, st));
         FZ_CUDA(launch_validate_outliers(drec, I.counts.n_delta, n, ctrl, st));

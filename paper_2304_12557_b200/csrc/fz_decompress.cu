@@ -150,9 +150,8 @@ __global__ void k_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, 
 // Both record lists in one launch: index k < nd checks the delta list, the rest the value list.
 // The same launch also records the per-tile delta-outlier ranges (k_record_tiles' device form:
 // drange[t] = first delta record at or after element 2048 t; readers clamp the entries).
-__global__ void k_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, uint32_t ntiles, uint32_t* drange)
+__device__ void validate_dev_work(const uint8_t* payload, uint64_t n, Ctrl* ctrl, uint32_t ntiles, uint32_t* drange)
 {
-    pdl_begin();
     const uint64_t nnz = ctrl->dec_nnz, nd = ctrl->dec_nd, nv = ctrl->dec_nv;
     const uint2* drec = reinterpret_cast<const uint2*>(payload + 16 * nnz);
     const uint2* vrec = drec + nd;
@@ -280,10 +279,16 @@ __device__ __forceinline__ Seg block_excl_seg(Seg x, Seg& total, uint32_t* wf, u
 // 1024 tiles (loc), block totals (bsum); the last block to finish (ticket in ctrl->scan_done,
 // zeroed with ctrl by k_init / k_decode_hdr / k_decode_init and reset here) scans the block
 // totals in place (exclusive) and writes the grand total to ctrl->nnz -- one launch.
+__device__ void validate_dev_work(const uint8_t* payload, uint64_t n, Ctrl* ctrl, uint32_t ntiles, uint32_t* drange);
+
 __global__ void __launch_bounds__(1024) k_nnz_block(const uint32_t* __restrict__ flags, uint32_t ntiles,
-                                                    uint32_t* loc, uint32_t* bsum, Ctrl* ctrl, uint64_t expect_nnz)
+                                                    uint32_t* loc, uint32_t* bsum, Ctrl* ctrl, uint64_t expect_nnz,
+                                                    const uint8_t* vpay, uint64_t vn, uint32_t* drange)
 {
     pdl_begin();
+    // device-parsed decode: the outlier-list validation and the per-tile delta ranges ride
+    // along (they need only the parsed header)
+    if (vpay != nullptr) validate_dev_work(vpay, vn, ctrl, ntiles, drange);
     __shared__ uint32_t wsum[33];
     __shared__ bool last;
     __shared__ unsigned long long carry;
@@ -1113,14 +1118,6 @@ cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, c
 }
 
 // fixed grids: the record counts are only known on the device
-cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
-                                cudaStream_t st)
-{
-    LaunchProf lp(K_VALIDATE, st);
-    const unsigned g = grid_for((uint64_t)ntiles + 1), grid = g > (unsigned)num_sms() ? g : (unsigned)num_sms();
-    return launch_pdl(k_validate_dev, dim3(grid), dim3(256), 0, st, payload, n, ctrl, ntiles, drange);
-}
-
 cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,
                                 cudaStream_t st)
 {
@@ -1131,12 +1128,13 @@ cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles,
 }
 
 cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum, Ctrl* ctrl,
-                                cudaStream_t st, uint64_t expect_nnz)
+                                cudaStream_t st, uint64_t expect_nnz, const uint8_t* vpay, uint64_t vn,
+                                uint32_t* drange)
 {
     const uint32_t nb = ntiles == 0 ? 1u : (ntiles + 1023) / 1024;   // one block even for no tiles (nnz = 0)
     LaunchProf lp(K_OFFSETS, st);
     return launch_pdl(k_nnz_block, dim3(nb), dim3(1024), 0, st, reinterpret_cast<const uint32_t*>(flags), ntiles, loc,
-                      bsum, ctrl, expect_nnz);
+                      bsum, ctrl, expect_nnz, vpay, vn, drange);
 }
 
 template <int NDIM>

@@ -176,14 +176,12 @@ DecodeLayout decode_layout(const fz_shape& s);
 cudaError_t launch_decode_init(Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_validate_outliers(const uint2* rec, uint64_t cnt, uint64_t n, Ctrl* ctrl,
                                      cudaStream_t st);
-cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum,
-                                Ctrl* ctrl, cudaStream_t st, uint64_t expect_nnz);
+cudaError_t launch_tile_offsets(const uint8_t* flags, uint32_t ntiles, uint32_t* loc, uint32_t* bsum, Ctrl* ctrl,
+                                cudaStream_t st, uint64_t expect_nnz, const uint8_t* vpay = nullptr, uint64_t vn = 0,
+                                uint32_t* drange = nullptr);
 // device-driven decode (counts parsed from the stream header on the device)
 cudaError_t launch_decode_hdr(Ctrl* ctrl, const uint8_t* in, uint64_t in_size, const fz_shape& s, uint64_t n,
                               uint64_t T, cudaStream_t st);
-// validation of both outlier lists + the per-tile delta-record ranges, one launch (device-parsed)
-cudaError_t launch_validate_dev(const uint8_t* payload, uint64_t n, Ctrl* ctrl, uint32_t ntiles, uint32_t* drange,
-                                cudaStream_t st);
 cudaError_t launch_record_tiles(const uint2* drec, uint64_t nd, uint32_t ntiles, uint64_t gbase, uint32_t* drange,
                                 cudaStream_t st);
 cudaError_t launch_decode_tiles(const DecodeArgs& a, cudaStream_t st, bool fuse_y = false);
